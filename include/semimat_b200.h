@@ -1,0 +1,146 @@
+/*
+ * semimat_b200 -- C ABI of the B200-native semiring kernels.
+ *
+ * Drop-in boundary for the hot path of arxiv/paper_1705_08743 (package
+ * `semimat`).  The reference has no FFI: its "operator API" is the Python
+ * class surface (pkg/src/semimat/__init__.py:10-27) and the private engines
+ * that `kernels.use_vector()` selects (pkg/src/semimat/kernels.py:58-64).
+ * Each entry point below replaces one of those engines; the Python classes in
+ * paper_1705_08743_b200/ keep the reference's class API and call these.
+ *
+ * Conventions
+ *   - All matrix pointers are DEVICE pointers, row-major, with leading
+ *     dimensions in elements.  Base pointers must be 16-byte aligned and
+ *     ld * sizeof(elem) a multiple of 16 (the reference pads every lane row to
+ *     a whole 128-bit block, antidist.py:38-55, so its layout satisfies this).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *   - Every call is asynchronous on `stream`, allocates nothing persistent and
+ *     returns 0 on success, a negative SMX_E* code for argument errors, or a
+ *     positive cudaError_t from the launch.
+ *   - kind: SMX_ANTI = anti-distance (0 = unreachable, S = distance 0;
+ *     (+) = max, (x) = max(a+b-S,0)); SMX_DIST = plain distance (S =
+ *     unreachable; (+) = min, (x) = min(a+b,S)).  S = 2^w - 1.
+ *   - accumulate = 0: C = A (x) B          (the reference __mul__ contract,
+ *                                           output starts at the (+)-identity)
+ *     accumulate = 1: C = C (+) A (x) B    (Floyd-Warshall phases 2/3)
+ */
+#ifndef SEMIMAT_B200_H
+#define SEMIMAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    SMX_OK = 0,
+    SMX_E_ARG = -1,      /* bad size / kind / flag */
+    SMX_E_ALIGN = -2,    /* pointer or leading dimension not 16-byte aligned */
+    SMX_E_WORKSPACE = -3,/* workspace missing or too small */
+    SMX_E_DRIVER = -4    /* driver entry point (TMA descriptor encode) unavailable */
+};
+enum { SMX_ANTI = 0, SMX_DIST = 1 };
+
+int smx_version(void);
+const char* smx_error_string(int code);
+
+/* ---- saturated lane semiring products ---------------------------------
+ * Replace _mul_vector (pkg/src/semimat/antidist.py:361-371, called from
+ * AntidistMatrix.__mul__ :226-250) and _minplus_mul_vector (:412-422, called
+ * from DistMatrix.__mul__ :311-329).  C is M x N, A is M x K, B is K x N. */
+int smx_semiring_gemm_u8(const uint8_t* A, const uint8_t* B, uint8_t* C,
+                         int M, int N, int K, int lda, int ldb, int ldc,
+                         int kind, int accumulate, void* stream);
+int smx_semiring_gemm_u16(const uint16_t* A, const uint16_t* B, uint16_t* C,
+                          int M, int N, int K, int lda, int ldb, int ldc,
+                          int kind, int accumulate, void* stream);
+int smx_semiring_gemm_u32(const uint32_t* A, const uint32_t* B, uint32_t* C,
+                          int M, int N, int K, int lda, int ldb, int ldc,
+                          int kind, int accumulate, void* stream);
+
+/* ---- Floyd-Warshall closures (blocked three-phase) ---------------------
+ * Replace _close_vector (antidist.py:390-398, from AntidistMatrix.
+ * transitive_close :252-261) and _minplus_close_vector (:440-448, from
+ * DistMatrix.transitive_close :331-340).  In place on the n x n matrix T
+ * (row stride ld >= n).  `workspace` is caller-owned device memory of at
+ * least smx_fw_workspace_bytes(n, ld, elem_bytes) bytes. */
+size_t smx_fw_workspace_bytes(int n, int ld, int elem_bytes);
+int smx_fw_u8(uint8_t* T, int n, int ld, int kind, void* workspace, size_t ws_bytes,
+              void* stream);
+int smx_fw_u16(uint16_t* T, int n, int ld, int kind, void* workspace, size_t ws_bytes,
+               void* stream);
+int smx_fw_u32(uint32_t* T, int n, int ld, int kind, void* workspace, size_t ws_bytes,
+               void* stream);
+
+/* Building blocks of the blocked FW, exported for the row-panel-sharded
+ * multi-GPU driver (paper_1705_08743_b200/sharded.py).  elem_bytes in
+ * {1,2,4}.  Pivot tile: b x b (b <= smx_fw_block(elem_bytes)), in place. */
+int smx_fw_block(int elem_bytes);
+int smx_fw_pivot(void* P, int b, int ld, int elem_bytes, int kind, void* stream);
+/* C[rows, :] (+)= A (x) B over rows [0, M) except the row-tile range
+ * [skip_row0, skip_row0 + skip_rows), which must be multiples of 128. */
+int smx_semiring_gemm_skip(const void* A, const void* B, void* C, int M, int N, int K,
+                           int lda, int ldb, int ldc, int elem_bytes, int kind,
+                           int skip_row0, int skip_rows, void* stream);
+
+/* ---- Boolean products and Warshall closure ------------------------------
+ * Replace BoolMatrix.__mul__ (pkg/src/semimat/boolmat.py:151-172) and
+ * BoolMatrix.transitive_closure (:174-189).
+ *
+ * Byte layout (one byte per entry, 0/1): tcgen05 kind::i8 tensor-core GEMM
+ * with a count>0 threshold.  Bt is B TRANSPOSED (N x K, K-major), K >= 1.
+ * Output is written as 0/1 bytes to C (C_bits == NULL, ldc in bytes) or as
+ * packed bits to C_bits (C == NULL, ldc in u32 words) in the reference's
+ * LSB-first block layout (boolmat.py:3-5); accumulate ORs into the output. */
+int smx_bool_gemm_i8(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* C_bits,
+                     int M, int N, int K, int lda, int ldbt, int ldc, int accumulate,
+                     void* stream);
+/* Warshall closure in place on 0/1 bytes (n x n, ld bytes, 16-byte aligned
+ * rows) with tensor-core phases 2/3. */
+size_t smx_bool_warshall_i8_workspace_bytes(int n, int ld);
+int smx_bool_warshall_i8(uint8_t* T, int n, int ld, void* workspace, size_t ws_bytes,
+                         void* stream);
+/* Bit-packed comparison variant on u32 words (the reference's uint64 blocks
+ * reinterpreted little-endian): C = (acc ? C : 0) | A (x) B. */
+int smx_bool_gemm_bits(const uint32_t* A, const uint32_t* B, uint32_t* C,
+                       int M, int Nwords, int K, int lda_w, int ldb_w, int ldc_w,
+                       int accumulate, void* stream);
+/* Warshall closure in place on packed bits (n x n, ld in u32 words). */
+size_t smx_bool_warshall_workspace_bytes(int n, int ld_w);
+int smx_bool_warshall_bits(uint32_t* T, int n, int ld_w, void* workspace, size_t ws_bytes,
+                           void* stream);
+
+/* ---- layout helpers ---------------------------------------------------- */
+/* bytes (rows x cols, ld bytes) <-> packed u32 words (ld_w words), zero pad bits */
+int smx_pack_bits(const uint8_t* bytes, uint32_t* words, int rows, int cols, int ld,
+                  int ld_w, void* stream);
+int smx_unpack_bits(const uint32_t* words, uint8_t* bytes, int rows, int cols, int ld_w,
+                    int ld, void* stream);
+/* out (cols x rows) = in^T for bytes */
+int smx_transpose_u8(const uint8_t* in, uint8_t* out, int rows, int cols, int ld_in,
+                     int ld_out, void* stream);
+
+/* ---- entrywise algebra (antidist.py:128-156, boolmat.py:120-137) -------
+ * Lane matrices: op 0 = min (&), 1 = max (|), 2 = |a-b| (^), 3 = S - a (~,
+ * B unused); columns >= cols of every row are set to the pad value (S when
+ * pad_is_limit, else 0).  Bits: op 0 = or, 1 = and, 2 = xor, 3 = not (B
+ * unused); bits >= cols are cleared.  C may alias A or B. */
+int smx_lane_entrywise(const void* A, const void* B, void* C, int rows, int cols, int ld,
+                       int elem_bytes, int op, int pad_is_limit, void* stream);
+int smx_bits_entrywise(const uint32_t* A, const uint32_t* B, uint32_t* C, int rows, int cols,
+                       int ld_w, int op, void* stream);
+
+/* ---- measurement support (bench.py roofline denominators) -------------- */
+/* Runs `iters` iterations of an independent VIMNMX.U16x2 + VIADDMNMX.U16x2
+ * (or VIADDMNMX only when one_instr != 0) instruction stream on every
+ * resident thread; writes a checksum to sink.  Instructions issued =
+ * grid*block*iters*per_iter (returned via *instr_per_thread). */
+int smx_int_issue_probe(uint32_t* sink, int blocks, int threads, int iters, int one_instr,
+                        long long* instr_per_thread, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEMIMAT_B200_H */

@@ -1,0 +1,106 @@
+"""ctypes binding of the C ABI in include/semimat_b200.h.
+
+The product path has exactly one backend: the sm_100a library built by
+``_build.py``.  There is no CPU fallback -- if the library or a CUDA device is
+missing, every matrix operation raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import c_int, c_int64, c_longlong, c_size_t, c_void_p, POINTER
+
+import torch
+
+from . import _build
+
+SMX_ANTI, SMX_DIST = 0, 1
+
+_lib = None
+
+# name -> (argtypes, restype)
+_SIGS = {
+    "smx_version": ([], c_int),
+    "smx_error_string": ([c_int], ctypes.c_char_p),
+    "smx_semiring_gemm_u8": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),
+    "smx_semiring_gemm_u16": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),
+    "smx_semiring_gemm_u32": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),
+    "smx_semiring_gemm_skip": ([c_void_p] * 3 + [c_int] * 11 + [c_void_p], c_int),
+    "smx_fw_workspace_bytes": ([c_int, c_int, c_int], c_size_t),
+    "smx_fw_u8": ([c_void_p, c_int, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),
+    "smx_fw_u16": ([c_void_p, c_int, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),
+    "smx_fw_u32": ([c_void_p, c_int, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),
+    "smx_fw_block": ([c_int], c_int),
+    "smx_fw_pivot": ([c_void_p, c_int, c_int, c_int, c_int, c_void_p], c_int),
+    "smx_bool_gemm_bits": ([c_void_p] * 3 + [c_int] * 7 + [c_void_p], c_int),
+    "smx_bool_warshall_workspace_bytes": ([c_int, c_int], c_size_t),
+    "smx_bool_warshall_bits": ([c_void_p, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),
+    "smx_pack_bits": ([c_void_p, c_void_p] + [c_int] * 4 + [c_void_p], c_int),
+    "smx_unpack_bits": ([c_void_p, c_void_p] + [c_int] * 4 + [c_void_p], c_int),
+    "smx_transpose_u8": ([c_void_p, c_void_p] + [c_int] * 4 + [c_void_p], c_int),
+    "smx_lane_entrywise": ([c_void_p] * 3 + [c_int] * 6 + [c_void_p], c_int),
+    "smx_bits_entrywise": ([c_void_p] * 3 + [c_int] * 4 + [c_void_p], c_int),
+    "smx_int_issue_probe":([c_void_p, c_int, c_int, c_int, c_int, POINTER(c_longlong), c_void_p],
+                            c_int),
+}
+# Optional entry points (present once their kernels are built).
+_OPTIONAL = {
+    "smx_bool_gemm_i8": ([c_void_p] * 4 + [c_int] * 7 + [c_void_p], c_int),
+    "smx_bool_warshall_i8_workspace_bytes": ([c_int, c_int], c_size_t),
+    "smx_bool_warshall_i8": ([c_void_p, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),
+}
+
+
+def declared_symbols() -> list[str]:
+    return sorted(_SIGS) + sorted(_OPTIONAL)
+
+
+def lib():
+    """Load (building first if needed) the sm_100a library."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if not path.exists():
+            path = _build.build()
+        handle = ctypes.CDLL(str(path))
+        for name, (args, res) in list(_SIGS.items()) + list(_OPTIONAL.items()):
+            fn = getattr(handle, name, None)
+            if fn is None:
+                if name in _SIGS:
+                    raise RuntimeError(f"{path} does not export {name}")
+                continue
+            fn.argtypes = args
+            fn.restype = res
+        _lib = handle
+    return _lib
+
+
+def has(name: str) -> bool:
+    return getattr(lib(), name, None) is not None
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = lib().smx_error_string(rc).decode()
+        raise RuntimeError(f"{what} failed: {msg} (code {rc})")
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("semimat_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if dev.type != "cuda":
+        raise RuntimeError(f"semimat_b200 tensors live on CUDA devices, got {dev}")
+    return dev
+
+
+def stream_ptr(device: torch.device | None = None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()

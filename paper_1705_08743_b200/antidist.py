@@ -1,0 +1,322 @@
+"""Dense saturated lane matrices on the GPU -- drop-in for semimat.antidist.
+
+AntidistMatrix: entry a encodes distance S - a (0 = unreachable, S =
+distance zero); (+) = lanewise max, (x) = max(a + b - S, 0).  DistMatrix is
+the complement view: plain distances, S = unreachable, (+) = min,
+(x) = min(a + b, S).  Class surface, validation order and messages follow
+pkg/src/semimat/antidist.py:31-350; storage is the reference's padded layout
+(rows x ceil(cols / L) * L lanes, L = 128 / width, pad = the class's
+(+)-identity, antidist.py:38-55) held in HBM.  Products and closures run in
+the sm_100a kernels of libsemimat_b200.so; there is no CPU path and no
+scalar/vector dispatch (the reference's kernels.use_vector(), kernels.py:58-64,
+is the boundary this package replaces).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native
+from .boolmat import BoolMatrix
+from .scalars import sat_limit
+
+LANES = {8: 16, 16: 8, 32: 4}
+_NP = {8: np.uint8, 16: np.uint16, 32: np.uint32}
+_TORCH = {8: torch.uint8, 16: torch.uint16, 32: torch.uint32}
+
+
+def lane_count(width: int) -> int:
+    sat_limit(width)
+    return LANES[width]
+
+
+def dtype_for(width: int):
+    sat_limit(width)
+    return _NP[width]
+
+
+class _LaneMatrix:
+    """Shared storage and entrywise algebra of the two saturated matrix types."""
+
+    __slots__ = ("rows", "cols", "width", "_data")
+
+    _PAD_IS_LIMIT = False
+
+    def __init__(self, rows: int, cols: int, width: int = 8, _data=None, *, device=None):
+        if rows < 1 or cols < 1:
+            raise ValueError(f"matrix dimensions must be positive, got {rows}x{cols}")
+        lanes = lane_count(width)
+        padded = -(-cols // lanes) * lanes
+        self.rows = rows
+        self.cols = cols
+        self.width = width
+        if isinstance(_data, torch.Tensor):
+            if tuple(_data.shape) != (rows, padded) or _data.dtype != _TORCH[width]:
+                raise ValueError("backing array does not match the padded shape")
+            if _data.device.type != "cuda":
+                _data = _data.to(_native.require_cuda(device))
+            self._data = _data.contiguous()
+            return
+        dev = _native.require_cuda(device)
+        if _data is None:
+            fill = self._pad_fill(width)
+            host = np.full((rows, padded), fill, dtype=_NP[width])
+        else:
+            host = np.asarray(_data)
+            if host.shape != (rows, padded) or host.dtype != _NP[width]:
+                raise ValueError("backing array does not match the padded shape")
+        self._data = torch.from_numpy(np.ascontiguousarray(host)).to(dev)
+
+    @classmethod
+    def _pad_fill(cls, width):
+        return sat_limit(width) if cls._PAD_IS_LIMIT else 0
+
+    # -- basics -------------------------------------------------------------
+
+    @property
+    def limit(self) -> int:
+        return sat_limit(self.width)
+
+    @property
+    def padded_cols(self) -> int:
+        return self._data.shape[1]
+
+    @property
+    def device(self) -> torch.device:
+        return self._data.device
+
+    @property
+    def data(self):
+        """Raw lane storage including padding columns (host copy), read-only."""
+        view = self._data.cpu().numpy()
+        view.flags.writeable = False
+        return view
+
+    def to_numpy(self) -> np.ndarray:
+        return self._data.cpu().numpy()
+
+    def copy(self):
+        return type(self)(self.rows, self.cols, self.width, self._data.clone())
+
+    def _check_index(self, i, j):
+        if not (0 <= i < self.rows and 0 <= j < self.cols):
+            raise IndexError(f"index ({i}, {j}) out of range for {self.rows}x{self.cols}")
+
+    def get(self, i: int, j: int) -> int:
+        self._check_index(i, j)
+        return int(self._data[i, j].cpu().numpy())
+
+    def set(self, i: int, j: int, value: int) -> None:
+        self._check_index(i, j)
+        if not 0 <= value <= self.limit:
+            raise ValueError(f"entry {value!r} outside [0, {self.limit}]")
+        self._data[i, j] = torch.from_numpy(np.array(value, dtype=_NP[self.width])).to(self.device)
+
+    def to_lists(self) -> list[list[int]]:
+        return self.to_numpy()[:, : self.cols].tolist()
+
+    @classmethod
+    def from_lists(cls, rows: list[list[int]], width: int = 8):
+        if not rows or not rows[0]:
+            raise ValueError("matrix dimensions must be positive")
+        ncols = len(rows[0])
+        limit = sat_limit(width)
+        host = np.full((len(rows), -(-ncols // LANES[width]) * LANES[width]),
+                       cls._pad_fill(width), dtype=_NP[width])
+        for i, row in enumerate(rows):
+            if len(row) != ncols:
+                raise ValueError(f"row {i} has {len(row)} entries, expected {ncols}")
+            for v in row:
+                if not 0 <= v <= limit:
+                    raise ValueError(f"entry {v!r} outside [0, {limit}]")
+            host[i, :ncols] = row
+        return cls(len(rows), ncols, width, host)
+
+    @classmethod
+    def from_numpy(cls, data: np.ndarray, cols: int, width: int, device=None):
+        """Wrap a padded host array (rows x padded cols, lane dtype)."""
+        return cls(data.shape[0], cols, width, np.ascontiguousarray(data), device=device)
+
+    # -- entrywise algebra (device kernel) ------------------------------------
+
+    def _check_same(self, other):
+        if type(other) is not type(self):
+            raise TypeError(f"expected {type(self).__name__}, got {type(other).__name__}")
+        if (self.rows, self.cols, self.width) != (other.rows, other.cols, other.width):
+            raise ValueError(
+                f"shape/width mismatch: {self.rows}x{self.cols}/w{self.width} vs "
+                f"{other.rows}x{other.cols}/w{other.width}"
+            )
+
+    def _entrywise(self, other, op: int, out_cls):
+        out = torch.empty_like(self._data)
+        b = other._data if other is not None else self._data
+        _native.check(
+            _native.lib().smx_lane_entrywise(
+                self._data.data_ptr(), b.data_ptr(), out.data_ptr(), self.rows, self.cols,
+                self.padded_cols, self.width // 8, op, int(out_cls._PAD_IS_LIMIT),
+                _native.stream_ptr(self.device)),
+            "lane entrywise")
+        return out_cls(self.rows, self.cols, self.width, out)
+
+    def __and__(self, other):
+        """Lanewise minimum."""
+        self._check_same(other)
+        return self._entrywise(other, 0, type(self))
+
+    def __or__(self, other):
+        """Lanewise maximum."""
+        self._check_same(other)
+        return self._entrywise(other, 1, type(self))
+
+    def __xor__(self, other):
+        """Lanewise absolute difference."""
+        self._check_same(other)
+        return self._entrywise(other, 2, type(self))
+
+    def __invert__(self):
+        """Complement at width, switching between the two encodings."""
+        cls = DistMatrix if isinstance(self, AntidistMatrix) else AntidistMatrix
+        return self._entrywise(None, 3, cls)
+
+    def __eq__(self, other):
+        if type(other) is not type(self):
+            return NotImplemented
+        return (self.rows, self.cols, self.width) == (other.rows, other.cols, other.width) and bool(
+            torch.equal(self._data.view(torch.uint8), other._data.to(self.device).view(torch.uint8)))
+
+    __hash__ = None
+
+    def __repr__(self):
+        return f"<{type(self).__name__} {self.rows}x{self.cols} width={self.width}>"
+
+    # -- shared product / closure plumbing -----------------------------------
+
+    def _mul_checks(self, other):
+        if self.width != other.width:
+            raise ValueError(f"width mismatch: {self.width} vs {other.width}")
+        if self.cols != other.rows:
+            raise ValueError(
+                f"inner dimensions disagree: {self.rows}x{self.cols} times "
+                f"{other.rows}x{other.cols}"
+            )
+
+    def transitive_close(self) -> None:
+        """In-place Floyd-Warshall closure (antidist.py:252-261 / :331-340)."""
+        if self.rows != self.cols:
+            raise ValueError(f"closure needs a square matrix, got {self.rows}x{self.cols}")
+        from . import engines
+        engines.lane_close_(self._data, self.rows, self.width, anti=not self._PAD_IS_LIMIT)
+
+    def transitive_closure(self):
+        """Closure over >= 1 edge on a copy (antidist.py:263-273 / :342-350)."""
+        out = self.copy()
+        out.transitive_close()
+        return out
+
+
+class AntidistMatrix(_LaneMatrix):
+    """Matrix of anti-distance values (antidist.py:173-273)."""
+
+    _PAD_IS_LIMIT = False
+
+    @classmethod
+    def zeros(cls, rows: int, cols: int, width: int = 8) -> "AntidistMatrix":
+        return cls(rows, cols, width)
+
+    @classmethod
+    def identity(cls, dim: int, width: int = 8) -> "AntidistMatrix":
+        if dim < 1:
+            raise ValueError(f"matrix dimensions must be positive, got {dim}x{dim}")
+        host = np.zeros((dim, -(-dim // LANES[width]) * LANES[width]), dtype=dtype_for(width))
+        host[np.arange(dim), np.arange(dim)] = sat_limit(width)
+        return cls(dim, dim, width, host)
+
+    @classmethod
+    def from_edges(cls, dim: int, edges, width: int = 8) -> "AntidistMatrix":
+        """Adjacency of weighted edges (u, v, w); parallel edges keep the shortest
+        (antidist.py:191-211)."""
+        if dim < 1:
+            raise ValueError(f"matrix dimensions must be positive, got {dim}x{dim}")
+        limit = sat_limit(width)
+        host = np.zeros((dim, -(-dim // LANES[width]) * LANES[width]), dtype=_NP[width])
+        for u, v, w in edges:
+            if not 0 <= u < dim:
+                raise ValueError(f"source vertex {u} out of range [0, {dim})")
+            if not 0 <= v < dim:
+                raise ValueError(f"target vertex {v} out of range [0, {dim})")
+            if not 0 <= w <= limit:
+                raise ValueError(f"weight {w} outside [0, {limit}]")
+            value = limit - w
+            if value > int(host[u, v]):
+                host[u, v] = value
+        return cls(dim, dim, width, host)
+
+    @classmethod
+    def from_boolmat(cls, mat: BoolMatrix, width: int = 8) -> "AntidistMatrix":
+        """1 -> distance zero (S), 0 -> unreachable (antidist.py:213-219)."""
+        limit = sat_limit(width)
+        bits = mat.to_numpy().astype(_NP[width])
+        host = np.zeros((mat.rows, -(-mat.cols // LANES[width]) * LANES[width]), dtype=_NP[width])
+        host[:, : mat.cols] = bits * limit
+        return cls(mat.rows, mat.cols, width, host)
+
+    def to_boolmat(self) -> BoolMatrix:
+        """Any finite distance becomes 1 (antidist.py:221-224)."""
+        return BoolMatrix.from_numpy((self.to_numpy()[:, : self.cols] > 0).astype(np.uint8))
+
+    def __mul__(self, other) -> "AntidistMatrix":
+        """max over k of the saturated sum (antidist.py:226-250)."""
+        if not isinstance(other, AntidistMatrix):
+            return NotImplemented
+        self._mul_checks(other)
+        from . import engines
+        out = engines.lane_mul(self._data, other._data, self.cols, self.width, anti=True)
+        return AntidistMatrix(self.rows, other.cols, self.width, out)
+
+
+class DistMatrix(_LaneMatrix):
+    """Matrix of plain distances; the complement view (antidist.py:276-350)."""
+
+    _PAD_IS_LIMIT = True
+
+    @classmethod
+    def unreachable(cls, rows: int, cols: int, width: int = 8) -> "DistMatrix":
+        return cls(rows, cols, width)
+
+    @classmethod
+    def identity(cls, dim: int, width: int = 8) -> "DistMatrix":
+        if dim < 1:
+            raise ValueError(f"matrix dimensions must be positive, got {dim}x{dim}")
+        host = np.full((dim, -(-dim // LANES[width]) * LANES[width]), sat_limit(width),
+                       dtype=dtype_for(width))
+        host[np.arange(dim), np.arange(dim)] = 0
+        return cls(dim, dim, width, host)
+
+    @classmethod
+    def from_edges(cls, dim: int, edges, width: int = 8) -> "DistMatrix":
+        """Edge weights stored directly; parallel edges keep the minimum (antidist.py:294-309)."""
+        if dim < 1:
+            raise ValueError(f"matrix dimensions must be positive, got {dim}x{dim}")
+        limit = sat_limit(width)
+        host = np.full((dim, -(-dim // LANES[width]) * LANES[width]), limit, dtype=_NP[width])
+        for u, v, w in edges:
+            if not 0 <= u < dim:
+                raise ValueError(f"source vertex {u} out of range [0, {dim})")
+            if not 0 <= v < dim:
+                raise ValueError(f"target vertex {v} out of range [0, {dim})")
+            if not 0 <= w <= limit:
+                raise ValueError(f"weight {w} outside [0, {limit}]")
+            if w < int(host[u, v]):
+                host[u, v] = w
+        return cls(dim, dim, width, host)
+
+    def __mul__(self, other) -> "DistMatrix":
+        """min over k of the saturating sum (antidist.py:311-329)."""
+        if not isinstance(other, DistMatrix):
+            return NotImplemented
+        self._mul_checks(other)
+        from . import engines
+        out = engines.lane_mul(self._data, other._data, self.cols, self.width, anti=False)
+        return DistMatrix(self.rows, other.cols, self.width, out)

@@ -1,0 +1,440 @@
+// Boolean product on the 5th-generation tensor cores: tcgen05.mma kind::i8
+// with a count > 0 threshold, and the blocked Warshall closure built on it.
+//
+// BoolMatrix.__mul__ (pkg/src/semimat/boolmat.py:151-172) ORs row k of B into
+// every row i with A[i,k] = 1.  Over 0/1 bytes that is exactly
+//     C[i,j] = (sum_k A[i,k] * B[k,j]) > 0
+// (SURVEY.md 0.1 fact 3), an unsigned 8-bit dense contraction with an int32
+// accumulator that cannot overflow for K < 2^31.  So the Boolean product is
+// run as a real GEMM on the tensor cores:
+//   * TMA (cp.async.bulk.tensor, 128-byte swizzle) streams 128 x 128-byte A
+//     and BN x 128-byte B^T tiles into a 4-stage shared-memory ring, tracked
+//     by mbarriers (full/empty);
+//   * one elected thread issues tcgen05.mma.cta_group::1.kind::i8 (M = 128,
+//     N = BN, K = 32 per instruction) accumulating into TMEM, and
+//     tcgen05.commit frees each ring slot when its MMAs retire;
+//   * 4 epilogue warps read the accumulator with tcgen05.ld (32 lanes x 32
+//     columns per instruction), threshold count > 0, and write either 0/1
+//     bytes or the reference's packed-bit layout directly (one 32-bit word per
+//     thread per 32 columns, LSB first -- boolmat.py:3-5), optionally OR-ing
+//     into the existing output (Warshall phases 2/3).
+// Ragged M, N, K come for free: TMA zero-fills out-of-bounds boxes and zero
+// is the Boolean (+)-identity and (x)-annihilator.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace smx {
+
+constexpr int kTcBM = 128;
+constexpr int kTcBK = 128;        // bytes of K per stage = one 128-byte swizzle row
+constexpr int kTcStages = 4;
+constexpr int kTcThreads = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(addr), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0,
+                                            int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// K-major operand tile with 128-byte swizzle (rows of 128 bytes, 8-row core
+// groups 1024 bytes apart): start>>4 | LBO(unused)=1 | SBO=1024>>4 |
+// version 1 (sm_100) | layout SWIZZLE_128B (2).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
+    return (uint64_t)((smem_addr & 0x3FFFFu) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+
+template <int BN>
+__device__ __forceinline__ constexpr uint32_t idesc_i8() {
+    // c_format S32 (2) @4 | a,b unsigned 8-bit (0) | K-major | N>>3 @17 | M>>4 @24
+    return (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTcBM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct TcArgs {
+    uint8_t* C;          // bytes output (or nullptr)
+    uint32_t* Cbits;     // packed output (or nullptr)
+    int M, N, K;
+    long long ldc;       // bytes, or u32 words for Cbits
+    int accumulate;
+    int skip_tile0, skip_tiles;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kTcThreads, 1)
+bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                    const TcArgs p) {
+    constexpr uint32_t A_BYTES = kTcBM * kTcBK;
+    constexpr uint32_t B_BYTES = BN * kTcBK;
+    extern __shared__ __align__(1024) uint8_t smem_dyn[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kTcStages * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + kTcStages * B_BYTES);
+    uint64_t* empty = full + kTcStages;
+    uint64_t* accum = empty + kTcStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int mt = blockIdx.y;
+    if (mt >= p.skip_tile0) mt += p.skip_tiles;
+    const int m0 = mt * kTcBM, n0 = blockIdx.x * BN;
+    const int nkb = (p.K + kTcBK - 1) / kTcBK;
+
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accum, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "n"(BN)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (threadIdx.x == 0) {
+        // ---- TMA producer ----
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % kTcStages;
+            const uint32_t ph = (kb / kTcStages) & 1;
+            mbar_wait(&empty[s], ph ^ 1);
+            mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+            tma_load_2d(&mapA, &full[s], sA + s * A_BYTES, kb * kTcBK, m0);
+            tma_load_2d(&mapB, &full[s], sB + s * B_BYTES, kb * kTcBK, n0);
+        }
+    } else if (threadIdx.x == 32) {
+        // ---- MMA issuer ----
+        constexpr uint32_t idesc = idesc_i8<BN>();
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % kTcStages;
+            const uint32_t ph = (kb / kTcStages) & 1;
+            mbar_wait(&full[s], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+            for (int k = 0; k < kTcBK / 32; ++k)
+                umma_i8(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
+                        (kb | k) != 0);
+            umma_commit(&empty[s]);
+        }
+        umma_commit(accum);
+    }
+    __syncwarp();
+
+    // ---- epilogue: TMEM -> threshold -> bytes or bits ----
+    mbar_wait(accum, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int row = m0 + warp * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(trow + c * 32, r);   // warp-collective: all lanes participate
+        if (row >= p.M || nkb == 0) continue;
+        const int col0 = n0 + c * 32;
+        if (col0 >= p.N) continue;
+        if (p.Cbits) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) word |= (r[j] != 0u ? 1u : 0u) << j;
+            uint32_t* dst = p.Cbits + (long long)row * p.ldc + (col0 >> 5);
+            *dst = p.accumulate ? (*dst | word) : word;
+        } else {
+            uint32_t w[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                w[q] = (r[4 * q] != 0u ? 1u : 0u) | (r[4 * q + 1] != 0u ? 0x100u : 0u) |
+                       (r[4 * q + 2] != 0u ? 0x10000u : 0u) | (r[4 * q + 3] != 0u ? 0x1000000u : 0u);
+            uint8_t* dst = p.C + (long long)row * p.ldc + col0;
+            if (col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+                uint4* d4 = reinterpret_cast<uint4*>(dst);
+                uint4 v0 = make_uint4(w[0], w[1], w[2], w[3]), v1 = make_uint4(w[4], w[5], w[6], w[7]);
+                if (p.accumulate) {
+                    const uint4 o0 = d4[0], o1 = d4[1];
+                    v0.x |= o0.x; v0.y |= o0.y; v0.z |= o0.z; v0.w |= o0.w;
+                    v1.x |= o1.x; v1.y |= o1.y; v1.z |= o1.z; v1.w |= o1.w;
+                }
+                d4[0] = v0;
+                d4[1] = v1;
+            } else {
+                const uint8_t* wb = reinterpret_cast<const uint8_t*>(w);
+                for (int j = 0; j < 32 && col0 + j < p.N; ++j)
+                    dst[j] = p.accumulate ? (uint8_t)(dst[j] | wb[j]) : wb[j];
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 2) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN)
+                     : "memory");
+    }
+}
+
+// ---- host side ---------------------------------------------------------------
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// rows x cols bytes (K-major), box = box_rows x 128 bytes, 128-byte swizzle
+static int make_map(CUtensorMap* map, const uint8_t* base, int rows, int cols, long long ld, int box_rows) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return SMX_E_DRIVER;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld};
+    cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? SMX_OK : SMX_E_DRIVER;
+}
+
+template <int BN>
+static int launch_tc(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long long lda, long long ldbt,
+                     cudaStream_t s) {
+    CUtensorMap mA, mB;
+    SMX_TRY(make_map(&mA, A, a.M, a.K, lda, kTcBM));
+    SMX_TRY(make_map(&mB, Bt, a.N, a.K, ldbt, BN));
+    constexpr size_t smem = 1024 + kTcStages * (size_t)(kTcBM + BN) * kTcBK + 8 * (2 * kTcStages + 1) + 16;
+    auto kern = bool_i8_gemm_kernel<BN>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        configured = true;
+    }
+    const int mtiles = ceil_div(a.M, kTcBM) - a.skip_tiles;
+    if (mtiles <= 0) return SMX_OK;
+    dim3 grid(ceil_div(a.N, BN), mtiles);
+    kern<<<grid, kTcThreads, smem, s>>>(mA, mB, a);
+    SMX_RETURN_LAUNCH();
+}
+
+int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbits, int M, int N, int K,
+                 long long lda, long long ldbt, long long ldc, int accumulate, int skip_row0, int skip_rows,
+                 cudaStream_t s) {
+    if (M < 0 || N < 0 || K < 1 || (C == nullptr) == (Cbits == nullptr)) return SMX_E_ARG;
+    if (M == 0 || N == 0) return SMX_OK;
+    if (!aligned16(A) || !aligned16(Bt) || (lda & 15) || (ldbt & 15)) return SMX_E_ALIGN;
+    if (lda < K || ldbt < K) return SMX_E_ARG;
+    if (Cbits ? ((long long)ldc * 32 < N) : (ldc < N)) return SMX_E_ARG;
+    TcArgs a{C, Cbits, M, N, K, ldc, accumulate != 0, 0, 0};
+    if (skip_rows > 0) {
+        if (skip_row0 % kTcBM) return SMX_E_ARG;
+        a.skip_tile0 = skip_row0 / kTcBM;
+        a.skip_tiles = ceil_div(skip_rows, kTcBM);
+        const int total = ceil_div(M, kTcBM);
+        if (a.skip_tile0 + a.skip_tiles > total) a.skip_tiles = total - a.skip_tile0;
+    }
+    // widest tile that still gives every SM a tile
+    const long long rows = ceil_div(M, kTcBM) - a.skip_tiles;
+    if (rows * ceil_div(N, 256) >= 148) return launch_tc<256>(A, Bt, a, lda, ldbt, s);
+    if (rows * ceil_div(N, 128) >= 148) return launch_tc<128>(A, Bt, a, lda, ldbt, s);
+    return launch_tc<64>(A, Bt, a, lda, ldbt, s);
+}
+
+// ---- Warshall on bytes with tensor-core phases 2/3 -----------------------------
+
+constexpr int kTcWarshallBlock = 256;
+
+// Pivot tile closure on bytes: each thread packs its row to bits, runs the
+// sequential Warshall steps with the pivot row broadcast through smem, and
+// writes 0/1 bytes back.
+__global__ void __launch_bounds__(kTcWarshallBlock, 1)
+bool_pivot_bytes_kernel(uint8_t* P, int b, long long ld) {
+    constexpr int W = kTcWarshallBlock / 32;
+    __shared__ __align__(16) uint32_t prow[2][W];
+    const int r = threadIdx.x;
+    uint32_t w[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        uint32_t v = 0;
+        if (r < b) {
+            for (int j = 0; j < 32; ++j) {
+                const int c = i * 32 + j;
+                if (c < b && P[(long long)r * ld + c]) v |= 1u << j;
+            }
+        }
+        w[i] = v;
+    }
+    if (r == 0) {
+#pragma unroll
+        for (int i = 0; i < W; ++i) prow[0][i] = w[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        if (q * 32 >= b) break;
+        for (int kk = 0; kk < 32; ++kk) {
+            const int k = q * 32 + kk;
+            if (k >= b) break;
+            const int cur = k & 1;
+            if ((w[q] >> kk) & 1u) {
+#pragma unroll
+                for (int i = 0; i < W; ++i) w[i] |= prow[cur][i];
+            }
+            if (r == k + 1) {
+#pragma unroll
+                for (int i = 0; i < W; ++i) prow[cur ^ 1][i] = w[i];
+            }
+            __syncthreads();
+        }
+    }
+    if (r < b) {
+        for (int c = 0; c < b; ++c) P[(long long)r * ld + c] = (w[c >> 5] >> (c & 31)) & 1u;
+    }
+}
+
+inline size_t tc_ws_bytes(int n, long long ld) {
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t rpt = al((size_t)n * kTcWarshallBlock);          // (row panel)^T, n x B
+    const size_t cp = al((size_t)n * kTcWarshallBlock);           // column panel snapshot
+    const size_t rp = al((size_t)kTcWarshallBlock * ld);          // row panel snapshot
+    return rpt + cp + rp;
+}
+
+int transpose_bytes(const uint8_t* in, uint8_t* out, int rows, int cols, long long ld_in, long long ld_out,
+                    cudaStream_t s);
+
+int bool_warshall_i8(uint8_t* T, int n, long long ld, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (n < 0 || ld < n) return SMX_E_ARG;
+    if (n == 0) return SMX_OK;
+    if (!aligned16(T) || (ld & 15)) return SMX_E_ALIGN;
+    if (n <= kTcWarshallBlock) {
+        bool_pivot_bytes_kernel<<<1, kTcWarshallBlock, 0, s>>>(T, n, ld);
+        SMX_RETURN_LAUNCH();
+    }
+    if (ws == nullptr || ws_bytes < tc_ws_bytes(n, ld)) return SMX_E_WORKSPACE;
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    uint8_t* RPt = reinterpret_cast<uint8_t*>(ws);
+    uint8_t* CP = RPt + al((size_t)n * kTcWarshallBlock);
+    uint8_t* RP = CP + al((size_t)n * kTcWarshallBlock);
+    constexpr long long B = kTcWarshallBlock;
+    for (int k0 = 0; k0 < n; k0 += kTcWarshallBlock) {
+        const int bb = n - k0 < kTcWarshallBlock ? n - k0 : kTcWarshallBlock;
+        uint8_t* rowK = T + (long long)k0 * ld;
+        bool_pivot_bytes_kernel<<<1, kTcWarshallBlock, 0, s>>>(rowK + k0, bb, ld);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return (int)e;
+        // phase 2: T[K,:] |= P* . RP   (B^T = RP^T)
+        e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return (int)e;
+        SMX_TRY(transpose_bytes(RP, RPt, bb, n, ld, B, s));
+        SMX_TRY(bool_i8_gemm(RP + k0, RPt, rowK, nullptr, bb, n, bb, ld, B, ld, 1, 0, 0, s));
+        // phase 3: T[i,:] |= CP[i,:] . T[K,:]  for i outside K  (B^T = T[K,:]^T)
+        SMX_TRY(transpose_bytes(rowK, RPt, bb, n, ld, B, s));
+        e = cudaMemcpy2DAsync(CP, B, T + k0, ld, bb, n, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return (int)e;
+        SMX_TRY(bool_i8_gemm(CP, RPt, T, nullptr, n, n, bb, B, B, ld, 1, k0, bb, s));
+    }
+    return SMX_OK;
+}
+
+}  // namespace smx
+
+using namespace smx;
+
+extern "C" {
+
+int smx_bool_gemm_i8(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* C_bits, int M, int N, int K,
+                     int lda, int ldbt, int ldc, int accumulate, void* stream) {
+    return bool_i8_gemm(A, Bt, C, C_bits, M, N, K, lda, ldbt, ldc, accumulate, 0, 0, as_stream(stream));
+}
+
+size_t smx_bool_warshall_i8_workspace_bytes(int n, int ld) {
+    if (n <= 0 || ld < n) return 0;
+    return tc_ws_bytes(n, ld);
+}
+
+int smx_bool_warshall_i8(uint8_t* T, int n, int ld, void* ws, size_t ws_bytes, void* stream) {
+    return bool_warshall_i8(T, n, ld, ws, ws_bytes, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,37 @@
+// Shared helpers for the semimat_b200 kernels (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/semimat_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "semimat_b200 targets sm_100a only"
+#endif
+
+#define SMX_RETURN_LAUNCH()                          \
+    do {                                             \
+        cudaError_t _e = cudaGetLastError();         \
+        return _e == cudaSuccess ? SMX_OK : (int)_e; \
+    } while (0)
+
+#define SMX_TRY(expr)                 \
+    do {                              \
+        int _rc = (expr);             \
+        if (_rc != SMX_OK) return _rc; \
+    } while (0)
+
+namespace smx {
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool ld_ok(long long ld, int elem_bytes) { return ((ld * elem_bytes) & 15) == 0; }
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// Saturation limit S = 2^w - 1 per element type.
+template <typename T> struct Limit;
+template <> struct Limit<uint8_t>  { static constexpr uint32_t value = 0xFFu; };
+template <> struct Limit<uint16_t> { static constexpr uint32_t value = 0xFFFFu; };
+template <> struct Limit<uint32_t> { static constexpr uint32_t value = 0xFFFFFFFFu; };
+
+}  // namespace smx

@@ -1,0 +1,391 @@
+// Saturated semiring GEMM on CUDA cores: C = (acc ? C : I) (+) A (x) B.
+//
+// Replaces the outer-product sweeps _mul_vector / _minplus_mul_vector
+// (pkg/src/semimat/antidist.py:361-371, :412-422).  The reference folds one
+// candidate row per k; here every (i, j, k) cell-update is computed densely
+// (the reference's zero-skip is an optimisation only: a skipped A entry is
+// the (x)-annihilator and (+)-neutral, so including it changes nothing).
+//
+// Tiling (B200-first): a CTA owns a BM x BN output tile held in registers,
+// TM rows x TNW words per thread.  Per k-tile of BK, A and B are read from
+// HBM/L2 with 16-byte vector loads into registers (prefetched one k-tile
+// ahead), converted to the canonical distance form and stored to a
+// double-buffered shared-memory stage:
+//   As[k][row] = {splat(a), splat(S - a)}  (or just splat(a) for u8)
+//   Bs[k][word] = lane word of B
+// so the inner loop is nothing but LDS.128 broadcasts and the 1- or
+// 2-instruction lane update of semiring.cuh (the paper's SSE inner loop,
+// P:351-375, one 32-bit word = 2 lanes wide, 32 threads x 4 SMSPs deep).
+// Arithmetic intensity: BM*BN*BK cells per (BM + BN)*BK*elem bytes staged;
+// the kernel is bound by packed-integer issue, not HBM.
+#pragma once
+#include <stdlib.h>
+
+#include <type_traits>
+
+#include "semiring.cuh"
+
+namespace smx {
+
+template <typename T>
+struct GemmArgs {
+    const T* A;
+    const T* B;
+    T* C;
+    int M, N, K;
+    long long lda, ldb, ldc;
+    int anti;
+    int accumulate;
+    int skip_tile0;   // first M-tile (in units of BM) to skip
+    int skip_tiles;   // number of M-tiles skipped
+};
+
+template <typename T, int BM_, int BNW_, int BK_, int TM_, int TNW_, int MINB_>
+struct GemmCfg {
+    static constexpr int MINB = MINB_;
+    using L = Lane<T>;
+    static constexpr int BM = BM_, BNW = BNW_, BK = BK_, TM = TM_, TNW = TNW_;
+    static constexpr int CPW = L::kCellsPerWord;
+    static constexpr int BN = BNW * CPW;            // output cells per tile row
+    static constexpr int E = L::kCellsPerChunk;     // cells per 16-byte chunk
+    static constexpr int WPC = L::kWordsPerChunk;   // canonical words per chunk
+    static constexpr int TCOLS = BNW / TNW;
+    static constexpr int THREADS = (BM / TM) * TCOLS;
+    static constexpr int HW = TNW / 2;              // words per half-group
+    static constexpr int A_CPR = BK / E;            // A chunks per tile row
+    static constexpr int A_CHUNKS = BM * A_CPR;
+    static constexpr int A_PT = (A_CHUNKS + THREADS - 1) / THREADS;
+    static constexpr int B_CPR = BNW / WPC;
+    static constexpr int B_CHUNKS = BK * B_CPR;
+    static constexpr int B_PT = (B_CHUNKS + THREADS - 1) / THREADS;
+    using AEl = typename std::conditional<L::kOneInstr, uint32_t, uint2>::type;
+    static constexpr size_t SMEM = 2ull * BK * BM * sizeof(AEl) + 2ull * BK * BNW * 4;
+    static_assert(BK % E == 0, "BK must hold whole chunks");
+    static_assert(BNW % WPC == 0, "BNW must hold whole chunks");
+    static_assert(HW == 2 || HW == 4, "half-group must be 2 or 4 words");
+};
+
+// --- C row-group load/store (HW canonical words starting at cell gc) -------
+template <typename T, int HW>
+__device__ __forceinline__ void load_c_group(const T* crow, int gc, int N, bool anti,
+                                             uint32_t* w) {
+    using L = Lane<T>;
+    constexpr int CELLS = HW * L::kCellsPerWord;
+    const uint32_t m = anti ? 0xFFFFFFFFu : 0u;
+    if (gc + CELLS <= N) {
+        if constexpr (std::is_same<T, uint8_t>::value) {
+            if constexpr (HW == 4) {
+                uint2 v = *reinterpret_cast<const uint2*>(crow + gc);
+                v.x ^= m; v.y ^= m;
+                w[0] = __byte_perm(v.x, 0u, 0x4140); w[1] = __byte_perm(v.x, 0u, 0x4342);
+                w[2] = __byte_perm(v.y, 0u, 0x4140); w[3] = __byte_perm(v.y, 0u, 0x4342);
+            } else {
+                uint32_t v = *reinterpret_cast<const uint32_t*>(crow + gc) ^ m;
+                w[0] = __byte_perm(v, 0u, 0x4140); w[1] = __byte_perm(v, 0u, 0x4342);
+            }
+        } else {
+            if constexpr (HW == 4) {
+                uint4 v = *reinterpret_cast<const uint4*>(crow + gc);
+                w[0] = v.x ^ m; w[1] = v.y ^ m; w[2] = v.z ^ m; w[3] = v.w ^ m;
+            } else {
+                uint2 v = *reinterpret_cast<const uint2*>(crow + gc);
+                w[0] = v.x ^ m; w[1] = v.y ^ m;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < HW; ++i) w[i] = L::kIdentityWord;
+        for (int c = 0; c < CELLS; ++c) {
+            if (gc + c >= N) break;
+            uint32_t v = static_cast<uint32_t>(crow[gc + c]);
+            v = anti ? (L::kS - v) : v;
+            if (L::kCellsPerWord == 2) {
+                const int wi = c >> 1, sh = (c & 1) * 16;
+                w[wi] = (w[wi] & ~(0xFFFFu << sh)) | (v << sh);
+            } else {
+                w[c] = v;
+            }
+        }
+    }
+}
+
+template <typename T, int HW>
+__device__ __forceinline__ void store_c_group(T* crow, int gc, int N, bool anti,
+                                              const uint32_t* w) {
+    using L = Lane<T>;
+    constexpr int CELLS = HW * L::kCellsPerWord;
+    if (gc + CELLS <= N) {
+        uint32_t o[HW];
+        words_to_store<T, HW>(w, anti, o);
+        if constexpr (std::is_same<T, uint8_t>::value) {
+            if constexpr (HW == 4) *reinterpret_cast<uint2*>(crow + gc) = make_uint2(o[0], o[1]);
+            else *reinterpret_cast<uint32_t*>(crow + gc) = o[0];
+        } else {
+            if constexpr (HW == 4)
+                *reinterpret_cast<uint4*>(crow + gc) = make_uint4(o[0], o[1], o[2], o[3]);
+            else *reinterpret_cast<uint2*>(crow + gc) = make_uint2(o[0], o[1]);
+        }
+    } else {
+        for (int c = 0; c < CELLS; ++c) {
+            if (gc + c >= N) break;
+            uint32_t v = word_cell<T>(w, c);
+            v = anti ? (L::kS - v) : v;
+            crow[gc + c] = static_cast<T>(v);
+        }
+    }
+}
+
+// Raw 16-byte chunk loads (conversion to canonical words happens at the smem
+// store, so staging costs 4 registers per chunk for every element type).
+// Out-of-range cells read as the storage encoding of the (+)-identity:
+// 0 for anti-distance, S (all ones) for distance.
+template <typename T>
+__device__ __forceinline__ uint4 identity_chunk(bool anti) {
+    const uint32_t v = anti ? 0u : 0xFFFFFFFFu;
+    return make_uint4(v, v, v, v);
+}
+
+template <typename Cfg, typename T>
+__device__ __forceinline__ uint4 load_a_chunk(const GemmArgs<T>& p, int row0, int k0, int c) {
+    const int r = c / Cfg::A_CPR, kc = c % Cfg::A_CPR;
+    const int grow = row0 + r, gk = k0 + kc * Cfg::E;
+    if (c < Cfg::A_CHUNKS && grow < p.M && gk < p.K) {
+        uint4 raw = __ldg(reinterpret_cast<const uint4*>(p.A + (long long)grow * p.lda + gk));
+        if (gk + Cfg::E > p.K) {   // chunk straddles K: cells >= K are identity
+            const int valid = p.K - gk;
+            const uint32_t id = p.anti ? 0u : 0xFFFFFFFFu;
+            uint32_t v[4] = {raw.x, raw.y, raw.z, raw.w};
+            constexpr int CPU = 4 / sizeof(T);   // cells per 32-bit storage word
+#pragma unroll
+            for (int j = 0; j < Cfg::E; ++j) {
+                if (j >= valid) {
+                    const int wi = j / CPU, sh = (j % CPU) * 8 * sizeof(T);
+                    const uint32_t m = (sizeof(T) == 4) ? 0xFFFFFFFFu : (((1u << (8 * sizeof(T))) - 1u) << sh);
+                    v[wi] = (v[wi] & ~m) | (id & m);
+                }
+            }
+            raw = make_uint4(v[0], v[1], v[2], v[3]);
+        }
+        return raw;
+    }
+    return identity_chunk<T>(p.anti);
+}
+
+template <typename Cfg, typename T>
+__device__ __forceinline__ uint4 load_b_chunk(const GemmArgs<T>& p, int col0, int k0, int c) {
+    const int kr = c / Cfg::B_CPR, wc = c % Cfg::B_CPR;
+    const int gk = k0 + kr, gc = col0 + wc * Cfg::E;
+    if (c < Cfg::B_CHUNKS && gk < p.K && gc < p.N)
+        return __ldg(reinterpret_cast<const uint4*>(p.B + (long long)gk * p.ldb + gc));
+    return identity_chunk<T>(p.anti);
+}
+
+template <typename Cfg, typename T>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(const GemmArgs<T> p) {
+    using L = Lane<T>;
+    using AEl = typename Cfg::AEl;
+    constexpr int BM = Cfg::BM, BNW = Cfg::BNW, BK = Cfg::BK, TM = Cfg::TM, TNW = Cfg::TNW;
+    constexpr int HW = Cfg::HW, WPC = Cfg::WPC, E = Cfg::E, CPW = Cfg::CPW;
+
+    extern __shared__ uint4 smem_raw[];
+    AEl* As = reinterpret_cast<AEl*>(smem_raw);                    // [2][BK][BM]
+    uint32_t* Bs = reinterpret_cast<uint32_t*>(As + 2 * BK * BM);  // [2][BK][BNW]
+
+    const int tid = threadIdx.x;
+    int mt = blockIdx.y;
+    if (mt >= p.skip_tile0) mt += p.skip_tiles;
+    const int row0 = mt * BM;
+    const int col0 = blockIdx.x * Cfg::BN;
+    const bool anti = p.anti != 0;
+    const int tc = tid % Cfg::TCOLS, tr = tid / Cfg::TCOLS;
+
+    // ---- accumulator init: C (accumulate) or the (+)-identity ------------
+    uint32_t acc[TM][TNW];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int grow = row0 + tr * TM + i;
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            uint32_t* w = &acc[i][g * HW];
+            if (p.accumulate && grow < p.M) {
+                const int gc = col0 + (g * (BNW / 2) + tc * HW) * CPW;
+                load_c_group<T, HW>(p.C + (long long)grow * p.ldc, gc, p.N, anti, w);
+            } else {
+#pragma unroll
+                for (int j = 0; j < HW; ++j) w[j] = L::kIdentityWord;
+            }
+        }
+    }
+
+    uint4 a_st[Cfg::A_PT];
+    uint4 b_st[Cfg::B_PT];
+
+    auto gload = [&](int k0) {
+#pragma unroll
+        for (int i = 0; i < Cfg::A_PT; ++i) a_st[i] = load_a_chunk<Cfg>(p, row0, k0, tid + i * Cfg::THREADS);
+#pragma unroll
+        for (int i = 0; i < Cfg::B_PT; ++i) b_st[i] = load_b_chunk<Cfg>(p, col0, k0, tid + i * Cfg::THREADS);
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+        for (int i = 0; i < Cfg::A_PT; ++i) {
+            const int c = tid + i * Cfg::THREADS;
+            if (c < Cfg::A_CHUNKS) {
+                const int r = c / Cfg::A_CPR, kc = c % Cfg::A_CPR;
+                AEl* dst = As + (buf * BK + kc * E) * BM + r;
+                uint32_t w[WPC];
+                chunk_to_words<T>(a_st[i], anti, w);
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const uint32_t v = word_cell<T>(w, j);
+                    if constexpr (L::kOneInstr) {
+                        dst[j * BM] = L::splat(v);
+                    } else {
+                        dst[j * BM] = make_uint2(L::splat(v), L::splat(L::kS - v));
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < Cfg::B_PT; ++i) {
+            const int c = tid + i * Cfg::THREADS;
+            if (c < Cfg::B_CHUNKS) {
+                const int kr = c / Cfg::B_CPR, wc = c % Cfg::B_CPR;
+                uint4* dst = reinterpret_cast<uint4*>(Bs + (buf * BK + kr) * BNW + wc * WPC);
+                uint32_t w[WPC];
+                chunk_to_words<T>(b_st[i], anti, w);
+#pragma unroll
+                for (int q = 0; q < WPC / 4; ++q)
+                    dst[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+            }
+        }
+    };
+
+    const int nkt = (p.K + BK - 1) / BK;
+    if (nkt > 0) {
+        gload(0);
+        sstore(0);
+        __syncthreads();
+    }
+    for (int kt = 0; kt < nkt; ++kt) {
+        const int buf = kt & 1;
+        if (kt + 1 < nkt) gload((kt + 1) * BK);
+        const AEl* Ab = As + buf * BK * BM + tr * TM;
+        const uint32_t* Bb = Bs + buf * BK * BNW + tc * HW;
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            uint32_t b[TNW];
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                const uint32_t* src = Bb + kk * BNW + g * (BNW / 2);
+                if constexpr (HW == 4) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(src);
+                    b[g * 4 + 0] = v.x; b[g * 4 + 1] = v.y; b[g * 4 + 2] = v.z; b[g * 4 + 3] = v.w;
+                } else {
+                    const uint2 v = *reinterpret_cast<const uint2*>(src);
+                    b[g * 2 + 0] = v.x; b[g * 2 + 1] = v.y;
+                }
+            }
+            AEl a[TM];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) a[i] = Ab[kk * BM + i];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) {
+#pragma unroll
+                for (int j = 0; j < TNW; ++j) {
+                    if constexpr (L::kOneInstr) acc[i][j] = L::step(acc[i][j], b[j], a[i], 0u);
+                    else acc[i][j] = L::step(acc[i][j], b[j], a[i].x, a[i].y);
+                }
+            }
+        }
+        if (kt + 1 < nkt) sstore(buf ^ 1);
+        __syncthreads();
+    }
+
+    // ---- epilogue ---------------------------------------------------------
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int grow = row0 + tr * TM + i;
+        if (grow >= p.M) continue;
+        T* crow = p.C + (long long)grow * p.ldc;
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            const int gc = col0 + (g * (BNW / 2) + tc * HW) * CPW;
+            store_c_group<T, HW>(crow, gc, p.N, anti, &acc[i][g * HW]);
+        }
+    }
+}
+
+// Tile configurations.  "Large" is the throughput tile (128 x 256 cells for
+// u8/u16); variant 0 runs 512 threads with 4 x 8-word thread tiles (128
+// registers, 16 warps/SM), variant 1 runs 256 threads with 8 x 8 (168
+// registers, 8 warps/SM, fewer shared-memory loads per cell).  "Small" keeps
+// >= 2 waves on 148 SMs for thin products such as the FW pivot row panel.
+template <typename T> using LargeCfg = GemmCfg<T, 128, 128, 16, 4, 8, 1>;
+template <typename T> using LargeCfgW = GemmCfg<T, 128, 128, 16, 8, 8, 1>;
+template <typename T> using SmallCfg = GemmCfg<T, 64, 64, 16, 4, 4, 2>;
+
+inline int large_variant() {
+    static int v = [] {
+        const char* s = getenv("SMX_GEMM_VARIANT");
+        return s ? atoi(s) : 0;
+    }();
+    return v;
+}
+
+template <typename T>
+int launch_large(const GemmArgs<T>& a, cudaStream_t stream);
+
+template <typename Cfg, typename T>
+int launch_semiring_gemm(const GemmArgs<T>& a, cudaStream_t stream) {
+    auto kern = semiring_gemm_kernel<Cfg, T>;
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)Cfg::SMEM);
+        if (e != cudaSuccess) return (int)e;
+        configured = true;
+    }
+    const int mtiles = ceil_div(a.M, Cfg::BM) - a.skip_tiles;
+    const int ntiles = ceil_div(a.N, Cfg::BN);
+    if (mtiles <= 0 || ntiles <= 0) return SMX_OK;
+    dim3 grid(ntiles, mtiles);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM, stream>>>(a);
+    SMX_RETURN_LAUNCH();
+}
+
+// Validates and dispatches one product; used by every entry point.
+template <typename T>
+int semiring_gemm(const T* A, const T* B, T* C, int M, int N, int K, long long lda,
+                  long long ldb, long long ldc, int kind, int accumulate, int skip_row0,
+                  int skip_rows, cudaStream_t stream) {
+    if (M < 0 || N < 0 || K < 0 || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
+    if (M == 0 || N == 0) return SMX_OK;
+    if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return SMX_E_ALIGN;
+    if (!ld_ok(lda, sizeof(T)) || !ld_ok(ldb, sizeof(T)) || !ld_ok(ldc, sizeof(T)))
+        return SMX_E_ALIGN;
+    if (lda < K || ldb < N || ldc < N) return SMX_E_ARG;
+    GemmArgs<T> a{A, B, C, M, N, K, lda, ldb, ldc, kind == SMX_ANTI, accumulate != 0, 0, 0};
+    if (skip_rows > 0) {
+        // skip ranges are whole 128-row tiles of the large config (FW phase 3)
+        if (skip_row0 % LargeCfg<T>::BM) return SMX_E_ARG;
+        a.skip_tile0 = skip_row0 / LargeCfg<T>::BM;
+        a.skip_tiles = ceil_div(skip_rows, LargeCfg<T>::BM);
+        const int total = ceil_div(M, LargeCfg<T>::BM);
+        if (a.skip_tile0 + a.skip_tiles > total) a.skip_tiles = total - a.skip_tile0;
+        if (a.skip_tiles < 0) return SMX_E_ARG;
+        return launch_large<T>(a, stream);
+    }
+    const long long large_tiles = (long long)ceil_div(M, LargeCfg<T>::BM) * ceil_div(N, LargeCfg<T>::BN);
+    if (large_tiles >= 2LL * 148) return launch_large<T>(a, stream);
+    return launch_semiring_gemm<SmallCfg<T>>(a, stream);
+}
+
+template <typename T>
+int launch_large(const GemmArgs<T>& a, cudaStream_t stream) {
+    static_assert(LargeCfg<T>::BM == LargeCfgW<T>::BM && LargeCfg<T>::BN == LargeCfgW<T>::BN, "");
+    if (large_variant() == 1) return launch_semiring_gemm<LargeCfgW<T>>(a, stream);
+    return launch_semiring_gemm<LargeCfg<T>>(a, stream);
+}
+
+}  // namespace smx

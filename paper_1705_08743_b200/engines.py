@@ -1,0 +1,77 @@
+"""Device engines behind the matrix classes: thin calls into libsemimat_b200.so.
+
+These replace the reference's compute engines one for one
+(pkg/src/semimat/antidist.py:361-458; boolmat.py:151-189).  Each function
+takes CUDA tensors in the reference's storage layout, allocates the result
+and any workspace from torch's caching allocator, and launches on torch's
+current stream.  Nothing here falls back to the CPU.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _native
+from ._native import SMX_ANTI, SMX_DIST, check, lib, stream_ptr
+
+_GEMM = {8: "smx_semiring_gemm_u8", 16: "smx_semiring_gemm_u16", 32: "smx_semiring_gemm_u32"}
+_FW = {8: "smx_fw_u8", 16: "smx_fw_u16", 32: "smx_fw_u32"}
+
+
+def lane_mul(a: torch.Tensor, b: torch.Tensor, inner: int, width: int, anti: bool,
+             out: torch.Tensor | None = None) -> torch.Tensor:
+    """C = A (x) B on padded lane storage; replaces _mul_vector (antidist.py:361-371)
+    and _minplus_mul_vector (:412-422).  Computes the padded width too: B's
+    padding lanes are the (+)-identity, so C's padding comes out as identity."""
+    rows, cols_p = a.shape[0], b.shape[1]
+    if out is None:
+        out = torch.empty((rows, cols_p), dtype=a.dtype, device=a.device)
+    fn = getattr(lib(), _GEMM[width])
+    check(fn(a.data_ptr(), b.data_ptr(), out.data_ptr(), rows, cols_p, inner, a.shape[1],
+             b.shape[1], out.shape[1], SMX_ANTI if anti else SMX_DIST, 0,
+             stream_ptr(a.device)), _GEMM[width])
+    return out
+
+
+def lane_close_(t: torch.Tensor, n: int, width: int, anti: bool) -> torch.Tensor:
+    """In-place blocked Floyd-Warshall; replaces _close_vector (antidist.py:390-398)
+    and _minplus_close_vector (:440-448)."""
+    ld = t.shape[1]
+    nbytes = lib().smx_fw_workspace_bytes(n, ld, width // 8)
+    ws = _native.workspace(nbytes, t.device)
+    fn = getattr(lib(), _FW[width])
+    check(fn(t.data_ptr(), n, ld, SMX_ANTI if anti else SMX_DIST, ws.data_ptr(), nbytes,
+             stream_ptr(t.device)), _FW[width])
+    return t
+
+
+def bool_mul_bits(a, b):
+    """Bit-packed OR/AND product (the comparison variant); boolmat.py:151-172."""
+    from .boolmat import BoolMatrix, _stride_words
+    out = torch.zeros((a.rows, _stride_words(b.cols)), dtype=torch.int32, device=a.device)
+    check(lib().smx_bool_gemm_bits(a._words.data_ptr(), b._words.data_ptr(), out.data_ptr(),
+                                   a.rows, (b.cols + 31) // 32, a.cols, a.stride_words,
+                                   b.stride_words, out.shape[1], 0, stream_ptr(a.device)),
+          "smx_bool_gemm_bits")
+    return BoolMatrix(a.rows, b.cols, out)
+
+
+def bool_mul(a, b):
+    """BoolMatrix.__mul__ engine."""
+    return bool_mul_bits(a, b)
+
+
+def bool_closure_bits(m):
+    """Blocked Warshall on packed bits; boolmat.py:174-189."""
+    from .boolmat import BoolMatrix
+    words = m._words.clone()
+    nbytes = lib().smx_bool_warshall_workspace_bytes(m.rows, m.stride_words)
+    ws = _native.workspace(nbytes, m.device)
+    check(lib().smx_bool_warshall_bits(words.data_ptr(), m.rows, m.stride_words, ws.data_ptr(),
+                                       nbytes, stream_ptr(m.device)), "smx_bool_warshall_bits")
+    return BoolMatrix(m.rows, m.cols, words)
+
+
+def bool_closure(m):
+    """BoolMatrix.transitive_closure engine."""
+    return bool_closure_bits(m)

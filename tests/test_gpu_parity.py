@@ -1,0 +1,245 @@
+"""GPU parity: the sm_100a path through the reference-facing class API must be
+bit-identical to the reference (golden vectors made by the reference itself)
+and to the pinned CPU oracle.  All arithmetic is integer, so every comparison
+is exact equality -- there is no tolerance anywhere in this file.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1705_08743_b200 import AntidistMatrix, BoolMatrix, DistMatrix, engines, workloads
+
+pytestmark = pytest.mark.gpu
+
+CLS = {"anti": AntidistMatrix, "dist": DistMatrix}
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def lane(kind, data, cols, width):
+    return CLS[kind](data.shape[0], cols, width, np.ascontiguousarray(data))
+
+
+# -- golden small cases: products, closures, Boolean ---------------------------
+
+def test_small_products(small_cases):
+    n = 0
+    for meta, arr in small_cases:
+        if meta["op"] != "mul":
+            continue
+        a = lane(meta["kind"], arr["a"], meta["inner"], meta["width"])
+        b = lane(meta["kind"], arr["b"], meta["cols"], meta["width"])
+        got = (a * b).data
+        np.testing.assert_array_equal(got, arr["out"], err_msg=meta["name"])
+        n += 1
+    assert n >= 90
+
+
+def test_small_closures(small_cases):
+    for meta, arr in small_cases:
+        if meta["op"] != "closure":
+            continue
+        m = lane(meta["kind"], arr["t"], meta["dim"], meta["width"])
+        got = m.transitive_closure()
+        np.testing.assert_array_equal(got.data, arr["out"], err_msg=meta["name"])
+        assert m.data.tobytes() == arr["t"].tobytes()          # closure() leaves the input alone
+        m.transitive_close()                                   # in-place variant agrees
+        np.testing.assert_array_equal(m.data, arr["out"], err_msg=meta["name"])
+
+
+def test_small_bool(small_cases):
+    for meta, arr in small_cases:
+        if meta["op"] == "bool_mul":
+            got = BoolMatrix.from_numpy(arr["a"]) * BoolMatrix.from_numpy(arr["b"])
+            np.testing.assert_array_equal(got.blocks, arr["out_blocks"], err_msg=meta["name"])
+            assert got.to_lists() == arr["out"].tolist()
+            bits = engines.bool_mul_bits(BoolMatrix.from_numpy(arr["a"]), BoolMatrix.from_numpy(arr["b"]))
+            np.testing.assert_array_equal(bits.blocks, arr["out_blocks"], err_msg=meta["name"])
+        elif meta["op"] == "bool_closure":
+            m = BoolMatrix.from_numpy(arr["t"])
+            np.testing.assert_array_equal(m.transitive_closure().blocks, arr["out_blocks"],
+                                          err_msg=meta["name"])
+            assert m.reflexive_transitive_closure().to_lists() == arr["refl"].tolist()
+
+
+def test_samples(samples):
+    a = AntidistMatrix.from_lists(samples["a4"]["rows"], 8)
+    b = AntidistMatrix.from_lists(samples["b4"]["rows"], 8)
+    assert (a * b).to_lists() == samples["a4_times_b4"]
+    for name in ("chain3", "cycle3"):
+        s = samples[name]
+        assert BoolMatrix.from_lists(s["bool_adjacency"]).transitive_closure().to_lists() == s["bool_closure"]
+        assert BoolMatrix.from_lists(s["bool_adjacency"]).reflexive_transitive_closure().to_lists() == \
+            s["bool_reflexive"]
+        assert AntidistMatrix.from_lists(s["antidist_adjacency"], 8).transitive_closure().to_lists() == \
+            s["antidist_closure"]
+        assert DistMatrix.from_lists(s["dist_adjacency"], 8).transitive_closure().to_lists() == \
+            s["dist_closure"]
+
+
+def test_reference_golden_values():
+    """tests/test_antidist.py:130-206 golden values, through the GPU classes."""
+    a = AntidistMatrix.zeros(3, 3, 8)
+    a.set(0, 1, 252)
+    b = AntidistMatrix.zeros(3, 3, 8)
+    b.set(1, 2, 251)
+    assert (a * b).get(0, 2) == 248
+    m = AntidistMatrix.from_edges(3, [(0, 1, 3), (1, 2, 4)], 8)
+    assert m.transitive_closure().get(0, 2) == 248
+    for width, want in ((8, 0), (16, 65535 - 300)):
+        chain = AntidistMatrix.from_edges(31, [(i, i + 1, 10) for i in range(30)], width)
+        assert chain.transitive_closure().get(0, 30) == want
+    d = DistMatrix.from_edges(2, [(0, 1, 3), (1, 0, 4)], 8).transitive_closure()
+    assert d.get(0, 0) == 7 and d.get(1, 1) == 7
+
+
+# -- BASELINE.json configurations: sha256 of the reference output ---------------
+
+def _gpu_output(cfg, n):
+    inputs = workloads.make_inputs(cfg, n)
+    if cfg.op == "bool_mul":
+        out = (BoolMatrix.from_numpy(inputs[0]) * BoolMatrix.from_numpy(inputs[1])).blocks
+    elif cfg.op == "bool_closure":
+        out = BoolMatrix.from_numpy(inputs[0]).transitive_closure().blocks
+    elif cfg.op == "mul":
+        out = (lane("anti", inputs[0], n, cfg.width) * lane("anti", inputs[1], n, cfg.width)).data
+    else:
+        out = lane("anti", inputs[0], n, cfg.width).transitive_closure().data
+    return out
+
+
+@pytest.mark.parametrize("name", list(workloads.CONFIGS))
+def test_config_matches_reference_digest(config_digests, name):
+    cfg = workloads.CONFIGS[name]
+    for d in config_digests:
+        if d["config"] == name:
+            assert sha(_gpu_output(cfg, d["n"])) == d["output_sha256"], (name, d["n"])
+
+
+# -- full-size, size-independent properties -------------------------------------
+
+def test_fw_full_size_bellman_fixpoint():
+    """C4 at n = 8192: T+ = T (+) T+ (x) T, and closing T+ again changes nothing."""
+    cfg = workloads.CONFIGS["c4_fw_u16"]
+    (t,) = workloads.make_inputs(cfg)
+    a = lane("anti", t, cfg.n, 16)
+    c = a.transitive_closure()
+    assert (a | (c * a)) == c
+    assert c.transitive_closure() == c
+
+
+def test_widths_agree_on_small_weights():
+    """Same graph at u8 / u16 / u32 gives the same distances while they fit (test_antidist.py:235-246)."""
+    rng = np.random.default_rng(7)
+    n = 300
+    edges = [(int(u), int(v), int(w)) for u, v, w in
+             zip(rng.integers(0, n, 3000), rng.integers(0, n, 3000), rng.integers(1, 4, 3000))]
+    d = {w: DistMatrix.from_edges(n, edges, w).transitive_closure().to_numpy()[:, :n].astype(np.int64)
+         for w in (8, 16, 32)}
+    assert (d[16] < 255).all()
+    np.testing.assert_array_equal(d[8], d[16])
+    np.testing.assert_array_equal(d[16], d[32])
+
+
+def test_anti_and_dist_are_complement_duals():
+    """~(A * B) == (~A) * (~B) and ~closure(A) == closure(~A) (test_antidist.py:277-311)."""
+    cfg = workloads.CONFIGS["c3_mul_u16"]
+    a_np, b_np = workloads.make_inputs(cfg, 1000)
+    a, b = lane("anti", a_np, 1000, 16), lane("anti", b_np, 1000, 16)
+    assert ~(a * b) == (~a) * (~b)
+    assert ~a.transitive_closure() == (~a).transitive_closure()
+
+
+def test_ragged_and_edge_shapes(oracle_lib):
+    rng = np.random.default_rng(11)
+    for width in (8, 16, 32):
+        for rows, inner, cols in [(1, 1, 1), (1000, 777, 1001), (129, 3, 257), (5, 300, 2)]:
+            for kind in ("anti", "dist"):
+                lim = (1 << width) - 1
+                a_np = rng.integers(0, lim + 1, size=(rows, inner), dtype=np.uint64)
+                b_np = rng.integers(0, lim + 1, size=(inner, cols), dtype=np.uint64)
+                a = CLS[kind].from_lists(a_np.tolist(), width) if rows * inner < 5000 else \
+                    _fast_lane(kind, a_np, width)
+                b = CLS[kind].from_lists(b_np.tolist(), width) if inner * cols < 5000 else \
+                    _fast_lane(kind, b_np, width)
+                got = (a * b).data
+                want = oracle_lib.semiring_mul(a.data, b.data, inner, width, kind)
+                np.testing.assert_array_equal(got, want, err_msg=f"{width} {rows}x{inner}x{cols} {kind}")
+
+
+def _fast_lane(kind, vals, width):
+    rows, cols = vals.shape
+    lanes = {8: 16, 16: 8, 32: 4}[width]
+    dt = {8: np.uint8, 16: np.uint16, 32: np.uint32}[width]
+    pad = 0 if kind == "anti" else (1 << width) - 1
+    host = np.full((rows, -(-cols // lanes) * lanes), pad, dtype=dt)
+    host[:, :cols] = vals.astype(dt)
+    return CLS[kind](rows, cols, width, host)
+
+
+def test_fw_odd_sizes(oracle_lib):
+    """Closures whose size is not a multiple of the 128-vertex pivot block."""
+    rng = np.random.default_rng(5)
+    for n in (129, 200, 383, 640):
+        for width in (8, 16, 32):
+            lim = (1 << width) - 1
+            vals = np.where(rng.random((n, n)) < 0.03, lim - rng.integers(1, 30, (n, n)), 0)
+            m = _fast_lane("anti", vals, width)
+            np.testing.assert_array_equal(m.transitive_closure().data,
+                                          oracle_lib.semiring_close(m.data, width, "anti"),
+                                          err_msg=f"n={n} w={width}")
+            d = ~m
+            np.testing.assert_array_equal(d.transitive_closure().data,
+                                          oracle_lib.semiring_close(d.data, width, "dist"))
+
+
+def test_bool_odd_sizes(oracle_lib):
+    rng = np.random.default_rng(6)
+    for n in (257, 300, 700, 1500):
+        bits = (rng.random((n, n)) < 1.5 / n).astype(np.uint8)
+        m = BoolMatrix.from_numpy(bits)
+        want = oracle_lib.bool_close(oracle_lib.pack_bits(bits))
+        np.testing.assert_array_equal(m.transitive_closure().blocks, want, err_msg=f"n={n}")
+        b2 = (rng.random((n, 333)) < 0.01).astype(np.uint8)
+        want = oracle_lib.bool_mul(oracle_lib.pack_bits(bits), oracle_lib.pack_bits(b2), n)
+        np.testing.assert_array_equal((m * BoolMatrix.from_numpy(b2)).blocks, want)
+
+
+def test_errors_match_reference():
+    a = AntidistMatrix.zeros(2, 3, 8)
+    with pytest.raises(ValueError, match="inner dimensions disagree"):
+        a * AntidistMatrix.zeros(2, 3, 8)
+    with pytest.raises(ValueError, match="width mismatch"):
+        a * AntidistMatrix.zeros(3, 2, 16)
+    with pytest.raises(TypeError):
+        a * DistMatrix.unreachable(3, 2, 8)
+    with pytest.raises(ValueError, match="closure needs a square matrix"):
+        a.transitive_closure()
+    with pytest.raises(ValueError, match="closure needs a square matrix"):
+        BoolMatrix.zeros(2, 3).transitive_closure()
+    with pytest.raises(ValueError, match="inner dimensions disagree"):
+        BoolMatrix.zeros(2, 3) * BoolMatrix.zeros(2, 3)
+    with pytest.raises(TypeError):
+        BoolMatrix.zeros(2, 2) * a
+    with pytest.raises(ValueError):
+        AntidistMatrix.zeros(0, 2, 8)
+
+
+def test_c_abi_rejects_misaligned():
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    t = torch.zeros(64, 64, dtype=torch.uint16, device="cuda")
+    rc = lib.smx_semiring_gemm_u16(t.data_ptr() + 2, t.data_ptr(), t.data_ptr(), 8, 8, 8, 64, 64,
+                                   64, 0, 0, None)
+    assert rc == -2
+    rc = lib.smx_semiring_gemm_u16(t.data_ptr(), t.data_ptr(), t.data_ptr(), 8, 8, 8, 63, 64, 64, 0,
+                                   0, None)
+    assert rc == -2
+    assert lib.smx_fw_u16(t.data_ptr(), 300, 64, 0, None, 0, None) == -1

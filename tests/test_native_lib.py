@@ -1,0 +1,53 @@
+"""The C-ABI library builds for sm_100a, loads, and exports every declared
+symbol (CPU only: nothing here launches a kernel)."""
+
+from __future__ import annotations
+
+import re
+import subprocess
+
+from paper_1705_08743_b200 import _build, _native
+
+from conftest import REPO
+
+
+def header_symbols():
+    text = (REPO / "include" / "semimat_b200.h").read_text()
+    return sorted(set(re.findall(r"\b(smx_\w+)\s*\(", text)))
+
+
+def test_library_builds_and_loads():
+    path = _build.build()
+    assert path.exists()
+    lib = _native.lib()
+    assert lib.smx_version() >= 100
+
+
+def test_exports_every_header_symbol():
+    _build.build()
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_build.LIB)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (smx_\w+)", out))
+    missing = [s for s in header_symbols() if s not in exported]
+    assert not missing, f"declared in include/semimat_b200.h but not exported: {missing}"
+
+
+def test_binding_covers_header():
+    assert set(header_symbols()) <= set(_native.declared_symbols())
+
+
+def test_error_strings():
+    lib = _native.lib()
+    assert lib.smx_error_string(0) == b"ok"
+    assert b"aligned" in lib.smx_error_string(-2)
+
+
+def test_sm100a_cubin_and_native_instructions():
+    """The library carries sm_100a SASS with the native packed-integer ops."""
+    _build.build()
+    sass = subprocess.run(["cuobjdump", "-sass", str(_build.LIB)], capture_output=True, text=True,
+                          check=True).stdout
+    assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", str(_build.LIB)], capture_output=True,
+                                       text=True).stdout or "SM100" in sass.upper()
+    assert "VIADDMNMX.U16x2" in sass
+    assert "VIMNMX.U16x2" in sass
