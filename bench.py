@@ -1,0 +1,469 @@
+"""Benchmark: semiring matmul & Floyd-Warshall cell-updates/s (n^3/s) vs roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--n N]
+    python bench.py --impl reference ...      # the reference algorithm on the host CPU
+
+Default workload (BASELINE.json configs[4], the largest single-GPU config):
+Floyd-Warshall closure of the n = 32768 anti-distance u16 graph (density 0.02,
+w ~ U[1, 1000]); one step = one transitive_closure() of the whole matrix
+(copy + closure, exactly the reference's AntidistMatrix.transitive_closure).
+For N > 1 the driver launches one rank per GPU under torch.distributed.run;
+the closure is row-panel sharded with an NCCL broadcast of each pivot row
+panel (paper_1705_08743_b200/sharded.py) -- strong scaling, fixed n.
+
+Reported beside the device-resident throughput (`value`):
+  e2e          the same metric through the public API with host buffers
+               (pinned H2D of the input + closure + D2H of the result per step)
+  roofline     the dominant kernel (FW phase-3 semiring GEMM, 93+% of the
+               step) timed live with CUDA events, against the packed-integer
+               issue peak measured in this run by smx_int_issue_probe
+  cpu_baseline the reference algorithm (C restatement, all host threads) on a
+               bounded sample of the same workload, rank 0 at N = 1 only
+  clocks       SM clocks and throttle reasons sampled during the timed region
+Inputs (2 GiB at n = 32768) are larger than the 126 MB L2, so no flush is
+needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "Semiring matmul & Floyd-Warshall cell-updates/s (N^3/s) vs roofline, 1-8 GPU"
+UNIT = "cell-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", default="c5_fw_u16")
+    ap.add_argument("--n", type=int, default=None, help="override the config's n (testing)")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons (NVML) while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        reasons = [name for bit, name in self.REASONS.items() if self.reasons & bit and bit != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- helpers
+
+def cuda_time(fn, iters: int, warmup: int = 1):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / 1e3 / iters
+
+
+def measure_issue_peak():
+    """Packed-integer issue rate of the semiring inner-loop SASS on every SM."""
+    import ctypes
+    import torch
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, threads, iters = sms * 8, 256, 40000
+    sink = torch.zeros(blocks * threads, dtype=torch.int32, device="cuda")
+    out = {}
+    for one in (0, 1):
+        ipt = ctypes.c_longlong(0)
+        fn = lambda: _native.check(lib.smx_int_issue_probe(  # noqa: E731
+            sink.data_ptr(), blocks, threads, iters, one, ctypes.byref(ipt),
+            _native.stream_ptr()), "probe")
+        t = cuda_time(fn, 3, 1)
+        out["one" if one else "pair"] = blocks * threads * ipt.value / t
+    return out, sms
+
+
+def load_traffic(workload: str):
+    p = REPO / "profiles" / "traffic.json"
+    if p.exists():
+        return json.loads(p.read_text()).get(workload)
+    return None
+
+
+# --------------------------------------------------------------------------- CPU (reference algorithm)
+
+def cpu_fw_sample(n_sample: int, threads: int = 0):
+    """The reference algorithm (C restatement of _close_vector, all host
+    threads) on the c5 generator at n_sample: returns (cells/s, seconds, out)."""
+    import oracle
+    from paper_1705_08743_b200 import workloads
+    (t,) = workloads.make_inputs(workloads.CONFIGS["c5_fw_u16"], n_sample)
+    t0 = time.perf_counter()
+    out = oracle.semiring_close(t, 16, "anti", threads=threads)
+    dt = time.perf_counter() - t0
+    return n_sample ** 3 / dt, dt, out, t
+
+
+def cpu_mul_sample(cfg, n_sample: int, threads: int = 0):
+    import oracle
+    from paper_1705_08743_b200 import workloads
+    a, b = workloads.make_inputs(cfg, n_sample)
+    t0 = time.perf_counter()
+    out = oracle.semiring_mul(a, b, n_sample, cfg.width, "anti", threads=threads)
+    dt = time.perf_counter() - t0
+    return n_sample ** 3 / dt, dt, out
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference algorithm on host cores, same metric."""
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_1705_08743_b200 import workloads
+    oracle.build()
+    cfg = workloads.CONFIGS[args.workload]
+    threads = oracle.max_threads()
+    n_sample = {"closure": 2048, "mul": 2048, "bool_mul": 1024, "bool_closure": 4096}[cfg.op]
+
+    def step():
+        if cfg.op == "closure":
+            return cpu_fw_sample(n_sample, threads)[1]
+        if cfg.op == "mul":
+            return cpu_mul_sample(cfg, n_sample, threads)[1]
+        inputs = workloads.make_inputs(cfg, n_sample)
+        t0 = time.perf_counter()
+        if cfg.op == "bool_mul":
+            oracle.bool_mul(oracle.pack_bits(inputs[0]), oracle.pack_bits(inputs[1]), n_sample, threads)
+        else:
+            oracle.bool_close(oracle.pack_bits(inputs[0]), threads)
+        return time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        step()
+    secs = [step() for _ in range(args.steps)]
+    total = sum(secs)
+    value = n_sample ** 3 * args.steps / total
+    sample = (f"{cfg.name} at n={n_sample} (same generator and seed), one "
+              f"{'closure' if 'closure' in cfg.op else 'product'} per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u16" if cfg.width == 16 else f"u{cfg.width}", "data": "synthetic (seeded generator)",
+        "config": {"workload": cfg.name, "n": n_sample, "full_n": cfg.n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference = the reference package's numpy engine restated in C (oracle/), "
+                "OpenMP over rows; the reference itself is pure Python/numpy (1 core)",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU
+
+def run_ours(args, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1705_08743_b200 import AntidistMatrix, _native, engines, sharded, workloads
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = workloads.CONFIGS[args.workload]
+    n = args.n or cfg.n
+    lib = _native.lib()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- inputs (host generation, then HBM) --------------------------------
+    block = lib.smx_fw_block(cfg.width // 8)
+    if cfg.op == "closure":
+        r0, r1 = sharded.row_range(n, world, rank, block) if world > 1 else (0, n)
+        (host,) = workloads.make_inputs(cfg, n, rows=(r0, r1))
+        src = torch.from_numpy(host).to(dev)
+        work = torch.empty_like(src)
+        ops = sharded.CudaFwOps(cfg.width, anti=True)
+        fw = sharded.ShardedFW(n=n, rank=rank, world=world, ops=ops)
+        ws_bytes = lib.smx_fw_workspace_bytes(n, src.shape[1], cfg.width // 8)
+        ws = _native.workspace(ws_bytes, dev)
+
+        def step():
+            work.copy_(src)
+            if world == 1:
+                _native.check(getattr(lib, f"smx_fw_u{cfg.width}")(
+                    work.data_ptr(), n, work.shape[1], _native.SMX_ANTI, ws.data_ptr(), ws_bytes,
+                    _native.stream_ptr(dev)), "fw")
+            else:
+                fw.run(work)
+        units_per_step = n ** 3
+    elif cfg.op == "mul":
+        r0, r1 = sharded.row_range(n, world, rank, 128) if world > 1 else (0, n)
+        a_host, b_host = workloads.make_inputs(cfg, n, rows=(r0, r1))
+        a, b = torch.from_numpy(a_host).to(dev), torch.from_numpy(b_host).to(dev)
+        out = torch.empty((a.shape[0], b.shape[1]), dtype=a.dtype, device=dev)
+
+        def step():
+            sharded.sharded_mul(a, b, n, cfg.width, True, out)
+        units_per_step = n ** 3
+    else:
+        raise SystemExit(f"bench workload {cfg.name}: use tools/perf_probe.py for Boolean configs")
+
+    # ---- timed region -------------------------------------------------------
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    launches0 = lib.smx_launch_count()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        s.record()
+        for _ in range(args.steps):
+            step()
+        e.record()
+        barrier()
+    launches = lib.smx_launch_count() - launches0
+    secs = s.elapsed_time(e) / 1e3
+    t = torch.tensor([secs], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    secs = float(t.item())
+    value = units_per_step * args.steps / secs
+
+    # ---- parity of this very run at the oracle size (rank 0, N = 1) ------------
+    result = {}
+    if rank == 0 and world == 1:
+        peaks, sms = measure_issue_peak()
+        result["peaks"] = peaks
+        # dominant kernel: the FW phase-3 / product semiring GEMM, timed alone
+        # at the exact shape it has inside the step
+        if cfg.op == "closure":
+            cp = torch.empty((n, block), dtype=src.dtype, device=dev)
+            rows_skip = (n // 2 // block) * block
+
+            def dom():
+                _native.check(lib.smx_semiring_gemm_skip(
+                    cp.data_ptr(), work.data_ptr(), work.data_ptr(), n, n, block, block,
+                    work.shape[1], work.shape[1], cfg.width // 8, _native.SMX_ANTI, rows_skip, block,
+                    _native.stream_ptr(dev)), "phase3")
+            cells = (n - block) * n * block
+            launches_per_step = -(-n // block)
+        else:
+            dom = step
+            cells = n ** 3
+            launches_per_step = 1
+        dom_secs = cuda_time(dom, 5 if n >= 16384 else 20, 2)
+        achieved = cells / dom_secs
+        per_cell = 0.5 if cfg.width == 8 else 1.0          # issued instructions per cell-update
+        peak_cells = peaks["one" if cfg.width == 8 else "pair"] / per_cell
+        traffic = load_traffic(cfg.name)
+        result["roofline"] = {
+            "bound": "int_issue", "achieved": achieved / 1e12, "peak": peak_cells / 1e12,
+            "unit": "Tcell/s", "frac": achieved / peak_cells, "traffic": traffic,
+            "kernel": "semiring_gemm_kernel (FW phase 3)" if cfg.op == "closure" else "semiring_gemm_kernel",
+            "share_of_step": min(1.0, dom_secs * launches_per_step / (secs / args.steps)),
+            "peak_source": f"measured in this run: smx_int_issue_probe, {sms} SMs, "
+                           f"{'VIADDMNMX.U16x2' if cfg.width == 8 else 'VIMNMX.U16x2+VIADDMNMX.U16x2'} "
+                           f"at {peaks['one' if cfg.width == 8 else 'pair'] / 1e12:.2f} Tinstr/s; "
+                           f"{per_cell} instr per cell-update",
+            "algorithmic_bytes_per_launch": (n * block + block * n + 2 * n * n) * cfg.width // 8
+            if cfg.op == "closure" else 3 * n * n * cfg.width // 8,
+        }
+        # e2e through the public API with host buffers
+        if cfg.op == "closure":
+            pinned = torch.from_numpy(host).pin_memory()
+            res_host = torch.empty_like(pinned).pin_memory()
+
+            def e2e_step():
+                m = AntidistMatrix(n, n, cfg.width, pinned.to(dev, non_blocking=True))
+                c = m.transitive_closure()
+                res_host.copy_(c._data, non_blocking=True)
+            h2d = d2h = pinned.numel() * pinned.element_size()
+        else:
+            pa, pb = torch.from_numpy(a_host).pin_memory(), torch.from_numpy(b_host).pin_memory()
+            res_host = torch.empty((n, b_host.shape[1]), dtype=pa.dtype).pin_memory()
+
+            def e2e_step():
+                ma = AntidistMatrix(n, n, cfg.width, pa.to(dev, non_blocking=True))
+                mb = AntidistMatrix(n, n, cfg.width, pb.to(dev, non_blocking=True))
+                res_host.copy_((ma * mb)._data, non_blocking=True)
+            h2d = (pa.numel() + pb.numel()) * pa.element_size()
+            d2h = res_host.numel() * res_host.element_size()
+        e2e_steps = 2 if n >= 16384 else 5
+        e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_secs = (time.perf_counter() - t0) / e2e_steps
+        result["e2e"] = {"value": units_per_step / e2e_secs, "unit": UNIT,
+                         "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                         "ms_per_step": e2e_secs * 1e3}
+        # CPU baseline + parity at the oracle size (same generator)
+        if not args.no_cpu:
+            import oracle
+            oracle.build()
+            thr = oracle.max_threads()
+            n_s = cfg.oracle_n
+            if cfg.op == "closure":
+                cps, cdt, cpu_out, t_in = cpu_fw_sample(n_s, thr)
+                gpu_out = AntidistMatrix(n_s, n_s, 16, t_in).transitive_closure().data
+            else:
+                cps, cdt, cpu_out = cpu_mul_sample(cfg, n_s, thr)
+                ai, bi = workloads.make_inputs(cfg, n_s)
+                gpu_out = (AntidistMatrix(n_s, n_s, cfg.width, ai) *
+                           AntidistMatrix(n_s, n_s, cfg.width, bi)).data
+            result["cpu_baseline"] = {
+                "value": cps, "unit": UNIT, "cores": thr, "kind": "port",
+                "sample": f"{cfg.name} generator at n={n_s}, one "
+                          f"{'closure' if cfg.op == 'closure' else 'product'} "
+                          f"({cdt:.2f} s), C restatement of the reference engine, OpenMP rows"}
+            result["parity"] = {"n": n_s, "bit_exact_vs_oracle": bool(np.array_equal(gpu_out, cpu_out))}
+        if not args.no_secondary:
+            result["secondary"] = secondary(dev)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": f"u{cfg.width}", "data": "synthetic (seeded generator, SURVEY 8(d))",
+            "config": {"workload": cfg.name, "op": cfg.op, "n": n, "density": cfg.p,
+                       "weights": f"U[1,{cfg.wmax}]", "seed": cfg.seed,
+                       "parallelism": f"row-panel x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (no flush needed)" if n * n * cfg.width // 8 > 126e6
+                       else "inputs fit L2"},
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+        }
+        line.update(result)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def secondary(dev):
+    """Quick device timings of the other BASELINE configs (full size)."""
+    import torch
+    from paper_1705_08743_b200 import AntidistMatrix, BoolMatrix, engines, workloads
+    out = {}
+    for name in ("c3_mul_u8", "c3_mul_u16"):
+        cfg = workloads.CONFIGS[name]
+        a, b = workloads.make_inputs(cfg)
+        ta, tb = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+        res = torch.empty_like(ta)
+        t = cuda_time(lambda: engines.lane_mul(ta, tb, cfg.n, cfg.width, True, res), 10, 2)
+        out[name] = {"n": cfg.n, "seconds": t, "cells_per_s": cfg.n ** 3 / t}
+    cfg = workloads.CONFIGS["c4_fw_u16"]
+    (t8k,) = workloads.make_inputs(cfg)
+    src = torch.from_numpy(t8k).to(dev)
+    w = torch.empty_like(src)
+
+    def fw8k():
+        w.copy_(src)
+        engines.lane_close_(w, cfg.n, 16, True)
+    t = cuda_time(fw8k, 5, 1)
+    out["c4_fw_u16"] = {"n": cfg.n, "seconds": t, "cells_per_s": cfg.n ** 3 / t}
+    cfg = workloads.CONFIGS["c1_bool_mul"]
+    a, b = workloads.make_inputs(cfg)
+    ma, mb = BoolMatrix.from_numpy(a), BoolMatrix.from_numpy(b)
+    for eng in ("bool_mul_tc", "bool_mul_bits"):
+        fn = getattr(engines, eng)
+        t = cuda_time(lambda: fn(ma, mb), 50, 5)
+        out[f"c1_{eng}"] = {"n": cfg.n, "seconds": t, "cells_per_s": cfg.n ** 3 / t,
+                            "note": "includes unpack/transpose/alloc of the public call"}
+    cfg = workloads.CONFIGS["c2_bool_warshall"]
+    (t2,) = workloads.make_inputs(cfg)
+    m2 = BoolMatrix.from_numpy(t2)
+    for eng in ("bool_closure_tc", "bool_closure_bits"):
+        fn = getattr(engines, eng)
+        t = cuda_time(lambda: fn(m2), 10, 2)
+        out[f"c2_{eng}"] = {"n": cfg.n, "seconds": t, "cells_per_s": cfg.n ** 3 / t}
+    return out
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    return run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

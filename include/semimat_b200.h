@@ -45,6 +45,8 @@ enum { SMX_ANTI = 0, SMX_DIST = 1 };
 
 int smx_version(void);
 const char* smx_error_string(int code);
+/* Number of kernels this library has launched in the process so far. */
+unsigned long long smx_launch_count(void);
 
 /* ---- saturated lane semiring products ---------------------------------
  * Replace _mul_vector (pkg/src/semimat/antidist.py:361-371, called from

@@ -22,10 +22,11 @@ _lib = None
 _SIGS = {
     "smx_version": ([], c_int),
     "smx_error_string": ([c_int], ctypes.c_char_p),
+    "smx_launch_count": ([], ctypes.c_ulonglong),
     "smx_semiring_gemm_u8": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),
     "smx_semiring_gemm_u16": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),
     "smx_semiring_gemm_u32": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),
-    "smx_semiring_gemm_skip": ([c_void_p] * 3 + [c_int] * 11 + [c_void_p], c_int),
+    "smx_semiring_gemm_skip": ([c_void_p] * 3 + [c_int] * 10 + [c_void_p], c_int),
     "smx_fw_workspace_bytes": ([c_int, c_int, c_int], c_size_t),
     "smx_fw_u8": ([c_void_p, c_int, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),
     "smx_fw_u16": ([c_void_p, c_int, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),
@@ -43,12 +44,12 @@ _SIGS = {
     "smx_int_issue_probe":([c_void_p, c_int, c_int, c_int, c_int, POINTER(c_longlong), c_void_p],
                             c_int),
 }
-# Optional entry points (present once their kernels are built).
-_OPTIONAL = {
+_SIGS.update({
     "smx_bool_gemm_i8": ([c_void_p] * 4 + [c_int] * 7 + [c_void_p], c_int),
     "smx_bool_warshall_i8_workspace_bytes": ([c_int, c_int], c_size_t),
     "smx_bool_warshall_i8": ([c_void_p, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),
-}
+})
+_OPTIONAL: dict = {}
 
 
 def declared_symbols() -> list[str]:

@@ -3,9 +3,18 @@
 
 #include "common.cuh"
 
+#include <atomic>
+
+namespace smx {
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace smx
+
 extern "C" {
 
 int smx_version(void) { return 100; }
+
+unsigned long long smx_launch_count(void) { return smx::g_launches.load(); }
 
 const char* smx_error_string(int code) {
     switch (code) {

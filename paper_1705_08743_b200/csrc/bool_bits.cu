@@ -254,9 +254,8 @@ int bool_warshall_bits(uint32_t* T, int n, long long ld_w, void* ws, size_t ws_b
         const int kw0 = k0 / 32, bw = (bb + 31) / 32;
         uint32_t* rowK = T + (long long)k0 * ld_w;
         bool_pivot_kernel<<<1, kWarshallBlock, 0, s>>>(rowK + kw0, bb, ld_w);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return (int)e;
-        e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld_w * 4, cudaMemcpyDeviceToDevice, s);
+        SMX_LAUNCHED_OR_RETURN();
+        cudaError_t e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld_w * 4, cudaMemcpyDeviceToDevice, s);
         if (e != cudaSuccess) return (int)e;
         SMX_TRY(bool_bits_gemm(RP + kw0, RP, rowK, bb, nw, bb, ld_w, ld_w, ld_w, 1, 0, 0, s));
         e = cudaMemcpy2DAsync(CP, ldcp * 4, T + kw0, ld_w * 4, (size_t)bw * 4, n,

@@ -401,10 +401,9 @@ int bool_warshall_i8(uint8_t* T, int n, long long ld, void* ws, size_t ws_bytes,
         const int bb = n - k0 < kTcWarshallBlock ? n - k0 : kTcWarshallBlock;
         uint8_t* rowK = T + (long long)k0 * ld;
         bool_pivot_bytes_kernel<<<1, kTcWarshallBlock, 0, s>>>(rowK + k0, bb, ld);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return (int)e;
+        SMX_LAUNCHED_OR_RETURN();
         // phase 2: T[K,:] |= P* . RP   (B^T = RP^T)
-        e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld, cudaMemcpyDeviceToDevice, s);
+        cudaError_t e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld, cudaMemcpyDeviceToDevice, s);
         if (e != cudaSuccess) return (int)e;
         SMX_TRY(transpose_bytes(RP, RPt, bb, n, ld, B, s));
         SMX_TRY(bool_i8_gemm(RP + k0, RPt, rowK, nullptr, bb, n, bb, ld, B, ld, 1, 0, 0, s));

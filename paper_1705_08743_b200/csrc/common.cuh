@@ -9,10 +9,25 @@
 #error "semimat_b200 targets sm_100a only"
 #endif
 
+namespace smx {
+// Counts every kernel this library launches (smx_launch_count), so bench.py
+// reports launches it observed rather than a formula.
+void count_launch();
+}
+
+// Placed directly after each kernel launch.
 #define SMX_RETURN_LAUNCH()                          \
     do {                                             \
+        smx::count_launch();                         \
         cudaError_t _e = cudaGetLastError();         \
         return _e == cudaSuccess ? SMX_OK : (int)_e; \
+    } while (0)
+
+#define SMX_LAUNCHED_OR_RETURN()                     \
+    do {                                             \
+        smx::count_launch();                         \
+        cudaError_t _e = cudaGetLastError();         \
+        if (_e != cudaSuccess) return (int)_e;       \
     } while (0)
 
 #define SMX_TRY(expr)                 \

@@ -56,9 +56,53 @@ def bool_mul_bits(a, b):
     return BoolMatrix(a.rows, b.cols, out)
 
 
+def _round16(x: int) -> int:
+    return -(-x // 16) * 16
+
+
+def bits_to_bytes(m, transpose: bool = False) -> torch.Tensor:
+    """Unpack a BoolMatrix to 0/1 bytes (rows x round16(cols)), or its transpose."""
+    rows, cols = m.rows, m.cols
+    b8 = torch.empty((rows, _round16(cols)), dtype=torch.uint8, device=m.device)
+    check(lib().smx_unpack_bits(m._words.data_ptr(), b8.data_ptr(), rows, cols, m.stride_words,
+                                b8.shape[1], stream_ptr(m.device)), "smx_unpack_bits")
+    if not transpose:
+        return b8
+    t8 = torch.empty((cols, _round16(rows)), dtype=torch.uint8, device=m.device)
+    check(lib().smx_transpose_u8(b8.data_ptr(), t8.data_ptr(), rows, cols, b8.shape[1],
+                                 t8.shape[1], stream_ptr(m.device)), "smx_transpose_u8")
+    return t8
+
+
+def bool_mul_tc(a, b):
+    """Tensor-core product: tcgen05 kind::i8 GEMM, count > 0, packed-bit epilogue."""
+    from .boolmat import BoolMatrix, _stride_words
+    a8 = bits_to_bytes(a)
+    bt8 = bits_to_bytes(b, transpose=True)
+    out = torch.zeros((a.rows, _stride_words(b.cols)), dtype=torch.int32, device=a.device)
+    check(lib().smx_bool_gemm_i8(a8.data_ptr(), bt8.data_ptr(), None, out.data_ptr(), a.rows,
+                                 b.cols, a.cols, a8.shape[1], bt8.shape[1], out.shape[1], 0,
+                                 stream_ptr(a.device)), "smx_bool_gemm_i8")
+    return BoolMatrix(a.rows, b.cols, out)
+
+
 def bool_mul(a, b):
-    """BoolMatrix.__mul__ engine."""
-    return bool_mul_bits(a, b)
+    """BoolMatrix.__mul__ engine: the tensor-core GEMM."""
+    return bool_mul_tc(a, b)
+
+
+def bool_closure_tc(m):
+    """Blocked Warshall on bytes with tensor-core phases 2/3."""
+    from .boolmat import BoolMatrix
+    t8 = bits_to_bytes(m)
+    nbytes = lib().smx_bool_warshall_i8_workspace_bytes(m.rows, t8.shape[1])
+    ws = _native.workspace(nbytes, m.device)
+    check(lib().smx_bool_warshall_i8(t8.data_ptr(), m.rows, t8.shape[1], ws.data_ptr(), nbytes,
+                                     stream_ptr(m.device)), "smx_bool_warshall_i8")
+    words = torch.empty_like(m._words)
+    check(lib().smx_pack_bits(t8.data_ptr(), words.data_ptr(), m.rows, m.cols, t8.shape[1],
+                              m.stride_words, stream_ptr(m.device)), "smx_pack_bits")
+    return BoolMatrix(m.rows, m.cols, words)
 
 
 def bool_closure_bits(m):

@@ -51,22 +51,31 @@ def bernoulli_bits(rng: np.random.Generator, rows: int, cols: int, p: float,
 
 
 def antidist_graph(rng: np.random.Generator, rows: int, cols: int, p: float,
-                   wmin: int, wmax: int, width: int, diag_zero: bool = False) -> np.ndarray:
-    """Padded anti-distance adjacency: edge (prob p) -> S - w, w ~ U[wmin, wmax]."""
+                   wmin: int, wmax: int, width: int, diag_zero: bool = False,
+                   keep: tuple[int, int] | None = None) -> np.ndarray:
+    """Padded anti-distance adjacency: edge (prob p) -> S - w, w ~ U[wmin, wmax].
+
+    ``keep=(r0, r1)`` returns only rows [r0, r1) (the whole stream is still
+    drawn, so the rows equal those of the full matrix) -- a rank's row panel.
+    """
     limit = (1 << width) - 1
     dtype = DTYPES[width]
-    out = np.zeros((rows, padded_cols(cols, width)), dtype=dtype)
+    k0, k1 = keep if keep is not None else (0, rows)
+    out = np.zeros((k1 - k0, padded_cols(cols, width)), dtype=dtype)
     step = _chunk_rows(cols)
     for r0 in range(0, rows, step):
         r1 = min(rows, r0 + step)
         mask = rng.random((r1 - r0, cols)) < p
         w = rng.integers(wmin, wmax + 1, size=int(mask.sum()), dtype=np.int64)
+        lo, hi = max(r0, k0), min(r1, k1)
+        if lo >= hi:
+            continue
         block = np.zeros((r1 - r0, cols), dtype=dtype)
         block[mask] = (limit - w).astype(dtype)
-        out[r0:r1, :cols] = block
+        out[lo - k0:hi - k0, :cols] = block[lo - r0:hi - r0]
     if diag_zero:
-        d = np.arange(min(rows, cols))
-        out[d, d] = limit
+        d = np.arange(max(k0, 0), min(k1, cols))
+        out[d - k0, d] = limit
     return out
 
 
@@ -102,12 +111,14 @@ CONFIGS = {
 }
 
 
-def make_inputs(cfg: Config, n: int | None = None):
+def make_inputs(cfg: Config, n: int | None = None, rows: tuple[int, int] | None = None):
     """Seeded inputs of ``cfg`` at size n (default: full size).
 
     Returns a tuple of numpy arrays: (A, B) for products, (T,) for closures.
     Boolean inputs are 0/1 uint8 n x n; lane inputs are n x padded(n) arrays
-    in the anti-distance encoding.
+    in the anti-distance encoding.  ``rows=(r0, r1)`` keeps only that row
+    panel of A / T (B stays whole) -- what one rank of a row-panel-sharded
+    run owns; the values are identical to the same rows of the full input.
     """
     n = cfg.n if n is None else n
     rng = np.random.default_rng(cfg.seed)
@@ -117,9 +128,9 @@ def make_inputs(cfg: Config, n: int | None = None):
     if cfg.op == "bool_closure":
         return (bernoulli_bits(rng, n, n, p, no_self_loops=True),)
     if cfg.op == "mul":
-        a = antidist_graph(rng, n, n, p, 1, cfg.wmax, cfg.width)
+        a = antidist_graph(rng, n, n, p, 1, cfg.wmax, cfg.width, keep=rows)
         b = antidist_graph(rng, n, n, p, 1, cfg.wmax, cfg.width)
         return a, b
     if cfg.op == "closure":
-        return (antidist_graph(rng, n, n, p, 1, cfg.wmax, cfg.width, diag_zero=True),)
+        return (antidist_graph(rng, n, n, p, 1, cfg.wmax, cfg.width, diag_zero=True, keep=rows),)
     raise ValueError(cfg.op)

@@ -243,3 +243,81 @@ def test_c_abi_rejects_misaligned():
                                    0, None)
     assert rc == -2
     assert lib.smx_fw_u16(t.data_ptr(), 300, 64, 0, None, 0, None) == -1
+
+
+# -- tensor-core Boolean engine, both output layouts -----------------------------
+
+def test_bool_tc_engines_match_reference(small_cases, config_digests):
+    for meta, arr in small_cases:
+        if meta["op"] == "bool_closure":
+            got = engines.bool_closure_tc(BoolMatrix.from_numpy(arr["t"]))
+            np.testing.assert_array_equal(got.blocks, arr["out_blocks"], err_msg=meta["name"])
+            got = engines.bool_closure_bits(BoolMatrix.from_numpy(arr["t"]))
+            np.testing.assert_array_equal(got.blocks, arr["out_blocks"], err_msg=meta["name"])
+    for name, fn in (("c2_bool_warshall", engines.bool_closure_tc),
+                     ("c2_bool_warshall", engines.bool_closure_bits)):
+        cfg = workloads.CONFIGS[name]
+        d = next(x for x in config_digests if x["config"] == name)
+        (t,) = workloads.make_inputs(cfg, d["n"])
+        assert sha(fn(BoolMatrix.from_numpy(t)).blocks) == d["output_sha256"]
+    cfg = workloads.CONFIGS["c1_bool_mul"]
+    d = next(x for x in config_digests if x["config"] == "c1_bool_mul")
+    a, b = workloads.make_inputs(cfg)
+    for fn in (engines.bool_mul_tc, engines.bool_mul_bits):
+        assert sha(fn(BoolMatrix.from_numpy(a), BoolMatrix.from_numpy(b)).blocks) == d["output_sha256"]
+
+
+def test_bool_tc_bytes_output_and_accumulate(oracle_lib):
+    """smx_bool_gemm_i8 byte epilogue, OR-accumulate, ragged M/N/K, all tile widths."""
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    rng = np.random.default_rng(3)
+    for m, n, k in [(1, 1, 1), (128, 64, 128), (300, 1000, 77), (1024, 520, 2000), (4096, 4096, 256)]:
+        a = (rng.random((m, k)) < 0.02).astype(np.uint8)
+        b = (rng.random((k, n)) < 0.02).astype(np.uint8)
+        c0 = (rng.random((m, n)) < 0.1).astype(np.uint8)
+        want = ((a.astype(np.int64) @ b.astype(np.int64)) > 0).astype(np.uint8)
+        r16 = lambda x: -(-x // 16) * 16  # noqa: E731
+        ta = torch.zeros((m, r16(k)), dtype=torch.uint8, device="cuda")
+        ta[:, :k] = torch.from_numpy(a)
+        tbt = torch.zeros((n, r16(k)), dtype=torch.uint8, device="cuda")
+        tbt[:, :k] = torch.from_numpy(np.ascontiguousarray(b.T))
+        for acc in (0, 1):
+            tc = torch.zeros((m, r16(n)), dtype=torch.uint8, device="cuda")
+            tc[:, :n] = torch.from_numpy(c0)
+            rc = lib.smx_bool_gemm_i8(ta.data_ptr(), tbt.data_ptr(), tc.data_ptr(), None, m, n, k,
+                                      ta.shape[1], tbt.shape[1], tc.shape[1], acc,
+                                      _native.stream_ptr())
+            assert rc == 0
+            exp = (want | c0) if acc else want
+            np.testing.assert_array_equal(tc[:, :n].cpu().numpy(), exp, err_msg=f"{m}x{n}x{k} acc={acc}")
+            assert (tc[:, n:].cpu().numpy() == 0).all()
+
+
+# -- row-panel-sharded closure: the GPU ops, ranks emulated in lockstep ----------
+
+@pytest.mark.parametrize("world,n", [(1, 1000), (2, 1000), (3, 1280), (8, 2048)])
+def test_sharded_fw_gpu_ops_lockstep(world, n, oracle_lib):
+    """ShardedFW with CudaFwOps for `world` ranks on one GPU, run round by round
+    in one process (the broadcast becomes a device copy; no rank ever waits on
+    another, so this is safe on a single GPU) -- bit-identical to the oracle."""
+    from paper_1705_08743_b200 import sharded
+    cfg = workloads.CONFIGS["c5_fw_u16"]
+    (full,) = workloads.make_inputs(cfg, n)
+    ranks = []
+    for r in range(world):
+        ops = sharded.CudaFwOps(16, anti=True)
+        fw = sharded.ShardedFW(n=n, rank=r, world=world, ops=ops)
+        ranks.append((fw, torch.from_numpy(full[fw.row0:fw.row1].copy()).cuda()))
+    block = ranks[0][0].block
+    for k0 in range(0, n, block):
+        owner = ranks[0][0].owner(k0)
+        begun = [fw.begin_round(local, k0) for fw, local in ranks]
+        src = begun[owner][0]
+        for r, (panel, _) in enumerate(begun):
+            if r != owner:
+                panel.copy_(src)
+        for (fw, local), (panel, skip) in zip(ranks, begun):
+            fw.end_round(local, panel, k0, skip)
+    got = torch.cat([local for _, local in ranks]).cpu().numpy()
+    np.testing.assert_array_equal(got, oracle_lib.semiring_close(full, 16, "anti"))
