@@ -47,6 +47,12 @@ int smx_version(void);
 const char* smx_error_string(int code);
 /* Number of kernels this library has launched in the process so far. */
 unsigned long long smx_launch_count(void);
+/* The u16/u32 semiring kernels run a k-tile with the 1-instruction update
+ * c = min(c, a + b) when the CTA has verified that every staged lane of that
+ * k-tile is below 2^(w-1) (so a + b cannot reach S and the clamp is a
+ * no-op); otherwise the general 2-instruction update.  Results are identical;
+ * this switch (default on) forces the general form.  Returns the old value. */
+int smx_set_bounded_fastpath(int enable);
 
 /* ---- saturated lane semiring products ---------------------------------
  * Replace _mul_vector (pkg/src/semimat/antidist.py:361-371, called from
@@ -75,6 +81,20 @@ int smx_fw_u16(uint16_t* T, int n, int ld, int kind, void* workspace, size_t ws_
                void* stream);
 int smx_fw_u32(uint32_t* T, int n, int ld, int kind, void* workspace, size_t ws_bytes,
                void* stream);
+
+/* smx_fw_* overlap each pivot block's phase 1/2 with the previous round's
+ * phase 3 on an internal high-priority side stream (forked from and joined
+ * back into `stream` with events, so it is graph-capturable).  Passing 0
+ * selects the plain serial schedule; results are identical.  Returns the
+ * previous setting. */
+int smx_set_fw_lookahead(int enable);
+
+/* Measurement hook: arm a CUDA-event trace of up to max_launches phase-3
+ * launches (the dominant kernel) of the following smx_fw_* calls; read back
+ * each launch's duration (ms) and cell-updates; returns the count (< 0 on a
+ * CUDA error).  Reading disarms the trace. */
+int smx_fw_trace_arm(int max_launches);
+int smx_fw_trace_read(float* ms, long long* cells, int cap);
 
 /* Building blocks of the blocked FW, exported for the row-panel-sharded
  * multi-GPU driver (paper_1705_08743_b200/sharded.py).  elem_bytes in

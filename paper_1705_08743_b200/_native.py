@@ -23,6 +23,10 @@ _SIGS = {
     "smx_version": ([], c_int),
     "smx_error_string": ([c_int], ctypes.c_char_p),
     "smx_launch_count": ([], ctypes.c_ulonglong),
+    "smx_set_bounded_fastpath": ([c_int], c_int),
+    "smx_set_fw_lookahead": ([c_int], c_int),
+    "smx_fw_trace_arm": ([c_int], c_int),
+    "smx_fw_trace_read": ([c_void_p, c_void_p, c_int], c_int),
     "smx_semiring_gemm_u8": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),
     "smx_semiring_gemm_u16": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),
     "smx_semiring_gemm_u32": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),

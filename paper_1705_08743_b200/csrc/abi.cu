@@ -7,7 +7,29 @@
 
 namespace smx {
 static std::atomic<unsigned long long> g_launches{0};
+static std::atomic<int> g_bounded{1};
+static std::atomic<int> g_lookahead{1};
+int lookahead_enabled() { return g_lookahead.load(std::memory_order_relaxed); }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int bounded_fastpath_enabled() { return g_bounded.load(std::memory_order_relaxed); }
+
+int side_stream(SideStream** out) {
+    static SideStream per_dev[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return (int)e;
+    if (dev < 0 || dev >= 64) return SMX_E_ARG;
+    SideStream& f = per_dev[dev];
+    if (!f.side) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if ((e = cudaStreamCreateWithPriority(&f.side, cudaStreamNonBlocking, hi)) != cudaSuccess) return (int)e;
+        if ((e = cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming)) != cudaSuccess) return (int)e;
+        if ((e = cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming)) != cudaSuccess) return (int)e;
+    }
+    *out = &f;
+    return SMX_OK;
+}
 }  // namespace smx
 
 extern "C" {
@@ -15,6 +37,14 @@ extern "C" {
 int smx_version(void) { return 100; }
 
 unsigned long long smx_launch_count(void) { return smx::g_launches.load(); }
+
+int smx_set_bounded_fastpath(int enable) {
+    return smx::g_bounded.exchange(enable ? 1 : 0);
+}
+
+int smx_set_fw_lookahead(int enable) {
+    return smx::g_lookahead.exchange(enable ? 1 : 0);
+}
 
 const char* smx_error_string(int code) {
     switch (code) {

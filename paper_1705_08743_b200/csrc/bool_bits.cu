@@ -1,5 +1,4 @@
-// Boolean products and Warshall closure on bit-packed rows, plus the
-// byte <-> bit layout helpers.
+// Boolean products and Warshall closure on bit-packed rows.
 //
 // Storage is the reference's own: bit j of row i at u64 block j>>6, bit j&63,
 // LSB first (pkg/src/semimat/boolmat.py:3-5), which read as little-endian u32
@@ -28,12 +27,22 @@ struct BitsArgs {
     int skip_tile0, skip_tiles;
 };
 
-constexpr int kBitsBM = 128, kBitsBNW = 64, kBitsTM = 4, kBitsTNW = 8;
-constexpr int kBitsThreads = (kBitsBM / kBitsTM) * (kBitsBNW / kBitsTNW);  // 256
+template <int BM_, int BNW_, int TM_, int TNW_, int MINB_>
+struct BitsCfg {
+    static constexpr int BM = BM_, BNW = BNW_, TM = TM_, TNW = TNW_, MINB = MINB_;
+    static constexpr int HW = TNW / 2, TCOLS = BNW / TNW;
+    static constexpr int THREADS = (BM / TM) * TCOLS;
+    static constexpr int B_CHUNKS = 32 * BNW / 4;                  // uint4 per k-word stage
+    static constexpr int B_PT = (B_CHUNKS + THREADS - 1) / THREADS;
+    static_assert(HW == 4, "half-groups are one uint4");
+};
+using BitsLarge = BitsCfg<128, 64, 4, 8, 2>;   // 256 threads, 128 x 2048 bits
+using BitsSmall = BitsCfg<64, 32, 2, 8, 2>;    // 128 threads, 64 x 1024 bits
 
-__global__ void __launch_bounds__(kBitsThreads, 2) bool_bits_gemm_kernel(const BitsArgs p) {
-    constexpr int BM = kBitsBM, BNW = kBitsBNW, TM = kBitsTM, TNW = kBitsTNW, HW = TNW / 2;
-    constexpr int TCOLS = BNW / TNW;
+template <typename Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_bits_gemm_kernel(const BitsArgs p) {
+    constexpr int BM = Cfg::BM, BNW = Cfg::BNW, TM = Cfg::TM, TNW = Cfg::TNW, HW = Cfg::HW;
+    constexpr int TCOLS = Cfg::TCOLS, THREADS = Cfg::THREADS;
     __shared__ uint32_t As[2][BM];            // one A word (32 k) per row
     __shared__ __align__(16) uint32_t Bs[2][32][BNW];
 
@@ -54,28 +63,29 @@ __global__ void __launch_bounds__(kBitsThreads, 2) bool_bits_gemm_kernel(const B
         }
     }
 
-    // staging: A: BM words (first BM threads); B: 32 x BNW words = 512 uint4
-    uint32_t a_st = 0;
-    uint4 b_st[2];
+    constexpr int A_PT = (BM + THREADS - 1) / THREADS;
+    uint32_t a_st[A_PT];
+    uint4 b_st[Cfg::B_PT];
     auto gload = [&](int kw) {  // kw: k-word index
         const int k0 = kw * 32;
-        if (tid < BM) {
-            const int grow = row0 + tid;
+#pragma unroll
+        for (int q = 0; q < A_PT; ++q) {
+            const int r = tid + q * THREADS, grow = row0 + r;
             uint32_t v = 0;
-            if (grow < p.M) {
+            if (r < BM && grow < p.M) {
                 v = p.A[(long long)grow * p.lda + kw];
                 const int valid = p.K - k0;
                 if (valid < 32) v &= (1u << valid) - 1u;
             }
-            a_st = v;
+            a_st[q] = v;
         }
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int c = tid + q * kBitsThreads;     // 0..511
+        for (int q = 0; q < Cfg::B_PT; ++q) {
+            const int c = tid + q * THREADS;
             const int kr = c / (BNW / 4), wc = (c % (BNW / 4)) * 4;
             const int gk = k0 + kr, gw = w0 + wc;
             uint4 v = make_uint4(0, 0, 0, 0);
-            if (gk < p.K) {
+            if (c < Cfg::B_CHUNKS && gk < p.K) {
                 const uint32_t* src = p.B + (long long)gk * p.ldb + gw;
                 if (gw + 4 <= p.Nw) v = *reinterpret_cast<const uint4*>(src);
                 else {
@@ -88,12 +98,18 @@ __global__ void __launch_bounds__(kBitsThreads, 2) bool_bits_gemm_kernel(const B
         }
     };
     auto sstore = [&](int buf) {
-        if (tid < BM) As[buf][tid] = a_st;
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int c = tid + q * kBitsThreads;
-            const int kr = c / (BNW / 4), wc = (c % (BNW / 4)) * 4;
-            *reinterpret_cast<uint4*>(&Bs[buf][kr][wc]) = b_st[q];
+        for (int q = 0; q < A_PT; ++q) {
+            const int r = tid + q * THREADS;
+            if (r < BM) As[buf][r] = a_st[q];
+        }
+#pragma unroll
+        for (int q = 0; q < Cfg::B_PT; ++q) {
+            const int c = tid + q * THREADS;
+            if (c < Cfg::B_CHUNKS) {
+                const int kr = c / (BNW / 4), wc = (c % (BNW / 4)) * 4;
+                *reinterpret_cast<uint4*>(&Bs[buf][kr][wc]) = b_st[q];
+            }
         }
     };
 
@@ -143,6 +159,15 @@ __global__ void __launch_bounds__(kBitsThreads, 2) bool_bits_gemm_kernel(const B
     }
 }
 
+template <typename Cfg>
+int launch_bits(const BitsArgs& a, cudaStream_t s) {
+    const int mtiles = ceil_div(a.M, Cfg::BM) - a.skip_tiles;
+    if (mtiles <= 0) return SMX_OK;
+    dim3 grid(ceil_div(a.Nw, Cfg::BNW), mtiles);
+    bool_bits_gemm_kernel<Cfg><<<grid, Cfg::THREADS, 0, s>>>(a);
+    SMX_RETURN_LAUNCH();
+}
+
 int bool_bits_gemm(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int Nw, int K,
                    long long lda, long long ldb, long long ldc, int accumulate, int skip_row0,
                    int skip_rows, cudaStream_t s) {
@@ -152,31 +177,35 @@ int bool_bits_gemm(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int
     if ((ldb & 3) || (ldc & 3)) return SMX_E_ALIGN;
     if (lda * 32 < K || ldb < Nw || ldc < Nw) return SMX_E_ARG;
     BitsArgs a{A, B, C, M, Nw, K, lda, ldb, ldc, accumulate != 0, 0, 0};
+    const long long large_tiles = (long long)ceil_div(M, BitsLarge::BM) * ceil_div(Nw, BitsLarge::BNW);
+    const bool large = large_tiles >= 2 * 148;
+    const int bm = large ? BitsLarge::BM : BitsSmall::BM;
     if (skip_rows > 0) {
-        if (skip_row0 % kBitsBM) return SMX_E_ARG;
-        a.skip_tile0 = skip_row0 / kBitsBM;
-        a.skip_tiles = ceil_div(skip_rows, kBitsBM);
-        const int total = ceil_div(M, kBitsBM);
+        if (skip_row0 % bm) return SMX_E_ARG;
+        a.skip_tile0 = skip_row0 / bm;
+        a.skip_tiles = ceil_div(skip_rows, bm);
+        const int total = ceil_div(M, bm);
         if (a.skip_tile0 + a.skip_tiles > total) a.skip_tiles = total - a.skip_tile0;
     }
-    const int mtiles = ceil_div(M, kBitsBM) - a.skip_tiles;
-    if (mtiles <= 0) return SMX_OK;
-    dim3 grid(ceil_div(Nw, kBitsBNW), mtiles);
-    bool_bits_gemm_kernel<<<grid, kBitsThreads, 0, s>>>(a);
-    SMX_RETURN_LAUNCH();
+    return large ? launch_bits<BitsLarge>(a, s) : launch_bits<BitsSmall>(a, s);
 }
 
 // ---- Warshall pivot tile on bits ------------------------------------------
-// b <= 256: one thread per tile row, the row (8 words) in registers.  Step k:
-// row k (as it stood after step k-1) comes from double-buffered smem; a row
-// whose bit k is set ORs it in (boolmat.py:184-188).
+// b <= 256 rows of 8 words, one thread per row.  The tile is closed in 8
+// sub-rounds of 32 pivots (blocked Warshall inside the CTA):
+//   * warp q owns exactly the 32 rows of sub-block q and runs the sequential
+//     Warshall steps for those pivots over its full rows, the pivot row
+//     broadcast by warp shuffles (no block barrier per step);
+//   * the other warps then fold the updated 32 rows in with one barrier:
+//     row |= OR_{k in sub-block, bit k of the row before the sub-round} row_k.
+// 2 barriers per 32 pivots instead of one per pivot.
 constexpr int kWarshallBlock = 256;
 
 __global__ void __launch_bounds__(kWarshallBlock, 1)
 bool_pivot_kernel(uint32_t* P, int b, long long ld_w) {
     constexpr int W = kWarshallBlock / 32;
-    __shared__ __align__(16) uint32_t prow[2][W];
-    const int r = threadIdx.x;
+    __shared__ __align__(16) uint32_t panel[32][W];
+    const int r = threadIdx.x, warp = r >> 5, lane = r & 31;
     const int nw = (b + 31) / 32;
     uint32_t w[W];
 #pragma unroll
@@ -189,30 +218,36 @@ bool_pivot_kernel(uint32_t* P, int b, long long ld_w) {
         }
         w[i] = v;
     }
-    if (r == 0) {
-#pragma unroll
-        for (int i = 0; i < W; ++i) prow[0][i] = w[i];
-    }
-    __syncthreads();
 #pragma unroll
     for (int q = 0; q < W; ++q) {
         if (q * 32 >= b) break;
-        for (int kk = 0; kk < 32; ++kk) {
-            const int k = q * 32 + kk;
-            if (k >= b) break;
-            const int cur = k & 1;
-            if ((w[q] >> kk) & 1u) {
-                const uint4 v0 = *reinterpret_cast<const uint4*>(&prow[cur][0]);
-                const uint4 v1 = *reinterpret_cast<const uint4*>(&prow[cur][4]);
-                w[0] |= v0.x; w[1] |= v0.y; w[2] |= v0.z; w[3] |= v0.w;
-                w[4] |= v1.x; w[5] |= v1.y; w[6] |= v1.z; w[7] |= v1.w;
-            }
-            if (r == k + 1) {
+        const uint32_t orig = w[q];
+        if (warp == q) {
+            const int steps = b - q * 32 < 32 ? b - q * 32 : 32;
+            for (int kk = 0; kk < steps; ++kk) {
+                uint32_t pv[W];
 #pragma unroll
-                for (int i = 0; i < W; ++i) prow[cur ^ 1][i] = w[i];
+                for (int i = 0; i < W; ++i) pv[i] = __shfl_sync(0xFFFFFFFFu, w[i], kk);
+                if ((w[q] >> kk) & 1u) {
+#pragma unroll
+                    for (int i = 0; i < W; ++i) w[i] |= pv[i];
+                }
             }
-            __syncthreads();
+            *reinterpret_cast<uint4*>(&panel[lane][0]) = make_uint4(w[0], w[1], w[2], w[3]);
+            *reinterpret_cast<uint4*>(&panel[lane][4]) = make_uint4(w[4], w[5], w[6], w[7]);
         }
+        __syncthreads();
+        if (warp != q) {
+            for (int kk = 0; kk < 32; ++kk) {
+                if ((orig >> kk) & 1u) {
+                    const uint4 v0 = *reinterpret_cast<const uint4*>(&panel[kk][0]);
+                    const uint4 v1 = *reinterpret_cast<const uint4*>(&panel[kk][4]);
+                    w[0] |= v0.x; w[1] |= v0.y; w[2] |= v0.z; w[3] |= v0.w;
+                    w[4] |= v1.x; w[5] |= v1.y; w[6] |= v1.z; w[7] |= v1.w;
+                }
+            }
+        }
+        __syncthreads();
     }
     if (r < b) {
         for (int i = 0; i < nw; ++i) {
@@ -227,15 +262,46 @@ bool_pivot_kernel(uint32_t* P, int b, long long ld_w) {
     }
 }
 
-// Warshall pivot tiles are aligned to kWarshallBlock = 256 bits = 8 words.
+// Column-panel snapshot of `cols` words for all rows (one thread per word).
+__global__ void copy_words_kernel(const uint32_t* __restrict__ src, long long ld, uint32_t* __restrict__ dst,
+                                  long long ldd, int rows, int cols) {
+    const long long total = (long long)rows * cols;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / cols), c = (int)(i % cols);
+        dst[r * ldd + c] = src[r * ld + c];
+    }
+}
+
+int copy_words(const uint32_t* src, long long ld, uint32_t* dst, long long ldd, int rows, int cols,
+               cudaStream_t s) {
+    long long blocks = ((long long)rows * cols + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    copy_words_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(src, ld, dst, ldd, rows, cols);
+    SMX_RETURN_LAUNCH();
+}
+
 inline size_t bits_ws_bytes(int n, long long ld_w) {
     const size_t rp = ((size_t)kWarshallBlock * ld_w * 4 + 255) & ~size_t(255);
     const size_t cp = (size_t)n * (kWarshallBlock / 32) * 4;
     return rp + ((cp + 255) & ~size_t(255));
 }
 
-int bool_warshall_bits(uint32_t* T, int n, long long ld_w, void* ws, size_t ws_bytes,
-                       cudaStream_t s) {
+// Pivot tile + pivot row panel of block [k0, k0 + bb).
+static int bits_pivot_and_row_panel(uint32_t* T, int n, long long ld_w, uint32_t* RP, int k0, int bb,
+                                    cudaStream_t s) {
+    const int kw0 = k0 / 32, nw = (n + 31) / 32;
+    uint32_t* rowK = T + (long long)k0 * ld_w;
+    bool_pivot_kernel<<<1, kWarshallBlock, 0, s>>>(rowK + kw0, bb, ld_w);
+    SMX_LAUNCHED_OR_RETURN();
+    cudaError_t e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld_w * 4, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return (int)e;
+    return bool_bits_gemm(RP + kw0, RP, rowK, bb, nw, bb, ld_w, ld_w, ld_w, 1, 0, 0, s);
+}
+
+// Same look-ahead schedule as fw_run_lookahead (fw.cu): pivot block r+1 is
+// closed on the side stream while the bulk of round r's update runs.
+int bool_warshall_bits(uint32_t* T, int n, long long ld_w, void* ws, size_t ws_bytes, cudaStream_t s) {
     if (n < 0 || ld_w * 32 < n) return SMX_E_ARG;
     if (n == 0) return SMX_OK;
     if (!aligned16(T) || (ld_w & 3)) return SMX_E_ALIGN;
@@ -249,84 +315,42 @@ int bool_warshall_bits(uint32_t* T, int n, long long ld_w, void* ws, size_t ws_b
     uint32_t* CP = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ws) +
                                                (((size_t)kWarshallBlock * ld_w * 4 + 255) & ~size_t(255)));
     constexpr long long ldcp = kWarshallBlock / 32;
-    for (int k0 = 0; k0 < n; k0 += kWarshallBlock) {
-        const int bb = n - k0 < kWarshallBlock ? n - k0 : kWarshallBlock;
-        const int kw0 = k0 / 32, bw = (bb + 31) / 32;
+    const int R = (n + kWarshallBlock - 1) / kWarshallBlock;
+    auto blk = [&](int r) { return n - r * kWarshallBlock < kWarshallBlock ? n - r * kWarshallBlock : kWarshallBlock; };
+
+    if (!lookahead_enabled()) {
+        for (int r = 0; r < R; ++r) {
+            const int k0 = r * kWarshallBlock, bb = blk(r), kw0 = k0 / 32, bw = (bb + 31) / 32;
+            SMX_TRY(bits_pivot_and_row_panel(T, n, ld_w, RP, k0, bb, s));
+            SMX_TRY(copy_words(T + kw0, ld_w, CP, ldcp, n, bw, s));
+            SMX_TRY(bool_bits_gemm(CP, T + (long long)k0 * ld_w, T, n, nw, bb, ldcp, ld_w, ld_w, 1, k0, bb, s));
+        }
+        return SMX_OK;
+    }
+    SideStream* ss = nullptr;
+    SMX_TRY(side_stream(&ss));
+    cudaError_t e;
+    SMX_TRY(bits_pivot_and_row_panel(T, n, ld_w, RP, 0, blk(0), s));
+    SMX_TRY(copy_words(T, ld_w, CP, ldcp, n, (blk(0) + 31) / 32, s));
+    for (int r = 0; r < R; ++r) {
+        const int k0 = r * kWarshallBlock, bb = blk(r);
         uint32_t* rowK = T + (long long)k0 * ld_w;
-        bool_pivot_kernel<<<1, kWarshallBlock, 0, s>>>(rowK + kw0, bb, ld_w);
-        SMX_LAUNCHED_OR_RETURN();
-        cudaError_t e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld_w * 4, cudaMemcpyDeviceToDevice, s);
-        if (e != cudaSuccess) return (int)e;
-        SMX_TRY(bool_bits_gemm(RP + kw0, RP, rowK, bb, nw, bb, ld_w, ld_w, ld_w, 1, 0, 0, s));
-        e = cudaMemcpy2DAsync(CP, ldcp * 4, T + kw0, ld_w * 4, (size_t)bw * 4, n,
-                              cudaMemcpyDeviceToDevice, s);
-        if (e != cudaSuccess) return (int)e;
-        SMX_TRY(bool_bits_gemm(CP, rowK, T, n, nw, bb, ldcp, ld_w, ld_w, 1, k0, bb, s));
+        if (r + 1 < R) {
+            const int k1 = k0 + kWarshallBlock, bb1 = blk(r + 1);
+            SMX_TRY(bool_bits_gemm(CP + k1 * ldcp, rowK, T + (long long)k1 * ld_w, bb1, nw, bb, ldcp, ld_w,
+                                   ld_w, 1, 0, 0, s));
+            if ((e = cudaEventRecord(ss->fork, s)) != cudaSuccess) return (int)e;
+            if ((e = cudaStreamWaitEvent(ss->side, ss->fork, 0)) != cudaSuccess) return (int)e;
+            SMX_TRY(bits_pivot_and_row_panel(T, n, ld_w, RP, k1, bb1, ss->side));
+            if ((e = cudaEventRecord(ss->join, ss->side)) != cudaSuccess) return (int)e;
+            SMX_TRY(bool_bits_gemm(CP, rowK, T, n, nw, bb, ldcp, ld_w, ld_w, 1, k0, bb + bb1, s));
+            SMX_TRY(copy_words(T + k1 / 32, ld_w, CP, ldcp, n, (bb1 + 31) / 32, s));
+            if ((e = cudaStreamWaitEvent(s, ss->join, 0)) != cudaSuccess) return (int)e;
+        } else {
+            SMX_TRY(bool_bits_gemm(CP, rowK, T, n, nw, bb, ldcp, ld_w, ld_w, 1, k0, bb, s));
+        }
     }
     return SMX_OK;
-}
-
-// ---- layout helpers ---------------------------------------------------------
-// pack: one warp per 32-column group of a row; lane l tests byte (r, 32g + l)
-// and a ballot forms the LSB-first word (bit l = column 32g + l).
-__global__ void pack_bits_kernel(const uint8_t* __restrict__ bytes, uint32_t* __restrict__ words,
-                                 int rows, int cols, long long ld, long long ld_w, int nw_out) {
-    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const long long total = (long long)rows * nw_out;
-    if (warp >= total) return;
-    const int r = (int)(warp / nw_out), wi = (int)(warp % nw_out);
-    const int c = wi * 32 + lane;
-    const bool bit = c < cols && bytes[(long long)r * ld + c] != 0;
-    const uint32_t word = __ballot_sync(0xFFFFFFFFu, bit);
-    if (lane == 0) words[(long long)r * ld_w + wi] = word;
-}
-
-// unpack: one thread per (row, word) writes 32 bytes; 4 bits -> 4 bytes with
-// the multiply-spread (x * 0x204081) & 0x01010101.
-__global__ void unpack_bits_kernel(const uint32_t* __restrict__ words, uint8_t* __restrict__ bytes,
-                                   int rows, int cols, long long ld_w, long long ld) {
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const int nw = (cols + 31) / 32;
-    if (t >= (long long)rows * nw) return;
-    const int r = (int)(t / nw), wi = (int)(t % nw);
-    const uint32_t w = words[(long long)r * ld_w + wi];
-    uint32_t o[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) o[q] = (((w >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
-    uint8_t* dst = bytes + (long long)r * ld + wi * 32;
-    const int valid = cols - wi * 32;
-    if (valid >= 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-        reinterpret_cast<uint4*>(dst)[0] = make_uint4(o[0], o[1], o[2], o[3]);
-        reinterpret_cast<uint4*>(dst)[1] = make_uint4(o[4], o[5], o[6], o[7]);
-    } else {
-        const uint8_t* ob = reinterpret_cast<const uint8_t*>(o);
-        for (int c = 0; c < 32 && c < valid; ++c) dst[c] = ob[c];
-    }
-}
-
-__global__ void transpose_u8_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
-                                    int rows, int cols, long long ld_in, long long ld_out) {
-    __shared__ uint8_t tile[64][65];
-    const int bx = blockIdx.x * 64, by = blockIdx.y * 64;
-    for (int i = threadIdx.y; i < 64; i += blockDim.y) {
-        const int r = by + i, c = bx + threadIdx.x;
-        tile[i][threadIdx.x] = (r < rows && c < cols) ? in[(long long)r * ld_in + c] : 0;
-    }
-    __syncthreads();
-    for (int i = threadIdx.y; i < 64; i += blockDim.y) {
-        const int r = bx + i, c = by + threadIdx.x;   // out row = in col
-        if (r < cols && c < rows) out[(long long)r * ld_out + c] = tile[threadIdx.x][i];
-    }
-}
-
-int transpose_bytes(const uint8_t* in, uint8_t* out, int rows, int cols, long long ld_in, long long ld_out,
-                    cudaStream_t s) {
-    if (rows < 0 || cols < 0 || ld_in < cols || ld_out < rows) return SMX_E_ARG;
-    if (rows == 0 || cols == 0) return SMX_OK;
-    dim3 grid(ceil_div(cols, 64), ceil_div(rows, 64));
-    transpose_u8_kernel<<<grid, dim3(64, 8), 0, s>>>(in, out, rows, cols, ld_in, ld_out);
-    SMX_RETURN_LAUNCH();
 }
 
 }  // namespace smx
@@ -347,37 +371,7 @@ size_t smx_bool_warshall_workspace_bytes(int n, int ld_w) {
 }
 
 int smx_bool_warshall_bits(uint32_t* T, int n, int ld_w, void* ws, size_t ws_bytes, void* stream) {
-    if (ws_bytes < bits_ws_bytes(n, ld_w)) return SMX_E_WORKSPACE;
     return bool_warshall_bits(T, n, ld_w, ws, ws_bytes, as_stream(stream));
-}
-
-int smx_pack_bits(const uint8_t* bytes, uint32_t* words, int rows, int cols, int ld, int ld_w,
-                  void* stream) {
-    if (rows < 0 || cols < 0 || ld < cols || (long long)ld_w * 32 < cols) return SMX_E_ARG;
-    if (rows == 0) return SMX_OK;
-    // write every word of the row stride so pad bits are zero
-    const int nw_out = ld_w;
-    const long long warps = (long long)rows * nw_out;
-    const int threads = 256;
-    const long long blocks = (warps * 32 + threads - 1) / threads;
-    pack_bits_kernel<<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(bytes, words, rows, cols, ld,
-                                                                        ld_w, nw_out);
-    SMX_RETURN_LAUNCH();
-}
-
-int smx_unpack_bits(const uint32_t* words, uint8_t* bytes, int rows, int cols, int ld_w, int ld,
-                    void* stream) {
-    if (rows < 0 || cols < 0 || ld < cols || (long long)ld_w * 32 < cols) return SMX_E_ARG;
-    if (rows == 0 || cols == 0) return SMX_OK;
-    const long long t = (long long)rows * ((cols + 31) / 32);
-    unpack_bits_kernel<<<(unsigned)((t + 255) / 256), 256, 0, as_stream(stream)>>>(words, bytes, rows,
-                                                                                 cols, ld_w, ld);
-    SMX_RETURN_LAUNCH();
-}
-
-int smx_transpose_u8(const uint8_t* in, uint8_t* out, int rows, int cols, int ld_in, int ld_out,
-                     void* stream) {
-    return transpose_bytes(in, out, rows, cols, ld_in, ld_out, as_stream(stream));
 }
 
 }  // extern "C"

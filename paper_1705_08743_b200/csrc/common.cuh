@@ -13,6 +13,16 @@ namespace smx {
 // Counts every kernel this library launches (smx_launch_count), so bench.py
 // reports launches it observed rather than a formula.
 void count_launch();
+
+// Per-device highest-priority side stream with fork/join events, used by the
+// look-ahead closure schedules (created once, reused; see abi.cu).
+struct SideStream {
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+int side_stream(SideStream** out);
+// smx_set_fw_lookahead switch, shared by the lane FW and Boolean Warshall.
+int lookahead_enabled();
 }
 
 // Placed directly after each kernel launch.

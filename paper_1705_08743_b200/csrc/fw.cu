@@ -77,27 +77,40 @@ fw_pivot_kernel(T* P, int b, long long ld, int anti) {
     if (g == 0) pcol[0][r] = cell_of(0);
     __syncthreads();
 
-    for (int k = 0; k < b; ++k) {
-        const int cur = k & 1;
-        const uint32_t e = pcol[cur][r];
-        const uint32_t a = L::splat(e), sa = L::splat(L::kS - e);
-        uint32_t rk[WPT];
+    // k = g0 * CPT + j with j unrolled, so the cell that becomes the next
+    // pivot column (local index (j + 1) % CPT of group g0 or g0 + 1) is a
+    // compile-time register, not a dynamic select.
+    for (int g0 = 0; g0 < TPR; ++g0) {
+        if (g0 * CPT >= b) break;
 #pragma unroll
-        for (int i = 0; i < WPT; i += 4) {
-            const uint4 v = *reinterpret_cast<const uint4*>(&prow[cur][g * WPT + i]);
-            rk[i] = v.x; rk[i + 1] = v.y; rk[i + 2] = v.z; rk[i + 3] = v.w;
-        }
+        for (int j = 0; j < CPT; ++j) {
+            const int k = g0 * CPT + j;
+            if (k >= b) break;
+            const int cur = k & 1;
+            const uint32_t e = pcol[cur][r];
+            const uint32_t a = L::splat(e), sa = L::splat(L::kS - e);
+            uint32_t rk[WPT];
 #pragma unroll
-        for (int i = 0; i < WPT; ++i) w[i] = L::step(w[i], rk[i], a, sa);
-        const int kn = k + 1;
-        if (kn < b) {
-            if (r == kn) {
-#pragma unroll
-                for (int i = 0; i < WPT; ++i) prow[cur ^ 1][g * WPT + i] = w[i];
+            for (int i = 0; i < WPT; i += 4) {
+                const uint4 v = *reinterpret_cast<const uint4*>(&prow[cur][g * WPT + i]);
+                rk[i] = v.x; rk[i + 1] = v.y; rk[i + 2] = v.z; rk[i + 3] = v.w;
             }
-            if (g == kn / CPT) pcol[cur ^ 1][r] = cell_of(kn - c0);
+#pragma unroll
+            for (int i = 0; i < WPT; ++i) w[i] = L::step(w[i], rk[i], a, sa);
+            const int kn = k + 1;
+            if (kn < b) {
+                if (r == kn) {
+#pragma unroll
+                    for (int i = 0; i < WPT; ++i) prow[cur ^ 1][g * WPT + i] = w[i];
+                }
+                const int jn = (j + 1) % CPT, gn = (j + 1 == CPT) ? g0 + 1 : g0;
+                if (g == gn) {
+                    const uint32_t word = w[jn / CPW];
+                    pcol[cur ^ 1][r] = (CPW == 2) ? ((word >> (16 * (jn % CPW))) & 0xFFFFu) : word;
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
     if (r < b) {
 #pragma unroll
@@ -128,6 +141,115 @@ inline size_t fw_ws_bytes(int n, long long ld, int eb) {
     return align256((size_t)kFwBlock * ld * eb) + align256((size_t)n * kFwBlock * eb);
 }
 
+// Column-panel snapshot CP[i, 0:bb] = T[i, k0:k0+bb] for all n rows (16-byte
+// vectors; bb * sizeof(T) is a multiple of 16 except in a ragged last block).
+template <typename T>
+__global__ void copy_panel_kernel(const T* __restrict__ src, long long ld, T* __restrict__ dst,
+                                  long long ldd, int rows, int cols) {
+    constexpr int E = 16 / sizeof(T);
+    const int cpr = (cols + E - 1) / E;
+    const long long total = (long long)rows * cpr;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / cpr), c = (int)(i % cpr) * E;
+        const T* s = src + r * ld + c;
+        T* d = dst + r * ldd + c;
+        if (c + E <= cols) *reinterpret_cast<uint4*>(d) = __ldg(reinterpret_cast<const uint4*>(s));
+        else
+            for (int j = 0; c + j < cols; ++j) d[j] = s[j];
+    }
+}
+
+template <typename T>
+int copy_panel(const T* src, long long ld, T* dst, long long ldd, int rows, int cols, cudaStream_t s) {
+    const long long work = (long long)rows * ((cols * (long long)sizeof(T) + 15) / 16);
+    long long blocks = (work + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    copy_panel_kernel<T><<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(src, ld, dst, ldd, rows, cols);
+    SMX_RETURN_LAUNCH();
+}
+
+
+// Optional CUDA-event trace of the phase-3 launches (the dominant kernel), so
+// bench.py can time that kernel live inside the timed region on the stream
+// it runs on.  Armed by smx_fw_trace_arm, filled by the next smx_fw_* call.
+struct FwTrace {
+    static constexpr int kCap = 2048;
+    cudaEvent_t ev[2 * kCap] = {};
+    long long cells[kCap] = {};
+    int count = 0, cap = 0;
+    bool armed = false;
+};
+static FwTrace g_trace;
+
+static void trace_begin(cudaStream_t s, long long cells) {
+    if (!g_trace.armed || g_trace.count >= g_trace.cap) return;
+    g_trace.cells[g_trace.count] = cells;
+    cudaEventRecord(g_trace.ev[2 * g_trace.count], s);
+}
+static void trace_end(cudaStream_t s) {
+    if (!g_trace.armed || g_trace.count >= g_trace.cap) return;
+    cudaEventRecord(g_trace.ev[2 * g_trace.count + 1], s);
+    ++g_trace.count;
+}
+
+// Pivot tile + pivot row panel of block [k0, k0+bb): T[K,:] (+)= T[K,K]* (x) T[K,:].
+template <typename T>
+int fw_pivot_and_row_panel(T* Tm, int n, long long ld, int kind, T* RP, int k0, int bb, cudaStream_t s) {
+    T* rowK = Tm + (long long)k0 * ld;
+    SMX_TRY(fw_pivot<T>(rowK + k0, bb, ld, kind, s));
+    cudaError_t e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld * sizeof(T), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return (int)e;
+    return semiring_gemm<T>(RP + k0, RP, rowK, bb, n, bb, ld, ld, ld, kind, 1, 0, 0, s);
+}
+
+// Look-ahead schedule.  The main stream s runs the phase-3 GEMMs; the side
+// stream computes pivot block r+1 (pivot tile + row panel) as soon as its
+// rows have received round r's update, concurrently with the bulk of round
+// r's phase 3:
+//   s   : 3a(r): rows K_{r+1}      -> fork ->  3b(r): rows outside K_r, K_{r+1}
+//         -> CP(r+1) snapshot -> wait(join) -> 3a(r+1) ...
+//   side: wait(fork) -> pivot(r+1), row panel(r+1) -> join
+// 3b(r) only reads CP(r) and T[K_r,:] and writes rows outside K_r u K_{r+1},
+// the side stream only touches rows K_{r+1} and RP, so the two never touch
+// the same bytes.  Rows K_{r+1} of CP(r+1) are copied while the side stream
+// may still write them, but phase 3 of round r+1 skips exactly those rows.
+template <typename T>
+int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, cudaStream_t s) {
+    SideStream* fs = nullptr;
+    SMX_TRY(side_stream(&fs));
+    constexpr long long ldcp = kFwBlock;
+    const int R = (n + kFwBlock - 1) / kFwBlock;
+    SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, 0, n < kFwBlock ? n : kFwBlock, s));
+    SMX_TRY(copy_panel<T>(Tm, ld, CP, ldcp, n, n < kFwBlock ? n : kFwBlock, s));
+    cudaError_t e;
+    for (int r = 0; r < R; ++r) {
+        const int k0 = r * kFwBlock, bb = n - k0 < kFwBlock ? n - k0 : kFwBlock;
+        T* rowK = Tm + (long long)k0 * ld;
+        if (r + 1 < R) {
+            const int k1 = k0 + kFwBlock, bb1 = n - k1 < kFwBlock ? n - k1 : kFwBlock;
+            // 3a: the next pivot block's rows first
+            SMX_TRY(semiring_gemm<T>(CP + k1 * ldcp, rowK, Tm + (long long)k1 * ld, bb1, n, bb, ldcp, ld, ld,
+                                     kind, 1, 0, 0, s));
+            if ((e = cudaEventRecord(fs->fork, s)) != cudaSuccess) return (int)e;
+            if ((e = cudaStreamWaitEvent(fs->side, fs->fork, 0)) != cudaSuccess) return (int)e;
+            SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side));
+            if ((e = cudaEventRecord(fs->join, fs->side)) != cudaSuccess) return (int)e;
+            // 3b: everything else (skips K_r and K_{r+1}, adjacent tiles)
+            trace_begin(s, (long long)(n - bb - bb1) * n * bb);
+            SMX_TRY(semiring_gemm<T>(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, k0, bb + bb1, s));
+            trace_end(s);
+            SMX_TRY(copy_panel<T>(Tm + k1, ld, CP, ldcp, n, bb1, s));
+            if ((e = cudaStreamWaitEvent(s, fs->join, 0)) != cudaSuccess) return (int)e;
+        } else {
+            trace_begin(s, (long long)(n - bb) * n * bb);
+            SMX_TRY(semiring_gemm<T>(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, k0, bb, s));
+            trace_end(s);
+        }
+    }
+    return SMX_OK;
+}
+
 template <typename T>
 int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cudaStream_t s) {
     if (n < 0 || ld < n || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
@@ -138,6 +260,7 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
     T* RP = reinterpret_cast<T*>(ws);
     T* CP = reinterpret_cast<T*>(reinterpret_cast<char*>(ws) + align256((size_t)kFwBlock * ld * sizeof(T)));
     const long long ldcp = kFwBlock;
+    if (lookahead_enabled()) return fw_run_lookahead<T>(Tm, n, ld, kind, RP, CP, s);
     for (int k0 = 0; k0 < n; k0 += kFwBlock) {
         const int bb = n - k0 < kFwBlock ? n - k0 : kFwBlock;
         T* rowK = Tm + (long long)k0 * ld;
@@ -149,7 +272,9 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
         e = cudaMemcpy2DAsync(CP, ldcp * sizeof(T), Tm + k0, ld * sizeof(T), bb * sizeof(T), n,
                               cudaMemcpyDeviceToDevice, s);
         if (e != cudaSuccess) return (int)e;
+        trace_begin(s, (long long)(n - bb) * n * bb);
         SMX_TRY(semiring_gemm<T>(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, k0, bb, s));
+        trace_end(s);
     }
     return SMX_OK;
 }
@@ -189,6 +314,34 @@ int smx_semiring_gemm_skip(const void* A, const void* B, void* C, int M, int N, 
                                                N, K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows, s);
         default: return SMX_E_ARG;
     }
+}
+
+int smx_fw_trace_arm(int max_launches) {
+    if (max_launches < 0) return SMX_E_ARG;
+    if (max_launches > FwTrace::kCap) max_launches = FwTrace::kCap;
+    for (int i = 0; i < 2 * max_launches; ++i) {
+        if (!g_trace.ev[i]) {
+            cudaError_t e = cudaEventCreate(&g_trace.ev[i]);
+            if (e != cudaSuccess) return (int)e;
+        }
+    }
+    g_trace.cap = max_launches;
+    g_trace.count = 0;
+    g_trace.armed = max_launches > 0;
+    return SMX_OK;
+}
+
+int smx_fw_trace_read(float* ms, long long* cells, int cap) {
+    g_trace.armed = false;
+    const int n = g_trace.count < cap ? g_trace.count : cap;
+    for (int i = 0; i < n; ++i) {
+        cudaError_t e = cudaEventSynchronize(g_trace.ev[2 * i + 1]);
+        if (e != cudaSuccess) return -(int)e;
+        e = cudaEventElapsedTime(&ms[i], g_trace.ev[2 * i], g_trace.ev[2 * i + 1]);
+        if (e != cudaSuccess) return -(int)e;
+        cells[i] = g_trace.cells[i];
+    }
+    return n;
 }
 
 int smx_fw_block(int elem_bytes) { return (elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4) ? kFwBlock : 0; }

@@ -1,0 +1,108 @@
+// Byte <-> bit layout helpers for Boolean matrices (the reference's LSB-first
+// 64-bit block rows, pkg/src/semimat/boolmat.py:3-5, read as u32 words) and a
+// byte transpose for the tensor-core B^T operand.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace smx {
+
+// ---- layout helpers ---------------------------------------------------------
+// pack: one warp per 32-column group of a row; lane l tests byte (r, 32g + l)
+// and a ballot forms the LSB-first word (bit l = column 32g + l).
+__global__ void pack_bits_kernel(const uint8_t* __restrict__ bytes, uint32_t* __restrict__ words,
+                                 int rows, int cols, long long ld, long long ld_w, int nw_out) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long total = (long long)rows * nw_out;
+    if (warp >= total) return;
+    const int r = (int)(warp / nw_out), wi = (int)(warp % nw_out);
+    const int c = wi * 32 + lane;
+    const bool bit = c < cols && bytes[(long long)r * ld + c] != 0;
+    const uint32_t word = __ballot_sync(0xFFFFFFFFu, bit);
+    if (lane == 0) words[(long long)r * ld_w + wi] = word;
+}
+
+// unpack: one thread per (row, word) writes 32 bytes; 4 bits -> 4 bytes with
+// the multiply-spread (x * 0x204081) & 0x01010101.
+__global__ void unpack_bits_kernel(const uint32_t* __restrict__ words, uint8_t* __restrict__ bytes,
+                                   int rows, int cols, long long ld_w, long long ld) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int nw = (cols + 31) / 32;
+    if (t >= (long long)rows * nw) return;
+    const int r = (int)(t / nw), wi = (int)(t % nw);
+    const uint32_t w = words[(long long)r * ld_w + wi];
+    uint32_t o[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = (((w >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
+    uint8_t* dst = bytes + (long long)r * ld + wi * 32;
+    const int valid = cols - wi * 32;
+    if (valid >= 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        reinterpret_cast<uint4*>(dst)[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    } else {
+        const uint8_t* ob = reinterpret_cast<const uint8_t*>(o);
+        for (int c = 0; c < 32 && c < valid; ++c) dst[c] = ob[c];
+    }
+}
+
+__global__ void transpose_u8_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                    int rows, int cols, long long ld_in, long long ld_out) {
+    __shared__ uint8_t tile[64][65];
+    const int bx = blockIdx.x * 64, by = blockIdx.y * 64;
+    for (int i = threadIdx.y; i < 64; i += blockDim.y) {
+        const int r = by + i, c = bx + threadIdx.x;
+        tile[i][threadIdx.x] = (r < rows && c < cols) ? in[(long long)r * ld_in + c] : 0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 64; i += blockDim.y) {
+        const int r = bx + i, c = by + threadIdx.x;   // out row = in col
+        if (r < cols && c < rows) out[(long long)r * ld_out + c] = tile[threadIdx.x][i];
+    }
+}
+
+int transpose_bytes(const uint8_t* in, uint8_t* out, int rows, int cols, long long ld_in, long long ld_out,
+                    cudaStream_t s) {
+    if (rows < 0 || cols < 0 || ld_in < cols || ld_out < rows) return SMX_E_ARG;
+    if (rows == 0 || cols == 0) return SMX_OK;
+    dim3 grid(ceil_div(cols, 64), ceil_div(rows, 64));
+    transpose_u8_kernel<<<grid, dim3(64, 8), 0, s>>>(in, out, rows, cols, ld_in, ld_out);
+    SMX_RETURN_LAUNCH();
+}
+
+}  // namespace smx
+
+using namespace smx;
+
+extern "C" {
+
+int smx_pack_bits(const uint8_t* bytes, uint32_t* words, int rows, int cols, int ld, int ld_w,
+                  void* stream) {
+    if (rows < 0 || cols < 0 || ld < cols || (long long)ld_w * 32 < cols) return SMX_E_ARG;
+    if (rows == 0) return SMX_OK;
+    // write every word of the row stride so pad bits are zero
+    const int nw_out = ld_w;
+    const long long warps = (long long)rows * nw_out;
+    const int threads = 256;
+    const long long blocks = (warps * 32 + threads - 1) / threads;
+    pack_bits_kernel<<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(bytes, words, rows, cols, ld,
+                                                                        ld_w, nw_out);
+    SMX_RETURN_LAUNCH();
+}
+
+int smx_unpack_bits(const uint32_t* words, uint8_t* bytes, int rows, int cols, int ld_w, int ld,
+                    void* stream) {
+    if (rows < 0 || cols < 0 || ld < cols || (long long)ld_w * 32 < cols) return SMX_E_ARG;
+    if (rows == 0 || cols == 0) return SMX_OK;
+    const long long t = (long long)rows * ((cols + 31) / 32);
+    unpack_bits_kernel<<<(unsigned)((t + 255) / 256), 256, 0, as_stream(stream)>>>(words, bytes, rows,
+                                                                                 cols, ld_w, ld);
+    SMX_RETURN_LAUNCH();
+}
+
+int smx_transpose_u8(const uint8_t* in, uint8_t* out, int rows, int cols, int ld_in, int ld_out,
+                     void* stream) {
+    return transpose_bytes(in, out, rows, cols, ld_in, ld_out, as_stream(stream));
+}
+
+}  // extern "C"

@@ -40,6 +40,11 @@ template <> struct Lane<uint16_t> {
                                                     uint32_t sa) {
         return __viaddmin_u16x2(__vminu2(b, sa), a, c);
     }
+    // lanes below 2^15 on both sides: a + b <= 65534 < S, no clamp needed
+    static constexpr uint32_t kHalfMask = 0x80008000u;
+    __device__ __forceinline__ static uint32_t step_bounded(uint32_t c, uint32_t b, uint32_t a) {
+        return __viaddmin_u16x2(a, b, c);
+    }
 };
 
 template <> struct Lane<uint8_t> {
@@ -52,6 +57,10 @@ template <> struct Lane<uint8_t> {
     __device__ __forceinline__ static uint32_t splat(uint32_t v) { return v * 0x10001u; }
     __device__ __forceinline__ static uint32_t step(uint32_t c, uint32_t b, uint32_t a,
                                                     uint32_t /*sa*/) {
+        return __viaddmin_u16x2(a, b, c);
+    }
+    static constexpr uint32_t kHalfMask = 0u;   // always the 1-instruction form
+    __device__ __forceinline__ static uint32_t step_bounded(uint32_t c, uint32_t b, uint32_t a) {
         return __viaddmin_u16x2(a, b, c);
     }
 };
@@ -67,6 +76,10 @@ template <> struct Lane<uint32_t> {
     __device__ __forceinline__ static uint32_t step(uint32_t c, uint32_t b, uint32_t a,
                                                     uint32_t sa) {
         return __viaddmin_u32(min(b, sa), a, c);
+    }
+    static constexpr uint32_t kHalfMask = 0x80000000u;
+    __device__ __forceinline__ static uint32_t step_bounded(uint32_t c, uint32_t b, uint32_t a) {
+        return __viaddmin_u32(a, b, c);
     }
 };
 

@@ -19,8 +19,6 @@
 // Arithmetic intensity: BM*BN*BK cells per (BM + BN)*BK*elem bytes staged;
 // the kernel is bound by packed-integer issue, not HBM.
 #pragma once
-#include <stdlib.h>
-
 #include <type_traits>
 
 #include "semiring.cuh"
@@ -38,7 +36,13 @@ struct GemmArgs {
     int accumulate;
     int skip_tile0;   // first M-tile (in units of BM) to skip
     int skip_tiles;   // number of M-tiles skipped
+    int allow_bounded;  // permit the verified 1-instruction k-tiles
 };
+
+// Process-wide switch for the bounded 1-instruction k-tiles (on by default;
+// smx_set_bounded_fastpath(0) forces the general 2-instruction form, for
+// measurement and tests -- results are identical either way).
+int bounded_fastpath_enabled();
 
 template <typename T, int BM_, int BNW_, int BK_, int TM_, int TNW_, int MINB_>
 struct GemmCfg {
@@ -226,7 +230,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
 #pragma unroll
         for (int i = 0; i < Cfg::B_PT; ++i) b_st[i] = load_b_chunk<Cfg>(p, col0, k0, tid + i * Cfg::THREADS);
     };
-    auto sstore = [&](int buf) {
+    // sstore returns whether every staged lane of this thread is below the
+    // half range (L::kHalfMask clear): if that holds for the whole CTA, no
+    // a + b of this k-tile can reach S and the 1-instruction update is exact.
+    auto sstore = [&](int buf) -> bool {
+        uint32_t hi = 0;
 #pragma unroll
         for (int i = 0; i < Cfg::A_PT; ++i) {
             const int c = tid + i * Cfg::THREADS;
@@ -235,6 +243,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
                 AEl* dst = As + (buf * BK + kc * E) * BM + r;
                 uint32_t w[WPC];
                 chunk_to_words<T>(a_st[i], anti, w);
+#pragma unroll
+                for (int q = 0; q < WPC; ++q) hi |= w[q];
 #pragma unroll
                 for (int j = 0; j < E; ++j) {
                     const uint32_t v = word_cell<T>(w, j);
@@ -255,21 +265,21 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
                 uint32_t w[WPC];
                 chunk_to_words<T>(b_st[i], anti, w);
 #pragma unroll
+                for (int q = 0; q < WPC; ++q) hi |= w[q];
+#pragma unroll
                 for (int q = 0; q < WPC / 4; ++q)
                     dst[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
             }
         }
+        return (hi & L::kHalfMask) == 0u;
     };
 
-    const int nkt = (p.K + BK - 1) / BK;
-    if (nkt > 0) {
-        gload(0);
-        sstore(0);
-        __syncthreads();
-    }
-    for (int kt = 0; kt < nkt; ++kt) {
-        const int buf = kt & 1;
-        if (kt + 1 < nkt) gload((kt + 1) * BK);
+    // One k-tile of updates.  BOUNDED selects the 1-instruction form
+    // c = min(c, a + b) (VIADDMNMX alone), exact when the CTA verified that all
+    // lanes of both staged tiles are < 2^(w-1), so a + b < S never wraps and
+    // never needs the S clamp (see semiring.cuh).
+    auto ktile = [&](int buf, auto bounded_tag) {
+        constexpr bool BOUNDED = decltype(bounded_tag)::value;
         const AEl* Ab = As + buf * BK * BM + tr * TM;
         const uint32_t* Bb = Bs + buf * BK * BNW + tc * HW;
 #pragma unroll
@@ -294,12 +304,31 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
 #pragma unroll
                 for (int j = 0; j < TNW; ++j) {
                     if constexpr (L::kOneInstr) acc[i][j] = L::step(acc[i][j], b[j], a[i], 0u);
+                    else if constexpr (BOUNDED) acc[i][j] = L::step_bounded(acc[i][j], b[j], a[i].x);
                     else acc[i][j] = L::step(acc[i][j], b[j], a[i].x, a[i].y);
                 }
             }
         }
-        if (kt + 1 < nkt) sstore(buf ^ 1);
-        __syncthreads();
+    };
+
+    const int nkt = (p.K + BK - 1) / BK;
+    bool bounded = false;
+    if (nkt > 0) {
+        gload(0);
+        bounded = __syncthreads_and(sstore(0)) && p.allow_bounded;
+    }
+    for (int kt = 0; kt < nkt; ++kt) {
+        const int buf = kt & 1;
+        if (kt + 1 < nkt) gload((kt + 1) * BK);
+        if constexpr (L::kOneInstr) {
+            ktile(buf, std::false_type{});
+        } else {
+            if (bounded) ktile(buf, std::true_type{});
+            else ktile(buf, std::false_type{});
+        }
+        bool ok = true;
+        if (kt + 1 < nkt) ok = sstore(buf ^ 1);
+        bounded = __syncthreads_and(ok) && p.allow_bounded;
     }
 
     // ---- epilogue ---------------------------------------------------------
@@ -316,22 +345,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
     }
 }
 
-// Tile configurations.  "Large" is the throughput tile (128 x 256 cells for
-// u8/u16); variant 0 runs 512 threads with 4 x 8-word thread tiles (128
-// registers, 16 warps/SM), variant 1 runs 256 threads with 8 x 8 (168
-// registers, 8 warps/SM, fewer shared-memory loads per cell).  "Small" keeps
-// >= 2 waves on 148 SMs for thin products such as the FW pivot row panel.
-template <typename T> using LargeCfg = GemmCfg<T, 128, 128, 16, 4, 8, 1>;
-template <typename T> using LargeCfgW = GemmCfg<T, 128, 128, 16, 8, 8, 1>;
+// Tile configurations.  "Large" is the throughput tile: 128 x 128 cells
+// (u8/u16; 128 x 64 for u32), 256 threads with 4-row x 8-word thread tiles,
+// 2 CTAs per SM so one CTA's C load / store overlaps the other's k-loop (a
+// measured 15-20% over one 512-thread 128 x 256 CTA per SM, which left the
+// prologue/epilogue exposed and quantised C3's 512 tiles into 4 waves).
+// "Small" keeps >= 2 waves on 148 SMs for thin products such as the FW
+// pivot row panel (128 x n).
+template <typename T> using LargeCfg = GemmCfg<T, 128, 64, 16, 4, 8, 2>;
 template <typename T> using SmallCfg = GemmCfg<T, 64, 64, 16, 4, 4, 2>;
-
-inline int large_variant() {
-    static int v = [] {
-        const char* s = getenv("SMX_GEMM_VARIANT");
-        return s ? atoi(s) : 0;
-    }();
-    return v;
-}
 
 template <typename T>
 int launch_large(const GemmArgs<T>& a, cudaStream_t stream);
@@ -365,7 +387,8 @@ int semiring_gemm(const T* A, const T* B, T* C, int M, int N, int K, long long l
     if (!ld_ok(lda, sizeof(T)) || !ld_ok(ldb, sizeof(T)) || !ld_ok(ldc, sizeof(T)))
         return SMX_E_ALIGN;
     if (lda < K || ldb < N || ldc < N) return SMX_E_ARG;
-    GemmArgs<T> a{A, B, C, M, N, K, lda, ldb, ldc, kind == SMX_ANTI, accumulate != 0, 0, 0};
+    GemmArgs<T> a{A, B, C, M, N, K, lda, ldb, ldc, kind == SMX_ANTI, accumulate != 0, 0, 0,
+                  bounded_fastpath_enabled()};
     if (skip_rows > 0) {
         // skip ranges are whole 128-row tiles of the large config (FW phase 3)
         if (skip_row0 % LargeCfg<T>::BM) return SMX_E_ARG;
@@ -383,8 +406,6 @@ int semiring_gemm(const T* A, const T* B, T* C, int M, int N, int K, long long l
 
 template <typename T>
 int launch_large(const GemmArgs<T>& a, cudaStream_t stream) {
-    static_assert(LargeCfg<T>::BM == LargeCfgW<T>::BM && LargeCfg<T>::BN == LargeCfgW<T>::BN, "");
-    if (large_variant() == 1) return launch_semiring_gemm<LargeCfgW<T>>(a, stream);
     return launch_semiring_gemm<LargeCfg<T>>(a, stream);
 }
 

@@ -16,6 +16,13 @@ row-sharded, B replicated) and runs as independent local GEMMs.  Both are
 bit-identical to the single-GPU closure because every closure order agrees
 (fw.cu header).
 
+On GPUs the rounds are pipelined (``run`` -> ``_run_lookahead``): the owner of
+block r+1 first updates its rows K_{r+1} with round r's panel, then -- on a
+high-priority side stream -- closes pivot r+1, updates its row panel and
+broadcasts it, while every rank's main stream applies round r to the rest of
+its rows.  The serial owner work and the NVLink transfer hide behind the
+bulk GEMM instead of stalling all ranks once per block.
+
 The per-rank compute steps are an injectable ``ops`` object: ``CudaFwOps``
 calls libsemimat_b200.so; the CPU tests inject an oracle-backed version to
 exercise this orchestration (owners, broadcasts, skip ranges) with gloo.
@@ -42,7 +49,8 @@ def row_range(n: int, world: int, rank: int, block: int) -> tuple[int, int]:
 
 
 class CudaFwOps:
-    """Per-rank FW steps on the GPU through the C ABI."""
+    """Per-rank FW steps on the GPU through the C ABI (launched on torch's
+    current stream, so callers control overlap with torch.cuda.stream)."""
 
     def __init__(self, width: int, anti: bool):
         self.width = width
@@ -66,20 +74,29 @@ class CudaFwOps:
             self._at(rp, 0, k0), rp.data_ptr(), self._at(t, r0, 0), b, n, b, ld, ld, ld, self.eb,
             self.kind, 0, 0, _native.stream_ptr(t.device)), "pivot row panel")
 
-    def rest_update(self, t: torch.Tensor, panel: torch.Tensor, k0: int, b: int, n: int,
-                    skip: tuple[int, int] | None) -> None:
+    def snapshot(self, t: torch.Tensor, k0: int, b: int) -> torch.Tensor:
+        """Column panel T[own rows, K] into a (rows x block) buffer."""
         rows = t.shape[0]
-        if rows == 0:
-            return
         if self._cp is None or self._cp.shape[0] < rows or self._cp.device != t.device:
-            self._cp = torch.empty((rows, self.block), dtype=t.dtype, device=t.device)
+            self._cp = torch.empty((max(rows, 1), self.block), dtype=t.dtype, device=t.device)
         cp = self._cp[:rows]
         cp[:, :b].copy_(t[:, k0:k0 + b])
-        s0, sn = skip if skip is not None else (0, 0)
+        return cp
+
+    def update_rows(self, t: torch.Tensor, cp: torch.Tensor, panel: torch.Tensor, b: int, n: int,
+                    lo: int, hi: int, skip: tuple[int, int] | None) -> None:
+        """T[lo:hi, :] (+)= CP[lo:hi] (x) panel, skipping local rows `skip`."""
+        if hi <= lo:
+            return
+        s0, sn = (skip[0] - lo, skip[1]) if skip is not None else (0, 0)
         _native.check(_native.lib().smx_semiring_gemm_skip(
-            cp.data_ptr(), panel.data_ptr(), t.data_ptr(), rows, n, b, cp.shape[1], panel.shape[1],
-            t.shape[1], self.eb, self.kind, s0, sn, _native.stream_ptr(t.device)),
+            self._at(cp, lo, 0), panel.data_ptr(), self._at(t, lo, 0), hi - lo, n, b, cp.shape[1],
+            panel.shape[1], t.shape[1], self.eb, self.kind, s0, sn, _native.stream_ptr(t.device)),
             "row-panel update")
+
+    def rest_update(self, t, panel, k0, b, n, skip) -> None:
+        cp = self.snapshot(t, k0, b)
+        self.update_rows(t, cp, panel, b, n, 0, t.shape[0], skip)
 
 
 @dataclass
@@ -92,40 +109,114 @@ class ShardedFW:
     world: int
     ops: object
     group: object = None
+    lookahead: bool = True
 
     def __post_init__(self):
         self.block = self.ops.block
         self.per = rows_per_rank(self.n, self.world, self.block)
         self.row0, self.row1 = row_range(self.n, self.world, self.rank, self.block)
+        self._recv = None
+        self._side = None
 
     def owner(self, k0: int) -> int:
         return k0 // self.per
 
+    def _bb(self, k0: int) -> int:
+        return min(self.block, self.n - k0)
+
+    def _recv_buf(self, local: torch.Tensor, slot: int) -> torch.Tensor:
+        if self._recv is None or self._recv[0].device != local.device:
+            self._recv = [torch.empty((self.block, local.shape[1]), dtype=local.dtype,
+                                      device=local.device) for _ in range(2)]
+        return self._recv[slot]
+
+    # -- simple schedule (also the step API of the single-GPU lockstep test) --
+
     def begin_round(self, local: torch.Tensor, k0: int):
         """Owner: close the pivot tile and update the pivot row panel.  Returns
         (panel, skip): the owner's panel rows, or this rank's receive buffer."""
-        bb = min(self.block, self.n - k0)
+        bb = self._bb(k0)
         if self.owner(k0) == self.rank:
             lk = k0 - self.row0
             self.ops.pivot(local, lk, k0, bb)
             self.ops.panel_update(local, lk, k0, bb, self.n)
             return local[lk:lk + bb], (lk, bb)
-        if getattr(self, "_recv", None) is None or self._recv.device != local.device:
-            self._recv = torch.empty((self.block, local.shape[1]), dtype=local.dtype,
-                                     device=local.device)
-        return self._recv[:bb], None
+        return self._recv_buf(local, 0)[:bb], None
 
     def end_round(self, local: torch.Tensor, panel: torch.Tensor, k0: int, skip) -> None:
         """Every rank: fold the pivot row panel into its own rows."""
-        bb = min(self.block, self.n - k0)
-        self.ops.rest_update(local, panel, k0, bb, self.n, skip)
+        self.ops.rest_update(local, panel, k0, self._bb(k0), self.n, skip)
+
+    def _bcast(self, panel: torch.Tensor, k0: int) -> None:
+        if self.world > 1:
+            dist.broadcast(panel.view(torch.uint8), src=self.owner(k0), group=self.group)
 
     def run(self, local: torch.Tensor) -> torch.Tensor:
+        if self.lookahead and hasattr(self.ops, "update_rows"):
+            return self._run_lookahead(local)
         for k0 in range(0, self.n, self.block):
             panel, skip = self.begin_round(local, k0)
-            if self.world > 1:
-                dist.broadcast(panel.view(torch.uint8), src=self.owner(k0), group=self.group)
+            self._bcast(panel, k0)
             self.end_round(local, panel, k0, skip)
+        return local
+
+    # -- pipelined schedule ----------------------------------------------------
+
+    def _panel(self, local: torch.Tensor, r: int) -> torch.Tensor:
+        k0 = r * self.block
+        bb = self._bb(k0)
+        if self.owner(k0) == self.rank:
+            lk = k0 - self.row0
+            return local[lk:lk + bb]
+        return self._recv_buf(local, r % 2)[:bb]
+
+    def _owner_work(self, local: torch.Tensor, r: int) -> None:
+        k0 = r * self.block
+        if self.owner(k0) == self.rank:
+            lk, bb = k0 - self.row0, self._bb(k0)
+            self.ops.pivot(local, lk, k0, bb)
+            self.ops.panel_update(local, lk, k0, bb, self.n)
+
+    def _run_lookahead(self, local: torch.Tensor) -> torch.Tensor:
+        import contextlib
+        n, B, ops = self.n, self.block, self.ops
+        R = -(-n // B)
+        rows = local.shape[0]
+        if local.is_cuda:
+            main = torch.cuda.current_stream(local.device)
+            if self._side is None:
+                self._side = torch.cuda.Stream(device=local.device, priority=-1)
+            side = self._side
+        else:   # CPU (tests): the same schedule, serialised in issue order
+            main = side = None
+        self._owner_work(local, 0)
+        self._bcast(self._panel(local, 0), 0)
+        for r in range(R):
+            k0, bb = r * B, self._bb(r * B)
+            panel = self._panel(local, r)
+            cp = ops.snapshot(local, k0, bb)
+            own_r = self.owner(k0) == self.rank
+            skip_lo, skip_n = (k0 - self.row0, bb) if own_r else (0, 0)
+            if r + 1 < R:
+                k1, bb1 = k0 + B, self._bb(k0 + B)
+                own_n = self.owner(k1) == self.rank
+                if own_n:                          # 3a: next pivot rows first
+                    lk1 = k1 - self.row0
+                    ops.update_rows(local, cp, panel, bb, n, lk1, lk1 + bb1, None)
+                    skip_lo, skip_n = (skip_lo, skip_n + bb1) if own_r else (lk1, bb1)
+                fork = main.record_event() if main is not None else None
+                with torch.cuda.stream(side) if side is not None else contextlib.nullcontext():
+                    if side is not None:
+                        side.wait_event(fork)
+                    self._owner_work(local, r + 1)
+                    self._bcast(self._panel(local, r + 1), k1)
+                    join = side.record_event() if side is not None else None
+                ops.update_rows(local, cp, panel, bb, n, 0, rows,
+                                (skip_lo, skip_n) if skip_n else None)   # 3b
+                if main is not None:
+                    main.wait_event(join)
+            else:
+                ops.update_rows(local, cp, panel, bb, n, 0, rows, (skip_lo, skip_n) if skip_n else None)
         return local
 
 

@@ -321,3 +321,84 @@ def test_sharded_fw_gpu_ops_lockstep(world, n, oracle_lib):
             fw.end_round(local, panel, k0, skip)
     got = torch.cat([local for _, local in ranks]).cpu().numpy()
     np.testing.assert_array_equal(got, oracle_lib.semiring_close(full, 16, "anti"))
+
+
+# -- the verified 1-instruction k-tiles ------------------------------------------
+
+@pytest.mark.parametrize("width", [16, 32])
+def test_bounded_fastpath_is_exact(width, oracle_lib):
+    """Tiles whose lanes are all < 2^(w-1) take the 1-instruction update; tiles
+    with larger values or unreachable entries take the general one.  Both must
+    equal the oracle, and forcing the general form must not change a bit."""
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    rng = np.random.default_rng(21)
+    half = 1 << (width - 1)
+    n = 700
+    cases = {
+        "all_bounded": rng.integers(0, half, size=(n, n), dtype=np.uint64),
+        "edge_of_bound": rng.integers(half - 3, half, size=(n, n), dtype=np.uint64),
+        "mixed": np.where(rng.random((n, n)) < 0.5, rng.integers(0, half, size=(n, n)),
+                          rng.integers(half, 1 << width, size=(n, n))).astype(np.uint64),
+        "sparse_unreachable": np.where(rng.random((n, n)) < 0.999, rng.integers(0, 50, size=(n, n)),
+                                       (1 << width) - 1).astype(np.uint64),
+    }
+    for name, vals in cases.items():
+        a = _fast_lane("dist", vals, width)
+        b = _fast_lane("dist", vals[::-1].copy(), width)
+        want = oracle_lib.semiring_mul(a.data, b.data, n, width, "dist")
+        np.testing.assert_array_equal((a * b).data, want, err_msg=name)
+        old = lib.smx_set_bounded_fastpath(0)
+        try:
+            np.testing.assert_array_equal((a * b).data, want, err_msg=name + " (general)")
+        finally:
+            lib.smx_set_bounded_fastpath(old)
+        anti = ~a
+        np.testing.assert_array_equal((anti * ~b).data,
+                                      oracle_lib.semiring_mul(anti.data, (~b).data, n, width, "anti"))
+
+
+def test_fw_fastpath_on_off_identical():
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    cfg = workloads.CONFIGS["c4_fw_u16"]
+    (t,) = workloads.make_inputs(cfg, 2048)
+    fast = lane("anti", t, 2048, 16).transitive_closure().data
+    old = lib.smx_set_bounded_fastpath(0)
+    try:
+        slow = lane("anti", t, 2048, 16).transitive_closure().data
+    finally:
+        lib.smx_set_bounded_fastpath(old)
+    np.testing.assert_array_equal(fast, slow)
+
+
+@pytest.mark.parametrize("n", [129, 300, 1000, 2048])
+def test_fw_lookahead_and_serial_schedules_agree(n, oracle_lib):
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    cfg = workloads.CONFIGS["c5_fw_u16"]
+    (t,) = workloads.make_inputs(cfg, n)
+    want = oracle_lib.semiring_close(t, 16, "anti")
+    for la in (1, 0):
+        old = lib.smx_set_fw_lookahead(la)
+        try:
+            for width_kind in ("anti", "dist"):
+                m = lane("anti", t, n, 16)
+                if width_kind == "dist":
+                    m = ~m
+                    np.testing.assert_array_equal((~m.transitive_closure()).data, want)
+                else:
+                    np.testing.assert_array_equal(m.transitive_closure().data, want)
+        finally:
+            lib.smx_set_fw_lookahead(old)
+
+
+@pytest.mark.parametrize("n", [640, 2048])
+def test_sharded_fw_gpu_lookahead_single_rank(n, oracle_lib):
+    """The pipelined ShardedFW schedule (side stream, double-buffered panel) on
+    the GPU ops at world = 1 -- bit-identical to the oracle."""
+    from paper_1705_08743_b200 import sharded
+    (full,) = workloads.make_inputs(workloads.CONFIGS["c5_fw_u16"], n)
+    local = torch.from_numpy(full.copy()).cuda()
+    sharded.ShardedFW(n=n, rank=0, world=1, ops=sharded.CudaFwOps(16, anti=True)).run(local)
+    np.testing.assert_array_equal(local.cpu().numpy(), oracle_lib.semiring_close(full, 16, "anti"))

@@ -41,16 +41,23 @@ class OracleFwOps:
         prod = oracle.semiring_mul(np.ascontiguousarray(rp[:, k0:k0 + b]), rp, b, self.width, self.kind)
         a[r0:r0 + b, :n] = self.fold(rp[:, :n], prod[:, :n])
 
-    def rest_update(self, t, panel, k0, b, n, skip):
+    def snapshot(self, t, k0, b):
+        return torch.from_numpy(np.ascontiguousarray(t.numpy()[:, k0:k0 + b]))
+
+    def update_rows(self, t, cp, panel, b, n, lo, hi, skip):
         a = t.numpy()
-        if a.shape[0] == 0:
+        if hi <= lo:
             return
-        cp = np.ascontiguousarray(a[:, k0:k0 + b])
-        prod = oracle.semiring_mul(cp, panel.numpy(), b, self.width, self.kind)
-        rows = np.ones(a.shape[0], dtype=bool)
+        prod = oracle.semiring_mul(np.ascontiguousarray(cp.numpy()[lo:hi]), panel.numpy(), b,
+                                   self.width, self.kind)
+        rows = np.zeros(a.shape[0], dtype=bool)
+        rows[lo:hi] = True
         if skip is not None:
             rows[skip[0]:skip[0] + skip[1]] = False
-        a[rows, :n] = self.fold(a[rows, :n], prod[rows, :n])
+        a[rows, :n] = self.fold(a[rows, :n], prod[rows[lo:hi], :n])
+
+    def rest_update(self, t, panel, k0, b, n, skip):
+        self.update_rows(t, self.snapshot(t, k0, b), panel, b, n, 0, t.shape[0], skip)
 
 
 def _free_port():
@@ -59,7 +66,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, width, anti, block, q):
+def _worker(rank, world, port, n, width, anti, block, lookahead, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -75,7 +82,8 @@ def _worker(rank, world, port, n, width, anti, block, q):
         if not anti:
             panel = ((1 << width) - 1 - panel.astype(np.int64)).astype(panel.dtype)
         local = torch.from_numpy(np.ascontiguousarray(panel))
-        fw = sharded.ShardedFW(n=n, rank=rank, world=world, ops=OracleFwOps(width, anti, block))
+        fw = sharded.ShardedFW(n=n, rank=rank, world=world, ops=OracleFwOps(width, anti, block),
+                               lookahead=lookahead)
         fw.run(local)
         full = sharded.gather_rows(local, n, world, block)
         if rank == 0:
@@ -84,16 +92,19 @@ def _worker(rank, world, port, n, width, anti, block, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,block,width,anti", [
-    (2, 200, 32, 16, True),
-    (2, 256, 64, 16, False),
-    (3, 230, 32, 8, True),
+@pytest.mark.parametrize("world,n,block,width,anti,lookahead", [
+    (2, 200, 32, 16, True, True),
+    (2, 200, 32, 16, True, False),
+    (2, 256, 64, 16, False, True),
+    (3, 230, 32, 8, True, True),
+    (3, 230, 32, 8, True, False),
+    (4, 300, 32, 16, True, True),
 ])
-def test_sharded_fw_matches_single_process(world, n, block, width, anti):
+def test_sharded_fw_matches_single_process(world, n, block, width, anti, lookahead):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, width, anti, block, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, width, anti, block, lookahead, q))
              for r in range(world)]
     for p in procs:
         p.start()
