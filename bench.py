@@ -316,8 +316,50 @@ def run_ours(args, world, rank, local_rank):
     secs = float(t.item())
     value = units_per_step * args.steps / secs
 
-    # ---- parity of this very run at the oracle size (rank 0, N = 1) ------------
     result = {}
+    if world > 1:
+        # e2e at N GPUs through the public sharded API: every rank copies its
+        # row panel in from pinned host memory, runs the sharded closure /
+        # product and copies its result rows back, all inside the timed loop
+        if cfg.op == "closure":
+            pin_in = torch.from_numpy(host).pin_memory()
+
+            def e2e_step():
+                work.copy_(pin_in, non_blocking=True)
+                fw.run(work)
+                pin_out.copy_(work, non_blocking=True)
+            pin_out = torch.empty_like(pin_in).pin_memory()
+            h2d, d2h = pin_in.numel() * pin_in.element_size(), pin_out.numel() * pin_out.element_size()
+        else:
+            pa, pb = torch.from_numpy(a_host).pin_memory(), torch.from_numpy(b_host).pin_memory()
+            pin_out = torch.empty((a_host.shape[0], b_host.shape[1]), dtype=pa.dtype).pin_memory()
+
+            def e2e_step():
+                a.copy_(pa, non_blocking=True)
+                b.copy_(pb, non_blocking=True)
+                sharded.sharded_mul(a, b, n, cfg.width, True, out)
+                pin_out.copy_(out, non_blocking=True)
+            h2d = (pa.numel() + pb.numel()) * pa.element_size()
+            d2h = pin_out.numel() * pin_out.element_size()
+        e2e_step()
+        barrier()
+        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2e_steps = 2
+        es.record()
+        for _ in range(e2e_steps):
+            e2e_step()
+        ee.record()
+        barrier()
+        te = torch.tensor([es.elapsed_time(ee) / 1e3 / e2e_steps], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_secs = float(te.item())
+        hb = torch.tensor([h2d, d2h], dtype=torch.float64, device=dev)
+        dist.all_reduce(hb)
+        result["e2e"] = {"value": units_per_step / e2e_secs, "unit": UNIT,
+                         "h2d_bytes_per_step": int(hb[0].item()), "d2h_bytes_per_step": int(hb[1].item()),
+                         "ms_per_step": e2e_secs * 1e3, "note": "summed over ranks; max time over ranks"}
+
+    # ---- parity of this very run at the oracle size (rank 0, N = 1) ------------
     if rank == 0 and world == 1:
         # dominant kernel, timed live in the timed region (trace / events above)
         if cfg.op == "closure":
@@ -466,7 +508,27 @@ def secondary(dev):
         fn = getattr(engines, eng)
         t = cuda_time(lambda: fn(ma, mb), 50, 5)
         out[f"c1_{eng}"] = {"n": cfg.n, "seconds": t, "cells_per_s": cfg.n ** 3 / t,
-                            "note": "includes unpack/transpose/alloc of the public call"}
+                            "note": "public BoolMatrix call incl. unpack/alloc/Python"}
+    # the tensor-core kernel alone (C1 shape and a throughput shape) against
+    # the measured dense int8 peak (cuBLAS torch._int_mm, 8192^3)
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    a8 = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device=dev)
+    t = cuda_time(lambda: torch._int_mm(a8, a8.t()), 10, 2)
+    int8_peak = 2 * 8192 ** 3 / t
+    del a8
+    tc = {"int8_peak_ops_per_s": int8_peak, "peak_source": "measured: torch._int_mm 8192^3 (cuBLAS)"}
+    for n_tc in (1024, 8192):
+        A = (torch.rand((n_tc, n_tc), device=dev) < 0.05).to(torch.uint8)
+        Bt = (torch.rand((n_tc, n_tc), device=dev) < 0.05).to(torch.uint8)
+        o = torch.zeros((n_tc, n_tc // 32), dtype=torch.int32, device=dev)
+        f = lambda: _native.check(lib.smx_bool_gemm_i8(  # noqa: E731
+            A.data_ptr(), Bt.data_ptr(), None, o.data_ptr(), n_tc, n_tc, n_tc, n_tc, n_tc, n_tc // 32, 0,
+            _native.stream_ptr(dev)), "tc")
+        t = cuda_time(f, 20 if n_tc <= 4096 else 5, 2)
+        tc[f"n{n_tc}"] = {"kernel_us": t * 1e6, "ops_per_s": 2 * n_tc ** 3 / t,
+                          "frac_of_int8_peak": 2 * n_tc ** 3 / t / int8_peak}
+    out["bool_tc_gemm_kernel"] = tc
     cfg = workloads.CONFIGS["c2_bool_warshall"]
     (t2,) = workloads.make_inputs(cfg)
     m2 = BoolMatrix.from_numpy(t2)

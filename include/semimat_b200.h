@@ -140,6 +140,10 @@ int smx_pack_bits(const uint8_t* bytes, uint32_t* words, int rows, int cols, int
                   int ld_w, void* stream);
 int smx_unpack_bits(const uint32_t* words, uint8_t* bytes, int rows, int cols, int ld_w,
                     int ld, void* stream);
+/* packed bits (rows x cols) -> 0/1 bytes of the TRANSPOSE (cols x rows, ld_out
+ * bytes): the K-major B^T operand of smx_bool_gemm_i8 in one pass */
+int smx_unpack_bits_transposed(const uint32_t* words, uint8_t* bytes_t, int rows, int cols,
+                               int ld_w, int ld_out, void* stream);
 /* out (cols x rows) = in^T for bytes */
 int smx_transpose_u8(const uint8_t* in, uint8_t* out, int rows, int cols, int ld_in,
                      int ld_out, void* stream);
@@ -153,6 +157,15 @@ int smx_lane_entrywise(const void* A, const void* B, void* C, int rows, int cols
                        int elem_bytes, int op, int pad_is_limit, void* stream);
 int smx_bits_entrywise(const uint32_t* A, const uint32_t* B, uint32_t* C, int rows, int cols,
                        int ld_w, int op, void* stream);
+
+/* ---- construction (antidist.py:191-211, :294-309) ---------------------
+ * Fill the n x ld matrix T with the (+)-identity (0 anti / S dist, padding
+ * included) and fold m weighted edges edges[3*i .. 3*i+2] = (u, v, w) into it,
+ * keeping the best parallel edge (anti: max of S - w; dist: min of w).
+ * Edges must already be validated (0 <= u, v < n, 0 <= w <= S); `edges` is a
+ * device array of int64. */
+int smx_from_edges(const long long* edges, long long m, void* T, int n, int ld, int elem_bytes,
+                   int kind, void* stream);
 
 /* ---- measurement support (bench.py roofline denominators) -------------- */
 /* Runs `iters` iterations of an independent VIMNMX.U16x2 + VIADDMNMX.U16x2

@@ -43,7 +43,10 @@ _SIGS = {
     "smx_pack_bits": ([c_void_p, c_void_p] + [c_int] * 4 + [c_void_p], c_int),
     "smx_unpack_bits": ([c_void_p, c_void_p] + [c_int] * 4 + [c_void_p], c_int),
     "smx_transpose_u8": ([c_void_p, c_void_p] + [c_int] * 4 + [c_void_p], c_int),
-    "smx_lane_entrywise": ([c_void_p] * 3 + [c_int] * 6 + [c_void_p], c_int),
+    "smx_unpack_bits_transposed": ([c_void_p, c_void_p] + [c_int] * 4 + [c_void_p], c_int),
+    "smx_from_edges": ([c_void_p, ctypes.c_longlong, c_void_p, c_int, c_int, c_int, c_int, c_void_p],
+                       c_int),
+    "smx_lane_entrywise":([c_void_p] * 3 + [c_int] * 6 + [c_void_p], c_int),
     "smx_bits_entrywise": ([c_void_p] * 3 + [c_int] * 4 + [c_void_p], c_int),
     "smx_int_issue_probe":([c_void_p, c_int, c_int, c_int, c_int, POINTER(c_longlong), c_void_p],
                             c_int),

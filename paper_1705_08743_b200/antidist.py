@@ -36,6 +36,37 @@ def dtype_for(width: int):
     return _NP[width]
 
 
+def _from_edges(cls, dim: int, edges, width: int):
+    """Validate like the reference (first offending edge, in edge order, same
+    messages: antidist.py:201-208) on the host, then fill + scatter on the GPU."""
+    if dim < 1:
+        raise ValueError(f"matrix dimensions must be positive, got {dim}x{dim}")
+    limit = sat_limit(width)
+    if not isinstance(edges, np.ndarray):
+        edges = list(edges)
+    arr = np.asarray(edges, dtype=np.int64).reshape(-1, 3) if len(edges) else np.zeros((0, 3), np.int64)
+    u, v, w = arr[:, 0], arr[:, 1], arr[:, 2]
+    bad_u = (u < 0) | (u >= dim)
+    bad_v = (v < 0) | (v >= dim)
+    bad_w = (w < 0) | (w > limit)
+    bad = bad_u | bad_v | bad_w
+    if bad.any():
+        i = int(np.argmax(bad))
+        if bad_u[i]:
+            raise ValueError(f"source vertex {int(u[i])} out of range [0, {dim})")
+        if bad_v[i]:
+            raise ValueError(f"target vertex {int(v[i])} out of range [0, {dim})")
+        raise ValueError(f"weight {int(w[i])} outside [0, {limit}]")
+    dev = _native.require_cuda()
+    data = torch.empty((dim, -(-dim // LANES[width]) * LANES[width]), dtype=_TORCH[width], device=dev)
+    dev_edges = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+    _native.check(_native.lib().smx_from_edges(
+        dev_edges.data_ptr(), arr.shape[0], data.data_ptr(), dim, data.shape[1], width // 8,
+        _native.SMX_DIST if cls._PAD_IS_LIMIT else _native.SMX_ANTI, _native.stream_ptr(dev)),
+        "smx_from_edges")
+    return cls(dim, dim, width, data)
+
+
 class _LaneMatrix:
     """Shared storage and entrywise algebra of the two saturated matrix types."""
 
@@ -236,22 +267,8 @@ class AntidistMatrix(_LaneMatrix):
     @classmethod
     def from_edges(cls, dim: int, edges, width: int = 8) -> "AntidistMatrix":
         """Adjacency of weighted edges (u, v, w); parallel edges keep the shortest
-        (antidist.py:191-211)."""
-        if dim < 1:
-            raise ValueError(f"matrix dimensions must be positive, got {dim}x{dim}")
-        limit = sat_limit(width)
-        host = np.zeros((dim, -(-dim // LANES[width]) * LANES[width]), dtype=_NP[width])
-        for u, v, w in edges:
-            if not 0 <= u < dim:
-                raise ValueError(f"source vertex {u} out of range [0, {dim})")
-            if not 0 <= v < dim:
-                raise ValueError(f"target vertex {v} out of range [0, {dim})")
-            if not 0 <= w <= limit:
-                raise ValueError(f"weight {w} outside [0, {limit}]")
-            value = limit - w
-            if value > int(host[u, v]):
-                host[u, v] = value
-        return cls(dim, dim, width, host)
+        (antidist.py:191-211).  Built on the device (smx_from_edges)."""
+        return _from_edges(cls, dim, edges, width)
 
     @classmethod
     def from_boolmat(cls, mat: BoolMatrix, width: int = 8) -> "AntidistMatrix":
@@ -296,21 +313,9 @@ class DistMatrix(_LaneMatrix):
 
     @classmethod
     def from_edges(cls, dim: int, edges, width: int = 8) -> "DistMatrix":
-        """Edge weights stored directly; parallel edges keep the minimum (antidist.py:294-309)."""
-        if dim < 1:
-            raise ValueError(f"matrix dimensions must be positive, got {dim}x{dim}")
-        limit = sat_limit(width)
-        host = np.full((dim, -(-dim // LANES[width]) * LANES[width]), limit, dtype=_NP[width])
-        for u, v, w in edges:
-            if not 0 <= u < dim:
-                raise ValueError(f"source vertex {u} out of range [0, {dim})")
-            if not 0 <= v < dim:
-                raise ValueError(f"target vertex {v} out of range [0, {dim})")
-            if not 0 <= w <= limit:
-                raise ValueError(f"weight {w} outside [0, {limit}]")
-            if w < int(host[u, v]):
-                host[u, v] = w
-        return cls(dim, dim, width, host)
+        """Edge weights stored directly; parallel edges keep the minimum
+        (antidist.py:294-309).  Built on the device (smx_from_edges)."""
+        return _from_edges(cls, dim, edges, width)
 
     def __mul__(self, other) -> "DistMatrix":
         """min over k of the saturating sum (antidist.py:311-329)."""

@@ -119,6 +119,7 @@ struct TcArgs {
     long long ldc;       // bytes, or u32 words for Cbits
     int accumulate;
     int skip_tile0, skip_tiles;
+    int splits;          // split-K factor (gridDim.z); > 1 ORs into a pre-set output
 };
 
 template <int BN>
@@ -140,7 +141,13 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     int mt = blockIdx.y;
     if (mt >= p.skip_tile0) mt += p.skip_tiles;
     const int m0 = mt * kTcBM, n0 = blockIdx.x * BN;
-    const int nkb = (p.K + kTcBK - 1) / kTcBK;
+    // split-K: CTA z handles k-blocks [kb_lo, kb_hi); partial counts are
+    // combined with atomicOr (OR is idempotent, so the merge is exact)
+    const int nkb_all = (p.K + kTcBK - 1) / kTcBK;
+    const int per = (nkb_all + p.splits - 1) / p.splits;
+    const int kb_lo = blockIdx.z * per;
+    const int kb_hi = min(nkb_all, kb_lo + per);
+    const int nkb = kb_hi > kb_lo ? kb_hi - kb_lo : 0;
 
     if (threadIdx.x == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
@@ -171,8 +178,8 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             const uint32_t ph = (kb / kTcStages) & 1;
             mbar_wait(&empty[s], ph ^ 1);
             mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-            tma_load_2d(&mapA, &full[s], sA + s * A_BYTES, kb * kTcBK, m0);
-            tma_load_2d(&mapB, &full[s], sB + s * B_BYTES, kb * kTcBK, n0);
+            tma_load_2d(&mapA, &full[s], sA + s * A_BYTES, (kb_lo + kb) * kTcBK, m0);
+            tma_load_2d(&mapB, &full[s], sB + s * B_BYTES, (kb_lo + kb) * kTcBK, n0);
         }
     } else if (threadIdx.x == 32) {
         // ---- MMA issuer ----
@@ -210,7 +217,22 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
 #pragma unroll
             for (int j = 0; j < 32; ++j) word |= (r[j] != 0u ? 1u : 0u) << j;
             uint32_t* dst = p.Cbits + (long long)row * p.ldc + (col0 >> 5);
-            *dst = p.accumulate ? (*dst | word) : word;
+            if (p.splits > 1) atomicOr(dst, word);
+            else *dst = p.accumulate ? (*dst | word) : word;
+        } else if (p.splits > 1) {
+            uint32_t w[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                w[q] = (r[4 * q] != 0u ? 1u : 0u) | (r[4 * q + 1] != 0u ? 0x100u : 0u) |
+                       (r[4 * q + 2] != 0u ? 0x10000u : 0u) | (r[4 * q + 3] != 0u ? 0x1000000u : 0u);
+            uint32_t* dst = reinterpret_cast<uint32_t*>(p.C + (long long)row * p.ldc + col0);
+            const int nq = min(8, (p.N - col0 + 3) / 4);
+            for (int q = 0; q < nq; ++q) {
+                uint32_t v = w[q];
+                const int valid = p.N - (col0 + 4 * q);
+                if (valid < 4) v &= (1u << (8 * valid)) - 1u;
+                if (v) atomicOr(dst + q, v);
+            }
         } else {
             uint32_t w[8];
 #pragma unroll
@@ -292,8 +314,28 @@ static int launch_tc(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long 
     }
     const int mtiles = ceil_div(a.M, kTcBM) - a.skip_tiles;
     if (mtiles <= 0) return SMX_OK;
-    dim3 grid(ceil_div(a.N, BN), mtiles);
-    kern<<<grid, kTcThreads, smem, s>>>(mA, mB, a);
+    TcArgs args = a;
+    // split K only for long, thin products (few tiles, >= 16 k-blocks): at
+    // C1's 1024^3 the extra zero-fill and atomics cost more than the
+    // latency they hide (12.7 -> 17.2 us measured), so it stays off there
+    const int tiles = mtiles * ceil_div(a.N, BN);
+    const int nkb = ceil_div(a.K, kTcBK);
+    int splits = 1;
+    if (tiles < 148 / 2 && nkb >= 16) {
+        splits = ceil_div(148, tiles);
+        if (splits > nkb / 8) splits = nkb / 8;
+    }
+    args.splits = splits;
+    if (splits > 1 && !a.accumulate) {
+        // partial results are OR-ed in: start from an all-zero output
+        const size_t row_bytes = a.Cbits ? (size_t)ceil_div(a.N, 32) * 4 : (size_t)a.N;
+        const size_t pitch = a.Cbits ? (size_t)a.ldc * 4 : (size_t)a.ldc;
+        void* base = a.Cbits ? (void*)a.Cbits : (void*)a.C;
+        cudaError_t e = cudaMemset2DAsync(base, pitch, 0, row_bytes, a.M, s);
+        if (e != cudaSuccess) return (int)e;
+    }
+    dim3 grid(ceil_div(a.N, BN), mtiles, splits);
+    kern<<<grid, kTcThreads, smem, s>>>(mA, mB, args);
     SMX_RETURN_LAUNCH();
 }
 
@@ -305,7 +347,7 @@ int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbit
     if (!aligned16(A) || !aligned16(Bt) || (lda & 15) || (ldbt & 15)) return SMX_E_ALIGN;
     if (lda < K || ldbt < K) return SMX_E_ARG;
     if (Cbits ? ((long long)ldc * 32 < N) : (ldc < N)) return SMX_E_ARG;
-    TcArgs a{C, Cbits, M, N, K, ldc, accumulate != 0, 0, 0};
+    TcArgs a{C, Cbits, M, N, K, ldc, accumulate != 0, 0, 0, 1};
     if (skip_rows > 0) {
         if (skip_row0 % kTcBM) return SMX_E_ARG;
         a.skip_tile0 = skip_row0 / kTcBM;

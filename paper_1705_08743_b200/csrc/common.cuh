@@ -3,7 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "../../include/semimat_b200.h"
+#include "semimat_b200.h"   // include/ (on the -I path of _build.py)
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "semimat_b200 targets sm_100a only"

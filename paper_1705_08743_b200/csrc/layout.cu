@@ -46,6 +46,41 @@ __global__ void unpack_bits_kernel(const uint32_t* __restrict__ words, uint8_t* 
     }
 }
 
+// Bits -> transposed bytes in one pass (the K-major B^T operand of the
+// tensor-core product straight from the reference's bit rows): a warp takes a
+// 32 (k) x 32 (j) bit tile; lane l holds row k0+l's word, 32 ballots turn the
+// tile around, lane l then owns output row j0+l and writes its 32 bytes.
+__global__ void unpack_bits_t_kernel(const uint32_t* __restrict__ words, uint8_t* __restrict__ out,
+                                     int rows, int cols, long long ld_w, long long ld_out) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int kt = (rows + 31) / 32, jt = (cols + 31) / 32;
+    if (warp >= (long long)kt * jt) return;
+    const int k0 = (int)(warp % kt) * 32, wj = (int)(warp / kt);
+    const int k = k0 + lane;
+    const uint32_t w = k < rows ? words[(long long)k * ld_w + wj] : 0u;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, (w >> jj) & 1u);
+        if (lane == jj) mine = m;
+    }
+    const int j = wj * 32 + lane;
+    if (j >= cols) return;
+    uint32_t o[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = (((mine >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
+    uint8_t* dst = out + (long long)j * ld_out + k0;
+    const int valid = rows - k0;
+    if (valid >= 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        reinterpret_cast<uint4*>(dst)[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    } else {
+        const uint8_t* ob = reinterpret_cast<const uint8_t*>(o);
+        for (int c = 0; c < 32 && c < valid; ++c) dst[c] = ob[c];
+    }
+}
+
 __global__ void transpose_u8_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
                                     int rows, int cols, long long ld_in, long long ld_out) {
     __shared__ uint8_t tile[64][65];
@@ -97,6 +132,16 @@ int smx_unpack_bits(const uint32_t* words, uint8_t* bytes, int rows, int cols, i
     const long long t = (long long)rows * ((cols + 31) / 32);
     unpack_bits_kernel<<<(unsigned)((t + 255) / 256), 256, 0, as_stream(stream)>>>(words, bytes, rows,
                                                                                  cols, ld_w, ld);
+    SMX_RETURN_LAUNCH();
+}
+
+int smx_unpack_bits_transposed(const uint32_t* words, uint8_t* bytes_t, int rows, int cols, int ld_w,
+                               int ld_out, void* stream) {
+    if (rows < 0 || cols < 0 || ld_out < rows || (long long)ld_w * 32 < cols) return SMX_E_ARG;
+    if (rows == 0 || cols == 0) return SMX_OK;
+    const long long warps = (long long)((rows + 31) / 32) * ((cols + 31) / 32);
+    unpack_bits_t_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, as_stream(stream)>>>(
+        words, bytes_t, rows, cols, ld_w, ld_out);
     SMX_RETURN_LAUNCH();
 }
 

@@ -63,15 +63,16 @@ def _round16(x: int) -> int:
 def bits_to_bytes(m, transpose: bool = False) -> torch.Tensor:
     """Unpack a BoolMatrix to 0/1 bytes (rows x round16(cols)), or its transpose."""
     rows, cols = m.rows, m.cols
+    if transpose:
+        t8 = torch.empty((cols, _round16(rows)), dtype=torch.uint8, device=m.device)
+        check(lib().smx_unpack_bits_transposed(m._words.data_ptr(), t8.data_ptr(), rows, cols,
+                                               m.stride_words, t8.shape[1], stream_ptr(m.device)),
+              "smx_unpack_bits_transposed")
+        return t8
     b8 = torch.empty((rows, _round16(cols)), dtype=torch.uint8, device=m.device)
     check(lib().smx_unpack_bits(m._words.data_ptr(), b8.data_ptr(), rows, cols, m.stride_words,
                                 b8.shape[1], stream_ptr(m.device)), "smx_unpack_bits")
-    if not transpose:
-        return b8
-    t8 = torch.empty((cols, _round16(rows)), dtype=torch.uint8, device=m.device)
-    check(lib().smx_transpose_u8(b8.data_ptr(), t8.data_ptr(), rows, cols, b8.shape[1],
-                                 t8.shape[1], stream_ptr(m.device)), "smx_transpose_u8")
-    return t8
+    return b8
 
 
 def bool_mul_tc(a, b):

@@ -169,6 +169,44 @@ def small_cases():
     return cases, manifest
 
 
+def entrywise_cases():
+    """Entrywise |, &, ^, ~ of the reference (antidist.py:128-156,
+    boolmat.py:120-137), incl. padding restoration and the Boolean bridge."""
+    cases, manifest = {}, []
+    rng = random.Random(777)
+    with kernels.forced_vector():
+        idx = 0
+        for width in (8, 16, 32):
+            for kind in ("anti", "dist"):
+                for rows, cols in [(1, 1), (3, 17), (5, 64), (9, 33), (2, 130)]:
+                    a = rand_lane(rng, rows, cols, width, kind, 0.3)
+                    b = rand_lane(rng, rows, cols, width, kind, 0.3)
+                    ma, mb = ref_lane(kind, a, cols, width), ref_lane(kind, b, cols, width)
+                    name = f"ew{idx}"
+                    manifest.append(dict(name=name, kind=kind, width=width, rows=rows, cols=cols))
+                    cases[f"{name}__a"], cases[f"{name}__b"] = a, b
+                    cases[f"{name}__or"] = np.array((ma | mb)._data)
+                    cases[f"{name}__and"] = np.array((ma & mb)._data)
+                    cases[f"{name}__xor"] = np.array((ma ^ mb)._data)
+                    cases[f"{name}__inv"] = np.array((~ma)._data)
+                    if kind == "anti":
+                        cases[f"{name}__toboolmat"] = np.array(ma.to_boolmat().to_lists(), dtype=np.uint8)
+                    idx += 1
+        for rows, cols in [(1, 1), (4, 63), (7, 64), (5, 65), (3, 200)]:
+            a = np.array([[rng.random() < 0.4 for _ in range(cols)] for _ in range(rows)], dtype=np.uint8)
+            b = np.array([[rng.random() < 0.4 for _ in range(cols)] for _ in range(rows)], dtype=np.uint8)
+            ma, mb = ref_bool(a), ref_bool(b)
+            name = f"bew{idx}"
+            manifest.append(dict(name=name, kind="bool", rows=rows, cols=cols))
+            cases[f"{name}__a"], cases[f"{name}__b"] = a, b
+            for op, m in (("or", ma | mb), ("and", ma & mb), ("xor", ma ^ mb), ("inv", ~ma)):
+                cases[f"{name}__{op}"] = np.array(m._blocks)
+            for w in (8, 16):
+                cases[f"{name}__fromboolmat{w}"] = np.array(AntidistMatrix.from_boolmat(ma, w)._data)
+            idx += 1
+    return cases, manifest
+
+
 def samples():
     """The reference's sample files, parsed with the reference's own loaders."""
     from semimat import graphio, matio
@@ -219,7 +257,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also digest C4 at n=8192")
     ap.add_argument("--only-digests", action="store_true")
+    ap.add_argument("--only-entrywise", action="store_true")
     args = ap.parse_args()
+
+    if not args.only_digests:
+        cases, manifest = entrywise_cases()
+        np.savez_compressed(HERE / "entrywise.npz", **cases)
+        (HERE / "entrywise.json").write_text(json.dumps(manifest, indent=0))
+        print(f"entrywise cases: {len(manifest)}")
+        if args.only_entrywise:
+            return
 
     if not args.only_digests:
         cases, manifest = small_cases()

@@ -402,3 +402,63 @@ def test_sharded_fw_gpu_lookahead_single_rank(n, oracle_lib):
     local = torch.from_numpy(full.copy()).cuda()
     sharded.ShardedFW(n=n, rank=0, world=1, ops=sharded.CudaFwOps(16, anti=True)).run(local)
     np.testing.assert_array_equal(local.cpu().numpy(), oracle_lib.semiring_close(full, 16, "anti"))
+
+
+# -- entrywise algebra and the Boolean bridge ---------------
+
+def test_entrywise_match_reference():
+    import json
+    from conftest import GOLDEN
+    manifest = json.loads((GOLDEN / "entrywise.json").read_text())
+    arrs = np.load(GOLDEN / "entrywise.npz")
+    for meta in manifest:
+        g = lambda k: arrs[f"{meta['name']}__{k}"]  # noqa: E731
+        if meta["kind"] == "bool":
+            a, b = BoolMatrix.from_numpy(g("a")), BoolMatrix.from_numpy(g("b"))
+            for op, got in (("or", a | b), ("and", a & b), ("xor", a ^ b), ("inv", ~a)):
+                np.testing.assert_array_equal(got.blocks, g(op), err_msg=f"{meta['name']} {op}")
+            for w in (8, 16):
+                np.testing.assert_array_equal(AntidistMatrix.from_boolmat(a, w).data, g(f"fromboolmat{w}"))
+        else:
+            a = lane(meta["kind"], g("a"), meta["cols"], meta["width"])
+            b = lane(meta["kind"], g("b"), meta["cols"], meta["width"])
+            for op, got in (("or", a | b), ("and", a & b), ("xor", a ^ b), ("inv", ~a)):
+                np.testing.assert_array_equal(got.data, g(op), err_msg=f"{meta['name']} {op}")
+            assert isinstance(~a, DistMatrix if meta["kind"] == "anti" else AntidistMatrix)
+            if meta["kind"] == "anti":
+                assert a.to_boolmat().to_lists() == g("toboolmat").tolist()
+
+
+# -- device construction from edge lists --------------------
+
+@pytest.mark.parametrize("width", [8, 16, 32])
+def test_from_edges_device(width):
+    rng = np.random.default_rng(width)
+    n, m = 300, 20000
+    lim = (1 << width) - 1
+    edges = np.stack([rng.integers(0, n, m), rng.integers(0, n, m),
+                      rng.integers(0, min(lim, 5000) + 1, m)], axis=1)
+    edges[:50, :2] = edges[50:100, :2]                       # force parallel edges
+    lanes = {8: 16, 16: 8, 32: 4}[width]
+    dt = {8: np.uint8, 16: np.uint16, 32: np.uint32}[width]
+    want_a = np.zeros((n, -(-n // lanes) * lanes), dtype=np.int64)
+    np.maximum.at(want_a, (edges[:, 0], edges[:, 1]), lim - edges[:, 2])
+    want_d = np.full((n, -(-n // lanes) * lanes), lim, dtype=np.int64)
+    np.minimum.at(want_d, (edges[:, 0], edges[:, 1]), edges[:, 2])
+    got_a = AntidistMatrix.from_edges(n, edges, width)
+    got_d = DistMatrix.from_edges(n, [tuple(e) for e in edges.tolist()], width)
+    np.testing.assert_array_equal(got_a.data, want_a.astype(dt))
+    np.testing.assert_array_equal(got_d.data, want_d.astype(dt))
+    assert AntidistMatrix.from_edges(4, [], width) == AntidistMatrix.zeros(4, 4, width)
+
+
+def test_from_edges_errors_match_reference():
+    with pytest.raises(ValueError, match="source vertex 5 out of range"):
+        AntidistMatrix.from_edges(2, [(0, 1, 1), (5, 0, 1), (0, 9, 1)], 8)
+    with pytest.raises(ValueError, match="target vertex 9 out of range"):
+        AntidistMatrix.from_edges(2, [(0, 1, 1), (0, 9, 1), (5, 0, 1)], 8)
+    with pytest.raises(ValueError, match="weight 300 outside"):
+        DistMatrix.from_edges(2, [(0, 1, 300)], 8)
+    m = AntidistMatrix.from_edges(2, [(0, 1, 3), (0, 1, 5)], 8)
+    assert m.get(0, 1) == 252
+    assert AntidistMatrix.from_edges(1, [(0, 0, 0)], 8).get(0, 0) == 255
