@@ -24,25 +24,37 @@
 
 namespace smx {
 
-constexpr int kFwBlock = 128;
+// Pivot block size: 256 vertices for u8/u16 (K = 256 per phase-3 CTA halves
+// the share of each CTA's C load/store and the number of rounds), 128 for
+// u32 (whose 1024-thread pivot tile would not fit the register file).
+template <typename T> struct FwBlock { static constexpr int value = sizeof(T) == 4 ? 128 : 256; };
+inline int fw_block_for(int eb) { return eb == 4 ? 128 : 256; }
+// Block used for an n-vertex closure: the 256 block halves the rounds and the
+// per-CTA C traffic of phase 3 (+10% at n = 32768), but its 1024-thread pivot
+// needs a whole SM's register file and so cannot start beside the phase-3
+// CTAs of the previous round; below 16384 vertices (phase 3 < ~3 ms) the
+// 128 block's cheaper pivot wins (+8% at n = 8192).
+template <typename T> inline int fw_block_for_n(int n) {
+    return (sizeof(T) < 4 && n >= 16384) ? 256 : 128;
+}
 
 // ---- phase 1: pivot tile closure ------------------------------------------
-// 1024 threads, 8 per tile row; each owns 128/8 cells of its row in
+// 1024 threads, 1024/B per tile row; each owns B*B/1024 cells of its row in
 // registers.  Step k reads pivot column value T[r,k] and pivot row T[k,:]
 // from double-buffered smem (one barrier per step); the owners of row k+1
 // and column k+1 publish them for the next step.  During step k row k and
 // column k do not change (T[k,k] >= 0 in distance form), so no hazard.
-template <typename T>
+template <typename T, int BLK>
 __global__ void __launch_bounds__(1024, 1)
 fw_pivot_kernel(T* P, int b, long long ld, int anti) {
     using L = Lane<T>;
     constexpr int CPW = L::kCellsPerWord;
-    constexpr int WPR = kFwBlock / CPW;   // words per tile row
-    constexpr int TPR = 8;                // threads per tile row
+    constexpr int WPR = BLK / CPW;        // words per tile row
+    constexpr int TPR = 1024 / BLK;       // threads per tile row
     constexpr int WPT = WPR / TPR;        // words per thread
     constexpr int CPT = WPT * CPW;        // cells per thread
     __shared__ __align__(16) uint32_t prow[2][WPR];
-    __shared__ uint32_t pcol[2][kFwBlock];
+    __shared__ uint32_t pcol[2][BLK];
 
     const int tid = threadIdx.x;
     const int r = tid / TPR, g = tid % TPR;
@@ -89,14 +101,14 @@ fw_pivot_kernel(T* P, int b, long long ld, int anti) {
             const int cur = k & 1;
             const uint32_t e = pcol[cur][r];
             const uint32_t a = L::splat(e), sa = L::splat(L::kS - e);
-            uint32_t rk[WPT];
 #pragma unroll
-            for (int i = 0; i < WPT; i += 4) {
+            for (int i = 0; i < WPT; i += 4) {   // 4 words at a time: bounded registers
                 const uint4 v = *reinterpret_cast<const uint4*>(&prow[cur][g * WPT + i]);
-                rk[i] = v.x; rk[i + 1] = v.y; rk[i + 2] = v.z; rk[i + 3] = v.w;
+                w[i] = L::step(w[i], v.x, a, sa);
+                w[i + 1] = L::step(w[i + 1], v.y, a, sa);
+                w[i + 2] = L::step(w[i + 2], v.z, a, sa);
+                w[i + 3] = L::step(w[i + 3], v.w, a, sa);
             }
-#pragma unroll
-            for (int i = 0; i < WPT; ++i) w[i] = L::step(w[i], rk[i], a, sa);
             const int kn = k + 1;
             if (kn < b) {
                 if (r == kn) {
@@ -129,8 +141,9 @@ fw_pivot_kernel(T* P, int b, long long ld, int anti) {
 
 template <typename T>
 int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s) {
-    if (b < 1 || b > kFwBlock || ld < b || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
-    fw_pivot_kernel<T><<<1, 1024, 0, s>>>(P, b, ld, kind == SMX_ANTI);
+    if (b < 1 || b > FwBlock<T>::value || ld < b || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
+    if (b <= 128) fw_pivot_kernel<T, 128><<<1, 1024, 0, s>>>(P, b, ld, kind == SMX_ANTI);
+    else fw_pivot_kernel<T, FwBlock<T>::value><<<1, 1024, 0, s>>>(P, b, ld, kind == SMX_ANTI);
     SMX_RETURN_LAUNCH();
 }
 
@@ -138,7 +151,8 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 inline size_t fw_ws_bytes(int n, long long ld, int eb) {
     // RP: pivot row panel snapshot (B x ld); CP: column panel snapshot (n x B)
-    return align256((size_t)kFwBlock * ld * eb) + align256((size_t)n * kFwBlock * eb);
+    const size_t B = fw_block_for(eb);
+    return align256(B * ld * eb) + align256((size_t)n * B * eb);
 }
 
 // Column-panel snapshot CP[i, 0:bb] = T[i, k0:k0+bb] for all n rows (16-byte
@@ -218,16 +232,17 @@ template <typename T>
 int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, cudaStream_t s) {
     SideStream* fs = nullptr;
     SMX_TRY(side_stream(&fs));
-    constexpr long long ldcp = kFwBlock;
-    const int R = (n + kFwBlock - 1) / kFwBlock;
-    SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, 0, n < kFwBlock ? n : kFwBlock, s));
-    SMX_TRY(copy_panel<T>(Tm, ld, CP, ldcp, n, n < kFwBlock ? n : kFwBlock, s));
+    const int BLK = fw_block_for_n<T>(n);
+    const long long ldcp = BLK;
+    const int R = (n + BLK - 1) / BLK;
+    SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, 0, n < BLK ? n : BLK, s));
+    SMX_TRY(copy_panel<T>(Tm, ld, CP, ldcp, n, n < BLK ? n : BLK, s));
     cudaError_t e;
     for (int r = 0; r < R; ++r) {
-        const int k0 = r * kFwBlock, bb = n - k0 < kFwBlock ? n - k0 : kFwBlock;
+        const int k0 = r * BLK, bb = n - k0 < BLK ? n - k0 : BLK;
         T* rowK = Tm + (long long)k0 * ld;
         if (r + 1 < R) {
-            const int k1 = k0 + kFwBlock, bb1 = n - k1 < kFwBlock ? n - k1 : kFwBlock;
+            const int k1 = k0 + BLK, bb1 = n - k1 < BLK ? n - k1 : BLK;
             // 3a: the next pivot block's rows first
             SMX_TRY(semiring_gemm<T>(CP + k1 * ldcp, rowK, Tm + (long long)k1 * ld, bb1, n, bb, ldcp, ld, ld,
                                      kind, 1, 0, 0, s));
@@ -255,14 +270,16 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
     if (n < 0 || ld < n || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
     if (n == 0) return SMX_OK;
     if (!aligned16(Tm) || !ld_ok(ld, sizeof(T))) return SMX_E_ALIGN;
-    if (n <= kFwBlock) return fw_pivot<T>(Tm, n, ld, kind, s);
+    const int BLK = fw_block_for_n<T>(n);
+    if (n <= FwBlock<T>::value) return fw_pivot<T>(Tm, n, ld, kind, s);
     if (ws == nullptr || ws_bytes < fw_ws_bytes(n, ld, sizeof(T))) return SMX_E_WORKSPACE;
     T* RP = reinterpret_cast<T*>(ws);
-    T* CP = reinterpret_cast<T*>(reinterpret_cast<char*>(ws) + align256((size_t)kFwBlock * ld * sizeof(T)));
-    const long long ldcp = kFwBlock;
+    T* CP = reinterpret_cast<T*>(reinterpret_cast<char*>(ws) +
+                                 align256((size_t)FwBlock<T>::value * ld * sizeof(T)));
+    const long long ldcp = BLK;
     if (lookahead_enabled()) return fw_run_lookahead<T>(Tm, n, ld, kind, RP, CP, s);
-    for (int k0 = 0; k0 < n; k0 += kFwBlock) {
-        const int bb = n - k0 < kFwBlock ? n - k0 : kFwBlock;
+    for (int k0 = 0; k0 < n; k0 += BLK) {
+        const int bb = n - k0 < BLK ? n - k0 : BLK;
         T* rowK = Tm + (long long)k0 * ld;
         SMX_TRY(fw_pivot<T>(rowK + k0, bb, ld, kind, s));
         cudaError_t e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld * sizeof(T),
@@ -344,7 +361,9 @@ int smx_fw_trace_read(float* ms, long long* cells, int cap) {
     return n;
 }
 
-int smx_fw_block(int elem_bytes) { return (elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4) ? kFwBlock : 0; }
+int smx_fw_block(int elem_bytes) {
+    return (elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4) ? fw_block_for(elem_bytes) : 0;
+}
 
 int smx_fw_pivot(void* P, int b, int ld, int elem_bytes, int kind, void* stream) {
     cudaStream_t s = as_stream(stream);

@@ -120,3 +120,32 @@ def bool_closure_bits(m):
 def bool_closure(m):
     """BoolMatrix.transitive_closure engine."""
     return bool_closure_bits(m)
+
+
+def closure_by_squaring(m, max_squarings: int = 64):
+    """Closure as A (x) (I (+) A)^(2^j), squared on the GPU to a fixpoint.
+
+    The reference's independent check (pkg/src/semimat/oracle.py:49-74,
+    acceptance criterion 6) run with the device products: an algorithm with
+    no shared code path with the blocked Floyd-Warshall / Warshall, used to
+    cross-check them at sizes the CPU oracle cannot reach.  Works for
+    BoolMatrix, AntidistMatrix and DistMatrix.
+    """
+    from .antidist import AntidistMatrix, DistMatrix
+    from .boolmat import BoolMatrix
+    if m.rows != m.cols:
+        raise ValueError(f"closure needs a square matrix, got {m.rows}x{m.cols}")
+    if isinstance(m, BoolMatrix):
+        eye = BoolMatrix.identity(m.rows)
+    elif isinstance(m, (AntidistMatrix, DistMatrix)):
+        eye = type(m).identity(m.rows, m.width)
+    else:
+        raise TypeError(f"expected a semimat matrix, got {type(m).__name__}")
+    # (+) with the identity: | is max (anti) / OR (bool); & is min (dist)
+    power = (eye & m) if isinstance(m, DistMatrix) else (eye | m)
+    for _ in range(max_squarings):
+        nxt = power * power
+        if nxt == power:
+            break
+        power = nxt
+    return m * power

@@ -462,3 +462,30 @@ def test_from_edges_errors_match_reference():
     m = AntidistMatrix.from_edges(2, [(0, 1, 3), (0, 1, 5)], 8)
     assert m.get(0, 1) == 252
     assert AntidistMatrix.from_edges(1, [(0, 0, 0)], 8).get(0, 0) == 255
+
+
+# -- an independent closure algorithm on the device ---------
+
+def test_closure_by_squaring_matches_fw_and_warshall():
+    """A (x) (I (+) A)^(2^j) by repeated GPU squaring (oracle.py:49-74) equals the
+    blocked FW / Warshall closure at sizes beyond the CPU oracle's reach."""
+    cfg = workloads.CONFIGS["c4_fw_u16"]
+    (t,) = workloads.make_inputs(cfg, 4096)
+    a = lane("anti", t, 4096, 16)
+    assert engines.closure_by_squaring(a) == a.transitive_closure()
+    d = ~a
+    assert engines.closure_by_squaring(d) == d.transitive_closure()
+    (b,) = workloads.make_inputs(workloads.CONFIGS["c2_bool_warshall"], 2048)
+    bm = BoolMatrix.from_numpy(b)
+    assert engines.closure_by_squaring(bm) == bm.transitive_closure()
+
+
+def test_fw_n16384_block256_matches_squaring():
+    """n >= 16384 takes the 256-vertex pivot block; cross-check the closure with
+    the independent repeated-squaring algorithm and the Bellman fixpoint."""
+    cfg = workloads.CONFIGS["c5_fw_u16"]
+    (t,) = workloads.make_inputs(cfg, 16384)
+    a = lane("anti", t, 16384, 16)
+    c = a.transitive_closure()
+    assert (a | (c * a)) == c
+    assert engines.closure_by_squaring(a) == c
