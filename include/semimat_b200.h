@@ -88,6 +88,15 @@ int smx_fw_u32(uint32_t* T, int n, int ld, int kind, void* workspace, size_t ws_
  * selects the plain serial schedule; results are identical.  Returns the
  * previous setting. */
 int smx_set_fw_lookahead(int enable);
+/* Side-stream kernels of the look-ahead: 1 = the small-footprint pivot
+ * (tile in shared memory) and row-panel tiles that fit beside phase-3 CTAs;
+ * 0 (default) = the regular pivot and tiles.  Results are identical.
+ * Returns the previous setting. */
+int smx_set_fw_side_lite(int enable);
+/* Pivot block of smx_fw_*: 0 = automatic (256 for u8/u16 at n >= 8192,
+ * else 128), or force 128 / 256 (u32 is always 128).  Returns the previous
+ * setting (or SMX_E_ARG). */
+int smx_set_fw_block(int block);
 
 /* Measurement hook: arm a CUDA-event trace of up to max_launches phase-3
  * launches (the dominant kernel) of the following smx_fw_* calls; read back

@@ -29,13 +29,16 @@ namespace smx {
 // u32 (whose 1024-thread pivot tile would not fit the register file).
 template <typename T> struct FwBlock { static constexpr int value = sizeof(T) == 4 ? 128 : 256; };
 inline int fw_block_for(int eb) { return eb == 4 ? 128 : 256; }
-// Block used for an n-vertex closure: the 256 block halves the rounds and the
-// per-CTA C traffic of phase 3 (+10% at n = 32768), but its 1024-thread pivot
-// needs a whole SM's register file and so cannot start beside the phase-3
-// CTAs of the previous round; below 16384 vertices (phase 3 < ~3 ms) the
-// 128 block's cheaper pivot wins (+8% at n = 8192).
+// Block used for an n-vertex closure: the 256 block halves the rounds and
+// doubles phase 3's K per CTA, amortising each CTA's C load/store (measured
+// +6% at n = 8192, +9% at 16384, +10% at 32768 over 128); its pivot is the
+// shared-memory kernel.  Below 8192 vertices the pivot chain no longer hides
+// behind phase 3 and the 128 block's register pivot wins.
+static int g_fw_block_override = 0;   // smx_set_fw_block: 0 = automatic
 template <typename T> inline int fw_block_for_n(int n) {
-    return (sizeof(T) < 4 && n >= 16384) ? 256 : 128;
+    if (g_fw_block_override == 128 || (g_fw_block_override == 256 && sizeof(T) == 4)) return 128;
+    if (g_fw_block_override == 256) return 256;
+    return (sizeof(T) < 4 && n >= 8192) ? 256 : 128;
 }
 
 // ---- phase 1: pivot tile closure ------------------------------------------
@@ -139,11 +142,97 @@ fw_pivot_kernel(T* P, int b, long long ld, int anti) {
     }
 }
 
+// Lightweight pivot closure for the look-ahead side stream: the tile lives in
+// shared memory (B x B/2 words) and 256 threads with few registers sweep it,
+// so the kernel fits on an SM *beside* two phase-3 CTAs (which hold most of
+// the register file) and starts as soon as it is launched instead of waiting
+// for a whole SM to drain.  Per step k every cell is updated in place from
+// row k and column k of the same buffer: neither changes during step k
+// (T[k][k] >= 0 in distance form), and a thread that rewrites the word
+// holding column k only changes the other lane of that word.
+template <typename T, int BLK>
+__global__ void __launch_bounds__(256)
+fw_pivot_lite_kernel(T* P, int b, long long ld, int anti) {
+    using L = Lane<T>;
+    constexpr int CPW = L::kCellsPerWord;
+    constexpr int WPR = BLK / CPW;               // words per tile row
+    constexpr int WORDS = BLK * WPR;
+    extern __shared__ __align__(16) uint32_t tile[];   // [BLK][WPR], distance form
+    const int tid = threadIdx.x;
+    auto to_dist = [&](uint32_t v) { return anti ? (L::kS - v) : v; };
+    for (int w = tid; w < WORDS; w += 256) {
+        const int r = w / WPR, c0 = (w % WPR) * CPW;
+        uint32_t word = 0;
+#pragma unroll
+        for (int l = 0; l < CPW; ++l) {
+            const int col = c0 + l;
+            const uint32_t v = (r < b && col < b) ? to_dist((uint32_t)P[(long long)r * ld + col]) : L::kS;
+            word |= (CPW == 2) ? (v << (16 * l)) : v;
+        }
+        tile[w] = word;
+    }
+    __syncthreads();
+    for (int k = 0; k < b; ++k) {
+        const uint32_t* prow = tile + k * WPR;
+        const int kw = k / CPW, ksh = (k % CPW) * 16;
+        for (int w4 = tid * 4; w4 < WORDS; w4 += 256 * 4) {
+            const int r = w4 / WPR, c = w4 % WPR;
+            uint32_t e = tile[r * WPR + kw];
+            if (CPW == 2) e = (e >> ksh) & 0xFFFFu;
+            const uint32_t a = L::splat(e), sa = L::splat(L::kS - e);
+            uint4 v = *reinterpret_cast<const uint4*>(tile + w4);
+            const uint4 pv = *reinterpret_cast<const uint4*>(prow + c);
+            v.x = L::step(v.x, pv.x, a, sa);
+            v.y = L::step(v.y, pv.y, a, sa);
+            v.z = L::step(v.z, pv.z, a, sa);
+            v.w = L::step(v.w, pv.w, a, sa);
+            *reinterpret_cast<uint4*>(tile + w4) = v;
+        }
+        __syncthreads();
+    }
+    for (int w = tid; w < WORDS; w += 256) {
+        const int r = w / WPR, c0 = (w % WPR) * CPW;
+        if (r >= b) continue;
+#pragma unroll
+        for (int l = 0; l < CPW; ++l) {
+            const int col = c0 + l;
+            if (col < b) {
+                const uint32_t v = (CPW == 2) ? ((tile[w] >> (16 * l)) & 0xFFFFu) : tile[w];
+                P[(long long)r * ld + col] = (T)(anti ? (L::kS - v) : v);
+            }
+        }
+    }
+}
+
+template <typename T, int BLK>
+int launch_pivot_lite(T* P, int b, long long ld, int kind, cudaStream_t s) {
+    constexpr size_t smem = (size_t)BLK * (BLK / Lane<T>::kCellsPerWord) * 4;
+    auto kern = fw_pivot_lite_kernel<T, BLK>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        configured = true;
+    }
+    kern<<<1, 256, smem, s>>>(P, b, ld, kind == SMX_ANTI);
+    SMX_RETURN_LAUNCH();
+}
+
+template <typename T>
+int fw_pivot_lite(T* P, int b, long long ld, int kind, cudaStream_t s) {
+    if (b < 1 || b > FwBlock<T>::value || ld < b || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
+    if (b <= 128) return launch_pivot_lite<T, 128>(P, b, ld, kind, s);
+    return launch_pivot_lite<T, FwBlock<T>::value>(P, b, ld, kind, s);
+}
+
 template <typename T>
 int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s) {
     if (b < 1 || b > FwBlock<T>::value || ld < b || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
-    if (b <= 128) fw_pivot_kernel<T, 128><<<1, 1024, 0, s>>>(P, b, ld, kind == SMX_ANTI);
-    else fw_pivot_kernel<T, FwBlock<T>::value><<<1, 1024, 0, s>>>(P, b, ld, kind == SMX_ANTI);
+    // The register-resident kernel unrolls CPT steps (16 cells/thread at 128);
+    // at 256 that unroll (64 steps x 32 words) no longer fits the instruction
+    // caches (measured 688 us per pivot), so 256 uses the shared-memory tile.
+    if (b > 128) return fw_pivot_lite<T>(P, b, ld, kind, s);
+    fw_pivot_kernel<T, 128><<<1, 1024, 0, s>>>(P, b, ld, kind == SMX_ANTI);
     SMX_RETURN_LAUNCH();
 }
 
@@ -209,13 +298,21 @@ static void trace_end(cudaStream_t s) {
 
 // Pivot tile + pivot row panel of block [k0, k0+bb): T[K,:] (+)= T[K,K]* (x) T[K,:].
 template <typename T>
-int fw_pivot_and_row_panel(T* Tm, int n, long long ld, int kind, T* RP, int k0, int bb, cudaStream_t s) {
+int fw_pivot_and_row_panel(T* Tm, int n, long long ld, int kind, T* RP, int k0, int bb, cudaStream_t s,
+                           bool lite = false) {
     T* rowK = Tm + (long long)k0 * ld;
-    SMX_TRY(fw_pivot<T>(rowK + k0, bb, ld, kind, s));
+    if (lite) SMX_TRY(fw_pivot_lite<T>(rowK + k0, bb, ld, kind, s));
+    else SMX_TRY(fw_pivot<T>(rowK + k0, bb, ld, kind, s));
     cudaError_t e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld * sizeof(T), cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return (int)e;
+    if (lite) return semiring_gemm_lite<T>(RP + k0, RP, rowK, bb, n, bb, ld, ld, ld, kind, s);
     return semiring_gemm<T>(RP + k0, RP, rowK, bb, n, bb, ld, ld, ld, kind, 1, 0, 0, s);
 }
+
+// Side-stream kernel footprint.  Measured: the co-residable Lite row-panel
+// tiles gain nothing over the regular ones (the side chain already hides
+// behind phase 3) and lose ~1-2%, so the regular tiles are the default.
+static int g_side_lite = 0;
 
 // Look-ahead schedule.  The main stream s runs the phase-3 GEMMs; the side
 // stream computes pivot block r+1 (pivot tile + row panel) as soon as its
@@ -248,7 +345,7 @@ int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, cudaStr
                                      kind, 1, 0, 0, s));
             if ((e = cudaEventRecord(fs->fork, s)) != cudaSuccess) return (int)e;
             if ((e = cudaStreamWaitEvent(fs->side, fs->fork, 0)) != cudaSuccess) return (int)e;
-            SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side));
+            SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
             if ((e = cudaEventRecord(fs->join, fs->side)) != cudaSuccess) return (int)e;
             // 3b: everything else (skips K_r and K_{r+1}, adjacent tiles)
             trace_begin(s, (long long)(n - bb - bb1) * n * bb);
@@ -331,6 +428,19 @@ int smx_semiring_gemm_skip(const void* A, const void* B, void* C, int M, int N, 
                                                N, K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows, s);
         default: return SMX_E_ARG;
     }
+}
+
+int smx_set_fw_block(int block) {
+    if (block != 0 && block != 128 && block != 256) return SMX_E_ARG;
+    const int old = g_fw_block_override;
+    g_fw_block_override = block;
+    return old;
+}
+
+int smx_set_fw_side_lite(int enable) {
+    const int old = g_side_lite;
+    g_side_lite = enable ? 1 : 0;
+    return old;
 }
 
 int smx_fw_trace_arm(int max_launches) {

@@ -62,8 +62,11 @@ struct GemmCfg {
     static constexpr int B_CPR = BNW / WPC;
     static constexpr int B_CHUNKS = BK * B_CPR;
     static constexpr int B_PT = (B_CHUNKS + THREADS - 1) / THREADS;
-    using AEl = typename std::conditional<L::kOneInstr, uint32_t, uint2>::type;
-    static constexpr size_t SMEM = 2ull * BK * BM * sizeof(AEl) + 2ull * BK * BNW * 4;
+    // A is staged as planes: splat(a) and (2-instruction form only) splat(S-a),
+    // so the bounded / one-instruction loop reads TM rows with one LDS.128.
+    static constexpr int APLANES = L::kOneInstr ? 1 : 2;
+    static constexpr size_t SMEM = 2ull * APLANES * BK * BM * 4 + 2ull * BK * BNW * 4;
+    static_assert(TM == 2 || TM == 4, "A fragment is one 8- or 16-byte load per plane");
     static_assert(BK % E == 0, "BK must hold whole chunks");
     static_assert(BNW % WPC == 0, "BNW must hold whole chunks");
     static_assert(HW == 2 || HW == 4, "half-group must be 2 or 4 words");
@@ -187,13 +190,12 @@ __device__ __forceinline__ uint4 load_b_chunk(const GemmArgs<T>& p, int col0, in
 template <typename Cfg, typename T>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(const GemmArgs<T> p) {
     using L = Lane<T>;
-    using AEl = typename Cfg::AEl;
     constexpr int BM = Cfg::BM, BNW = Cfg::BNW, BK = Cfg::BK, TM = Cfg::TM, TNW = Cfg::TNW;
-    constexpr int HW = Cfg::HW, WPC = Cfg::WPC, E = Cfg::E, CPW = Cfg::CPW;
+    constexpr int HW = Cfg::HW, WPC = Cfg::WPC, E = Cfg::E, CPW = Cfg::CPW, AP = Cfg::APLANES;
 
     extern __shared__ uint4 smem_raw[];
-    AEl* As = reinterpret_cast<AEl*>(smem_raw);                    // [2][BK][BM]
-    uint32_t* Bs = reinterpret_cast<uint32_t*>(As + 2 * BK * BM);  // [2][BK][BNW]
+    uint32_t* As = reinterpret_cast<uint32_t*>(smem_raw);     // [2][AP][BK][BM]
+    uint32_t* Bs = As + 2 * AP * BK * BM;                     // [2][BK][BNW]
 
     const int tid = threadIdx.x;
     int mt = blockIdx.y;
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
             const int c = tid + i * Cfg::THREADS;
             if (c < Cfg::A_CHUNKS) {
                 const int r = c / Cfg::A_CPR, kc = c % Cfg::A_CPR;
-                AEl* dst = As + (buf * BK + kc * E) * BM + r;
+                uint32_t* dst = As + (buf * AP * BK + kc * E) * BM + r;
                 uint32_t w[WPC];
                 chunk_to_words<T>(a_st[i], anti, w);
 #pragma unroll
@@ -248,11 +250,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
 #pragma unroll
                 for (int j = 0; j < E; ++j) {
                     const uint32_t v = word_cell<T>(w, j);
-                    if constexpr (L::kOneInstr) {
-                        dst[j * BM] = L::splat(v);
-                    } else {
-                        dst[j * BM] = make_uint2(L::splat(v), L::splat(L::kS - v));
-                    }
+                    dst[j * BM] = L::splat(v);
+                    if constexpr (AP == 2) dst[BK * BM + j * BM] = L::splat(L::kS - v);
                 }
             }
         }
@@ -280,7 +279,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
     // never needs the S clamp (see semiring.cuh).
     auto ktile = [&](int buf, auto bounded_tag) {
         constexpr bool BOUNDED = decltype(bounded_tag)::value;
-        const AEl* Ab = As + buf * BK * BM + tr * TM;
+        const uint32_t* Ab = As + buf * AP * BK * BM + tr * TM;   // plane 0: splat(a)
         const uint32_t* Bb = Bs + buf * BK * BNW + tc * HW;
 #pragma unroll
         for (int kk = 0; kk < BK; ++kk) {
@@ -296,16 +295,25 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
                     b[g * 2 + 0] = v.x; b[g * 2 + 1] = v.y;
                 }
             }
-            AEl a[TM];
-#pragma unroll
-            for (int i = 0; i < TM; ++i) a[i] = Ab[kk * BM + i];
+            uint32_t a[TM], sa[TM];
+            auto load_rows = [&](const uint32_t* src, uint32_t* dst) {
+                if constexpr (TM == 4) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(src);
+                    dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;
+                } else {
+                    const uint2 v = *reinterpret_cast<const uint2*>(src);
+                    dst[0] = v.x; dst[1] = v.y;
+                }
+            };
+            load_rows(Ab + kk * BM, a);
+            if constexpr (!L::kOneInstr && !BOUNDED) load_rows(Ab + BK * BM + kk * BM, sa);
 #pragma unroll
             for (int i = 0; i < TM; ++i) {
 #pragma unroll
                 for (int j = 0; j < TNW; ++j) {
                     if constexpr (L::kOneInstr) acc[i][j] = L::step(acc[i][j], b[j], a[i], 0u);
-                    else if constexpr (BOUNDED) acc[i][j] = L::step_bounded(acc[i][j], b[j], a[i].x);
-                    else acc[i][j] = L::step(acc[i][j], b[j], a[i].x, a[i].y);
+                    else if constexpr (BOUNDED) acc[i][j] = L::step_bounded(acc[i][j], b[j], a[i]);
+                    else acc[i][j] = L::step(acc[i][j], b[j], a[i], sa[i]);
                 }
             }
         }
@@ -356,6 +364,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
 // staged byte, and the longer k-tile measured +4% on C3 u8; u16 is best at 16.)
 template <typename T> using LargeCfg = GemmCfg<T, 128, 64, (sizeof(T) == 1 ? 32 : 16), 4, 8, 2>;
 template <typename T> using SmallCfg = GemmCfg<T, 64, 64, 16, 4, 4, 2>;
+// "Lite": 128 threads with 2 x 4-word thread tiles (~8K registers, 12 KB
+// smem per CTA) -- small enough to run beside two Large CTAs on one SM, for
+// the look-ahead side stream's pivot row panel while phase 3 fills the GPU.
+template <typename T> using LiteCfg = GemmCfg<T, 32, 32, 16, 2, 4, 4>;
 
 template <typename T>
 int launch_large(const GemmArgs<T>& a, cudaStream_t stream);
@@ -409,6 +421,18 @@ int semiring_gemm(const T* A, const T* B, T* C, int M, int N, int K, long long l
 template <typename T>
 int launch_large(const GemmArgs<T>& a, cudaStream_t stream) {
     return launch_semiring_gemm<LargeCfg<T>>(a, stream);
+}
+
+// Accumulating product with the co-residable Lite tiles (no row skip).
+template <typename T>
+int semiring_gemm_lite(const T* A, const T* B, T* C, int M, int N, int K, long long lda, long long ldb,
+                       long long ldc, int kind, cudaStream_t stream) {
+    if (M < 0 || N < 0 || K < 0 || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
+    if (M == 0 || N == 0) return SMX_OK;
+    if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return SMX_E_ALIGN;
+    if (!ld_ok(lda, sizeof(T)) || !ld_ok(ldb, sizeof(T)) || !ld_ok(ldc, sizeof(T))) return SMX_E_ALIGN;
+    GemmArgs<T> a{A, B, C, M, N, K, lda, ldb, ldc, kind == SMX_ANTI, 1, 0, 0, bounded_fastpath_enabled()};
+    return launch_semiring_gemm<LiteCfg<T>>(a, stream);
 }
 
 }  // namespace smx
