@@ -128,6 +128,13 @@ int smx_semiring_gemm_skip(const void* A, const void* B, void* C, int M, int N, 
 int smx_bool_gemm_i8(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* C_bits,
                      int M, int N, int K, int lda, int ldbt, int ldc, int accumulate,
                      void* stream);
+/* BoolMatrix.__mul__ on packed bit rows in one call (unpack A, fused
+ * bits -> B^T bytes, tcgen05 product with the packed-bit epilogue).  C rows
+ * are fully written, padding words zeroed.  Workspace: see
+ * smx_bool_mul_tc_workspace_bytes. */
+size_t smx_bool_mul_tc_workspace_bytes(int M, int N, int K);
+int smx_bool_mul_tc(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int N, int K,
+                    int lda_w, int ldb_w, int ldc_w, void* workspace, size_t ws_bytes, void* stream);
 /* Warshall closure in place on 0/1 bytes (n x n, ld bytes, 16-byte aligned
  * rows) with tensor-core phases 2/3. */
 size_t smx_bool_warshall_i8_workspace_bytes(int n, int ld);

@@ -54,6 +54,8 @@ _SIGS = {
                             c_int),
 }
 _SIGS.update({
+    "smx_bool_mul_tc_workspace_bytes": ([c_int, c_int, c_int], c_size_t),
+    "smx_bool_mul_tc": ([c_void_p] * 3 + [c_int] * 6 + [c_void_p, c_size_t, c_void_p], c_int),
     "smx_bool_gemm_i8": ([c_void_p] * 4 + [c_int] * 7 + [c_void_p], c_int),
     "smx_bool_warshall_i8_workspace_bytes": ([c_int, c_int], c_size_t),
     "smx_bool_warshall_i8": ([c_void_p, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),

@@ -458,11 +458,53 @@ int bool_warshall_i8(uint8_t* T, int n, long long ld, void* ws, size_t ws_bytes,
     return SMX_OK;
 }
 
+int unpack_bits(const uint32_t* words, uint8_t* bytes, int rows, int cols, long long ld_w, long long ld,
+                cudaStream_t s);
+int unpack_bits_transposed(const uint32_t* words, uint8_t* out, int rows, int cols, long long ld_w,
+                           long long ld_out, cudaStream_t s);
+
+inline long long round16(long long x) { return (x + 15) & ~15LL; }
+
+inline size_t bool_mul_ws_bytes(int M, int N, int K) {
+    return (size_t)((M * round16(K) + 255) & ~255LL) + (size_t)N * round16(K);
+}
+
+// BoolMatrix.__mul__ on the reference's bit rows in one call: A bits ->
+// bytes, B bits -> B^T bytes (fused transpose), tensor-core product with the
+// packed-bit epilogue.  Workspace: M x K + N x K bytes (rows rounded to 16).
+int bool_mul_tc(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int N, int K, long long lda_w,
+                long long ldb_w, long long ldc_w, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (M < 0 || N < 0 || K < 1) return SMX_E_ARG;
+    if (M == 0 || N == 0) return SMX_OK;
+    if (ws == nullptr || ws_bytes < bool_mul_ws_bytes(M, N, K)) return SMX_E_WORKSPACE;
+    uint8_t* a8 = reinterpret_cast<uint8_t*>(ws);
+    uint8_t* bt8 = a8 + ((M * round16(K) + 255) & ~255LL);
+    SMX_TRY(unpack_bits(A, a8, M, K, lda_w, round16(K), s));
+    SMX_TRY(unpack_bits_transposed(B, bt8, K, N, ldb_w, round16(K), s));
+    // words past ceil(N/32) in each output row are padding: keep them zero
+    const long long nw = (N + 31) / 32;
+    if (ldc_w > nw) {
+        cudaError_t e = cudaMemset2DAsync(C + nw, ldc_w * 4, 0, (ldc_w - nw) * 4, M, s);
+        if (e != cudaSuccess) return (int)e;
+    }
+    return bool_i8_gemm(a8, bt8, nullptr, C, M, N, K, round16(K), round16(K), ldc_w, 0, 0, 0, s);
+}
+
 }  // namespace smx
 
 using namespace smx;
 
 extern "C" {
+
+size_t smx_bool_mul_tc_workspace_bytes(int M, int N, int K) {
+    if (M <= 0 || N <= 0 || K <= 0) return 0;
+    return bool_mul_ws_bytes(M, N, K);
+}
+
+int smx_bool_mul_tc(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int N, int K, int lda_w,
+                    int ldb_w, int ldc_w, void* ws, size_t ws_bytes, void* stream) {
+    return bool_mul_tc(A, B, C, M, N, K, lda_w, ldb_w, ldc_w, ws, ws_bytes, as_stream(stream));
+}
 
 int smx_bool_gemm_i8(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* C_bits, int M, int N, int K,
                      int lda, int ldbt, int ldc, int accumulate, void* stream) {

@@ -105,6 +105,25 @@ int transpose_bytes(const uint8_t* in, uint8_t* out, int rows, int cols, long lo
     SMX_RETURN_LAUNCH();
 }
 
+int unpack_bits(const uint32_t* words, uint8_t* bytes, int rows, int cols, long long ld_w, long long ld,
+                cudaStream_t s) {
+    if (rows < 0 || cols < 0 || ld < cols || ld_w * 32 < cols) return SMX_E_ARG;
+    if (rows == 0 || cols == 0) return SMX_OK;
+    const long long t = (long long)rows * ((cols + 31) / 32);
+    unpack_bits_kernel<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(words, bytes, rows, cols, ld_w, ld);
+    SMX_RETURN_LAUNCH();
+}
+
+int unpack_bits_transposed(const uint32_t* words, uint8_t* out, int rows, int cols, long long ld_w,
+                           long long ld_out, cudaStream_t s) {
+    if (rows < 0 || cols < 0 || ld_out < rows || ld_w * 32 < cols) return SMX_E_ARG;
+    if (rows == 0 || cols == 0) return SMX_OK;
+    const long long warps = (long long)((rows + 31) / 32) * ((cols + 31) / 32);
+    unpack_bits_t_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(words, out, rows, cols, ld_w,
+                                                                             ld_out);
+    SMX_RETURN_LAUNCH();
+}
+
 }  // namespace smx
 
 using namespace smx;
@@ -127,22 +146,12 @@ int smx_pack_bits(const uint8_t* bytes, uint32_t* words, int rows, int cols, int
 
 int smx_unpack_bits(const uint32_t* words, uint8_t* bytes, int rows, int cols, int ld_w, int ld,
                     void* stream) {
-    if (rows < 0 || cols < 0 || ld < cols || (long long)ld_w * 32 < cols) return SMX_E_ARG;
-    if (rows == 0 || cols == 0) return SMX_OK;
-    const long long t = (long long)rows * ((cols + 31) / 32);
-    unpack_bits_kernel<<<(unsigned)((t + 255) / 256), 256, 0, as_stream(stream)>>>(words, bytes, rows,
-                                                                                 cols, ld_w, ld);
-    SMX_RETURN_LAUNCH();
+    return unpack_bits(words, bytes, rows, cols, ld_w, ld, as_stream(stream));
 }
 
 int smx_unpack_bits_transposed(const uint32_t* words, uint8_t* bytes_t, int rows, int cols, int ld_w,
                                int ld_out, void* stream) {
-    if (rows < 0 || cols < 0 || ld_out < rows || (long long)ld_w * 32 < cols) return SMX_E_ARG;
-    if (rows == 0 || cols == 0) return SMX_OK;
-    const long long warps = (long long)((rows + 31) / 32) * ((cols + 31) / 32);
-    unpack_bits_t_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, as_stream(stream)>>>(
-        words, bytes_t, rows, cols, ld_w, ld_out);
-    SMX_RETURN_LAUNCH();
+    return unpack_bits_transposed(words, bytes_t, rows, cols, ld_w, ld_out, as_stream(stream));
 }
 
 int smx_transpose_u8(const uint8_t* in, uint8_t* out, int rows, int cols, int ld_in, int ld_out,

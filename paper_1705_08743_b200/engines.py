@@ -76,14 +76,16 @@ def bits_to_bytes(m, transpose: bool = False) -> torch.Tensor:
 
 
 def bool_mul_tc(a, b):
-    """Tensor-core product: tcgen05 kind::i8 GEMM, count > 0, packed-bit epilogue."""
+    """Tensor-core product: tcgen05 kind::i8 GEMM, count > 0, packed-bit epilogue
+    (one C-ABI call: unpack, fused B^T unpack, product)."""
     from .boolmat import BoolMatrix, _stride_words
-    a8 = bits_to_bytes(a)
-    bt8 = bits_to_bytes(b, transpose=True)
-    out = torch.zeros((a.rows, _stride_words(b.cols)), dtype=torch.int32, device=a.device)
-    check(lib().smx_bool_gemm_i8(a8.data_ptr(), bt8.data_ptr(), None, out.data_ptr(), a.rows,
-                                 b.cols, a.cols, a8.shape[1], bt8.shape[1], out.shape[1], 0,
-                                 stream_ptr(a.device)), "smx_bool_gemm_i8")
+    L = lib()
+    out = torch.empty((a.rows, _stride_words(b.cols)), dtype=torch.int32, device=a.device)
+    nbytes = L.smx_bool_mul_tc_workspace_bytes(a.rows, b.cols, a.cols)
+    ws = _native.workspace(nbytes, a.device)
+    check(L.smx_bool_mul_tc(a._words.data_ptr(), b._words.data_ptr(), out.data_ptr(), a.rows, b.cols,
+                            a.cols, a.stride_words, b.stride_words, out.shape[1], ws.data_ptr(), nbytes,
+                            stream_ptr(a.device)), "smx_bool_mul_tc")
     return BoolMatrix(a.rows, b.cols, out)
 
 
