@@ -153,9 +153,13 @@ def measure_issue_peak():
 
 
 def load_traffic(workload: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (dram__bytes_read.sum + dram__bytes_write.sum)."""
     p = REPO / "profiles" / "traffic.json"
     if p.exists():
-        return json.loads(p.read_text()).get(workload)
+        entry = json.loads(p.read_text()).get(workload)
+        if entry:
+            return entry["bytes_per_launch"]
     return None
 
 
@@ -391,6 +395,7 @@ def run_ours(args, world, rank, local_rank):
         result["roofline"] = {
             "bound": "int_issue", "achieved": achieved / 1e12, "peak": peak_cells / 1e12,
             "unit": "Tcell/s", "frac": achieved / peak_cells, "traffic": traffic,
+            "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
             "kernel": "semiring_gemm_kernel (FW phase 3)" if cfg.op == "closure" else "semiring_gemm_kernel",
             "launches_timed": dom_launches,
             "avg_launch_ms": dom_secs_total / dom_launches * 1e3,
