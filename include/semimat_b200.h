@@ -50,7 +50,12 @@ unsigned long long smx_launch_count(void);
 /* The u16/u32 semiring kernels run a k-tile with the 1-instruction update
  * c = min(c, a + b) when the CTA has verified that every staged lane of that
  * k-tile is below 2^(w-1) (so a + b cannot reach S and the clamp is a
- * no-op); otherwise the general 2-instruction update.  Results are identical;
+ * no-op); otherwise the general 2-instruction update.  The public products
+ * (smx_semiring_gemm_u16/u32) additionally certify every A row and B column
+ * as "S or < 2^(w-2)" in a first pass; a CTA whose rows, columns and C tile
+ * are all certified runs its whole K loop with the 1-instruction update in
+ * a shifted encoding (S -> 2^(w-1)-1, results >= that map back to S), which
+ * covers sparse inputs with unreachable entries.  Results are identical;
  * this switch (default on) forces the general form.  Returns the old value. */
 int smx_set_bounded_fastpath(int enable);
 

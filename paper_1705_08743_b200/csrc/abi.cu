@@ -13,6 +13,32 @@ int lookahead_enabled() { return g_lookahead.load(std::memory_order_relaxed); }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int bounded_fastpath_enabled() { return g_bounded.load(std::memory_order_relaxed); }
 
+int scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+    static bool pool_configured[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMX_E_ARG;
+    if (!pool_configured[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long threshold = ~0ULL;   // keep freed blocks cached
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+        }
+        pool_configured[dev] = true;
+    }
+    cudaError_t e = cudaMallocAsync(p, bytes, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return (int)e;
+    }
+    return SMX_OK;
+}
+
+int scratch_free(void* p, cudaStream_t s) {
+    cudaError_t e = cudaFreeAsync(p, s);
+    return e == cudaSuccess ? SMX_OK : (int)e;
+}
+
 int side_stream(SideStream** out) {
     static SideStream per_dev[64];
     int dev = 0;

@@ -407,12 +407,12 @@ int smx_semiring_gemm_u8(const uint8_t* A, const uint8_t* B, uint8_t* C, int M, 
 int smx_semiring_gemm_u16(const uint16_t* A, const uint16_t* B, uint16_t* C, int M, int N, int K,
                           int lda, int ldb, int ldc, int kind, int accumulate, void* stream) {
     return semiring_gemm<uint16_t>(A, B, C, M, N, K, lda, ldb, ldc, kind, accumulate, 0, 0,
-                                   as_stream(stream));
+                                   as_stream(stream), /*certify=*/true);
 }
 int smx_semiring_gemm_u32(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int N, int K,
                           int lda, int ldb, int ldc, int kind, int accumulate, void* stream) {
     return semiring_gemm<uint32_t>(A, B, C, M, N, K, lda, ldb, ldc, kind, accumulate, 0, 0,
-                                   as_stream(stream));
+                                   as_stream(stream), /*certify=*/true);
 }
 
 int smx_semiring_gemm_skip(const void* A, const void* B, void* C, int M, int N, int K, int lda,

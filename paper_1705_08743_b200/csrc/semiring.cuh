@@ -45,6 +45,20 @@ template <> struct Lane<uint16_t> {
     __device__ __forceinline__ static uint32_t step_bounded(uint32_t c, uint32_t b, uint32_t a) {
         return __viaddmin_u16x2(a, b, c);
     }
+    // Sparse-bounded certificate and shifted encoding: every lane is either
+    // S (unreachable) or < 2^14.  Shifting S to S' = 2^15 - 1 makes every
+    // sum <= 65534 (no wrap); finite + finite <= 32766 < S', anything with
+    // an S' operand >= S', so "result >= S'" is exactly "unreachable".
+    __device__ __forceinline__ static bool cert_ok(uint32_t w) {
+        const uint32_t is_s = __vcmpeq2(w, 0xFFFFFFFFu);
+        return ((w & ~is_s) & 0xC000C000u) == 0u;
+    }
+    __device__ __forceinline__ static uint32_t to_shifted(uint32_t w) {
+        return w - (__vcmpeq2(w, 0xFFFFFFFFu) & 0x80008000u);
+    }
+    __device__ __forceinline__ static uint32_t from_shifted(uint32_t w) {
+        return w | __vcmpgeu2(w, 0x7FFF7FFFu);
+    }
 };
 
 template <> struct Lane<uint8_t> {
@@ -63,6 +77,9 @@ template <> struct Lane<uint8_t> {
     __device__ __forceinline__ static uint32_t step_bounded(uint32_t c, uint32_t b, uint32_t a) {
         return __viaddmin_u16x2(a, b, c);
     }
+    __device__ __forceinline__ static bool cert_ok(uint32_t) { return true; }
+    __device__ __forceinline__ static uint32_t to_shifted(uint32_t w) { return w; }
+    __device__ __forceinline__ static uint32_t from_shifted(uint32_t w) { return w; }
 };
 
 template <> struct Lane<uint32_t> {
@@ -81,6 +98,10 @@ template <> struct Lane<uint32_t> {
     __device__ __forceinline__ static uint32_t step_bounded(uint32_t c, uint32_t b, uint32_t a) {
         return __viaddmin_u32(a, b, c);
     }
+    // as for u16 with 2^30 / S' = 2^31 - 1
+    __device__ __forceinline__ static bool cert_ok(uint32_t w) { return w == kS || w < 0x40000000u; }
+    __device__ __forceinline__ static uint32_t to_shifted(uint32_t w) { return w == kS ? 0x7FFFFFFFu : w; }
+    __device__ __forceinline__ static uint32_t from_shifted(uint32_t w) { return w >= 0x7FFFFFFFu ? kS : w; }
 };
 
 // ---- chunk <-> canonical words ------------------------------------------

@@ -37,6 +37,13 @@ struct GemmArgs {
     int skip_tile0;   // first M-tile (in units of BM) to skip
     int skip_tiles;   // number of M-tiles skipped
     int allow_bounded;  // permit the verified 1-instruction k-tiles
+    // Optional "sparse-bounded" row/column certificates (lane_flags_kernel):
+    // rowflags[i] = every lane of A row i (k < K) is S or < 2^(w-2);
+    // colflags[j] = the same for B column j.  A CTA whose rows, columns and
+    // C tile are all certified runs every k-tile with the 1-instruction
+    // update in a shifted encoding (see semiring_gemm_kernel).
+    const uint8_t* rowflags;
+    const uint8_t* colflags;
 };
 
 // Process-wide switch for the bounded 1-instruction k-tiles (on by default;
@@ -187,7 +194,10 @@ __device__ __forceinline__ uint4 load_b_chunk(const GemmArgs<T>& p, int col0, in
     return identity_chunk<T>(p.anti);
 }
 
-template <typename Cfg, typename T>
+// CERT: instantiate the sparse-bounded certificate logic (only the certified
+// public products use it; the Floyd-Warshall instantiation carries none of
+// its registers or branches).
+template <typename Cfg, typename T, bool CERT>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(const GemmArgs<T> p) {
     using L = Lane<T>;
     constexpr int BM = Cfg::BM, BNW = Cfg::BNW, BK = Cfg::BK, TM = Cfg::TM, TNW = Cfg::TNW;
@@ -223,6 +233,30 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
         }
     }
 
+    // ---- sparse-bounded CTA: all A rows / B columns certified (S or small)
+    // and the C tile too -> whole K loop in the shifted 1-instruction form.
+    bool sparse = false;
+    if constexpr (!L::kOneInstr && CERT) {
+        if (p.rowflags != nullptr && p.allow_bounded) {
+            bool ok = true;
+            for (int i = tid; i < BM; i += Cfg::THREADS)
+                if (row0 + i < p.M && !p.rowflags[row0 + i]) ok = false;
+            for (int j = tid; j < Cfg::BN; j += Cfg::THREADS)
+                if (col0 + j < p.N && !p.colflags[col0 + j]) ok = false;
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TNW; ++j) ok = ok && L::cert_ok(acc[i][j]);
+            sparse = __syncthreads_and(ok);
+            if (sparse) {
+#pragma unroll
+                for (int i = 0; i < TM; ++i)
+#pragma unroll
+                    for (int j = 0; j < TNW; ++j) acc[i][j] = L::to_shifted(acc[i][j]);
+            }
+        }
+    }
+
     uint4 a_st[Cfg::A_PT];
     uint4 b_st[Cfg::B_PT];
 
@@ -245,6 +279,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
                 uint32_t* dst = As + (buf * AP * BK + kc * E) * BM + r;
                 uint32_t w[WPC];
                 chunk_to_words<T>(a_st[i], anti, w);
+                if (sparse) {
+#pragma unroll
+                    for (int q = 0; q < WPC; ++q) w[q] = L::to_shifted(w[q]);
+#pragma unroll
+                    for (int j = 0; j < E; ++j) dst[j * BM] = L::splat(word_cell<T>(w, j));
+                    continue;
+                }
 #pragma unroll
                 for (int q = 0; q < WPC; ++q) hi |= w[q];
 #pragma unroll
@@ -264,7 +305,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
                 uint32_t w[WPC];
                 chunk_to_words<T>(b_st[i], anti, w);
 #pragma unroll
-                for (int q = 0; q < WPC; ++q) hi |= w[q];
+                for (int q = 0; q < WPC; ++q) {
+                    hi |= w[q];
+                    if (sparse) w[q] = L::to_shifted(w[q]);
+                }
 #pragma unroll
                 for (int q = 0; q < WPC / 4; ++q)
                     dst[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
@@ -331,7 +375,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
         if constexpr (L::kOneInstr) {
             ktile(buf, std::false_type{});
         } else {
-            if (bounded) ktile(buf, std::true_type{});
+            if (bounded || sparse) ktile(buf, std::true_type{});
             else ktile(buf, std::false_type{});
         }
         bool ok = true;
@@ -340,6 +384,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
     }
 
     // ---- epilogue ---------------------------------------------------------
+    if constexpr (!L::kOneInstr) {
+        if (sparse) {
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TNW; ++j) acc[i][j] = L::from_shifted(acc[i][j]);
+        }
+    }
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
         const int grow = row0 + tr * TM + i;
@@ -374,7 +426,22 @@ int launch_large(const GemmArgs<T>& a, cudaStream_t stream);
 
 template <typename Cfg, typename T>
 int launch_semiring_gemm(const GemmArgs<T>& a, cudaStream_t stream) {
-    auto kern = semiring_gemm_kernel<Cfg, T>;
+    if (a.rowflags != nullptr) {
+        auto kern = semiring_gemm_kernel<Cfg, T, true>;
+        static bool configured = false;  // per instantiation
+        if (!configured) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)Cfg::SMEM);
+            if (e != cudaSuccess) return (int)e;
+            configured = true;
+        }
+        const int mtiles = ceil_div(a.M, Cfg::BM) - a.skip_tiles;
+        const int ntiles = ceil_div(a.N, Cfg::BN);
+        if (mtiles <= 0 || ntiles <= 0) return SMX_OK;
+        kern<<<dim3(ntiles, mtiles), Cfg::THREADS, Cfg::SMEM, stream>>>(a);
+        SMX_RETURN_LAUNCH();
+    }
+    auto kern = semiring_gemm_kernel<Cfg, T, false>;
     static bool configured = false;  // per instantiation
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -390,11 +457,106 @@ int launch_semiring_gemm(const GemmArgs<T>& a, cudaStream_t stream) {
     SMX_RETURN_LAUNCH();
 }
 
+// ---- sparse-bounded certificates -------------------------------------------
+// rowflags[i] (A, over k < K) and colflags[j] (B, over k < K): 1 iff every
+// lane in distance form is S or < 2^(w-2) (Lane<T>::cert_ok).  One warp per A
+// row (coalesced along k); one thread per 16-byte column chunk of B walking
+// down its K rows (coalesced across threads).
+template <typename T>
+__global__ void lane_rowflags_kernel(const T* __restrict__ A, int M, int K, long long lda, bool anti,
+                                     uint8_t* __restrict__ flags) {
+    using L = Lane<T>;
+    constexpr int E = L::kCellsPerChunk;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= M) return;
+    const T* row = A + warp * lda;
+    bool ok = true;
+    for (int k = lane * E; k < K; k += 32 * E) {
+        uint4 raw = __ldg(reinterpret_cast<const uint4*>(row + k));
+        if (k + E > K) {   // cells >= K: identity (S), which certifies
+            T* cells = reinterpret_cast<T*>(&raw);
+            const T id = anti ? T(0) : T(L::kS);
+            for (int j = K - k; j < E; ++j) cells[j] = id;
+        }
+        uint32_t w[Lane<T>::kWordsPerChunk];
+        chunk_to_words<T>(raw, anti, w);
+#pragma unroll
+        for (int q = 0; q < Lane<T>::kWordsPerChunk; ++q) ok = ok && L::cert_ok(w[q]);
+    }
+    ok = __all_sync(0xFFFFFFFFu, ok);
+    if (lane == 0) flags[warp] = ok ? 1 : 0;
+}
+
+// Column flags start at 1 (memset); each thread checks one 16-byte column
+// chunk over a 64-row slice of K and clears the flags that fail (concurrent
+// writers only ever store 0, so the race is benign).
+constexpr int kColFlagSlice = 64;
+
+template <typename T>
+__global__ void lane_colflags_kernel(const T* __restrict__ B, int N, int K, long long ldb, bool anti,
+                                     uint8_t* __restrict__ flags) {
+    using L = Lane<T>;
+    constexpr int E = L::kCellsPerChunk, WPC = L::kWordsPerChunk, CPW = L::kCellsPerWord;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int c0 = (int)t * E;
+    if (c0 >= N) return;
+    const int k0 = blockIdx.y * kColFlagSlice, k1 = min(K, k0 + kColFlagSlice);
+    bool ok[WPC];
+#pragma unroll
+    for (int q = 0; q < WPC; ++q) ok[q] = true;
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) {
+        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(B + k * ldb + c0));
+        uint32_t w[WPC];
+        chunk_to_words<T>(raw, anti, w);
+#pragma unroll
+        for (int q = 0; q < WPC; ++q) ok[q] = ok[q] && L::cert_ok(w[q]);
+    }
+    // per-word verdicts cover CPW cells each (u16: a pair of columns)
+#pragma unroll
+    for (int q = 0; q < WPC; ++q)
+#pragma unroll
+        for (int l = 0; l < CPW; ++l) {
+            const int c = c0 + q * CPW + l;
+            if (c < N && !ok[q]) flags[c] = 0;
+        }
+}
+
+template <typename T>
+int launch_lane_flags(const T* A, int M, int K, long long lda, const T* B, int N, long long ldb, bool anti,
+                      uint8_t* rowflags, uint8_t* colflags, cudaStream_t s) {
+    const long long rt = (long long)M * 32;
+    lane_rowflags_kernel<T><<<(unsigned)((rt + 255) / 256), 256, 0, s>>>(A, M, K, lda, anti, rowflags);
+    SMX_LAUNCHED_OR_RETURN();
+    cudaError_t e = cudaMemsetAsync(colflags, 1, (size_t)N, s);
+    if (e != cudaSuccess) return (int)e;
+    const long long ct = (N + Lane<T>::kCellsPerChunk - 1) / Lane<T>::kCellsPerChunk;
+    dim3 grid((unsigned)((ct + 127) / 128), (unsigned)((K + kColFlagSlice - 1) / kColFlagSlice));
+    lane_colflags_kernel<T><<<grid, 128, 0, s>>>(B, N, K, ldb, anti, colflags);
+    SMX_RETURN_LAUNCH();
+}
+
+// Stream-ordered scratch for the certificates (cudaMallocAsync from the
+// device's default pool, kept cached by a high release threshold).
+int scratch_alloc(void** p, size_t bytes, cudaStream_t s);
+int scratch_free(void* p, cudaStream_t s);
+
+// Certify only products large enough to amortise the flag pass.
+inline bool worth_certifying(int M, int N, int K) {
+    return (long long)M * N >= (1LL << 20) && K >= 64;
+}
+
 // Validates and dispatches one product; used by every entry point.
+// `certify`: compute the sparse-bounded row/column certificates first (the
+// public product entry points).  Floyd-Warshall's phase-3 calls leave it off:
+// their tiles are almost all finite-and-small after the first rounds, where
+// the per-k-tile bounded vote already applies, and the extra pass and CTA
+// prologue measured -7% on the closure.
 template <typename T>
 int semiring_gemm(const T* A, const T* B, T* C, int M, int N, int K, long long lda,
                   long long ldb, long long ldc, int kind, int accumulate, int skip_row0,
-                  int skip_rows, cudaStream_t stream) {
+                  int skip_rows, cudaStream_t stream, bool certify = false) {
     if (M < 0 || N < 0 || K < 0 || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
     if (M == 0 || N == 0) return SMX_OK;
     if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return SMX_E_ALIGN;
@@ -402,7 +564,21 @@ int semiring_gemm(const T* A, const T* B, T* C, int M, int N, int K, long long l
         return SMX_E_ALIGN;
     if (lda < K || ldb < N || ldc < N) return SMX_E_ARG;
     GemmArgs<T> a{A, B, C, M, N, K, lda, ldb, ldc, kind == SMX_ANTI, accumulate != 0, 0, 0,
-                  bounded_fastpath_enabled()};
+                  bounded_fastpath_enabled(), nullptr, nullptr};
+    // sparse-bounded certificates for u16/u32 products worth it
+    void* flags = nullptr;
+    if (certify && !Lane<T>::kOneInstr && a.allow_bounded && worth_certifying(M, N, K)) {
+        if (scratch_alloc(&flags, (size_t)M + N, stream) == SMX_OK) {
+            uint8_t* rf = reinterpret_cast<uint8_t*>(flags);
+            SMX_TRY(launch_lane_flags<T>(A, M, K, lda, B, N, ldb, a.anti, rf, rf + M, stream));
+            a.rowflags = rf;
+            a.colflags = rf + M;
+        }
+    }
+    struct FreeOnExit {
+        void* p; cudaStream_t s;
+        ~FreeOnExit() { if (p) scratch_free(p, s); }
+    } guard{flags, stream};
     if (skip_rows > 0) {
         // skip ranges are whole 128-row tiles of the large config (FW phase 3)
         if (skip_row0 % LargeCfg<T>::BM) return SMX_E_ARG;
@@ -431,7 +607,8 @@ int semiring_gemm_lite(const T* A, const T* B, T* C, int M, int N, int K, long l
     if (M == 0 || N == 0) return SMX_OK;
     if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return SMX_E_ALIGN;
     if (!ld_ok(lda, sizeof(T)) || !ld_ok(ldb, sizeof(T)) || !ld_ok(ldc, sizeof(T))) return SMX_E_ALIGN;
-    GemmArgs<T> a{A, B, C, M, N, K, lda, ldb, ldc, kind == SMX_ANTI, 1, 0, 0, bounded_fastpath_enabled()};
+    GemmArgs<T> a{A, B, C, M, N, K, lda, ldb, ldc, kind == SMX_ANTI, 1, 0, 0, bounded_fastpath_enabled(),
+                  nullptr, nullptr};
     return launch_semiring_gemm<LiteCfg<T>>(a, stream);
 }
 

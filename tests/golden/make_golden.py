@@ -207,6 +207,27 @@ def entrywise_cases():
     return cases, manifest
 
 
+def matio_cases():
+    """The reference's SRMAT1 bytes and text for assorted matrices
+    (matio.py:37-149), incl. the 65-column Boolean padding case."""
+    from semimat import matio
+    rng = random.Random(4242)
+    out = []
+    for rows, cols in [(1, 1), (3, 65), (5, 64), (2, 130)]:
+        bits = np.array([[rng.random() < 0.4 for _ in range(cols)] for _ in range(rows)], dtype=np.uint8)
+        m = ref_bool(bits)
+        out.append(dict(kind="bool", bits=bits.tolist(), binary=matio.to_binary(m).hex(),
+                        text=matio.format_text(m)))
+    for width in (8, 16, 32):
+        for kind in ("anti", "dist"):
+            for rows, cols in [(1, 1), (3, 17), (4, 9)]:
+                data = rand_lane(rng, rows, cols, width, kind, 0.3)
+                m = ref_lane(kind, data, cols, width)
+                out.append(dict(kind=kind, width=width, rows=m.to_lists(), binary=matio.to_binary(m).hex(),
+                                text=matio.format_text(m)))
+    return out
+
+
 def samples():
     """The reference's sample files, parsed with the reference's own loaders."""
     from semimat import graphio, matio
@@ -265,6 +286,7 @@ def main():
         np.savez_compressed(HERE / "entrywise.npz", **cases)
         (HERE / "entrywise.json").write_text(json.dumps(manifest, indent=0))
         print(f"entrywise cases: {len(manifest)}")
+        (HERE / "matio.json").write_text(json.dumps(matio_cases(), indent=0))
         if args.only_entrywise:
             return
 

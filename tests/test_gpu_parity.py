@@ -494,3 +494,71 @@ def test_fw_n16384_block256_matches_squaring():
     c = a.transitive_closure()
     assert (a | (c * a)) == c
     assert engines.closure_by_squaring(a) == c
+
+
+@pytest.mark.parametrize("width", [16, 32])
+def test_sparse_bounded_certificates_are_exact(width, oracle_lib):
+    """Large products take the certified shifted 1-instruction form when every
+    A row / B column / C tile lane is S or < 2^(w-2); values at the edge of the
+    certificate (2^(w-2) - 1) and just past it (2^(w-2)) must both be exact."""
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    rng = np.random.default_rng(33)
+    q = 1 << (width - 2)
+    S = (1 << width) - 1
+    n = 1100                                             # M*N >= 2^20: certified path
+    edge = np.where(rng.random((n, n)) < 0.5, S, rng.integers(q - 4, q, size=(n, n))).astype(np.uint64)
+    over = edge.copy()
+    over[rng.integers(0, n, 50), rng.integers(0, n, 50)] = q   # breaks the certificate
+    sparse = np.where(rng.random((n, n)) < 0.9, S, rng.integers(0, 1000, size=(n, n))).astype(np.uint64)
+    for name, vals in (("edge", edge), ("over", over), ("sparse", sparse)):
+        a = _fast_lane("dist", vals, width)
+        b = _fast_lane("dist", vals.T.copy(), width)
+        want = oracle_lib.semiring_mul(a.data, b.data, n, width, "dist")
+        np.testing.assert_array_equal((a * b).data, want, err_msg=name)
+        old = lib.smx_set_bounded_fastpath(0)
+        try:
+            np.testing.assert_array_equal((a * b).data, want, err_msg=name + " (general)")
+        finally:
+            lib.smx_set_bounded_fastpath(old)
+        aa, ba = ~a, ~b
+        np.testing.assert_array_equal((aa * ba).data,
+                                      oracle_lib.semiring_mul(aa.data, ba.data, n, width, "anti"),
+                                      err_msg=name + " anti")
+
+
+# -- SRMAT1 / text I/O to and from HBM (SURVEY 8(f) item 3) ----------------------
+
+def test_matio_matches_reference_bytes(tmp_path):
+    import json
+    from conftest import GOLDEN
+    from paper_1705_08743_b200 import matio
+    for case in json.loads((GOLDEN / "matio.json").read_text()):
+        if case["kind"] == "bool":
+            m = BoolMatrix.from_lists(case["bits"])
+        else:
+            m = CLS[case["kind"]].from_lists(case["rows"], case["width"])
+        assert matio.to_binary(m).hex() == case["binary"]
+        assert matio.format_text(m) == case["text"]
+        back = matio.from_binary(bytes.fromhex(case["binary"]))
+        assert type(back) is type(m) and back == m
+        assert matio.parse_text(case["text"]) == m
+        p = tmp_path / "m.bin"
+        matio.save(m, p, binary=True)
+        assert matio.load(p) == m
+        matio.save(m, p)
+        assert matio.load(p) == m
+
+
+def test_matio_errors_match_reference():
+    from paper_1705_08743_b200 import matio
+    with pytest.raises(matio.MatrixFormatError, match="truncated header"):
+        matio.from_binary(b"SRMAT1")
+    with pytest.raises(matio.MatrixFormatError, match="bad magic"):
+        matio.from_binary(b"XXXXXX" + bytes(10))
+    bad = bytearray(matio.to_binary(BoolMatrix.from_lists([[1] * 65])))
+    bad[-1] |= 0x80                                   # a padding bit of the final block
+    with pytest.raises(matio.MatrixFormatError, match="nonzero padding bits"):
+        matio.from_binary(bytes(bad))
+    with pytest.raises(matio.MatrixFormatError, match="expected 3 values"):
+        matio.parse_text("antidist 8 1 3\n1 2\n")

@@ -140,3 +140,23 @@ def test_oracle_reproduces_reference_digest(oracle_lib, config_digests, name):
     else:
         out = oracle_lib.semiring_close(inputs[0], cfg.width, "anti")
     assert sha(out) == d["output_sha256"]
+
+
+def test_matio_fixture_is_self_consistent():
+    """The reference bytes decode to the reference rows (host-only check of the
+    fixture itself, so a corrupt fixture fails on the CPU too)."""
+    import json
+    import struct
+    from conftest import GOLDEN
+    for case in json.loads((GOLDEN / "matio.json").read_text()):
+        raw = bytes.fromhex(case["binary"])
+        magic, tag, width, rows, cols = struct.unpack_from("<6sBBII", raw)
+        assert magic == b"SRMAT1"
+        if case["kind"] == "bool":
+            assert tag == ord("B") and width == 0
+            blocks = np.frombuffer(raw[16:], dtype="<u8").reshape(rows, -1)
+            bits = np.unpackbits(blocks.view(np.uint8).reshape(rows, -1), axis=1, bitorder="little")
+            assert bits[:, :cols].tolist() == case["bits"]
+        else:
+            dt = {8: "<u1", 16: "<u2", 32: "<u4"}[width]
+            assert np.frombuffer(raw[16:], dtype=dt).reshape(rows, cols).tolist() == case["rows"]
