@@ -25,6 +25,7 @@ struct BitsArgs {
     long long lda, ldb, ldc;   // in words
     int accumulate;
     int skip_tile0, skip_tiles;
+    int kw_per;   // k-words per CTA (split-K when < ceil(K/32))
 };
 
 template <int BM_, int BNW_, int TM_, int TNW_, int MINB_>
@@ -52,6 +53,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_bits_gemm_kernel
     const int row0 = mt * BM, w0 = blockIdx.x * BNW;
     const int tc = tid % TCOLS, tr = tid / TCOLS;
 
+    // split-K: this CTA covers k-words [kw_lo, kw_hi); partial rows are OR-ed
+    // into C with atomicOr (OR is idempotent: the merge is exact)
+    const int nkw_all = (p.K + 31) / 32;
+    const int kw_lo = blockIdx.z * p.kw_per;
+    const int kw_hi = min(nkw_all, kw_lo + p.kw_per);
+    const bool split = p.kw_per < nkw_all;
+
     uint32_t acc[TM][TNW];
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
@@ -59,7 +67,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_bits_gemm_kernel
 #pragma unroll
         for (int j = 0; j < TNW; ++j) {
             const int gw = w0 + (j / HW) * (BNW / 2) + tc * HW + (j % HW);
-            acc[i][j] = (p.accumulate && grow < p.M && gw < p.Nw) ? p.C[(long long)grow * p.ldc + gw] : 0u;
+            acc[i][j] = (!split && p.accumulate && grow < p.M && gw < p.Nw)
+                            ? p.C[(long long)grow * p.ldc + gw] : 0u;
         }
     }
 
@@ -113,10 +122,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_bits_gemm_kernel
         }
     };
 
-    const int nkw = (p.K + 31) / 32;
-    if (nkw > 0) { gload(0); sstore(0); __syncthreads(); }
-    for (int kw = 0; kw < nkw; ++kw) {
-        const int buf = kw & 1;
+    if (kw_lo < kw_hi) { gload(kw_lo); sstore(0); __syncthreads(); }
+    for (int kw = kw_lo; kw < kw_hi; ++kw) {
+        const int buf = (kw - kw_lo) & 1;
+        const int nkw = kw_hi;
         if (kw + 1 < nkw) gload(kw + 1);
         uint32_t aw[TM];
 #pragma unroll
@@ -148,7 +157,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_bits_gemm_kernel
         for (int g = 0; g < 2; ++g) {
             const int gw = w0 + g * (BNW / 2) + tc * HW;
             uint32_t* dst = p.C + (long long)grow * p.ldc + gw;
-            if (gw + 4 <= p.Nw) {
+            if (split) {
+                for (int j = 0; j < 4; ++j)
+                    if (gw + j < p.Nw && acc[i][g * 4 + j]) atomicOr(dst + j, acc[i][g * 4 + j]);
+            } else if (gw + 4 <= p.Nw) {
                 *reinterpret_cast<uint4*>(dst) = make_uint4(acc[i][g * 4], acc[i][g * 4 + 1],
                                                             acc[i][g * 4 + 2], acc[i][g * 4 + 3]);
             } else {
@@ -160,10 +172,28 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_bits_gemm_kernel
 }
 
 template <typename Cfg>
-int launch_bits(const BitsArgs& a, cudaStream_t s) {
+int launch_bits(const BitsArgs& a_in, cudaStream_t s) {
+    BitsArgs a = a_in;
     const int mtiles = ceil_div(a.M, Cfg::BM) - a.skip_tiles;
     if (mtiles <= 0) return SMX_OK;
-    dim3 grid(ceil_div(a.Nw, Cfg::BNW), mtiles);
+    const int ntiles = ceil_div(a.Nw, Cfg::BNW);
+    const int nkw = ceil_div(a.K, 32);
+    // Thin products (the 256-row pivot panels of Warshall) are K-latency
+    // bound with a handful of CTAs: split K across CTAs and OR the partial
+    // rows together with atomics.  Needs C pre-set (accumulate, or zeroed).
+    int splits = 1;
+    const int tiles = mtiles * ntiles;
+    if (tiles < 2 * sm_count() && nkw >= 2) {
+        splits = ceil_div(2 * sm_count(), tiles);
+        if (splits > nkw) splits = nkw;
+    }
+    a.kw_per = ceil_div(nkw, splits);
+    splits = nkw > 0 ? ceil_div(nkw, a.kw_per) : 1;
+    if (splits > 1 && !a.accumulate) {
+        cudaError_t e = cudaMemset2DAsync(a.C, (size_t)a.ldc * 4, 0, (size_t)a.Nw * 4, a.M, s);
+        if (e != cudaSuccess) return (int)e;
+    }
+    dim3 grid(ntiles, mtiles, splits);
     bool_bits_gemm_kernel<Cfg><<<grid, Cfg::THREADS, 0, s>>>(a);
     SMX_RETURN_LAUNCH();
 }
@@ -176,7 +206,7 @@ int bool_bits_gemm(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int
     if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return SMX_E_ALIGN;
     if ((ldb & 3) || (ldc & 3)) return SMX_E_ALIGN;
     if (lda * 32 < K || ldb < Nw || ldc < Nw) return SMX_E_ARG;
-    BitsArgs a{A, B, C, M, Nw, K, lda, ldb, ldc, accumulate != 0, 0, 0};
+    BitsArgs a{A, B, C, M, Nw, K, lda, ldb, ldc, accumulate != 0, 0, 0, 0};
     const long long large_tiles = (long long)ceil_div(M, BitsLarge::BM) * ceil_div(Nw, BitsLarge::BNW);
     const bool large = large_tiles >= 2 * 148;
     const int bm = large ? BitsLarge::BM : BitsSmall::BM;

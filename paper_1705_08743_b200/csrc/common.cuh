@@ -53,6 +53,19 @@ inline bool ld_ok(long long ld, int elem_bytes) { return ((ld * elem_bytes) & 15
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// SM count of the current device (queried once per device).
+inline int sm_count() {
+    static int cached[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (!cached[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = n > 0 ? n : 148;
+    }
+    return cached[dev];
+}
+
 // Saturation limit S = 2^w - 1 per element type.
 template <typename T> struct Limit;
 template <> struct Limit<uint8_t>  { static constexpr uint32_t value = 0xFFu; };
