@@ -29,7 +29,9 @@ namespace smx {
 
 constexpr int kTcBM = 128;
 constexpr int kTcBK = 128;        // bytes of K per stage = one 128-byte swizzle row
-constexpr int kTcStages = 4;
+// TMA ring depth per tile width (192 KB of operand stages): deep enough that a
+// short-K product (C1: 8 k-blocks) issues every load up front.
+template <int BN> struct TcStages { static constexpr int value = BN <= 64 ? 8 : (BN <= 128 ? 6 : 4); };
 constexpr int kTcThreads = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -131,6 +133,7 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     extern __shared__ __align__(1024) uint8_t smem_dyn[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
+    constexpr int kTcStages = TcStages<BN>::value;
     uint8_t* sB = smem + kTcStages * A_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + kTcStages * B_BYTES);
     uint64_t* empty = full + kTcStages;
@@ -304,6 +307,7 @@ static int launch_tc(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long 
     CUtensorMap mA, mB;
     SMX_TRY(make_map(&mA, A, a.M, a.K, lda, kTcBM));
     SMX_TRY(make_map(&mB, Bt, a.N, a.K, ldbt, BN));
+    constexpr int kTcStages = TcStages<BN>::value;
     constexpr size_t smem = 1024 + kTcStages * (size_t)(kTcBM + BN) * kTcBK + 8 * (2 * kTcStages + 1) + 16;
     auto kern = bool_i8_gemm_kernel<BN>;
     static bool configured = false;
