@@ -25,6 +25,7 @@ _SIGS = {
     "smx_launch_count": ([], ctypes.c_ulonglong),
     "smx_set_bounded_fastpath": ([c_int], c_int),
     "smx_set_fw_lookahead": ([c_int], c_int),
+    "smx_set_graphs": ([c_int], c_int),
     "smx_set_fw_side_lite": ([c_int], c_int),
     "smx_set_fw_block": ([c_int], c_int),
     "smx_fw_trace_arm": ([c_int], c_int),

@@ -4,11 +4,15 @@
 #include "common.cuh"
 
 #include <atomic>
+#include <cstring>
+#include <mutex>
+#include <vector>
 
 namespace smx {
 static std::atomic<unsigned long long> g_launches{0};
 static std::atomic<int> g_bounded{1};
 static std::atomic<int> g_lookahead{1};
+static std::atomic<int> g_graphs{1};
 int lookahead_enabled() { return g_lookahead.load(std::memory_order_relaxed); }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int bounded_fastpath_enabled() { return g_bounded.load(std::memory_order_relaxed); }
@@ -56,9 +60,85 @@ int side_stream(SideStream** out) {
     *out = &f;
     return SMX_OK;
 }
+namespace {
+struct GraphEntry {
+    GraphKey key;
+    int dev;
+    cudaGraphExec_t exec;
+    unsigned long long launches;   // kernels recorded in the graph
+    unsigned long long stamp;      // LRU
+};
+constexpr size_t kMaxGraphs = 16;
+std::mutex g_graph_mu;
+std::vector<GraphEntry> g_graph_cache;
+unsigned long long g_graph_clock = 0;
+cudaStream_t g_capture_stream[64] = {};
+
+bool same_key(const GraphKey& a, const GraphKey& b) {
+    return a.fn == b.fn && std::memcmp(a.v, b.v, sizeof(a.v)) == 0;
+}
+}  // namespace
+
+int run_graphed(const GraphKey& key, cudaStream_t user, bool eager,
+                const std::function<int(cudaStream_t)>& body) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (eager || !g_graphs.load(std::memory_order_relaxed) ||
+        cudaStreamIsCapturing(user, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return body(user);
+    }
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return (int)e;
+    if (dev < 0 || dev >= 64) return body(user);
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    for (auto& g : g_graph_cache) {
+        if (g.dev == dev && same_key(g.key, key)) {
+            g.stamp = ++g_graph_clock;
+            if ((e = cudaGraphLaunch(g.exec, user)) != cudaSuccess) return (int)e;
+            g_launches.fetch_add(g.launches, std::memory_order_relaxed);
+            return SMX_OK;
+        }
+    }
+    cudaStream_t& cap = g_capture_stream[dev];
+    if (!cap && (e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking)) != cudaSuccess) return (int)e;
+    if ((e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return (int)e;
+    const unsigned long long before = g_launches.load();
+    const int rc = body(cap);
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(cap, &graph);
+    if (rc != SMX_OK || e != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        return rc != SMX_OK ? rc : (int)e;
+    }
+    GraphEntry ent{key, dev, nullptr, g_launches.load() - before, ++g_graph_clock};
+    e = cudaGraphInstantiate(&ent.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return (int)e;
+    if ((e = cudaGraphLaunch(ent.exec, user)) != cudaSuccess) {
+        cudaGraphExecDestroy(ent.exec);
+        return (int)e;
+    }
+    if (g_graph_cache.size() >= kMaxGraphs) {
+        size_t lru = 0;
+        for (size_t i = 1; i < g_graph_cache.size(); ++i)
+            if (g_graph_cache[i].stamp < g_graph_cache[lru].stamp) lru = i;
+        // the evicted graph may still be executing: destroy is deferred by the driver
+        cudaGraphExecDestroy(g_graph_cache[lru].exec);
+        g_graph_cache.erase(g_graph_cache.begin() + lru);
+    }
+    g_graph_cache.push_back(ent);
+    return SMX_OK;
+}
+
 }  // namespace smx
 
 extern "C" {
+
+int smx_set_graphs(int enable) {
+    return smx::g_graphs.exchange(enable ? 1 : 0);
+}
 
 int smx_version(void) { return 100; }
 

@@ -375,13 +375,15 @@ static int bits_pivot_and_row_panel(uint32_t* T, int n, long long ld_w, uint32_t
     return bool_bits_gemm(RP + kw0, RP, rowK, bb, nw, bb, ld_w, ld_w, ld_w, 1, 0, 0, s);
 }
 
+static int bool_warshall_schedule(uint32_t* T, int n, long long ld_w, uint32_t* RP, uint32_t* CP,
+                                  cudaStream_t s);
+
 // Same look-ahead schedule as fw_run_lookahead (fw.cu): pivot block r+1 is
 // closed on the side stream while the bulk of round r's update runs.
 int bool_warshall_bits(uint32_t* T, int n, long long ld_w, void* ws, size_t ws_bytes, cudaStream_t s) {
     if (n < 0 || ld_w * 32 < n) return SMX_E_ARG;
     if (n == 0) return SMX_OK;
     if (!aligned16(T) || (ld_w & 3)) return SMX_E_ALIGN;
-    const int nw = (n + 31) / 32;
     if (n <= kWarshallBlock) {
         bool_pivot_kernel<<<1, kWarshallBlock, 0, s>>>(T, n, ld_w);
         SMX_RETURN_LAUNCH();
@@ -390,6 +392,19 @@ int bool_warshall_bits(uint32_t* T, int n, long long ld_w, void* ws, size_t ws_b
     uint32_t* RP = reinterpret_cast<uint32_t*>(ws);
     uint32_t* CP = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ws) +
                                                (((size_t)kWarshallBlock * ld_w * 4 + 255) & ~size_t(255)));
+    GraphKey key;
+    key.fn = 200;
+    const unsigned long long kv[] = {(uintptr_t)T, (unsigned long long)n, (unsigned long long)ld_w,
+                                     (uintptr_t)ws, ws_bytes, (unsigned long long)lookahead_enabled()};
+    for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
+    return run_graphed(key, s, false, [&](cudaStream_t st) -> int {
+        return bool_warshall_schedule(T, n, ld_w, RP, CP, st);
+    });
+}
+
+static int bool_warshall_schedule(uint32_t* T, int n, long long ld_w, uint32_t* RP, uint32_t* CP,
+                                  cudaStream_t s) {
+    const int nw = (n + 31) / 32;
     constexpr long long ldcp = kWarshallBlock / 32;
     const int R = (n + kWarshallBlock - 1) / kWarshallBlock;
     auto blk = [&](int r) { return n - r * kWarshallBlock < kWarshallBlock ? n - r * kWarshallBlock : kWarshallBlock; };

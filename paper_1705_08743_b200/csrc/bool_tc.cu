@@ -483,15 +483,24 @@ int bool_mul_tc(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int N,
     if (ws == nullptr || ws_bytes < bool_mul_ws_bytes(M, N, K)) return SMX_E_WORKSPACE;
     uint8_t* a8 = reinterpret_cast<uint8_t*>(ws);
     uint8_t* bt8 = a8 + ((M * round16(K) + 255) & ~255LL);
-    SMX_TRY(unpack_bits(A, a8, M, K, lda_w, round16(K), s));
-    SMX_TRY(unpack_bits_transposed(B, bt8, K, N, ldb_w, round16(K), s));
-    // words past ceil(N/32) in each output row are padding: keep them zero
-    const long long nw = (N + 31) / 32;
-    if (ldc_w > nw) {
-        cudaError_t e = cudaMemset2DAsync(C + nw, ldc_w * 4, 0, (ldc_w - nw) * 4, M, s);
-        if (e != cudaSuccess) return (int)e;
-    }
-    return bool_i8_gemm(a8, bt8, nullptr, C, M, N, K, round16(K), round16(K), ldc_w, 0, 0, 0, s);
+    GraphKey key;
+    key.fn = 300;
+    const unsigned long long kv[] = {(uintptr_t)A, (uintptr_t)B, (uintptr_t)C, (unsigned long long)M,
+                                     (unsigned long long)N, (unsigned long long)K, (unsigned long long)lda_w,
+                                     (unsigned long long)ldb_w, (unsigned long long)ldc_w, (uintptr_t)ws,
+                                     ws_bytes};
+    for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
+    return run_graphed(key, s, false, [&](cudaStream_t st) -> int {
+        SMX_TRY(unpack_bits(A, a8, M, K, lda_w, round16(K), st));
+        SMX_TRY(unpack_bits_transposed(B, bt8, K, N, ldb_w, round16(K), st));
+        // words past ceil(N/32) in each output row are padding: keep them zero
+        const long long nw = (N + 31) / 32;
+        if (ldc_w > nw) {
+            cudaError_t e = cudaMemset2DAsync(C + nw, ldc_w * 4, 0, (ldc_w - nw) * 4, M, st);
+            if (e != cudaSuccess) return (int)e;
+        }
+        return bool_i8_gemm(a8, bt8, nullptr, C, M, N, K, round16(K), round16(K), ldc_w, 0, 0, 0, st);
+    });
 }
 
 }  // namespace smx

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
+
 #include "semimat_b200.h"   // include/ (on the -I path of _build.py)
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -23,6 +25,20 @@ struct SideStream {
 int side_stream(SideStream** out);
 // smx_set_fw_lookahead switch, shared by the lane FW and Boolean Warshall.
 int lookahead_enabled();
+
+// Multi-launch schedules (closures, the one-call Boolean product) are
+// recorded once into a CUDA graph per distinct call -- same entry point,
+// pointers, sizes and switches -- and replayed afterwards, so the host issues
+// one graph launch instead of 5-8 launches and event waits per round.
+// run_graphed captures body() on a private stream and launches the graph on
+// `user`; when graphs are off (smx_set_graphs), the caller's stream is itself
+// being captured, or `eager` is set, body(user) runs directly.
+struct GraphKey {
+    int fn = 0;
+    unsigned long long v[14] = {};
+};
+int run_graphed(const GraphKey& key, cudaStream_t user, bool eager,
+                const std::function<int(cudaStream_t)>& body);
 }
 
 // Placed directly after each kernel launch.

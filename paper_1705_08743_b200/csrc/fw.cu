@@ -363,6 +363,9 @@ int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, cudaStr
 }
 
 template <typename T>
+int fw_run_serial(T* Tm, int n, long long ld, int kind, T* RP, T* CP, int BLK, cudaStream_t s);
+
+template <typename T>
 int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cudaStream_t s) {
     if (n < 0 || ld < n || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
     if (n == 0) return SMX_OK;
@@ -374,7 +377,24 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
     T* CP = reinterpret_cast<T*>(reinterpret_cast<char*>(ws) +
                                  align256((size_t)FwBlock<T>::value * ld * sizeof(T)));
     const long long ldcp = BLK;
-    if (lookahead_enabled()) return fw_run_lookahead<T>(Tm, n, ld, kind, RP, CP, s);
+    GraphKey key;
+    key.fn = 100 + (int)sizeof(T);
+    const unsigned long long kv[] = {(uintptr_t)Tm, (unsigned long long)n, (unsigned long long)ld,
+                                     (unsigned long long)kind, (uintptr_t)ws, ws_bytes,
+                                     (unsigned long long)lookahead_enabled(), (unsigned long long)g_side_lite,
+                                     (unsigned long long)g_fw_block_override,
+                                     (unsigned long long)bounded_fastpath_enabled()};
+    for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
+    // the phase-3 trace records host-side state per launch: trace runs stay eager
+    return run_graphed(key, s, g_trace.armed, [&](cudaStream_t st) -> int {
+        if (lookahead_enabled()) return fw_run_lookahead<T>(Tm, n, ld, kind, RP, CP, st);
+        return fw_run_serial<T>(Tm, n, ld, kind, RP, CP, BLK, st);
+    });
+}
+
+template <typename T>
+int fw_run_serial(T* Tm, int n, long long ld, int kind, T* RP, T* CP, int BLK, cudaStream_t s) {
+    const long long ldcp = BLK;
     for (int k0 = 0; k0 < n; k0 += BLK) {
         const int bb = n - k0 < BLK ? n - k0 : BLK;
         T* rowK = Tm + (long long)k0 * ld;

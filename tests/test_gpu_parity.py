@@ -562,3 +562,79 @@ def test_matio_errors_match_reference():
         matio.from_binary(bytes(bad))
     with pytest.raises(matio.MatrixFormatError, match="expected 3 values"):
         matio.parse_text("antidist 8 1 3\n1 2\n")
+
+
+# -- graph replay (smx_set_graphs) ---------------------------------------------
+
+def test_graph_replay_tracks_buffer_contents(oracle_lib):
+    """Replayed graphs read the buffers' current contents: closing the same
+    buffer with new data each call (graph hit after the first) matches the
+    oracle, for FW u16, bit Warshall and the tensor-core product; the same
+    calls inside a user's torch.cuda.graph capture run into that capture."""
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    n = 700
+    ins = [workloads.make_inputs(workloads.CONFIGS[c], n)[0] for c in ("c5_fw_u16", "c4_fw_u16")]
+    m = lane("anti", ins[0], n, 16)
+    buf = m._data
+    before = lib.smx_launch_count()
+    for t in (ins[0], ins[1], ins[0], ins[1]):
+        buf.copy_(lane("anti", t, n, 16)._data)
+        engines.lane_close_(buf, n, 16, True)
+        got = lane("anti", t, n, 16)
+        got._data.copy_(buf)
+        np.testing.assert_array_equal(got.data, oracle_lib.semiring_close(t, 16, "anti"))
+    assert lib.smx_launch_count() - before >= 4 * 10   # replays still count their kernels
+
+    # a user capture around the call: the library launches into it eagerly
+    g = torch.cuda.CUDAGraph()
+    buf.copy_(lane("anti", ins[0], n, 16)._data)
+    with torch.cuda.graph(g):
+        engines.lane_close_(buf, n, 16, True)
+    buf.copy_(lane("anti", ins[1], n, 16)._data)
+    g.replay()
+    torch.cuda.synchronize()
+    got = lane("anti", ins[1], n, 16)
+    got._data.copy_(buf)
+    np.testing.assert_array_equal(got.data, oracle_lib.semiring_close(ins[1], 16, "anti"))
+
+    # bit Warshall on one buffer, two graphs-hit calls with different contents
+    rng = np.random.default_rng(5)
+    nb = 1100
+    mats = [rng.random((nb, nb)) < p for p in (2 / nb, 1 / nb)]
+    bm = BoolMatrix.from_numpy(mats[0])
+    words = bm._words.clone()
+    nbytes = lib.smx_bool_warshall_workspace_bytes(nb, bm.stride_words)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    for mat in (mats[0], mats[1], mats[0]):
+        words.copy_(BoolMatrix.from_numpy(mat)._words)
+        _native.check(lib.smx_bool_warshall_bits(words.data_ptr(), nb, bm.stride_words, ws.data_ptr(), nbytes,
+                                                 _native.stream_ptr()), "warshall")
+        from oracle import pack_bits
+        got = BoolMatrix(nb, nb, words.clone()).blocks
+        np.testing.assert_array_equal(got, oracle_lib.bool_close(pack_bits(mat)))
+
+    # tensor-core product: same operand buffers, new contents
+    a = BoolMatrix.from_numpy(mats[0][:, :900])
+    b = BoolMatrix.from_numpy(mats[1][:900, :])
+    first = engines.bool_mul_tc(a, b).to_numpy()
+    a._words.copy_(BoolMatrix.from_numpy(mats[1][:, :900])._words)
+    second = engines.bool_mul_tc(a, b).to_numpy()
+    ref2 = (mats[1][:, :900].astype(np.int32) @ mats[1][:900, :].astype(np.int32)) > 0
+    ref1 = (mats[0][:, :900].astype(np.int32) @ mats[1][:900, :].astype(np.int32)) > 0
+    np.testing.assert_array_equal(first, ref1)
+    np.testing.assert_array_equal(second, ref2)
+
+
+def test_graphs_off_matches_graphs_on():
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    (t,) = workloads.make_inputs(workloads.CONFIGS["c4_fw_u16"], 1500)
+    outs = []
+    for on in (1, 0):
+        old = lib.smx_set_graphs(on)
+        try:
+            outs.append(lane("dist", t, 1500, 16).transitive_closure().data)
+        finally:
+            lib.smx_set_graphs(old)
+    np.testing.assert_array_equal(outs[0], outs[1])

@@ -43,3 +43,19 @@ for eng in ("bool_closure_tc", "bool_closure_bits"):
     fn = getattr(engines, eng)
     res[f"c2_{eng}_us"] = timeit(lambda: fn(m), 10, 2) * 1e6
 print(json.dumps(res, indent=1))
+
+# CUDA-graph replay of the C2 closure: separates GPU time from host launch cost
+ws = torch.empty(max(1, lib.smx_bool_warshall_workspace_bytes(m.rows, m.stride_words)), dtype=torch.uint8, device="cuda")
+work = m._words.clone()
+st = torch.cuda.Stream()
+def c2_call():
+    _native.check(lib.smx_bool_warshall_bits(work.data_ptr(), m.rows, m.stride_words, ws.data_ptr(), ws.numel(),
+                                            torch.cuda.current_stream().cuda_stream), "warshall")
+with torch.cuda.stream(st):
+    c2_call(); torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        c2_call()
+torch.cuda.synchronize()
+res2 = {"c2_bits_eager_us": timeit(c2_call, 20, 3) * 1e6, "c2_bits_graph_us": timeit(g.replay, 20, 3) * 1e6}
+print(json.dumps(res2, indent=1))
