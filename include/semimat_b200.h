@@ -110,6 +110,12 @@ int smx_set_fw_side_lite(int enable);
  * else 128), or force 128 / 256 (u32 is always 128).  Returns the previous
  * setting (or SMX_E_ARG). */
 int smx_set_fw_block(int block);
+/* u16 phase 3 of smx_fw_u16: 1 (default) = pack the column/row panel into
+ * canonical operand tiles with per-tile bounded flags once per round and run
+ * the warp-specialised bulk-copy kernel; 0 = the register-staged kernel of
+ * smx_semiring_gemm_u16.  Results are identical.  Returns the previous
+ * setting. */
+int smx_set_fw_packed(int enable);
 
 /* Measurement hook: arm a CUDA-event trace of up to max_launches phase-3
  * launches (the dominant kernel) of the following smx_fw_* calls; read back

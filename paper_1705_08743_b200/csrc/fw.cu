@@ -20,7 +20,7 @@
 // Phases 2 and 3 are the semiring GEMM of semiring_gemm.cuh.
 #include <cuda_runtime.h>
 
-#include "semiring_gemm.cuh"
+#include "semiring_packed.cuh"
 
 namespace smx {
 
@@ -239,9 +239,26 @@ int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s) {
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 inline size_t fw_ws_bytes(int n, long long ld, int eb) {
-    // RP: pivot row panel snapshot (B x ld); CP: column panel snapshot (n x B)
+    // RP: pivot row panel snapshot (B x ld); CP: column panel snapshot (n x B);
+    // u16: the packed phase-3 operand tiles (semiring_packed.cuh)
     const size_t B = fw_block_for(eb);
-    return align256(B * ld * eb) + align256((size_t)n * B * eb);
+    const size_t base = align256(B * ld * eb) + align256((size_t)n * B * eb);
+    return eb == 2 ? base + align256(packed_u16_ws_bytes(n, n, (int)B)) : base;
+}
+
+// smx_set_fw_packed: u16 phase 3 on the warp-specialised packed-tile kernel
+static int g_fw_packed = 1;
+
+// Phase 3 (3b) product: C rows outside [skip0, skip0 + skipn) (+)= CP (x) rowK.
+template <typename T>
+int fw_phase3(const T* CP, long long ldcp, const T* rowK, T* Tm, int n, long long ld, int bb, int kind,
+              int skip0, int skipn, void* pws, size_t pws_bytes, cudaStream_t s) {
+    if constexpr (std::is_same<T, uint16_t>::value) {
+        if (g_fw_packed && pws != nullptr)
+            return semiring_gemm_packed_u16(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, skip0, skipn, pws,
+                                            pws_bytes, s);
+    }
+    return semiring_gemm<T>(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, skip0, skipn, s);
 }
 
 // Column-panel snapshot CP[i, 0:bb] = T[i, k0:k0+bb] for all n rows (16-byte
@@ -326,7 +343,8 @@ static int g_side_lite = 0;
 // the same bytes.  Rows K_{r+1} of CP(r+1) are copied while the side stream
 // may still write them, but phase 3 of round r+1 skips exactly those rows.
 template <typename T>
-int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, cudaStream_t s) {
+int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, void* pws, size_t pws_bytes,
+                     cudaStream_t s) {
     SideStream* fs = nullptr;
     SMX_TRY(side_stream(&fs));
     const int BLK = fw_block_for_n<T>(n);
@@ -349,13 +367,13 @@ int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, cudaStr
             if ((e = cudaEventRecord(fs->join, fs->side)) != cudaSuccess) return (int)e;
             // 3b: everything else (skips K_r and K_{r+1}, adjacent tiles)
             trace_begin(s, (long long)(n - bb - bb1) * n * bb);
-            SMX_TRY(semiring_gemm<T>(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, k0, bb + bb1, s));
+            SMX_TRY(fw_phase3<T>(CP, ldcp, rowK, Tm, n, ld, bb, kind, k0, bb + bb1, pws, pws_bytes, s));
             trace_end(s);
             SMX_TRY(copy_panel<T>(Tm + k1, ld, CP, ldcp, n, bb1, s));
             if ((e = cudaStreamWaitEvent(s, fs->join, 0)) != cudaSuccess) return (int)e;
         } else {
             trace_begin(s, (long long)(n - bb) * n * bb);
-            SMX_TRY(semiring_gemm<T>(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, k0, bb, s));
+            SMX_TRY(fw_phase3<T>(CP, ldcp, rowK, Tm, n, ld, bb, kind, k0, bb, pws, pws_bytes, s));
             trace_end(s);
         }
     }
@@ -363,7 +381,8 @@ int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, cudaStr
 }
 
 template <typename T>
-int fw_run_serial(T* Tm, int n, long long ld, int kind, T* RP, T* CP, int BLK, cudaStream_t s);
+int fw_run_serial(T* Tm, int n, long long ld, int kind, T* RP, T* CP, void* pws, size_t pws_bytes, int BLK,
+                  cudaStream_t s);
 
 template <typename T>
 int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cudaStream_t s) {
@@ -376,24 +395,28 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
     T* RP = reinterpret_cast<T*>(ws);
     T* CP = reinterpret_cast<T*>(reinterpret_cast<char*>(ws) +
                                  align256((size_t)FwBlock<T>::value * ld * sizeof(T)));
-    const long long ldcp = BLK;
+    const size_t pws_off = align256((size_t)FwBlock<T>::value * ld * sizeof(T)) +
+                           align256((size_t)n * FwBlock<T>::value * sizeof(T));
+    void* pws = sizeof(T) == 2 ? reinterpret_cast<char*>(ws) + pws_off : nullptr;
+    const size_t pws_bytes = sizeof(T) == 2 ? ws_bytes - pws_off : 0;
     GraphKey key;
     key.fn = 100 + (int)sizeof(T);
     const unsigned long long kv[] = {(uintptr_t)Tm, (unsigned long long)n, (unsigned long long)ld,
                                      (unsigned long long)kind, (uintptr_t)ws, ws_bytes,
                                      (unsigned long long)lookahead_enabled(), (unsigned long long)g_side_lite,
-                                     (unsigned long long)g_fw_block_override,
+                                     (unsigned long long)g_fw_block_override, (unsigned long long)g_fw_packed,
                                      (unsigned long long)bounded_fastpath_enabled()};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     // the phase-3 trace records host-side state per launch: trace runs stay eager
     return run_graphed(key, s, g_trace.armed, [&](cudaStream_t st) -> int {
-        if (lookahead_enabled()) return fw_run_lookahead<T>(Tm, n, ld, kind, RP, CP, st);
-        return fw_run_serial<T>(Tm, n, ld, kind, RP, CP, BLK, st);
+        if (lookahead_enabled()) return fw_run_lookahead<T>(Tm, n, ld, kind, RP, CP, pws, pws_bytes, st);
+        return fw_run_serial<T>(Tm, n, ld, kind, RP, CP, pws, pws_bytes, BLK, st);
     });
 }
 
 template <typename T>
-int fw_run_serial(T* Tm, int n, long long ld, int kind, T* RP, T* CP, int BLK, cudaStream_t s) {
+int fw_run_serial(T* Tm, int n, long long ld, int kind, T* RP, T* CP, void* pws, size_t pws_bytes, int BLK,
+                  cudaStream_t s) {
     const long long ldcp = BLK;
     for (int k0 = 0; k0 < n; k0 += BLK) {
         const int bb = n - k0 < BLK ? n - k0 : BLK;
@@ -407,7 +430,7 @@ int fw_run_serial(T* Tm, int n, long long ld, int kind, T* RP, T* CP, int BLK, c
                               cudaMemcpyDeviceToDevice, s);
         if (e != cudaSuccess) return (int)e;
         trace_begin(s, (long long)(n - bb) * n * bb);
-        SMX_TRY(semiring_gemm<T>(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, k0, bb, s));
+        SMX_TRY(fw_phase3<T>(CP, ldcp, rowK, Tm, n, ld, bb, kind, k0, bb, pws, pws_bytes, s));
         trace_end(s);
     }
     return SMX_OK;
@@ -448,6 +471,12 @@ int smx_semiring_gemm_skip(const void* A, const void* B, void* C, int M, int N, 
                                                N, K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows, s);
         default: return SMX_E_ARG;
     }
+}
+
+int smx_set_fw_packed(int enable) {
+    const int old = g_fw_packed;
+    g_fw_packed = enable ? 1 : 0;
+    return old;
 }
 
 int smx_set_fw_block(int block) {

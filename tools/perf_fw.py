@@ -31,11 +31,14 @@ for n in sizes:
     src = torch.from_numpy(T).cuda(); w = src.clone()
     def f():
         w.copy_(src); engines.lane_close_(w, n, 16, True)
-    for fast, la, lite, blk in ((1, 1, 1, 0), (1, 1, 1, 128), (1, 1, 1, 256), (1, 1, 0, 256), (1, 0, 1, 0)):
+    variants = [(1, 1, 0, 0, 1), (1, 1, 0, 0, 0), (1, 0, 0, 0, 1)]
+    if os.environ.get("PERF_FW_ALL"):
+        variants += [(1, 1, 1, 0, 1), (1, 1, 0, 128, 1), (1, 1, 0, 256, 1)]
+    for fast, la, lite, blk, packed in variants:
         lib.smx_set_bounded_fastpath(fast); lib.smx_set_fw_lookahead(la); lib.smx_set_fw_side_lite(lite)
-        lib.smx_set_fw_block(blk)
+        lib.smx_set_fw_block(blk); lib.smx_set_fw_packed(packed)
         t = timeit(f, 3 if n <= 8192 else 1, 1)
-        res[f"fw{n}_fast{fast}_la{la}_lite{lite}_b{blk}"] = n**3 / t
-    lib.smx_set_bounded_fastpath(1); lib.smx_set_fw_lookahead(1); lib.smx_set_fw_side_lite(1)
-    lib.smx_set_fw_block(0)
+        res[f"fw{n}_fast{fast}_la{la}_lite{lite}_b{blk}_packed{packed}"] = n**3 / t
+    lib.smx_set_bounded_fastpath(1); lib.smx_set_fw_lookahead(1); lib.smx_set_fw_side_lite(0)
+    lib.smx_set_fw_block(0); lib.smx_set_fw_packed(1)
 print(json.dumps({k: (f"{v:.4e}" if isinstance(v, float) else v) for k, v in res.items()}))
