@@ -31,10 +31,10 @@ struct PackedU16 {
     static constexpr int TCOLS = BNW / TNW;            // 8
     static constexpr int CONSUMERS = (BM / TM) * TCOLS;  // 256
     static constexpr int THREADS = CONSUMERS + 32;     // + producer warp
-    static constexpr int STAGES = 4;
+    static constexpr int STAGES = 6;
     static constexpr int A_TILE_WORDS = BK * BM;       // 2048 words = 8 KB
     static constexpr int B_TILE_WORDS = BK * BNW;      // 1024 words = 4 KB
-    static constexpr size_t SMEM = (size_t)STAGES * (A_TILE_WORDS + B_TILE_WORDS) * 4 + 1024;
+    static constexpr size_t SMEM = (size_t)STAGES * (A_TILE_WORDS + B_TILE_WORDS) * 4 + BM * BN * 2 + 1024;
 };
 
 struct PackedArgs {
@@ -150,6 +150,11 @@ __device__ __forceinline__ void pk_bulk_load(void* dst, const void* src, uint32_
 }
 
 // ---- the GEMM ------------------------------------------------------------------
+// Accumulation order: the consumers start from the (+)-identity, run the K
+// loop, and fold C in at the end (min is associative and commutative, so the
+// result is bit-identical).  The producer prefetches an interior C tile into
+// shared memory with row bulk copies while the K loop runs, so neither the C
+// read latency nor the operand-flag reads sit on a warp's critical path.
 __global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(const PackedArgs p) {
     using L = Lane<uint16_t>;
     using G = PackedU16;
@@ -159,66 +164,75 @@ __global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(
     extern __shared__ __align__(128) uint4 smem_raw[];
     uint32_t* As = reinterpret_cast<uint32_t*>(smem_raw);              // [ST][BK][BM]
     uint32_t* Bs = As + ST * G::A_TILE_WORDS;                          // [ST][BK][BNW]
-    uint64_t* full = reinterpret_cast<uint64_t*>(Bs + ST * G::B_TILE_WORDS);
+    uint16_t* Cs = reinterpret_cast<uint16_t*>(Bs + ST * G::B_TILE_WORDS);   // [BM][BN] (raw C)
+    uint64_t* full = reinterpret_cast<uint64_t*>(Cs + BM * G::BN);
     uint64_t* empty = full + ST;
-    uint32_t* flag = reinterpret_cast<uint32_t*>(empty + ST);
+    uint64_t* cbar = empty + ST;
+    uint32_t* flag = reinterpret_cast<uint32_t*>(cbar + 1);
 
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     int mt = blockIdx.y;
     if (mt >= p.skip_tile0) mt += p.skip_tiles;
     const int nt = blockIdx.x;
     const int KT = p.KT;
+    const int row0 = mt * BM, col0 = nt * G::BN;
+    const bool c_async = p.accumulate && KT > 0 && row0 + BM <= p.M && col0 + G::BN <= p.N;
 
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
             pk_mbar_init(&full[s], 1);
             pk_mbar_init(&empty[s], G::CONSUMERS / 32);
         }
+        pk_mbar_init(cbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
     if (tid >= G::CONSUMERS) {
-        // producer warp: one lane streams the tiles
-        if (tid == G::CONSUMERS) {
-            const uint32_t* a_src = p.Ap + (size_t)mt * KT * G::A_TILE_WORDS;
-            for (int kt = 0; kt < KT; ++kt) {
-                const int s = kt % ST;
-                if (kt >= ST) pk_mbar_wait(&empty[s], ((kt / ST) - 1) & 1);
-                flag[s] = p.allow_bounded && p.fA[(size_t)mt * KT + kt] && p.fB[(size_t)kt * p.NT + nt];
-                pk_mbar_expect_tx(&full[s], (G::A_TILE_WORDS + G::B_TILE_WORDS) * 4);
-                pk_bulk_load(As + s * G::A_TILE_WORDS, a_src + (size_t)kt * G::A_TILE_WORDS,
-                             G::A_TILE_WORDS * 4, &full[s]);
-                pk_bulk_load(Bs + s * G::B_TILE_WORDS,
-                             p.Bp + ((size_t)kt * p.NT + nt) * G::B_TILE_WORDS, G::B_TILE_WORDS * 4,
-                             &full[s]);
+        // ---- producer warp ----
+        const uint32_t* a_src = p.Ap + (size_t)mt * KT * G::A_TILE_WORDS;
+        for (int kb = 0; kb < KT; kb += 32) {
+            // bounded flags of 32 k-tiles in one round trip (one per lane)
+            const int k = kb + lane;
+            const bool f = k < KT && p.allow_bounded && p.fA[(size_t)mt * KT + k] != 0 &&
+                           p.fB[(size_t)k * p.NT + nt] != 0;
+            const uint32_t fmask = __ballot_sync(0xFFFFFFFFu, f);
+            if (lane == 0) {
+                const int kend = KT - kb < 32 ? KT : kb + 32;
+                for (int kt = kb; kt < kend; ++kt) {
+                    const int s = kt % ST;
+                    if (kt >= ST) pk_mbar_wait(&empty[s], ((kt / ST) - 1) & 1);
+                    flag[s] = (fmask >> (kt - kb)) & 1u;
+                    pk_mbar_expect_tx(&full[s], (G::A_TILE_WORDS + G::B_TILE_WORDS) * 4);
+                    pk_bulk_load(As + s * G::A_TILE_WORDS, a_src + (size_t)kt * G::A_TILE_WORDS,
+                                 G::A_TILE_WORDS * 4, &full[s]);
+                    pk_bulk_load(Bs + s * G::B_TILE_WORDS,
+                                 p.Bp + ((size_t)kt * p.NT + nt) * G::B_TILE_WORDS, G::B_TILE_WORDS * 4,
+                                 &full[s]);
+                    // the C tile goes behind the first ring fill, so the
+                    // first operand tiles arrive first
+                    if (c_async && kt == (KT < ST ? KT : ST) - 1) {
+                        pk_mbar_expect_tx(cbar, BM * G::BN * 2);
+                        for (int r = 0; r < BM; ++r)
+                            pk_bulk_load(Cs + r * G::BN, p.C + (long long)(row0 + r) * p.ldc + col0, G::BN * 2,
+                                         cbar);
+                    }
+                }
             }
+            __syncwarp();
         }
         return;
     }
 
     const int tc = tid % G::TCOLS, tr = tid / G::TCOLS;
-    const int row0 = mt * BM, col0 = nt * G::BN;
     const bool anti = p.anti != 0;
 
     uint32_t acc[TM][TNW];
 #pragma unroll
-    for (int i = 0; i < TM; ++i) {
-        const int grow = row0 + tr * TM + i;
+    for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
-            uint32_t* w = &acc[i][g * HW];
-            if (p.accumulate && grow < p.M) {
-                const int gc = col0 + (g * (BNW / 2) + tc * HW) * 2;
-                load_c_group<uint16_t, HW>(p.C + (long long)grow * p.ldc, gc, p.N, anti, w);
-            } else {
-#pragma unroll
-                for (int j = 0; j < HW; ++j) w[j] = L::kIdentityWord;
-            }
-        }
-    }
+        for (int j = 0; j < TNW; ++j) acc[i][j] = L::kIdentityWord;
 
-    const int lane = tid & 31;
     for (int kt = 0; kt < KT; ++kt) {
         const int s = kt % ST;
         pk_mbar_wait(&full[s], (kt / ST) & 1);
@@ -258,6 +272,9 @@ __global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(
         if (lane == 0) pk_mbar_arrive(&empty[s]);
     }
 
+    // ---- fold C in and store ----
+    const uint32_t cm = anti ? 0xFFFFFFFFu : 0u;
+    if (c_async) pk_mbar_wait(cbar, 0);
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
         const int grow = row0 + tr * TM + i;
@@ -265,8 +282,19 @@ __global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(
         uint16_t* crow = p.C + (long long)grow * p.ldc;
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
-            const int gc = col0 + (g * (BNW / 2) + tc * HW) * 2;
-            store_c_group<uint16_t, HW>(crow, gc, p.N, anti, &acc[i][g * HW]);
+            const int cc = (g * (BNW / 2) + tc * HW) * 2;   // cell offset in the tile
+            uint32_t* w = &acc[i][g * HW];
+            if (c_async) {
+                const uint4 v = *reinterpret_cast<const uint4*>(Cs + (tr * TM + i) * G::BN + cc);
+                w[0] = __vminu2(w[0], v.x ^ cm); w[1] = __vminu2(w[1], v.y ^ cm);
+                w[2] = __vminu2(w[2], v.z ^ cm); w[3] = __vminu2(w[3], v.w ^ cm);
+            } else if (p.accumulate) {
+                uint32_t c[HW];
+                load_c_group<uint16_t, HW>(crow, col0 + cc, p.N, anti, c);
+#pragma unroll
+                for (int j = 0; j < HW; ++j) w[j] = __vminu2(w[j], c[j]);
+            }
+            store_c_group<uint16_t, HW>(crow, col0 + cc, p.N, anti, w);
         }
     }
 }
