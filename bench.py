@@ -396,7 +396,8 @@ def run_ours(args, world, rank, local_rank):
             "bound": "int_issue", "achieved": achieved / 1e12, "peak": peak_cells / 1e12,
             "unit": "Tcell/s", "frac": achieved / peak_cells, "traffic": traffic,
             "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
-            "kernel": "semiring_gemm_kernel (FW phase 3)" if cfg.op == "closure" else "semiring_gemm_kernel",
+            "kernel": ("packed_gemm_u16_kernel (FW phase 3; timed with its 2 operand-pack launches)"
+                       if cfg.op == "closure" else "semiring_gemm_kernel"),
             "launches_timed": dom_launches,
             "avg_launch_ms": dom_secs_total / dom_launches * 1e3,
             "share_of_step": dom_secs_total / dom_launches *

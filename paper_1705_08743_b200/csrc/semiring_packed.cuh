@@ -191,6 +191,18 @@ __global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(
     if (tid >= G::CONSUMERS) {
         // ---- producer warp ----
         const uint32_t* a_src = p.Ap + (size_t)mt * KT * G::A_TILE_WORDS;
+        const int first = KT < ST ? KT : ST;
+        auto issue = [&](int kt, int s) {
+            pk_bulk_load(As + s * G::A_TILE_WORDS, a_src + (size_t)kt * G::A_TILE_WORDS, G::A_TILE_WORDS * 4,
+                         &full[s]);
+            pk_bulk_load(Bs + s * G::B_TILE_WORDS, p.Bp + ((size_t)kt * p.NT + nt) * G::B_TILE_WORDS,
+                         G::B_TILE_WORDS * 4, &full[s]);
+        };
+        // The first ring fill goes out before the flag reads: a stage's
+        // complete_tx may land before its expect_tx (the tx-count goes
+        // transiently negative; the phase cannot complete until the arrive).
+        if (lane == 0)
+            for (int kt = 0; kt < first; ++kt) issue(kt, kt);
         for (int kb = 0; kb < KT; kb += 32) {
             // bounded flags of 32 k-tiles in one round trip (one per lane)
             const int k = kb + lane;
@@ -204,14 +216,10 @@ __global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(
                     if (kt >= ST) pk_mbar_wait(&empty[s], ((kt / ST) - 1) & 1);
                     flag[s] = (fmask >> (kt - kb)) & 1u;
                     pk_mbar_expect_tx(&full[s], (G::A_TILE_WORDS + G::B_TILE_WORDS) * 4);
-                    pk_bulk_load(As + s * G::A_TILE_WORDS, a_src + (size_t)kt * G::A_TILE_WORDS,
-                                 G::A_TILE_WORDS * 4, &full[s]);
-                    pk_bulk_load(Bs + s * G::B_TILE_WORDS,
-                                 p.Bp + ((size_t)kt * p.NT + nt) * G::B_TILE_WORDS, G::B_TILE_WORDS * 4,
-                                 &full[s]);
+                    if (kt >= first) issue(kt, s);
                     // the C tile goes behind the first ring fill, so the
                     // first operand tiles arrive first
-                    if (c_async && kt == (KT < ST ? KT : ST) - 1) {
+                    if (c_async && kt == first - 1) {
                         pk_mbar_expect_tx(cbar, BM * G::BN * 2);
                         for (int r = 0; r < BM; ++r)
                             pk_bulk_load(Cs + r * G::BN, p.C + (long long)(row0 + r) * p.ldc + col0, G::BN * 2,
