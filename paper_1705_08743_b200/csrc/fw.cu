@@ -465,8 +465,23 @@ int smx_semiring_gemm_skip(const void* A, const void* B, void* C, int M, int N, 
     switch (elem_bytes) {
         case 1: return semiring_gemm<uint8_t>((const uint8_t*)A, (const uint8_t*)B, (uint8_t*)C, M, N,
                                               K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows, s);
-        case 2: return semiring_gemm<uint16_t>((const uint16_t*)A, (const uint16_t*)B, (uint16_t*)C, M,
-                                               N, K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows, s);
+        case 2:
+            // bulk row-panel updates of the sharded closure: the packed phase-3
+            // kernel, its operand tiles in stream-ordered scratch
+            if (g_fw_packed && (long long)M * N >= (1LL << 24) && K > 0 && aligned16(A) && aligned16(B) &&
+                aligned16(C)) {
+                const size_t bytes = packed_u16_ws_bytes(M, N, K);
+                void* ws = nullptr;
+                if (scratch_alloc(&ws, bytes, s) == SMX_OK) {
+                    const int rc = semiring_gemm_packed_u16((const uint16_t*)A, (const uint16_t*)B, (uint16_t*)C,
+                                                            M, N, K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows,
+                                                            ws, bytes, s);
+                    scratch_free(ws, s);
+                    return rc;
+                }
+            }
+            return semiring_gemm<uint16_t>((const uint16_t*)A, (const uint16_t*)B, (uint16_t*)C, M,
+                                           N, K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows, s);
         case 4: return semiring_gemm<uint32_t>((const uint32_t*)A, (const uint32_t*)B, (uint32_t*)C, M,
                                                N, K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows, s);
         default: return SMX_E_ARG;

@@ -638,3 +638,44 @@ def test_graphs_off_matches_graphs_on():
         finally:
             lib.smx_set_graphs(old)
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("kind", ["anti", "dist"])
+def test_packed_skip_gemm_matches_register_kernel_and_oracle(kind, oracle_lib):
+    """smx_semiring_gemm_skip u16 at a size that takes the packed phase-3
+    kernel (ragged M/N, a skipped row range): equal to the register-staged
+    kernel (smx_set_fw_packed(0)) everywhere and to the oracle on 300 rows."""
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    rng = np.random.default_rng(11)
+    M, N, K = 4200, 4100, 256
+    S = 0xFFFF
+    def mat(r, c, dens):
+        v = rng.integers(0, 30000, (r, c), dtype=np.uint32)
+        v[rng.random((r, c)) > dens] = S if kind == "dist" else 0
+        if kind == "anti":
+            v[rng.random((r, c)) < dens / 4] = S - rng.integers(0, 1000)  # near-zero distances
+        return v.astype(np.uint16)
+    a, b, c = mat(M, K, 0.5), mat(K, N, 0.5), mat(M, N, 0.3)
+    ldc = 4104
+    cpad = np.zeros((M, ldc), dtype=np.uint16); cpad[:, :N] = c
+    bpad = np.zeros((K, ldc), dtype=np.uint16); bpad[:, :N] = b
+    kid = 0 if kind == "anti" else 1
+    outs = []
+    for packed in (1, 0):
+        old = lib.smx_set_fw_packed(packed)
+        try:
+            ta = torch.from_numpy(a.view(np.int16)).cuda()
+            tb = torch.from_numpy(bpad.view(np.int16)).cuda()
+            tc = torch.from_numpy(cpad.view(np.int16)).cuda()
+            _native.check(lib.smx_semiring_gemm_skip(ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), M, N, K, K,
+                                                     ldc, ldc, 2, kid, 1024, 256, _native.stream_ptr()), "skip")
+            torch.cuda.synchronize()
+            outs.append(tc.cpu().numpy().view(np.uint16)[:, :N].copy())
+        finally:
+            lib.smx_set_fw_packed(old)
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[0][1024:1280], c[1024:1280])   # skipped rows untouched
+    prod = oracle_lib.semiring_mul(a[:300], b, K, 16, kind)
+    want = np.maximum(c[:300], prod) if kind == "anti" else np.minimum(c[:300], prod)
+    np.testing.assert_array_equal(outs[0][:300], want)
