@@ -380,6 +380,52 @@ int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, void* p
     return SMX_OK;
 }
 
+// u16 look-ahead on packed operand tiles.  Round r on the main stream:
+//   pack B(r) from T[K_r,:]  ->  3a: packed rows K_{r+1}  -> fork ->
+//   3b: packed rows outside K_r, K_{r+1}  ->  pack A(r+1) from T[:, K_{r+1}]
+//   -> wait(join)
+// The packed A tiles are the column-panel snapshot (no separate CP copy).
+// pack A(r+1) reads rows K_{r+1} while the side stream may still rewrite
+// them, but only tiles of rows K_{r+2} (3a) and of rows outside K_{r+1} u
+// K_{r+2} (3b) are read in round r+1, as with the CP copy of fw_run_lookahead.
+inline int fw_run_lookahead_packed(uint16_t* Tm, int n, long long ld, int kind, uint16_t* RP, void* pws,
+                                   size_t pws_bytes, cudaStream_t s) {
+    SideStream* fs = nullptr;
+    SMX_TRY(side_stream(&fs));
+    const int BLK = fw_block_for_n<uint16_t>(n);
+    const int R = (n + BLK - 1) / BLK;
+    auto blk = [&](int r) { return n - r * BLK < BLK ? n - r * BLK : BLK; };
+    SMX_TRY(fw_pivot_and_row_panel<uint16_t>(Tm, n, ld, kind, RP, 0, blk(0), s));
+    SMX_TRY(packed_u16_pack(Tm, nullptr, n, n, blk(0), ld, ld, kind, pws, pws_bytes, s));
+    cudaError_t e;
+    for (int r = 0; r < R; ++r) {
+        const int k0 = r * BLK, bb = blk(r);
+        uint16_t* rowK = Tm + (long long)k0 * ld;
+        SMX_TRY(packed_u16_pack(nullptr, rowK, n, n, bb, ld, ld, kind, pws, pws_bytes, s));
+        if (r + 1 < R) {
+            const int k1 = k0 + BLK, bb1 = blk(r + 1);
+            // 3a: the next pivot block's rows first
+            SMX_TRY(packed_u16_run(Tm, n, n, bb, ld, kind, 1, k1 / PackedU16::BM, ceil_div(bb1, PackedU16::BM), 0,
+                                   0, pws, pws_bytes, s));
+            if ((e = cudaEventRecord(fs->fork, s)) != cudaSuccess) return (int)e;
+            if ((e = cudaStreamWaitEvent(fs->side, fs->fork, 0)) != cudaSuccess) return (int)e;
+            SMX_TRY(fw_pivot_and_row_panel<uint16_t>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
+            if ((e = cudaEventRecord(fs->join, fs->side)) != cudaSuccess) return (int)e;
+            // 3b: everything else (skips K_r and K_{r+1}, adjacent tiles)
+            trace_begin(s, (long long)(n - bb - bb1) * n * bb);
+            SMX_TRY(packed_u16_run(Tm, n, n, bb, ld, kind, 1, 0, -1, k0, bb + bb1, pws, pws_bytes, s));
+            trace_end(s);
+            SMX_TRY(packed_u16_pack(Tm + k1, nullptr, n, n, bb1, ld, ld, kind, pws, pws_bytes, s));
+            if ((e = cudaStreamWaitEvent(s, fs->join, 0)) != cudaSuccess) return (int)e;
+        } else {
+            trace_begin(s, (long long)(n - bb) * n * bb);
+            SMX_TRY(packed_u16_run(Tm, n, n, bb, ld, kind, 1, 0, -1, k0, bb, pws, pws_bytes, s));
+            trace_end(s);
+        }
+    }
+    return SMX_OK;
+}
+
 template <typename T>
 int fw_run_serial(T* Tm, int n, long long ld, int kind, T* RP, T* CP, void* pws, size_t pws_bytes, int BLK,
                   cudaStream_t s);
@@ -409,6 +455,10 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     // the phase-3 trace records host-side state per launch: trace runs stay eager
     return run_graphed(key, s, g_trace.armed, [&](cudaStream_t st) -> int {
+        if constexpr (std::is_same<T, uint16_t>::value) {
+            if (lookahead_enabled() && g_fw_packed && pws != nullptr)
+                return fw_run_lookahead_packed(Tm, n, ld, kind, RP, pws, pws_bytes, st);
+        }
         if (lookahead_enabled()) return fw_run_lookahead<T>(Tm, n, ld, kind, RP, CP, pws, pws_bytes, st);
         return fw_run_serial<T>(Tm, n, ld, kind, RP, CP, pws, pws_bytes, BLK, st);
     });

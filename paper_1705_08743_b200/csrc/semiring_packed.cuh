@@ -46,7 +46,8 @@ struct PackedArgs {
     int M, N, KT, NT;
     long long ldc;
     int anti, accumulate, allow_bounded;
-    int skip_tile0, skip_tiles;
+    int row_tile0;                // first 128-row tile of the launch window
+    int skip_tile0, skip_tiles;   // tiles skipped inside the window
 };
 
 // ---- pack kernels -----------------------------------------------------------
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(
     uint32_t* flag = reinterpret_cast<uint32_t*>(cbar + 1);
 
     const int tid = threadIdx.x, lane = tid & 31;
-    int mt = blockIdx.y;
+    int mt = p.row_tile0 + blockIdx.y;
     if (mt >= p.skip_tile0) mt += p.skip_tiles;
     const int nt = blockIdx.x;
     const int KT = p.KT;
@@ -315,48 +316,85 @@ inline size_t packed_u16_ws_bytes(int M, int N, int K) {
            al(KT * NT);
 }
 
-// C (+)= A (x) B, u16, accumulate, rows [skip_row0, skip_row0 + skip_rows)
-// left untouched (whole 128-row tiles).  ws: packed_u16_ws_bytes(M, N, K).
-inline int semiring_gemm_packed_u16(const uint16_t* A, const uint16_t* B, uint16_t* C, int M, int N, int K,
-                                    long long lda, long long ldb, long long ldc, int kind, int accumulate,
-                                    int skip_row0, int skip_rows, void* ws, size_t ws_bytes, cudaStream_t s) {
+// Views of a packed workspace laid out by packed_u16_ws_bytes(M, N, K).
+struct PackedWs {
+    uint32_t* Ap;
+    uint32_t* Bp;
+    uint8_t* fA;
+    uint8_t* fB;
+    int MT, NT, KT;
+};
+inline PackedWs packed_views(void* ws, int M, int N, int K) {
+    using G = PackedU16;
+    PackedWs v;
+    v.MT = ceil_div(M, G::BM);
+    v.NT = ceil_div(N, G::BN);
+    v.KT = ceil_div(K, G::BK);
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    char* w = reinterpret_cast<char*>(ws);
+    v.Ap = reinterpret_cast<uint32_t*>(w);
+    w += al((size_t)v.MT * v.KT * G::A_TILE_WORDS * 4);
+    v.Bp = reinterpret_cast<uint32_t*>(w);
+    w += al((size_t)v.KT * v.NT * G::B_TILE_WORDS * 4);
+    v.fA = reinterpret_cast<uint8_t*>(w);
+    w += al((size_t)v.MT * v.KT);
+    v.fB = reinterpret_cast<uint8_t*>(w);
+    return v;
+}
+
+inline int packed_check(const void* A, const void* B, int M, int N, int K, long long lda, long long ldb, int kind,
+                        void* ws, size_t ws_bytes) {
+    if (M < 0 || N < 0 || K < 0 || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
+    if ((A && !aligned16(A)) || (B && !aligned16(B))) return SMX_E_ALIGN;
+    if (!ld_ok(lda, 2) || !ld_ok(ldb, 2)) return SMX_E_ALIGN;
+    if (lda < K || ldb < N) return SMX_E_ARG;
+    if (ws == nullptr || ws_bytes < packed_u16_ws_bytes(M, N, K)) return SMX_E_WORKSPACE;
+    return SMX_OK;
+}
+
+// Pack A (M x K; A == nullptr skips it) and/or B (K x N; B == nullptr skips).
+inline int packed_u16_pack(const uint16_t* A, const uint16_t* B, int M, int N, int K, long long lda, long long ldb,
+                           int kind, void* ws, size_t ws_bytes, cudaStream_t s) {
+    SMX_TRY(packed_check(A, B, M, N, K, lda, ldb, kind, ws, ws_bytes));
+    if (M == 0 || N == 0 || K == 0) return SMX_OK;
+    const PackedWs v = packed_views(ws, M, N, K);
+    const int anti = kind == SMX_ANTI;
+    if (A) {
+        pack_a_u16_kernel<<<dim3(v.KT, v.MT), 128, 0, s>>>(A, M, K, lda, anti, v.KT, v.Ap, v.fA);
+        SMX_LAUNCHED_OR_RETURN();
+    }
+    if (B) {
+        pack_b_u16_kernel<<<dim3(v.NT, v.KT), 256, 0, s>>>(B, K, N, ldb, anti, v.NT, v.Bp, v.fB);
+        SMX_LAUNCHED_OR_RETURN();
+    }
+    return SMX_OK;
+}
+
+// C rows (+)= packed A (x) packed B over the 128-row tiles
+// [row_tile0, row_tile0 + row_tiles) minus the rows [skip_row0, skip_row0 +
+// skip_rows) (whole tiles, inside the window).  row_tiles < 0: to the end.
+inline int packed_u16_run(uint16_t* C, int M, int N, int K, long long ldc, int kind, int accumulate, int row_tile0,
+                          int row_tiles, int skip_row0, int skip_rows, void* ws, size_t ws_bytes, cudaStream_t s) {
     using G = PackedU16;
     if (M < 0 || N < 0 || K < 0 || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
     if (M == 0 || N == 0) return SMX_OK;
-    if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return SMX_E_ALIGN;
-    if (!ld_ok(lda, 2) || !ld_ok(ldb, 2) || !ld_ok(ldc, 2)) return SMX_E_ALIGN;
-    if (lda < K || ldb < N || ldc < N) return SMX_E_ARG;
+    if (!aligned16(C) || !ld_ok(ldc, 2)) return SMX_E_ALIGN;
+    if (ldc < N) return SMX_E_ARG;
     if (ws == nullptr || ws_bytes < packed_u16_ws_bytes(M, N, K)) return SMX_E_WORKSPACE;
-    const int MT = ceil_div(M, G::BM), NT = ceil_div(N, G::BN), KT = ceil_div(K, G::BK);
-    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-    char* w = reinterpret_cast<char*>(ws);
-    uint32_t* Ap = reinterpret_cast<uint32_t*>(w);
-    w += al((size_t)MT * KT * G::A_TILE_WORDS * 4);
-    uint32_t* Bp = reinterpret_cast<uint32_t*>(w);
-    w += al((size_t)KT * NT * G::B_TILE_WORDS * 4);
-    uint8_t* fA = reinterpret_cast<uint8_t*>(w);
-    w += al((size_t)MT * KT);
-    uint8_t* fB = reinterpret_cast<uint8_t*>(w);
-    const int anti = kind == SMX_ANTI;
-
-    PackedArgs a{Ap, Bp, fA, fB, C, M, N, KT, NT, ldc, anti, accumulate != 0, bounded_fastpath_enabled(), 0, 0};
+    const PackedWs v = packed_views(ws, M, N, K);
+    if (row_tile0 < 0 || row_tile0 > v.MT) return SMX_E_ARG;
+    if (row_tiles < 0 || row_tile0 + row_tiles > v.MT) row_tiles = v.MT - row_tile0;
+    PackedArgs a{v.Ap, v.Bp, v.fA, v.fB, C, M, N, v.KT, v.NT, ldc, kind == SMX_ANTI, accumulate != 0,
+                 bounded_fastpath_enabled(), row_tile0, v.MT, 0};
     if (skip_rows > 0) {
         if (skip_row0 % G::BM) return SMX_E_ARG;
         a.skip_tile0 = skip_row0 / G::BM;
         a.skip_tiles = ceil_div(skip_rows, G::BM);
-        if (a.skip_tile0 + a.skip_tiles > MT) a.skip_tiles = MT - a.skip_tile0;
-        if (a.skip_tiles < 0) return SMX_E_ARG;
-    } else {
-        a.skip_tile0 = MT;
+        if (a.skip_tile0 < row_tile0 || a.skip_tile0 > row_tile0 + row_tiles) return SMX_E_ARG;
+        if (a.skip_tile0 + a.skip_tiles > row_tile0 + row_tiles) a.skip_tiles = row_tile0 + row_tiles - a.skip_tile0;
     }
-    const int mtiles = MT - a.skip_tiles;
+    const int mtiles = row_tiles - a.skip_tiles;
     if (mtiles <= 0) return SMX_OK;
-    if (KT > 0) {
-        pack_a_u16_kernel<<<dim3(KT, MT), 128, 0, s>>>(A, M, K, lda, anti, KT, Ap, fA);
-        SMX_LAUNCHED_OR_RETURN();
-        pack_b_u16_kernel<<<dim3(NT, KT), 256, 0, s>>>(B, K, N, ldb, anti, NT, Bp, fB);
-        SMX_LAUNCHED_OR_RETURN();
-    }
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(packed_gemm_u16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -364,8 +402,19 @@ inline int semiring_gemm_packed_u16(const uint16_t* A, const uint16_t* B, uint16
         if (e != cudaSuccess) return (int)e;
         configured = true;
     }
-    packed_gemm_u16_kernel<<<dim3(NT, mtiles), G::THREADS, G::SMEM, s>>>(a);
+    packed_gemm_u16_kernel<<<dim3(v.NT, mtiles), G::THREADS, G::SMEM, s>>>(a);
     SMX_RETURN_LAUNCH();
+}
+
+// C (+)= A (x) B, u16, rows [skip_row0, skip_row0 + skip_rows) left untouched
+// (whole 128-row tiles).  ws: packed_u16_ws_bytes(M, N, K).
+inline int semiring_gemm_packed_u16(const uint16_t* A, const uint16_t* B, uint16_t* C, int M, int N, int K,
+                                    long long lda, long long ldb, long long ldc, int kind, int accumulate,
+                                    int skip_row0, int skip_rows, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (A == nullptr || B == nullptr) return SMX_E_ARG;
+    if (M == 0 || N == 0) return SMX_OK;
+    SMX_TRY(packed_u16_pack(A, B, M, N, K, lda, ldb, kind, ws, ws_bytes, s));
+    return packed_u16_run(C, M, N, K, ldc, kind, accumulate, 0, -1, skip_row0, skip_rows, ws, ws_bytes, s);
 }
 
 }  // namespace smx
