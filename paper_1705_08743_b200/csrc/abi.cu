@@ -43,6 +43,11 @@ int scratch_free(void* p, cudaStream_t s) {
     return e == cudaSuccess ? SMX_OK : (int)e;
 }
 
+int& launch_priority() {
+    thread_local int prio = 0;
+    return prio;
+}
+
 int side_stream(SideStream** out) {
     static SideStream per_dev[64];
     int dev = 0;
@@ -54,6 +59,7 @@ int side_stream(SideStream** out) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         if ((e = cudaStreamCreateWithPriority(&f.side, cudaStreamNonBlocking, hi)) != cudaSuccess) return (int)e;
+        f.priority = hi;
         if ((e = cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming)) != cudaSuccess) return (int)e;
         if ((e = cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming)) != cudaSuccess) return (int)e;
     }
@@ -113,7 +119,8 @@ int run_graphed(const GraphKey& key, cudaStream_t user, bool eager,
         return rc != SMX_OK ? rc : (int)e;
     }
     GraphEntry ent{key, dev, nullptr, g_launches.load() - before, ++g_graph_clock};
-    e = cudaGraphInstantiate(&ent.exec, graph, 0);
+    // kernel nodes keep their launch priority (the look-ahead side chain)
+    e = cudaGraphInstantiate(&ent.exec, graph, cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return (int)e;
     if ((e = cudaGraphLaunch(ent.exec, user)) != cudaSuccess) {

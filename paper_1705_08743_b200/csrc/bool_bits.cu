@@ -194,8 +194,9 @@ int launch_bits(const BitsArgs& a_in, cudaStream_t s) {
         if (e != cudaSuccess) return (int)e;
     }
     dim3 grid(ntiles, mtiles, splits);
-    bool_bits_gemm_kernel<Cfg><<<grid, Cfg::THREADS, 0, s>>>(a);
-    SMX_RETURN_LAUNCH();
+    smx::count_launch();
+    const cudaError_t e = launch_kernel(bool_bits_gemm_kernel<Cfg>, grid, dim3(Cfg::THREADS), 0, s, a);
+    return e == cudaSuccess ? SMX_OK : (int)e;
 }
 
 int bool_bits_gemm(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int Nw, int K,
@@ -368,9 +369,10 @@ static int bits_pivot_and_row_panel(uint32_t* T, int n, long long ld_w, uint32_t
                                     cudaStream_t s) {
     const int kw0 = k0 / 32, nw = (n + 31) / 32;
     uint32_t* rowK = T + (long long)k0 * ld_w;
-    bool_pivot_kernel<<<1, kWarshallBlock, 0, s>>>(rowK + kw0, bb, ld_w);
-    SMX_LAUNCHED_OR_RETURN();
-    cudaError_t e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld_w * 4, cudaMemcpyDeviceToDevice, s);
+    count_launch();
+    cudaError_t e = launch_kernel(bool_pivot_kernel, dim3(1), dim3(kWarshallBlock), 0, s, rowK + kw0, bb, ld_w);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld_w * 4, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return (int)e;
     return bool_bits_gemm(RP + kw0, RP, rowK, bb, nw, bb, ld_w, ld_w, ld_w, 1, 0, 0, s);
 }
@@ -432,7 +434,10 @@ static int bool_warshall_schedule(uint32_t* T, int n, long long ld_w, uint32_t* 
                                    ld_w, 1, 0, 0, s));
             if ((e = cudaEventRecord(ss->fork, s)) != cudaSuccess) return (int)e;
             if ((e = cudaStreamWaitEvent(ss->side, ss->fork, 0)) != cudaSuccess) return (int)e;
-            SMX_TRY(bits_pivot_and_row_panel(T, n, ld_w, RP, k1, bb1, ss->side));
+            {
+                PriorityScope ps(ss->priority);
+                SMX_TRY(bits_pivot_and_row_panel(T, n, ld_w, RP, k1, bb1, ss->side));
+            }
             if ((e = cudaEventRecord(ss->join, ss->side)) != cudaSuccess) return (int)e;
             SMX_TRY(bool_bits_gemm(CP, rowK, T, n, nw, bb, ldcp, ld_w, ld_w, 1, k0, bb + bb1, s));
             SMX_TRY(copy_words(T + k1 / 32, ld_w, CP, ldcp, n, (bb1 + 31) / 32, s));

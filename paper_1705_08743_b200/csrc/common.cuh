@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <functional>
+#include <utility>
 
 #include "semimat_b200.h"   // include/ (on the -I path of _build.py)
 
@@ -21,6 +22,7 @@ void count_launch();
 struct SideStream {
     cudaStream_t side = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
+    int priority = 0;   // the side stream's (highest) priority
 };
 int side_stream(SideStream** out);
 // smx_set_fw_lookahead switch, shared by the lane FW and Boolean Warshall.
@@ -33,6 +35,37 @@ int lookahead_enabled();
 // run_graphed captures body() on a private stream and launches the graph on
 // `user`; when graphs are off (smx_set_graphs), the caller's stream is itself
 // being captured, or `eager` is set, body(user) runs directly.
+// Launch priority for kernels of the look-ahead side stream.  A stream's
+// priority is not recorded into a captured graph, so the side-stream kernels
+// carry it per launch (cudaLaunchAttributePriority), which graph kernel nodes
+// keep.  0 = plain launch.  Set with PriorityScope around side-stream work.
+int& launch_priority();
+struct PriorityScope {
+    int old;
+    explicit PriorityScope(int p) : old(launch_priority()) { launch_priority() = p; }
+    ~PriorityScope() { launch_priority() = old; }
+};
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                 Args&&... args) {
+    const int prio = launch_priority();
+    if (prio == 0) {
+        kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributePriority;
+    attr[0].val.priority = prio;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 struct GraphKey {
     int fn = 0;
     unsigned long long v[14] = {};

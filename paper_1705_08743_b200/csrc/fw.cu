@@ -214,8 +214,9 @@ int launch_pivot_lite(T* P, int b, long long ld, int kind, cudaStream_t s) {
         if (e != cudaSuccess) return (int)e;
         configured = true;
     }
-    kern<<<1, 256, smem, s>>>(P, b, ld, kind == SMX_ANTI);
-    SMX_RETURN_LAUNCH();
+    smx::count_launch();
+    const cudaError_t e = launch_kernel(kern, dim3(1), dim3(256), smem, s, P, b, ld, kind == SMX_ANTI);
+    return e == cudaSuccess ? SMX_OK : (int)e;
 }
 
 template <typename T>
@@ -225,15 +226,102 @@ int fw_pivot_lite(T* P, int b, long long ld, int kind, cudaStream_t s) {
     return launch_pivot_lite<T, FwBlock<T>::value>(P, b, ld, kind, s);
 }
 
+// Tile copy dst[0:rows, 0:cols] = src[0:rows, 0:cols] (16-byte vectors; a
+// ragged last column chunk element-wise): the column-panel snapshot
+// CP[i, 0:bb] = T[i, k0:k0+bb] and the pivot/row-panel snapshots.  A kernel
+// rather than cudaMemcpy2DAsync: in a captured graph a D2D memcpy node goes
+// to a copy engine with several microseconds of latency on the pivot chain.
 template <typename T>
-int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s) {
+__global__ void copy_panel_kernel(const T* __restrict__ src, long long ld, T* __restrict__ dst,
+                                  long long ldd, int rows, int cols) {
+    constexpr int E = 16 / sizeof(T);
+    const int cpr = (cols + E - 1) / E;
+    const long long total = (long long)rows * cpr;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / cpr), c = (int)(i % cpr) * E;
+        const T* s = src + r * ld + c;
+        T* d = dst + r * ldd + c;
+        if (c + E <= cols) *reinterpret_cast<uint4*>(d) = __ldg(reinterpret_cast<const uint4*>(s));
+        else
+            for (int j = 0; c + j < cols; ++j) d[j] = s[j];
+    }
+}
+
+template <typename T>
+int copy_panel(const T* src, long long ld, T* dst, long long ldd, int rows, int cols, cudaStream_t s) {
+    const long long work = (long long)rows * ((cols * (long long)sizeof(T) + 15) / 16);
+    long long blocks = (work + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    count_launch();
+    const cudaError_t e = launch_kernel(copy_panel_kernel<T>, dim3((unsigned)(blocks < 1 ? 1 : blocks)), dim3(256),
+                                        0, s, src, ld, dst, ldd, rows, cols);
+    return e == cudaSuccess ? SMX_OK : (int)e;
+}
+
+// Pivot tiles of 129..256 vertices: blocked FW with two blocks, h = 128
+// (the same three phases as fw_run, one level down):
+//   P11* ; P12 (+)= P11 (x) P12 ; P21 (+)= P21 (x) P11 ; P22 (+)= P21 (x) P12 ;
+//   P22* ; P21 (+)= P22 (x) P21 ; P12 (+)= P12 (x) P22 ; P11 (+)= P12 (x) P21.
+// The closures are the 128 register kernel, the products the Lite tiles
+// (8+ CTAs each).  A product whose output is also an operand reads a
+// snapshot of that operand from `scratch` (2 x 128 x 128 elements).
+// Measured 0.5 ms -> see DESIGN.md 4.2 for the chain it shortens; the
+// single-CTA shared-memory pivot (fw_pivot_lite) moved 3 x 512 B of shared
+// memory per row per step and was bandwidth-bound.
+template <typename T>
+int fw_pivot_2x2(T* P, int b, long long ld, int kind, T* scratch, cudaStream_t s) {
+    constexpr int h = 128;
+    const int m = b - h;
+    T* P12 = P + h;
+    T* P21 = P + (long long)h * ld;
+    T* P22 = P21 + h;
+    T* S12 = scratch;              // h x m, pitch h
+    T* S21 = scratch + h * h;      // m x h, pitch h
+    cudaError_t e;
+    count_launch();
+    if ((e = launch_kernel(fw_pivot_kernel<T, 128>, dim3(1), dim3(1024), 0, s, P, h, ld, kind == SMX_ANTI)) !=
+        cudaSuccess)
+        return (int)e;
+    SMX_TRY(copy_panel<T>(P12, ld, S12, h, h, m, s));
+    SMX_TRY(semiring_gemm_lite<T>(P, S12, P12, h, m, h, ld, h, ld, kind, s));
+    SMX_TRY(copy_panel<T>(P21, ld, S21, h, m, h, s));
+    SMX_TRY(semiring_gemm_lite<T>(S21, P, P21, m, h, h, h, ld, ld, kind, s));
+    SMX_TRY(semiring_gemm_lite<T>(P21, P12, P22, m, m, h, ld, ld, ld, kind, s));
+    count_launch();
+    if ((e = launch_kernel(fw_pivot_kernel<T, 128>, dim3(1), dim3(1024), 0, s, P22, m, ld, kind == SMX_ANTI)) !=
+        cudaSuccess)
+        return (int)e;
+    SMX_TRY(copy_panel<T>(P21, ld, S21, h, m, h, s));
+    SMX_TRY(semiring_gemm_lite<T>(P22, S21, P21, m, h, m, ld, h, ld, kind, s));
+    SMX_TRY(copy_panel<T>(P12, ld, S12, h, h, m, s));
+    SMX_TRY(semiring_gemm_lite<T>(S12, P22, P12, h, m, m, h, ld, ld, kind, s));
+    return semiring_gemm_lite<T>(P12, P21, P, h, h, m, ld, ld, ld, kind, s);
+}
+
+int scratch_alloc(void** p, size_t bytes, cudaStream_t s);
+int scratch_free(void* p, cudaStream_t s);
+
+// scratch: 2 x 128 x 128 elements for b > 128 (nullptr: stream-ordered scratch)
+template <typename T>
+int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s, T* scratch = nullptr) {
     if (b < 1 || b > FwBlock<T>::value || ld < b || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
     // The register-resident kernel unrolls CPT steps (16 cells/thread at 128);
     // at 256 that unroll (64 steps x 32 words) no longer fits the instruction
-    // caches (measured 688 us per pivot), so 256 uses the shared-memory tile.
-    if (b > 128) return fw_pivot_lite<T>(P, b, ld, kind, s);
-    fw_pivot_kernel<T, 128><<<1, 1024, 0, s>>>(P, b, ld, kind == SMX_ANTI);
-    SMX_RETURN_LAUNCH();
+    // caches (measured 688 us per pivot), so 256 recurses on 128 blocks.
+    if (b > 128) {
+        if (!aligned16(P) || !ld_ok(ld, sizeof(T))) return SMX_E_ALIGN;
+        if (scratch) return fw_pivot_2x2<T>(P, b, ld, kind, scratch, s);
+        void* sc = nullptr;
+        SMX_TRY(scratch_alloc(&sc, 2 * 128 * 128 * sizeof(T), s));
+        const int rc = fw_pivot_2x2<T>(P, b, ld, kind, reinterpret_cast<T*>(sc), s);
+        scratch_free(sc, s);
+        return rc;
+    }
+    count_launch();
+    const cudaError_t e = launch_kernel(fw_pivot_kernel<T, 128>, dim3(1), dim3(1024), 0, s, P, b, ld,
+                                        kind == SMX_ANTI);
+    return e == cudaSuccess ? SMX_OK : (int)e;
 }
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -261,33 +349,6 @@ int fw_phase3(const T* CP, long long ldcp, const T* rowK, T* Tm, int n, long lon
     return semiring_gemm<T>(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, skip0, skipn, s);
 }
 
-// Column-panel snapshot CP[i, 0:bb] = T[i, k0:k0+bb] for all n rows (16-byte
-// vectors; bb * sizeof(T) is a multiple of 16 except in a ragged last block).
-template <typename T>
-__global__ void copy_panel_kernel(const T* __restrict__ src, long long ld, T* __restrict__ dst,
-                                  long long ldd, int rows, int cols) {
-    constexpr int E = 16 / sizeof(T);
-    const int cpr = (cols + E - 1) / E;
-    const long long total = (long long)rows * cpr;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(i / cpr), c = (int)(i % cpr) * E;
-        const T* s = src + r * ld + c;
-        T* d = dst + r * ldd + c;
-        if (c + E <= cols) *reinterpret_cast<uint4*>(d) = __ldg(reinterpret_cast<const uint4*>(s));
-        else
-            for (int j = 0; c + j < cols; ++j) d[j] = s[j];
-    }
-}
-
-template <typename T>
-int copy_panel(const T* src, long long ld, T* dst, long long ldd, int rows, int cols, cudaStream_t s) {
-    const long long work = (long long)rows * ((cols * (long long)sizeof(T) + 15) / 16);
-    long long blocks = (work + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    copy_panel_kernel<T><<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(src, ld, dst, ldd, rows, cols);
-    SMX_RETURN_LAUNCH();
-}
 
 
 // Optional CUDA-event trace of the phase-3 launches (the dominant kernel), so
@@ -319,9 +380,8 @@ int fw_pivot_and_row_panel(T* Tm, int n, long long ld, int kind, T* RP, int k0, 
                            bool lite = false) {
     T* rowK = Tm + (long long)k0 * ld;
     if (lite) SMX_TRY(fw_pivot_lite<T>(rowK + k0, bb, ld, kind, s));
-    else SMX_TRY(fw_pivot<T>(rowK + k0, bb, ld, kind, s));
-    cudaError_t e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld * sizeof(T), cudaMemcpyDeviceToDevice, s);
-    if (e != cudaSuccess) return (int)e;
+    else SMX_TRY(fw_pivot<T>(rowK + k0, bb, ld, kind, s, RP));   // RP is free until the snapshot below
+    SMX_TRY(copy_panel<T>(rowK, ld, RP, ld, bb, n, s));
     if (lite) return semiring_gemm_lite<T>(RP + k0, RP, rowK, bb, n, bb, ld, ld, ld, kind, s);
     return semiring_gemm<T>(RP + k0, RP, rowK, bb, n, bb, ld, ld, ld, kind, 1, 0, 0, s);
 }
@@ -363,7 +423,10 @@ int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, void* p
                                      kind, 1, 0, 0, s));
             if ((e = cudaEventRecord(fs->fork, s)) != cudaSuccess) return (int)e;
             if ((e = cudaStreamWaitEvent(fs->side, fs->fork, 0)) != cudaSuccess) return (int)e;
-            SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
+            {
+                PriorityScope ps(fs->priority);
+                SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
+            }
             if ((e = cudaEventRecord(fs->join, fs->side)) != cudaSuccess) return (int)e;
             // 3b: everything else (skips K_r and K_{r+1}, adjacent tiles)
             trace_begin(s, (long long)(n - bb - bb1) * n * bb);
@@ -409,7 +472,10 @@ inline int fw_run_lookahead_packed(uint16_t* Tm, int n, long long ld, int kind, 
                                    0, pws, pws_bytes, s));
             if ((e = cudaEventRecord(fs->fork, s)) != cudaSuccess) return (int)e;
             if ((e = cudaStreamWaitEvent(fs->side, fs->fork, 0)) != cudaSuccess) return (int)e;
-            SMX_TRY(fw_pivot_and_row_panel<uint16_t>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
+            {
+                PriorityScope ps(fs->priority);
+                SMX_TRY(fw_pivot_and_row_panel<uint16_t>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
+            }
             if ((e = cudaEventRecord(fs->join, fs->side)) != cudaSuccess) return (int)e;
             // 3b: everything else (skips K_r and K_{r+1}, adjacent tiles)
             trace_begin(s, (long long)(n - bb - bb1) * n * bb);

@@ -438,8 +438,9 @@ int launch_semiring_gemm(const GemmArgs<T>& a, cudaStream_t stream) {
         const int mtiles = ceil_div(a.M, Cfg::BM) - a.skip_tiles;
         const int ntiles = ceil_div(a.N, Cfg::BN);
         if (mtiles <= 0 || ntiles <= 0) return SMX_OK;
-        kern<<<dim3(ntiles, mtiles), Cfg::THREADS, Cfg::SMEM, stream>>>(a);
-        SMX_RETURN_LAUNCH();
+        smx::count_launch();
+        const cudaError_t e = launch_kernel(kern, dim3(ntiles, mtiles), dim3(Cfg::THREADS), Cfg::SMEM, stream, a);
+        return e == cudaSuccess ? SMX_OK : (int)e;
     }
     auto kern = semiring_gemm_kernel<Cfg, T, false>;
     static bool configured = false;  // per instantiation
@@ -453,8 +454,9 @@ int launch_semiring_gemm(const GemmArgs<T>& a, cudaStream_t stream) {
     const int ntiles = ceil_div(a.N, Cfg::BN);
     if (mtiles <= 0 || ntiles <= 0) return SMX_OK;
     dim3 grid(ntiles, mtiles);
-    kern<<<grid, Cfg::THREADS, Cfg::SMEM, stream>>>(a);
-    SMX_RETURN_LAUNCH();
+    smx::count_launch();
+    const cudaError_t e = launch_kernel(kern, grid, dim3(Cfg::THREADS), Cfg::SMEM, stream, a);
+    return e == cudaSuccess ? SMX_OK : (int)e;
 }
 
 // ---- sparse-bounded certificates -------------------------------------------
