@@ -565,6 +565,9 @@ int smx_semiring_gemm_u8(const uint8_t* A, const uint8_t* B, uint8_t* C, int M, 
 }
 int smx_semiring_gemm_u16(const uint16_t* A, const uint16_t* B, uint16_t* C, int M, int N, int K,
                           int lda, int ldb, int ldc, int kind, int accumulate, void* stream) {
+    if (g_fw_packed && (long long)M * N >= (1LL << 22) && K >= 256)
+        return semiring_gemm_packed_public_u16(A, B, C, M, N, K, lda, ldb, ldc, kind, accumulate,
+                                               as_stream(stream));
     return semiring_gemm<uint16_t>(A, B, C, M, N, K, lda, ldb, ldc, kind, accumulate, 0, 0,
                                    as_stream(stream), /*certify=*/true);
 }

@@ -48,6 +48,7 @@ struct PackedArgs {
     int anti, accumulate, allow_bounded;
     int row_tile0;                // first 128-row tile of the launch window
     int skip_tile0, skip_tiles;   // tiles skipped inside the window
+    const int* cert;              // nullable: nonzero = operands packed in the shifted encoding
 };
 
 // ---- pack kernels -----------------------------------------------------------
@@ -55,7 +56,8 @@ struct PackedArgs {
 // 16-byte loads), writes 16 splat words down column r of the tile.
 __global__ void __launch_bounds__(128) pack_a_u16_kernel(const uint16_t* __restrict__ A, int M, int K,
                                                         long long lda, int anti, int KT,
-                                                        uint32_t* __restrict__ Ap, uint8_t* __restrict__ fA) {
+                                                        uint32_t* __restrict__ Ap, uint8_t* __restrict__ fA,
+                                                        const int* __restrict__ cert) {
     using L = Lane<uint16_t>;
     const int kt = blockIdx.x, mt = blockIdx.y, r = threadIdx.x;
     const int row = mt * PackedU16::BM + r, k0 = kt * PackedU16::BK;
@@ -77,10 +79,12 @@ __global__ void __launch_bounds__(128) pack_a_u16_kernel(const uint16_t* __restr
     }
     uint32_t hi = 0;
     uint32_t* dst = Ap + ((size_t)mt * KT + kt) * PackedU16::A_TILE_WORDS + r;
+    const bool sh = cert != nullptr && *cert != 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         hi |= v[i];
-        dst[i * PackedU16::BM] = L::splat(v[i]);
+        const uint32_t w = L::splat(v[i]);
+        dst[i * PackedU16::BM] = sh ? L::to_shifted(w) : w;
     }
     const int ok = __syncthreads_and((hi & 0x8000u) == 0u);
     if (r == 0) fA[(size_t)mt * KT + kt] = (uint8_t)ok;
@@ -90,7 +94,8 @@ __global__ void __launch_bounds__(128) pack_a_u16_kernel(const uint16_t* __restr
 // k-row t/16, chunk t%16, writes them as 4 canonical words.
 __global__ void __launch_bounds__(256) pack_b_u16_kernel(const uint16_t* __restrict__ B, int K, int N,
                                                         long long ldb, int anti, int NT,
-                                                        uint32_t* __restrict__ Bp, uint8_t* __restrict__ fB) {
+                                                        uint32_t* __restrict__ Bp, uint8_t* __restrict__ fB,
+                                                        const int* __restrict__ cert) {
     const int nt = blockIdx.x, kt = blockIdx.y, t = threadIdx.x;
     const int kk = t >> 4, c = t & 15;
     const int k = kt * PackedU16::BK + kk, col = nt * PackedU16::BN + c * 8;
@@ -110,6 +115,10 @@ __global__ void __launch_bounds__(256) pack_b_u16_kernel(const uint16_t* __restr
         w = make_uint4(e[0], e[1], e[2], e[3]);
     }
     const uint32_t hi = (w.x | w.y | w.z | w.w) & 0x80008000u;
+    if (cert != nullptr && *cert != 0) {
+        using L = Lane<uint16_t>;
+        w = make_uint4(L::to_shifted(w.x), L::to_shifted(w.y), L::to_shifted(w.z), L::to_shifted(w.w));
+    }
     *reinterpret_cast<uint4*>(Bp + ((size_t)kt * NT + nt) * PackedU16::B_TILE_WORDS + kk * PackedU16::BNW + c * 4) = w;
     const int ok = __syncthreads_and(hi == 0u);
     if (t == 0) fB[(size_t)kt * NT + nt] = (uint8_t)ok;
@@ -207,8 +216,9 @@ __global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(
         for (int kb = 0; kb < KT; kb += 32) {
             // bounded flags of 32 k-tiles in one round trip (one per lane)
             const int k = kb + lane;
-            const bool f = k < KT && p.allow_bounded && p.fA[(size_t)mt * KT + k] != 0 &&
-                           p.fB[(size_t)k * p.NT + nt] != 0;
+            const bool f = k < KT && p.allow_bounded &&
+                           ((p.cert != nullptr && *p.cert != 0) ||
+                            (p.fA[(size_t)mt * KT + k] != 0 && p.fB[(size_t)k * p.NT + nt] != 0));
             const uint32_t fmask = __ballot_sync(0xFFFFFFFFu, f);
             if (lane == 0) {
                 const int kend = KT - kb < 32 ? KT : kb + 32;
@@ -282,6 +292,12 @@ __global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(
     }
 
     // ---- fold C in and store ----
+    if (p.cert != nullptr && *p.cert != 0) {
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TNW; ++j) acc[i][j] = L::from_shifted(acc[i][j]);
+    }
     const uint32_t cm = anti ? 0xFFFFFFFFu : 0u;
     if (c_async) pk_mbar_wait(cbar, 0);
 #pragma unroll
@@ -354,17 +370,17 @@ inline int packed_check(const void* A, const void* B, int M, int N, int K, long 
 
 // Pack A (M x K; A == nullptr skips it) and/or B (K x N; B == nullptr skips).
 inline int packed_u16_pack(const uint16_t* A, const uint16_t* B, int M, int N, int K, long long lda, long long ldb,
-                           int kind, void* ws, size_t ws_bytes, cudaStream_t s) {
+                           int kind, void* ws, size_t ws_bytes, cudaStream_t s, const int* cert = nullptr) {
     SMX_TRY(packed_check(A, B, M, N, K, lda, ldb, kind, ws, ws_bytes));
     if (M == 0 || N == 0 || K == 0) return SMX_OK;
     const PackedWs v = packed_views(ws, M, N, K);
     const int anti = kind == SMX_ANTI;
     if (A) {
-        pack_a_u16_kernel<<<dim3(v.KT, v.MT), 128, 0, s>>>(A, M, K, lda, anti, v.KT, v.Ap, v.fA);
+        pack_a_u16_kernel<<<dim3(v.KT, v.MT), 128, 0, s>>>(A, M, K, lda, anti, v.KT, v.Ap, v.fA, cert);
         SMX_LAUNCHED_OR_RETURN();
     }
     if (B) {
-        pack_b_u16_kernel<<<dim3(v.NT, v.KT), 256, 0, s>>>(B, K, N, ldb, anti, v.NT, v.Bp, v.fB);
+        pack_b_u16_kernel<<<dim3(v.NT, v.KT), 256, 0, s>>>(B, K, N, ldb, anti, v.NT, v.Bp, v.fB, cert);
         SMX_LAUNCHED_OR_RETURN();
     }
     return SMX_OK;
@@ -374,7 +390,8 @@ inline int packed_u16_pack(const uint16_t* A, const uint16_t* B, int M, int N, i
 // [row_tile0, row_tile0 + row_tiles) minus the rows [skip_row0, skip_row0 +
 // skip_rows) (whole tiles, inside the window).  row_tiles < 0: to the end.
 inline int packed_u16_run(uint16_t* C, int M, int N, int K, long long ldc, int kind, int accumulate, int row_tile0,
-                          int row_tiles, int skip_row0, int skip_rows, void* ws, size_t ws_bytes, cudaStream_t s) {
+                          int row_tiles, int skip_row0, int skip_rows, void* ws, size_t ws_bytes, cudaStream_t s,
+                          const int* cert = nullptr) {
     using G = PackedU16;
     if (M < 0 || N < 0 || K < 0 || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
     if (M == 0 || N == 0) return SMX_OK;
@@ -385,7 +402,7 @@ inline int packed_u16_run(uint16_t* C, int M, int N, int K, long long ldc, int k
     if (row_tile0 < 0 || row_tile0 > v.MT) return SMX_E_ARG;
     if (row_tiles < 0 || row_tile0 + row_tiles > v.MT) row_tiles = v.MT - row_tile0;
     PackedArgs a{v.Ap, v.Bp, v.fA, v.fB, C, M, N, v.KT, v.NT, ldc, kind == SMX_ANTI, accumulate != 0,
-                 bounded_fastpath_enabled(), row_tile0, v.MT, 0};
+                 bounded_fastpath_enabled(), row_tile0, v.MT, 0, cert};
     if (skip_rows > 0) {
         if (skip_row0 % G::BM) return SMX_E_ARG;
         a.skip_tile0 = skip_row0 / G::BM;
@@ -415,6 +432,81 @@ inline int semiring_gemm_packed_u16(const uint16_t* A, const uint16_t* B, uint16
     if (M == 0 || N == 0) return SMX_OK;
     SMX_TRY(packed_u16_pack(A, B, M, N, K, lda, ldb, kind, ws, ws_bytes, s));
     return packed_u16_run(C, M, N, K, ldc, kind, accumulate, 0, -1, skip_row0, skip_rows, ws, ws_bytes, s);
+}
+
+// Global sparse-bounded certificate of a u16 operand (rows x cols, ld): clears
+// *cert if any lane in distance form is neither S nor < 2^14 (Lane::cert_ok).
+// Concurrent writers only store 0.
+__global__ void cert_u16_kernel(const uint16_t* __restrict__ X, int rows, int cols, long long ld, int anti,
+                                int* __restrict__ cert) {
+    using L = Lane<uint16_t>;
+    const int cpr = (cols + 7) / 8;
+    const long long total = (long long)rows * cpr;
+    const uint32_t m = anti ? 0xFFFFFFFFu : 0u;
+    bool ok = true;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / cpr), c = (int)(i % cpr) * 8;
+        uint4 w = __ldg(reinterpret_cast<const uint4*>(X + r * ld + c));
+        w.x ^= m; w.y ^= m; w.z ^= m; w.w ^= m;
+        if (c + 8 > cols) {   // cells >= cols: identity (S), which certifies
+            uint32_t e[4] = {w.x, w.y, w.z, w.w};
+            for (int j = cols - c; j < 8; ++j) e[j >> 1] |= 0xFFFFu << ((j & 1) * 16);
+            w = make_uint4(e[0], e[1], e[2], e[3]);
+        }
+        ok = ok && L::cert_ok(w.x) && L::cert_ok(w.y) && L::cert_ok(w.z) && L::cert_ok(w.w);
+    }
+    if (!__all_sync(0xFFFFFFFFu, ok) && (threadIdx.x & 31) == 0) *cert = 0;
+}
+
+// Public u16 product on the packed kernel.  K is processed in chunks so the
+// packed operands stay <= ~384 MB of stream-ordered scratch; a certificate
+// pass first decides, for the whole product, whether the operands can be
+// packed in the shifted 1-instruction encoding (semiring.cuh, Lane<uint16_t>):
+// then every k-tile runs VIADDMNMX alone, and results map back to S before C
+// is folded in.  Otherwise tiles use the per-tile bounded flags.
+inline int semiring_gemm_packed_public_u16(const uint16_t* A, const uint16_t* B, uint16_t* C, int M, int N, int K,
+                                           long long lda, long long ldb, long long ldc, int kind, int accumulate,
+                                           cudaStream_t s) {
+    using G = PackedU16;
+    if (M < 0 || N < 0 || K < 0 || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
+    if (M == 0 || N == 0) return SMX_OK;
+    if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return SMX_E_ALIGN;
+    if (!ld_ok(lda, 2) || !ld_ok(ldb, 2) || !ld_ok(ldc, 2)) return SMX_E_ALIGN;
+    if (lda < K || ldb < N || ldc < N) return SMX_E_ARG;
+    long long kc = (384LL << 20) / ((long long)G::BM * ceil_div(M, G::BM) * 4 + (long long)G::BN * ceil_div(N, G::BN) * 2);
+    kc = kc / 256 * 256;
+    if (kc < 256) kc = 256;
+    if (kc > K) kc = K;
+    const size_t ws_bytes = packed_u16_ws_bytes(M, N, (int)kc);
+    void* scratch = nullptr;
+    SMX_TRY(scratch_alloc(&scratch, ws_bytes + 256, s));
+    struct FreeOnExit {
+        void* p; cudaStream_t s;
+        ~FreeOnExit() { scratch_free(p, s); }
+    } guard{scratch, s};
+    int* cert = reinterpret_cast<int*>(scratch);
+    void* ws = reinterpret_cast<char*>(scratch) + 256;
+    const int anti = kind == SMX_ANTI;
+    const int* certp = nullptr;
+    if (bounded_fastpath_enabled() && K > 0) {
+        cudaError_t e = cudaMemsetAsync(cert, 0xFF, sizeof(int), s);
+        if (e != cudaSuccess) return (int)e;
+        const int blocks = 4 * sm_count();
+        cert_u16_kernel<<<blocks, 256, 0, s>>>(A, M, K, lda, anti, cert);
+        SMX_LAUNCHED_OR_RETURN();
+        cert_u16_kernel<<<blocks, 256, 0, s>>>(B, K, N, ldb, anti, cert);
+        SMX_LAUNCHED_OR_RETURN();
+        certp = cert;
+    }
+    if (K == 0) return packed_u16_run(C, M, N, 0, ldc, kind, accumulate, 0, -1, 0, 0, ws, ws_bytes, s);
+    for (long long k0 = 0; k0 < K; k0 += kc) {
+        const int kk = (int)(K - k0 < kc ? K - k0 : kc);
+        SMX_TRY(packed_u16_pack(A + k0, B + k0 * ldb, M, N, kk, lda, ldb, kind, ws, ws_bytes, s, certp));
+        SMX_TRY(packed_u16_run(C, M, N, kk, ldc, kind, k0 == 0 ? accumulate : 1, 0, -1, 0, 0, ws, ws_bytes, s,
+                               certp));
+    }
+    return SMX_OK;
 }
 
 }  // namespace smx

@@ -679,3 +679,49 @@ def test_packed_skip_gemm_matches_register_kernel_and_oracle(kind, oracle_lib):
     prod = oracle_lib.semiring_mul(a[:300], b, K, 16, kind)
     want = np.maximum(c[:300], prod) if kind == "anti" else np.minimum(c[:300], prod)
     np.testing.assert_array_equal(outs[0][:300], want)
+
+
+@pytest.mark.parametrize("case", ["certified", "one_large", "full_range"])
+@pytest.mark.parametrize("kind", ["anti", "dist"])
+def test_public_u16_product_packed_path(case, kind, oracle_lib):
+    """smx_semiring_gemm_u16 at sizes that take the packed kernel: the
+    product-wide shifted encoding (certified), a single large lane that voids
+    the certificate, and full-range lanes (per-tile flags) -- each equal to
+    the register-staged kernel and to the oracle on 256 rows.  K = 700 spans
+    a ragged last k-tile."""
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    rng = np.random.default_rng({"certified": 1, "one_large": 2, "full_range": 3}[case])
+    M, N, K = 2100, 2056, 700
+    S = 0xFFFF
+    hi = 60000 if case == "full_range" else 1000
+    def mat(r, c):
+        v = rng.integers(0, hi, (r, c), dtype=np.uint32)
+        v[rng.random((r, c)) > 0.2] = S
+        return v
+    a, b = mat(M, K), mat(K, N)
+    if case == "one_large":
+        a[1234, 77] = 40000
+    if kind == "anti":
+        a, b = S - a, S - b
+    a, b = a.astype(np.uint16), b.astype(np.uint16)
+    lda, ldn = 704, 2056
+    apad = np.zeros((M, lda), np.uint16); apad[:, :K] = a
+    kid = 0 if kind == "anti" else 1
+    outs = []
+    for packed in (1, 0):
+        old = lib.smx_set_fw_packed(packed)
+        try:
+            ta = torch.from_numpy(apad.view(np.int16)).cuda()
+            tb = torch.from_numpy(b.view(np.int16)).cuda()
+            tc = torch.empty((M, ldn), dtype=torch.int16, device="cuda")
+            _native.check(lib.smx_semiring_gemm_u16(ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), M, N, K, lda, ldn,
+                                                    ldn, kid, 0, _native.stream_ptr()), "u16 product")
+            torch.cuda.synchronize()
+            outs.append(tc.cpu().numpy().view(np.uint16).copy())
+        finally:
+            lib.smx_set_fw_packed(old)
+    np.testing.assert_array_equal(outs[0], outs[1])
+    rows = np.r_[0:128, 1200:1328]
+    want = oracle_lib.semiring_mul(apad[rows], b, K, 16, kind)
+    np.testing.assert_array_equal(outs[0][rows], want)
