@@ -106,9 +106,10 @@ int smx_set_graphs(int enable);
  * 0 (default) = the regular pivot and tiles.  Results are identical.
  * Returns the previous setting. */
 int smx_set_fw_side_lite(int enable);
-/* Pivot block of smx_fw_*: 0 = automatic (256 for u8/u16 at n >= 8192,
- * else 128), or force 128 / 256 (u32 is always 128).  Returns the previous
- * setting (or SMX_E_ARG). */
+/* Pivot block of smx_fw_*: 0 = automatic (u16: 512 at n >= 16384, 256 at
+ * n >= 8192; u8: 256 at n >= 8192; else 128), or force 128 / 256 / 512
+ * (clamped to smx_fw_block: u8 256, u32 128).  Returns the previous setting
+ * (or SMX_E_ARG). */
 int smx_set_fw_block(int block);
 /* Packed u16 kernel: 1 (default) = smx_fw_u16's phase 3, large
  * smx_semiring_gemm_u16 products (M*N >= 2^22, K >= 256) and large

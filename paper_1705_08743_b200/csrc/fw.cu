@@ -24,20 +24,22 @@
 
 namespace smx {
 
-// Pivot block size: 256 vertices for u8/u16 (K = 256 per phase-3 CTA halves
-// the share of each CTA's C load/store and the number of rounds), 128 for
-// u32 (whose 1024-thread pivot tile would not fit the register file).
-template <typename T> struct FwBlock { static constexpr int value = sizeof(T) == 4 ? 128 : 256; };
-inline int fw_block_for(int eb) { return eb == 4 ? 128 : 256; }
-// Block used for an n-vertex closure: the 256 block halves the rounds and
-// doubles phase 3's K per CTA, amortising each CTA's C load/store (measured
-// +6% at n = 8192, +9% at 16384, +10% at 32768 over 128); its pivot is the
-// shared-memory kernel.  Below 8192 vertices the pivot chain no longer hides
-// behind phase 3 and the 128 block's register pivot wins.
+// Largest pivot block: 512 vertices for u16 (the packed phase 3 runs K = 512
+// per CTA), 256 for u8, 128 for u32 (whose 1024-thread pivot tile would not
+// fit the register file).  Tiles above 128 close by 2 x 2 recursion.
+template <typename T> struct FwBlock { static constexpr int value = sizeof(T) == 4 ? 128 : (sizeof(T) == 2 ? 512 : 256); };
+inline int fw_block_for(int eb) { return eb == 4 ? 128 : (eb == 2 ? 512 : 256); }
+// Block used for an n-vertex closure.  A larger block halves the rounds and
+// doubles phase 3's K per CTA, amortising each CTA's ramp and C fold; it
+// costs a longer pivot chain, which must hide behind one round's phase 3.
+// Measured (u16): 256 over 128 +6% at n = 8192, +9% at 16384, +10% at 32768;
+// 512 over 256 at n >= 16384: see DESIGN.md 4.2.  Below 8192 vertices the
+// pivot chain no longer hides behind phase 3 and 128 wins.
 static int g_fw_block_override = 0;   // smx_set_fw_block: 0 = automatic
 template <typename T> inline int fw_block_for_n(int n) {
-    if (g_fw_block_override == 128 || (g_fw_block_override == 256 && sizeof(T) == 4)) return 128;
-    if (g_fw_block_override == 256) return 256;
+    const int mx = FwBlock<T>::value;
+    if (g_fw_block_override != 0) return g_fw_block_override < mx ? g_fw_block_override : mx;
+    if (sizeof(T) == 2 && n >= 16384) return 512;
     return (sizeof(T) < 4 && n >= 8192) ? 256 : 128;
 }
 
@@ -223,7 +225,8 @@ template <typename T>
 int fw_pivot_lite(T* P, int b, long long ld, int kind, cudaStream_t s) {
     if (b < 1 || b > FwBlock<T>::value || ld < b || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
     if (b <= 128) return launch_pivot_lite<T, 128>(P, b, ld, kind, s);
-    return launch_pivot_lite<T, FwBlock<T>::value>(P, b, ld, kind, s);
+    if (b > 256) return SMX_E_ARG;   // the shared-memory tile holds at most 256 x 256
+    return launch_pivot_lite<T, (FwBlock<T>::value < 256 ? FwBlock<T>::value : 256)>(P, b, ld, kind, s);
 }
 
 // Tile copy dst[0:rows, 0:cols] = src[0:rows, 0:cols] (16-byte vectors; a
@@ -259,39 +262,36 @@ int copy_panel(const T* src, long long ld, T* dst, long long ldd, int rows, int 
     return e == cudaSuccess ? SMX_OK : (int)e;
 }
 
-// Pivot tiles of 129..256 vertices: blocked FW with two blocks, h = 128
-// (the same three phases as fw_run, one level down):
+// Pivot tiles above 128 vertices: blocked FW with two blocks, h = 128 for
+// b <= 256 and h = 256 above (the same three phases as fw_run, one level
+// down):
 //   P11* ; P12 (+)= P11 (x) P12 ; P21 (+)= P21 (x) P11 ; P22 (+)= P21 (x) P12 ;
 //   P22* ; P21 (+)= P22 (x) P21 ; P12 (+)= P12 (x) P22 ; P11 (+)= P12 (x) P21.
-// The closures are the 128 register kernel, the products the Lite tiles
-// (8+ CTAs each).  A product whose output is also an operand reads a
-// snapshot of that operand from `scratch` (2 x 128 x 128 elements).
-// Measured 0.5 ms -> see DESIGN.md 4.2 for the chain it shortens; the
-// single-CTA shared-memory pivot (fw_pivot_lite) moved 3 x 512 B of shared
-// memory per row per step and was bandwidth-bound.
+// The closures recurse down to the 128 register kernel, the products are
+// Lite tiles.  A product whose output is also an operand reads a snapshot of
+// that operand from `scratch` (2 x h x h elements; the nested closures reuse
+// it, as the snapshots are dead while they run).  256: 185 us, against
+// 500 us for the single-CTA shared-memory pivot (fw_pivot_lite), which moved
+// 3 x 512 B of shared memory per row per step and was bandwidth-bound.
+template <typename T>
+int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s, T* scratch);
+
 template <typename T>
 int fw_pivot_2x2(T* P, int b, long long ld, int kind, T* scratch, cudaStream_t s) {
-    constexpr int h = 128;
+    const int h = b <= 256 ? 128 : 256;
     const int m = b - h;
     T* P12 = P + h;
     T* P21 = P + (long long)h * ld;
     T* P22 = P21 + h;
-    T* S12 = scratch;              // h x m, pitch h
-    T* S21 = scratch + h * h;      // m x h, pitch h
-    cudaError_t e;
-    count_launch();
-    if ((e = launch_kernel(fw_pivot_kernel<T, 128>, dim3(1), dim3(1024), 0, s, P, h, ld, kind == SMX_ANTI)) !=
-        cudaSuccess)
-        return (int)e;
+    T* S12 = scratch;                  // h x m, pitch h
+    T* S21 = scratch + (size_t)h * h;  // m x h, pitch h
+    SMX_TRY(fw_pivot<T>(P, h, ld, kind, s, scratch));
     SMX_TRY(copy_panel<T>(P12, ld, S12, h, h, m, s));
     SMX_TRY(semiring_gemm_lite<T>(P, S12, P12, h, m, h, ld, h, ld, kind, s));
     SMX_TRY(copy_panel<T>(P21, ld, S21, h, m, h, s));
     SMX_TRY(semiring_gemm_lite<T>(S21, P, P21, m, h, h, h, ld, ld, kind, s));
     SMX_TRY(semiring_gemm_lite<T>(P21, P12, P22, m, m, h, ld, ld, ld, kind, s));
-    count_launch();
-    if ((e = launch_kernel(fw_pivot_kernel<T, 128>, dim3(1), dim3(1024), 0, s, P22, m, ld, kind == SMX_ANTI)) !=
-        cudaSuccess)
-        return (int)e;
+    SMX_TRY(fw_pivot<T>(P22, m, ld, kind, s, scratch));
     SMX_TRY(copy_panel<T>(P21, ld, S21, h, m, h, s));
     SMX_TRY(semiring_gemm_lite<T>(P22, S21, P21, m, h, m, ld, h, ld, kind, s));
     SMX_TRY(copy_panel<T>(P12, ld, S12, h, h, m, s));
@@ -302,9 +302,10 @@ int fw_pivot_2x2(T* P, int b, long long ld, int kind, T* scratch, cudaStream_t s
 int scratch_alloc(void** p, size_t bytes, cudaStream_t s);
 int scratch_free(void* p, cudaStream_t s);
 
-// scratch: 2 x 128 x 128 elements for b > 128 (nullptr: stream-ordered scratch)
+// scratch: 2 x h x h elements for b > 128, h as in fw_pivot_2x2 (nullptr:
+// stream-ordered scratch)
 template <typename T>
-int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s, T* scratch = nullptr) {
+int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s, T* scratch) {
     if (b < 1 || b > FwBlock<T>::value || ld < b || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
     // The register-resident kernel unrolls CPT steps (16 cells/thread at 128);
     // at 256 that unroll (64 steps x 32 words) no longer fits the instruction
@@ -313,7 +314,8 @@ int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s, T* scratch = n
         if (!aligned16(P) || !ld_ok(ld, sizeof(T))) return SMX_E_ALIGN;
         if (scratch) return fw_pivot_2x2<T>(P, b, ld, kind, scratch, s);
         void* sc = nullptr;
-        SMX_TRY(scratch_alloc(&sc, 2 * 128 * 128 * sizeof(T), s));
+        const size_t h = b <= 256 ? 128 : 256;
+        SMX_TRY(scratch_alloc(&sc, 2 * h * h * sizeof(T), s));
         const int rc = fw_pivot_2x2<T>(P, b, ld, kind, reinterpret_cast<T*>(sc), s);
         scratch_free(sc, s);
         return rc;
@@ -379,7 +381,7 @@ template <typename T>
 int fw_pivot_and_row_panel(T* Tm, int n, long long ld, int kind, T* RP, int k0, int bb, cudaStream_t s,
                            bool lite = false) {
     T* rowK = Tm + (long long)k0 * ld;
-    if (lite) SMX_TRY(fw_pivot_lite<T>(rowK + k0, bb, ld, kind, s));
+    if (lite && bb <= 256) SMX_TRY(fw_pivot_lite<T>(rowK + k0, bb, ld, kind, s));
     else SMX_TRY(fw_pivot<T>(rowK + k0, bb, ld, kind, s, RP));   // RP is free until the snapshot below
     SMX_TRY(copy_panel<T>(rowK, ld, RP, ld, bb, n, s));
     if (lite) return semiring_gemm_lite<T>(RP + k0, RP, rowK, bb, n, bb, ld, ld, ld, kind, s);
@@ -502,7 +504,7 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
     if (n == 0) return SMX_OK;
     if (!aligned16(Tm) || !ld_ok(ld, sizeof(T))) return SMX_E_ALIGN;
     const int BLK = fw_block_for_n<T>(n);
-    if (n <= FwBlock<T>::value) return fw_pivot<T>(Tm, n, ld, kind, s);
+    if (n <= FwBlock<T>::value) return fw_pivot<T>(Tm, n, ld, kind, s, nullptr);
     if (ws == nullptr || ws_bytes < fw_ws_bytes(n, ld, sizeof(T))) return SMX_E_WORKSPACE;
     T* RP = reinterpret_cast<T*>(ws);
     T* CP = reinterpret_cast<T*>(reinterpret_cast<char*>(ws) +
@@ -537,7 +539,7 @@ int fw_run_serial(T* Tm, int n, long long ld, int kind, T* RP, T* CP, void* pws,
     for (int k0 = 0; k0 < n; k0 += BLK) {
         const int bb = n - k0 < BLK ? n - k0 : BLK;
         T* rowK = Tm + (long long)k0 * ld;
-        SMX_TRY(fw_pivot<T>(rowK + k0, bb, ld, kind, s));
+        SMX_TRY(fw_pivot<T>(rowK + k0, bb, ld, kind, s, RP));   // RP is free until the snapshot
         cudaError_t e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld * sizeof(T),
                                         cudaMemcpyDeviceToDevice, s);
         if (e != cudaSuccess) return (int)e;
@@ -614,7 +616,7 @@ int smx_set_fw_packed(int enable) {
 }
 
 int smx_set_fw_block(int block) {
-    if (block != 0 && block != 128 && block != 256) return SMX_E_ARG;
+    if (block != 0 && block != 128 && block != 256 && block != 512) return SMX_E_ARG;
     const int old = g_fw_block_override;
     g_fw_block_override = block;
     return old;
@@ -661,9 +663,9 @@ int smx_fw_block(int elem_bytes) {
 int smx_fw_pivot(void* P, int b, int ld, int elem_bytes, int kind, void* stream) {
     cudaStream_t s = as_stream(stream);
     switch (elem_bytes) {
-        case 1: return fw_pivot<uint8_t>((uint8_t*)P, b, ld, kind, s);
-        case 2: return fw_pivot<uint16_t>((uint16_t*)P, b, ld, kind, s);
-        case 4: return fw_pivot<uint32_t>((uint32_t*)P, b, ld, kind, s);
+        case 1: return fw_pivot<uint8_t>((uint8_t*)P, b, ld, kind, s, nullptr);
+        case 2: return fw_pivot<uint16_t>((uint16_t*)P, b, ld, kind, s, nullptr);
+        case 4: return fw_pivot<uint32_t>((uint32_t*)P, b, ld, kind, s, nullptr);
         default: return SMX_E_ARG;
     }
 }

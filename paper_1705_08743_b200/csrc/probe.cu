@@ -1,33 +1,41 @@
 // Instruction-issue microbenchmark for the roofline denominator of the
 // CUDA-core semiring kernels: the packed-integer issue peak
 // is MEASURED on the box, not assumed.  Each thread runs 16 independent
-// accumulator chains of exactly the instruction pair the semiring inner loop
-// uses (VIMNMX.U16x2 + VIADDMNMX.U16x2), or VIADDMNMX.U16x2 alone (the u8
+// accumulator pairs of exactly the instruction pair the semiring inner loop
+// uses (VIMNMX.U16x2 + VIADDMNMX.U16x2), or VIADDMNMX.U16x2 alone (the
 // one-instruction form), so the result is the sustained issue rate of the
-// same SASS mix on every SM.
+// same SASS mix on every SM.  bench.py also reports it per SM per clock
+// against the nominal 64 lanes/clk/SM of the packed-integer pipe.
 #include "common.cuh"
 
 namespace smx {
 
 template <bool ONE>
 __global__ void __launch_bounds__(256) int_issue_probe_kernel(uint32_t* sink, int iters, uint32_t seed) {
-    uint32_t c[16];
-    uint32_t b = seed ^ threadIdx.x, a = seed * 3u + blockIdx.x, sa = ~a;
+    // 32 accumulators in 16 independent pairs (c[i] reads c[i ^ 16]): every
+    // SMSP has 8+ warps x 16 chains in flight, so latency never binds; 4
+    // sweeps per iteration keep the loop and operand bookkeeping (3-4 ops)
+    // under 3% of the issued instructions.
+    uint32_t c[32];
+    uint32_t a = seed * 3u + blockIdx.x, sa = ~a;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) c[i] = seed + i * 0x01010101u + threadIdx.x;
+    for (int i = 0; i < 32; ++i) c[i] = seed + i * 0x01010101u + threadIdx.x;
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            if (ONE) c[i] = __viaddmin_u16x2(a, c[i], c[(i + 1) & 15]);
-            else c[i] = __viaddmin_u16x2(__vminu2(c[i], sa), a, c[(i + 5) & 15]);
+        for (int rep = 0; rep < 4; ++rep) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const uint32_t o = c[i ^ 16];
+                if (ONE) c[i] = __viaddmin_u16x2(a, c[i], o);
+                else c[i] = __viaddmin_u16x2(__vminu2(c[i], sa), a, o);
+            }
         }
-        b += 1u;
-        a ^= b;
+        a += 0x00010001u;
         sa = ~a;
     }
     uint32_t x = 0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) x ^= c[i];
+    for (int i = 0; i < 32; ++i) x ^= c[i];
     if (x == 0x9E3779B9u) sink[blockIdx.x * blockDim.x + threadIdx.x] = x;  // keep the work
 }
 
@@ -36,9 +44,9 @@ __global__ void __launch_bounds__(256) int_issue_probe_kernel(uint32_t* sink, in
 extern "C" int smx_int_issue_probe(uint32_t* sink, int blocks, int threads, int iters, int one_instr,
                                    long long* instr_per_thread, void* stream) {
     if (blocks <= 0 || threads <= 0 || threads > 256 || iters <= 0) return SMX_E_ARG;
-    // semiring instructions per thread (the 3 bookkeeping ALU ops per
-    // iteration are excluded: they only dilute the measured rate by 3/35)
-    if (instr_per_thread) *instr_per_thread = (long long)iters * (one_instr ? 16 : 32);
+    // semiring instructions per thread (the loop's 3-4 bookkeeping ops per
+    // 128 or 256 semiring instructions are excluded)
+    if (instr_per_thread) *instr_per_thread = (long long)iters * 4 * (one_instr ? 32 : 64);
     if (one_instr)
         smx::int_issue_probe_kernel<true><<<blocks, threads, 0, smx::as_stream(stream)>>>(sink, iters, 12345u);
     else

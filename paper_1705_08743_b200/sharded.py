@@ -56,7 +56,9 @@ class CudaFwOps:
         self.width = width
         self.eb = width // 8
         self.kind = _native.SMX_ANTI if anti else _native.SMX_DIST
-        self.block = _native.lib().smx_fw_block(self.eb)
+        # at most 256: row panels stay fine-grained across ranks, and the
+        # owner's pivot chain stays short against 1/P of a round's phase 3
+        self.block = min(_native.lib().smx_fw_block(self.eb), 256)
         self._cp = None
 
     def _at(self, t: torch.Tensor, r: int, c: int) -> int:

@@ -372,7 +372,7 @@ def test_fw_fastpath_on_off_identical():
     np.testing.assert_array_equal(fast, slow)
 
 
-@pytest.mark.parametrize("n", [129, 300, 1000, 2048])
+@pytest.mark.parametrize("n", [129, 300, 1000, 1100, 2048])
 def test_fw_lookahead_and_serial_schedules_agree(n, oracle_lib):
     from paper_1705_08743_b200 import _native
     lib = _native.lib()
@@ -380,7 +380,7 @@ def test_fw_lookahead_and_serial_schedules_agree(n, oracle_lib):
     (t,) = workloads.make_inputs(cfg, n)
     want = oracle_lib.semiring_close(t, 16, "anti")
     for la, lite, blk in ((1, 0, 0), (0, 0, 0), (1, 1, 0), (1, 0, 256), (1, 1, 256), (0, 0, 256),
-                          (1, 0, 128)):
+                          (1, 0, 128), (1, 0, 512), (0, 0, 512), (1, 1, 512)):
         olds = (lib.smx_set_fw_lookahead(la), lib.smx_set_fw_side_lite(lite), lib.smx_set_fw_block(blk))
         try:
             for width_kind in ("anti", "dist"):

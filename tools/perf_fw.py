@@ -33,7 +33,7 @@ for n in sizes:
         w.copy_(src); engines.lane_close_(w, n, 16, True)
     variants = [(1, 1, 0, 0, 1), (1, 1, 0, 0, 0), (1, 0, 0, 0, 1)]
     if os.environ.get("PERF_FW_ALL"):
-        variants += [(1, 1, 1, 0, 1), (1, 1, 0, 128, 1), (1, 1, 0, 256, 1)]
+        variants += [(1, 1, 1, 0, 1), (1, 1, 0, 128, 1), (1, 1, 0, 256, 1), (1, 1, 0, 512, 1)]
     for fast, la, lite, blk, packed in variants:
         lib.smx_set_bounded_fastpath(fast); lib.smx_set_fw_lookahead(la); lib.smx_set_fw_side_lite(lite)
         lib.smx_set_fw_block(blk); lib.smx_set_fw_packed(packed)
