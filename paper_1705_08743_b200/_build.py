@@ -55,7 +55,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(src: Path) -> Path:
         obj = OBJ / (src.stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        # SMX_EXTRA_NVCC_FLAGS: tuning experiments only (e.g. -DSMX_PACKED_BK=32)
+        extra = os.environ.get("SMX_EXTRA_NVCC_FLAGS", "").split()
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)

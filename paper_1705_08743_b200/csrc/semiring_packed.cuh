@@ -23,17 +23,24 @@
 #pragma once
 #include "semiring_gemm.cuh"
 
+#ifndef SMX_PACKED_BK
+#define SMX_PACKED_BK 32
+#endif
+#ifndef SMX_PACKED_STAGES
+#define SMX_PACKED_STAGES 3
+#endif
+
 namespace smx {
 
 struct PackedU16 {
-    static constexpr int BM = 128, BNW = 64, BK = 16, TM = 4, TNW = 8, HW = 4;
+    static constexpr int BM = 128, BNW = 64, BK = SMX_PACKED_BK, TM = 4, TNW = 8, HW = 4;
     static constexpr int BN = 2 * BNW;                 // cells
     static constexpr int TCOLS = BNW / TNW;            // 8
     static constexpr int CONSUMERS = (BM / TM) * TCOLS;  // 256
     static constexpr int THREADS = CONSUMERS + 32;     // + producer warp
-    static constexpr int STAGES = 6;
-    static constexpr int A_TILE_WORDS = BK * BM;       // 2048 words = 8 KB
-    static constexpr int B_TILE_WORDS = BK * BNW;      // 1024 words = 4 KB
+    static constexpr int STAGES = SMX_PACKED_STAGES;
+    static constexpr int A_TILE_WORDS = BK * BM;       // 4096 words = 16 KB
+    static constexpr int B_TILE_WORDS = BK * BNW;      // 2048 words = 8 KB
     static constexpr size_t SMEM = (size_t)STAGES * (A_TILE_WORDS + B_TILE_WORDS) * 4 + BM * BN * 2 + 1024;
 };
 
@@ -52,74 +59,84 @@ struct PackedArgs {
 };
 
 // ---- pack kernels -----------------------------------------------------------
-// One CTA of 128 threads per A tile: thread r reads 16 cells of row r (two
-// 16-byte loads), writes 16 splat words down column r of the tile.
+// One CTA of 128 threads per A tile: thread r reads BK cells of row r (16-byte
+// loads), writes BK splat words down column r of the tile.
 __global__ void __launch_bounds__(128) pack_a_u16_kernel(const uint16_t* __restrict__ A, int M, int K,
                                                         long long lda, int anti, int KT,
                                                         uint32_t* __restrict__ Ap, uint8_t* __restrict__ fA,
                                                         const int* __restrict__ cert) {
     using L = Lane<uint16_t>;
+    constexpr int BK = PackedU16::BK;
     const int kt = blockIdx.x, mt = blockIdx.y, r = threadIdx.x;
-    const int row = mt * PackedU16::BM + r, k0 = kt * PackedU16::BK;
+    const int row = mt * PackedU16::BM + r, k0 = kt * BK;
     const uint32_t m = anti ? 0xFFFFu : 0u;
-    uint32_t v[16];
-    if (row < M && k0 + 16 <= K) {
-        const uint4* src = reinterpret_cast<const uint4*>(A + (long long)row * lda + k0);
-        const uint4 x = __ldg(src), y = __ldg(src + 1);
-        const uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+    const bool sh = cert != nullptr && *cert != 0;
+    uint32_t* dst = Ap + ((size_t)mt * KT + kt) * PackedU16::A_TILE_WORDS + r;
+    uint32_t hi = 0;
+#pragma unroll
+    for (int q = 0; q < BK / 8; ++q) {
+        const int kq = k0 + q * 8;
+        uint32_t v[8];
+        if (row < M && kq + 8 <= K) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(A + (long long)row * lda + kq));
+            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                v[2 * i] = (w[i] & 0xFFFFu) ^ m;
+                v[2 * i + 1] = (w[i] >> 16) ^ m;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                v[i] = (row < M && kq + i < K) ? ((uint32_t)A[(long long)row * lda + kq + i] ^ m) : L::kS;
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            v[2 * i] = (w[i] & 0xFFFFu) ^ m;
-            v[2 * i + 1] = (w[i] >> 16) ^ m;
+            hi |= v[i];
+            const uint32_t w = L::splat(v[i]);
+            dst[(q * 8 + i) * PackedU16::BM] = sh ? L::to_shifted(w) : w;
         }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-            v[i] = (row < M && k0 + i < K) ? ((uint32_t)A[(long long)row * lda + k0 + i] ^ m) : L::kS;
-    }
-    uint32_t hi = 0;
-    uint32_t* dst = Ap + ((size_t)mt * KT + kt) * PackedU16::A_TILE_WORDS + r;
-    const bool sh = cert != nullptr && *cert != 0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        hi |= v[i];
-        const uint32_t w = L::splat(v[i]);
-        dst[i * PackedU16::BM] = sh ? L::to_shifted(w) : w;
     }
     const int ok = __syncthreads_and((hi & 0x8000u) == 0u);
     if (r == 0) fA[(size_t)mt * KT + kt] = (uint8_t)ok;
 }
 
-// One CTA of 256 threads per B tile: thread t reads 8 cells (16 bytes) of
-// k-row t/16, chunk t%16, writes them as 4 canonical words.
+// One CTA of 256 threads per B tile: each 16-byte chunk (8 cells of one
+// k-row) becomes 4 canonical words; BK x 16 chunks per tile.
 __global__ void __launch_bounds__(256) pack_b_u16_kernel(const uint16_t* __restrict__ B, int K, int N,
                                                         long long ldb, int anti, int NT,
                                                         uint32_t* __restrict__ Bp, uint8_t* __restrict__ fB,
                                                         const int* __restrict__ cert) {
+    using L = Lane<uint16_t>;
+    constexpr int BK = PackedU16::BK;
     const int nt = blockIdx.x, kt = blockIdx.y, t = threadIdx.x;
-    const int kk = t >> 4, c = t & 15;
-    const int k = kt * PackedU16::BK + kk, col = nt * PackedU16::BN + c * 8;
     const uint32_t m = anti ? 0xFFFFFFFFu : 0u;
-    uint4 w = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-    if (k < K && col + 8 <= N) {
-        w = __ldg(reinterpret_cast<const uint4*>(B + (long long)k * ldb + col));
-        w.x ^= m; w.y ^= m; w.z ^= m; w.w ^= m;
-    } else if (k < K) {
-        uint32_t e[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-        for (int j = 0; j < 8; ++j) {
-            if (col + j >= N) break;
-            const uint32_t x = ((uint32_t)B[(long long)k * ldb + col + j] ^ m) & 0xFFFFu;
-            const int sh = (j & 1) * 16;
-            e[j >> 1] = (e[j >> 1] & ~(0xFFFFu << sh)) | (x << sh);
+    const bool sh = cert != nullptr && *cert != 0;
+    uint32_t hi = 0;
+#pragma unroll
+    for (int q = 0; q < BK * 16 / 256; ++q) {
+        const int ch = t + q * 256;
+        const int kk = ch >> 4, c = ch & 15;
+        const int k = kt * BK + kk, col = nt * PackedU16::BN + c * 8;
+        uint4 w = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        if (k < K && col + 8 <= N) {
+            w = __ldg(reinterpret_cast<const uint4*>(B + (long long)k * ldb + col));
+            w.x ^= m; w.y ^= m; w.z ^= m; w.w ^= m;
+        } else if (k < K) {
+            uint32_t e[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+            for (int j = 0; j < 8; ++j) {
+                if (col + j >= N) break;
+                const uint32_t x = ((uint32_t)B[(long long)k * ldb + col + j] ^ m) & 0xFFFFu;
+                const int s2 = (j & 1) * 16;
+                e[j >> 1] = (e[j >> 1] & ~(0xFFFFu << s2)) | (x << s2);
+            }
+            w = make_uint4(e[0], e[1], e[2], e[3]);
         }
-        w = make_uint4(e[0], e[1], e[2], e[3]);
+        hi |= (w.x | w.y | w.z | w.w) & 0x80008000u;
+        if (sh) w = make_uint4(L::to_shifted(w.x), L::to_shifted(w.y), L::to_shifted(w.z), L::to_shifted(w.w));
+        *reinterpret_cast<uint4*>(Bp + ((size_t)kt * NT + nt) * PackedU16::B_TILE_WORDS + kk * PackedU16::BNW +
+                                  c * 4) = w;
     }
-    const uint32_t hi = (w.x | w.y | w.z | w.w) & 0x80008000u;
-    if (cert != nullptr && *cert != 0) {
-        using L = Lane<uint16_t>;
-        w = make_uint4(L::to_shifted(w.x), L::to_shifted(w.y), L::to_shifted(w.z), L::to_shifted(w.w));
-    }
-    *reinterpret_cast<uint4*>(Bp + ((size_t)kt * NT + nt) * PackedU16::B_TILE_WORDS + kk * PackedU16::BNW + c * 4) = w;
     const int ok = __syncthreads_and(hi == 0u);
     if (t == 0) fB[(size_t)kt * NT + nt] = (uint8_t)ok;
 }
