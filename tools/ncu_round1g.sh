@@ -1,0 +1,5 @@
+set -x
+NCU=/usr/local/cuda/bin/ncu
+B32="python bench.py --steps 1 --warmup 1 --no-secondary --no-cpu"
+$B32 > gpurun_out/plain_b32.log 2>&1 && $NCU --set full --clock-control none --import-source on -k regex:packed_gemm -s 41 -c 1 -o gpurun_out/prof_fw32k_packed_3b $B32 > gpurun_out/ncu_b32full.log 2>&1
+ls -la gpurun_out | tail -3
