@@ -255,13 +255,17 @@ def run_ours(args, world, rank, local_rank):
         torch.cuda.synchronize()
 
     # ---- inputs (host generation, then HBM) --------------------------------
-    block = lib.smx_fw_block(cfg.width // 8)
+    if world > 1:
+        block = sharded.CudaFwOps.block_for(n, world, cfg.width)
+    else:   # the single-GPU closure's own choice (smx_fw_block_for)
+        block = lib.smx_fw_block_for(n, cfg.width // 8)
     if cfg.op == "closure":
+        ops = sharded.CudaFwOps(cfg.width, anti=True, block=block)
+        block = ops.block if world > 1 else block
         r0, r1 = sharded.row_range(n, world, rank, block) if world > 1 else (0, n)
         (host,) = workloads.make_inputs(cfg, n, rows=(r0, r1))
         src = torch.from_numpy(host).to(dev)
         work = torch.empty_like(src)
-        ops = sharded.CudaFwOps(cfg.width, anti=True)
         fw = sharded.ShardedFW(n=n, rank=rank, world=world, ops=ops)
         ws_bytes = lib.smx_fw_workspace_bytes(n, src.shape[1], cfg.width // 8)
         ws = _native.workspace(ws_bytes, dev)

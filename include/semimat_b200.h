@@ -131,6 +131,9 @@ int smx_fw_trace_read(float* ms, long long* cells, int cap);
  * multi-GPU driver (paper_1705_08743_b200/sharded.py).  elem_bytes in
  * {1,2,4}.  Pivot tile: b x b (b <= smx_fw_block(elem_bytes)), in place. */
 int smx_fw_block(int elem_bytes);
+/* The pivot block smx_fw_* uses for an n-vertex closure under the current
+ * smx_set_fw_block setting (<= smx_fw_block(elem_bytes)). */
+int smx_fw_block_for(int n, int elem_bytes);
 int smx_fw_pivot(void* P, int b, int ld, int elem_bytes, int kind, void* stream);
 /* C[rows, :] (+)= A (x) B over rows [0, M) except the row-tile range
  * [skip_row0, skip_row0 + skip_rows), which must be multiples of 128. */

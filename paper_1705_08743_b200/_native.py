@@ -29,6 +29,7 @@ _SIGS = {
     "smx_set_fw_side_lite": ([c_int], c_int),
     "smx_set_fw_block": ([c_int], c_int),
     "smx_set_fw_packed": ([c_int], c_int),
+    "smx_fw_block_for": ([c_int, c_int], c_int),
     "smx_fw_trace_arm": ([c_int], c_int),
     "smx_fw_trace_read": ([c_void_p, c_void_p, c_int], c_int),
     "smx_semiring_gemm_u8": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),

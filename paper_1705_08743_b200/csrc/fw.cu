@@ -609,6 +609,15 @@ int smx_semiring_gemm_skip(const void* A, const void* B, void* C, int M, int N, 
     }
 }
 
+int smx_fw_block_for(int n, int elem_bytes) {
+    switch (elem_bytes) {
+        case 1: return fw_block_for_n<uint8_t>(n);
+        case 2: return fw_block_for_n<uint16_t>(n);
+        case 4: return fw_block_for_n<uint32_t>(n);
+        default: return SMX_E_ARG;
+    }
+}
+
 int smx_set_fw_packed(int enable) {
     const int old = g_fw_packed;
     g_fw_packed = enable ? 1 : 0;

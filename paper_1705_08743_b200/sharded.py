@@ -52,14 +52,23 @@ class CudaFwOps:
     """Per-rank FW steps on the GPU through the C ABI (launched on torch's
     current stream, so callers control overlap with torch.cuda.stream)."""
 
-    def __init__(self, width: int, anti: bool):
+    def __init__(self, width: int, anti: bool, block: int | None = None):
         self.width = width
         self.eb = width // 8
         self.kind = _native.SMX_ANTI if anti else _native.SMX_DIST
-        # at most 256: row panels stay fine-grained across ranks, and the
-        # owner's pivot chain stays short against 1/P of a round's phase 3
-        self.block = min(_native.lib().smx_fw_block(self.eb), 256)
+        mx = _native.lib().smx_fw_block(self.eb)
+        # default 256: row panels stay fine-grained across ranks, and the
+        # owner's pivot chain stays short against 1/P of a round's phase 3;
+        # callers with >= 4096 rows per rank pass 512 (see block_for)
+        self.block = min(block or 256, mx)
         self._cp = None
+
+    @staticmethod
+    def block_for(n: int, world: int, width: int) -> int:
+        """Pivot block of the sharded closure: 512 (u16) once every rank holds
+        >= 4096 rows -- the owner's 512 chain then still hides behind its
+        rank's phase 3 -- else 256."""
+        return 512 if width == 16 and n // max(world, 1) >= 4096 else 256
 
     def _at(self, t: torch.Tensor, r: int, c: int) -> int:
         return t.data_ptr() + (r * t.shape[1] + c) * self.eb

@@ -296,8 +296,9 @@ def test_bool_tc_bytes_output_and_accumulate(oracle_lib):
 
 # -- row-panel-sharded closure: the GPU ops, ranks emulated in lockstep ----------
 
-@pytest.mark.parametrize("world,n", [(1, 1000), (2, 1000), (3, 1280), (8, 2048)])
-def test_sharded_fw_gpu_ops_lockstep(world, n, oracle_lib):
+@pytest.mark.parametrize("world,n,block", [(1, 1000, None), (2, 1000, None), (3, 1280, None), (8, 2048, None),
+                                           (2, 2100, 512), (3, 1536, 512)])
+def test_sharded_fw_gpu_ops_lockstep(world, n, block, oracle_lib):
     """ShardedFW with CudaFwOps for `world` ranks on one GPU, run round by round
     in one process (the broadcast becomes a device copy; no rank ever waits on
     another, so this is safe on a single GPU) -- bit-identical to the oracle."""
@@ -306,7 +307,7 @@ def test_sharded_fw_gpu_ops_lockstep(world, n, oracle_lib):
     (full,) = workloads.make_inputs(cfg, n)
     ranks = []
     for r in range(world):
-        ops = sharded.CudaFwOps(16, anti=True)
+        ops = sharded.CudaFwOps(16, anti=True, block=block)
         fw = sharded.ShardedFW(n=n, rank=r, world=world, ops=ops)
         ranks.append((fw, torch.from_numpy(full[fw.row0:fw.row1].copy()).cuda()))
     block = ranks[0][0].block
