@@ -51,9 +51,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", default="c5_fw_u16")
-    ap.add_argument("--n", type=int, default=None, help="override the config's n (testing)")
+    ap.add_argument("--n", "--size", dest="n", type=int, default=None,
+                    help="override the config's n (testing; --size under torchrun)")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--check", action="store_true",
+                    help="N > 1: compare the gathered sharded closure with the single-GPU one")
     return ap.parse_args()
 
 
@@ -241,10 +244,19 @@ def run_ours(args, world, rank, local_rank):
     import torch.distributed as dist
     from paper_1705_08743_b200 import AntidistMatrix, _native, engines, sharded, workloads
 
+    # SMX_BENCH_BACKEND=gloo: functional check of the multi-rank path with more
+    # ranks than GPUs (ranks share a device; gloo's host-side broadcast means no
+    # kernel ever waits on another rank).  Timings from such a run mean nothing.
+    backend = os.environ.get("SMX_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local_rank %= torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfg = workloads.CONFIGS[args.workload]
     n = args.n or cfg.n
     lib = _native.lib()
@@ -366,6 +378,19 @@ def run_ours(args, world, rank, local_rank):
         result["e2e"] = {"value": units_per_step / e2e_secs, "unit": UNIT,
                          "h2d_bytes_per_step": int(hb[0].item()), "d2h_bytes_per_step": int(hb[1].item()),
                          "ms_per_step": e2e_secs * 1e3, "note": "summed over ranks; max time over ranks"}
+        if args.check and cfg.op == "closure":
+            # the gathered sharded result against the single-GPU closure of the
+            # same input (bit-exact; the single-GPU path is oracle-checked)
+            torch.cuda.synchronize()
+            full = sharded.gather_rows(work, n, world, block)
+            if rank == 0:
+                (ref_host,) = workloads.make_inputs(cfg, n)
+                ref = torch.from_numpy(ref_host).to(dev)
+                rws = _native.workspace(lib.smx_fw_workspace_bytes(n, ref.shape[1], cfg.width // 8), dev)
+                _native.check(getattr(lib, f"smx_fw_u{cfg.width}")(
+                    ref.data_ptr(), n, ref.shape[1], _native.SMX_ANTI, rws.data_ptr(), rws.numel(),
+                    _native.stream_ptr(dev)), "fw")
+                result["parity_sharded"] = {"n": n, "bit_exact_vs_single_gpu": bool(torch.equal(full, ref))}
 
     # ---- parity of this very run at the oracle size (rank 0, N = 1) ------------
     if rank == 0 and world == 1:
