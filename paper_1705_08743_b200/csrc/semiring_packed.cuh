@@ -1,5 +1,6 @@
 // Warp-specialised u16 semiring GEMM over pre-packed operand tiles: the
-// Floyd-Warshall phase-3 kernel (antidist.py:390-398 / :440-448 via fw.cu).
+// Floyd-Warshall phase-3 kernel (antidist.py:390-398 / :440-448 via fw.cu)
+// and the large public u16 products (antidist.py:361-371 / :412-422).
 //
 // semiring_gemm_kernel (semiring_gemm.cuh) stages every k-tile through
 // registers: each thread loads 16-byte chunks from global, converts them to
@@ -9,17 +10,21 @@
 // stalls left.  Phase 3 reuses each operand tile across a whole row or column
 // of output tiles, so that per-tile conversion work is repeated 256 times.
 //
-// Here the conversion happens once per round, in two small pack kernels that
-// write each 128 x 16 A tile (splat words, [BK][BM]) and 16 x 128 B tile
-// (canonical words, [BK][BNW]) contiguously, together with a per-tile flag
-// "every lane < 2^15" -- the bounded test, decided once per tile instead of
-// voted per CTA.  The GEMM then runs one producer warp that streams tiles
-// with 1-D bulk async copies (cp.async.bulk + mbarrier complete_tx) into a
-// 4-stage ring, and 8 consumer warps that only wait, compute and arrive:
-// no staging registers, no global loads and no CTA barrier in the k-loop.
-// The consumer's inner loop is the same LDS.128 + VIADDMNMX.U16x2 sequence
-// (1 instruction per 2 cells on bounded tiles, 2 otherwise; S - a of the
-// general form is ~splat(a), 1 LOP per A value).
+// Here the conversion happens once per round (or once per product K-chunk),
+// in two small pack kernels that write each 128 x BK A tile (splat words,
+// [BK][BM]) and BK x 128 B tile (canonical words, [BK][BNW]) contiguously,
+// together with a per-tile flag "every lane < 2^15" -- the bounded test,
+// decided once per tile instead of voted per CTA.  Public products may
+// instead be packed in the product-wide shifted encoding (cert_u16_kernel).
+// The GEMM runs one producer warp that streams tiles with 1-D bulk async
+// copies (cp.async.bulk + mbarrier complete_tx) into a SMX_PACKED_STAGES ring
+// of SMX_PACKED_BK-deep k-tiles (3 x 32 by default: 24 KB stages), and 8
+// consumer warps that only wait, compute and arrive: no staging registers,
+// no global loads and no CTA barrier in the k-loop.  The consumer's inner
+// loop is the same LDS.128 + VIADDMNMX.U16x2 sequence (1 instruction per 2
+// cells on bounded tiles, 2 otherwise; S - a of the general form is
+// ~splat(a), 1 LOP per A value).  Measured: 95.9% ALU-pipe busy on a
+// phase-3 launch at n = 32768 (profiles/r01g_ncu_fw32768_packed_3b.txt).
 #pragma once
 #include "semiring_gemm.cuh"
 
