@@ -111,13 +111,13 @@ int smx_set_fw_side_lite(int enable);
  * (clamped to smx_fw_block: u8 256, u32 128).  Returns the previous setting
  * (or SMX_E_ARG). */
 int smx_set_fw_block(int block);
-/* Packed u16 kernel: 1 (default) = smx_fw_u16's phase 3, large
- * smx_semiring_gemm_u16 products (M*N >= 2^22, K >= 256) and large
- * smx_semiring_gemm_skip u16 updates pack their operands into canonical tiles
- * (with per-tile bounded flags, or the product-wide shifted encoding when a
- * certificate pass allows it) and run the warp-specialised bulk-copy kernel;
- * 0 = the register-staged kernel.  Results are identical.  Returns the
- * previous setting. */
+/* Packed u8/u16 kernel: 1 (default) = smx_fw_u8/u16's phase 3, large
+ * smx_semiring_gemm_u8/u16 products (M*N >= 2^22, K >= 256) and large
+ * smx_semiring_gemm_skip u8/u16 updates pack their operands into canonical
+ * tiles (with per-tile bounded flags, or for u16 products the product-wide
+ * shifted encoding when a certificate pass allows it) and run the
+ * warp-specialised bulk-copy kernel; 0 = the register-staged kernel.
+ * Results are identical.  Returns the previous setting. */
 int smx_set_fw_packed(int enable);
 
 /* Measurement hook: arm a CUDA-event trace of up to max_launches phase-3

@@ -333,7 +333,7 @@ inline size_t fw_ws_bytes(int n, long long ld, int eb) {
     // u16: the packed phase-3 operand tiles (semiring_packed.cuh)
     const size_t B = fw_block_for(eb);
     const size_t base = align256(B * ld * eb) + align256((size_t)n * B * eb);
-    return eb == 2 ? base + align256(packed_u16_ws_bytes(n, n, (int)B)) : base;
+    return eb <= 2 ? base + align256(packed_ws_bytes(n, n, (int)B)) : base;
 }
 
 // smx_set_fw_packed: u16 phase 3 on the warp-specialised packed-tile kernel
@@ -343,10 +343,10 @@ static int g_fw_packed = 1;
 template <typename T>
 int fw_phase3(const T* CP, long long ldcp, const T* rowK, T* Tm, int n, long long ld, int bb, int kind,
               int skip0, int skipn, void* pws, size_t pws_bytes, cudaStream_t s) {
-    if constexpr (std::is_same<T, uint16_t>::value) {
+    if constexpr (sizeof(T) <= 2) {
         if (g_fw_packed && pws != nullptr)
-            return semiring_gemm_packed_u16(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, skip0, skipn, pws,
-                                            pws_bytes, s);
+            return semiring_gemm_packed<T>(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, skip0, skipn, pws,
+                                           pws_bytes, s);
     }
     return semiring_gemm<T>(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, skip0, skipn, s);
 }
@@ -453,41 +453,42 @@ int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, void* p
 // pack A(r+1) reads rows K_{r+1} while the side stream may still rewrite
 // them, but only tiles of rows K_{r+2} (3a) and of rows outside K_{r+1} u
 // K_{r+2} (3b) are read in round r+1, as with the CP copy of fw_run_lookahead.
-inline int fw_run_lookahead_packed(uint16_t* Tm, int n, long long ld, int kind, uint16_t* RP, void* pws,
+template <typename T>
+int fw_run_lookahead_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws,
                                    size_t pws_bytes, cudaStream_t s) {
     SideStream* fs = nullptr;
     SMX_TRY(side_stream(&fs));
-    const int BLK = fw_block_for_n<uint16_t>(n);
+    const int BLK = fw_block_for_n<T>(n);
     const int R = (n + BLK - 1) / BLK;
     auto blk = [&](int r) { return n - r * BLK < BLK ? n - r * BLK : BLK; };
-    SMX_TRY(fw_pivot_and_row_panel<uint16_t>(Tm, n, ld, kind, RP, 0, blk(0), s));
-    SMX_TRY(packed_u16_pack(Tm, nullptr, n, n, blk(0), ld, ld, kind, pws, pws_bytes, s));
+    SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, 0, blk(0), s));
+    SMX_TRY(packed_pack<T>(Tm, nullptr, n, n, blk(0), ld, ld, kind, pws, pws_bytes, s));
     cudaError_t e;
     for (int r = 0; r < R; ++r) {
         const int k0 = r * BLK, bb = blk(r);
-        uint16_t* rowK = Tm + (long long)k0 * ld;
-        SMX_TRY(packed_u16_pack(nullptr, rowK, n, n, bb, ld, ld, kind, pws, pws_bytes, s));
+        T* rowK = Tm + (long long)k0 * ld;
+        SMX_TRY(packed_pack<T>(nullptr, rowK, n, n, bb, ld, ld, kind, pws, pws_bytes, s));
         if (r + 1 < R) {
             const int k1 = k0 + BLK, bb1 = blk(r + 1);
             // 3a: the next pivot block's rows first
-            SMX_TRY(packed_u16_run(Tm, n, n, bb, ld, kind, 1, k1 / PackedU16::BM, ceil_div(bb1, PackedU16::BM), 0,
+            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / PackedCfg<T>::BM, ceil_div(bb1, PackedCfg<T>::BM), 0,
                                    0, pws, pws_bytes, s));
             if ((e = cudaEventRecord(fs->fork, s)) != cudaSuccess) return (int)e;
             if ((e = cudaStreamWaitEvent(fs->side, fs->fork, 0)) != cudaSuccess) return (int)e;
             {
                 PriorityScope ps(fs->priority);
-                SMX_TRY(fw_pivot_and_row_panel<uint16_t>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
+                SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
             }
             if ((e = cudaEventRecord(fs->join, fs->side)) != cudaSuccess) return (int)e;
             // 3b: everything else (skips K_r and K_{r+1}, adjacent tiles)
             trace_begin(s, (long long)(n - bb - bb1) * n * bb);
-            SMX_TRY(packed_u16_run(Tm, n, n, bb, ld, kind, 1, 0, -1, k0, bb + bb1, pws, pws_bytes, s));
+            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, 0, -1, k0, bb + bb1, pws, pws_bytes, s));
             trace_end(s);
-            SMX_TRY(packed_u16_pack(Tm + k1, nullptr, n, n, bb1, ld, ld, kind, pws, pws_bytes, s));
+            SMX_TRY(packed_pack<T>(Tm + k1, nullptr, n, n, bb1, ld, ld, kind, pws, pws_bytes, s));
             if ((e = cudaStreamWaitEvent(s, fs->join, 0)) != cudaSuccess) return (int)e;
         } else {
             trace_begin(s, (long long)(n - bb) * n * bb);
-            SMX_TRY(packed_u16_run(Tm, n, n, bb, ld, kind, 1, 0, -1, k0, bb, pws, pws_bytes, s));
+            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, 0, -1, k0, bb, pws, pws_bytes, s));
             trace_end(s);
         }
     }
@@ -511,8 +512,8 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
                                  align256((size_t)FwBlock<T>::value * ld * sizeof(T)));
     const size_t pws_off = align256((size_t)FwBlock<T>::value * ld * sizeof(T)) +
                            align256((size_t)n * FwBlock<T>::value * sizeof(T));
-    void* pws = sizeof(T) == 2 ? reinterpret_cast<char*>(ws) + pws_off : nullptr;
-    const size_t pws_bytes = sizeof(T) == 2 ? ws_bytes - pws_off : 0;
+    void* pws = sizeof(T) <= 2 ? reinterpret_cast<char*>(ws) + pws_off : nullptr;
+    const size_t pws_bytes = sizeof(T) <= 2 ? ws_bytes - pws_off : 0;
     GraphKey key;
     key.fn = 100 + (int)sizeof(T);
     const unsigned long long kv[] = {(uintptr_t)Tm, (unsigned long long)n, (unsigned long long)ld,
@@ -523,9 +524,9 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     // the phase-3 trace records host-side state per launch: trace runs stay eager
     return run_graphed(key, s, g_trace.armed, [&](cudaStream_t st) -> int {
-        if constexpr (std::is_same<T, uint16_t>::value) {
+        if constexpr (sizeof(T) <= 2) {
             if (lookahead_enabled() && g_fw_packed && pws != nullptr)
-                return fw_run_lookahead_packed(Tm, n, ld, kind, RP, pws, pws_bytes, st);
+                return fw_run_lookahead_packed<T>(Tm, n, ld, kind, RP, pws, pws_bytes, st);
         }
         if (lookahead_enabled()) return fw_run_lookahead<T>(Tm, n, ld, kind, RP, CP, pws, pws_bytes, st);
         return fw_run_serial<T>(Tm, n, ld, kind, RP, CP, pws, pws_bytes, BLK, st);
@@ -554,6 +555,27 @@ int fw_run_serial(T* Tm, int n, long long ld, int kind, T* RP, T* CP, void* pws,
     return SMX_OK;
 }
 
+// Bulk row-panel updates of the sharded closure take the packed kernel, its
+// operand tiles in stream-ordered scratch.
+template <typename T>
+static int gemm_skip(const T* A, const T* B, T* C, int M, int N, int K, int lda, int ldb, int ldc, int kind,
+                     int skip_row0, int skip_rows, cudaStream_t s) {
+    if constexpr (sizeof(T) <= 2) {
+        if (g_fw_packed && (long long)M * N >= (1LL << 24) && K > 0 && aligned16(A) && aligned16(B) &&
+            aligned16(C)) {
+            const size_t bytes = packed_ws_bytes(M, N, K);
+            void* ws = nullptr;
+            if (scratch_alloc(&ws, bytes, s) == SMX_OK) {
+                const int rc = semiring_gemm_packed<T>(A, B, C, M, N, K, lda, ldb, ldc, kind, 1, skip_row0,
+                                                       skip_rows, ws, bytes, s);
+                scratch_free(ws, s);
+                return rc;
+            }
+        }
+    }
+    return semiring_gemm<T>(A, B, C, M, N, K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows, s);
+}
+
 }  // namespace smx
 
 using namespace smx;
@@ -562,6 +584,9 @@ extern "C" {
 
 int smx_semiring_gemm_u8(const uint8_t* A, const uint8_t* B, uint8_t* C, int M, int N, int K,
                          int lda, int ldb, int ldc, int kind, int accumulate, void* stream) {
+    if (g_fw_packed && (long long)M * N >= (1LL << 22) && K >= 256)
+        return semiring_gemm_packed_public<uint8_t>(A, B, C, M, N, K, lda, ldb, ldc, kind, accumulate,
+                                                    as_stream(stream));
     return semiring_gemm<uint8_t>(A, B, C, M, N, K, lda, ldb, ldc, kind, accumulate, 0, 0,
                                   as_stream(stream));
 }
@@ -584,27 +609,12 @@ int smx_semiring_gemm_skip(const void* A, const void* B, void* C, int M, int N, 
                            int skip_rows, void* stream) {
     cudaStream_t s = as_stream(stream);
     switch (elem_bytes) {
-        case 1: return semiring_gemm<uint8_t>((const uint8_t*)A, (const uint8_t*)B, (uint8_t*)C, M, N,
-                                              K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows, s);
-        case 2:
-            // bulk row-panel updates of the sharded closure: the packed phase-3
-            // kernel, its operand tiles in stream-ordered scratch
-            if (g_fw_packed && (long long)M * N >= (1LL << 24) && K > 0 && aligned16(A) && aligned16(B) &&
-                aligned16(C)) {
-                const size_t bytes = packed_u16_ws_bytes(M, N, K);
-                void* ws = nullptr;
-                if (scratch_alloc(&ws, bytes, s) == SMX_OK) {
-                    const int rc = semiring_gemm_packed_u16((const uint16_t*)A, (const uint16_t*)B, (uint16_t*)C,
-                                                            M, N, K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows,
-                                                            ws, bytes, s);
-                    scratch_free(ws, s);
-                    return rc;
-                }
-            }
-            return semiring_gemm<uint16_t>((const uint16_t*)A, (const uint16_t*)B, (uint16_t*)C, M,
-                                           N, K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows, s);
-        case 4: return semiring_gemm<uint32_t>((const uint32_t*)A, (const uint32_t*)B, (uint32_t*)C, M,
-                                               N, K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows, s);
+        case 1: return gemm_skip<uint8_t>((const uint8_t*)A, (const uint8_t*)B, (uint8_t*)C, M, N, K, lda, ldb,
+                                          ldc, kind, skip_row0, skip_rows, s);
+        case 2: return gemm_skip<uint16_t>((const uint16_t*)A, (const uint16_t*)B, (uint16_t*)C, M, N, K, lda, ldb,
+                                           ldc, kind, skip_row0, skip_rows, s);
+        case 4: return gemm_skip<uint32_t>((const uint32_t*)A, (const uint32_t*)B, (uint32_t*)C, M, N, K, lda,
+                                           ldb, ldc, kind, skip_row0, skip_rows, s);
         default: return SMX_E_ARG;
     }
 }

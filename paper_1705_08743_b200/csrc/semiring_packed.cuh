@@ -37,7 +37,11 @@
 
 namespace smx {
 
-struct PackedU16 {
+// T = uint16_t, or uint8_t widened to u16 lanes (Lane<uint8_t>: a + b <= 510
+// cannot wrap and C starts <= 255, so every u8 tile takes the 1-instruction
+// update).  The packed tiles hold the same u16x2 lane words for both.
+template <typename T>
+struct PackedCfg {
     static constexpr int BM = 128, BNW = 64, BK = SMX_PACKED_BK, TM = 4, TNW = 8, HW = 4;
     static constexpr int BN = 2 * BNW;                 // cells
     static constexpr int TCOLS = BNW / TNW;            // 8
@@ -46,15 +50,18 @@ struct PackedU16 {
     static constexpr int STAGES = SMX_PACKED_STAGES;
     static constexpr int A_TILE_WORDS = BK * BM;       // 4096 words = 16 KB
     static constexpr int B_TILE_WORDS = BK * BNW;      // 2048 words = 8 KB
-    static constexpr size_t SMEM = (size_t)STAGES * (A_TILE_WORDS + B_TILE_WORDS) * 4 + BM * BN * 2 + 1024;
+    static constexpr int C_TILE_BYTES = BM * BN * (int)sizeof(T);
+    static constexpr size_t SMEM = (size_t)STAGES * (A_TILE_WORDS + B_TILE_WORDS) * 4 + C_TILE_BYTES + 1024;
 };
+using PackedU16 = PackedCfg<uint16_t>;
 
-struct PackedArgs {
+template <typename T>
+struct PackedArgsT {
     const uint32_t* Ap;    // [MT][KT][BK][BM] splat(canonical a)
     const uint32_t* Bp;    // [KT][NT][BK][BNW] canonical words
     const uint8_t* fA;     // [MT][KT]
     const uint8_t* fB;     // [KT][NT]
-    uint16_t* C;
+    T* C;
     int M, N, KT, NT;
     long long ldc;
     int anti, accumulate, allow_bounded;
@@ -64,83 +71,97 @@ struct PackedArgs {
 };
 
 // ---- pack kernels -----------------------------------------------------------
+// Canonical (distance-form) lane value of one storage cell.
+template <typename T>
+__device__ __forceinline__ uint32_t canon_cell(T x, int anti) {
+    return anti ? (Lane<T>::kS - (uint32_t)x) : (uint32_t)x;
+}
+
 // One CTA of 128 threads per A tile: thread r reads BK cells of row r (16-byte
 // loads), writes BK splat words down column r of the tile.
-__global__ void __launch_bounds__(128) pack_a_u16_kernel(const uint16_t* __restrict__ A, int M, int K,
-                                                        long long lda, int anti, int KT,
-                                                        uint32_t* __restrict__ Ap, uint8_t* __restrict__ fA,
-                                                        const int* __restrict__ cert) {
-    using L = Lane<uint16_t>;
-    constexpr int BK = PackedU16::BK;
+template <typename T>
+__global__ void __launch_bounds__(128) pack_a_kernel(const T* __restrict__ A, int M, int K, long long lda,
+                                                    int anti, int KT, uint32_t* __restrict__ Ap,
+                                                    uint8_t* __restrict__ fA, const int* __restrict__ cert) {
+    using L = Lane<T>;
+    using G = PackedCfg<T>;
+    constexpr int BK = G::BK, E = L::kCellsPerChunk, WPC = L::kWordsPerChunk;
     const int kt = blockIdx.x, mt = blockIdx.y, r = threadIdx.x;
-    const int row = mt * PackedU16::BM + r, k0 = kt * BK;
-    const uint32_t m = anti ? 0xFFFFu : 0u;
+    const int row = mt * G::BM + r, k0 = kt * BK;
     const bool sh = cert != nullptr && *cert != 0;
-    uint32_t* dst = Ap + ((size_t)mt * KT + kt) * PackedU16::A_TILE_WORDS + r;
+    uint32_t* dst = Ap + ((size_t)mt * KT + kt) * G::A_TILE_WORDS + r;
     uint32_t hi = 0;
 #pragma unroll
-    for (int q = 0; q < BK / 8; ++q) {
-        const int kq = k0 + q * 8;
-        uint32_t v[8];
-        if (row < M && kq + 8 <= K) {
-            const uint4 x = __ldg(reinterpret_cast<const uint4*>(A + (long long)row * lda + kq));
-            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                v[2 * i] = (w[i] & 0xFFFFu) ^ m;
-                v[2 * i + 1] = (w[i] >> 16) ^ m;
-            }
+    for (int q = 0; q < BK / E; ++q) {
+        const int kq = k0 + q * E;
+        uint32_t w[WPC];
+        if (row < M && kq + E <= K) {
+            chunk_to_words<T>(__ldg(reinterpret_cast<const uint4*>(A + (long long)row * lda + kq)), anti != 0, w);
         } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                v[i] = (row < M && kq + i < K) ? ((uint32_t)A[(long long)row * lda + kq + i] ^ m) : L::kS;
+            for (int i = 0; i < WPC; ++i) w[i] = L::kIdentityWord;
+            for (int j = 0; j < E; ++j) {
+                if (row >= M || kq + j >= K) break;
+                const uint32_t v = canon_cell<T>(A[(long long)row * lda + kq + j], anti);
+                const int s2 = (j & 1) * 16;
+                w[j >> 1] = (w[j >> 1] & ~(0xFFFFu << s2)) | (v << s2);
+            }
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            hi |= v[i];
-            const uint32_t w = L::splat(v[i]);
-            dst[(q * 8 + i) * PackedU16::BM] = sh ? L::to_shifted(w) : w;
+        for (int j = 0; j < E; ++j) {
+            const uint32_t v = word_cell<T>(w, j);
+            hi |= v;
+            const uint32_t sw = L::splat(v);
+            dst[(q * E + j) * G::BM] = sh ? L::to_shifted(sw) : sw;
         }
     }
-    const int ok = __syncthreads_and((hi & 0x8000u) == 0u);
+    const int ok = __syncthreads_and((hi & (L::kHalfMask & 0xFFFFu)) == 0u);
     if (r == 0) fA[(size_t)mt * KT + kt] = (uint8_t)ok;
 }
 
-// One CTA of 256 threads per B tile: each 16-byte chunk (8 cells of one
-// k-row) becomes 4 canonical words; BK x 16 chunks per tile.
-__global__ void __launch_bounds__(256) pack_b_u16_kernel(const uint16_t* __restrict__ B, int K, int N,
-                                                        long long ldb, int anti, int NT,
-                                                        uint32_t* __restrict__ Bp, uint8_t* __restrict__ fB,
-                                                        const int* __restrict__ cert) {
-    using L = Lane<uint16_t>;
-    constexpr int BK = PackedU16::BK;
+// One CTA of 256 threads per B tile: each 16-byte chunk of a k-row becomes
+// WPC canonical words; a k-row of the tile is 64 words.
+template <typename T>
+__global__ void __launch_bounds__(256) pack_b_kernel(const T* __restrict__ B, int K, int N, long long ldb,
+                                                    int anti, int NT, uint32_t* __restrict__ Bp,
+                                                    uint8_t* __restrict__ fB, const int* __restrict__ cert) {
+    using L = Lane<T>;
+    using G = PackedCfg<T>;
+    constexpr int BK = G::BK, E = L::kCellsPerChunk, WPC = L::kWordsPerChunk;
+    constexpr int CPR = G::BN / E;   // chunks per k-row
     const int nt = blockIdx.x, kt = blockIdx.y, t = threadIdx.x;
-    const uint32_t m = anti ? 0xFFFFFFFFu : 0u;
     const bool sh = cert != nullptr && *cert != 0;
     uint32_t hi = 0;
 #pragma unroll
-    for (int q = 0; q < BK * 16 / 256; ++q) {
+    for (int q = 0; q < (BK * CPR + 255) / 256; ++q) {
         const int ch = t + q * 256;
-        const int kk = ch >> 4, c = ch & 15;
-        const int k = kt * BK + kk, col = nt * PackedU16::BN + c * 8;
-        uint4 w = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        if (k < K && col + 8 <= N) {
-            w = __ldg(reinterpret_cast<const uint4*>(B + (long long)k * ldb + col));
-            w.x ^= m; w.y ^= m; w.z ^= m; w.w ^= m;
-        } else if (k < K) {
-            uint32_t e[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-            for (int j = 0; j < 8; ++j) {
-                if (col + j >= N) break;
-                const uint32_t x = ((uint32_t)B[(long long)k * ldb + col + j] ^ m) & 0xFFFFu;
+        if (ch >= BK * CPR) break;
+        const int kk = ch / CPR, c = ch % CPR;
+        const int k = kt * BK + kk, col = nt * G::BN + c * E;
+        uint32_t w[WPC];
+        if (k < K && col + E <= N) {
+            chunk_to_words<T>(__ldg(reinterpret_cast<const uint4*>(B + (long long)k * ldb + col)), anti != 0, w);
+        } else {
+#pragma unroll
+            for (int i = 0; i < WPC; ++i) w[i] = L::kIdentityWord;
+            for (int j = 0; j < E; ++j) {
+                if (k >= K || col + j >= N) break;
+                const uint32_t v = canon_cell<T>(B[(long long)k * ldb + col + j], anti);
                 const int s2 = (j & 1) * 16;
-                e[j >> 1] = (e[j >> 1] & ~(0xFFFFu << s2)) | (x << s2);
+                w[j >> 1] = (w[j >> 1] & ~(0xFFFFu << s2)) | (v << s2);
             }
-            w = make_uint4(e[0], e[1], e[2], e[3]);
         }
-        hi |= (w.x | w.y | w.z | w.w) & 0x80008000u;
-        if (sh) w = make_uint4(L::to_shifted(w.x), L::to_shifted(w.y), L::to_shifted(w.z), L::to_shifted(w.w));
-        *reinterpret_cast<uint4*>(Bp + ((size_t)kt * NT + nt) * PackedU16::B_TILE_WORDS + kk * PackedU16::BNW +
-                                  c * 4) = w;
+        uint32_t* dst = Bp + ((size_t)kt * NT + nt) * G::B_TILE_WORDS + kk * G::BNW + c * WPC;
+#pragma unroll
+        for (int i = 0; i < WPC; i += 4) {
+            uint32_t o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                hi |= w[i + j] & L::kHalfMask;
+                o[j] = sh ? L::to_shifted(w[i + j]) : w[i + j];
+            }
+            *reinterpret_cast<uint4*>(dst + i) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
     }
     const int ok = __syncthreads_and(hi == 0u);
     if (t == 0) fB[(size_t)kt * NT + nt] = (uint8_t)ok;
@@ -187,16 +208,17 @@ __device__ __forceinline__ void pk_bulk_load(void* dst, const void* src, uint32_
 // result is bit-identical).  The producer prefetches an interior C tile into
 // shared memory with row bulk copies while the K loop runs, so neither the C
 // read latency nor the operand-flag reads sit on a warp's critical path.
-__global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(const PackedArgs p) {
-    using L = Lane<uint16_t>;
-    using G = PackedU16;
+template <typename T>
+__global__ void __launch_bounds__(PackedCfg<T>::THREADS, 2) packed_gemm_kernel(const PackedArgsT<T> p) {
+    using L = Lane<T>;
+    using G = PackedCfg<T>;
     constexpr int BM = G::BM, BNW = G::BNW, BK = G::BK, TM = G::TM, TNW = G::TNW, HW = G::HW;
     constexpr int ST = G::STAGES;
 
     extern __shared__ __align__(128) uint4 smem_raw[];
     uint32_t* As = reinterpret_cast<uint32_t*>(smem_raw);              // [ST][BK][BM]
     uint32_t* Bs = As + ST * G::A_TILE_WORDS;                          // [ST][BK][BNW]
-    uint16_t* Cs = reinterpret_cast<uint16_t*>(Bs + ST * G::B_TILE_WORDS);   // [BM][BN] (raw C)
+    T* Cs = reinterpret_cast<T*>(Bs + ST * G::B_TILE_WORDS);   // [BM][BN] (raw C)
     uint64_t* full = reinterpret_cast<uint64_t*>(Cs + BM * G::BN);
     uint64_t* empty = full + ST;
     uint64_t* cbar = empty + ST;
@@ -238,9 +260,10 @@ __global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(
         for (int kb = 0; kb < KT; kb += 32) {
             // bounded flags of 32 k-tiles in one round trip (one per lane)
             const int k = kb + lane;
-            const bool f = k < KT && p.allow_bounded &&
+            // (u8: always -- its update is the 1-instruction form)
+            const bool f = k < KT && (L::kOneInstr || (p.allow_bounded &&
                            ((p.cert != nullptr && *p.cert != 0) ||
-                            (p.fA[(size_t)mt * KT + k] != 0 && p.fB[(size_t)k * p.NT + nt] != 0));
+                            (p.fA[(size_t)mt * KT + k] != 0 && p.fB[(size_t)k * p.NT + nt] != 0))));
             const uint32_t fmask = __ballot_sync(0xFFFFFFFFu, f);
             if (lane == 0) {
                 const int kend = KT - kb < 32 ? KT : kb + 32;
@@ -253,10 +276,10 @@ __global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(
                     // the C tile goes behind the first ring fill, so the
                     // first operand tiles arrive first
                     if (c_async && kt == first - 1) {
-                        pk_mbar_expect_tx(cbar, BM * G::BN * 2);
+                        pk_mbar_expect_tx(cbar, G::C_TILE_BYTES);
                         for (int r = 0; r < BM; ++r)
-                            pk_bulk_load(Cs + r * G::BN, p.C + (long long)(row0 + r) * p.ldc + col0, G::BN * 2,
-                                         cbar);
+                            pk_bulk_load(Cs + r * G::BN, p.C + (long long)(row0 + r) * p.ldc + col0,
+                                         G::BN * (int)sizeof(T), cbar);
                     }
                 }
             }
@@ -303,7 +326,7 @@ __global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(
                 const uint32_t a[TM] = {av.x, av.y, av.z, av.w};
 #pragma unroll
                 for (int i = 0; i < TM; ++i) {
-                    const uint32_t sa = ~a[i];   // splat(S - a): S = 0xFFFF per lane
+                    const uint32_t sa = ~a[i];   // u16: splat(S - a), S = 0xFFFF per lane (u8: unused)
 #pragma unroll
                     for (int j = 0; j < TNW; ++j) acc[i][j] = L::step(acc[i][j], b[j], a[i], sa);
                 }
@@ -314,47 +337,47 @@ __global__ void __launch_bounds__(PackedU16::THREADS, 2) packed_gemm_u16_kernel(
     }
 
     // ---- fold C in and store ----
-    if (p.cert != nullptr && *p.cert != 0) {
+    if constexpr (!L::kOneInstr) {
+        if (p.cert != nullptr && *p.cert != 0) {
 #pragma unroll
-        for (int i = 0; i < TM; ++i)
+            for (int i = 0; i < TM; ++i)
 #pragma unroll
-            for (int j = 0; j < TNW; ++j) acc[i][j] = L::from_shifted(acc[i][j]);
+                for (int j = 0; j < TNW; ++j) acc[i][j] = L::from_shifted(acc[i][j]);
+        }
     }
-    const uint32_t cm = anti ? 0xFFFFFFFFu : 0u;
     if (c_async) pk_mbar_wait(cbar, 0);
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
         const int grow = row0 + tr * TM + i;
         if (grow >= p.M) continue;
-        uint16_t* crow = p.C + (long long)grow * p.ldc;
+        T* crow = p.C + (long long)grow * p.ldc;
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
             const int cc = (g * (BNW / 2) + tc * HW) * 2;   // cell offset in the tile
             uint32_t* w = &acc[i][g * HW];
-            if (c_async) {
-                const uint4 v = *reinterpret_cast<const uint4*>(Cs + (tr * TM + i) * G::BN + cc);
-                w[0] = __vminu2(w[0], v.x ^ cm); w[1] = __vminu2(w[1], v.y ^ cm);
-                w[2] = __vminu2(w[2], v.z ^ cm); w[3] = __vminu2(w[3], v.w ^ cm);
-            } else if (p.accumulate) {
+            if (c_async || p.accumulate) {
                 uint32_t c[HW];
-                load_c_group<uint16_t, HW>(crow, col0 + cc, p.N, anti, c);
+                if (c_async) load_c_group<T, HW>(Cs + (tr * TM + i) * G::BN, cc, G::BN, anti, c);
+                else load_c_group<T, HW>(crow, col0 + cc, p.N, anti, c);
 #pragma unroll
                 for (int j = 0; j < HW; ++j) w[j] = __vminu2(w[j], c[j]);
             }
-            store_c_group<uint16_t, HW>(crow, col0 + cc, p.N, anti, w);
+            store_c_group<T, HW>(crow, col0 + cc, p.N, anti, w);
         }
     }
 }
 
-// Workspace for one packed product of M x K by K x N (A tiles, B tiles, flags).
-inline size_t packed_u16_ws_bytes(int M, int N, int K) {
-    const size_t MT = ceil_div(M, PackedU16::BM), NT = ceil_div(N, PackedU16::BN), KT = ceil_div(K, PackedU16::BK);
+// Workspace for one packed product of M x K by K x N (A tiles, B tiles, flags;
+// the same for u8 and u16: both pack u16x2 lane words).
+inline size_t packed_ws_bytes(int M, int N, int K) {
+    using G = PackedU16;
+    const size_t MT = ceil_div(M, G::BM), NT = ceil_div(N, G::BN), KT = ceil_div(K, G::BK);
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-    return al(MT * KT * PackedU16::A_TILE_WORDS * 4) + al(KT * NT * PackedU16::B_TILE_WORDS * 4) + al(MT * KT) +
-           al(KT * NT);
+    return al(MT * KT * G::A_TILE_WORDS * 4) + al(KT * NT * G::B_TILE_WORDS * 4) + al(MT * KT) + al(KT * NT);
 }
+inline size_t packed_u16_ws_bytes(int M, int N, int K) { return packed_ws_bytes(M, N, K); }
 
-// Views of a packed workspace laid out by packed_u16_ws_bytes(M, N, K).
+// Views of a packed workspace laid out by packed_ws_bytes(M, N, K).
 struct PackedWs {
     uint32_t* Ap;
     uint32_t* Bp;
@@ -380,29 +403,31 @@ inline PackedWs packed_views(void* ws, int M, int N, int K) {
     return v;
 }
 
+template <typename T>
 inline int packed_check(const void* A, const void* B, int M, int N, int K, long long lda, long long ldb, int kind,
                         void* ws, size_t ws_bytes) {
     if (M < 0 || N < 0 || K < 0 || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
     if ((A && !aligned16(A)) || (B && !aligned16(B))) return SMX_E_ALIGN;
-    if (!ld_ok(lda, 2) || !ld_ok(ldb, 2)) return SMX_E_ALIGN;
+    if (!ld_ok(lda, sizeof(T)) || !ld_ok(ldb, sizeof(T))) return SMX_E_ALIGN;
     if (lda < K || ldb < N) return SMX_E_ARG;
-    if (ws == nullptr || ws_bytes < packed_u16_ws_bytes(M, N, K)) return SMX_E_WORKSPACE;
+    if (ws == nullptr || ws_bytes < packed_ws_bytes(M, N, K)) return SMX_E_WORKSPACE;
     return SMX_OK;
 }
 
 // Pack A (M x K; A == nullptr skips it) and/or B (K x N; B == nullptr skips).
-inline int packed_u16_pack(const uint16_t* A, const uint16_t* B, int M, int N, int K, long long lda, long long ldb,
-                           int kind, void* ws, size_t ws_bytes, cudaStream_t s, const int* cert = nullptr) {
-    SMX_TRY(packed_check(A, B, M, N, K, lda, ldb, kind, ws, ws_bytes));
+template <typename T>
+inline int packed_pack(const T* A, const T* B, int M, int N, int K, long long lda, long long ldb, int kind, void* ws,
+                       size_t ws_bytes, cudaStream_t s, const int* cert = nullptr) {
+    SMX_TRY(packed_check<T>(A, B, M, N, K, lda, ldb, kind, ws, ws_bytes));
     if (M == 0 || N == 0 || K == 0) return SMX_OK;
     const PackedWs v = packed_views(ws, M, N, K);
     const int anti = kind == SMX_ANTI;
     if (A) {
-        pack_a_u16_kernel<<<dim3(v.KT, v.MT), 128, 0, s>>>(A, M, K, lda, anti, v.KT, v.Ap, v.fA, cert);
+        pack_a_kernel<T><<<dim3(v.KT, v.MT), 128, 0, s>>>(A, M, K, lda, anti, v.KT, v.Ap, v.fA, cert);
         SMX_LAUNCHED_OR_RETURN();
     }
     if (B) {
-        pack_b_u16_kernel<<<dim3(v.NT, v.KT), 256, 0, s>>>(B, K, N, ldb, anti, v.NT, v.Bp, v.fB, cert);
+        pack_b_kernel<T><<<dim3(v.NT, v.KT), 256, 0, s>>>(B, K, N, ldb, anti, v.NT, v.Bp, v.fB, cert);
         SMX_LAUNCHED_OR_RETURN();
     }
     return SMX_OK;
@@ -411,20 +436,21 @@ inline int packed_u16_pack(const uint16_t* A, const uint16_t* B, int M, int N, i
 // C rows (+)= packed A (x) packed B over the 128-row tiles
 // [row_tile0, row_tile0 + row_tiles) minus the rows [skip_row0, skip_row0 +
 // skip_rows) (whole tiles, inside the window).  row_tiles < 0: to the end.
-inline int packed_u16_run(uint16_t* C, int M, int N, int K, long long ldc, int kind, int accumulate, int row_tile0,
-                          int row_tiles, int skip_row0, int skip_rows, void* ws, size_t ws_bytes, cudaStream_t s,
-                          const int* cert = nullptr) {
-    using G = PackedU16;
+template <typename T>
+inline int packed_run(T* C, int M, int N, int K, long long ldc, int kind, int accumulate, int row_tile0,
+                      int row_tiles, int skip_row0, int skip_rows, void* ws, size_t ws_bytes, cudaStream_t s,
+                      const int* cert = nullptr) {
+    using G = PackedCfg<T>;
     if (M < 0 || N < 0 || K < 0 || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
     if (M == 0 || N == 0) return SMX_OK;
-    if (!aligned16(C) || !ld_ok(ldc, 2)) return SMX_E_ALIGN;
+    if (!aligned16(C) || !ld_ok(ldc, sizeof(T))) return SMX_E_ALIGN;
     if (ldc < N) return SMX_E_ARG;
-    if (ws == nullptr || ws_bytes < packed_u16_ws_bytes(M, N, K)) return SMX_E_WORKSPACE;
+    if (ws == nullptr || ws_bytes < packed_ws_bytes(M, N, K)) return SMX_E_WORKSPACE;
     const PackedWs v = packed_views(ws, M, N, K);
     if (row_tile0 < 0 || row_tile0 > v.MT) return SMX_E_ARG;
     if (row_tiles < 0 || row_tile0 + row_tiles > v.MT) row_tiles = v.MT - row_tile0;
-    PackedArgs a{v.Ap, v.Bp, v.fA, v.fB, C, M, N, v.KT, v.NT, ldc, kind == SMX_ANTI, accumulate != 0,
-                 bounded_fastpath_enabled(), row_tile0, v.MT, 0, cert};
+    PackedArgsT<T> a{v.Ap, v.Bp, v.fA, v.fB, C, M, N, v.KT, v.NT, ldc, kind == SMX_ANTI, accumulate != 0,
+                     bounded_fastpath_enabled(), row_tile0, v.MT, 0, cert};
     if (skip_rows > 0) {
         if (skip_row0 % G::BM) return SMX_E_ARG;
         a.skip_tile0 = skip_row0 / G::BM;
@@ -434,26 +460,45 @@ inline int packed_u16_run(uint16_t* C, int M, int N, int K, long long ldc, int k
     }
     const int mtiles = row_tiles - a.skip_tiles;
     if (mtiles <= 0) return SMX_OK;
-    static bool configured = false;
+    static bool configured = false;   // per instantiation
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(packed_gemm_u16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(packed_gemm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)G::SMEM);
         if (e != cudaSuccess) return (int)e;
         configured = true;
     }
-    packed_gemm_u16_kernel<<<dim3(v.NT, mtiles), G::THREADS, G::SMEM, s>>>(a);
+    packed_gemm_kernel<T><<<dim3(v.NT, mtiles), G::THREADS, G::SMEM, s>>>(a);
     SMX_RETURN_LAUNCH();
 }
 
-// C (+)= A (x) B, u16, rows [skip_row0, skip_row0 + skip_rows) left untouched
-// (whole 128-row tiles).  ws: packed_u16_ws_bytes(M, N, K).
+// C (+)= A (x) B, rows [skip_row0, skip_row0 + skip_rows) left untouched
+// (whole 128-row tiles).  ws: packed_ws_bytes(M, N, K).
+template <typename T>
+inline int semiring_gemm_packed(const T* A, const T* B, T* C, int M, int N, int K, long long lda, long long ldb,
+                                long long ldc, int kind, int accumulate, int skip_row0, int skip_rows, void* ws,
+                                size_t ws_bytes, cudaStream_t s) {
+    if (A == nullptr || B == nullptr) return SMX_E_ARG;
+    if (M == 0 || N == 0) return SMX_OK;
+    SMX_TRY(packed_pack<T>(A, B, M, N, K, lda, ldb, kind, ws, ws_bytes, s));
+    return packed_run<T>(C, M, N, K, ldc, kind, accumulate, 0, -1, skip_row0, skip_rows, ws, ws_bytes, s);
+}
+
+// u16 spellings used by fw.cu
+inline int packed_u16_pack(const uint16_t* A, const uint16_t* B, int M, int N, int K, long long lda, long long ldb,
+                           int kind, void* ws, size_t ws_bytes, cudaStream_t s, const int* cert = nullptr) {
+    return packed_pack<uint16_t>(A, B, M, N, K, lda, ldb, kind, ws, ws_bytes, s, cert);
+}
+inline int packed_u16_run(uint16_t* C, int M, int N, int K, long long ldc, int kind, int accumulate, int row_tile0,
+                          int row_tiles, int skip_row0, int skip_rows, void* ws, size_t ws_bytes, cudaStream_t s,
+                          const int* cert = nullptr) {
+    return packed_run<uint16_t>(C, M, N, K, ldc, kind, accumulate, row_tile0, row_tiles, skip_row0, skip_rows, ws,
+                                ws_bytes, s, cert);
+}
 inline int semiring_gemm_packed_u16(const uint16_t* A, const uint16_t* B, uint16_t* C, int M, int N, int K,
                                     long long lda, long long ldb, long long ldc, int kind, int accumulate,
                                     int skip_row0, int skip_rows, void* ws, size_t ws_bytes, cudaStream_t s) {
-    if (A == nullptr || B == nullptr) return SMX_E_ARG;
-    if (M == 0 || N == 0) return SMX_OK;
-    SMX_TRY(packed_u16_pack(A, B, M, N, K, lda, ldb, kind, ws, ws_bytes, s));
-    return packed_u16_run(C, M, N, K, ldc, kind, accumulate, 0, -1, skip_row0, skip_rows, ws, ws_bytes, s);
+    return semiring_gemm_packed<uint16_t>(A, B, C, M, N, K, lda, ldb, ldc, kind, accumulate, skip_row0, skip_rows,
+                                          ws, ws_bytes, s);
 }
 
 // Global sparse-bounded certificate of a u16 operand (rows x cols, ld): clears
@@ -487,20 +532,20 @@ __global__ void cert_u16_kernel(const uint16_t* __restrict__ X, int rows, int co
 // packed in the shifted 1-instruction encoding (semiring.cuh, Lane<uint16_t>):
 // then every k-tile runs VIADDMNMX alone, and results map back to S before C
 // is folded in.  Otherwise tiles use the per-tile bounded flags.
-inline int semiring_gemm_packed_public_u16(const uint16_t* A, const uint16_t* B, uint16_t* C, int M, int N, int K,
-                                           long long lda, long long ldb, long long ldc, int kind, int accumulate,
-                                           cudaStream_t s) {
-    using G = PackedU16;
+template <typename T>
+inline int semiring_gemm_packed_public(const T* A, const T* B, T* C, int M, int N, int K, long long lda,
+                                       long long ldb, long long ldc, int kind, int accumulate, cudaStream_t s) {
+    using G = PackedCfg<T>;
     if (M < 0 || N < 0 || K < 0 || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
     if (M == 0 || N == 0) return SMX_OK;
     if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return SMX_E_ALIGN;
-    if (!ld_ok(lda, 2) || !ld_ok(ldb, 2) || !ld_ok(ldc, 2)) return SMX_E_ALIGN;
+    if (!ld_ok(lda, sizeof(T)) || !ld_ok(ldb, sizeof(T)) || !ld_ok(ldc, sizeof(T))) return SMX_E_ALIGN;
     if (lda < K || ldb < N || ldc < N) return SMX_E_ARG;
     long long kc = (384LL << 20) / ((long long)G::BM * ceil_div(M, G::BM) * 4 + (long long)G::BN * ceil_div(N, G::BN) * 2);
     kc = kc / 256 * 256;
     if (kc < 256) kc = 256;
     if (kc > K) kc = K;
-    const size_t ws_bytes = packed_u16_ws_bytes(M, N, (int)kc);
+    const size_t ws_bytes = packed_ws_bytes(M, N, (int)kc);
     void* scratch = nullptr;
     SMX_TRY(scratch_alloc(&scratch, ws_bytes + 256, s));
     struct FreeOnExit {
@@ -511,24 +556,31 @@ inline int semiring_gemm_packed_public_u16(const uint16_t* A, const uint16_t* B,
     void* ws = reinterpret_cast<char*>(scratch) + 256;
     const int anti = kind == SMX_ANTI;
     const int* certp = nullptr;
-    if (bounded_fastpath_enabled() && K > 0) {
+    // (u8 needs no certificate: every u8 tile is the 1-instruction form)
+    if (!Lane<T>::kOneInstr && bounded_fastpath_enabled() && K > 0) {
         cudaError_t e = cudaMemsetAsync(cert, 0xFF, sizeof(int), s);
         if (e != cudaSuccess) return (int)e;
         const int blocks = 4 * sm_count();
-        cert_u16_kernel<<<blocks, 256, 0, s>>>(A, M, K, lda, anti, cert);
+        cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(A), M, K, lda, anti, cert);
         SMX_LAUNCHED_OR_RETURN();
-        cert_u16_kernel<<<blocks, 256, 0, s>>>(B, K, N, ldb, anti, cert);
+        cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(B), K, N, ldb, anti, cert);
         SMX_LAUNCHED_OR_RETURN();
         certp = cert;
     }
-    if (K == 0) return packed_u16_run(C, M, N, 0, ldc, kind, accumulate, 0, -1, 0, 0, ws, ws_bytes, s);
+    if (K == 0) return packed_run<T>(C, M, N, 0, ldc, kind, accumulate, 0, -1, 0, 0, ws, ws_bytes, s);
     for (long long k0 = 0; k0 < K; k0 += kc) {
         const int kk = (int)(K - k0 < kc ? K - k0 : kc);
-        SMX_TRY(packed_u16_pack(A + k0, B + k0 * ldb, M, N, kk, lda, ldb, kind, ws, ws_bytes, s, certp));
-        SMX_TRY(packed_u16_run(C, M, N, kk, ldc, kind, k0 == 0 ? accumulate : 1, 0, -1, 0, 0, ws, ws_bytes, s,
-                               certp));
+        SMX_TRY(packed_pack<T>(A + k0, B + k0 * ldb, M, N, kk, lda, ldb, kind, ws, ws_bytes, s, certp));
+        SMX_TRY(packed_run<T>(C, M, N, kk, ldc, kind, k0 == 0 ? accumulate : 1, 0, -1, 0, 0, ws, ws_bytes, s,
+                              certp));
     }
     return SMX_OK;
+}
+
+inline int semiring_gemm_packed_public_u16(const uint16_t* A, const uint16_t* B, uint16_t* C, int M, int N, int K,
+                                           long long lda, long long ldb, long long ldc, int kind, int accumulate,
+                                           cudaStream_t s) {
+    return semiring_gemm_packed_public<uint16_t>(A, B, C, M, N, K, lda, ldb, ldc, kind, accumulate, s);
 }
 
 }  // namespace smx

@@ -682,7 +682,7 @@ def test_packed_skip_gemm_matches_register_kernel_and_oracle(kind, oracle_lib):
     np.testing.assert_array_equal(outs[0][:300], want)
 
 
-@pytest.mark.parametrize("case", ["certified", "one_large", "full_range"])
+@pytest.mark.parametrize("case", ["certified", "one_large", "full_range", "u8"])
 @pytest.mark.parametrize("kind", ["anti", "dist"])
 def test_public_u16_product_packed_path(case, kind, oracle_lib):
     """smx_semiring_gemm_u16 at sizes that take the packed kernel: the
@@ -692,10 +692,11 @@ def test_public_u16_product_packed_path(case, kind, oracle_lib):
     a ragged last k-tile."""
     from paper_1705_08743_b200 import _native
     lib = _native.lib()
-    rng = np.random.default_rng({"certified": 1, "one_large": 2, "full_range": 3}[case])
+    rng = np.random.default_rng({"certified": 1, "one_large": 2, "full_range": 3, "u8": 4}[case])
     M, N, K = 2100, 2056, 700
-    S = 0xFFFF
-    hi = 60000 if case == "full_range" else 1000
+    w = 8 if case == "u8" else 16
+    S = (1 << w) - 1
+    hi = {"full_range": 60000, "u8": 250}.get(case, 1000)
     def mat(r, c):
         v = rng.integers(0, hi, (r, c), dtype=np.uint32)
         v[rng.random((r, c)) > 0.2] = S
@@ -705,24 +706,49 @@ def test_public_u16_product_packed_path(case, kind, oracle_lib):
         a[1234, 77] = 40000
     if kind == "anti":
         a, b = S - a, S - b
-    a, b = a.astype(np.uint16), b.astype(np.uint16)
-    lda, ldn = 704, 2056
-    apad = np.zeros((M, lda), np.uint16); apad[:, :K] = a
+    dt, st = (np.uint8, np.int8) if w == 8 else (np.uint16, np.int16)
+    a, b = a.astype(dt), b.astype(dt)
+    lda, ldn = 704, 2064
+    apad = np.zeros((M, lda), dt); apad[:, :K] = a
+    bpad = np.zeros((K, ldn), dt); bpad[:, :N] = b
     kid = 0 if kind == "anti" else 1
     outs = []
     for packed in (1, 0):
         old = lib.smx_set_fw_packed(packed)
         try:
-            ta = torch.from_numpy(apad.view(np.int16)).cuda()
-            tb = torch.from_numpy(b.view(np.int16)).cuda()
-            tc = torch.empty((M, ldn), dtype=torch.int16, device="cuda")
-            _native.check(lib.smx_semiring_gemm_u16(ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), M, N, K, lda, ldn,
-                                                    ldn, kid, 0, _native.stream_ptr()), "u16 product")
+            ta = torch.from_numpy(apad.view(st)).cuda()
+            tb = torch.from_numpy(bpad.view(st)).cuda()
+            tc = torch.empty((M, ldn), dtype=ta.dtype, device="cuda")
+            fn = getattr(lib, f"smx_semiring_gemm_u{w}")
+            _native.check(fn(ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), M, N, K, lda, ldn, ldn, kid, 0,
+                             _native.stream_ptr()), "product")
             torch.cuda.synchronize()
-            outs.append(tc.cpu().numpy().view(np.uint16).copy())
+            outs.append(tc.cpu().numpy().view(dt)[:, :N].copy())
         finally:
             lib.smx_set_fw_packed(old)
     np.testing.assert_array_equal(outs[0], outs[1])
     rows = np.r_[0:128, 1200:1328]
-    want = oracle_lib.semiring_mul(apad[rows], b, K, 16, kind)
+    want = oracle_lib.semiring_mul(apad[rows], b, K, w, kind)
     np.testing.assert_array_equal(outs[0][rows], want)
+
+
+@pytest.mark.parametrize("n", [1100, 2304])
+def test_fw_u8_packed_and_register_paths_agree(n, oracle_lib):
+    """u8 closures through the packed phase 3 (default) and the register-staged
+    one (smx_set_fw_packed(0)), both schedules: equal to the oracle."""
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    rng = np.random.default_rng(n)
+    cpad = -(-n // 16) * 16
+    t = np.zeros((n, cpad), np.uint8)
+    t[:, :n] = np.where(rng.random((n, n)) < 0.05, 255 - rng.integers(1, 60, (n, n)), 0)
+    np.fill_diagonal(t, 255)
+    want = oracle_lib.semiring_close(t, 8, "anti")
+    for packed, la in ((1, 1), (1, 0), (0, 1)):
+        olds = (lib.smx_set_fw_packed(packed), lib.smx_set_fw_lookahead(la))
+        try:
+            np.testing.assert_array_equal(lane("anti", t, n, 8).transitive_closure().data, want,
+                                          err_msg=f"packed={packed} la={la}")
+        finally:
+            lib.smx_set_fw_packed(olds[0])
+            lib.smx_set_fw_lookahead(olds[1])
