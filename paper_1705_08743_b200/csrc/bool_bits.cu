@@ -354,8 +354,10 @@ int copy_words(const uint32_t* src, long long ld, uint32_t* dst, long long ldd, 
                cudaStream_t s) {
     long long blocks = ((long long)rows * cols + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    copy_words_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(src, ld, dst, ldd, rows, cols);
-    SMX_RETURN_LAUNCH();
+    count_launch();
+    const cudaError_t e = launch_kernel(copy_words_kernel, dim3((unsigned)(blocks < 1 ? 1 : blocks)), dim3(256), 0,
+                                        s, src, ld, dst, ldd, rows, cols);
+    return e == cudaSuccess ? SMX_OK : (int)e;
 }
 
 inline size_t bits_ws_bytes(int n, long long ld_w) {
@@ -372,8 +374,9 @@ static int bits_pivot_and_row_panel(uint32_t* T, int n, long long ld_w, uint32_t
     count_launch();
     cudaError_t e = launch_kernel(bool_pivot_kernel, dim3(1), dim3(kWarshallBlock), 0, s, rowK + kw0, bb, ld_w);
     if (e != cudaSuccess) return (int)e;
-    e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld_w * 4, cudaMemcpyDeviceToDevice, s);
-    if (e != cudaSuccess) return (int)e;
+    // row-panel snapshot as a kernel: a D2D memcpy node in a captured graph
+    // goes to a copy engine with microseconds of latency on the pivot chain
+    SMX_TRY(copy_words(rowK, ld_w, RP, ld_w, bb, nw, s));
     return bool_bits_gemm(RP + kw0, RP, rowK, bb, nw, bb, ld_w, ld_w, ld_w, 1, 0, 0, s);
 }
 
