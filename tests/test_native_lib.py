@@ -51,3 +51,21 @@ def test_sm100a_cubin_and_native_instructions():
                                        text=True).stdout or "SM100" in sass.upper()
     assert "VIADDMNMX.U16x2" in sass
     assert "VIMNMX.U16x2" in sass
+
+
+def test_hot_kernels_use_blackwell_paths():
+    """Per-kernel SASS: the packed semiring kernel streams tiles with bulk
+    async copies and mbarriers and updates with VIADDMNMX.U16x2; the Boolean
+    tensor-core kernel issues tcgen05 MMAs fed by TMA and reads TMEM."""
+    _build.build()
+    import sys
+    sys.path.insert(0, str(_build.REPO / "tools"))
+    from sass_census import census
+    funcs = census(_build.LIB)
+    packed = [c for name, c in funcs.items() if "packed_gemm_kernelIt" in name]
+    tc = [c for name, c in funcs.items() if "bool_i8_gemm_kernel" in name]
+    assert packed and tc
+    for c in packed:
+        assert c["UBLKCP"] > 0 and c["SYNCS.PHASECHK.TRANS64.TRYWAIT"] > 0 and c["VIADDMNMX.U16x2"] > 0
+    for c in tc:
+        assert c["UTCIMMA"] > 0 and c["UTMALDG"] > 0 and c["LDTM"] > 0
