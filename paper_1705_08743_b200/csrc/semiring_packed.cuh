@@ -34,6 +34,17 @@
 #ifndef SMX_PACKED_STAGES
 #define SMX_PACKED_STAGES 3
 #endif
+// C tile handling and residency.  Default: 3 CTAs per SM (72 registers,
+// 73 KB of shared memory each) with C read from global in the epilogue -- the
+// other two CTAs cover its latency.  SMX_PACKED_CSMEM=1 instead prefetches C
+// into shared memory with bulk copies, which costs 32 KB and so the third CTA
+// (2 CTAs/SM: 1.6% slower on the n=32768 closure).
+#ifndef SMX_PACKED_CSMEM
+#define SMX_PACKED_CSMEM 0
+#endif
+#ifndef SMX_PACKED_MINB
+#define SMX_PACKED_MINB 3
+#endif
 
 namespace smx {
 
@@ -51,7 +62,10 @@ struct PackedCfg {
     static constexpr int A_TILE_WORDS = BK * BM;       // 4096 words = 16 KB
     static constexpr int B_TILE_WORDS = BK * BNW;      // 2048 words = 8 KB
     static constexpr int C_TILE_BYTES = BM * BN * (int)sizeof(T);
-    static constexpr size_t SMEM = (size_t)STAGES * (A_TILE_WORDS + B_TILE_WORDS) * 4 + C_TILE_BYTES + 1024;
+    static constexpr bool CSMEM = SMX_PACKED_CSMEM != 0;
+    static constexpr int MINB = SMX_PACKED_MINB;
+    static constexpr size_t SMEM =
+        (size_t)STAGES * (A_TILE_WORDS + B_TILE_WORDS) * 4 + (CSMEM ? C_TILE_BYTES : 0) + 1024;
 };
 using PackedU16 = PackedCfg<uint16_t>;
 
@@ -209,7 +223,8 @@ __device__ __forceinline__ void pk_bulk_load(void* dst, const void* src, uint32_
 // shared memory with row bulk copies while the K loop runs, so neither the C
 // read latency nor the operand-flag reads sit on a warp's critical path.
 template <typename T>
-__global__ void __launch_bounds__(PackedCfg<T>::THREADS, 2) packed_gemm_kernel(const PackedArgsT<T> p) {
+__global__ void __launch_bounds__(PackedCfg<T>::THREADS, PackedCfg<T>::MINB)
+packed_gemm_kernel(const PackedArgsT<T> p) {
     using L = Lane<T>;
     using G = PackedCfg<T>;
     constexpr int BM = G::BM, BNW = G::BNW, BK = G::BK, TM = G::TM, TNW = G::TNW, HW = G::HW;
@@ -219,7 +234,7 @@ __global__ void __launch_bounds__(PackedCfg<T>::THREADS, 2) packed_gemm_kernel(c
     uint32_t* As = reinterpret_cast<uint32_t*>(smem_raw);              // [ST][BK][BM]
     uint32_t* Bs = As + ST * G::A_TILE_WORDS;                          // [ST][BK][BNW]
     T* Cs = reinterpret_cast<T*>(Bs + ST * G::B_TILE_WORDS);   // [BM][BN] (raw C)
-    uint64_t* full = reinterpret_cast<uint64_t*>(Cs + BM * G::BN);
+    uint64_t* full = reinterpret_cast<uint64_t*>(Cs + (G::CSMEM ? BM * G::BN : 0));
     uint64_t* empty = full + ST;
     uint64_t* cbar = empty + ST;
     uint32_t* flag = reinterpret_cast<uint32_t*>(cbar + 1);
@@ -230,7 +245,7 @@ __global__ void __launch_bounds__(PackedCfg<T>::THREADS, 2) packed_gemm_kernel(c
     const int nt = blockIdx.x;
     const int KT = p.KT;
     const int row0 = mt * BM, col0 = nt * G::BN;
-    const bool c_async = p.accumulate && KT > 0 && row0 + BM <= p.M && col0 + G::BN <= p.N;
+    const bool c_async = G::CSMEM && p.accumulate && KT > 0 && row0 + BM <= p.M && col0 + G::BN <= p.N;
 
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
