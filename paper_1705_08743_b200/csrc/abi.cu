@@ -50,11 +50,13 @@ int& launch_priority() {
 
 int side_stream(SideStream** out) {
     static SideStream per_dev[64];
+    static std::mutex mu;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return (int)e;
     if (dev < 0 || dev >= 64) return SMX_E_ARG;
     SideStream& f = per_dev[dev];
+    std::lock_guard<std::mutex> lock(mu);
     if (!f.side) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);

@@ -20,6 +20,8 @@
 // Phases 2 and 3 are the semiring GEMM of semiring_gemm.cuh.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "semiring_packed.cuh"
 
 namespace smx {
@@ -35,10 +37,11 @@ inline int fw_block_for(int eb) { return eb == 4 ? 128 : (eb == 2 ? 512 : 256); 
 // Measured (u16): 256 over 128 +6% at n = 8192, +9% at 16384, +10% at 32768;
 // 512 over 256 at n >= 16384: see DESIGN.md 4.2.  Below 8192 vertices the
 // pivot chain no longer hides behind phase 3 and 128 wins.
-static int g_fw_block_override = 0;   // smx_set_fw_block: 0 = automatic
+static std::atomic<int> g_fw_block_override{0};   // smx_set_fw_block: 0 = automatic
 template <typename T> inline int fw_block_for_n(int n) {
     const int mx = FwBlock<T>::value;
-    if (g_fw_block_override != 0) return g_fw_block_override < mx ? g_fw_block_override : mx;
+    const int ov = g_fw_block_override.load(std::memory_order_relaxed);
+    if (ov != 0) return ov < mx ? ov : mx;
     if (sizeof(T) == 2 && n >= 16384) return 512;
     return (sizeof(T) < 4 && n >= 8192) ? 256 : 128;
 }
@@ -337,7 +340,7 @@ inline size_t fw_ws_bytes(int n, long long ld, int eb) {
 }
 
 // smx_set_fw_packed: u16 phase 3 on the warp-specialised packed-tile kernel
-static int g_fw_packed = 1;
+static std::atomic<int> g_fw_packed{1};
 
 // Phase 3 (3b) product: C rows outside [skip0, skip0 + skipn) (+)= CP (x) rowK.
 template <typename T>
@@ -391,7 +394,7 @@ int fw_pivot_and_row_panel(T* Tm, int n, long long ld, int kind, T* RP, int k0, 
 // Side-stream kernel footprint.  Measured: the co-residable Lite row-panel
 // tiles gain nothing over the regular ones (the side chain already hides
 // behind phase 3) and lose ~1-2%, so the regular tiles are the default.
-static int g_side_lite = 0;
+static std::atomic<int> g_side_lite{0};
 
 // Look-ahead schedule.  The main stream s runs the phase-3 GEMMs; the side
 // stream computes pivot block r+1 (pivot tile + row panel) as soon as its
@@ -518,8 +521,8 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
     key.fn = 100 + (int)sizeof(T);
     const unsigned long long kv[] = {(uintptr_t)Tm, (unsigned long long)n, (unsigned long long)ld,
                                      (unsigned long long)kind, (uintptr_t)ws, ws_bytes,
-                                     (unsigned long long)lookahead_enabled(), (unsigned long long)g_side_lite,
-                                     (unsigned long long)g_fw_block_override, (unsigned long long)g_fw_packed,
+                                     (unsigned long long)lookahead_enabled(), (unsigned long long)g_side_lite.load(),
+                                     (unsigned long long)g_fw_block_override.load(), (unsigned long long)g_fw_packed.load(),
                                      (unsigned long long)bounded_fastpath_enabled()};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     // the phase-3 trace records host-side state per launch: trace runs stay eager
@@ -629,22 +632,16 @@ int smx_fw_block_for(int n, int elem_bytes) {
 }
 
 int smx_set_fw_packed(int enable) {
-    const int old = g_fw_packed;
-    g_fw_packed = enable ? 1 : 0;
-    return old;
+    return g_fw_packed.exchange(enable ? 1 : 0);
 }
 
 int smx_set_fw_block(int block) {
     if (block != 0 && block != 128 && block != 256 && block != 512) return SMX_E_ARG;
-    const int old = g_fw_block_override;
-    g_fw_block_override = block;
-    return old;
+    return g_fw_block_override.exchange(block);
 }
 
 int smx_set_fw_side_lite(int enable) {
-    const int old = g_side_lite;
-    g_side_lite = enable ? 1 : 0;
-    return old;
+    return g_side_lite.exchange(enable ? 1 : 0);
 }
 
 int smx_fw_trace_arm(int max_launches) {
