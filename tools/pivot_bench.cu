@@ -197,6 +197,81 @@ __global__ void __launch_bounds__(B, 1) v0(const uint32_t* src, uint32_t* P, int
     for (int i = 0; i < W; ++i) P[r * ld_w + i] = src[r * ld_w + i];
 }
 
+__device__ __forceinline__ uint32_t close32_v6(uint32_t d) { return close32(d); }
+
+// V6: V5 with 512 threads: thread t owns words [4h, 4h+4) of row t % 256,
+// h = t / 256, so warp q (q < 4) or q + 4 (q >= 4)... holds the diagonal word
+// of K_q for its 32 rows and runs the 32x32 closure directly.
+__global__ void __launch_bounds__(2 * B, 1) v6(const uint32_t* src, uint32_t* P, int ld_w) {
+    __shared__ __align__(16) uint32_t orig[32][W];
+    __shared__ __align__(16) uint32_t tab[8][16][W];
+    __shared__ uint32_t dtab[8][16];
+    __shared__ uint32_t dp[32];
+    __shared__ uint32_t mrow[B];   // each row's K_q word (original) for the other half
+    const int t = threadIdx.x, r = t & (B - 1), h = t >> 8, warp = t >> 5, lane = t & 31;
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = src[r * ld_w + 4 * h + i];
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        const int hq = q >> 2, iq = q & 3;   // the half and slot holding word q
+        const int wq = (hq << 3) + q;        // hmm: warp index of rows K_q in half hq: (hq*256 + 32q)/32
+        (void)wq;
+        const bool own = h == hq;            // this thread holds word q of its row
+        if (own) mrow[r] = w[iq];
+        // rows K_q: write their original 4 words into orig
+        if ((r >> 5) == q) {
+            *reinterpret_cast<uint4*>(&orig[r & 31][4 * h]) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        if (own && (r >> 5) == q) dp[r & 31] = 0;   // placeholder, closure below
+        __syncthreads();
+        if (warp == hq * 8 + q) {   // lanes = rows K_q, half hq: word q in slot iq
+            dp[lane] = close32_v6(w[iq]);
+        }
+        __syncthreads();
+        {
+            const int g = t >> 6, e = (t >> 2) & 15, part = t & 3;   // 512 threads: (g,e) x 4 parts of 2 words
+            uint2 acc = make_uint2(0, 0);
+#pragma unroll
+            for (int bit = 0; bit < 4; ++bit)
+                if ((e >> bit) & 1) {
+                    const uint2 v = *reinterpret_cast<const uint2*>(&orig[4 * g + bit][2 * part]);
+                    acc.x |= v.x; acc.y |= v.y;
+                }
+            *reinterpret_cast<uint2*>(&tab[g][e][2 * part]) = acc;
+            if (t < 128) {
+                const int g2 = t >> 4, e2 = t & 15;
+                uint32_t d = 0;
+#pragma unroll
+                for (int bit = 0; bit < 4; ++bit)
+                    if ((e2 >> bit) & 1) d |= dp[4 * g2 + bit];
+                dtab[g2][e2] = d;
+            }
+        }
+        __syncthreads();
+        uint32_t m = mrow[r];
+        if ((r >> 5) == q) {
+            m = dp[r & 31];
+        } else if (m) {
+            uint32_t ext = m;
+#pragma unroll
+            for (int g = 0; g < W; ++g) ext |= dtab[g][(m >> (4 * g)) & 15];
+            m = ext;
+        }
+        if (__any_sync(0xFFFFFFFFu, m != 0)) {
+#pragma unroll
+            for (int g = 0; g < W; ++g) {
+                const int e = (m >> (4 * g)) & 15;
+                const uint4 v = *reinterpret_cast<const uint4*>(&tab[g][e][4 * h]);
+                w[0] |= v.x; w[1] |= v.y; w[2] |= v.z; w[3] |= v.w;
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) P[r * ld_w + 4 * h + i] = w[i];
+}
+
 static void cpu_ref(std::vector<uint32_t>& m, int ld_w) {
     for (int k = 0; k < B; ++k)
         for (int i = 0; i < B; ++i)
@@ -242,6 +317,7 @@ int main() {
         check("v3sparse", timeit([&] { v3<true><<<1, B>>>(src, dst, ld_w); }, 200));
         check("v3full", timeit([&] { v3<false><<<1, B>>>(src, dst, ld_w); }, 200));
         check("v5", timeit([&] { v5<<<1, B>>>(src, dst, ld_w); }, 200));
+        check("v6", timeit([&] { v6<<<1, 2 * B>>>(src, dst, ld_w); }, 200));
         cudaFree(src); cudaFree(dst);
     }
     cudaError_t e = cudaDeviceSynchronize();
