@@ -64,6 +64,7 @@ int side_stream(SideStream** out) {
         f.priority = hi;
         if ((e = cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming)) != cudaSuccess) return (int)e;
         if ((e = cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming)) != cudaSuccess) return (int)e;
+        if ((e = cudaEventCreateWithFlags(&f.aux, cudaEventDisableTiming)) != cudaSuccess) return (int)e;
     }
     *out = &f;
     return SMX_OK;

@@ -21,7 +21,7 @@ void count_launch();
 // look-ahead closure schedules (created once, reused; see abi.cu).
 struct SideStream {
     cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, aux = nullptr;
     int priority = 0;   // the side stream's (highest) priority
 };
 int side_stream(SideStream** out);

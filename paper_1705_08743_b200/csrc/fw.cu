@@ -448,17 +448,22 @@ int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, void* p
     return SMX_OK;
 }
 
-// u16 look-ahead on packed operand tiles.  Round r on the main stream:
-//   pack B(r) from T[K_r,:]  ->  3a: packed rows K_{r+1}  -> fork ->
-//   3b: packed rows outside K_r, K_{r+1}  ->  pack A(r+1) from T[:, K_{r+1}]
-//   -> wait(join)
+// u8/u16 look-ahead on packed operand tiles.  Round r:
+//   main: pack B(r) from T[K_r,:] -> fork -> 3b: packed rows outside K_r,
+//         K_{r+1} -> wait(3a done) -> pack A(r+1) from T[:, K_{r+1}] -> wait(join)
+//   side: wait(fork) -> 3a: packed rows K_{r+1} -> record(3a done) ->
+//         pivot(r+1) -> row panel(r+1) -> record(join)
+// 3a sits on the side chain, so the main stream never runs the one-wave 3a
+// product on a mostly idle GPU: the side chain (3a, pivot, row panel) hides
+// behind 3b.  3a writes rows K_{r+1}, which 3b skips; both only read the
+// packed tiles, and pack A(r+1) (which rewrites them) waits for 3a.
 // The packed A tiles are the column-panel snapshot (no separate CP copy).
 // pack A(r+1) reads rows K_{r+1} while the side stream may still rewrite
 // them, but only tiles of rows K_{r+2} (3a) and of rows outside K_{r+1} u
 // K_{r+2} (3b) are read in round r+1, as with the CP copy of fw_run_lookahead.
 template <typename T>
-int fw_run_lookahead_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws,
-                                   size_t pws_bytes, cudaStream_t s) {
+int fw_run_lookahead_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, size_t pws_bytes,
+                            cudaStream_t s) {
     SideStream* fs = nullptr;
     SMX_TRY(side_stream(&fs));
     const int BLK = fw_block_for_n<T>(n);
@@ -473,13 +478,14 @@ int fw_run_lookahead_packed(T* Tm, int n, long long ld, int kind, T* RP, void* p
         SMX_TRY(packed_pack<T>(nullptr, rowK, n, n, bb, ld, ld, kind, pws, pws_bytes, s));
         if (r + 1 < R) {
             const int k1 = k0 + BLK, bb1 = blk(r + 1);
-            // 3a: the next pivot block's rows first
-            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / PackedCfg<T>::BM, ceil_div(bb1, PackedCfg<T>::BM), 0,
-                                   0, pws, pws_bytes, s));
             if ((e = cudaEventRecord(fs->fork, s)) != cudaSuccess) return (int)e;
             if ((e = cudaStreamWaitEvent(fs->side, fs->fork, 0)) != cudaSuccess) return (int)e;
             {
                 PriorityScope ps(fs->priority);
+                // 3a: the next pivot block's rows
+                SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / PackedCfg<T>::BM,
+                                      ceil_div(bb1, PackedCfg<T>::BM), 0, 0, pws, pws_bytes, fs->side));
+                if ((e = cudaEventRecord(fs->aux, fs->side)) != cudaSuccess) return (int)e;
                 SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
             }
             if ((e = cudaEventRecord(fs->join, fs->side)) != cudaSuccess) return (int)e;
@@ -487,6 +493,7 @@ int fw_run_lookahead_packed(T* Tm, int n, long long ld, int kind, T* RP, void* p
             trace_begin(s, (long long)(n - bb - bb1) * n * bb);
             SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, 0, -1, k0, bb + bb1, pws, pws_bytes, s));
             trace_end(s);
+            if ((e = cudaStreamWaitEvent(s, fs->aux, 0)) != cudaSuccess) return (int)e;
             SMX_TRY(packed_pack<T>(Tm + k1, nullptr, n, n, bb1, ld, ld, kind, pws, pws_bytes, s));
             if ((e = cudaStreamWaitEvent(s, fs->join, 0)) != cudaSuccess) return (int)e;
         } else {
