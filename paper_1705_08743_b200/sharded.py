@@ -16,12 +16,12 @@ row-sharded, B replicated) and runs as independent local GEMMs.  Both are
 bit-identical to the single-GPU closure because every closure order agrees
 (fw.cu header).
 
-On GPUs the rounds are pipelined (``run`` -> ``_run_lookahead``): the owner of
-block r+1 first updates its rows K_{r+1} with round r's panel, then -- on a
-high-priority side stream -- closes pivot r+1, updates its row panel and
-broadcasts it, while every rank's main stream applies round r to the rest of
-its rows.  The serial owner work and the NVLink transfer hide behind the
-bulk GEMM instead of stalling all ranks once per block.
+On GPUs the rounds are pipelined (``run`` -> ``_run_lookahead``): on a
+high-priority side stream the owner of block r+1 updates its rows K_{r+1}
+with round r's panel, closes pivot r+1, updates its row panel and broadcasts
+it, while every rank's main stream applies round r to the rest of its rows.
+The serial owner work and the NVLink transfer hide behind the bulk GEMM
+instead of stalling all ranks once per block.
 
 The per-rank compute steps are an injectable ``ops`` object: ``CudaFwOps``
 calls libsemimat_b200.so; the CPU tests inject an oracle-backed version to
@@ -211,14 +211,15 @@ class ShardedFW:
             if r + 1 < R:
                 k1, bb1 = k0 + B, self._bb(k0 + B)
                 own_n = self.owner(k1) == self.rank
-                if own_n:                          # 3a: next pivot rows first
-                    lk1 = k1 - self.row0
-                    ops.update_rows(local, cp, panel, bb, n, lk1, lk1 + bb1, None)
+                lk1 = k1 - self.row0
+                if own_n:
                     skip_lo, skip_n = (skip_lo, skip_n + bb1) if own_r else (lk1, bb1)
                 fork = main.record_event() if main is not None else None
                 with torch.cuda.stream(side) if side is not None else contextlib.nullcontext():
                     if side is not None:
                         side.wait_event(fork)
+                    if own_n:                      # 3a: next pivot rows, on the side chain
+                        ops.update_rows(local, cp, panel, bb, n, lk1, lk1 + bb1, None)
                     self._owner_work(local, r + 1)
                     self._bcast(self._panel(local, r + 1), k1)
                     join = side.record_event() if side is not None else None
