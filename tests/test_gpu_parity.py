@@ -731,6 +731,18 @@ def test_public_u16_product_packed_path(case, kind, oracle_lib):
     want = oracle_lib.semiring_mul(apad[rows], b, K, w, kind)
     np.testing.assert_array_equal(outs[0][rows], want)
 
+    # accumulate = 1 into a random C: C (+)= A (x) B, folded after the K loop
+    c0 = mat(M, N).astype(dt) if kind == "dist" else (S - mat(M, N)).astype(dt)
+    cpad = np.zeros((M, ldn), dt); cpad[:, :N] = c0
+    tc = torch.from_numpy(cpad.view(st)).cuda()
+    _native.check(getattr(lib, f"smx_semiring_gemm_u{w}")(
+        torch.from_numpy(apad.view(st)).cuda().data_ptr(), torch.from_numpy(bpad.view(st)).cuda().data_ptr(),
+        tc.data_ptr(), M, N, K, lda, ldn, ldn, kid, 1, _native.stream_ptr()), "accumulate")
+    torch.cuda.synchronize()
+    got = tc.cpu().numpy().view(dt)[:, :N]
+    comb = np.maximum if kind == "anti" else np.minimum
+    np.testing.assert_array_equal(got, comb(c0, outs[0]))
+
 
 @pytest.mark.parametrize("n", [1100, 2304])
 def test_fw_u8_packed_and_register_paths_agree(n, oracle_lib):
