@@ -374,10 +374,13 @@ static int bits_pivot_and_row_panel(uint32_t* T, int n, long long ld_w, uint32_t
     count_launch();
     cudaError_t e = launch_kernel(bool_pivot_kernel, dim3(1), dim3(kWarshallBlock), 0, s, rowK + kw0, bb, ld_w);
     if (e != cudaSuccess) return (int)e;
-    // row-panel snapshot as a kernel: a D2D memcpy node in a captured graph
-    // goes to a copy engine with microseconds of latency on the pivot chain
-    SMX_TRY(copy_words(rowK, ld_w, RP, ld_w, bb, nw, s));
-    return bool_bits_gemm(RP + kw0, RP, rowK, bb, nw, bb, ld_w, ld_w, ld_w, 1, 0, 0, s);
+    // Row panel in place, no snapshot: T[K,:] |= P* . T[K,:] with P* = T[K,K]
+    // closed.  A CTA may read rows K that another CTA has already OR-ed into;
+    // those bits are paths through K, and P* . (T[K,:] | P* . T[K,:]) =
+    // P* . T[K,:] because P* . P* = P*.  The P* tile itself is rewritten with
+    // its own value.  So any interleaving gives the same result.
+    (void)RP;
+    return bool_bits_gemm(rowK + kw0, rowK, rowK, bb, nw, bb, ld_w, ld_w, ld_w, 1, 0, 0, s);
 }
 
 static int bool_warshall_schedule(uint32_t* T, int n, long long ld_w, uint32_t* RP, uint32_t* CP,

@@ -385,10 +385,15 @@ int fw_pivot_and_row_panel(T* Tm, int n, long long ld, int kind, T* RP, int k0, 
                            bool lite = false) {
     T* rowK = Tm + (long long)k0 * ld;
     if (lite && bb <= 256) SMX_TRY(fw_pivot_lite<T>(rowK + k0, bb, ld, kind, s));
-    else SMX_TRY(fw_pivot<T>(rowK + k0, bb, ld, kind, s, RP));   // RP is free until the snapshot below
-    SMX_TRY(copy_panel<T>(rowK, ld, RP, ld, bb, n, s));
-    if (lite) return semiring_gemm_lite<T>(RP + k0, RP, rowK, bb, n, bb, ld, ld, ld, kind, s);
-    return semiring_gemm<T>(RP + k0, RP, rowK, bb, n, bb, ld, ld, ld, kind, 1, 0, 0, s);
+    else SMX_TRY(fw_pivot<T>(rowK + k0, bb, ld, kind, s, RP));   // RP: the pivot's scratch
+    // Row panel in place, no snapshot: T[K,:] (+)= P* (x) T[K,:] with
+    // P* = T[K,K] closed.  A CTA may read (through the read-only path) rows K
+    // that another CTA has already updated; every such value lies between the
+    // old value and the final one, and P* (x) final = P* (x) old because
+    // P* (x) P* = P* (closure, weights >= 0) -- so the result is the same for
+    // any interleaving.  The P* tile itself is rewritten with its own value.
+    if (lite) return semiring_gemm_lite<T>(rowK + k0, rowK, rowK, bb, n, bb, ld, ld, ld, kind, s);
+    return semiring_gemm<T>(rowK + k0, rowK, rowK, bb, n, bb, ld, ld, ld, kind, 1, 0, 0, s);
 }
 
 // Side-stream kernel footprint.  Measured: the co-residable Lite row-panel

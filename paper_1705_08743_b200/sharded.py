@@ -79,10 +79,12 @@ class CudaFwOps:
                       "smx_fw_pivot")
 
     def panel_update(self, t: torch.Tensor, r0: int, k0: int, b: int, n: int) -> None:
-        rp = t[r0:r0 + b].clone()
+        """T[K,:] (+)= T[K,K]* (x) T[K,:] in place (no snapshot needed: the
+        pivot tile is closed, so every interleaving gives the same result;
+        see fw_pivot_and_row_panel in fw.cu)."""
         ld = t.shape[1]
         _native.check(_native.lib().smx_semiring_gemm_skip(
-            self._at(rp, 0, k0), rp.data_ptr(), self._at(t, r0, 0), b, n, b, ld, ld, ld, self.eb,
+            self._at(t, r0, k0), self._at(t, r0, 0), self._at(t, r0, 0), b, n, b, ld, ld, ld, self.eb,
             self.kind, 0, 0, _native.stream_ptr(t.device)), "pivot row panel")
 
     def snapshot(self, t: torch.Tensor, k0: int, b: int) -> torch.Tensor:
