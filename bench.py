@@ -444,6 +444,20 @@ def run_ours(args, world, rank, local_rank):
                             f"(ceiling 0.5); verified-bounded / certified tiles and u8 need 1"),
             "algorithmic_bytes_per_launch": alg_bytes,
         }
+        # the other roof: DRAM bandwidth the dominant kernel draws, against the
+        # driver-measured HBM copy bandwidth (MEASURED_PEAKS.json)
+        avg_s = dom_secs_total / dom_launches
+        hbm = None
+        mp = REPO / "MEASURED_PEAKS.json"
+        if mp.exists():
+            try:
+                hbm = float(json.loads(mp.read_text()).get("hbm_gbs"))
+            except (ValueError, TypeError):
+                hbm = None
+        bytes_l = traffic if traffic else alg_bytes
+        result["roofline"]["hbm_gbs_achieved"] = bytes_l / avg_s / 1e9
+        result["roofline"]["hbm_gbs_peak"] = hbm
+        result["roofline"]["hbm_frac"] = (bytes_l / avg_s / 1e9 / hbm) if hbm else None
         # e2e through the public API with host buffers
         if cfg.op == "closure":
             pinned = torch.from_numpy(host).pin_memory()
