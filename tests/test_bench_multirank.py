@@ -1,0 +1,43 @@
+"""bench.py's multi-rank path end to end: torchrun with 2 ranks, the sharded
+closure gathered and compared with the single-GPU closure (--check).
+
+The ranks share this box's one GPU over gloo: gloo's broadcast is host-side,
+so no kernel ever waits on another rank's kernel.  Timings from this run mean
+nothing; the driver's NCCL runs on N GPUs use the same code path.
+"""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REPO = Path(__file__).resolve().parent.parent
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("nproc,size", [(2, 2048), (3, 1500)])
+def test_bench_sharded_closure_matches_single_gpu(nproc, size):
+    env = dict(os.environ, SMX_BENCH_BACKEND="gloo", OMP_NUM_THREADS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(REPO / "bench.py"),
+           "--gpus", str(nproc), "--size", str(size), "--steps", "1", "--warmup", "1", "--check",
+           "--no-secondary", "--no-cpu"]
+    r = subprocess.run(cmd, cwd=REPO, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == nproc
+    assert d["parity_sharded"] == {"n": size, "bit_exact_vs_single_gpu": True}
+    assert d["gpu_launches"] > 0
