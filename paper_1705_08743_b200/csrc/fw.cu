@@ -4,20 +4,26 @@
 // Replaces _close_vector / _minplus_close_vector
 // (pkg/src/semimat/antidist.py:390-398, :440-448).  The reference sweeps k
 // one vertex at a time over the whole matrix; here k advances in blocks of
-// B = 128 vertices (SURVEY.md 0.1 fact 2 verifies the blocked order is
-// bit-identical: x -> min(x, S) is a semiring homomorphism from (min,+) on
-// [0, inf] onto the clipped lanes, so every correct closure order agrees):
+// B = 128 / 256 / 512 vertices (fw_block_for_n; SURVEY.md 0.1 fact 2
+// verifies the blocked order is bit-identical: x -> min(x, S) is a semiring
+// homomorphism from (min,+) on [0, inf] onto the clipped lanes, so every
+// correct closure order agrees):
 //
 //   round r, pivot block K = [k0, k0 + bb):
-//   1. pivot   : close the bb x bb tile T[K,K] in place (one CTA, tile in
-//                registers, pivot row/column broadcast through smem).
-//   2. row     : T[K,:] (+)= T[K,K]* (x) T[K,:]   (snapshot RP of the panel)
+//   1. pivot   : close the bb x bb tile T[K,K] in place (the 128 register
+//                kernel, or a 2 x 2 blocked recursion on it above 128).
+//   2. row     : T[K,:] (+)= T[K,K]* (x) T[K,:], in place (see
+//                fw_pivot_and_row_panel for why no snapshot is needed).
 //   3. rest    : T[i,:] (+)= T[i,K] (x) T[K,:] for every i outside K, with
-//                T[i,K] read from a snapshot CP of the column panel.  The
-//                j in K part of this product is exactly the column-panel
-//                update T[i,K] (x) (I (+) T[K,K]*), so phases 2b and 3 fuse
-//                into one semiring GEMM over the full row width.
-// Phases 2 and 3 are the semiring GEMM of semiring_gemm.cuh.
+//                T[i,K] read from a snapshot of the column panel (the packed
+//                A tiles on the u8/u16 path, CP otherwise).  The j in K part
+//                of this product is exactly the column-panel update
+//                T[i,K] (x) (I (+) T[K,K]*), so phases 2b and 3 fuse into one
+//                semiring GEMM over the full row width.
+// Phase 3 is the packed kernel of semiring_packed.cuh (u8/u16) or the
+// register-staged one of semiring_gemm.cuh (u32, smx_set_fw_packed(0)); the
+// look-ahead schedules overlap round r's phase 3 with round r+1's steps 1-2
+// on a high-priority side stream.
 #include <cuda_runtime.h>
 
 #include <atomic>
