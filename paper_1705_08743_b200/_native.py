@@ -114,6 +114,7 @@ def stream_ptr(device: torch.device | None = None) -> int:
 
 
 def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    """Scratch for one library call, from torch's stream-aware caching allocator."""
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
 
 

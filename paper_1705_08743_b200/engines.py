@@ -16,6 +16,7 @@ from ._native import SMX_ANTI, SMX_DIST, check, lib, stream_ptr
 
 _GEMM = {8: "smx_semiring_gemm_u8", 16: "smx_semiring_gemm_u16", 32: "smx_semiring_gemm_u32"}
 _FW = {8: "smx_fw_u8", 16: "smx_fw_u16", 32: "smx_fw_u32"}
+_TC_WS: dict = {}   # (M, N, K) -> smx_bool_mul_tc_workspace_bytes
 
 
 def lane_mul(a: torch.Tensor, b: torch.Tensor, inner: int, width: int, anti: bool,
@@ -81,7 +82,10 @@ def bool_mul_tc(a, b):
     from .boolmat import BoolMatrix, _stride_words
     L = lib()
     out = torch.empty((a.rows, _stride_words(b.cols)), dtype=torch.int32, device=a.device)
-    nbytes = L.smx_bool_mul_tc_workspace_bytes(a.rows, b.cols, a.cols)
+    key = (a.rows, b.cols, a.cols)
+    nbytes = _TC_WS.get(key)
+    if nbytes is None:
+        nbytes = _TC_WS[key] = L.smx_bool_mul_tc_workspace_bytes(a.rows, b.cols, a.cols)
     ws = _native.workspace(nbytes, a.device)
     check(L.smx_bool_mul_tc(a._words.data_ptr(), b._words.data_ptr(), out.data_ptr(), a.rows, b.cols,
                             a.cols, a.stride_words, b.stride_words, out.shape[1], ws.data_ptr(), nbytes,

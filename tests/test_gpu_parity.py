@@ -735,9 +735,11 @@ def test_public_u16_product_packed_path(case, kind, oracle_lib):
     c0 = mat(M, N).astype(dt) if kind == "dist" else (S - mat(M, N)).astype(dt)
     cpad = np.zeros((M, ldn), dt); cpad[:, :N] = c0
     tc = torch.from_numpy(cpad.view(st)).cuda()
+    ta = torch.from_numpy(apad.view(st)).cuda()   # kept alive across the async call
+    tb = torch.from_numpy(bpad.view(st)).cuda()
     _native.check(getattr(lib, f"smx_semiring_gemm_u{w}")(
-        torch.from_numpy(apad.view(st)).cuda().data_ptr(), torch.from_numpy(bpad.view(st)).cuda().data_ptr(),
-        tc.data_ptr(), M, N, K, lda, ldn, ldn, kid, 1, _native.stream_ptr()), "accumulate")
+        ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), M, N, K, lda, ldn, ldn, kid, 1, _native.stream_ptr()),
+        "accumulate")
     torch.cuda.synchronize()
     got = tc.cpu().numpy().view(dt)[:, :N]
     comb = np.maximum if kind == "anti" else np.minimum
