@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "bool_pivot.cuh"
 
 namespace smx {
 
@@ -370,51 +371,63 @@ int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbit
 
 constexpr int kTcWarshallBlock = 256;
 
-// Pivot tile closure on bytes: each thread packs its row to bits, runs the
-// sequential Warshall steps with the pivot row broadcast through smem, and
-// writes 0/1 bytes back.
-__global__ void __launch_bounds__(kTcWarshallBlock, 1)
+// Pivot tile closure on bytes: each thread packs its row of 0/1 bytes to
+// bits, the tile is closed by the bit-packed table pivot (bool_pivot.cuh),
+// and the rows are unpacked back to bytes.
+__global__ void __launch_bounds__(kWarshallBlock, 1)
 bool_pivot_bytes_kernel(uint8_t* P, int b, long long ld) {
-    constexpr int W = kTcWarshallBlock / 32;
-    __shared__ __align__(16) uint32_t prow[2][W];
+    constexpr int W = kWarshallBlock / 32;
+    __shared__ __align__(16) PivotSmem sm;
     const int r = threadIdx.x;
+    uint8_t* row = P + (long long)r * ld;
+    const bool vec = b == kWarshallBlock && (reinterpret_cast<uintptr_t>(row) & 15) == 0;
     uint32_t w[W];
 #pragma unroll
     for (int i = 0; i < W; ++i) {
         uint32_t v = 0;
         if (r < b) {
-            for (int j = 0; j < 32; ++j) {
-                const int c = i * 32 + j;
-                if (c < b && P[(long long)r * ld + c]) v |= 1u << j;
+            if (vec) {
+                const uint4* src = reinterpret_cast<const uint4*>(row + i * 32);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint4 x = src[h];
+                    const uint32_t q[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t o = __vcmpne4(q[j], 0u) & 0x01010101u;   // 0/1 per byte
+                        const uint32_t nib = (o & 1u) | ((o >> 7) & 2u) | ((o >> 14) & 4u) | ((o >> 21) & 8u);
+                        v |= nib << (16 * h + 4 * j);
+                    }
+                }
+            } else {
+                for (int j = 0; j < 32; ++j) {
+                    const int c = i * 32 + j;
+                    if (c < b && row[c]) v |= 1u << j;
+                }
             }
         }
         w[i] = v;
     }
-    if (r == 0) {
-#pragma unroll
-        for (int i = 0; i < W; ++i) prow[0][i] = w[i];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < W; ++q) {
-        if (q * 32 >= b) break;
-        for (int kk = 0; kk < 32; ++kk) {
-            const int k = q * 32 + kk;
-            if (k >= b) break;
-            const int cur = k & 1;
-            if ((w[q] >> kk) & 1u) {
-#pragma unroll
-                for (int i = 0; i < W; ++i) w[i] |= prow[cur][i];
-            }
-            if (r == k + 1) {
-#pragma unroll
-                for (int i = 0; i < W; ++i) prow[cur ^ 1][i] = w[i];
-            }
-            __syncthreads();
-        }
-    }
+    close_tile_bits(w, b, sm);
     if (r < b) {
-        for (int c = 0; c < b; ++c) P[(long long)r * ld + c] = (w[c >> 5] >> (c & 31)) & 1u;
+        if (vec) {
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                uint4* dst = reinterpret_cast<uint4*>(row + i * 32);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t q[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t nib = (w[i] >> (16 * h + 4 * j)) & 0xFu;
+                        q[j] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+                    }
+                    dst[h] = make_uint4(q[0], q[1], q[2], q[3]);
+                }
+            }
+        } else {
+            for (int c = 0; c < b; ++c) row[c] = (w[c >> 5] >> (c & 31)) & 1u;
+        }
     }
 }
 
