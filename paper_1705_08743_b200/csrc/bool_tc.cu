@@ -456,23 +456,32 @@ int bool_warshall_i8(uint8_t* T, int n, long long ld, void* ws, size_t ws_bytes,
     uint8_t* CP = RPt + al((size_t)n * kTcWarshallBlock);
     uint8_t* RP = CP + al((size_t)n * kTcWarshallBlock);
     constexpr long long B = kTcWarshallBlock;
-    for (int k0 = 0; k0 < n; k0 += kTcWarshallBlock) {
-        const int bb = n - k0 < kTcWarshallBlock ? n - k0 : kTcWarshallBlock;
-        uint8_t* rowK = T + (long long)k0 * ld;
-        bool_pivot_bytes_kernel<<<1, kTcWarshallBlock, 0, s>>>(rowK + k0, bb, ld);
-        SMX_LAUNCHED_OR_RETURN();
-        // phase 2: T[K,:] |= P* . RP   (B^T = RP^T)
-        cudaError_t e = cudaMemcpyAsync(RP, rowK, (size_t)bb * ld, cudaMemcpyDeviceToDevice, s);
-        if (e != cudaSuccess) return (int)e;
-        SMX_TRY(transpose_bytes(RP, RPt, bb, n, ld, B, s));
-        SMX_TRY(bool_i8_gemm(RP + k0, RPt, rowK, nullptr, bb, n, bb, ld, B, ld, 1, 0, 0, s));
-        // phase 3: T[i,:] |= CP[i,:] . T[K,:]  for i outside K  (B^T = T[K,:]^T)
-        SMX_TRY(transpose_bytes(rowK, RPt, bb, n, ld, B, s));
-        e = cudaMemcpy2DAsync(CP, B, T + k0, ld, bb, n, cudaMemcpyDeviceToDevice, s);
-        if (e != cudaSuccess) return (int)e;
-        SMX_TRY(bool_i8_gemm(CP, RPt, T, nullptr, n, n, bb, B, B, ld, 1, k0, bb, s));
-    }
-    return SMX_OK;
+    (void)RP;
+    GraphKey key;
+    key.fn = 301;
+    const unsigned long long kv[] = {(uintptr_t)T, (unsigned long long)n, (unsigned long long)ld, (uintptr_t)ws,
+                                     ws_bytes};
+    for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
+    return run_graphed(key, s, false, [&](cudaStream_t st) -> int {
+        for (int k0 = 0; k0 < n; k0 += kTcWarshallBlock) {
+            const int bb = n - k0 < kTcWarshallBlock ? n - k0 : kTcWarshallBlock;
+            uint8_t* rowK = T + (long long)k0 * ld;
+            count_launch();
+            bool_pivot_bytes_kernel<<<1, kTcWarshallBlock, 0, st>>>(rowK + k0, bb, ld);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return (int)e;
+            // phase 2 in place: T[K,:] |= P* . T[K,:]  (B^T = T[K,:]^T snapshot;
+            // reading P* while it is rewritten with its own value is exact)
+            SMX_TRY(transpose_bytes(rowK, RPt, bb, n, ld, B, st));
+            SMX_TRY(bool_i8_gemm(rowK + k0, RPt, rowK, nullptr, bb, n, bb, ld, B, ld, 1, 0, 0, st));
+            // phase 3: T[i,:] |= CP[i,:] . T[K,:]  for i outside K  (B^T = T[K,:]^T)
+            SMX_TRY(transpose_bytes(rowK, RPt, bb, n, ld, B, st));
+            e = cudaMemcpy2DAsync(CP, B, T + k0, ld, bb, n, cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return (int)e;
+            SMX_TRY(bool_i8_gemm(CP, RPt, T, nullptr, n, n, bb, B, B, ld, 1, k0, bb, st));
+        }
+        return SMX_OK;
+    });
 }
 
 int unpack_bits(const uint32_t* words, uint8_t* bytes, int rows, int cols, long long ld_w, long long ld,
