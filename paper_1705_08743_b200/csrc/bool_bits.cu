@@ -222,10 +222,16 @@ int bool_bits_gemm(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int
     return large ? launch_bits<BitsLarge>(a, s) : launch_bits<BitsSmall>(a, s);
 }
 
-__global__ void __launch_bounds__(kWarshallBlock, 1)
-bool_pivot_kernel(uint32_t* P, int b, long long ld_w) {
-    constexpr int W = kWarshallBlock / 32;
-    __shared__ __align__(16) PivotSmem sm;
+// Warshall blocks: 256 vertices, or 512 for large n (kMaxWarshallBlock).
+constexpr int kMaxWarshallBlock = 512;
+#ifndef SMX_BOOL_BLOCK512_MIN_N
+#define SMX_BOOL_BLOCK512_MIN_N 8192
+#endif
+constexpr int kBoolBlock512MinN = SMX_BOOL_BLOCK512_MIN_N;
+
+template <int W>   // tile words per row: 8 (256 vertices) or 16 (512)
+__global__ void __launch_bounds__(32 * W, 1) bool_pivot_kernel(uint32_t* P, int b, long long ld_w) {
+    __shared__ __align__(16) PivotSmemT<W> sm;
     const int r = threadIdx.x;
     const int nw = (b + 31) / 32;
     uint32_t w[W];
@@ -239,7 +245,7 @@ bool_pivot_kernel(uint32_t* P, int b, long long ld_w) {
         }
         w[i] = v;
     }
-    close_tile_bits(w, b, sm);
+    close_tile_bits<W>(w, b, sm);
     if (r < b) {
         for (int i = 0; i < nw; ++i) {
             const int valid = b - i * 32;
@@ -252,6 +258,19 @@ bool_pivot_kernel(uint32_t* P, int b, long long ld_w) {
         }
     }
 }
+
+static int launch_bool_pivot(uint32_t* P, int b, long long ld_w, cudaStream_t s) {
+    count_launch();
+    const cudaError_t e = b <= kWarshallBlock
+                              ? launch_kernel(bool_pivot_kernel<8>, dim3(1), dim3(256), 0, s, P, b, ld_w)
+                              : launch_kernel(bool_pivot_kernel<16>, dim3(1), dim3(512), 0, s, P, b, ld_w);
+    return e == cudaSuccess ? SMX_OK : (int)e;
+}
+
+// Block for an n-vertex closure.  Measured (ms, 256 / 512 blocks): n = 4096
+// 0.33 / 0.46, 8192 1.79 / 1.51, 16384 10.1 / 10.1 -- halving the rounds pays
+// once each round's phase 3 is long enough to hide the 512 pivot chain.
+static int bool_block_for_n(int n) { return n >= kBoolBlock512MinN ? 512 : kWarshallBlock; }
 
 // Column-panel snapshot of `cols` words for all rows (one thread per word).
 __global__ void copy_words_kernel(const uint32_t* __restrict__ src, long long ld, uint32_t* __restrict__ dst,
@@ -275,8 +294,8 @@ int copy_words(const uint32_t* src, long long ld, uint32_t* dst, long long ldd, 
 }
 
 inline size_t bits_ws_bytes(int n, long long ld_w) {
-    const size_t rp = ((size_t)kWarshallBlock * ld_w * 4 + 255) & ~size_t(255);
-    const size_t cp = (size_t)n * (kWarshallBlock / 32) * 4;
+    const size_t rp = ((size_t)kMaxWarshallBlock * ld_w * 4 + 255) & ~size_t(255);
+    const size_t cp = (size_t)n * (kMaxWarshallBlock / 32) * 4;
     return rp + ((cp + 255) & ~size_t(255));
 }
 
@@ -285,9 +304,7 @@ static int bits_pivot_and_row_panel(uint32_t* T, int n, long long ld_w, uint32_t
                                     cudaStream_t s) {
     const int kw0 = k0 / 32, nw = (n + 31) / 32;
     uint32_t* rowK = T + (long long)k0 * ld_w;
-    count_launch();
-    cudaError_t e = launch_kernel(bool_pivot_kernel, dim3(1), dim3(kWarshallBlock), 0, s, rowK + kw0, bb, ld_w);
-    if (e != cudaSuccess) return (int)e;
+    SMX_TRY(launch_bool_pivot(rowK + kw0, bb, ld_w, s));
     // Row panel in place, no snapshot: T[K,:] |= P* . T[K,:] with P* = T[K,K]
     // closed.  A CTA may read rows K that another CTA has already OR-ed into;
     // those bits are paths through K, and P* . (T[K,:] | P* . T[K,:]) =
@@ -306,18 +323,16 @@ int bool_warshall_bits(uint32_t* T, int n, long long ld_w, void* ws, size_t ws_b
     if (n < 0 || ld_w * 32 < n) return SMX_E_ARG;
     if (n == 0) return SMX_OK;
     if (!aligned16(T) || (ld_w & 3)) return SMX_E_ALIGN;
-    if (n <= kWarshallBlock) {
-        bool_pivot_kernel<<<1, kWarshallBlock, 0, s>>>(T, n, ld_w);
-        SMX_RETURN_LAUNCH();
-    }
+    if (n <= kWarshallBlock) return launch_bool_pivot(T, n, ld_w, s);
     if (ws == nullptr || ws_bytes < bits_ws_bytes(n, ld_w)) return SMX_E_WORKSPACE;
     uint32_t* RP = reinterpret_cast<uint32_t*>(ws);
     uint32_t* CP = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ws) +
-                                               (((size_t)kWarshallBlock * ld_w * 4 + 255) & ~size_t(255)));
+                                               (((size_t)kMaxWarshallBlock * ld_w * 4 + 255) & ~size_t(255)));
     GraphKey key;
     key.fn = 200;
     const unsigned long long kv[] = {(uintptr_t)T, (unsigned long long)n, (unsigned long long)ld_w,
-                                     (uintptr_t)ws, ws_bytes, (unsigned long long)lookahead_enabled()};
+                                     (uintptr_t)ws, ws_bytes, (unsigned long long)lookahead_enabled(),
+                                     (unsigned long long)bool_block_for_n(n)};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     return run_graphed(key, s, false, [&](cudaStream_t st) -> int {
         return bool_warshall_schedule(T, n, ld_w, RP, CP, st);
@@ -327,13 +342,14 @@ int bool_warshall_bits(uint32_t* T, int n, long long ld_w, void* ws, size_t ws_b
 static int bool_warshall_schedule(uint32_t* T, int n, long long ld_w, uint32_t* RP, uint32_t* CP,
                                   cudaStream_t s) {
     const int nw = (n + 31) / 32;
-    constexpr long long ldcp = kWarshallBlock / 32;
-    const int R = (n + kWarshallBlock - 1) / kWarshallBlock;
-    auto blk = [&](int r) { return n - r * kWarshallBlock < kWarshallBlock ? n - r * kWarshallBlock : kWarshallBlock; };
+    const int BLK = bool_block_for_n(n);
+    const long long ldcp = BLK / 32;
+    const int R = (n + BLK - 1) / BLK;
+    auto blk = [&](int r) { return n - r * BLK < BLK ? n - r * BLK : BLK; };
 
     if (!lookahead_enabled()) {
         for (int r = 0; r < R; ++r) {
-            const int k0 = r * kWarshallBlock, bb = blk(r), kw0 = k0 / 32, bw = (bb + 31) / 32;
+            const int k0 = r * BLK, bb = blk(r), kw0 = k0 / 32, bw = (bb + 31) / 32;
             SMX_TRY(bits_pivot_and_row_panel(T, n, ld_w, RP, k0, bb, s));
             SMX_TRY(copy_words(T + kw0, ld_w, CP, ldcp, n, bw, s));
             SMX_TRY(bool_bits_gemm(CP, T + (long long)k0 * ld_w, T, n, nw, bb, ldcp, ld_w, ld_w, 1, k0, bb, s));
@@ -346,10 +362,10 @@ static int bool_warshall_schedule(uint32_t* T, int n, long long ld_w, uint32_t* 
     SMX_TRY(bits_pivot_and_row_panel(T, n, ld_w, RP, 0, blk(0), s));
     SMX_TRY(copy_words(T, ld_w, CP, ldcp, n, (blk(0) + 31) / 32, s));
     for (int r = 0; r < R; ++r) {
-        const int k0 = r * kWarshallBlock, bb = blk(r);
+        const int k0 = r * BLK, bb = blk(r);
         uint32_t* rowK = T + (long long)k0 * ld_w;
         if (r + 1 < R) {
-            const int k1 = k0 + kWarshallBlock, bb1 = blk(r + 1);
+            const int k1 = k0 + BLK, bb1 = blk(r + 1);
             SMX_TRY(bool_bits_gemm(CP + k1 * ldcp, rowK, T + (long long)k1 * ld_w, bb1, nw, bb, ldcp, ld_w,
                                    ld_w, 1, 0, 0, s));
             if ((e = cudaEventRecord(ss->fork, s)) != cudaSuccess) return (int)e;

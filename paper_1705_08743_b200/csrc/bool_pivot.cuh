@@ -40,37 +40,46 @@ __device__ __forceinline__ uint32_t close32(uint32_t d) {
     return d;
 }
 
-// Close the b x b (b <= 256) bit tile held one row per thread in w[8]
-// (row r = threadIdx.x; bits beyond b already cleared), in place.
-struct PivotSmem {
-    uint32_t orig[32][8];
-    uint32_t tab[8][16][8];
+// Close the b x b bit tile (b <= 32 W) held one row per thread in w[W]
+// (row r = threadIdx.x, 32 W threads; bits beyond b already cleared), in
+// place.  W = 8 (256-vertex tiles) or 16 (512).
+template <int W>
+struct PivotSmemT {
+    uint32_t orig[32][W];
+    uint32_t tab[8][16][W];
     uint32_t dtab[8][16];
     uint32_t dp[32];
 };
+using PivotSmem = PivotSmemT<8>;
 
-__device__ __forceinline__ void close_tile_bits(uint32_t (&w)[8], int b, PivotSmem& sm) {
-    constexpr int W = kWarshallBlock / 32;
+template <int W>
+__device__ __forceinline__ void close_tile_bits(uint32_t (&w)[W], int b, PivotSmemT<W>& sm) {
+    static_assert(W % 4 == 0, "rows are moved as uint4");
+    constexpr int PARTS = W / 4;   // uint4 parts per table entry
     const int r = threadIdx.x, warp = r >> 5, lane = r & 31;
 #pragma unroll
     for (int q = 0; q < W; ++q) {
         if (q * 32 >= b) break;
         if (warp == q) {
-            *reinterpret_cast<uint4*>(&sm.orig[lane][0]) = make_uint4(w[0], w[1], w[2], w[3]);
-            *reinterpret_cast<uint4*>(&sm.orig[lane][4]) = make_uint4(w[4], w[5], w[6], w[7]);
+#pragma unroll
+            for (int p = 0; p < PARTS; ++p)
+                *reinterpret_cast<uint4*>(&sm.orig[lane][4 * p]) =
+                    make_uint4(w[4 * p], w[4 * p + 1], w[4 * p + 2], w[4 * p + 3]);
             sm.dp[lane] = close32(w[q]);
         }
         __syncthreads();
         {
-            const int g = r >> 5, e = (r >> 1) & 15, h = r & 1;
+            // 128 table entries x PARTS uint4 parts = 32 W threads
+            const int entry = r / PARTS, part = r % PARTS;
+            const int g = entry >> 4, e = entry & 15;
             uint4 acc = make_uint4(0, 0, 0, 0);
 #pragma unroll
             for (int bit = 0; bit < 4; ++bit)
                 if ((e >> bit) & 1) {
-                    const uint4 v = *reinterpret_cast<const uint4*>(&sm.orig[4 * g + bit][4 * h]);
+                    const uint4 v = *reinterpret_cast<const uint4*>(&sm.orig[4 * g + bit][4 * part]);
                     acc.x |= v.x; acc.y |= v.y; acc.z |= v.z; acc.w |= v.w;
                 }
-            *reinterpret_cast<uint4*>(&sm.tab[g][e][4 * h]) = acc;
+            *reinterpret_cast<uint4*>(&sm.tab[g][e][4 * part]) = acc;
             if (r < 128) {
                 const int g2 = r >> 4, e2 = r & 15;
                 uint32_t d = 0;
@@ -87,17 +96,18 @@ __device__ __forceinline__ void close_tile_bits(uint32_t (&w)[8], int b, PivotSm
         } else if (m) {
             uint32_t ext = m;
 #pragma unroll
-            for (int g = 0; g < W; ++g) ext |= sm.dtab[g][(m >> (4 * g)) & 15];
+            for (int g = 0; g < 8; ++g) ext |= sm.dtab[g][(m >> (4 * g)) & 15];
             m = ext;
         }
         if (__any_sync(0xFFFFFFFFu, m != 0)) {
 #pragma unroll
-            for (int g = 0; g < W; ++g) {
+            for (int g = 0; g < 8; ++g) {
                 const int e = (m >> (4 * g)) & 15;
-                const uint4 v0 = *reinterpret_cast<const uint4*>(&sm.tab[g][e][0]);
-                const uint4 v1 = *reinterpret_cast<const uint4*>(&sm.tab[g][e][4]);
-                w[0] |= v0.x; w[1] |= v0.y; w[2] |= v0.z; w[3] |= v0.w;
-                w[4] |= v1.x; w[5] |= v1.y; w[6] |= v1.z; w[7] |= v1.w;
+#pragma unroll
+                for (int p = 0; p < PARTS; ++p) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(&sm.tab[g][e][4 * p]);
+                    w[4 * p] |= v.x; w[4 * p + 1] |= v.y; w[4 * p + 2] |= v.z; w[4 * p + 3] |= v.w;
+                }
             }
         }
         __syncthreads();

@@ -766,3 +766,15 @@ def test_fw_u8_packed_and_register_paths_agree(n, oracle_lib):
         finally:
             lib.smx_set_fw_packed(olds[0])
             lib.smx_set_fw_lookahead(olds[1])
+
+
+def test_bool_warshall_512_blocks_ragged(oracle_lib):
+    """n >= 8192 takes 512-vertex Warshall blocks (16-word pivot tiles, 512
+    threads); a ragged n and a denser graph exercise partial tiles and the
+    table pivot's dense path.  Bit-exact against the C oracle."""
+    from oracle import pack_bits
+    rng = np.random.default_rng(77)
+    n = 8300
+    a = rng.random((n, n), dtype=np.float32) < 3.0 / n
+    got = BoolMatrix.from_numpy(a).transitive_closure().blocks
+    np.testing.assert_array_equal(got, oracle_lib.bool_close(pack_bits(a)))
