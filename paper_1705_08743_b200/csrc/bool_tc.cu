@@ -488,6 +488,9 @@ int unpack_bits(const uint32_t* words, uint8_t* bytes, int rows, int cols, long 
                 cudaStream_t s);
 int unpack_bits_transposed(const uint32_t* words, uint8_t* out, int rows, int cols, long long ld_w,
                            long long ld_out, cudaStream_t s);
+int unpack_ab(const uint32_t* a_words, uint8_t* a_bytes, int a_rows, int a_cols, long long a_ldw, long long a_ld,
+              const uint32_t* b_words, uint8_t* bt, int b_rows, int b_cols, long long b_ldw, long long b_ldt,
+              cudaStream_t s);
 
 inline long long round16(long long x) { return (x + 15) & ~15LL; }
 
@@ -513,8 +516,7 @@ int bool_mul_tc(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int N,
                                      ws_bytes};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     return run_graphed(key, s, false, [&](cudaStream_t st) -> int {
-        SMX_TRY(unpack_bits(A, a8, M, K, lda_w, round16(K), st));
-        SMX_TRY(unpack_bits_transposed(B, bt8, K, N, ldb_w, round16(K), st));
+        SMX_TRY(unpack_ab(A, a8, M, K, lda_w, round16(K), B, bt8, K, N, ldb_w, round16(K), st));
         // words past ceil(N/32) in each output row are padding: keep them zero
         const long long nw = (N + 31) / 32;
         if (ldc_w > nw) {

@@ -81,6 +81,62 @@ __global__ void unpack_bits_t_kernel(const uint32_t* __restrict__ words, uint8_t
     }
 }
 
+// Both operands of the one-call tensor-core product in one launch: blocks
+// [0, a_blocks) unpack A's bit rows (unpack_bits_kernel), the rest turn B's
+// bit rows into the transposed K-major byte operand (unpack_bits_t_kernel).
+__global__ void unpack_ab_kernel(const uint32_t* __restrict__ a_words, uint8_t* __restrict__ a_bytes, int a_rows,
+                                 int a_cols, long long a_ldw, long long a_ld, int a_blocks,
+                                 const uint32_t* __restrict__ b_words, uint8_t* __restrict__ bt, int b_rows,
+                                 int b_cols, long long b_ldw, long long b_ldt) {
+    if ((int)blockIdx.x < a_blocks) {
+        const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        const int nw = (a_cols + 31) / 32;
+        if (t >= (long long)a_rows * nw) return;
+        const int r = (int)(t / nw), wi = (int)(t % nw);
+        const uint32_t w = a_words[(long long)r * a_ldw + wi];
+        uint32_t o[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] = (((w >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
+        uint8_t* dst = a_bytes + (long long)r * a_ld + wi * 32;
+        const int valid = a_cols - wi * 32;
+        if (valid >= 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+            reinterpret_cast<uint4*>(dst)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+            reinterpret_cast<uint4*>(dst)[1] = make_uint4(o[4], o[5], o[6], o[7]);
+        } else {
+            const uint8_t* ob = reinterpret_cast<const uint8_t*>(o);
+            for (int c = 0; c < 32 && c < valid; ++c) dst[c] = ob[c];
+        }
+        return;
+    }
+    const long long warp = ((long long)(blockIdx.x - a_blocks) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int kt = (b_rows + 31) / 32, jt = (b_cols + 31) / 32;
+    if (warp >= (long long)kt * jt) return;
+    const int k0 = (int)(warp % kt) * 32, wj = (int)(warp / kt);
+    const int k = k0 + lane;
+    const uint32_t w = k < b_rows ? b_words[(long long)k * b_ldw + wj] : 0u;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, (w >> jj) & 1u);
+        if (lane == jj) mine = m;
+    }
+    const int j = wj * 32 + lane;
+    if (j >= b_cols) return;
+    uint32_t o[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = (((mine >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
+    uint8_t* dst = bt + (long long)j * b_ldt + k0;
+    const int valid = b_rows - k0;
+    if (valid >= 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        reinterpret_cast<uint4*>(dst)[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    } else {
+        const uint8_t* ob = reinterpret_cast<const uint8_t*>(o);
+        for (int c = 0; c < 32 && c < valid; ++c) dst[c] = ob[c];
+    }
+}
+
 __global__ void transpose_u8_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
                                     int rows, int cols, long long ld_in, long long ld_out) {
     __shared__ uint8_t tile[64][65];
@@ -111,6 +167,24 @@ int unpack_bits(const uint32_t* words, uint8_t* bytes, int rows, int cols, long 
     if (rows == 0 || cols == 0) return SMX_OK;
     const long long t = (long long)rows * ((cols + 31) / 32);
     unpack_bits_kernel<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(words, bytes, rows, cols, ld_w, ld);
+    SMX_RETURN_LAUNCH();
+}
+
+// A (a_rows x a_cols bits) -> bytes, and B (b_rows x b_cols bits) -> B^T
+// bytes (b_cols x b_rows), in one launch.
+int unpack_ab(const uint32_t* a_words, uint8_t* a_bytes, int a_rows, int a_cols, long long a_ldw, long long a_ld,
+              const uint32_t* b_words, uint8_t* bt, int b_rows, int b_cols, long long b_ldw, long long b_ldt,
+              cudaStream_t s) {
+    if (a_rows < 0 || a_cols < 0 || a_ld < a_cols || a_ldw * 32 < a_cols) return SMX_E_ARG;
+    if (b_rows < 0 || b_cols < 0 || b_ldt < b_rows || b_ldw * 32 < b_cols) return SMX_E_ARG;
+    const long long ta = (long long)a_rows * ((a_cols + 31) / 32);
+    const long long a_blocks = (ta + 255) / 256;
+    const long long warps = (long long)((b_rows + 31) / 32) * ((b_cols + 31) / 32);
+    const long long b_blocks = (warps * 32 + 255) / 256;
+    if (a_blocks + b_blocks == 0) return SMX_OK;
+    unpack_ab_kernel<<<(unsigned)(a_blocks + b_blocks), 256, 0, s>>>(a_words, a_bytes, a_rows, a_cols, a_ldw, a_ld,
+                                                                   (int)a_blocks, b_words, bt, b_rows, b_cols,
+                                                                   b_ldw, b_ldt);
     SMX_RETURN_LAUNCH();
 }
 
