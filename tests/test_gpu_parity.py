@@ -486,13 +486,22 @@ def test_closure_by_squaring_matches_fw_and_warshall():
     assert engines.closure_by_squaring(bm) == bm.transitive_closure()
 
 
-def test_fw_n16384_block256_matches_squaring():
-    """n >= 16384 takes the 256-vertex pivot block; cross-check the closure with
-    the independent repeated-squaring algorithm and the Bellman fixpoint."""
+@pytest.mark.parametrize("block", [512, 256])
+def test_fw_n16384_matches_squaring(block):
+    """n >= 16384 takes the 512-vertex pivot block by default (256 forced here
+    too); cross-check the closure with the independent repeated-squaring
+    algorithm and the Bellman fixpoint."""
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
     cfg = workloads.CONFIGS["c5_fw_u16"]
     (t,) = workloads.make_inputs(cfg, 16384)
     a = lane("anti", t, 16384, 16)
-    c = a.transitive_closure()
+    old = lib.smx_set_fw_block(block)
+    try:
+        assert lib.smx_fw_block_for(16384, 2) == block
+        c = a.transitive_closure()
+    finally:
+        lib.smx_set_fw_block(old)
     assert (a | (c * a)) == c
     assert engines.closure_by_squaring(a) == c
 
