@@ -361,7 +361,8 @@ def run_ours(args, world, rank, local_rank):
                 pin_out.copy_(out, non_blocking=True)
             h2d = (pa.numel() + pb.numel()) * pa.element_size()
             d2h = pin_out.numel() * pin_out.element_size()
-        e2e_step()
+        for _ in range(3):   # warm-up (see the N = 1 e2e below)
+            e2e_step()
         barrier()
         es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e2e_steps = 2
@@ -479,7 +480,11 @@ def run_ours(args, world, rank, local_rank):
             h2d = (pa.numel() + pb.numel()) * pa.element_size()
             d2h = res_host.numel() * res_host.element_size()
         e2e_steps = 2 if n >= 16384 else 5
-        e2e_step()
+        # 3 warm-up calls: the caching allocator hands the step's input and
+        # result buffers out in an alternating order, so the library records
+        # one replay graph per buffer layout before the timed steps
+        for _ in range(3):
+            e2e_step()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
