@@ -94,9 +94,10 @@ int smx_fw_u32(uint32_t* T, int n, int ld, int kind, void* workspace, size_t ws_
  * previous setting. */
 int smx_set_fw_lookahead(int enable);
 /* Graph replay of multi-launch calls (smx_fw_*, smx_bool_warshall_bits,
- * smx_bool_mul_tc): the first call with a given (entry, pointers, sizes,
- * switches) records its launches into a CUDA graph, later identical calls
- * replay it with one cudaGraphLaunch on `stream` (16 graphs kept, LRU).
+ * smx_bool_warshall_i8, smx_bool_mul_tc): the first call with a given
+ * (entry, pointers, sizes, switches) launches eagerly, the second records its
+ * launches into a CUDA graph, later identical calls replay it with one
+ * cudaGraphLaunch on `stream` (16 graphs kept, LRU).
  * Calls on a stream that is itself being captured run eagerly into the
  * caller's capture.  1 = on (default), 0 = always launch eagerly.  Results
  * are identical.  Returns the previous setting. */
