@@ -177,6 +177,10 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
 
     if (threadIdx.x == 0) {
         // ---- TMA producer ----
+        // Programmatic dependent launch (bool_mul_tc): everything above ran
+        // while the operand-unpack kernel was still finishing; the operands
+        // are read only after it completes.  A no-op without the attribute.
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % kTcStages;
             const uint32_t ph = (kb / kTcStages) & 1;
@@ -304,7 +308,7 @@ static int make_map(CUtensorMap* map, const uint8_t* base, int rows, int cols, l
 
 template <int BN>
 static int launch_tc(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long long lda, long long ldbt,
-                     cudaStream_t s) {
+                     cudaStream_t s, bool pdl = false) {
     CUtensorMap mA, mB;
     SMX_TRY(make_map(&mA, A, a.M, a.K, lda, kTcBM));
     SMX_TRY(make_map(&mB, Bt, a.N, a.K, ldbt, BN));
@@ -340,13 +344,30 @@ static int launch_tc(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long 
         if (e != cudaSuccess) return (int)e;
     }
     dim3 grid(ceil_div(a.N, BN), mtiles, splits);
-    kern<<<grid, kTcThreads, smem, s>>>(mA, mB, args);
-    SMX_RETURN_LAUNCH();
+    if (!pdl) {
+        kern<<<grid, kTcThreads, smem, s>>>(mA, mB, args);
+        SMX_RETURN_LAUNCH();
+    }
+    // overlap this kernel's launch and prologue (barriers, TMEM allocation,
+    // descriptor prefetch) with the tail of the preceding kernel
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    count_launch();
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mB, args);
+    return e == cudaSuccess ? SMX_OK : (int)e;
 }
 
 int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbits, int M, int N, int K,
                  long long lda, long long ldbt, long long ldc, int accumulate, int skip_row0, int skip_rows,
-                 cudaStream_t s) {
+                 cudaStream_t s, bool pdl = false) {
     if (M < 0 || N < 0 || K < 1 || (C == nullptr) == (Cbits == nullptr)) return SMX_E_ARG;
     if (M == 0 || N == 0) return SMX_OK;
     if (!aligned16(A) || !aligned16(Bt) || (lda & 15) || (ldbt & 15)) return SMX_E_ALIGN;
@@ -362,9 +383,9 @@ int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbit
     }
     // widest tile that still gives every SM a tile
     const long long rows = ceil_div(M, kTcBM) - a.skip_tiles;
-    if (rows * ceil_div(N, 256) >= 148) return launch_tc<256>(A, Bt, a, lda, ldbt, s);
-    if (rows * ceil_div(N, 128) >= 148) return launch_tc<128>(A, Bt, a, lda, ldbt, s);
-    return launch_tc<64>(A, Bt, a, lda, ldbt, s);
+    if (rows * ceil_div(N, 256) >= 148) return launch_tc<256>(A, Bt, a, lda, ldbt, s, pdl);
+    if (rows * ceil_div(N, 128) >= 148) return launch_tc<128>(A, Bt, a, lda, ldbt, s, pdl);
+    return launch_tc<64>(A, Bt, a, lda, ldbt, s, pdl);
 }
 
 // ---- Warshall on bytes with tensor-core phases 2/3 -----------------------------
@@ -523,7 +544,8 @@ int bool_mul_tc(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int N,
             cudaError_t e = cudaMemset2DAsync(C + nw, ldc_w * 4, 0, (ldc_w - nw) * 4, M, st);
             if (e != cudaSuccess) return (int)e;
         }
-        return bool_i8_gemm(a8, bt8, nullptr, C, M, N, K, round16(K), round16(K), ldc_w, 0, 0, 0, st);
+        return bool_i8_gemm(a8, bt8, nullptr, C, M, N, K, round16(K), round16(K), ldc_w, 0, 0, 0, st,
+                            /*pdl=*/ldc_w == nw);
     });
 }
 
