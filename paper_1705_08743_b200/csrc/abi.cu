@@ -48,6 +48,11 @@ int& launch_priority() {
     return prio;
 }
 
+bool& launch_pdl_next() {
+    thread_local bool pdl = false;
+    return pdl;
+}
+
 int side_stream(SideStream** out) {
     static SideStream per_dev[64];
     static std::mutex mu;

@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_bits_gemm_kernel
     __shared__ uint32_t As[2][BM];            // one A word (32 k) per row
     __shared__ __align__(16) uint32_t Bs[2][32][BNW];
 
+    pdl_wait();   // PDL launches: the preceding kernel's output is read below
     const int tid = threadIdx.x;
     int mt = blockIdx.y;
     if (mt >= p.skip_tile0) mt += p.skip_tiles;
@@ -275,6 +276,7 @@ static int bool_block_for_n(int n) { return n >= kBoolBlock512MinN ? 512 : kWars
 // Column-panel snapshot of `cols` words for all rows (one thread per word).
 __global__ void copy_words_kernel(const uint32_t* __restrict__ src, long long ld, uint32_t* __restrict__ dst,
                                   long long ldd, int rows, int cols) {
+    pdl_wait();
     const long long total = (long long)rows * cols;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
@@ -305,6 +307,7 @@ static int bits_pivot_and_row_panel(uint32_t* T, int n, long long ld_w, uint32_t
     const int kw0 = k0 / 32, nw = (n + 31) / 32;
     uint32_t* rowK = T + (long long)k0 * ld_w;
     SMX_TRY(launch_bool_pivot(rowK + kw0, bb, ld_w, s));
+    PdlNext pdl;   // the row panel directly follows the pivot kernel
     // Row panel in place, no snapshot: T[K,:] |= P* . T[K,:] with P* = T[K,K]
     // closed.  A CTA may read rows K that another CTA has already OR-ed into;
     // those bits are paths through K, and P* . (T[K,:] | P* . T[K,:]) =
@@ -376,7 +379,10 @@ static int bool_warshall_schedule(uint32_t* T, int n, long long ld_w, uint32_t* 
             }
             if ((e = cudaEventRecord(ss->join, ss->side)) != cudaSuccess) return (int)e;
             SMX_TRY(bool_bits_gemm(CP, rowK, T, n, nw, bb, ldcp, ld_w, ld_w, 1, k0, bb + bb1, s));
-            SMX_TRY(copy_words(T + k1 / 32, ld_w, CP, ldcp, n, (bb1 + 31) / 32, s));
+            {
+                PdlNext pdl;   // the column-panel copy directly follows 3b
+                SMX_TRY(copy_words(T + k1 / 32, ld_w, CP, ldcp, n, (bb1 + 31) / 32, s));
+            }
             if ((e = cudaStreamWaitEvent(s, ss->join, 0)) != cudaSuccess) return (int)e;
         } else {
             SMX_TRY(bool_bits_gemm(CP, rowK, T, n, nw, bb, ldcp, ld_w, ld_w, 1, k0, bb, s));

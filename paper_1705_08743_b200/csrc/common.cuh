@@ -45,11 +45,25 @@ struct PriorityScope {
     explicit PriorityScope(int p) : old(launch_priority()) { launch_priority() = p; }
     ~PriorityScope() { launch_priority() = old; }
 };
+// Programmatic dependent launch for the next launch_kernel call on this
+// thread (consumed by it): the kernel may start while the preceding kernel in
+// the stream finishes, and must execute griddepcontrol.wait (pdl_wait())
+// before touching anything that kernel writes.  Only for a kernel that
+// directly follows another kernel in the same stream.
+bool& launch_pdl_next();
+struct PdlNext {   // scoped: a path that launches nothing leaves no stale flag
+    PdlNext() { launch_pdl_next() = true; }
+    ~PdlNext() { launch_pdl_next() = false; }
+};
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                                  Args&&... args) {
     const int prio = launch_priority();
-    if (prio == 0) {
+    const bool pdl = launch_pdl_next();
+    launch_pdl_next() = false;
+    if (prio == 0 && !pdl) {
         kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
         return cudaGetLastError();
     }
@@ -58,11 +72,20 @@ inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, 
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributePriority;
-    attr[0].val.priority = prio;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (prio != 0) {
+        attr[na].id = cudaLaunchAttributePriority;
+        attr[na].val.priority = prio;
+        ++na;
+    }
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

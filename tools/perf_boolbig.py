@@ -3,7 +3,7 @@ import sys, json
 sys.path.insert(0, "/root/repo")
 import numpy as np, torch
 from paper_1705_08743_b200 import BoolMatrix, engines
-def timeit(fn, iters=3, warm=1):
+def timeit(fn, iters=3, warm=3):
     for _ in range(warm): fn()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
