@@ -109,7 +109,15 @@ def require_cuda(device=None) -> torch.device:
     return dev
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_ptr(device: torch.device | None = None) -> int:
+    """cudaStream_t of torch's current stream on `device` (the raw accessor
+    costs 0.1 us per call against 2 us for current_stream().cuda_stream)."""
+    if _raw_stream is not None:
+        idx = device.index if isinstance(device, torch.device) else device
+        return _raw_stream(torch.cuda.current_device() if idx is None else idx)
     return torch.cuda.current_stream(device).cuda_stream
 
 

@@ -17,6 +17,21 @@ from ._native import SMX_ANTI, SMX_DIST, check, lib, stream_ptr
 _GEMM = {8: "smx_semiring_gemm_u8", 16: "smx_semiring_gemm_u16", 32: "smx_semiring_gemm_u32"}
 _FW = {8: "smx_fw_u8", 16: "smx_fw_u16", 32: "smx_fw_u32"}
 _TC_WS: dict = {}   # (M, N, K) -> smx_bool_mul_tc_workspace_bytes
+_SCRATCH: dict = {}  # (device index, stream) -> grow-only scratch
+
+
+def _stream_scratch(device: torch.device, sp: int, nbytes: int) -> torch.Tensor:
+    """Per-(device, stream) grow-only scratch (<= 64 MB) for the one-call product:
+    calls on one stream are ordered, so the buffer can be reused, which saves
+    an allocator round trip per call.  Fresh (not kept) inside a stream
+    capture, whose graph may later replay on another stream."""
+    if nbytes > (64 << 20) or torch.cuda.is_current_stream_capturing():
+        return _native.workspace(nbytes, device)   # large: the allocation cost is noise
+    key = (device.index, sp)
+    buf = _SCRATCH.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = _SCRATCH[key] = _native.workspace(nbytes, device)
+    return buf
 
 
 def lane_mul(a: torch.Tensor, b: torch.Tensor, inner: int, width: int, anti: bool,
@@ -86,10 +101,11 @@ def bool_mul_tc(a, b):
     nbytes = _TC_WS.get(key)
     if nbytes is None:
         nbytes = _TC_WS[key] = L.smx_bool_mul_tc_workspace_bytes(a.rows, b.cols, a.cols)
-    ws = _native.workspace(nbytes, a.device)
+    sp = stream_ptr(a.device)
+    ws = _stream_scratch(a.device, sp, nbytes)
     check(L.smx_bool_mul_tc(a._words.data_ptr(), b._words.data_ptr(), out.data_ptr(), a.rows, b.cols,
                             a.cols, a.stride_words, b.stride_words, out.shape[1], ws.data_ptr(), nbytes,
-                            stream_ptr(a.device)), "smx_bool_mul_tc")
+                            sp), "smx_bool_mul_tc")
     return BoolMatrix(a.rows, b.cols, out)
 
 

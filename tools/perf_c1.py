@@ -35,3 +35,15 @@ with torch.cuda.stream(s2):
         for _ in range(20): direct()
 res["device_per_call_us (20 calls in one graph)"] = timeit(g.replay, 20, 3) / 20
 print(json.dumps(res, indent=1))
+
+# host-side cost per call (no sync inside the loop): if it exceeds the GPU
+# time per call, the public call is host-bound
+import time
+for name, fn in (("public", lambda: ma * mb), ("engine", lambda: engines.bool_mul_tc(ma, mb)), ("direct", direct)):
+    for _ in range(50): fn()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(500): fn()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    print(f"host_us_per_call {name}: {(t1 - t0) / 500 * 1e6:.2f}")
