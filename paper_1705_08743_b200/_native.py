@@ -8,7 +8,7 @@ missing, every matrix operation raises.
 from __future__ import annotations
 
 import ctypes
-from ctypes import c_int, c_int64, c_longlong, c_size_t, c_void_p, POINTER
+from ctypes import c_int, c_longlong, c_size_t, c_void_p, POINTER
 
 import torch
 

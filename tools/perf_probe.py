@@ -5,7 +5,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import ctypes
 import numpy as np
 import torch
-from paper_1705_08743_b200 import _native, engines, workloads, AntidistMatrix, BoolMatrix
+from paper_1705_08743_b200 import _native, engines, workloads, BoolMatrix
 
 def timeit(fn, iters=5, warm=2):
     for _ in range(warm): fn()
