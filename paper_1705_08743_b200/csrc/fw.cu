@@ -493,11 +493,17 @@ int fw_run_lookahead_packed(T* Tm, int n, long long ld, int kind, T* RP, void* p
             if ((e = cudaStreamWaitEvent(fs->side, fs->fork, 0)) != cudaSuccess) return (int)e;
             {
                 PriorityScope ps(fs->priority);
+#ifdef SMX_TRACE_SIDE   // development builds: side-chain spans as trace entries with cells = -1
+                trace_begin(fs->side, -1);
+#endif
                 // 3a: the next pivot block's rows
                 SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / PackedCfg<T>::BM,
                                       ceil_div(bb1, PackedCfg<T>::BM), 0, 0, pws, pws_bytes, fs->side));
                 if ((e = cudaEventRecord(fs->aux, fs->side)) != cudaSuccess) return (int)e;
                 SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
+#ifdef SMX_TRACE_SIDE
+                trace_end(fs->side);
+#endif
             }
             if ((e = cudaEventRecord(fs->join, fs->side)) != cudaSuccess) return (int)e;
             // 3b: everything else (skips K_r and K_{r+1}, adjacent tiles)
