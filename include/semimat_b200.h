@@ -87,6 +87,31 @@ int smx_fw_u16(uint16_t* T, int n, int ld, int kind, void* workspace, size_t ws_
 int smx_fw_u32(uint32_t* T, int n, int ld, int kind, void* workspace, size_t ws_bytes,
                void* stream);
 
+/* Closure of a matrix held in HOST memory: the same result as
+ * copying host_in (n x ld, row-major, the reference's padded layout) into T,
+ * smx_fw_*, and copying T back into host_out -- the user-visible work of
+ * AntidistMatrix(.., data).transitive_closure().data (antidist.py:263-273)
+ * -- with the two PCIe copies overlapped with the closure: rows are copied
+ * in group by group and enter the rounds as they arrive, and the last rows'
+ * result is copied out chunk by chunk while the rest finishes (fw.cu,
+ * fw_host_run).  T (device, n x ld) is the working matrix and holds the
+ * closure afterwards too.  host_out may equal host_in.  Stream-ordered:
+ * host_out is complete once `stream` reaches the end of the call.  Page-locked
+ * host buffers give the overlap; pageable ones work but copy synchronously.
+ * `workspace`: smx_fw_host_workspace_bytes(n, ld, elem_bytes) bytes. */
+size_t smx_fw_host_workspace_bytes(int n, int ld, int elem_bytes);
+int smx_fw_host_u8(const uint8_t* host_in, uint8_t* host_out, uint8_t* T, int n, int ld, int kind,
+                   void* workspace, size_t ws_bytes, void* stream);
+int smx_fw_host_u16(const uint16_t* host_in, uint16_t* host_out, uint16_t* T, int n, int ld,
+                    int kind, void* workspace, size_t ws_bytes, void* stream);
+/* Streamed schedule of smx_fw_host_*: 0 = never (copy in, close, copy out),
+ * 1 = automatic (default: from n = 16384), 2 = whenever the closure has at
+ * least 8 pivot blocks.  Results are identical.  Returns the previous mode
+ * (or SMX_E_ARG). */
+int smx_set_fw_host_stream(int mode);
+int smx_fw_host_u32(const uint32_t* host_in, uint32_t* host_out, uint32_t* T, int n, int ld,
+                    int kind, void* workspace, size_t ws_bytes, void* stream);
+
 /* smx_fw_* overlap each pivot block's phase 1/2 with the previous round's
  * phase 3 on an internal high-priority side stream (forked from and joined
  * back into `stream` with events, so it is graph-capturable).  Passing 0

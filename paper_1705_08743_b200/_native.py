@@ -40,6 +40,11 @@ _SIGS = {
     "smx_fw_u8": ([c_void_p, c_int, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),
     "smx_fw_u16": ([c_void_p, c_int, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),
     "smx_fw_u32": ([c_void_p, c_int, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),
+    "smx_set_fw_host_stream": ([c_int], c_int),
+    "smx_fw_host_workspace_bytes": ([c_int, c_int, c_int], c_size_t),
+    "smx_fw_host_u8": ([c_void_p] * 3 + [c_int] * 3 + [c_void_p, c_size_t, c_void_p], c_int),
+    "smx_fw_host_u16": ([c_void_p] * 3 + [c_int] * 3 + [c_void_p, c_size_t, c_void_p], c_int),
+    "smx_fw_host_u32": ([c_void_p] * 3 + [c_int] * 3 + [c_void_p, c_size_t, c_void_p], c_int),
     "smx_fw_block": ([c_int], c_int),
     "smx_fw_pivot": ([c_void_p, c_int, c_int, c_int, c_int, c_void_p], c_int),
     "smx_bool_gemm_bits": ([c_void_p] * 3 + [c_int] * 7 + [c_void_p], c_int),

@@ -246,6 +246,25 @@ class _LaneMatrix:
         out.transitive_close()
         return out
 
+    @classmethod
+    def closure_of_host(cls, data, width: int, out=None):
+        """``cls(n, n, width, data).transitive_closure()`` for a square matrix
+        in host memory, with its result also copied back to host memory, in
+        one library call (smx_fw_host_*) whose PCIe copies overlap the
+        closure.  ``data``: the padded lane storage (n x padded) as a CPU
+        tensor (page-locked for the overlap) or array; ``out``: optional CPU
+        tensor of the same shape to receive the result.  Returns
+        (closure matrix on the device, host result); the host result is
+        complete after ``torch.cuda.current_stream().synchronize()``."""
+        host = data if isinstance(data, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(data))
+        lanes = lane_count(width)
+        n = host.shape[0]
+        if host.dim() != 2 or host.shape[1] != -(-n // lanes) * lanes or host.dtype != _TORCH[width]:
+            raise ValueError("backing array does not match the padded shape")
+        from . import engines
+        res, dev = engines.lane_close_host(host.contiguous(), n, width, anti=not cls._PAD_IS_LIMIT, out=out)
+        return cls(n, n, width, dev), res
+
 
 class AntidistMatrix(_LaneMatrix):
     """Matrix of anti-distance values (antidist.py:173-273)."""

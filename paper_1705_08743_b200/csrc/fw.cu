@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
+#include <vector>
 
 #include "semiring_packed.cuh"
 
@@ -472,22 +474,30 @@ int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, void* p
 // pack A(r+1) reads rows K_{r+1} while the side stream may still rewrite
 // them, but only tiles of rows K_{r+2} (3a) and of rows outside K_{r+1} u
 // K_{r+2} (3b) are read in round r+1, as with the CP copy of fw_run_lookahead.
+//
+// Rounds [ra, rb) over the row window [lo, hi) (the whole closure: rows
+// [0, n), rounds [0, R)).  Every pivot block of those rounds lies inside the
+// window; lo is a multiple of the 128-row tile, hi one too or n.  Rows
+// outside the window are neither read as A nor written (the host-streamed
+// closure below runs rounds on the rows that have arrived so far).
 template <typename T>
-int fw_run_lookahead_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, size_t pws_bytes,
-                            cudaStream_t s) {
+int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, size_t pws_bytes, int lo, int hi,
+                     int ra, int rb, cudaStream_t s) {
+    using G = PackedCfg<T>;
     SideStream* fs = nullptr;
     SMX_TRY(side_stream(&fs));
     const int BLK = fw_block_for_n<T>(n);
-    const int R = (n + BLK - 1) / BLK;
     auto blk = [&](int r) { return n - r * BLK < BLK ? n - r * BLK : BLK; };
-    SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, 0, blk(0), s));
-    SMX_TRY(packed_pack<T>(Tm, nullptr, n, n, blk(0), ld, ld, kind, pws, pws_bytes, s));
+    const int t0 = lo / G::BM, tiles = ceil_div(hi, G::BM) - t0;
+    if (ra >= rb) return SMX_OK;
+    SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, ra * BLK, blk(ra), s));
+    SMX_TRY(packed_pack_a_rows<T>(Tm + ra * BLK, n, n, blk(ra), ld, kind, pws, pws_bytes, t0, tiles, s));
     cudaError_t e;
-    for (int r = 0; r < R; ++r) {
+    for (int r = ra; r < rb; ++r) {
         const int k0 = r * BLK, bb = blk(r);
         T* rowK = Tm + (long long)k0 * ld;
         SMX_TRY(packed_pack<T>(nullptr, rowK, n, n, bb, ld, ld, kind, pws, pws_bytes, s));
-        if (r + 1 < R) {
+        if (r + 1 < rb) {
             const int k1 = k0 + BLK, bb1 = blk(r + 1);
             if ((e = cudaEventRecord(fs->fork, s)) != cudaSuccess) return (int)e;
             if ((e = cudaStreamWaitEvent(fs->side, fs->fork, 0)) != cudaSuccess) return (int)e;
@@ -497,8 +507,8 @@ int fw_run_lookahead_packed(T* Tm, int n, long long ld, int kind, T* RP, void* p
                 trace_begin(fs->side, -1);
 #endif
                 // 3a: the next pivot block's rows
-                SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / PackedCfg<T>::BM,
-                                      ceil_div(bb1, PackedCfg<T>::BM), 0, 0, pws, pws_bytes, fs->side));
+                SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / G::BM, ceil_div(bb1, G::BM), 0, 0, pws,
+                                      pws_bytes, fs->side));
                 if ((e = cudaEventRecord(fs->aux, fs->side)) != cudaSuccess) return (int)e;
                 SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
 #ifdef SMX_TRACE_SIDE
@@ -506,20 +516,27 @@ int fw_run_lookahead_packed(T* Tm, int n, long long ld, int kind, T* RP, void* p
 #endif
             }
             if ((e = cudaEventRecord(fs->join, fs->side)) != cudaSuccess) return (int)e;
-            // 3b: everything else (skips K_r and K_{r+1}, adjacent tiles)
-            trace_begin(s, (long long)(n - bb - bb1) * n * bb);
-            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, 0, -1, k0, bb + bb1, pws, pws_bytes, s));
+            // 3b: everything else in the window (skips K_r and K_{r+1}, adjacent tiles)
+            trace_begin(s, (long long)(hi - lo - bb - bb1) * n * bb);
+            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, t0, tiles, k0, bb + bb1, pws, pws_bytes, s));
             trace_end(s);
             if ((e = cudaStreamWaitEvent(s, fs->aux, 0)) != cudaSuccess) return (int)e;
-            SMX_TRY(packed_pack<T>(Tm + k1, nullptr, n, n, bb1, ld, ld, kind, pws, pws_bytes, s));
+            SMX_TRY(packed_pack_a_rows<T>(Tm + k1, n, n, bb1, ld, kind, pws, pws_bytes, t0, tiles, s));
             if ((e = cudaStreamWaitEvent(s, fs->join, 0)) != cudaSuccess) return (int)e;
         } else {
-            trace_begin(s, (long long)(n - bb) * n * bb);
-            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, 0, -1, k0, bb, pws, pws_bytes, s));
+            trace_begin(s, (long long)(hi - lo - bb) * n * bb);
+            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, t0, tiles, k0, bb, pws, pws_bytes, s));
             trace_end(s);
         }
     }
     return SMX_OK;
+}
+
+template <typename T>
+int fw_run_lookahead_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, size_t pws_bytes,
+                            cudaStream_t s) {
+    const int BLK = fw_block_for_n<T>(n);
+    return fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, pws_bytes, 0, n, 0, (n + BLK - 1) / BLK, s);
 }
 
 template <typename T>
@@ -580,6 +597,213 @@ int fw_run_serial(T* Tm, int n, long long ld, int kind, T* RP, T* CP, void* pws,
         trace_end(s);
     }
     return SMX_OK;
+}
+
+// ---- closure of a host matrix (smx_fw_host_*) -------------------------------
+// Host in -> device -> closure -> host out in one call, with the PCIe copies
+// hidden behind the closure instead of before and after it.  Two exact
+// identities let rows enter and leave the computation at different times
+// (d_X(i, x): shortest walk i -> x with >= 1 edge and intermediates in X;
+// rows are in distance form, saturation commutes with both: SURVEY 0.1 fact 2):
+//
+//  * ingest (first vertex of [0, s) on the walk): rows that arrive after the
+//    rows [0, s) were closed over intermediates [0, s) catch up with ONE
+//    product of K = s,
+//        T[G, :] (+)= T[G, 0:s] (x) T[0:s, :],
+//    then join the ordinary rounds.  A walk i -> x through [0, s) leaves i by
+//    a single edge (i, l), l the first vertex of [0, s) on it, and continues
+//    as a walk l -> x over [0, s): that is T[i, l] (x) d_[0,s)(l, x).
+//  * egress (first vertex of L on the walk): once the last rows L are
+//    closed (their own rounds, on rows L only), every other row finishes with
+//    ONE product of K = |L|,
+//        T[i, :] (+)= T[i, L] (x) T[L, :],
+//    T[i, L] closed over [0, n) \ L: the walk i -> l (l the first vertex of L)
+//    avoids L, the rest l -> x is anything.  So rows [0, n) \ L finish chunk
+//    by chunk, and each chunk's D2H starts as soon as its product is done.
+// Any in-place update that a later K-block of the same product reads is the
+// weight of a real walk of the same kind, so it can only tighten towards the
+// exact value (the argument of fw_pivot_and_row_panel).  Every (row, pivot)
+// pair is still applied exactly once: no extra work.
+//
+// Rows arrive in groups [0, B), [B, 2B), [2B, 4B), ... [8B, 16B), [16B, 64B),
+// ..., the last one running to n; the main stream waits for each group's H2D event only when
+// it needs that group, so the copy engine and the SMs run concurrently.  The
+// products run one pivot block of K per launch, like phase 3: with K = 512
+// the packed operands of a launch (~60 MB) stay in L2, while K = 2048 spills
+// and ran the catch-up products 12% slower (n = 32768: 1080 vs 1040 ms).
+namespace {
+struct CopyStreams {
+    cudaStream_t in = nullptr, out = nullptr;
+    std::vector<cudaEvent_t> ev;
+    std::mutex mu;   // one streamed call at a time per device (shared events)
+};
+int copy_streams(CopyStreams** out) {
+    static CopyStreams per_dev[64];
+    static std::mutex mu;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return (int)e;
+    if (dev < 0 || dev >= 64) return SMX_E_ARG;
+    CopyStreams& c = per_dev[dev];
+    std::lock_guard<std::mutex> lock(mu);
+    if (!c.in) {
+        if ((e = cudaStreamCreateWithFlags(&c.in, cudaStreamNonBlocking)) != cudaSuccess) return (int)e;
+        if ((e = cudaStreamCreateWithFlags(&c.out, cudaStreamNonBlocking)) != cudaSuccess) return (int)e;
+    }
+    *out = &c;
+    return SMX_OK;
+}
+int copy_events(CopyStreams* c, size_t count) {
+    while (c->ev.size() < count) {
+        cudaEvent_t ev;
+        cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return (int)e;
+        c->ev.push_back(ev);
+    }
+    return SMX_OK;
+}
+}  // namespace
+
+// The last four pivot blocks L are closed alone at the end (egress); their
+// four row blocks stay packed as B while the other rows finish.
+constexpr int kFwHostTailBlocks = 4;
+// smx_set_fw_host_stream: 0 = never stream (copy in, close, copy out),
+// 1 = automatic, 2 = stream whenever the closure has >= 8 pivot blocks (tests).
+// Automatic streams from n = 16384: below that the copies are a few ms and
+// the small early windows' rounds, bound by the pivot chain, cost more than
+// the overlap saves (n = 8192: 23.7 ms streamed vs 23.0 ms serial; 16384:
+// 141 vs 152 ms; 32768: 1040 vs 1105 ms, tools/perf_host_fw.py).
+static std::atomic<int> g_fw_host_stream{1};
+
+inline size_t fw_host_slot_bytes(int n, int eb) { return align256(packed_ws_bytes(n, n, fw_block_for(eb))); }
+inline size_t fw_host_ws_bytes(int n, long long ld, int eb) {
+    const size_t base = fw_ws_bytes(n, ld, eb);
+    return eb <= 2 ? base + kFwHostTailBlocks * fw_host_slot_bytes(n, eb) : base;
+}
+
+// Egress chunk boundaries over rows [0, sL): from the end, 1, 1, 2, 4, 8, 16,
+// 16, ... blocks, so each chunk's D2H (0.85 ms per 1024 rows at n = 32768)
+// hides behind the next chunk's product (2 ms per 1024 rows) and only the
+// last block of rows is copied after the final product.
+inline std::vector<int> fw_host_egress_cuts(int sL, int BLK) {
+    std::vector<int> sizes;
+    int left = sL / BLK, next = 1, ones = 0;
+    while (left > 0) {
+        const int take = next < left ? next : left;
+        sizes.push_back(take);
+        left -= take;
+        if (next == 1 && ones++ == 0) continue;   // two single blocks at the end
+        if (next < 16) next *= 2;
+    }
+    std::vector<int> cuts{0};
+    for (auto it = sizes.rbegin(); it != sizes.rend(); ++it) cuts.push_back(cuts.back() + *it * BLK);
+    return cuts;
+}
+
+template <typename T>
+int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes,
+                cudaStream_t s) {
+    using G = PackedCfg<T>;
+    if (n < 0 || ld < n || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
+    if (n == 0) return SMX_OK;
+    if (hin == nullptr || hout == nullptr || Tm == nullptr) return SMX_E_ARG;
+    if (!aligned16(Tm) || !ld_ok(ld, sizeof(T))) return SMX_E_ALIGN;
+    const size_t row_bytes = (size_t)ld * sizeof(T);
+    const int BLK = fw_block_for_n<T>(n);
+    const int R = (n + BLK - 1) / BLK;
+    cudaError_t e;
+    bool streamed = false;
+    if constexpr (sizeof(T) <= 2) {
+        const int mode = g_fw_host_stream.load(std::memory_order_relaxed);
+        streamed = lookahead_enabled() && g_fw_packed && R >= 2 * kFwHostTailBlocks &&
+                   (mode == 2 || (mode == 1 && n >= 16384));
+    }
+    if (!streamed) {   // small or u32: copy in, close, copy out, in stream order
+        if ((e = cudaMemcpyAsync(Tm, hin, (size_t)n * row_bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+            return (int)e;
+        SMX_TRY(fw_run<T>(Tm, n, ld, kind, ws, ws_bytes, s));
+        e = cudaMemcpyAsync(hout, Tm, (size_t)n * row_bytes, cudaMemcpyDeviceToHost, s);
+        return e == cudaSuccess ? SMX_OK : (int)e;
+    }
+    if (ws == nullptr || ws_bytes < fw_host_ws_bytes(n, ld, sizeof(T))) return SMX_E_WORKSPACE;
+    T* RP = reinterpret_cast<T*>(ws);
+    const size_t pws_off = align256((size_t)FwBlock<T>::value * ld * sizeof(T)) +
+                           align256((size_t)n * FwBlock<T>::value * sizeof(T));
+    void* pws = reinterpret_cast<char*>(ws) + pws_off;
+    const size_t slot = fw_host_slot_bytes(n, sizeof(T));
+    auto egress_slot = [&](int j) { return reinterpret_cast<char*>(ws) + fw_ws_bytes(n, ld, sizeof(T)) + j * slot; };
+
+    const int sL = (R - kFwHostTailBlocks) * BLK;   // L = rows [sL, n)
+    std::vector<int> ends;                          // ingest groups; the last one runs to n
+    // Doubling while a group's work (~n r^2 cells) is shorter than the next
+    // group's copy, x4 after that: the SMs never wait on the copy engine
+    // after the first block (n = 32768: 512, 1024, 2048, 4096, 8192, n).
+    for (long long x = BLK; x < sL; x *= (x < 16LL * BLK ? 2 : 4)) ends.push_back((int)x);
+    ends.push_back(n);
+    const std::vector<int> cuts = fw_host_egress_cuts(sL, BLK);
+    const int chunks = (int)cuts.size() - 1;
+
+    CopyStreams* cs = nullptr;
+    SMX_TRY(copy_streams(&cs));
+    std::lock_guard<std::mutex> lock(cs->mu);
+    // events: fork, join, one per group, one per D2H piece (L + chunks)
+    SMX_TRY(copy_events(cs, 2 + ends.size() + 1 + chunks));
+    cudaEvent_t ev_fork = cs->ev[0], ev_join = cs->ev[1];
+    cudaEvent_t* ev_in = cs->ev.data() + 2;
+    cudaEvent_t* ev_out = ev_in + ends.size();
+    if ((e = cudaEventRecord(ev_fork, s)) != cudaSuccess) return (int)e;
+    if ((e = cudaStreamWaitEvent(cs->in, ev_fork, 0)) != cudaSuccess) return (int)e;
+    if ((e = cudaStreamWaitEvent(cs->out, ev_fork, 0)) != cudaSuccess) return (int)e;
+    for (size_t g = 0, r0 = 0; g < ends.size(); r0 = ends[g], ++g) {
+        if ((e = cudaMemcpyAsync(Tm + r0 * ld, hin + r0 * ld, (ends[g] - r0) * row_bytes, cudaMemcpyHostToDevice,
+                                 cs->in)) != cudaSuccess)
+            return (int)e;
+        if ((e = cudaEventRecord(ev_in[g], cs->in)) != cudaSuccess) return (int)e;
+    }
+    auto d2h = [&](int r0, int r1, cudaEvent_t ev) -> int {
+        cudaError_t e2;
+        if ((e2 = cudaEventRecord(ev, s)) != cudaSuccess) return (int)e2;
+        if ((e2 = cudaStreamWaitEvent(cs->out, ev, 0)) != cudaSuccess) return (int)e2;
+        e2 = cudaMemcpyAsync(hout + (size_t)r0 * ld, Tm + (size_t)r0 * ld, (size_t)(r1 - r0) * row_bytes,
+                             cudaMemcpyDeviceToHost, cs->out);
+        return e2 == cudaSuccess ? SMX_OK : (int)e2;
+    };
+
+    for (size_t g = 0, r0 = 0; g < ends.size(); r0 = ends[g], ++g) {
+        const int r1 = ends[g];
+        const int t0 = (int)r0 / G::BM, tiles = ceil_div(r1, G::BM) - t0;
+        if ((e = cudaStreamWaitEvent(s, ev_in[g], 0)) != cudaSuccess) return (int)e;
+        // ingest: T[G, :] (+)= T[G, 0:r0] (x) T[0:r0, :], one pivot block of K per launch
+        for (int k0 = 0; k0 < (int)r0; k0 += BLK) {
+            SMX_TRY(packed_pack<T>(nullptr, Tm + (long long)k0 * ld, n, n, BLK, ld, ld, kind, pws, slot, s));
+            SMX_TRY(packed_pack_a_rows<T>(Tm + k0, n, n, BLK, ld, kind, pws, slot, t0, tiles, s));
+            SMX_TRY(packed_run<T>(Tm, n, n, BLK, ld, kind, 1, t0, tiles, 0, 0, pws, slot, s));
+        }
+        // the group's rounds over every row that has arrived (the last group:
+        // all rows, up to the blocks of L)
+        const int rb = (r1 < n ? r1 : sL) / BLK;
+        SMX_TRY(fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, slot, 0, r1, (int)r0 / BLK, rb, s));
+    }
+    // L: its rounds on rows L alone; then L is final
+    SMX_TRY(fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, slot, sL, n, sL / BLK, R, s));
+    SMX_TRY(d2h(sL, n, ev_out[0]));
+    // egress: rows [0, sL) (+)= T[rows, L] (x) T[L, :]; L's blocks packed once as B
+    for (int j = 0; j < kFwHostTailBlocks; ++j) {
+        const int k0 = sL + j * BLK, bb = n - k0 < BLK ? n - k0 : BLK;
+        SMX_TRY(packed_pack<T>(nullptr, Tm + (long long)k0 * ld, n, n, bb, ld, ld, kind, egress_slot(j), slot, s));
+    }
+    for (int c = 0; c < chunks; ++c) {
+        const int t0 = cuts[c] / G::BM, tiles = ceil_div(cuts[c + 1], G::BM) - t0;
+        for (int j = 0; j < kFwHostTailBlocks; ++j) {
+            const int k0 = sL + j * BLK, bb = n - k0 < BLK ? n - k0 : BLK;
+            SMX_TRY(packed_pack_a_rows<T>(Tm + k0, n, n, bb, ld, kind, egress_slot(j), slot, t0, tiles, s));
+            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, t0, tiles, 0, 0, egress_slot(j), slot, s));
+        }
+        SMX_TRY(d2h(cuts[c], cuts[c + 1], ev_out[1 + c]));
+    }
+    if ((e = cudaEventRecord(ev_join, cs->out)) != cudaSuccess) return (int)e;
+    e = cudaStreamWaitEvent(s, ev_join, 0);
+    return e == cudaSuccess ? SMX_OK : (int)e;
 }
 
 // Bulk row-panel updates of the sharded closure take the packed kernel, its
@@ -723,6 +947,27 @@ int smx_fw_u16(uint16_t* T, int n, int ld, int kind, void* ws, size_t ws_bytes, 
 }
 int smx_fw_u32(uint32_t* T, int n, int ld, int kind, void* ws, size_t ws_bytes, void* stream) {
     return fw_run<uint32_t>(T, n, ld, kind, ws, ws_bytes, as_stream(stream));
+}
+
+size_t smx_fw_host_workspace_bytes(int n, int ld, int elem_bytes) {
+    if (n <= 0 || ld < n) return 0;
+    return fw_host_ws_bytes(n, ld, elem_bytes);
+}
+int smx_set_fw_host_stream(int mode) {
+    if (mode < 0 || mode > 2) return SMX_E_ARG;
+    return g_fw_host_stream.exchange(mode);
+}
+int smx_fw_host_u8(const uint8_t* host_in, uint8_t* host_out, uint8_t* T, int n, int ld, int kind, void* ws,
+                   size_t ws_bytes, void* stream) {
+    return fw_host_run<uint8_t>(host_in, host_out, T, n, ld, kind, ws, ws_bytes, as_stream(stream));
+}
+int smx_fw_host_u16(const uint16_t* host_in, uint16_t* host_out, uint16_t* T, int n, int ld, int kind, void* ws,
+                    size_t ws_bytes, void* stream) {
+    return fw_host_run<uint16_t>(host_in, host_out, T, n, ld, kind, ws, ws_bytes, as_stream(stream));
+}
+int smx_fw_host_u32(const uint32_t* host_in, uint32_t* host_out, uint32_t* T, int n, int ld, int kind, void* ws,
+                    size_t ws_bytes, void* stream) {
+    return fw_host_run<uint32_t>(host_in, host_out, T, n, ld, kind, ws, ws_bytes, as_stream(stream));
 }
 
 }  // extern "C"

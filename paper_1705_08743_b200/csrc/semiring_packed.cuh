@@ -96,11 +96,12 @@ __device__ __forceinline__ uint32_t canon_cell(T x, int anti) {
 template <typename T>
 __global__ void __launch_bounds__(128) pack_a_kernel(const T* __restrict__ A, int M, int K, long long lda,
                                                     int anti, int KT, uint32_t* __restrict__ Ap,
-                                                    uint8_t* __restrict__ fA, const int* __restrict__ cert) {
+                                                    uint8_t* __restrict__ fA, const int* __restrict__ cert,
+                                                    int mt0 = 0) {
     using L = Lane<T>;
     using G = PackedCfg<T>;
     constexpr int BK = G::BK, E = L::kCellsPerChunk, WPC = L::kWordsPerChunk;
-    const int kt = blockIdx.x, mt = blockIdx.y, r = threadIdx.x;
+    const int kt = blockIdx.x, mt = mt0 + blockIdx.y, r = threadIdx.x;
     const int row = mt * G::BM + r, k0 = kt * BK;
     const bool sh = cert != nullptr && *cert != 0;
     uint32_t* dst = Ap + ((size_t)mt * KT + kt) * G::A_TILE_WORDS + r;
@@ -446,6 +447,24 @@ inline int packed_pack(const T* A, const T* B, int M, int N, int K, long long ld
         SMX_LAUNCHED_OR_RETURN();
     }
     return SMX_OK;
+}
+
+// Pack only the A tiles of the 128-row tiles [tile0, tile0 + tiles) of an
+// M x K operand (the workspace keeps the packed_ws_bytes(M, N, K) layout, so
+// packed_run over the same row window reads them).  The host-streamed closure
+// (fw.cu) packs just the rows it is about to update.
+template <typename T>
+inline int packed_pack_a_rows(const T* A, int M, int N, int K, long long lda, int kind, void* ws, size_t ws_bytes,
+                              int tile0, int tiles, cudaStream_t s) {
+    SMX_TRY(packed_check<T>(A, nullptr, M, N, K, lda, lda, kind, ws, ws_bytes));   // (no B: ldb unused)
+    if (M == 0 || N == 0 || K == 0) return SMX_OK;
+    const PackedWs v = packed_views(ws, M, N, K);
+    if (tile0 < 0 || tile0 > v.MT) return SMX_E_ARG;
+    if (tiles < 0 || tile0 + tiles > v.MT) tiles = v.MT - tile0;
+    if (tiles == 0) return SMX_OK;
+    pack_a_kernel<T><<<dim3(v.KT, tiles), 128, 0, s>>>(A, M, K, lda, kind == SMX_ANTI, v.KT, v.Ap, v.fA, nullptr,
+                                                       tile0);
+    SMX_RETURN_LAUNCH();
 }
 
 // C rows (+)= packed A (x) packed B over the 128-row tiles

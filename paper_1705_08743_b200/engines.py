@@ -61,6 +61,33 @@ def lane_close_(t: torch.Tensor, n: int, width: int, anti: bool) -> torch.Tensor
     return t
 
 
+_FW_HOST = {8: "smx_fw_host_u8", 16: "smx_fw_host_u16", 32: "smx_fw_host_u32"}
+
+
+def lane_close_host(host: torch.Tensor, n: int, width: int, anti: bool, out: torch.Tensor | None = None,
+                    device=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Closure of a matrix in host memory into host memory (smx_fw_host_*):
+    the PCIe copies in and out run concurrently with the closure.  `host` and
+    `out` are CPU tensors in the padded lane layout (page-locked for overlap).
+    Returns (out, device copy of the closure); `out` is complete when the
+    current stream reaches this point (synchronize before reading it)."""
+    if host.device.type != "cpu" or not host.is_contiguous():
+        raise ValueError("host matrix must be a contiguous CPU tensor")
+    if out is None:
+        out = torch.empty_like(host, pin_memory=True)
+    if out.shape != host.shape or out.dtype != host.dtype or out.device.type != "cpu" or not out.is_contiguous():
+        raise ValueError("out must be a contiguous CPU tensor shaped like the input")
+    dev = _native.require_cuda(device)
+    t = torch.empty(host.shape, dtype=host.dtype, device=dev)
+    ld = host.shape[1]
+    nbytes = lib().smx_fw_host_workspace_bytes(n, ld, width // 8)
+    ws = _native.workspace(nbytes, dev)
+    check(getattr(lib(), _FW_HOST[width])(host.data_ptr(), out.data_ptr(), t.data_ptr(), n, ld,
+                                          SMX_ANTI if anti else SMX_DIST, ws.data_ptr(), nbytes,
+                                          stream_ptr(dev)), _FW_HOST[width])
+    return out, t
+
+
 def bool_mul_bits(a, b):
     """Bit-packed OR/AND product (the comparison variant); boolmat.py:151-172."""
     from .boolmat import BoolMatrix, _stride_words
