@@ -12,8 +12,10 @@ the closure is row-panel sharded with an NCCL broadcast of each pivot row
 panel (paper_1705_08743_b200/sharded.py) -- strong scaling, fixed n.
 
 Reported beside the device-resident throughput (`value`):
-  e2e          the same metric through the public API with host buffers
-               (pinned H2D of the input + closure + D2H of the result per step)
+  e2e          the same metric through the public API with host buffers:
+               AntidistMatrix.closure_of_host (smx_fw_host_u16) per step, the
+               pinned H2D of the input and D2H of the result overlapped with
+               the closure inside the one call
   roofline     the dominant kernel (FW phase-3 semiring GEMM, 93+% of the
                step) timed live with CUDA events, against the packed-integer
                issue peak measured in this run by smx_int_issue_probe
@@ -481,9 +483,8 @@ def run_ours(args, world, rank, local_rank):
             h2d = (pa.numel() + pb.numel()) * pa.element_size()
             d2h = res_host.numel() * res_host.element_size()
         e2e_steps = 2 if n >= 16384 else 5
-        # 3 warm-up calls: the caching allocator hands the step's input and
-        # result buffers out in an alternating order, so the library records
-        # one replay graph per buffer layout before the timed steps
+        # 3 warm-up calls (the product's public path records one replay graph
+        # per buffer layout the caching allocator hands out)
         for _ in range(3):
             e2e_step()
         torch.cuda.synchronize()
