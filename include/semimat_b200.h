@@ -118,6 +118,10 @@ int smx_fw_host_u32(const uint32_t* host_in, uint32_t* host_out, uint32_t* T, in
  * selects the plain serial schedule; results are identical.  Returns the
  * previous setting. */
 int smx_set_fw_lookahead(int enable);
+/* Pivot tiles of up to 128 vertices (u8/u16): 1 = the blocked kernel (32-
+ * vertex sub-blocks, 7 barriers each; default), 0 = the register kernel (one
+ * barrier per vertex).  Results are identical.  Returns the previous setting. */
+int smx_set_fw_pivot_blocked(int enable);
 /* Graph replay of multi-launch calls (smx_fw_*, smx_bool_warshall_bits,
  * smx_bool_warshall_i8, smx_bool_mul_tc): the first call with a given
  * (entry, pointers, sizes, switches) launches eagerly, the second records its

@@ -155,6 +155,154 @@ fw_pivot_kernel(T* P, int b, long long ld, int anti) {
     }
 }
 
+// Blocked pivot closure (u8/u16 tiles up to 128 vertices): Floyd-Warshall
+// inside one CTA in 32-vertex sub-blocks, on a 32 KB shared-memory tile in
+// distance form.  Per sub-block K:
+//   P1  D = T[K,K] closed by one warp, vertex at a time, rows in registers
+//       and row k broadcast by shuffles (no CTA barrier inside);
+//   P2  T[K,:] (+)= D* (x) T[K,:]      (the row panel, in place);
+//   P3  T[i,:] (+)= T[i,K] (x) T[K,:]  for i outside K (the j in K part is the
+//       column panel: T[K,K] = D* by then).
+// 3 barriers per sub-block instead of one per vertex (fw_pivot_kernel: 128
+// barriers, 58 us), and 512 threads with few registers and 32 KB of shared
+// memory, so it fits on an SM in place of one retired phase-3 CTA instead of
+// waiting for a whole SM to drain.  Every in-place read of a value another
+// thread may already have lowered reads the weight of a real walk of the
+// same kind (the fw_pivot_and_row_panel argument), so any interleaving gives
+// the same bits.
+template <typename T>
+__global__ void __launch_bounds__(512, 3)
+fw_pivot_blocked_kernel(T* P, int b, long long ld, int anti) {
+    using L = Lane<T>;
+    static_assert(L::kCellsPerWord == 2, "u8 / u16 lanes");
+    constexpr int WPR = 64;                 // words per tile row (128 cells)
+    constexpr int APITCH = 34;              // splat rows: 32 k + 2 (no bank conflicts between row slots)
+    __shared__ __align__(16) uint32_t tile[128 * WPR];
+    __shared__ __align__(16) uint32_t As[96 * APITCH];   // P3's A operand, splat, per row slot
+    const int tid = threadIdx.x;
+    auto to_dist = [&](uint32_t v) { return anti ? (L::kS - v) : v; };
+    auto cell = [&](int r, int c) {         // one cell of the tile
+        const uint32_t w = tile[r * WPR + (c >> 1)];
+        return (c & 1) ? (w >> 16) : (w & 0xFFFFu);
+    };
+    // 8 global loads of a thread in flight at a time, then their tile stores
+    for (int i0 = 0; i0 < 128 * WPR / 512; i0 += 4) {
+        uint32_t v[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int w = tid + (i0 + i) * 512, r = w / WPR, c = (w % WPR) * 2;
+            v[2 * i] = (r < b && c < b) ? (uint32_t)P[(long long)r * ld + c] : 0u;
+            v[2 * i + 1] = (r < b && c + 1 < b) ? (uint32_t)P[(long long)r * ld + c + 1] : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int w = tid + (i0 + i) * 512, r = w / WPR, c = (w % WPR) * 2;
+            const uint32_t v0 = (r < b && c < b) ? to_dist(v[2 * i]) : L::kS;
+            const uint32_t v1 = (r < b && c + 1 < b) ? to_dist(v[2 * i + 1]) : L::kS;
+            tile[w] = v0 | (v1 << 16);
+        }
+    }
+    __syncthreads();
+    const int nsb = (b + 31) / 32;
+    const int g = tid >> 4, q = tid & 15;   // 32 row slots x 16 word slots
+    for (int kb = 0; kb < nsb; ++kb) {
+        const int K0 = kb * 32, KW0 = kb * 16;
+        // P1: warp 0 closes D with the vertex-at-a-time sweep, lane j holding
+        // D's row j (16 words) in registers; row k reaches the other lanes by
+        // shuffles, so the 32 steps need no CTA barrier (row k does not change
+        // during step k: T[k][k] >= 0 in distance form)
+        if (tid < 32) {
+            uint32_t w[16];
+            const uint4* src = reinterpret_cast<const uint4*>(&tile[(K0 + tid) * WPR + KW0]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint4 v = src[i];
+                w[4 * i] = v.x; w[4 * i + 1] = v.y; w[4 * i + 2] = v.z; w[4 * i + 3] = v.w;
+            }
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const uint32_t e = (w[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
+                const uint32_t a = L::splat(e), sa = L::splat(L::kS - e);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) w[i] = L::step(w[i], __shfl_sync(0xFFFFFFFFu, w[i], k), a, sa);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(&tile[(K0 + tid) * WPR + KW0]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+        }
+        __syncthreads();
+        // P2: row K0 + g, words 4q .. 4q + 3
+        {
+            uint4* rw = reinterpret_cast<uint4*>(&tile[(K0 + g) * WPR + 4 * q]);
+            uint4 acc = *rw;
+#pragma unroll 4
+            for (int k = 0; k < 32; ++k) {
+                const uint32_t e = cell(K0 + g, K0 + k);
+                const uint32_t a = L::splat(e), sa = L::splat(L::kS - e);
+                const uint4 bw = *reinterpret_cast<const uint4*>(&tile[(K0 + k) * WPR + 4 * q]);
+                acc.x = L::step(acc.x, bw.x, a, sa);
+                acc.y = L::step(acc.y, bw.y, a, sa);
+                acc.z = L::step(acc.z, bw.z, a, sa);
+                acc.w = L::step(acc.w, bw.w, a, sa);
+            }
+            *rw = acc;
+        }
+        // P3's A operand: splat(T[i][K0 + k]) for the 96 rows outside K (not
+        // written by P2), one LDS.64 per row and k pair in the P3 loop
+#pragma unroll
+        for (int i = 0; i < 96 * 32 / 512; ++i) {
+            const int x = tid + i * 512, slot = x >> 5, k = x & 31;
+            const int row = slot < K0 ? slot : slot + 32;
+            As[slot * APITCH + k] = L::splat(cell(row, K0 + k));
+        }
+        __syncthreads();
+        // P3: rows outside K, three per thread (96 rows), words 4q .. 4q + 3
+        {
+            int rows[3];
+            uint4 acc[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const int idx = 3 * g + i;
+                rows[i] = idx < K0 ? idx : idx + 32;
+                acc[i] = *reinterpret_cast<const uint4*>(&tile[rows[i] * WPR + 4 * q]);
+            }
+            const bool live = rows[0] < b;   // rows[] ascend: all padding beyond
+#pragma unroll 2
+            for (int kk = 0; kk < 16 && live; ++kk) {
+                const uint4 b0 = *reinterpret_cast<const uint4*>(&tile[(K0 + 2 * kk) * WPR + 4 * q]);
+                const uint4 b1 = *reinterpret_cast<const uint4*>(&tile[(K0 + 2 * kk + 1) * WPR + 4 * q]);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const uint2 av = *reinterpret_cast<const uint2*>(&As[(3 * g + i) * APITCH + 2 * kk]);
+                    const uint32_t a0 = av.x, s0 = L::kIdentityWord - av.x;   // splat(S - e)
+                    const uint32_t a1 = av.y, s1 = L::kIdentityWord - av.y;
+                    acc[i].x = L::step(L::step(acc[i].x, b0.x, a0, s0), b1.x, a1, s1);
+                    acc[i].y = L::step(L::step(acc[i].y, b0.y, a0, s0), b1.y, a1, s1);
+                    acc[i].z = L::step(L::step(acc[i].z, b0.z, a0, s0), b1.z, a1, s1);
+                    acc[i].w = L::step(L::step(acc[i].w, b0.w, a0, s0), b1.w, a1, s1);
+                }
+            }
+            if (live) {
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    *reinterpret_cast<uint4*>(&tile[rows[i] * WPR + 4 * q]) = acc[i];
+            }
+        }
+        __syncthreads();
+    }
+    for (int w = tid; w < 128 * WPR; w += 512) {
+        const int r = w / WPR, c = (w % WPR) * 2;
+        if (r >= b || c >= b) continue;
+        const uint32_t v = tile[w];
+        P[(long long)r * ld + c] = (T)(anti ? (L::kS - (v & 0xFFFFu)) : (v & 0xFFFFu));
+        if (c + 1 < b) P[(long long)r * ld + c + 1] = (T)(anti ? (L::kS - (v >> 16)) : (v >> 16));
+    }
+}
+
+// smx_set_fw_pivot_blocked: u8/u16 pivot tiles <= 128 on the blocked kernel
+// (default) or on the one-barrier-per-vertex register kernel.
+static std::atomic<int> g_pivot_blocked{1};
+
 // Lightweight pivot closure for the look-ahead side stream: the tile lives in
 // shared memory (B x B/2 words) and 256 threads with few registers sweep it,
 // so the kernel fits on an SM *beside* two phase-3 CTAs (which hold most of
@@ -332,6 +480,13 @@ int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s, T* scratch) {
         return rc;
     }
     count_launch();
+    if constexpr (sizeof(T) <= 2) {
+        if (g_pivot_blocked.load(std::memory_order_relaxed)) {
+            const cudaError_t e = launch_kernel(fw_pivot_blocked_kernel<T>, dim3(1), dim3(512), 0, s, P, b, ld,
+                                                kind == SMX_ANTI);
+            return e == cudaSuccess ? SMX_OK : (int)e;
+        }
+    }
     const cudaError_t e = launch_kernel(fw_pivot_kernel<T, 128>, dim3(1), dim3(1024), 0, s, P, b, ld,
                                         kind == SMX_ANTI);
     return e == cudaSuccess ? SMX_OK : (int)e;
@@ -564,7 +719,8 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
                                      (unsigned long long)kind, (uintptr_t)ws, ws_bytes,
                                      (unsigned long long)lookahead_enabled(), (unsigned long long)g_side_lite.load(),
                                      (unsigned long long)g_fw_block_override.load(), (unsigned long long)g_fw_packed.load(),
-                                     (unsigned long long)bounded_fastpath_enabled()};
+                                     (unsigned long long)bounded_fastpath_enabled(),
+                                     (unsigned long long)g_pivot_blocked.load()};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     // the phase-3 trace records host-side state per launch: trace runs stay eager
     return run_graphed(key, s, g_trace.armed, [&](cudaStream_t st) -> int {
@@ -886,6 +1042,10 @@ int smx_set_fw_packed(int enable) {
 int smx_set_fw_block(int block) {
     if (block != 0 && block != 128 && block != 256 && block != 512) return SMX_E_ARG;
     return g_fw_block_override.exchange(block);
+}
+
+int smx_set_fw_pivot_blocked(int enable) {
+    return g_pivot_blocked.exchange(enable ? 1 : 0);
 }
 
 int smx_set_fw_side_lite(int enable) {

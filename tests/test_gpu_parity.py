@@ -787,3 +787,43 @@ def test_bool_warshall_512_blocks_ragged(oracle_lib):
     a = rng.random((n, n), dtype=np.float32) < 3.0 / n
     got = BoolMatrix.from_numpy(a).transitive_closure().blocks
     np.testing.assert_array_equal(got, oracle_lib.bool_close(pack_bits(a)))
+
+
+@pytest.mark.parametrize("w", [8, 16])
+def test_pivot_kernels_blocked_and_register_agree(w, oracle_lib):
+    """smx_fw_pivot on tiles of 1..128 vertices: the blocked kernel (32-vertex
+    sub-blocks, squaring pivot) and the one-barrier-per-vertex register kernel
+    both equal the oracle closure, anti and dist, dense and sparse, inside a
+    larger padded matrix (only the b x b tile changes)."""
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    S = (1 << w) - 1
+    dt = np.uint8 if w == 8 else np.uint16
+    rng = np.random.default_rng(70 + w)
+    for b in (1, 5, 31, 32, 33, 64, 100, 127, 128):
+        for density in (0.05, 0.6):
+            for kind in ("anti", "dist"):
+                ld = 160
+                full = rng.integers(0, S + 1, (140, ld)).astype(dt)
+                v = rng.integers(1, min(S, 300), (b, b))
+                tile = np.where(rng.random((b, b)) < density, v, S)
+                if kind == "anti":
+                    tile = S - tile
+                full[:b, :b] = tile.astype(dt)
+                pad = ((b + 15) // 16) * 16 if w == 8 else ((b + 7) // 8) * 8
+                t_or = np.full((b, pad), 0 if kind == "anti" else S, dt)
+                t_or[:, :b] = full[:b, :b]
+                want = oracle_lib.semiring_close(t_or, w, kind)[:, :b]
+                for blocked in (1, 0):
+                    old = lib.smx_set_fw_pivot_blocked(blocked)
+                    try:
+                        dev = torch.from_numpy(full.copy()).cuda()
+                        _native.check(lib.smx_fw_pivot(dev.data_ptr(), b, ld, w // 8, 0 if kind == "anti" else 1,
+                                                       _native.stream_ptr()), "pivot")
+                        got = dev.cpu().numpy()
+                    finally:
+                        lib.smx_set_fw_pivot_blocked(old)
+                    np.testing.assert_array_equal(got[:b, :b], want, err_msg=f"b={b} {kind} blocked={blocked}")
+                    outside = full.copy()
+                    outside[:b, :b] = got[:b, :b]
+                    np.testing.assert_array_equal(got, outside)          # nothing outside the tile moves
