@@ -426,12 +426,16 @@ int copy_panel(const T* src, long long ld, T* dst, long long ldd, int rows, int 
 // down):
 //   P11* ; P12 (+)= P11 (x) P12 ; P21 (+)= P21 (x) P11 ; P22 (+)= P21 (x) P12 ;
 //   P22* ; P21 (+)= P22 (x) P21 ; P12 (+)= P12 (x) P22 ; P11 (+)= P12 (x) P21.
-// The closures recurse down to the 128 register kernel, the products are
-// Lite tiles.  A product whose output is also an operand reads a snapshot of
-// that operand from `scratch` (2 x h x h elements; the nested closures reuse
-// it, as the snapshots are dead while they run).  256: 185 us, against
-// 500 us for the single-CTA shared-memory pivot (fw_pivot_lite), which moved
-// 3 x 512 B of shared memory per row per step and was bandwidth-bound.
+// The closures recurse down to the 128 kernels, the products are Lite tiles.
+// The four panel products run in place, with no operand snapshot: one
+// operand is a closed tile X*, and a value another CTA has already lowered
+// is the weight of a real walk of the same kind, so it can only tighten
+// towards the exact result (the fw_pivot_and_row_panel argument).  256:
+// 146 us with the blocked leaves and the snapshots (185 us with the register
+// leaves), against 500 us for the single-CTA shared-memory pivot
+// (fw_pivot_lite), which moved 3 x 512 B of shared memory per row per step
+// and was bandwidth-bound.  (`scratch` is no longer read; the signature
+// keeps it.)
 template <typename T>
 int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s, T* scratch);
 
@@ -442,19 +446,13 @@ int fw_pivot_2x2(T* P, int b, long long ld, int kind, T* scratch, cudaStream_t s
     T* P12 = P + h;
     T* P21 = P + (long long)h * ld;
     T* P22 = P21 + h;
-    T* S12 = scratch;                  // h x m, pitch h
-    T* S21 = scratch + (size_t)h * h;  // m x h, pitch h
     SMX_TRY(fw_pivot<T>(P, h, ld, kind, s, scratch));
-    SMX_TRY(copy_panel<T>(P12, ld, S12, h, h, m, s));
-    SMX_TRY(semiring_gemm_lite<T>(P, S12, P12, h, m, h, ld, h, ld, kind, s));
-    SMX_TRY(copy_panel<T>(P21, ld, S21, h, m, h, s));
-    SMX_TRY(semiring_gemm_lite<T>(S21, P, P21, m, h, h, h, ld, ld, kind, s));
+    SMX_TRY(semiring_gemm_lite<T>(P, P12, P12, h, m, h, ld, ld, ld, kind, s));     // P12 (+)= P11* (x) P12
+    SMX_TRY(semiring_gemm_lite<T>(P21, P, P21, m, h, h, ld, ld, ld, kind, s));     // P21 (+)= P21 (x) P11*
     SMX_TRY(semiring_gemm_lite<T>(P21, P12, P22, m, m, h, ld, ld, ld, kind, s));
     SMX_TRY(fw_pivot<T>(P22, m, ld, kind, s, scratch));
-    SMX_TRY(copy_panel<T>(P21, ld, S21, h, m, h, s));
-    SMX_TRY(semiring_gemm_lite<T>(P22, S21, P21, m, h, m, ld, h, ld, kind, s));
-    SMX_TRY(copy_panel<T>(P12, ld, S12, h, h, m, s));
-    SMX_TRY(semiring_gemm_lite<T>(S12, P22, P12, h, m, m, h, ld, ld, kind, s));
+    SMX_TRY(semiring_gemm_lite<T>(P22, P21, P21, m, h, m, ld, ld, ld, kind, s));   // P21 (+)= P22* (x) P21
+    SMX_TRY(semiring_gemm_lite<T>(P12, P22, P12, h, m, m, ld, ld, ld, kind, s));   // P12 (+)= P12 (x) P22*
     return semiring_gemm_lite<T>(P12, P21, P, h, h, m, ld, ld, ld, kind, s);
 }
 

@@ -791,20 +791,21 @@ def test_bool_warshall_512_blocks_ragged(oracle_lib):
 
 @pytest.mark.parametrize("w", [8, 16])
 def test_pivot_kernels_blocked_and_register_agree(w, oracle_lib):
-    """smx_fw_pivot on tiles of 1..128 vertices: the blocked kernel (32-vertex
-    sub-blocks, squaring pivot) and the one-barrier-per-vertex register kernel
-    both equal the oracle closure, anti and dist, dense and sparse, inside a
-    larger padded matrix (only the b x b tile changes)."""
+    """smx_fw_pivot on tiles of 1..512 vertices: the blocked 128 kernel and the
+    one-barrier-per-vertex register kernel (as leaves of the in-place 2 x 2
+    recursion above 128) both equal the oracle closure, anti and dist, dense
+    and sparse, inside a larger padded matrix (only the b x b tile changes)."""
     from paper_1705_08743_b200 import _native
     lib = _native.lib()
     S = (1 << w) - 1
     dt = np.uint8 if w == 8 else np.uint16
     rng = np.random.default_rng(70 + w)
-    for b in (1, 5, 31, 32, 33, 64, 100, 127, 128):
+    sizes = (1, 5, 31, 32, 33, 64, 100, 127, 128, 129, 200, 256) + ((300, 512) if w == 16 else ())
+    for b in sizes:
         for density in (0.05, 0.6):
             for kind in ("anti", "dist"):
-                ld = 160
-                full = rng.integers(0, S + 1, (140, ld)).astype(dt)
+                ld = ((b + 32 + 15) // 16) * 16
+                full = rng.integers(0, S + 1, (b + 12, ld)).astype(dt)
                 v = rng.integers(1, min(S, 300), (b, b))
                 tile = np.where(rng.random((b, b)) < density, v, S)
                 if kind == "anti":
