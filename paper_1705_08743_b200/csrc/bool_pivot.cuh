@@ -15,7 +15,9 @@ namespace smx {
 // The fold reads nibble tables (method of four Russians): tab[g][e] is the OR
 // of the original rows {4g+b : bit b of e}, dtab[g][e] the same over D+.  A
 // row then needs 8 table entries instead of up to 32 pivot rows, which cuts
-// the shared-memory traffic that bound the per-pivot version 4x.
+// the shared-memory traffic that bound the per-pivot version 4x.  Two
+// barriers per sub-round: the next sub-round's pivot warp publishes its rows
+// and closes its diagonal block during the other warps' fold.
 constexpr int kWarshallBlock = 256;
 
 __device__ __forceinline__ uint32_t close32(uint32_t d) {
@@ -48,26 +50,44 @@ struct PivotSmemT {
     uint32_t orig[32][W];
     uint32_t tab[8][16][W];
     uint32_t dtab[8][16];
-    uint32_t dp[32];
+    uint32_t dp[2][32];   // D+ of the current / next sub-round
 };
 using PivotSmem = PivotSmemT<8>;
+
+// w[q] for a runtime q without dynamic register indexing (which would put w
+// in local memory).
+template <int W>
+__device__ __forceinline__ uint32_t word_at(const uint32_t (&w)[W], int q) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) v = (i == q) ? w[i] : v;
+    return v;
+}
+
+// Warp q publishes its rows (the sub-round's original pivot rows) and closes
+// its 32 x 32 diagonal block.
+template <int W>
+__device__ __forceinline__ void publish_pivot_rows(const uint32_t (&w)[W], int q, PivotSmemT<W>& sm) {
+    constexpr int PARTS = W / 4;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int p = 0; p < PARTS; ++p)
+        *reinterpret_cast<uint4*>(&sm.orig[lane][4 * p]) = make_uint4(w[4 * p], w[4 * p + 1], w[4 * p + 2], w[4 * p + 3]);
+    sm.dp[q & 1][lane] = close32(word_at<W>(w, q));
+}
 
 template <int W>
 __device__ __forceinline__ void close_tile_bits(uint32_t (&w)[W], int b, PivotSmemT<W>& sm) {
     static_assert(W % 4 == 0, "rows are moved as uint4");
     constexpr int PARTS = W / 4;   // uint4 parts per table entry
     const int r = threadIdx.x, warp = r >> 5, lane = r & 31;
-#pragma unroll
-    for (int q = 0; q < W; ++q) {
-        if (q * 32 >= b) break;
-        if (warp == q) {
-#pragma unroll
-            for (int p = 0; p < PARTS; ++p)
-                *reinterpret_cast<uint4*>(&sm.orig[lane][4 * p]) =
-                    make_uint4(w[4 * p], w[4 * p + 1], w[4 * p + 2], w[4 * p + 3]);
-            sm.dp[lane] = close32(w[q]);
-        }
-        __syncthreads();
+    const int nq = (b + 31) / 32;
+    if (warp == 0) publish_pivot_rows<W>(w, 0, sm);
+    __syncthreads();
+    // not unrolled: the unrolled sub-rounds were ~19k instructions and the
+    // kernel stalled on instruction fetch (ncu: "no instruction" the top stall)
+#pragma unroll 1
+    for (int q = 0; q < nq; ++q) {
         {
             // 128 table entries x PARTS uint4 parts = 32 W threads
             const int entry = r / PARTS, part = r % PARTS;
@@ -85,14 +105,14 @@ __device__ __forceinline__ void close_tile_bits(uint32_t (&w)[W], int b, PivotSm
                 uint32_t d = 0;
 #pragma unroll
                 for (int bit = 0; bit < 4; ++bit)
-                    if ((e2 >> bit) & 1) d |= sm.dp[4 * g2 + bit];
+                    if ((e2 >> bit) & 1) d |= sm.dp[q & 1][4 * g2 + bit];
                 sm.dtab[g2][e2] = d;
             }
         }
         __syncthreads();
-        uint32_t m = w[q];
+        uint32_t m = word_at<W>(w, q);
         if (warp == q) {
-            m = sm.dp[lane];
+            m = sm.dp[q & 1][lane];
         } else if (m) {
             uint32_t ext = m;
 #pragma unroll
@@ -110,6 +130,10 @@ __device__ __forceinline__ void close_tile_bits(uint32_t (&w)[W], int b, PivotSm
                 }
             }
         }
+        // the next sub-round's pivot warp publishes right after its own fold,
+        // while the other warps are still folding: the fold reads only tab /
+        // dtab / dp[q & 1], and orig is read only before the barrier above
+        if (warp == q + 1 && q + 1 < nq) publish_pivot_rows<W>(w, q + 1, sm);
         __syncthreads();
     }
 }
