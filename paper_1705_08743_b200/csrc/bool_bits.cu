@@ -344,18 +344,22 @@ int bool_warshall_bits(uint32_t* T, int n, long long ld_w, void* ws, size_t ws_b
 
 static int bool_warshall_schedule(uint32_t* T, int n, long long ld_w, uint32_t* RP, uint32_t* CP,
                                   cudaStream_t s) {
+    // Phase 3 reads its A operand, the column panel T[:, K], straight from T:
+    // the launch also ORs into T[:, K] (its j in K part), and a bit it reads
+    // after another CTA set it is a real path through K, so the result is the
+    // same for any interleaving (the row-panel argument of
+    // bits_pivot_and_row_panel) -- no column-panel snapshot per round.
+    (void)CP;
     const int nw = (n + 31) / 32;
     const int BLK = bool_block_for_n(n);
-    const long long ldcp = BLK / 32;
     const int R = (n + BLK - 1) / BLK;
     auto blk = [&](int r) { return n - r * BLK < BLK ? n - r * BLK : BLK; };
 
     if (!lookahead_enabled()) {
         for (int r = 0; r < R; ++r) {
-            const int k0 = r * BLK, bb = blk(r), kw0 = k0 / 32, bw = (bb + 31) / 32;
+            const int k0 = r * BLK, bb = blk(r), kw0 = k0 / 32;
             SMX_TRY(bits_pivot_and_row_panel(T, n, ld_w, RP, k0, bb, s));
-            SMX_TRY(copy_words(T + kw0, ld_w, CP, ldcp, n, bw, s));
-            SMX_TRY(bool_bits_gemm(CP, T + (long long)k0 * ld_w, T, n, nw, bb, ldcp, ld_w, ld_w, 1, k0, bb, s));
+            SMX_TRY(bool_bits_gemm(T + kw0, T + (long long)k0 * ld_w, T, n, nw, bb, ld_w, ld_w, ld_w, 1, k0, bb, s));
         }
         return SMX_OK;
     }
@@ -363,14 +367,14 @@ static int bool_warshall_schedule(uint32_t* T, int n, long long ld_w, uint32_t* 
     SMX_TRY(side_stream(&ss));
     cudaError_t e;
     SMX_TRY(bits_pivot_and_row_panel(T, n, ld_w, RP, 0, blk(0), s));
-    SMX_TRY(copy_words(T, ld_w, CP, ldcp, n, (blk(0) + 31) / 32, s));
     for (int r = 0; r < R; ++r) {
-        const int k0 = r * BLK, bb = blk(r);
+        const int k0 = r * BLK, bb = blk(r), kw0 = k0 / 32;
         uint32_t* rowK = T + (long long)k0 * ld_w;
         if (r + 1 < R) {
             const int k1 = k0 + BLK, bb1 = blk(r + 1);
-            SMX_TRY(bool_bits_gemm(CP + k1 * ldcp, rowK, T + (long long)k1 * ld_w, bb1, nw, bb, ldcp, ld_w,
-                                   ld_w, 1, 0, 0, s));
+            // 3a: the next pivot block's rows
+            SMX_TRY(bool_bits_gemm(T + (long long)k1 * ld_w + kw0, rowK, T + (long long)k1 * ld_w, bb1, nw, bb,
+                                   ld_w, ld_w, ld_w, 1, 0, 0, s));
             if ((e = cudaEventRecord(ss->fork, s)) != cudaSuccess) return (int)e;
             if ((e = cudaStreamWaitEvent(ss->side, ss->fork, 0)) != cudaSuccess) return (int)e;
             {
@@ -378,14 +382,12 @@ static int bool_warshall_schedule(uint32_t* T, int n, long long ld_w, uint32_t* 
                 SMX_TRY(bits_pivot_and_row_panel(T, n, ld_w, RP, k1, bb1, ss->side));
             }
             if ((e = cudaEventRecord(ss->join, ss->side)) != cudaSuccess) return (int)e;
-            SMX_TRY(bool_bits_gemm(CP, rowK, T, n, nw, bb, ldcp, ld_w, ld_w, 1, k0, bb + bb1, s));
-            {
-                PdlNext pdl;   // the column-panel copy directly follows 3b
-                SMX_TRY(copy_words(T + k1 / 32, ld_w, CP, ldcp, n, (bb1 + 31) / 32, s));
-            }
+            // 3b: every other row (reads T[:, K_r] of rows outside K_r u K_{r+1}
+            // only, which the side stream does not touch)
+            SMX_TRY(bool_bits_gemm(T + kw0, rowK, T, n, nw, bb, ld_w, ld_w, ld_w, 1, k0, bb + bb1, s));
             if ((e = cudaStreamWaitEvent(s, ss->join, 0)) != cudaSuccess) return (int)e;
         } else {
-            SMX_TRY(bool_bits_gemm(CP, rowK, T, n, nw, bb, ldcp, ld_w, ld_w, 1, k0, bb, s));
+            SMX_TRY(bool_bits_gemm(T + kw0, rowK, T, n, nw, bb, ld_w, ld_w, ld_w, 1, k0, bb, s));
         }
     }
     return SMX_OK;
