@@ -122,6 +122,11 @@ int smx_set_fw_lookahead(int enable);
  * vertex sub-blocks, 7 barriers each; default), 0 = the register kernel (one
  * barrier per vertex).  Results are identical.  Returns the previous setting. */
 int smx_set_fw_pivot_blocked(int enable);
+/* Bit-packed Boolean GEMM (smx_bool_gemm_bits and the bit Warshall): 1 = the
+ * four-Russians kernel (per 32 k, 8 nibble-table lookups; default), 0 = the
+ * per-k predicate kernel.  Results are identical.  Returns the previous
+ * setting. */
+int smx_set_bits_m4r(int enable);
 /* Graph replay of multi-launch calls (smx_fw_*, smx_bool_warshall_bits,
  * smx_bool_warshall_i8, smx_bool_mul_tc): the first call with a given
  * (entry, pointers, sizes, switches) launches eagerly, the second records its

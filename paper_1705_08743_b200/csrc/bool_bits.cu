@@ -13,6 +13,8 @@
 // per warp.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "bool_pivot.cuh"
 
@@ -173,6 +175,180 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_bits_gemm_kernel
     }
 }
 
+// Method of four Russians (the paper's "sum of column-by-row outer products"
+// taken four k at a time): per k-word stage the CTA builds, for each nibble
+// g of the 32 k, the 16 ORs of subsets of B rows 4g..4g+3 (Tb[g][e]), and a
+// row then ORs in one table entry per nibble -- 8 lookups for 32 k instead
+// of a predicate test per k.  ALU work per 32 k per 8-word group: 8 x (1
+// extract + 8 OR) against 32 x (1 test + 8 predicated OR).  Entries are
+// stored with their 16-byte chunks rotated by e (chunk c at c ^ (e & 7)):
+// threads reading different entries at the same columns then hit different
+// banks.  Table build: each of 8 x BNW/4 work items loads 4 B rows x 4 words
+// and writes the 16 entries of its columns.
+template <typename Cfg>
+struct M4rSmem {
+    static constexpr int CH = Cfg::BNW / 4;                    // 16-byte chunks per entry
+    static constexpr int ITEMS = 8 * CH;                       // (nibble, chunk) build items
+    static constexpr int IT_PT = (ITEMS + Cfg::THREADS - 1) / Cfg::THREADS;
+    static constexpr size_t TAB_WORDS = 8 * 16 * Cfg::BNW;
+    static constexpr size_t BYTES = 2 * (TAB_WORDS * 4 + Cfg::BM * 4);
+};
+
+__device__ __forceinline__ int m4r_chunk(int c, int e, int nch) { return c ^ (e & (nch - 1) & 7); }
+
+template <typename Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_m4r_gemm_kernel(const BitsArgs p) {
+    constexpr int BM = Cfg::BM, BNW = Cfg::BNW, TM = Cfg::TM, TNW = Cfg::TNW, HW = Cfg::HW;
+    constexpr int TCOLS = Cfg::TCOLS, THREADS = Cfg::THREADS;
+    using SM = M4rSmem<Cfg>;
+    constexpr int CH = SM::CH;
+    extern __shared__ __align__(16) uint32_t m4r_smem[];
+    uint32_t* Tb = m4r_smem;                                  // [2][8][16][BNW]
+    uint32_t* As = m4r_smem + 2 * SM::TAB_WORDS;              // [2][BM]
+
+    pdl_wait();
+    const int tid = threadIdx.x;
+    int mt = blockIdx.y;
+    if (mt >= p.skip_tile0) mt += p.skip_tiles;
+    const int row0 = mt * BM, w0 = blockIdx.x * BNW;
+    const int tc = tid % TCOLS, tr = tid / TCOLS;
+    const int nkw_all = (p.K + 31) / 32;
+    const int kw_lo = blockIdx.z * p.kw_per;
+    const int kw_hi = min(nkw_all, kw_lo + p.kw_per);
+    const bool split = p.kw_per < nkw_all;
+
+    uint32_t acc[TM][TNW];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int grow = row0 + tr * TM + i;
+#pragma unroll
+        for (int j = 0; j < TNW; ++j) {
+            const int gw = w0 + (j / HW) * (BNW / 2) + tc * HW + (j % HW);
+            acc[i][j] = (!split && p.accumulate && grow < p.M && gw < p.Nw)
+                            ? p.C[(long long)grow * p.ldc + gw] : 0u;
+        }
+    }
+
+    constexpr int A_PT = (BM + THREADS - 1) / THREADS;
+    uint32_t a_st[A_PT];
+    uint4 b_st[SM::IT_PT][4];
+    auto gload = [&](int kw) {
+        const int k0 = kw * 32;
+#pragma unroll
+        for (int q = 0; q < A_PT; ++q) {
+            const int r = tid + q * THREADS, grow = row0 + r;
+            uint32_t v = 0;
+            if (r < BM && grow < p.M) {
+                v = p.A[(long long)grow * p.lda + kw];
+                const int valid = p.K - k0;
+                if (valid < 32) v &= (1u << valid) - 1u;
+            }
+            a_st[q] = v;
+        }
+#pragma unroll
+        for (int q = 0; q < SM::IT_PT; ++q) {
+            const int it = tid + q * THREADS;
+            const int g = it / CH, c = it % CH, gw = w0 + c * 4;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int gk = k0 + 4 * g + b;
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (it < SM::ITEMS && gk < p.K) {
+                    const uint32_t* src = p.B + (long long)gk * p.ldb + gw;
+                    if (gw + 4 <= p.Nw) v = *reinterpret_cast<const uint4*>(src);
+                    else {
+                        if (gw + 0 < p.Nw) v.x = src[0];
+                        if (gw + 1 < p.Nw) v.y = src[1];
+                        if (gw + 2 < p.Nw) v.z = src[2];
+                    }
+                }
+                b_st[q][b] = v;
+            }
+        }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < A_PT; ++q) {
+            const int r = tid + q * THREADS;
+            if (r < BM) As[buf * BM + r] = a_st[q];
+        }
+        uint32_t* tab = Tb + buf * SM::TAB_WORDS;
+#pragma unroll
+        for (int q = 0; q < SM::IT_PT; ++q) {
+            const int it = tid + q * THREADS;
+            if (it >= SM::ITEMS) break;
+            const int g = it / CH, c = it % CH;
+            // entries 0..7 from rows 0..2, then 8..15 = those | row 3 (8 live uint4)
+            uint4 t[8];
+            t[0] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int e = 1; e < 8; ++e) {
+                const int hb = e >= 4 ? 2 : (e >= 2 ? 1 : 0);   // highest set bit
+                const uint4 lo = t[e ^ (1 << hb)], r = b_st[q][hb];
+                t[e] = make_uint4(lo.x | r.x, lo.y | r.y, lo.z | r.z, lo.w | r.w);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                *reinterpret_cast<uint4*>(tab + (g * 16 + e) * BNW + m4r_chunk(c, e, CH) * 4) = t[e];
+            const uint4 r3 = b_st[q][3];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const uint4 v = make_uint4(t[e].x | r3.x, t[e].y | r3.y, t[e].z | r3.z, t[e].w | r3.w);
+                *reinterpret_cast<uint4*>(tab + (g * 16 + e + 8) * BNW + m4r_chunk(c, e + 8, CH) * 4) = v;
+            }
+        }
+    };
+
+    if (kw_lo < kw_hi) { gload(kw_lo); sstore(0); __syncthreads(); }
+    for (int kw = kw_lo; kw < kw_hi; ++kw) {
+        const int buf = (kw - kw_lo) & 1;
+        if (kw + 1 < kw_hi) gload(kw + 1);
+        const uint32_t* tab = Tb + buf * SM::TAB_WORDS;
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+            const uint32_t a = As[buf * BM + tr * TM + i];
+            if (a == 0u) continue;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                const int e = (a >> (4 * g)) & 15;
+                const uint32_t* ent = tab + (g * 16 + e) * BNW;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int c = h * (CH / 2) + tc;
+                    const uint4 v = *reinterpret_cast<const uint4*>(ent + m4r_chunk(c, e, CH) * 4);
+                    acc[i][4 * h] |= v.x; acc[i][4 * h + 1] |= v.y; acc[i][4 * h + 2] |= v.z; acc[i][4 * h + 3] |= v.w;
+                }
+            }
+        }
+        if (kw + 1 < kw_hi) sstore(buf ^ 1);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int grow = row0 + tr * TM + i;
+        if (grow >= p.M) continue;
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            const int gw = w0 + g * (BNW / 2) + tc * HW;
+            uint32_t* dst = p.C + (long long)grow * p.ldc + gw;
+            if (split) {
+                for (int j = 0; j < 4; ++j)
+                    if (gw + j < p.Nw && acc[i][g * 4 + j]) atomicOr(dst + j, acc[i][g * 4 + j]);
+            } else if (gw + 4 <= p.Nw) {
+                *reinterpret_cast<uint4*>(dst) = make_uint4(acc[i][g * 4], acc[i][g * 4 + 1],
+                                                            acc[i][g * 4 + 2], acc[i][g * 4 + 3]);
+            } else {
+                for (int j = 0; j < 4; ++j)
+                    if (gw + j < p.Nw) dst[j] = acc[i][g * 4 + j];
+            }
+        }
+    }
+}
+
+// smx_set_bits_m4r: the four-Russians bit GEMM (1, default) or the per-k
+// predicate kernel (0).
+static std::atomic<int> g_bits_m4r{1};
+
 template <typename Cfg>
 int launch_bits(const BitsArgs& a_in, cudaStream_t s) {
     BitsArgs a = a_in;
@@ -197,6 +373,18 @@ int launch_bits(const BitsArgs& a_in, cudaStream_t s) {
     }
     dim3 grid(ntiles, mtiles, splits);
     smx::count_launch();
+    if (g_bits_m4r.load(std::memory_order_relaxed)) {
+        constexpr size_t smem = M4rSmem<Cfg>::BYTES;
+        static bool configured = false;   // per instantiation
+        if (!configured) {
+            cudaError_t e = cudaFuncSetAttribute(bool_m4r_gemm_kernel<Cfg>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return (int)e;
+            configured = true;
+        }
+        const cudaError_t e = launch_kernel(bool_m4r_gemm_kernel<Cfg>, grid, dim3(Cfg::THREADS), smem, s, a);
+        return e == cudaSuccess ? SMX_OK : (int)e;
+    }
     const cudaError_t e = launch_kernel(bool_bits_gemm_kernel<Cfg>, grid, dim3(Cfg::THREADS), 0, s, a);
     return e == cudaSuccess ? SMX_OK : (int)e;
 }
@@ -335,7 +523,7 @@ int bool_warshall_bits(uint32_t* T, int n, long long ld_w, void* ws, size_t ws_b
     key.fn = 200;
     const unsigned long long kv[] = {(uintptr_t)T, (unsigned long long)n, (unsigned long long)ld_w,
                                      (uintptr_t)ws, ws_bytes, (unsigned long long)lookahead_enabled(),
-                                     (unsigned long long)bool_block_for_n(n)};
+                                     (unsigned long long)bool_block_for_n(n), (unsigned long long)g_bits_m4r.load()};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     return run_graphed(key, s, false, [&](cudaStream_t st) -> int {
         return bool_warshall_schedule(T, n, ld_w, RP, CP, st);
@@ -398,6 +586,10 @@ static int bool_warshall_schedule(uint32_t* T, int n, long long ld_w, uint32_t* 
 using namespace smx;
 
 extern "C" {
+
+int smx_set_bits_m4r(int enable) {
+    return g_bits_m4r.exchange(enable ? 1 : 0);
+}
 
 int smx_bool_gemm_bits(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int Nwords, int K,
                        int lda_w, int ldb_w, int ldc_w, int accumulate, void* stream) {

@@ -828,3 +828,38 @@ def test_pivot_kernels_blocked_and_register_agree(w, oracle_lib):
                     outside = full.copy()
                     outside[:b, :b] = got[:b, :b]
                     np.testing.assert_array_equal(got, outside)          # nothing outside the tile moves
+
+
+@pytest.mark.parametrize("m4r", [1, 0])
+def test_bits_gemm_four_russians_and_predicate_kernels(m4r, oracle_lib):
+    """The bit-packed product (engines.bool_mul_bits) on the four-Russians
+    kernel and on the per-k predicate kernel: ragged shapes, densities from
+    sparse to dense, small and large tile configurations, split-K -- equal to
+    the oracle; and the bit Warshall closure with either kernel equal to the
+    reference digest at C2's size."""
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    old = lib.smx_set_bits_m4r(m4r)
+    try:
+        rng = np.random.default_rng(80 + m4r)
+        for (m, k, n), p in [((1, 1, 1), 0.5), ((300, 700, 1000), 0.01), ((300, 700, 1000), 0.3),
+                             ((1024, 1024, 1024), 0.05), ((2049, 100, 33), 0.2), ((64, 5000, 70), 0.002),
+                             ((4096, 256, 4096), 0.01)]:
+            a = (rng.random((m, k)) < p).astype(np.uint8)
+            b = (rng.random((k, n)) < p).astype(np.uint8)
+            got = engines.bool_mul_bits(BoolMatrix.from_numpy(a), BoolMatrix.from_numpy(b)).blocks
+            want = oracle_lib.bool_mul(oracle_lib.pack_bits(a), oracle_lib.pack_bits(b), k)
+            np.testing.assert_array_equal(got, want, err_msg=f"{m}x{k}x{n} p={p} m4r={m4r}")
+        cfg = workloads.CONFIGS["c2_bool_warshall"]
+        (t,) = workloads.make_inputs(cfg)
+        out = BoolMatrix.from_numpy(t).transitive_closure().blocks
+        (d,) = [x for x in json_digests() if x["config"] == "c2_bool_warshall"]
+        assert sha(out) == d["output_sha256"]
+    finally:
+        lib.smx_set_bits_m4r(old)
+
+
+def json_digests():
+    import json
+    from pathlib import Path
+    return json.loads((Path(__file__).parent / "golden" / "config_digests.json").read_text())
