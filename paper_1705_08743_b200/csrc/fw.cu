@@ -656,15 +656,30 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
             if ((e = cudaStreamWaitEvent(fs->side, fs->fork, 0)) != cudaSuccess) return (int)e;
             {
                 PriorityScope ps(fs->priority);
-#ifdef SMX_TRACE_SIDE   // development builds: side-chain spans as trace entries with cells = -1
+#if defined(SMX_TRACE_SIDE) && !defined(SMX_TRACE_SIDE_PARTS)   // development builds: side-chain spans (cells = -1)
                 trace_begin(fs->side, -1);
+#endif
+#ifdef SMX_TRACE_SIDE_PARTS   // 3a, pivot, row panel as separate entries (cells -2, -3, -4)
+                trace_begin(fs->side, -2);
 #endif
                 // 3a: the next pivot block's rows
                 SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / G::BM, ceil_div(bb1, G::BM), 0, 0, pws,
                                       pws_bytes, fs->side));
+#ifdef SMX_TRACE_SIDE_PARTS
+                trace_end(fs->side);
+                trace_begin(fs->side, -3);
+                SMX_TRY(fw_pivot<T>(Tm + (long long)k1 * ld + k1, bb1, ld, kind, fs->side, RP));
+                trace_end(fs->side);
+                trace_begin(fs->side, -4);
+                SMX_TRY(semiring_gemm<T>(Tm + (long long)k1 * ld + k1, Tm + (long long)k1 * ld, Tm + (long long)k1 * ld,
+                                         bb1, n, bb1, ld, ld, ld, kind, 1, 0, 0, fs->side));
+                trace_end(fs->side);
+#endif
                 if ((e = cudaEventRecord(fs->aux, fs->side)) != cudaSuccess) return (int)e;
+#ifndef SMX_TRACE_SIDE_PARTS
                 SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
-#ifdef SMX_TRACE_SIDE
+#endif
+#if defined(SMX_TRACE_SIDE) && !defined(SMX_TRACE_SIDE_PARTS)
                 trace_end(fs->side);
 #endif
             }

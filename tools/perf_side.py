@@ -16,8 +16,11 @@ for n in [int(x) for x in (sys.argv[1:] or ["8192"])]:
         engines.lane_close_(w, n, 16, True); torch.cuda.synchronize()
         ms = (ctypes.c_float * cap)(); cells = (ctypes.c_longlong * cap)()
         k = lib.smx_fw_trace_read(ms, cells, cap)
-    side = [ms[i] for i in range(k) if cells[i] < 0]
+    side = [ms[i] for i in range(k) if cells[i] == -1]
     p3 = [ms[i] for i in range(k) if cells[i] >= 0]
+    parts = {name: [ms[i] for i in range(k) if cells[i] == code] for code, name in ((-2, "3a"), (-3, "pivot"), (-4, "row_panel"))}
+    if any(parts.values()):   # -DSMX_TRACE_SIDE_PARTS
+        print(json.dumps({"n": n, **{f"{name}_ms_mean": sum(v) / max(len(v), 1) for name, v in parts.items()}}))
     print(json.dumps({"n": n, "rounds": len(p3), "side_ms_mean": sum(side) / max(len(side), 1),
                       "side_ms_max": max(side) if side else None, "p3_ms_mean": sum(p3) / max(len(p3), 1),
                       "side_longer_than_p3": sum(1 for a, b in zip(side, p3) if a > b)}))
