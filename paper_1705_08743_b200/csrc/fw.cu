@@ -494,10 +494,15 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 inline size_t fw_ws_bytes(int n, long long ld, int eb) {
     // RP: pivot row panel snapshot (B x ld); CP: column panel snapshot (n x B);
-    // u16: the packed phase-3 operand tiles (semiring_packed.cuh)
+    // u8/u16: the packed phase-3 operand tiles (semiring_packed.cuh) and a
+    // 256-byte slot for the per-round operand certificate (fw_rounds_packed)
     const size_t B = fw_block_for(eb);
     const size_t base = align256(B * ld * eb) + align256((size_t)n * B * eb);
-    return eb <= 2 ? base + align256(packed_ws_bytes(n, n, (int)B)) : base;
+    return eb <= 2 ? base + align256(packed_ws_bytes(n, n, (int)B)) + 256 : base;
+}
+// The certificate slot: the last 256 bytes of fw_ws_bytes (u8/u16).
+inline int* fw_cert_slot(void* ws, int n, long long ld, int eb) {
+    return reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + fw_ws_bytes(n, ld, eb) - 256);
 }
 
 // smx_set_fw_packed: u16 phase 3 on the warp-specialised packed-tile kernel
@@ -633,9 +638,20 @@ int fw_run_lookahead(T* Tm, int n, long long ld, int kind, T* RP, T* CP, void* p
 // window; lo is a multiple of the 128-row tile, hi one too or n.  Rows
 // outside the window are neither read as A nor written (the host-streamed
 // closure below runs rounds on the rows that have arrived so far).
+// The first kFwCertRounds rounds of a call run certified when their operands
+// allow it: the column panel and the row panel hold only unreachable (S) or
+// lanes < 2^14 -- true of the input graph (weights <= 1000) -- so every tile
+// takes the 1-instruction shifted encoding of the public products
+// (Lane<uint16_t>::to_shifted).  Without it round 0 runs the general
+// 2-instruction form on every tile (the input is 98% unreachable, so no tile
+// passes the per-tile bounded test): measured 16.5 against 33.9 Tcell/s at
+// n = 32768.  Later rounds are bounded anyway.  A certified round packs its
+// A tiles after the previous round's join (its row panel must be final).
+constexpr int kFwCertRounds = 2;
+
 template <typename T>
 int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, size_t pws_bytes, int lo, int hi,
-                     int ra, int rb, cudaStream_t s) {
+                     int ra, int rb, cudaStream_t s, int* cert = nullptr) {
     using G = PackedCfg<T>;
     SideStream* fs = nullptr;
     SMX_TRY(side_stream(&fs));
@@ -643,13 +659,31 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
     auto blk = [&](int r) { return n - r * BLK < BLK ? n - r * BLK : BLK; };
     const int t0 = lo / G::BM, tiles = ceil_div(hi, G::BM) - t0;
     if (ra >= rb) return SMX_OK;
+    const bool can_cert = cert != nullptr && !Lane<T>::kOneInstr && bounded_fastpath_enabled();
+    auto certified = [&](int r) { return can_cert && r - ra < kFwCertRounds; };
     SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, ra * BLK, blk(ra), s));
-    SMX_TRY(packed_pack_a_rows<T>(Tm + ra * BLK, n, n, blk(ra), ld, kind, pws, pws_bytes, t0, tiles, s));
+    if (!certified(ra))
+        SMX_TRY(packed_pack_a_rows<T>(Tm + ra * BLK, n, n, blk(ra), ld, kind, pws, pws_bytes, t0, tiles, s));
     cudaError_t e;
     for (int r = ra; r < rb; ++r) {
         const int k0 = r * BLK, bb = blk(r);
         T* rowK = Tm + (long long)k0 * ld;
-        SMX_TRY(packed_pack<T>(nullptr, rowK, n, n, bb, ld, ld, kind, pws, pws_bytes, s));
+        const int* cr = nullptr;
+        if constexpr (sizeof(T) == 2) {
+            if (certified(r)) {
+                if ((e = cudaMemsetAsync(cert, 0xFF, sizeof(int), s)) != cudaSuccess) return (int)e;
+                const int blocks = 4 * sm_count();
+                cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(Tm + (long long)lo * ld + k0),
+                                                       hi - lo, bb, ld, kind == SMX_ANTI, cert);
+                SMX_LAUNCHED_OR_RETURN();
+                cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(rowK), bb, n, ld,
+                                                       kind == SMX_ANTI, cert);
+                SMX_LAUNCHED_OR_RETURN();
+                cr = cert;
+                SMX_TRY(packed_pack_a_rows<T>(Tm + k0, n, n, bb, ld, kind, pws, pws_bytes, t0, tiles, s, cr));
+            }
+        }
+        SMX_TRY(packed_pack<T>(nullptr, rowK, n, n, bb, ld, ld, kind, pws, pws_bytes, s, cr));
         if (r + 1 < rb) {
             const int k1 = k0 + BLK, bb1 = blk(r + 1);
             if ((e = cudaEventRecord(fs->fork, s)) != cudaSuccess) return (int)e;
@@ -664,7 +698,7 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
 #endif
                 // 3a: the next pivot block's rows
                 SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / G::BM, ceil_div(bb1, G::BM), 0, 0, pws,
-                                      pws_bytes, fs->side));
+                                      pws_bytes, fs->side, cr));
 #ifdef SMX_TRACE_SIDE_PARTS
                 trace_end(fs->side);
                 trace_begin(fs->side, -3);
@@ -686,14 +720,15 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
             if ((e = cudaEventRecord(fs->join, fs->side)) != cudaSuccess) return (int)e;
             // 3b: everything else in the window (skips K_r and K_{r+1}, adjacent tiles)
             trace_begin(s, (long long)(hi - lo - bb - bb1) * n * bb);
-            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, t0, tiles, k0, bb + bb1, pws, pws_bytes, s));
+            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, t0, tiles, k0, bb + bb1, pws, pws_bytes, s, cr));
             trace_end(s);
             if ((e = cudaStreamWaitEvent(s, fs->aux, 0)) != cudaSuccess) return (int)e;
-            SMX_TRY(packed_pack_a_rows<T>(Tm + k1, n, n, bb1, ld, kind, pws, pws_bytes, t0, tiles, s));
+            if (!certified(r + 1))   // (a certified round packs its own A after the join)
+                SMX_TRY(packed_pack_a_rows<T>(Tm + k1, n, n, bb1, ld, kind, pws, pws_bytes, t0, tiles, s));
             if ((e = cudaStreamWaitEvent(s, fs->join, 0)) != cudaSuccess) return (int)e;
         } else {
             trace_begin(s, (long long)(hi - lo - bb) * n * bb);
-            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, t0, tiles, k0, bb, pws, pws_bytes, s));
+            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, t0, tiles, k0, bb, pws, pws_bytes, s, cr));
             trace_end(s);
         }
     }
@@ -702,9 +737,9 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
 
 template <typename T>
 int fw_run_lookahead_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, size_t pws_bytes,
-                            cudaStream_t s) {
+                            cudaStream_t s, int* cert = nullptr) {
     const int BLK = fw_block_for_n<T>(n);
-    return fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, pws_bytes, 0, n, 0, (n + BLK - 1) / BLK, s);
+    return fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, pws_bytes, 0, n, 0, (n + BLK - 1) / BLK, s, cert);
 }
 
 template <typename T>
@@ -739,7 +774,8 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
     return run_graphed(key, s, g_trace.armed, [&](cudaStream_t st) -> int {
         if constexpr (sizeof(T) <= 2) {
             if (lookahead_enabled() && g_fw_packed && pws != nullptr)
-                return fw_run_lookahead_packed<T>(Tm, n, ld, kind, RP, pws, pws_bytes, st);
+                return fw_run_lookahead_packed<T>(Tm, n, ld, kind, RP, pws, pws_bytes, st,
+                                                  fw_cert_slot(ws, n, ld, sizeof(T)));
         }
         if (lookahead_enabled()) return fw_run_lookahead<T>(Tm, n, ld, kind, RP, CP, pws, pws_bytes, st);
         return fw_run_serial<T>(Tm, n, ld, kind, RP, CP, pws, pws_bytes, BLK, st);
@@ -900,6 +936,7 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
                            align256((size_t)n * FwBlock<T>::value * sizeof(T));
     void* pws = reinterpret_cast<char*>(ws) + pws_off;
     const size_t slot = fw_host_slot_bytes(n, sizeof(T));
+    int* cert = fw_cert_slot(ws, n, ld, sizeof(T));
     auto egress_slot = [&](int j) { return reinterpret_cast<char*>(ws) + fw_ws_bytes(n, ld, sizeof(T)) + j * slot; };
 
     const int sL = (R - kFwHostTailBlocks) * BLK;   // L = rows [sL, n)
@@ -951,10 +988,10 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
         // the group's rounds over every row that has arrived (the last group:
         // all rows, up to the blocks of L)
         const int rb = (r1 < n ? r1 : sL) / BLK;
-        SMX_TRY(fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, slot, 0, r1, (int)r0 / BLK, rb, s));
+        SMX_TRY(fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, slot, 0, r1, (int)r0 / BLK, rb, s, cert));
     }
     // L: its rounds on rows L alone; then L is final
-    SMX_TRY(fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, slot, sL, n, sL / BLK, R, s));
+    SMX_TRY(fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, slot, sL, n, sL / BLK, R, s, cert));
     SMX_TRY(d2h(sL, n, ev_out[0]));
     // egress: rows [0, sL) (+)= T[rows, L] (x) T[L, :]; L's blocks packed once as B
     for (int j = 0; j < kFwHostTailBlocks; ++j) {

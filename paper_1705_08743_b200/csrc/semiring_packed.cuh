@@ -455,14 +455,14 @@ inline int packed_pack(const T* A, const T* B, int M, int N, int K, long long ld
 // (fw.cu) packs just the rows it is about to update.
 template <typename T>
 inline int packed_pack_a_rows(const T* A, int M, int N, int K, long long lda, int kind, void* ws, size_t ws_bytes,
-                              int tile0, int tiles, cudaStream_t s) {
+                              int tile0, int tiles, cudaStream_t s, const int* cert = nullptr) {
     SMX_TRY(packed_check<T>(A, nullptr, M, N, K, lda, lda, kind, ws, ws_bytes));   // (no B: ldb unused)
     if (M == 0 || N == 0 || K == 0) return SMX_OK;
     const PackedWs v = packed_views(ws, M, N, K);
     if (tile0 < 0 || tile0 > v.MT) return SMX_E_ARG;
     if (tiles < 0 || tile0 + tiles > v.MT) tiles = v.MT - tile0;
     if (tiles == 0) return SMX_OK;
-    pack_a_kernel<T><<<dim3(v.KT, tiles), 128, 0, s>>>(A, M, K, lda, kind == SMX_ANTI, v.KT, v.Ap, v.fA, nullptr,
+    pack_a_kernel<T><<<dim3(v.KT, tiles), 128, 0, s>>>(A, M, K, lda, kind == SMX_ANTI, v.KT, v.Ap, v.fA, cert,
                                                        tile0);
     SMX_RETURN_LAUNCH();
 }
