@@ -979,11 +979,28 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
         const int r1 = ends[g];
         const int t0 = (int)r0 / G::BM, tiles = ceil_div(r1, G::BM) - t0;
         if ((e = cudaStreamWaitEvent(s, ev_in[g], 0)) != cudaSuccess) return (int)e;
-        // ingest: T[G, :] (+)= T[G, 0:r0] (x) T[0:r0, :], one pivot block of K per launch
+        // ingest: T[G, :] (+)= T[G, 0:r0] (x) T[0:r0, :], one pivot block of K per launch.
+        // The first block's A tiles are the raw arrived rows (mostly
+        // unreachable): certified like fw_rounds_packed's first rounds; later
+        // blocks read rows the first product has already filled in.
         for (int k0 = 0; k0 < (int)r0; k0 += BLK) {
-            SMX_TRY(packed_pack<T>(nullptr, Tm + (long long)k0 * ld, n, n, BLK, ld, ld, kind, pws, slot, s));
-            SMX_TRY(packed_pack_a_rows<T>(Tm + k0, n, n, BLK, ld, kind, pws, slot, t0, tiles, s));
-            SMX_TRY(packed_run<T>(Tm, n, n, BLK, ld, kind, 1, t0, tiles, 0, 0, pws, slot, s));
+            const int* cr = nullptr;
+            if constexpr (sizeof(T) == 2) {
+                if (k0 == 0 && bounded_fastpath_enabled()) {
+                    if ((e = cudaMemsetAsync(cert, 0xFF, sizeof(int), s)) != cudaSuccess) return (int)e;
+                    const int blocks = 4 * sm_count();
+                    cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(Tm + r0 * ld),
+                                                           r1 - (int)r0, BLK, ld, kind == SMX_ANTI, cert);
+                    SMX_LAUNCHED_OR_RETURN();
+                    cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(Tm), BLK, n, ld,
+                                                           kind == SMX_ANTI, cert);
+                    SMX_LAUNCHED_OR_RETURN();
+                    cr = cert;
+                }
+            }
+            SMX_TRY(packed_pack<T>(nullptr, Tm + (long long)k0 * ld, n, n, BLK, ld, ld, kind, pws, slot, s, cr));
+            SMX_TRY(packed_pack_a_rows<T>(Tm + k0, n, n, BLK, ld, kind, pws, slot, t0, tiles, s, cr));
+            SMX_TRY(packed_run<T>(Tm, n, n, BLK, ld, kind, 1, t0, tiles, 0, 0, pws, slot, s, cr));
         }
         // the group's rounds over every row that has arrived (the last group:
         // all rows, up to the blocks of L)
