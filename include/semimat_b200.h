@@ -175,6 +175,13 @@ int smx_fw_pivot(void* P, int b, int ld, int elem_bytes, int kind, void* stream)
 int smx_semiring_gemm_skip(const void* A, const void* B, void* C, int M, int N, int K,
                            int lda, int ldb, int ldc, int elem_bytes, int kind,
                            int skip_row0, int skip_rows, void* stream);
+/* The same product with an operand certificate first (u16): if every lane of
+ * A and B is unreachable or < 2^14, all tiles run the 1-instruction shifted
+ * encoding.  For the first rounds of a closure, whose operands are the
+ * mostly unreachable input graph; same result. */
+int smx_semiring_gemm_skip_certified(const void* A, const void* B, void* C, int M, int N, int K,
+                                     int lda, int ldb, int ldc, int elem_bytes, int kind,
+                                     int skip_row0, int skip_rows, void* stream);
 
 /* ---- Boolean products and Warshall closure ------------------------------
  * Replace BoolMatrix.__mul__ (pkg/src/semimat/boolmat.py:151-172) and

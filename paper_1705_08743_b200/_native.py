@@ -38,6 +38,7 @@ _SIGS = {
     "smx_semiring_gemm_u16": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),
     "smx_semiring_gemm_u32": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),
     "smx_semiring_gemm_skip": ([c_void_p] * 3 + [c_int] * 10 + [c_void_p], c_int),
+    "smx_semiring_gemm_skip_certified": ([c_void_p] * 3 + [c_int] * 10 + [c_void_p], c_int),
     "smx_fw_workspace_bytes": ([c_int, c_int, c_int], c_size_t),
     "smx_fw_u8": ([c_void_p, c_int, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),
     "smx_fw_u16": ([c_void_p, c_int, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),

@@ -1031,17 +1031,39 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
 
 // Bulk row-panel updates of the sharded closure take the packed kernel, its
 // operand tiles in stream-ordered scratch.
+// certify: the sharded closure's first rounds (fw_rounds_packed's certified
+// rounds): check A and B for the shifted 1-instruction encoding first.
 template <typename T>
 static int gemm_skip(const T* A, const T* B, T* C, int M, int N, int K, int lda, int ldb, int ldc, int kind,
-                     int skip_row0, int skip_rows, cudaStream_t s) {
+                     int skip_row0, int skip_rows, cudaStream_t s, bool certify = false) {
     if constexpr (sizeof(T) <= 2) {
         if (g_fw_packed && (long long)M * N >= (1LL << 24) && K > 0 && aligned16(A) && aligned16(B) &&
             aligned16(C)) {
             const size_t bytes = packed_ws_bytes(M, N, K);
             void* ws = nullptr;
-            if (scratch_alloc(&ws, bytes, s) == SMX_OK) {
-                const int rc = semiring_gemm_packed<T>(A, B, C, M, N, K, lda, ldb, ldc, kind, 1, skip_row0,
-                                                       skip_rows, ws, bytes, s);
+            if (scratch_alloc(&ws, bytes + 256, s) == SMX_OK) {
+                int* cert = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + bytes);
+                const int* cr = nullptr;
+                int rc = SMX_OK;
+                if (sizeof(T) == 2 && certify && bounded_fastpath_enabled()) {
+                    cudaError_t e = cudaMemsetAsync(cert, 0xFF, sizeof(int), s);
+                    if (e != cudaSuccess) rc = (int)e;
+                    const int blocks = 4 * sm_count();
+                    if (rc == SMX_OK) {
+                        cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(A), M, K, lda,
+                                                               kind == SMX_ANTI, cert);
+                        cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(B), K, N, ldb,
+                                                               kind == SMX_ANTI, cert);
+                        count_launch();
+                        count_launch();
+                        const cudaError_t le = cudaGetLastError();
+                        if (le != cudaSuccess) rc = (int)le;
+                    }
+                    cr = cert;
+                }
+                if (rc == SMX_OK) rc = packed_pack<T>(A, B, M, N, K, lda, ldb, kind, ws, bytes, s, cr);
+                if (rc == SMX_OK)
+                    rc = packed_run<T>(C, M, N, K, ldc, kind, 1, 0, -1, skip_row0, skip_rows, ws, bytes, s, cr);
                 scratch_free(ws, s);
                 return rc;
             }
@@ -1076,6 +1098,26 @@ int smx_semiring_gemm_u32(const uint32_t* A, const uint32_t* B, uint32_t* C, int
                           int lda, int ldb, int ldc, int kind, int accumulate, void* stream) {
     return semiring_gemm<uint32_t>(A, B, C, M, N, K, lda, ldb, ldc, kind, accumulate, 0, 0,
                                    as_stream(stream), /*certify=*/true);
+}
+
+static int gemm_skip_entry(const void* A, const void* B, void* C, int M, int N, int K, int lda, int ldb, int ldc,
+                           int elem_bytes, int kind, int skip_row0, int skip_rows, void* stream, bool certify) {
+    cudaStream_t s = as_stream(stream);
+    switch (elem_bytes) {
+        case 1: return gemm_skip<uint8_t>((const uint8_t*)A, (const uint8_t*)B, (uint8_t*)C, M, N, K, lda, ldb,
+                                          ldc, kind, skip_row0, skip_rows, s);
+        case 2: return gemm_skip<uint16_t>((const uint16_t*)A, (const uint16_t*)B, (uint16_t*)C, M, N, K, lda, ldb,
+                                           ldc, kind, skip_row0, skip_rows, s, certify);
+        case 4: return gemm_skip<uint32_t>((const uint32_t*)A, (const uint32_t*)B, (uint32_t*)C, M, N, K, lda,
+                                           ldb, ldc, kind, skip_row0, skip_rows, s);
+        default: return SMX_E_ARG;
+    }
+}
+
+int smx_semiring_gemm_skip_certified(const void* A, const void* B, void* C, int M, int N, int K, int lda,
+                                     int ldb, int ldc, int elem_bytes, int kind, int skip_row0,
+                                     int skip_rows, void* stream) {
+    return gemm_skip_entry(A, B, C, M, N, K, lda, ldb, ldc, elem_bytes, kind, skip_row0, skip_rows, stream, true);
 }
 
 int smx_semiring_gemm_skip(const void* A, const void* B, void* C, int M, int N, int K, int lda,

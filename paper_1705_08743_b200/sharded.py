@@ -62,6 +62,10 @@ class CudaFwOps:
         # callers with >= 4096 rows per rank pass 512 (see block_for)
         self.block = min(block or 256, mx)
         self._cp = None
+        # set by ShardedFW for its first two rounds: their operands are the
+        # mostly unreachable input graph, so the updates certify them for the
+        # 1-instruction shifted encoding (fw.cu, fw_rounds_packed)
+        self.certify = False
 
     @staticmethod
     def block_for(n: int, world: int, width: int) -> int:
@@ -102,7 +106,9 @@ class CudaFwOps:
         if hi <= lo:
             return
         s0, sn = (skip[0] - lo, skip[1]) if skip is not None else (0, 0)
-        _native.check(_native.lib().smx_semiring_gemm_skip(
+        fn = (_native.lib().smx_semiring_gemm_skip_certified if self.certify
+              else _native.lib().smx_semiring_gemm_skip)
+        _native.check(fn(
             self._at(cp, lo, 0), panel.data_ptr(), self._at(t, lo, 0), hi - lo, n, b, cp.shape[1],
             panel.shape[1], t.shape[1], self.eb, self.kind, s0, sn, _native.stream_ptr(t.device)),
             "row-panel update")
@@ -206,6 +212,8 @@ class ShardedFW:
         self._bcast(self._panel(local, 0), 0)
         for r in range(R):
             k0, bb = r * B, self._bb(r * B)
+            if hasattr(ops, "certify"):
+                ops.certify = r < 2
             panel = self._panel(local, r)
             cp = ops.snapshot(local, k0, bb)
             own_r = self.owner(k0) == self.rank
@@ -231,6 +239,8 @@ class ShardedFW:
                     main.wait_event(join)
             else:
                 ops.update_rows(local, cp, panel, bb, n, 0, rows, (skip_lo, skip_n) if skip_n else None)
+        if hasattr(ops, "certify"):
+            ops.certify = False
         return local
 
 
