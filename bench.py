@@ -170,6 +170,14 @@ def load_traffic(workload: str):
 
 # --------------------------------------------------------------------------- CPU (reference algorithm)
 
+# Size of the bounded CPU sample (cpu_baseline and the --impl reference arm):
+# about 10 s of the reference algorithm on the box's host cores.  For the
+# closure that is the C4 size, n = 8192 (9 s with 16 threads; the 128 MiB
+# matrix no longer sits in the host caches, as the full-size one would not:
+# 6.1e10 cell-updates/s there against 1.3-2.2e11 at n = 2048 / 4096).
+CPU_SAMPLE_N = {"closure": 8192, "mul": 4096, "bool_mul": 1024, "bool_closure": 4096}
+
+
 def cpu_fw_sample(n_sample: int, threads: int = 0):
     """The reference algorithm (C restatement of _close_vector, all host
     threads) on the c5 generator at n_sample: returns (cells/s, seconds, out)."""
@@ -201,7 +209,7 @@ def run_reference(args, world, rank):
     oracle.build()
     cfg = workloads.CONFIGS[args.workload]
     threads = oracle.max_threads()
-    n_sample = {"closure": 2048, "mul": 2048, "bool_mul": 1024, "bool_closure": 4096}[cfg.op]
+    n_sample = CPU_SAMPLE_N[cfg.op]
 
     def step():
         if cfg.op == "closure":
@@ -501,7 +509,7 @@ def run_ours(args, world, rank, local_rank):
             import oracle
             oracle.build()
             thr = oracle.max_threads()
-            n_s = cfg.oracle_n
+            n_s = CPU_SAMPLE_N[cfg.op]
             if cfg.op == "closure":
                 cps, cdt, cpu_out, t_in = cpu_fw_sample(n_s, thr)
                 gpu_out = AntidistMatrix(n_s, n_s, 16, t_in).transitive_closure().data
