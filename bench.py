@@ -210,6 +210,8 @@ def run_reference(args, world, rank):
     cfg = workloads.CONFIGS[args.workload]
     threads = oracle.max_threads()
     n_sample = CPU_SAMPLE_N[cfg.op]
+    if cfg.op == "closure" and args.steps + args.warmup > 16:
+        n_sample = 4096   # keep a long --steps/--warmup run within a few minutes (0.3 s per step)
 
     def step():
         if cfg.op == "closure":
