@@ -195,6 +195,12 @@ int smx_semiring_gemm_skip_certified(const void* A, const void* B, void* C, int 
 int smx_bool_gemm_i8(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* C_bits,
                      int M, int N, int K, int lda, int ldbt, int ldc, int accumulate,
                      void* stream);
+/* Kernel choice for packed-bit products of at most one wave of 128 x 64
+ * tiles (e.g. C1, 1024^3): 0 = automatic (K >= 1024: K split over a 4-CTA
+ * cluster on 128 x 256 tiles, partial bits OR-merged over DSMEM), 1 = the
+ * plain one-CTA-per-tile kernel, 2 = split 2 x (128 x 128), 3 = split
+ * 4 x (128 x 256).  Results are identical.  Returns the previous setting. */
+int smx_set_tc_variant(int variant);
 /* BoolMatrix.__mul__ on packed bit rows in one call (unpack A, fused
  * bits -> B^T bytes, tcgen05 product with the packed-bit epilogue).  C rows
  * are fully written, padding words zeroed.  Workspace: see
@@ -240,6 +246,38 @@ int smx_lane_entrywise(const void* A, const void* B, void* C, int rows, int cols
                        int elem_bytes, int op, int pad_is_limit, void* stream);
 int smx_bits_entrywise(const uint32_t* A, const uint32_t* B, uint32_t* C, int rows, int cols,
                        int ld_w, int op, void* stream);
+
+/* ---- lane kernels (kernels.py:129-204) ---------------
+ * The paper's 128-bit block primitives over a flat array of nlanes lanes
+ * (nlanes * elem_bytes a multiple of 16): op 0 = subsat max(a-b,0),
+ * 1 = addsat min(a+b,S), 2 = max, 3 = min, 4 = |a-b|, 5 = clonenot S-a (B
+ * unused).  Replaces subsat/addsat/maxlanes/minlanes/absdiff/clonenot
+ * (kernels.py:129-189) and np_subsat/np_addsat/np_absdiff (:195-204). */
+int smx_lane_op(const void* A, const void* B, void* C, long long nlanes, int elem_bytes, int op,
+                void* stream);
+
+/* ---- Boolean bridge (antidist.py:213-224) -------------------------------
+ * from_boolmat: lanes = S where the bit is set, else 0; padding lanes 0.
+ * to_boolmat: bit = (lane > 0) for columns < cols; every other bit of the
+ * ld_w words 0. */
+int smx_lanes_from_bits(const uint32_t* words, int ld_w, void* out, int rows, int cols, int ld,
+                        int elem_bytes, void* stream);
+int smx_lanes_to_bits(const void* in, int ld, uint32_t* words, int ld_w, int rows, int cols,
+                      int elem_bytes, void* stream);
+
+/* ---- batched small matrices (one launch per batch) ----------------------
+ * `batch` independent problems, each matrix `stride_*` elements (words for
+ * bits, lanes for lane matrices) after the previous one.
+ * Boolean product (boolmat.py:151-172) on packed rows: C = A (x) B, padding
+ * words of C zeroed.  Boolean Warshall (boolmat.py:174-189), n <= 512, in
+ * place.  Lane Floyd-Warshall (antidist.py:390-398, :440-448), n <= 128, in
+ * place, padding lanes untouched. */
+int smx_bool_mul_batched(const uint32_t* A, const uint32_t* B, uint32_t* C, int batch, int M, int N,
+                         int K, int lda_w, int ldb_w, int ldc_w, long long stride_a,
+                         long long stride_b, long long stride_c, void* stream);
+int smx_bool_warshall_batched(uint32_t* T, int batch, int n, int ld_w, long long stride, void* stream);
+int smx_fw_batched(void* T, int batch, int n, int ld, long long stride, int elem_bytes, int kind,
+                   void* stream);
 
 /* ---- construction (antidist.py:191-211, :294-309) ---------------------
  * Fill the n x ld matrix T with the (+)-identity (0 anti / S dist, padding

@@ -53,7 +53,8 @@ def _load():
                 fn = getattr(lib, name)
                 fn.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, u32, ci]
                 fn.restype = None
-            for name in (f"orc_anti_close_{suf}", f"orc_minplus_close_{suf}"):
+            for name in (f"orc_anti_close_{suf}", f"orc_minplus_close_{suf}",
+                         f"orc_anti_close_blocked_{suf}", f"orc_minplus_close_blocked_{suf}"):
                 fn = getattr(lib, name)
                 fn.argtypes = [vp, i64, i64, i64, u32, ci]
                 fn.restype = None
@@ -109,6 +110,18 @@ def semiring_close(t: np.ndarray, width: int, kind: str, threads: int = 0) -> np
     """
     out = np.array(_lane(t, width), copy=True)
     name = ("orc_anti_close_" if kind == "anti" else "orc_minplus_close_") + _SUFFIX[width]
+    getattr(_load(), name)(_ptr(out), out.shape[0], out.shape[1], out.shape[1],
+                           _limit(width), threads)
+    return out
+
+
+def semiring_close_blocked(t: np.ndarray, width: int, kind: str, threads: int = 0) -> np.ndarray:
+    """The same closure as ``semiring_close`` in the cache-blocked three-phase
+    order (semimat_oracle.c, DEFINE_CLOSE_BLOCKED): bit-identical to the
+    reference's sweep (pinned by
+    tests/test_oracle_golden.py), fast enough for the full-size C5 pin."""
+    out = np.array(_lane(t, width), copy=True)
+    name = ("orc_anti_close_blocked_" if kind == "anti" else "orc_minplus_close_blocked_") + _SUFFIX[width]
     getattr(_load(), name)(_ptr(out), out.shape[0], out.shape[1], out.shape[1],
                            _limit(width), threads)
     return out

@@ -201,3 +201,126 @@ ORC_API void orc_bool_close(uint64_t* t, int64_t dim, int64_t bwords, int64_t ld
 }
 
 ORC_API int orc_max_threads(void) { return orc_threads(0); }
+
+/* ---------------------------------------------------------------------------
+ * Cache-blocked restatement of the same closures (test infrastructure for the
+ * full-size C5 pin, n = 32768, where the plain k-sweep above streams the whole
+ * 2 GiB matrix once per k and would take hours on the build host).
+ *
+ * Same per-cell arithmetic as _close_vector / _minplus_close_vector
+ * (antidist.py:390-398, :440-448; the np_subsat / np_addsat rewrites of
+ * kernels.py:195-200) and the same zero / S skip; only the order of the
+ * (i, j, k) updates changes, to the classic blocked three-phase schedule:
+ *   1. the pivot tile T[K,K] by the plain in-place k-sweep;
+ *   2. the pivot row panel T[K,J] and column panel T[I,K], k-sweep over K
+ *      with the closed pivot tile;
+ *   3. every other tile T[I,J] (+)= T[I,K] (x) T[K,J].
+ * That this order is bit-identical to the reference's vertex-at-a-time sweep
+ * is SURVEY.md 0.1 fact 2 (x -> min(x, S) is a semiring homomorphism from
+ * (min,+) on [0,inf]); tests/test_oracle_golden.py checks it against the
+ * plain sweep above and against the reference's own sha256 of the C4 n = 8192
+ * closure, so it is pinned independently of the GPU path.
+ * ------------------------------------------------------------------------- */
+#define ORC_BLK 128
+#define ORC_JT 2048
+
+#define DEFINE_CLOSE_BLOCKED(T, SUF)                                               \
+static void orc_fold_anti_##SUF(T* o, const T* x, T e, T S, int64_t n) {          \
+    const T gap = (T)(S - e);                                                      \
+    for (int64_t j = 0; j < n; ++j) {                                              \
+        const T v = x[j];                                                          \
+        const T cand = (T)((v > gap ? v : gap) - gap);                             \
+        o[j] = o[j] > cand ? o[j] : cand;                                          \
+    }                                                                              \
+}                                                                                  \
+static void orc_fold_minplus_##SUF(T* o, const T* x, T e, T S, int64_t n) {       \
+    const T room = (T)(S - e);                                                     \
+    for (int64_t j = 0; j < n; ++j) {                                              \
+        const T v = x[j];                                                          \
+        const T cand = (T)((v < room ? v : room) + e);                             \
+        o[j] = o[j] < cand ? o[j] : cand;                                          \
+    }                                                                              \
+}                                                                                  \
+/* k-outer sweep of rows [i0,i1) x cols [j0,j1) over pivots [k0,k1) */            \
+static void orc_sweep_##SUF(T* t, int64_t ld, int64_t i0, int64_t i1, int64_t j0,  \
+                            int64_t j1, int64_t k0, int64_t k1, T S, int anti) {   \
+    for (int64_t k = k0; k < k1; ++k)                                              \
+        for (int64_t i = i0; i < i1; ++i) {                                        \
+            const T e = t[i * ld + k];                                             \
+            if (anti ? e == 0 : e == S) continue;                                  \
+            if (anti) orc_fold_anti_##SUF(t + i * ld + j0, t + k * ld + j0, e, S, j1 - j0); \
+            else orc_fold_minplus_##SUF(t + i * ld + j0, t + k * ld + j0, e, S, j1 - j0); \
+        }                                                                          \
+}                                                                                  \
+static void orc_close_blocked_##SUF(T* t, int64_t dim, int64_t cols, int64_t ld,    \
+                                    uint32_t limit, int threads, int anti) {       \
+    const T S = (T)limit;                                                          \
+    const int nt = orc_threads(threads);                                           \
+    const int64_t nb = (dim + ORC_BLK - 1) / ORC_BLK;                              \
+    const int64_t njt = (cols + ORC_JT - 1) / ORC_JT;                              \
+    for (int64_t kb = 0; kb < nb; ++kb) {                                          \
+        const int64_t k0 = kb * ORC_BLK, k1 = k0 + ORC_BLK < dim ? k0 + ORC_BLK : dim; \
+        orc_sweep_##SUF(t, ld, k0, k1, k0, k1, k0, k1, S, anti);                   \
+        /* row panel T[K, outside K] (padding columns included) and column    \
+         * panel T[outside K, K]; both read only the closed pivot tile and     \
+         * their own tiles */                                                  \
+        _Pragma("omp parallel for schedule(dynamic, 1) num_threads(nt)")          \
+        for (int64_t x = 0; x < njt + nb; ++x) {                                  \
+            if (x < njt) {                                                         \
+                int64_t j0 = x * ORC_JT, j1 = j0 + ORC_JT < cols ? j0 + ORC_JT : cols; \
+                if (j0 < k0) {                                                     \
+                    int64_t e1 = j1 < k0 ? j1 : k0;                                \
+                    orc_sweep_##SUF(t, ld, k0, k1, j0, e1, k0, k1, S, anti);       \
+                }                                                                  \
+                if (j1 > k1) {                                                     \
+                    int64_t s0 = j0 > k1 ? j0 : k1;                                \
+                    orc_sweep_##SUF(t, ld, k0, k1, s0, j1, k0, k1, S, anti);       \
+                }                                                                  \
+            } else {                                                               \
+                int64_t ib = x - njt;                                              \
+                if (ib == kb) continue;                                            \
+                int64_t i0 = ib * ORC_BLK, i1 = i0 + ORC_BLK < dim ? i0 + ORC_BLK : dim; \
+                orc_sweep_##SUF(t, ld, i0, i1, k0, k1, k0, k1, S, anti);           \
+            }                                                                      \
+        }                                                                          \
+        /* everything else: T[I,J] (+)= T[I,K] (x) T[K,J], rows i-outer */       \
+        _Pragma("omp parallel for schedule(dynamic, 1) num_threads(nt)")          \
+        for (int64_t x = 0; x < nb * njt; ++x) {                                  \
+            const int64_t ib = x / njt, jt = x % njt;                              \
+            if (ib == kb) continue;                                                \
+            const int64_t i0 = ib * ORC_BLK, i1 = i0 + ORC_BLK < dim ? i0 + ORC_BLK : dim; \
+            const int64_t j0 = jt * ORC_JT, j1 = j0 + ORC_JT < cols ? j0 + ORC_JT : cols; \
+            for (int64_t i = i0; i < i1; ++i) {                                    \
+                T* row = t + i * ld;                                               \
+                for (int64_t k = k0; k < k1; ++k) {                                \
+                    const T e = row[k];                                            \
+                    if (anti ? e == 0 : e == S) continue;                          \
+                    /* skip the pivot columns: they are the column panel,      \
+                     * already final */                                        \
+                    if (j0 < k0) {                                                 \
+                        int64_t e1 = j1 < k0 ? j1 : k0;                            \
+                        if (anti) orc_fold_anti_##SUF(row + j0, t + k * ld + j0, e, S, e1 - j0); \
+                        else orc_fold_minplus_##SUF(row + j0, t + k * ld + j0, e, S, e1 - j0); \
+                    }                                                              \
+                    if (j1 > k1) {                                                 \
+                        int64_t s0 = j0 > k1 ? j0 : k1;                            \
+                        if (anti) orc_fold_anti_##SUF(row + s0, t + k * ld + s0, e, S, j1 - s0); \
+                        else orc_fold_minplus_##SUF(row + s0, t + k * ld + s0, e, S, j1 - s0); \
+                    }                                                              \
+                }                                                                  \
+            }                                                                      \
+        }                                                                          \
+    }                                                                              \
+}                                                                                  \
+ORC_API void orc_anti_close_blocked_##SUF(T* t, int64_t dim, int64_t cols, int64_t ld, \
+                                          uint32_t limit, int threads) {           \
+    orc_close_blocked_##SUF(t, dim, cols, ld, limit, threads, 1);                  \
+}                                                                                  \
+ORC_API void orc_minplus_close_blocked_##SUF(T* t, int64_t dim, int64_t cols, int64_t ld, \
+                                             uint32_t limit, int threads) {        \
+    orc_close_blocked_##SUF(t, dim, cols, ld, limit, threads, 0);                  \
+}
+
+DEFINE_CLOSE_BLOCKED(uint8_t, u8)
+DEFINE_CLOSE_BLOCKED(uint16_t, u16)
+DEFINE_CLOSE_BLOCKED(uint32_t, u32)

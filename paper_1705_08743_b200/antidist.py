@@ -179,6 +179,8 @@ class _LaneMatrix:
                 f"shape/width mismatch: {self.rows}x{self.cols}/w{self.width} vs "
                 f"{other.rows}x{other.cols}/w{other.width}"
             )
+        if self.device != other.device:
+            raise ValueError(f"operands live on different devices: {self.device} vs {other.device}")
 
     def _entrywise(self, other, op: int, out_cls):
         out = torch.empty_like(self._data)
@@ -232,6 +234,8 @@ class _LaneMatrix:
                 f"inner dimensions disagree: {self.rows}x{self.cols} times "
                 f"{other.rows}x{other.cols}"
             )
+        if self.device != other.device:
+            raise ValueError(f"operands live on different devices: {self.device} vs {other.device}")
 
     def transitive_close(self) -> None:
         """In-place Floyd-Warshall closure (antidist.py:252-261 / :331-340)."""
@@ -291,16 +295,25 @@ class AntidistMatrix(_LaneMatrix):
 
     @classmethod
     def from_boolmat(cls, mat: BoolMatrix, width: int = 8) -> "AntidistMatrix":
-        """1 -> distance zero (S), 0 -> unreachable (antidist.py:213-219)."""
-        limit = sat_limit(width)
-        bits = mat.to_numpy().astype(_NP[width])
-        host = np.zeros((mat.rows, -(-mat.cols // LANES[width]) * LANES[width]), dtype=_NP[width])
-        host[:, : mat.cols] = bits * limit
-        return cls(mat.rows, mat.cols, width, host)
+        """1 -> distance zero (S), 0 -> unreachable (antidist.py:213-219); one
+        device pass from the packed bit rows (smx_lanes_from_bits)."""
+        lanes = lane_count(width)
+        padded = -(-mat.cols // lanes) * lanes
+        out = torch.empty((mat.rows, padded), dtype=_TORCH[width], device=mat.device)
+        _native.check(_native.lib().smx_lanes_from_bits(
+            mat._words.data_ptr(), mat.stride_words, out.data_ptr(), mat.rows, mat.cols, padded,
+            width // 8, _native.stream_ptr(mat.device)), "smx_lanes_from_bits")
+        return cls(mat.rows, mat.cols, width, out)
 
     def to_boolmat(self) -> BoolMatrix:
-        """Any finite distance becomes 1 (antidist.py:221-224)."""
-        return BoolMatrix.from_numpy((self.to_numpy()[:, : self.cols] > 0).astype(np.uint8))
+        """Any finite distance becomes 1 (antidist.py:221-224); one device pass
+        to the packed bit rows (smx_lanes_to_bits)."""
+        from .boolmat import _stride_words
+        words = torch.empty((self.rows, _stride_words(self.cols)), dtype=torch.int32, device=self.device)
+        _native.check(_native.lib().smx_lanes_to_bits(
+            self._data.data_ptr(), self.padded_cols, words.data_ptr(), words.shape[1], self.rows,
+            self.cols, self.width // 8, _native.stream_ptr(self.device)), "smx_lanes_to_bits")
+        return BoolMatrix(self.rows, self.cols, words)
 
     def __mul__(self, other) -> "AntidistMatrix":
         """max over k of the saturated sum (antidist.py:226-250)."""

@@ -15,6 +15,22 @@ static std::atomic<int> g_lookahead{1};
 static std::atomic<int> g_graphs{1};
 int lookahead_enabled() { return g_lookahead.load(std::memory_order_relaxed); }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int set_max_smem(const void* func, size_t bytes) {
+    struct Entry { int dev; const void* fn; size_t bytes; };
+    static std::mutex mu;
+    static std::vector<Entry> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return (int)e;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Entry& x : done)
+        if (x.dev == dev && x.fn == func && x.bytes >= bytes) return SMX_OK;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return (int)e;
+    done.push_back({dev, func, bytes});
+    return SMX_OK;
+}
 int bounded_fastpath_enabled() { return g_bounded.load(std::memory_order_relaxed); }
 
 int scratch_alloc(void** p, size_t bytes, cudaStream_t s) {

@@ -375,13 +375,7 @@ int launch_bits(const BitsArgs& a_in, cudaStream_t s) {
     smx::count_launch();
     if (g_bits_m4r.load(std::memory_order_relaxed)) {
         constexpr size_t smem = M4rSmem<Cfg>::BYTES;
-        static bool configured = false;   // per instantiation
-        if (!configured) {
-            cudaError_t e = cudaFuncSetAttribute(bool_m4r_gemm_kernel<Cfg>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return (int)e;
-            configured = true;
-        }
+        SMX_TRY(set_max_smem((const void*)bool_m4r_gemm_kernel<Cfg>, smem));
         const cudaError_t e = launch_kernel(bool_m4r_gemm_kernel<Cfg>, grid, dim3(Cfg::THREADS), smem, s, a);
         return e == cudaSuccess ? SMX_OK : (int)e;
     }

@@ -16,6 +16,11 @@ namespace smx {
 // Counts every kernel this library launches (smx_launch_count), so bench.py
 // reports launches it observed rather than a formula.
 void count_launch();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `func` on the current
+// device, done once per (device, function, size) and thread-safe: a process
+// that drives several GPUs, or calls from several threads, never launches a
+// kernel whose > 48 KB opt-in was set on another device only.
+int set_max_smem(const void* func, size_t bytes);
 
 // Per-device highest-priority side stream with fork/join events, used by the
 // look-ahead closure schedules (created once, reused; see abi.cu).

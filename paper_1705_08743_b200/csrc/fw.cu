@@ -369,12 +369,7 @@ template <typename T, int BLK>
 int launch_pivot_lite(T* P, int b, long long ld, int kind, cudaStream_t s) {
     constexpr size_t smem = (size_t)BLK * (BLK / Lane<T>::kCellsPerWord) * 4;
     auto kern = fw_pivot_lite_kernel<T, BLK>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        configured = true;
-    }
+    SMX_TRY(set_max_smem((const void*)kern, smem));
     smx::count_launch();
     const cudaError_t e = launch_kernel(kern, dim3(1), dim3(256), smem, s, P, b, ld, kind == SMX_ANTI);
     return e == cudaSuccess ? SMX_OK : (int)e;
@@ -1037,8 +1032,12 @@ template <typename T>
 static int gemm_skip(const T* A, const T* B, T* C, int M, int N, int K, int lda, int ldb, int ldc, int kind,
                      int skip_row0, int skip_rows, cudaStream_t s, bool certify = false) {
     if constexpr (sizeof(T) <= 2) {
+        // the packed path (and its certificate pass, which reads 16-byte
+        // vectors at X + r*ld) needs 16-byte aligned bases AND row strides;
+        // anything else takes the register-staged GEMM below
         if (g_fw_packed && (long long)M * N >= (1LL << 24) && K > 0 && aligned16(A) && aligned16(B) &&
-            aligned16(C)) {
+            aligned16(C) && ld_ok(lda, sizeof(T)) && ld_ok(ldb, sizeof(T)) && ld_ok(ldc, sizeof(T)) &&
+            lda >= K && ldb >= N && ldc >= N) {
             const size_t bytes = packed_ws_bytes(M, N, K);
             void* ws = nullptr;
             if (scratch_alloc(&ws, bytes + 256, s) == SMX_OK) {
@@ -1123,16 +1122,7 @@ int smx_semiring_gemm_skip_certified(const void* A, const void* B, void* C, int 
 int smx_semiring_gemm_skip(const void* A, const void* B, void* C, int M, int N, int K, int lda,
                            int ldb, int ldc, int elem_bytes, int kind, int skip_row0,
                            int skip_rows, void* stream) {
-    cudaStream_t s = as_stream(stream);
-    switch (elem_bytes) {
-        case 1: return gemm_skip<uint8_t>((const uint8_t*)A, (const uint8_t*)B, (uint8_t*)C, M, N, K, lda, ldb,
-                                          ldc, kind, skip_row0, skip_rows, s);
-        case 2: return gemm_skip<uint16_t>((const uint16_t*)A, (const uint16_t*)B, (uint16_t*)C, M, N, K, lda, ldb,
-                                           ldc, kind, skip_row0, skip_rows, s);
-        case 4: return gemm_skip<uint32_t>((const uint32_t*)A, (const uint32_t*)B, (uint32_t*)C, M, N, K, lda,
-                                           ldb, ldc, kind, skip_row0, skip_rows, s);
-        default: return SMX_E_ARG;
-    }
+    return gemm_skip_entry(A, B, C, M, N, K, lda, ldb, ldc, elem_bytes, kind, skip_row0, skip_rows, stream, false);
 }
 
 int smx_fw_block_for(int n, int elem_bytes) {

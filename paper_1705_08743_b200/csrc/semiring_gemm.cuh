@@ -428,13 +428,7 @@ template <typename Cfg, typename T>
 int launch_semiring_gemm(const GemmArgs<T>& a, cudaStream_t stream) {
     if (a.rowflags != nullptr) {
         auto kern = semiring_gemm_kernel<Cfg, T, true>;
-        static bool configured = false;  // per instantiation
-        if (!configured) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)Cfg::SMEM);
-            if (e != cudaSuccess) return (int)e;
-            configured = true;
-        }
+        SMX_TRY(set_max_smem((const void*)kern, Cfg::SMEM));
         const int mtiles = ceil_div(a.M, Cfg::BM) - a.skip_tiles;
         const int ntiles = ceil_div(a.N, Cfg::BN);
         if (mtiles <= 0 || ntiles <= 0) return SMX_OK;
@@ -443,13 +437,7 @@ int launch_semiring_gemm(const GemmArgs<T>& a, cudaStream_t stream) {
         return e == cudaSuccess ? SMX_OK : (int)e;
     }
     auto kern = semiring_gemm_kernel<Cfg, T, false>;
-    static bool configured = false;  // per instantiation
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)Cfg::SMEM);
-        if (e != cudaSuccess) return (int)e;
-        configured = true;
-    }
+    SMX_TRY(set_max_smem((const void*)kern, Cfg::SMEM));
     const int mtiles = ceil_div(a.M, Cfg::BM) - a.skip_tiles;
     const int ntiles = ceil_div(a.N, Cfg::BN);
     if (mtiles <= 0 || ntiles <= 0) return SMX_OK;

@@ -494,13 +494,7 @@ inline int packed_run(T* C, int M, int N, int K, long long ldc, int kind, int ac
     }
     const int mtiles = row_tiles - a.skip_tiles;
     if (mtiles <= 0) return SMX_OK;
-    static bool configured = false;   // per instantiation
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(packed_gemm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)G::SMEM);
-        if (e != cudaSuccess) return (int)e;
-        configured = true;
-    }
+    SMX_TRY(set_max_smem((const void*)packed_gemm_kernel<T>, G::SMEM));
     packed_gemm_kernel<T><<<dim3(v.NT, mtiles), G::THREADS, G::SMEM, s>>>(a);
     SMX_RETURN_LAUNCH();
 }

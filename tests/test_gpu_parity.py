@@ -119,7 +119,8 @@ def _gpu_output(cfg, n):
 def test_config_matches_reference_digest(config_digests, name):
     cfg = workloads.CONFIGS[name]
     for d in config_digests:
-        if d["config"] == name:
+        # full-size oracle pins (band digests) have their own test
+        if d["config"] == name and "band_sha256" not in d:
             assert sha(_gpu_output(cfg, d["n"])) == d["output_sha256"], (name, d["n"])
 
 

@@ -160,3 +160,45 @@ def test_matio_fixture_is_self_consistent():
         else:
             dt = {8: "<u1", 16: "<u2", 32: "<u4"}[width]
             assert np.frombuffer(raw[16:], dtype=dt).reshape(rows, cols).tolist() == case["rows"]
+
+
+def test_blocked_oracle_matches_reference_cases(oracle_lib, small_cases):
+    """The cache-blocked closure (used for the full-size C5 pin) reproduces
+    every reference closure fixture, anti and dist, all widths."""
+    n = 0
+    for meta, arr in small_cases:
+        if meta["op"] != "closure":
+            continue
+        got = oracle_lib.semiring_close_blocked(arr["t"], meta["width"], meta["kind"])
+        np.testing.assert_array_equal(got, arr["out"], err_msg=meta["name"])
+        n += 1
+    assert n >= 70
+
+
+@pytest.mark.parametrize("width,kind", [(8, "anti"), (16, "dist"), (32, "anti"), (16, "anti")])
+def test_blocked_oracle_matches_plain_sweep(oracle_lib, width, kind):
+    """Blocked order == the reference's vertex-at-a-time sweep on sizes that
+    straddle the 128 block and the 2048 column tile (ragged, padded)."""
+    rng = np.random.default_rng(width * 7 + len(kind))
+    S = LIMIT[width]
+    dt = {8: np.uint8, 16: np.uint16, 32: np.uint32}[width]
+    lanes = {8: 16, 16: 8, 32: 4}[width]
+    for n in (1, 127, 129, 300, 2100):
+        cp = -(-n // lanes) * lanes
+        mask = rng.random((n, n)) < min(1.0, 3.0 / n)
+        vals = S - rng.integers(1, 1000 if width > 8 else 254, size=(n, n))
+        t = np.full((n, cp), 0 if kind == "anti" else S, dtype=dt)
+        t[:, :n] = np.where(mask, vals if kind == "anti" else S - vals, t[:, :n])
+        np.testing.assert_array_equal(oracle_lib.semiring_close_blocked(t, width, kind),
+                                      oracle_lib.semiring_close(t, width, kind), err_msg=str(n))
+
+
+def test_blocked_oracle_reproduces_reference_c4_8192(oracle_lib, config_digests):
+    """The blocked oracle at the full C4 size equals the reference's own
+    sha256 (a 26-minute run of the reference's numpy engine), so the
+    full-size C5 digest it produced (tools/oracle_full_digest.py) is anchored
+    to the reference at scale, not only to the plain restatement."""
+    d = next(x for x in config_digests if x["config"] == "c4_fw_u16" and x["n"] == 8192)
+    (t,) = workloads.make_inputs(workloads.CONFIGS["c4_fw_u16"], 8192)
+    assert sha(t) == d["input_sha256"][0]
+    assert sha(oracle_lib.semiring_close_blocked(t, 16, "anti")) == d["output_sha256"]
