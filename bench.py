@@ -168,6 +168,89 @@ def load_traffic(workload: str):
     return None
 
 
+def read_fw_trace(lib, cap):
+    """(seconds, cell-updates) of each launch smx_fw_trace_arm recorded."""
+    import ctypes
+    ms_arr = (ctypes.c_float * cap)()
+    cells_arr = (ctypes.c_longlong * cap)()
+    cnt = lib.smx_fw_trace_read(ms_arr, cells_arr, cap)
+    if cnt < 0:
+        raise RuntimeError(f"phase-3 trace read failed ({cnt})")
+    return [(ms_arr[i] / 1e3, cells_arr[i]) for i in range(cnt)]
+
+
+def sharded_roofline(trace, step_secs, n, block, world, dev):
+    """Per-rank roofline of the sharded closure: every rank's bulk updates
+    (3b) of the first timed step, CUDA-event timed on its main stream inside
+    smx_fw_sharded, against that rank's own measured issue ceiling; gathered
+    to every rank."""
+    import torch
+    import torch.distributed as dist
+    trace = trace or []
+    dom = sum(t for t, _ in trace)
+    cells = sum(c for _, c in trace)
+    peaks, sms = measure_issue_peak()
+    issue = max(peaks["one"], peaks["pair"])
+    mine = torch.tensor([cells / dom if dom else 0.0, 2.0 * issue, dom, float(len(trace)), float(cells)],
+                        dtype=torch.float64, device=dev)
+    every = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(every, mine)
+    rows = [r.tolist() for r in every]
+    fr = [r[0] / r[1] for r in rows]
+    r0 = rows[0]
+    return {
+        "bound": "int_issue", "achieved": r0[0] / 1e12, "peak": r0[1] / 1e12, "unit": "Tcell/s",
+        "frac": fr[0], "traffic": None,
+        "kernel": "packed_gemm_u16_kernel (sharded bulk row update 3b, per round)",
+        "sms": sms, "issue_rate": r0[1] / 2.0,
+        "launches_timed": int(r0[3]), "avg_launch_ms": r0[2] / max(r0[3], 1) * 1e3,
+        "share_of_step": r0[2] / step_secs,
+        "per_rank_frac": fr, "per_rank_share_of_step": [r[2] / step_secs for r in rows],
+        "min_frac": min(fr), "max_frac": max(fr),
+        "aggregate_achieved": sum(r[0] for r in rows) / 1e12,
+        "peak_source": "measured on every rank: smx_int_issue_probe x 2 cells per u16x2 instruction",
+        "algorithmic_bytes_per_launch": (2 * (n // world) * block + 2 * (n // world) * n) * 2,
+    }
+
+
+def full_size_digest(config: str, n: int):
+    """The CPU oracle's committed digest of this config's closure at size n
+    (tests/golden/config_digests.json; at n = 32768 from
+    tools/oracle_full_digest.py), or None."""
+    p = REPO / "tests" / "golden" / "config_digests.json"
+    if not p.exists():
+        return None
+    for d in json.loads(p.read_text()):
+        if d["config"] == config and d["n"] == n:
+            return d
+    return None
+
+
+def sharded_parity(work, cfg, n, world, rank, block, dev, digest):
+    """The gathered sharded closure, bit for bit: against the oracle's
+    committed sha256 when one exists for (config, n), else against the
+    single-GPU closure of the same input (itself oracle-checked)."""
+    import hashlib
+    import torch
+    from paper_1705_08743_b200 import _native, sharded, workloads
+    torch.cuda.synchronize()
+    full = sharded.gather_rows(work, n, world, block)
+    if rank != 0:
+        return None
+    if digest is not None:
+        got = hashlib.sha256(full.cpu().numpy().tobytes()).hexdigest()
+        return {"n": n, "bit_exact_vs_oracle_digest": got == digest["output_sha256"],
+                "oracle_sha256": digest["output_sha256"][:16]}
+    lib = _native.lib()
+    (ref_host,) = workloads.make_inputs(cfg, n)
+    ref = torch.from_numpy(ref_host).to(dev)
+    rws = _native.workspace(lib.smx_fw_workspace_bytes(n, ref.shape[1], cfg.width // 8), dev)
+    _native.check(getattr(lib, f"smx_fw_u{cfg.width}")(
+        ref.data_ptr(), n, ref.shape[1], _native.SMX_ANTI, rws.data_ptr(), rws.numel(),
+        _native.stream_ptr(dev)), "fw")
+    return {"n": n, "bit_exact_vs_single_gpu": bool(torch.equal(full, ref))}
+
+
 # --------------------------------------------------------------------------- CPU (reference algorithm)
 
 # Size of the bounded CPU sample (cpu_baseline and the --impl reference arm):
@@ -176,6 +259,7 @@ def load_traffic(workload: str):
 # matrix no longer sits in the host caches, as the full-size one would not:
 # 6.1e10 cell-updates/s there against 1.3-2.2e11 at n = 2048 / 4096).
 CPU_SAMPLE_N = {"closure": 8192, "mul": 4096, "bool_mul": 1024, "bool_closure": 4096}
+REF_MAX_STEPS, REF_MAX_WARMUP = 4, 1
 
 
 def cpu_fw_sample(n_sample: int, threads: int = 0):
@@ -200,6 +284,32 @@ def cpu_mul_sample(cfg, n_sample: int, threads: int = 0):
     return n_sample ** 3 / dt, dt, out
 
 
+def cpu_baseline_and_parity(cfg):
+    """cpu_baseline (the reference algorithm, C restatement, all host threads,
+    on CPU_SAMPLE_N of the same generator) and this GPU's result on the same
+    sample compared bit for bit."""
+    import oracle
+    from paper_1705_08743_b200 import AntidistMatrix, workloads
+    oracle.build()
+    thr = oracle.max_threads()
+    n_s = CPU_SAMPLE_N[cfg.op]
+    if cfg.op == "closure":
+        cps, cdt, cpu_out, t_in = cpu_fw_sample(n_s, thr)
+        gpu_out = AntidistMatrix(n_s, n_s, 16, t_in).transitive_closure().data
+    else:
+        cps, cdt, cpu_out = cpu_mul_sample(cfg, n_s, thr)
+        ai, bi = workloads.make_inputs(cfg, n_s)
+        gpu_out = (AntidistMatrix(n_s, n_s, cfg.width, ai) * AntidistMatrix(n_s, n_s, cfg.width, bi)).data
+    return {
+        "cpu_baseline": {
+            "value": cps, "unit": UNIT, "cores": thr, "kind": "port",
+            "sample": f"{cfg.name} generator at n={n_s}, one "
+                      f"{'closure' if cfg.op == 'closure' else 'product'} "
+                      f"({cdt:.2f} s), C restatement of the reference engine, OpenMP rows"},
+        "parity": {"n": n_s, "bit_exact_vs_oracle": bool(np.array_equal(gpu_out, cpu_out))},
+    }
+
+
 def run_reference(args, world, rank):
     """--impl reference: the reference algorithm on host cores, same metric."""
     if rank != 0:
@@ -209,9 +319,11 @@ def run_reference(args, world, rank):
     oracle.build()
     cfg = workloads.CONFIGS[args.workload]
     threads = oracle.max_threads()
+    # the same sample as cpu_baseline on every run (n fixed); a long --steps /
+    # --warmup request is bounded by capping the number of CPU steps instead
+    # (~9 s each at n = 8192 on 16 host threads), so the arm ends in ~1 min
     n_sample = CPU_SAMPLE_N[cfg.op]
-    if cfg.op == "closure" and args.steps + args.warmup > 16:
-        n_sample = 4096   # keep a long --steps/--warmup run within a few minutes (0.3 s per step)
+    steps, warmup = max(1, min(args.steps, REF_MAX_STEPS)), min(args.warmup, REF_MAX_WARMUP)
 
     def step():
         if cfg.op == "closure":
@@ -226,19 +338,21 @@ def run_reference(args, world, rank):
             oracle.bool_close(oracle.pack_bits(inputs[0]), threads)
         return time.perf_counter() - t0
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
-    secs = [step() for _ in range(args.steps)]
+    secs = [step() for _ in range(steps)]
     total = sum(secs)
-    value = n_sample ** 3 * args.steps / total
+    value = n_sample ** 3 * steps / total
     sample = (f"{cfg.name} at n={n_sample} (same generator and seed), one "
               f"{'closure' if 'closure' in cfg.op else 'product'} per step")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "steps": steps, "warmup": warmup, "steps_requested": args.steps, "warmup_requested": args.warmup,
+        "ms_per_step": total / steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u16" if cfg.width == 16 else f"u{cfg.width}", "data": "synthetic (seeded generator)",
-        "config": {"workload": cfg.name, "n": n_sample, "full_n": cfg.n},
+        "config": {"workload": cfg.name, "n": n_sample, "full_n": cfg.n,
+                   "sample": "the cpu_baseline sample of the GPU arm (same n, generator and seed)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -266,7 +380,15 @@ def run_ours(args, world, rank, local_rank):
     dev = torch.device("cuda", local_rank)
     if world > 1:
         if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
+            # communicator setup lines (rank, nranks, transport) in the log
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            # NCCL's internal stream at the highest priority: the pivot-panel
+            # broadcast is on the critical path of the next round and must not
+            # queue behind the bulk GEMM's CTAs (sharded.py, _bcast)
+            opts = dist.ProcessGroupNCCL.Options()
+            opts.is_high_priority_stream = True
+            dist.init_process_group("nccl", device_id=dev, pg_options=opts)
         else:
             dist.init_process_group(backend)
     cfg = workloads.CONFIGS[args.workload]
@@ -279,18 +401,18 @@ def run_ours(args, world, rank, local_rank):
         torch.cuda.synchronize()
 
     # ---- inputs (host generation, then HBM) --------------------------------
-    if world > 1:
-        block = sharded.CudaFwOps.block_for(n, world, cfg.width)
+    if world > 1:   # the sharded closure's block (smx_fw_sharded_block)
+        block = lib.smx_fw_sharded_block(n, world, cfg.width // 8)
     else:   # the single-GPU closure's own choice (smx_fw_block_for)
         block = lib.smx_fw_block_for(n, cfg.width // 8)
     if cfg.op == "closure":
-        ops = sharded.CudaFwOps(cfg.width, anti=True, block=block)
-        block = ops.block if world > 1 else block
         r0, r1 = sharded.row_range(n, world, rank, block) if world > 1 else (0, n)
         (host,) = workloads.make_inputs(cfg, n, rows=(r0, r1))
         src = torch.from_numpy(host).to(dev)
         work = torch.empty_like(src)
-        fw = sharded.ShardedFW(n=n, rank=rank, world=world, ops=ops)
+        # the C-ABI sharded closure (csrc/sharded.cu): NCCL broadcast on the
+        # library's high-priority side stream, or a gloo callback
+        fw = sharded.NativeShardedFW(n, rank, world, cfg.width, anti=True, block=block)
         ws_bytes = lib.smx_fw_workspace_bytes(n, src.shape[1], cfg.width // 8)
         ws = _native.workspace(ws_bytes, dev)
 
@@ -325,11 +447,12 @@ def run_ours(args, world, rank, local_rank):
     # first timed step (FW), or around each product (mul), on its own stream
     rounds = -(-n // block)
     step_events = []
-    if cfg.op == "closure" and world == 1:
+    if cfg.op == "closure":
+        # phase-3 (3b at N > 1) launches of the first timed step, CUDA-event timed
         _native.check(lib.smx_fw_trace_arm(rounds), "trace arm")
     with ClockSampler(local_rank) as clocks:
         s.record()
-        for _ in range(args.steps):
+        for i in range(args.steps):
             if cfg.op == "mul":
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record()
@@ -340,6 +463,8 @@ def run_ours(args, world, rank, local_rank):
                 step()
         e.record()
         barrier()
+    if cfg.op == "closure" and world > 1:
+        sharded_trace = read_fw_trace(lib, rounds)
     launches = lib.smx_launch_count() - launches0
     secs = s.elapsed_time(e) / 1e3
     t = torch.tensor([secs], dtype=torch.float64, device=dev)
@@ -391,19 +516,11 @@ def run_ours(args, world, rank, local_rank):
         result["e2e"] = {"value": units_per_step / e2e_secs, "unit": UNIT,
                          "h2d_bytes_per_step": int(hb[0].item()), "d2h_bytes_per_step": int(hb[1].item()),
                          "ms_per_step": e2e_secs * 1e3, "note": "summed over ranks; max time over ranks"}
-        if args.check and cfg.op == "closure":
-            # the gathered sharded result against the single-GPU closure of the
-            # same input (bit-exact; the single-GPU path is oracle-checked)
-            torch.cuda.synchronize()
-            full = sharded.gather_rows(work, n, world, block)
-            if rank == 0:
-                (ref_host,) = workloads.make_inputs(cfg, n)
-                ref = torch.from_numpy(ref_host).to(dev)
-                rws = _native.workspace(lib.smx_fw_workspace_bytes(n, ref.shape[1], cfg.width // 8), dev)
-                _native.check(getattr(lib, f"smx_fw_u{cfg.width}")(
-                    ref.data_ptr(), n, ref.shape[1], _native.SMX_ANTI, rws.data_ptr(), rws.numel(),
-                    _native.stream_ptr(dev)), "fw")
-                result["parity_sharded"] = {"n": n, "bit_exact_vs_single_gpu": bool(torch.equal(full, ref))}
+        if cfg.op == "closure":
+            result["roofline"] = sharded_roofline(sharded_trace, secs / args.steps, n, block, world, dev)
+            digest = full_size_digest(cfg.name, n)
+            if args.check or (digest is not None and backend == "nccl"):
+                result["parity_sharded"] = sharded_parity(work, cfg, n, world, rank, block, dev, digest)
 
     # ---- parity of this very run at the oracle size (rank 0, N = 1) ------------
     if rank == 0 and world == 1:
@@ -508,26 +625,13 @@ def run_ours(args, world, rank, local_rank):
                          "ms_per_step": e2e_secs * 1e3}
         # CPU baseline + parity at the oracle size (same generator)
         if not args.no_cpu:
-            import oracle
-            oracle.build()
-            thr = oracle.max_threads()
-            n_s = CPU_SAMPLE_N[cfg.op]
-            if cfg.op == "closure":
-                cps, cdt, cpu_out, t_in = cpu_fw_sample(n_s, thr)
-                gpu_out = AntidistMatrix(n_s, n_s, 16, t_in).transitive_closure().data
-            else:
-                cps, cdt, cpu_out = cpu_mul_sample(cfg, n_s, thr)
-                ai, bi = workloads.make_inputs(cfg, n_s)
-                gpu_out = (AntidistMatrix(n_s, n_s, cfg.width, ai) *
-                           AntidistMatrix(n_s, n_s, cfg.width, bi)).data
-            result["cpu_baseline"] = {
-                "value": cps, "unit": UNIT, "cores": thr, "kind": "port",
-                "sample": f"{cfg.name} generator at n={n_s}, one "
-                          f"{'closure' if cfg.op == 'closure' else 'product'} "
-                          f"({cdt:.2f} s), C restatement of the reference engine, OpenMP rows"}
-            result["parity"] = {"n": n_s, "bit_exact_vs_oracle": bool(np.array_equal(gpu_out, cpu_out))}
+            result.update(cpu_baseline_and_parity(cfg))
         if not args.no_secondary:
             result["secondary"] = secondary(dev)
+
+    if rank == 0 and world > 1 and not args.no_cpu and backend == "nccl":
+        # the same bounded CPU sample at N > 1 (after the timed region; rank 0)
+        result.update(cpu_baseline_and_parity(cfg))
 
     if rank == 0:
         line = {
@@ -619,9 +723,28 @@ def secondary(dev):
     return out
 
 
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` (N > 1) started as a plain process: re-run this
+    command as N ranks under torch.distributed.run (127.0.0.1, a free port),
+    the layout the driver uses; rank 0 prints the line."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args)
     world, rank, local = dist_env()
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args, world, rank)
     return run_ours(args, world, rank, local)

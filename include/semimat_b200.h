@@ -39,7 +39,8 @@ enum {
     SMX_E_ARG = -1,      /* bad size / kind / flag */
     SMX_E_ALIGN = -2,    /* pointer or leading dimension not 16-byte aligned */
     SMX_E_WORKSPACE = -3,/* workspace missing or too small */
-    SMX_E_DRIVER = -4    /* driver entry point (TMA descriptor encode) unavailable */
+    SMX_E_DRIVER = -4,   /* driver entry point (TMA descriptor encode) unavailable */
+    SMX_E_COMM = -5      /* the exchange (broadcast callback / NCCL) failed or is unavailable */
 };
 enum { SMX_ANTI = 0, SMX_DIST = 1 };
 
@@ -183,6 +184,36 @@ int smx_semiring_gemm_skip_certified(const void* A, const void* B, void* C, int 
                                      int lda, int ldb, int ldc, int elem_bytes, int kind,
                                      int skip_row0, int skip_rows, void* stream);
 
+/* ---- row-panel-sharded Floyd-Warshall, one call per rank
+ * Rank `rank` of `world` holds rows [row0, row0 + rows) of the n x n matrix
+ * (row stride ld) at T, where row0 = rank * per, per = ceil(n / world)
+ * rounded up to whole `block`s (smx_fw_sharded_block).  Closes its rows in
+ * place: per pivot block the owner closes the pivot tile and updates its row
+ * panel, the panel (block x ld lanes) is broadcast with `bcast`, and every
+ * rank folds it into its rows; pipelined so the owner's chain and the
+ * broadcast of block r+1 run on a high-priority side stream beside round r.
+ * The gathered panels equal smx_fw_*'s closure bit for bit.  Replaces the
+ * reference's _close_vector / _minplus_close_vector (antidist.py:390-398,
+ * :440-448) for a matrix spread over GPUs.
+ *
+ * bcast(buf, bytes, root, ctx, stream): broadcast `bytes` at device pointer
+ * buf from rank `root` to every rank, ordered on `stream` (enqueue or
+ * complete before returning); return 0 on success.  smx_nccl_broadcast is
+ * one (ctx = an ncclComm_t); any other transport can be plugged in.
+ * Workspace: smx_fw_sharded_workspace_bytes(rows, ld, elem_bytes, block). */
+typedef int (*smx_bcast_fn)(void* buf, size_t bytes, int root, void* ctx, void* stream);
+int smx_nccl_broadcast(void* buf, size_t bytes, int root, void* nccl_comm, void* stream);
+int smx_fw_sharded_block(int n, int world, int elem_bytes);
+size_t smx_fw_sharded_workspace_bytes(int rows, int ld, int elem_bytes, int block);
+int smx_fw_sharded(void* T, int n, int row0, int rows, int ld, int elem_bytes, int kind, int rank,
+                   int world, int block, smx_bcast_fn bcast, void* ctx, void* workspace,
+                   size_t ws_bytes, void* stream);
+/* The survey's entry point: u16, NCCL.  Rank, world size and block come from
+ * the communicator (ncclComm_t passed as void*; NCCL is loaded at run time,
+ * the process's copy if one is loaded, e.g. torch's). */
+int smx_fw_sharded_u16(uint16_t* Tpanel, int n, int row0, int rows, int ld, int kind, void* nccl_comm,
+                       void* workspace, size_t ws_bytes, void* stream);
+
 /* ---- Boolean products and Warshall closure ------------------------------
  * Replace BoolMatrix.__mul__ (pkg/src/semimat/boolmat.py:151-172) and
  * BoolMatrix.transitive_closure (:174-189).
@@ -195,12 +226,14 @@ int smx_semiring_gemm_skip_certified(const void* A, const void* B, void* C, int 
 int smx_bool_gemm_i8(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* C_bits,
                      int M, int N, int K, int lda, int ldbt, int ldc, int accumulate,
                      void* stream);
-/* Kernel choice for packed-bit products of at most one wave of 128 x 64
- * tiles (e.g. C1, 1024^3): 0 = automatic (K >= 1024: K split over a 4-CTA
- * cluster on 128 x 256 tiles, partial bits OR-merged over DSMEM), 1 = the
- * plain one-CTA-per-tile kernel, 2 = split 2 x (128 x 128), 3 = split
- * 4 x (128 x 256).  Results are identical.  Returns the previous setting. */
-int smx_set_tc_variant(int variant);
+/* Output tile width (N) of the tensor-core Boolean GEMM: 0 = automatic (the
+ * widest of 256 / 128 / 64 that still gives every SM a tile), or force 64,
+ * 128 or 256.  Results are identical.  Returns the previous setting. */
+int smx_set_tc_tile_n(int bn);
+/* Development trace of the plain tensor-core kernel: buf (device, >= 16 + 2 *
+ * CTAs u64) receives clock64 phase stamps of CTA 0 in [0, 7) and globaltimer
+ * entry/exit of every CTA from [16]; NULL disarms. */
+int smx_tc_trace_arm(unsigned long long* buf);
 /* BoolMatrix.__mul__ on packed bit rows in one call (unpack A, fused
  * bits -> B^T bytes, tcgen05 product with the packed-bit epilogue).  C rows
  * are fully written, padding words zeroed.  Workspace: see

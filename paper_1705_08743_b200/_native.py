@@ -72,13 +72,22 @@ _SIGS.update({
     "smx_bool_warshall_i8": ([c_void_p, c_int, c_int, c_void_p, c_size_t, c_void_p], c_int),
 })
 _SIGS.update({
-    "smx_set_tc_variant": ([c_int], c_int),
+    "smx_set_tc_tile_n": ([c_int], c_int),
+    "smx_tc_trace_arm": ([c_void_p], c_int),
     "smx_lane_op": ([c_void_p] * 3 + [c_longlong, c_int, c_int, c_void_p], c_int),
     "smx_lanes_from_bits": ([c_void_p, c_int, c_void_p] + [c_int] * 4 + [c_void_p], c_int),
     "smx_lanes_to_bits": ([c_void_p, c_int, c_void_p] + [c_int] * 4 + [c_void_p], c_int),
     "smx_bool_mul_batched": ([c_void_p] * 3 + [c_int] * 7 + [c_longlong] * 3 + [c_void_p], c_int),
     "smx_bool_warshall_batched": ([c_void_p, c_int, c_int, c_int, c_longlong, c_void_p], c_int),
     "smx_fw_batched": ([c_void_p, c_int, c_int, c_int, c_longlong, c_int, c_int, c_void_p], c_int),
+})
+BCAST_FN = ctypes.CFUNCTYPE(c_int, c_void_p, c_size_t, c_int, c_void_p, c_void_p)
+_SIGS.update({
+    "smx_nccl_broadcast": ([c_void_p, c_size_t, c_int, c_void_p, c_void_p], c_int),
+    "smx_fw_sharded_block": ([c_int, c_int, c_int], c_int),
+    "smx_fw_sharded_workspace_bytes": ([c_int, c_int, c_int, c_int], c_size_t),
+    "smx_fw_sharded": ([c_void_p] + [c_int] * 9 + [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p], c_int),
+    "smx_fw_sharded_u16": ([c_void_p] + [c_int] * 5 + [c_void_p, c_void_p, c_size_t, c_void_p], c_int),
 })
 _OPTIONAL: dict = {}
 

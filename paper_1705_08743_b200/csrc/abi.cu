@@ -209,6 +209,7 @@ const char* smx_error_string(int code) {
         case SMX_E_ALIGN: return "pointer or leading dimension not 16-byte aligned";
         case SMX_E_WORKSPACE: return "workspace missing or too small";
         case SMX_E_DRIVER: return "CUDA driver entry point unavailable";
+        case SMX_E_COMM: return "collective (broadcast callback or NCCL) failed or unavailable";
         default: return code > 0 ? cudaGetErrorString((cudaError_t)code) : "unknown error";
     }
 }

@@ -123,7 +123,16 @@ struct TcArgs {
     int accumulate;
     int skip_tile0, skip_tiles;
     int splits;          // split-K factor (gridDim.z); > 1 ORs into a pre-set output
+    // development trace (smx_tc_trace_arm; nullptr otherwise): per CTA,
+    // globaltimer at entry and exit, and for CTA 0 clock64 at each phase
+    unsigned long long* trace;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 template <int BN>
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -142,6 +151,10 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const bool tr0 = p.trace && cta == 0;
+    if (p.trace && threadIdx.x == 0) p.trace[16 + 2 * cta] = gtimer();
+    if (tr0 && threadIdx.x == 0) p.trace[0] = clock64();
     int mt = blockIdx.y;
     if (mt >= p.skip_tile0) mt += p.skip_tiles;
     const int m0 = mt * kTcBM, n0 = blockIdx.x * BN;
@@ -174,6 +187,7 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    if (tr0 && threadIdx.x == 0) p.trace[1] = clock64();
 
     if (threadIdx.x == 0) {
         // ---- TMA producer ----
@@ -189,6 +203,7 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             tma_load_2d(&mapA, &full[s], sA + s * A_BYTES, (kb_lo + kb) * kTcBK, m0);
             tma_load_2d(&mapB, &full[s], sB + s * B_BYTES, (kb_lo + kb) * kTcBK, n0);
         }
+        if (tr0) p.trace[2] = clock64();
     } else if (threadIdx.x == 32) {
         // ---- MMA issuer ----
         constexpr uint32_t idesc = idesc_i8<BN>();
@@ -196,6 +211,7 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             const int s = kb % kTcStages;
             const uint32_t ph = (kb / kTcStages) & 1;
             mbar_wait(&full[s], ph);
+            if (tr0 && (kb == 0 || kb == nkb - 1)) p.trace[kb == 0 ? 3 : 4] = clock64();
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
 #pragma unroll
@@ -211,6 +227,7 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     // ---- epilogue: TMEM -> threshold -> bytes or bits ----
     mbar_wait(accum, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tr0 && threadIdx.x == 0) p.trace[5] = clock64();
     const int row = m0 + warp * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
 #pragma unroll 1
@@ -267,134 +284,12 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (tr0 && threadIdx.x == 0) p.trace[6] = clock64();
+    if (p.trace && threadIdx.x == 0) p.trace[17 + 2 * cta] = gtimer();
     if (warp == 2) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN)
                      : "memory");
     }
-}
-
-// ---- split-K across a thread-block cluster (small products, packed bits) -------
-//
-// C1 (1024^3) has 128 output tiles of 128 x 64: one per SM, each streaming
-// 192 KB of operands through TMA for only 8 k-blocks -- the product is bound
-// by L2 -> SM operand traffic (24 MB in all) and pipeline fill, not by the
-// tensor cores.  Here a cluster of KS CTAs shares one wider output tile
-// (128 x BN) and splits K: each CTA streams (128 + BN) x K/KS bytes, so the
-// total operand traffic drops to M*K*(N/BN) + N*K*(M/128) (BN = 256, KS = 4:
-// 12 MB) and each SM ingests half as much.  Every CTA thresholds its partial
-// counts to bits (a partial count > 0 already proves the output bit: OR is
-// idempotent, so the merge is exact) and parks its 128 x BN/32 words in its
-// own shared memory; after a cluster barrier CTA r ORs the KS partners'
-// words of rows [r*128/KS, (r+1)*128/KS) over DSMEM and stores them.  No
-// output memset, no global atomics.
-template <int BN, int KS>
-__global__ void __launch_bounds__(kTcThreads, 1)
-bool_i8_gemm_splitk_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                           const TcArgs p) {
-    constexpr uint32_t A_BYTES = kTcBM * kTcBK;
-    constexpr uint32_t B_BYTES = BN * kTcBK;
-    constexpr int WPR = BN / 32;                  // output words per row of the tile
-    extern __shared__ __align__(1024) uint8_t smem_dyn[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-    const int nkb_all = (p.K + kTcBK - 1) / kTcBK;
-    const int per = (nkb_all + KS - 1) / KS;      // k-blocks per CTA (stages = per, host-checked)
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + per * A_BYTES;
-    uint32_t* sbits = reinterpret_cast<uint32_t*>(sB + per * B_BYTES);     // [128][WPR]
-    uint64_t* full = reinterpret_cast<uint64_t*>(sbits + kTcBM * WPR);
-    uint64_t* accum = full + per;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
-
-    uint32_t rank;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.y * kTcBM, n0 = blockIdx.x * BN;
-    const int kb_lo = (int)rank * per;
-    const int kb_hi = min(nkb_all, kb_lo + per);
-    const int nkb = kb_hi > kb_lo ? kb_hi - kb_lo : 0;
-
-    if (threadIdx.x == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
-        for (int s = 0; s < per; ++s) mbar_init(&full[s], 1);
-        mbar_init(accum, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(tmem_slot)), "n"(BN) : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = *tmem_slot;
-
-    if (threadIdx.x == 0) {
-        // every k-block has its own stage: issue all loads up front
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        for (int kb = 0; kb < nkb; ++kb) {
-            mbar_expect_tx(&full[kb], A_BYTES + B_BYTES);
-            tma_load_2d(&mapA, &full[kb], sA + kb * A_BYTES, (kb_lo + kb) * kTcBK, m0);
-            tma_load_2d(&mapB, &full[kb], sB + kb * B_BYTES, (kb_lo + kb) * kTcBK, n0);
-        }
-    } else if (threadIdx.x == 32) {
-        constexpr uint32_t idesc = idesc_i8<BN>();
-        for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait(&full[kb], 0);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t a0 = smem_u32(sA + kb * A_BYTES), b0 = smem_u32(sB + kb * B_BYTES);
-#pragma unroll
-            for (int k = 0; k < kTcBK / 32; ++k)
-                umma_i8(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
-                        (kb | k) != 0);
-        }
-        umma_commit(accum);
-    }
-    __syncwarp();
-
-    // partial counts -> bits in this CTA's shared memory
-    mbar_wait(accum, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int trow_i = warp * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-#pragma unroll 1
-    for (int c = 0; c < WPR; ++c) {
-        uint32_t r[32];
-        tmem_ld32(trow + c * 32, r);
-        uint32_t word = 0;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) word |= (r[j] != 0u ? 1u : 0u) << j;
-        sbits[trow_i * WPR + c] = nkb ? word : 0u;
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    // make every CTA's words visible cluster-wide
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    if (warp == 2)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN) : "memory");
-    // CTA `rank` merges and stores rows [rank*R, (rank+1)*R) of the tile
-    constexpr int R = kTcBM / KS;
-    const uint32_t local = smem_u32(sbits);
-    for (int x = threadIdx.x; x < R * WPR; x += kTcThreads) {
-        const int rr = (int)rank * R + x / WPR, c = x % WPR;
-        const uint32_t off = (uint32_t)(rr * WPR + c) * 4u;
-        uint32_t v = 0;
-#pragma unroll
-        for (int q = 0; q < KS; ++q) {
-            uint32_t remote, w;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + off), "r"(q));
-            asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(w) : "r"(remote) : "memory");
-            v |= w;
-        }
-        const int row = m0 + rr, col0 = n0 + c * 32;
-        if (row < p.M && col0 < p.N) {
-            if (p.N - col0 < 32) v &= (1u << (p.N - col0)) - 1u;
-            uint32_t* dst = p.Cbits + (long long)row * p.ldc + (col0 >> 5);
-            *dst = p.accumulate ? (*dst | v) : v;
-        }
-    }
-    // partners may still be reading this CTA's words
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // ---- host side ---------------------------------------------------------------
@@ -485,50 +380,11 @@ static int launch_tc(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long 
 }
 
 
-// Split-K cluster variant (packed-bit output only).  Returns SMX_E_ARG when
-// the shape does not fit it (the caller then uses the plain kernel).
-template <int BN, int KS>
-static int launch_tc_splitk(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long long lda, long long ldbt,
-                            cudaStream_t s, bool pdl) {
-    const int nkb = ceil_div(a.K, kTcBK);
-    const int per = ceil_div(nkb, KS);
-    constexpr size_t fixed = 1024 + (size_t)kTcBM * (BN / 32) * 4 + 16 + 8;
-    const size_t smem = fixed + (size_t)per * (kTcBM + BN) * kTcBK + 8 * (per + 1);
-    if (smem > 227 * 1024 || a.Cbits == nullptr || a.skip_tiles) return SMX_E_ARG;
-    CUtensorMap mA, mB;
-    SMX_TRY(make_map(&mA, A, a.M, a.K, lda, kTcBM));
-    SMX_TRY(make_map(&mB, Bt, a.N, a.K, ldbt, BN));
-    auto kern = bool_i8_gemm_splitk_kernel<BN, KS>;
-    SMX_TRY(set_max_smem((const void*)kern, smem));
-    cudaError_t e;
-    TcArgs args = a;
-    args.splits = 1;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ceil_div(a.N, BN), ceil_div(a.M, kTcBM), KS);
-    cfg.blockDim = dim3(kTcThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = KS;
-    int na = 1;
-    if (pdl) {
-        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
-    cfg.attrs = attr;
-    cfg.numAttrs = na;
-    count_launch();
-    e = cudaLaunchKernelEx(&cfg, kern, mA, mB, args);
-    return e == cudaSuccess ? SMX_OK : (int)e;
-}
-
-// 0 = automatic, 1 = always the plain kernel, 2 = split-K 128 x 128 x 2,
-// 3 = split-K 128 x 256 x 4 (tuning switch; results are identical)
-static int g_tc_variant = 0;
+// Output tile width of smx_bool_gemm_i8: 0 = automatic (the widest tile that
+// still gives every SM a tile), or force 64 / 128 / 256 (tuning switch;
+// results are identical).
+static int g_tc_tile_n = 0;
+static unsigned long long* g_tc_trace = nullptr;
 
 int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbits, int M, int N, int K,
                  long long lda, long long ldbt, long long ldc, int accumulate, int skip_row0, int skip_rows,
@@ -538,7 +394,7 @@ int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbit
     if (!aligned16(A) || !aligned16(Bt) || (lda & 15) || (ldbt & 15)) return SMX_E_ALIGN;
     if (lda < K || ldbt < K) return SMX_E_ARG;
     if (Cbits ? ((long long)ldc * 32 < N) : (ldc < N)) return SMX_E_ARG;
-    TcArgs a{C, Cbits, M, N, K, ldc, accumulate != 0, 0, 0, 1};
+    TcArgs a{C, Cbits, M, N, K, ldc, accumulate != 0, 0, 0, 1, g_tc_trace};
     if (skip_rows > 0) {
         if (skip_row0 % kTcBM) return SMX_E_ARG;
         a.skip_tile0 = skip_row0 / kTcBM;
@@ -546,18 +402,9 @@ int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbit
         const int total = ceil_div(M, kTcBM);
         if (a.skip_tile0 + a.skip_tiles > total) a.skip_tiles = total - a.skip_tile0;
     }
-    // small packed-bit products: split K across a cluster (see the kernel)
-    if (Cbits && skip_rows == 0) {
-        int v = g_tc_variant;
-        if (v == 0) {
-            // automatic: one wave of plain 128 x 64 tiles or fewer, K deep
-            // enough for 4 slices of >= 2 k-blocks
-            const long long tiles64 = (long long)ceil_div(M, kTcBM) * ceil_div(N, 64);
-            if (tiles64 <= 148 && K >= 8 * kTcBK) v = 3;
-        }
-        if (v == 2 && launch_tc_splitk<128, 2>(A, Bt, a, lda, ldbt, s, pdl) == SMX_OK) return SMX_OK;
-        if (v == 3 && launch_tc_splitk<256, 4>(A, Bt, a, lda, ldbt, s, pdl) == SMX_OK) return SMX_OK;
-    }
+    if (g_tc_tile_n == 64) return launch_tc<64>(A, Bt, a, lda, ldbt, s, pdl);
+    if (g_tc_tile_n == 128) return launch_tc<128>(A, Bt, a, lda, ldbt, s, pdl);
+    if (g_tc_tile_n == 256) return launch_tc<256>(A, Bt, a, lda, ldbt, s, pdl);
     // widest tile that still gives every SM a tile
     const long long rows = ceil_div(M, kTcBM) - a.skip_tiles;
     if (rows * ceil_div(N, 256) >= 148) return launch_tc<256>(A, Bt, a, lda, ldbt, s, pdl);
@@ -742,10 +589,17 @@ int smx_bool_mul_tc(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, in
     return bool_mul_tc(A, B, C, M, N, K, lda_w, ldb_w, ldc_w, ws, ws_bytes, as_stream(stream));
 }
 
-int smx_set_tc_variant(int v) {
-    if (v < 0 || v > 3) return SMX_E_ARG;
-    const int old = g_tc_variant;
-    g_tc_variant = v;
+// development: trace buffer (device, >= 16 + 2 * CTAs u64) for the next
+// plain-kernel products; nullptr disarms
+int smx_tc_trace_arm(unsigned long long* buf) {
+    g_tc_trace = buf;
+    return SMX_OK;
+}
+
+int smx_set_tc_tile_n(int bn) {
+    if (bn != 0 && bn != 64 && bn != 128 && bn != 256) return SMX_E_ARG;
+    const int old = g_tc_tile_n;
+    g_tc_tile_n = bn;
     return old;
 }
 

@@ -21,6 +21,10 @@ void count_launch();
 // that drives several GPUs, or calls from several threads, never launches a
 // kernel whose > 48 KB opt-in was set on another device only.
 int set_max_smem(const void* func, size_t bytes);
+// smx_fw_trace_arm measurement hook (fw.cu): CUDA events around a dominant-
+// kernel launch on `s` with its cell-update count; no-ops unless armed.
+void trace_begin(cudaStream_t s, long long cells);
+void trace_end(cudaStream_t s);
 
 // Per-device highest-priority side stream with fork/join events, used by the
 // look-ahead closure schedules (created once, reused; see abi.cu).

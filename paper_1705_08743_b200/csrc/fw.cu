@@ -529,12 +529,12 @@ struct FwTrace {
 };
 static FwTrace g_trace;
 
-static void trace_begin(cudaStream_t s, long long cells) {
+void trace_begin(cudaStream_t s, long long cells) {
     if (!g_trace.armed || g_trace.count >= g_trace.cap) return;
     g_trace.cells[g_trace.count] = cells;
     cudaEventRecord(g_trace.ev[2 * g_trace.count], s);
 }
-static void trace_end(cudaStream_t s) {
+void trace_end(cudaStream_t s) {
     if (!g_trace.armed || g_trace.count >= g_trace.cap) return;
     cudaEventRecord(g_trace.ev[2 * g_trace.count + 1], s);
     ++g_trace.count;

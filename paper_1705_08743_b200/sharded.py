@@ -129,6 +129,10 @@ class ShardedFW:
     ops: object
     group: object = None
     lookahead: bool = True
+    # measurement hook (bench.py's per-rank roofline): when a list, every bulk
+    # row update (phase 3b) of the pipelined schedule appends (start event,
+    # end event, cell-updates), the events recorded on the main stream
+    trace: list | None = None
 
     def __post_init__(self):
         self.block = self.ops.block
@@ -167,6 +171,10 @@ class ShardedFW:
         self.ops.rest_update(local, panel, k0, self._bb(k0), self.n, skip)
 
     def _bcast(self, panel: torch.Tensor, k0: int) -> None:
+        # NCCL runs this on its own internal stream, ordered after the current
+        # (side) stream; create the process group with
+        # ProcessGroupNCCL.Options(is_high_priority_stream=True) (bench.py
+        # does) so the panel is not queued behind the bulk GEMM's CTAs
         if self.world > 1:
             dist.broadcast(panel.view(torch.uint8), src=self.owner(k0), group=self.group)
 
@@ -233,8 +241,15 @@ class ShardedFW:
                     self._owner_work(local, r + 1)
                     self._bcast(self._panel(local, r + 1), k1)
                     join = side.record_event() if side is not None else None
+                traced = self.trace is not None and main is not None
+                if traced:
+                    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    ev0.record(main)
                 ops.update_rows(local, cp, panel, bb, n, 0, rows,
                                 (skip_lo, skip_n) if skip_n else None)   # 3b
+                if traced:
+                    ev1.record(main)
+                    self.trace.append((ev0, ev1, (rows - skip_n) * n * bb))
                 if main is not None:
                     main.wait_event(join)
             else:
@@ -260,3 +275,94 @@ def gather_rows(local: torch.Tensor, n: int, world: int, block: int, group=None)
     parts = [torch.empty_like(padded) for _ in range(world)]
     dist.all_gather([p.view(torch.uint8) for p in parts], padded.view(torch.uint8), group=group)
     return torch.cat(parts)[:n]
+
+
+class NativeShardedFW:
+    """The same pipelined row-panel closure as one C-ABI call per rank
+    (smx_fw_sharded, csrc/sharded.cu): the orchestration runs in C++ and the
+    broadcast is enqueued on the library's high-priority side stream.
+
+    transport "nccl": smx_nccl_broadcast on the NCCL communicator of the
+    default process group (torch's ProcessGroupNCCL, ``_comm_ptr``).
+    transport "callback": a Python broadcast over torch.distributed (gloo in
+    the tests); the side stream is synchronised before each broadcast, so no
+    kernel ever waits on another rank.
+    """
+
+    def __init__(self, n: int, rank: int, world: int, width: int = 16, anti: bool = True,
+                 block: int | None = None, group=None, transport: str | None = None, bcast_py=None):
+        self.n, self.rank, self.world, self.width = n, rank, world, width
+        self.eb = width // 8
+        self.kind = _native.SMX_ANTI if anti else _native.SMX_DIST
+        lib = _native.lib()
+        self.block = block or lib.smx_fw_sharded_block(n, world, self.eb)
+        self.row0, self.row1 = row_range(n, world, rank, self.block)
+        self.group = group
+        if transport is None:
+            transport = "nccl" if world > 1 and dist.get_backend(group) == "nccl" else "callback"
+        self.transport = transport
+        # transport "callback" with bcast_py(view, root, stream_ptr): a custom
+        # exchange that enqueues on the given stream (tools/emulate_rank.py)
+        self.bcast_py = bcast_py
+        self._ws = None
+        self._cb = None
+        self._local = None
+
+    def _nccl_comm(self, device) -> int:
+        pg = self.group or dist.distributed_c10d._get_default_group()
+        return pg._get_backend(device)._comm_ptr()
+
+    def _callback(self):
+        import ctypes
+
+        def bcast(buf, nbytes, root, ctx, stream):
+            try:
+                if self.bcast_py is None:
+                    # stream may be NULL (torch's legacy default stream)
+                    if stream:
+                        torch.cuda.ExternalStream(stream).synchronize()
+                    else:
+                        torch.cuda.synchronize()
+                view = None
+                for base in (self._local, self._ws):
+                    lo = base.data_ptr()
+                    if lo <= buf and buf + nbytes <= lo + base.numel() * base.element_size():
+                        flat = base.view(torch.uint8).reshape(-1)
+                        view = flat[buf - lo: buf - lo + nbytes]
+                        break
+                if view is None:
+                    return -5
+                if self.bcast_py is not None:
+                    self.bcast_py(view, root, stream)
+                    return 0
+                dist.broadcast(view, src=root, group=self.group)
+                torch.cuda.synchronize()
+                return 0
+            except Exception:   # never let an exception cross the C frame
+                import sys
+                import traceback
+                traceback.print_exc(file=sys.stderr)
+                return -5
+        self._cb = _native.BCAST_FN(bcast)
+        return ctypes.cast(self._cb, ctypes.c_void_p).value, None
+
+    def run(self, local: torch.Tensor) -> torch.Tensor:
+        import ctypes
+        lib = _native.lib()
+        rows, ld = local.shape[0], local.shape[1]
+        nbytes = lib.smx_fw_sharded_workspace_bytes(rows, ld, self.eb, self.block)
+        if self._ws is None or self._ws.numel() < nbytes or self._ws.device != local.device:
+            self._ws = _native.workspace(nbytes, local.device)
+        self._local = local
+        if self.world == 1:
+            fn, ctx = None, None
+        elif self.transport == "nccl":
+            fn = ctypes.cast(lib.smx_nccl_broadcast, ctypes.c_void_p).value
+            ctx = self._nccl_comm(local.device)
+        else:
+            fn, ctx = self._callback()
+        _native.check(lib.smx_fw_sharded(
+            local.data_ptr(), self.n, self.row0, rows, ld, self.eb, self.kind, self.rank, self.world,
+            self.block, fn, ctx, self._ws.data_ptr(), nbytes, _native.stream_ptr(local.device)),
+            "smx_fw_sharded")
+        return local

@@ -1,6 +1,6 @@
 """GPU parity for the round-2 kernels and boundary fixes.
 
-* the cluster split-K tensor-core Boolean product (every variant) against the
+* the tensor-core Boolean product at every output tile width against the
   oracle, C1 and ragged shapes;
 * the batched small-matrix kernels at their size limits against the oracle;
 * the certified update of the sharded closure (smx_semiring_gemm_skip_certified)
@@ -10,8 +10,6 @@ Every comparison is exact equality.
 """
 
 from __future__ import annotations
-
-import ctypes
 
 import numpy as np
 import pytest
@@ -40,11 +38,11 @@ def _random_lane(rng, n, width, kind, p=0.3):
     return t
 
 
-# -- tensor-core Boolean product: split-K cluster variants ----------------------
+# -- tensor-core Boolean product: every tile width --------------------------------
 
 @pytest.mark.parametrize("shape", [(1024, 1024, 1024), (1000, 777, 1001), (128, 64, 1024), (300, 1030, 2050),
                                    (1024, 1024, 4096)])
-def test_tc_variants_match_oracle(shape, oracle_lib):
+def test_tc_tile_widths_match_oracle(shape, oracle_lib):
     m, n, k = shape
     lib = _native.lib()
     rng = np.random.default_rng(m + n + k)
@@ -52,37 +50,14 @@ def test_tc_variants_match_oracle(shape, oracle_lib):
     b = (rng.random((k, n)) < 0.05).astype(np.uint8)
     want = oracle_lib.bool_mul(oracle_lib.pack_bits(a), oracle_lib.pack_bits(b), k)
     ma, mb = BoolMatrix.from_numpy(a), BoolMatrix.from_numpy(b)
-    old = lib.smx_set_tc_variant(0)
+    old = lib.smx_set_tc_tile_n(0)
     try:
-        for v in (0, 1, 2, 3):
-            lib.smx_set_tc_variant(v)
-            got = (ma * mb).blocks
-            np.testing.assert_array_equal(got, want, err_msg=f"variant {v} {shape}")
+        for bn in (0, 64, 128, 256):
+            lib.smx_set_tc_tile_n(bn)
+            np.testing.assert_array_equal((ma * mb).blocks, want, err_msg=f"tile {bn} {shape}")
     finally:
-        lib.smx_set_tc_variant(old)
-
-
-def test_tc_split_variant_accumulates_into_bits(oracle_lib):
-    """smx_bool_gemm_i8 with packed-bit output and accumulate = 1 on the split
-    cluster kernel: C |= A . B, padding words untouched."""
-    lib = _native.lib()
-    rng = np.random.default_rng(5)
-    m = n = k = 1024
-    a = (rng.random((m, k)) < 0.02).astype(np.uint8)
-    bt = (rng.random((n, k)) < 0.02).astype(np.uint8)
-    c0 = (rng.random((m, n)) < 0.1).astype(np.uint8)
-    want = oracle_lib.bool_mul(oracle_lib.pack_bits(a), oracle_lib.pack_bits(bt.T.copy()), k) | \
-        oracle_lib.pack_bits(c0)
-    cw = torch.from_numpy(oracle_lib.pack_bits(c0).view(np.int32).copy()).cuda()
-    ta, tbt = torch.from_numpy(a).cuda(), torch.from_numpy(bt).cuda()
-    old = lib.smx_set_tc_variant(3)
-    try:
-        rc = lib.smx_bool_gemm_i8(ta.data_ptr(), tbt.data_ptr(), None, cw.data_ptr(), m, n, k, k, k,
-                                  cw.shape[1], 1, _native.stream_ptr())
-        assert rc == 0
-    finally:
-        lib.smx_set_tc_variant(old)
-    np.testing.assert_array_equal(cw.cpu().numpy().view(np.uint64), want)
+        lib.smx_set_tc_tile_n(old)
+    assert lib.smx_set_tc_tile_n(100) < 0
 
 
 # -- batched kernels at their limits ----------------------------------------------

@@ -3,7 +3,8 @@
 Back-to-back launches timed with CUDA events on the launching stream:
   null      torch.cuda._sleep(0): the launch floor of any kernel here
   int_mm    torch._int_mm (cuBLAS int8) at 1024^3: the library baseline
-  tc        smx_bool_gemm_i8 (our tcgen05 kernel, bytes in, bits out)
+  tc        smx_bool_gemm_i8 (our tcgen05 kernel, bytes in, bits out), per
+            output tile width (bn0 = automatic)
   tc_graph  the same, 20 launches per CUDA graph replay
   public    BoolMatrix.__mul__ (unpack + PDL kernel, graph replay)
 Prints one JSON object.
@@ -49,6 +50,8 @@ def main():
     dev = torch.device("cuda")
     res = {"n": n}
     res["null_us"] = timeit(lambda: torch.cuda._sleep(0))
+    f, per = graphed(lambda: torch.cuda._sleep(0))
+    res["null_graph_us"] = timeit(f, 50, 5) / per
     a8 = torch.randint(-127, 127, (n, n), dtype=torch.int8, device=dev)
     b8 = torch.randint(-127, 127, (n, n), dtype=torch.int8, device=dev)
     res["int_mm_us"] = timeit(lambda: torch._int_mm(a8, b8.t()))
@@ -61,9 +64,14 @@ def main():
     def tc():
         _native.check(lib.smx_bool_gemm_i8(A.data_ptr(), Bt.data_ptr(), None, out.data_ptr(), n, n, n, n, n,
                                            n // 32, 0, _native.stream_ptr(dev)), "tc")
-    res["tc_us"] = timeit(tc)
-    f, per = graphed(tc)
-    res["tc_graph_us"] = timeit(f, 50, 5) / per
+    old = lib.smx_set_tc_tile_n(0)
+    for bn in (0, 64, 128, 256):
+        lib.smx_set_tc_tile_n(bn)
+        res[f"tc_bn{bn}_us"] = timeit(tc)
+        f, per = graphed(tc)
+        res[f"tc_bn{bn}_graph_us"] = timeit(f, 50, 5) / per
+    lib.smx_set_tc_tile_n(old)
+    res["tc_us"], res["tc_graph_us"] = res["tc_bn0_us"], res["tc_bn0_graph_us"]
     if n == 1024:
         a, b = workloads.make_inputs(workloads.CONFIGS["c1_bool_mul"])
         ma, mb = BoolMatrix.from_numpy(a), BoolMatrix.from_numpy(b)
