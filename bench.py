@@ -623,6 +623,21 @@ def run_ours(args, world, rank, local_rank):
         result["e2e"] = {"value": units_per_step / e2e_secs, "unit": UNIT,
                          "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                          "ms_per_step": e2e_secs * 1e3}
+        if cfg.op == "closure":
+            # the literal drop-in call with host data in and out, serial copies:
+            # AntidistMatrix(n, n, w, host).transitive_closure().data
+            # (antidist.py:263-273; .data is the host view the reference returns)
+            def dropin_step():
+                return AntidistMatrix(n, n, cfg.width, host).transitive_closure().data
+            dropin_step()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(2):
+                dropin_step()
+            d_secs = (time.perf_counter() - t0) / 2
+            result["e2e_dropin"] = {"value": units_per_step / d_secs, "unit": UNIT, "ms_per_step": d_secs * 1e3,
+                                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                                    "call": "AntidistMatrix(n, n, 16, host_ndarray).transitive_closure().data"}
         # CPU baseline + parity at the oracle size (same generator)
         if not args.no_cpu:
             result.update(cpu_baseline_and_parity(cfg))
@@ -685,6 +700,39 @@ def secondary(dev):
         engines.lane_close_(w, cfg.n, 16, True)
     t = cuda_time(fw8k, 5, 2)   # 2 warm-ups: the second records the replay graph
     out["c4_fw_u16"] = {"n": cfg.n, "seconds": t, "cells_per_s": cfg.n ** 3 / t}
+    # the same graph as a DistMatrix (min-plus closure of the complement,
+    # antidist.py:331-350) and at u32 lanes (kernels.py:35): same distances
+    peaks, _ = measure_issue_peak()
+    issue = max(peaks["one"], peaks["pair"])
+    ref8k = w.clone()
+    dsrc = (65535 - src.to(torch.int32)).to(torch.uint16)
+    wd = torch.empty_like(dsrc)
+
+    def fw8k_dist():
+        wd.copy_(dsrc)
+        engines.lane_close_(wd, cfg.n, 16, False)
+    t = cuda_time(fw8k_dist, 5, 2)
+    same = bool(torch.equal((65535 - wd.to(torch.int32)).to(torch.uint16), ref8k))
+    out["c4_fw_u16_dist"] = {"n": cfg.n, "seconds": t, "cells_per_s": cfg.n ** 3 / t,
+                             "frac_of_issue_ceiling": cfg.n ** 3 / t / (2 * issue),
+                             "complement_of_anti_closure": same}
+    s32 = src.to(torch.int64)
+    src32 = torch.where(s32 == 0, torch.zeros_like(s32), s32 + (2 ** 32 - 65536)).to(torch.uint32)
+    w32 = torch.empty_like(src32)
+
+    def fw8k_u32():
+        w32.copy_(src32)
+        engines.lane_close_(w32, cfg.n, 32, True)
+    t = cuda_time(fw8k_u32, 3, 2)
+    r32 = w32.to(torch.int64)
+    back = torch.where(r32 == 0, torch.zeros_like(r32), r32 - (2 ** 32 - 65536))
+    out["c4_fw_u32"] = {"n": cfg.n, "seconds": t, "cells_per_s": cfg.n ** 3 / t,
+                        "frac_of_issue_ceiling": cfg.n ** 3 / t / issue,
+                        "ceiling_note": "u32: 1 cell per instruction at best (VIADDMNMX on bounded tiles)",
+                        "same_distances_as_u16": bool(torch.equal(back.to(torch.int32),
+                                                                  ref8k.to(torch.int32)))}
+    out["c4_fw_u16"]["frac_of_issue_ceiling"] = out["c4_fw_u16"]["cells_per_s"] / (2 * issue)
+    del ref8k, dsrc, wd, s32, src32, w32, r32, back
     cfg = workloads.CONFIGS["c1_bool_mul"]
     a, b = workloads.make_inputs(cfg)
     ma, mb = BoolMatrix.from_numpy(a), BoolMatrix.from_numpy(b)
