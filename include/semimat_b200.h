@@ -128,6 +128,22 @@ int smx_set_fw_pivot_blocked(int enable);
  * per-k predicate kernel.  Results are identical.  Returns the previous
  * setting. */
 int smx_set_bits_m4r(int enable);
+/* Bit Warshall for 512 <= n <= 8192, n a multiple of 256: 1 = one persistent
+ * cooperative launch for the whole closure (a work queue of row panel / 3a /
+ * 3b tiles synchronised by device counters, the pivot closed by the CTA that
+ * finishes the last 3a tile); 0 (default, faster as measured) = the blocked
+ * schedule of one launch per phase.  Results are identical.  Returns the
+ * previous setting. */
+int smx_set_bool_persistent(int enable);
+/* Pivot block of the blocked bit Warshall: 0 = automatic (256, or 512 from
+ * n = 8192), or force 128 / 256 / 512.  Results are identical.  Returns the
+ * previous setting (or SMX_E_ARG). */
+int smx_set_bool_block(int block);
+/* Development trace of the persistent closure: buf (device, 4 * cap_items
+ * u64) receives per work item start / dependencies-met / end globaltimer
+ * stamps and (CTA, type, round); the last R slots hold the pivots.  NULL
+ * disarms.  Graph replay is keyed without it: use with smx_set_graphs(0). */
+int smx_bool_persist_trace_arm(unsigned long long* buf, int cap_items);
 /* Graph replay of multi-launch calls (smx_fw_*, smx_bool_warshall_bits,
  * smx_bool_warshall_i8, smx_bool_mul_tc): the first call with a given
  * (entry, pointers, sizes, switches) launches eagerly, the second records its

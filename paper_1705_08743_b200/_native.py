@@ -29,6 +29,9 @@ _SIGS = {
     "smx_set_fw_side_lite": ([c_int], c_int),
     "smx_set_fw_pivot_blocked": ([c_int], c_int),
     "smx_set_bits_m4r": ([c_int], c_int),
+    "smx_set_bool_persistent": ([c_int], c_int),
+    "smx_set_bool_block": ([c_int], c_int),
+    "smx_bool_persist_trace_arm": ([c_void_p, c_int], c_int),
     "smx_set_fw_block": ([c_int], c_int),
     "smx_set_fw_packed": ([c_int], c_int),
     "smx_fw_block_for": ([c_int, c_int], c_int),

@@ -196,26 +196,37 @@ struct M4rSmem {
 
 __device__ __forceinline__ int m4r_chunk(int c, int e, int nch) { return c ^ (e & (nch - 1) & 7); }
 
-template <typename Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_m4r_gemm_kernel(const BitsArgs p) {
+// Operand loads of the four-Russians tile.  CG = true reads through L2 only
+// (ld.global.cg): the persistent Warshall kernel reads rows that other CTAs
+// of the same launch have just OR-ed into, which a stale L1 line would miss.
+template <bool CG>
+__device__ __forceinline__ uint32_t m4r_ld(const uint32_t* p) {
+    if constexpr (CG) return __ldcg(p);
+    else return *p;
+}
+template <bool CG>
+__device__ __forceinline__ uint4 m4r_ld4(const uint32_t* p) {
+    if constexpr (CG) return __ldcg(reinterpret_cast<const uint4*>(p));
+    else return *reinterpret_cast<const uint4*>(p);
+}
+
+// One output tile (row tile mt, word tile nt) over k-words [kw_lo, kw_hi):
+// C |= A (x) B.  split: partial rows are OR-ed into C with atomics (other
+// tiles cover the rest of K); otherwise the tile's C rows are read first
+// (accumulate) and stored whole.
+template <typename Cfg, bool CG>
+__device__ __forceinline__ void m4r_tile(const BitsArgs& p, int mt, int nt, int kw_lo, int kw_hi, bool split,
+                                         uint32_t* m4r_smem) {
     constexpr int BM = Cfg::BM, BNW = Cfg::BNW, TM = Cfg::TM, TNW = Cfg::TNW, HW = Cfg::HW;
     constexpr int TCOLS = Cfg::TCOLS, THREADS = Cfg::THREADS;
     using SM = M4rSmem<Cfg>;
     constexpr int CH = SM::CH;
-    extern __shared__ __align__(16) uint32_t m4r_smem[];
     uint32_t* Tb = m4r_smem;                                  // [2][8][16][BNW]
     uint32_t* As = m4r_smem + 2 * SM::TAB_WORDS;              // [2][BM]
 
-    pdl_wait();
     const int tid = threadIdx.x;
-    int mt = blockIdx.y;
-    if (mt >= p.skip_tile0) mt += p.skip_tiles;
-    const int row0 = mt * BM, w0 = blockIdx.x * BNW;
+    const int row0 = mt * BM, w0 = nt * BNW;
     const int tc = tid % TCOLS, tr = tid / TCOLS;
-    const int nkw_all = (p.K + 31) / 32;
-    const int kw_lo = blockIdx.z * p.kw_per;
-    const int kw_hi = min(nkw_all, kw_lo + p.kw_per);
-    const bool split = p.kw_per < nkw_all;
 
     uint32_t acc[TM][TNW];
 #pragma unroll
@@ -225,7 +236,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_m4r_gemm_kernel(
         for (int j = 0; j < TNW; ++j) {
             const int gw = w0 + (j / HW) * (BNW / 2) + tc * HW + (j % HW);
             acc[i][j] = (!split && p.accumulate && grow < p.M && gw < p.Nw)
-                            ? p.C[(long long)grow * p.ldc + gw] : 0u;
+                            ? m4r_ld<CG>(p.C + (long long)grow * p.ldc + gw) : 0u;
         }
     }
 
@@ -239,7 +250,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_m4r_gemm_kernel(
             const int r = tid + q * THREADS, grow = row0 + r;
             uint32_t v = 0;
             if (r < BM && grow < p.M) {
-                v = p.A[(long long)grow * p.lda + kw];
+                v = m4r_ld<CG>(p.A + (long long)grow * p.lda + kw);
                 const int valid = p.K - k0;
                 if (valid < 32) v &= (1u << valid) - 1u;
             }
@@ -255,11 +266,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_m4r_gemm_kernel(
                 uint4 v = make_uint4(0, 0, 0, 0);
                 if (it < SM::ITEMS && gk < p.K) {
                     const uint32_t* src = p.B + (long long)gk * p.ldb + gw;
-                    if (gw + 4 <= p.Nw) v = *reinterpret_cast<const uint4*>(src);
+                    if (gw + 4 <= p.Nw) v = m4r_ld4<CG>(src);
                     else {
-                        if (gw + 0 < p.Nw) v.x = src[0];
-                        if (gw + 1 < p.Nw) v.y = src[1];
-                        if (gw + 2 < p.Nw) v.z = src[2];
+                        if (gw + 0 < p.Nw) v.x = m4r_ld<CG>(src);
+                        if (gw + 1 < p.Nw) v.y = m4r_ld<CG>(src + 1);
+                        if (gw + 2 < p.Nw) v.z = m4r_ld<CG>(src + 2);
                     }
                 }
                 b_st[q][b] = v;
@@ -343,6 +354,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_m4r_gemm_kernel(
             }
         }
     }
+}
+
+template <typename Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) bool_m4r_gemm_kernel(const BitsArgs p) {
+    extern __shared__ __align__(16) uint32_t m4r_smem[];
+    pdl_wait();
+    int mt = blockIdx.y;
+    if (mt >= p.skip_tile0) mt += p.skip_tiles;
+    const int nkw_all = (p.K + 31) / 32;
+    const int kw_lo = blockIdx.z * p.kw_per;
+    const int kw_hi = min(nkw_all, kw_lo + p.kw_per);
+    m4r_tile<Cfg, false>(p, mt, blockIdx.x, kw_lo, kw_hi, p.kw_per < nkw_all, m4r_smem);
 }
 
 // smx_set_bits_m4r: the four-Russians bit GEMM (1, default) or the per-k
@@ -444,7 +467,8 @@ __global__ void __launch_bounds__(32 * W, 1) bool_pivot_kernel(uint32_t* P, int 
 
 static int launch_bool_pivot(uint32_t* P, int b, long long ld_w, cudaStream_t s) {
     count_launch();
-    const cudaError_t e = b <= kWarshallBlock
+    const cudaError_t e = b <= 128 ? launch_kernel(bool_pivot_kernel<4>, dim3(1), dim3(128), 0, s, P, b, ld_w)
+                          : b <= kWarshallBlock
                               ? launch_kernel(bool_pivot_kernel<8>, dim3(1), dim3(256), 0, s, P, b, ld_w)
                               : launch_kernel(bool_pivot_kernel<16>, dim3(1), dim3(512), 0, s, P, b, ld_w);
     return e == cudaSuccess ? SMX_OK : (int)e;
@@ -453,7 +477,11 @@ static int launch_bool_pivot(uint32_t* P, int b, long long ld_w, cudaStream_t s)
 // Block for an n-vertex closure.  Measured (ms, 256 / 512 blocks): n = 4096
 // 0.33 / 0.46, 8192 1.79 / 1.51, 16384 10.1 / 10.1 -- halving the rounds pays
 // once each round's phase 3 is long enough to hide the 512 pivot chain.
-static int bool_block_for_n(int n) { return n >= kBoolBlock512MinN ? 512 : kWarshallBlock; }
+static int g_bool_block = 0;   // smx_set_bool_block: 0 = automatic, else 128 / 256 / 512
+static int bool_block_for_n(int n) {
+    if (g_bool_block) return g_bool_block;
+    return n >= kBoolBlock512MinN ? 512 : kWarshallBlock;
+}
 
 // Column-panel snapshot of `cols` words for all rows (one thread per word).
 __global__ void copy_words_kernel(const uint32_t* __restrict__ src, long long ld, uint32_t* __restrict__ dst,
@@ -477,10 +505,235 @@ int copy_words(const uint32_t* src, long long ld, uint32_t* dst, long long ldd, 
     return e == cudaSuccess ? SMX_OK : (int)e;
 }
 
+// ---- persistent Warshall: the whole closure in one launch (n <= 8192) ---------
+//
+// The blocked schedule above is bound by its per-round chain at n = 4096
+// (3a -> pivot -> row panel: three launches, ~15 us per round against ~4 us
+// of phase-3 work).  Here one cooperative launch keeps every CTA resident and
+// hands out work items from a global queue in schedule order; each item
+// waits on device counters for exactly what it reads, so rounds overlap and
+// no launch boundary sits on the chain:
+//   RP(r)  row panel  T[K_r, :] |= P*_r . T[K_r, :]       waits pivot r
+//   A3(r)  3a         T[K_r+1, :] |= T[K_r+1, K_r] . T[K_r, :]
+//                                                          waits RP(r), 3b(r-1)
+//   B3(r)  3b         T[X, :] |= T[X, K_r] . T[K_r, :], X = rows outside
+//                     K_r u K_r+1                          waits RP(r), 3b(r-1)
+//   pivot(r+1)        run by the CTA that completes the last A3(r) item
+// Item g only waits on items with smaller indices (or the pivot run right
+// after one of them), and all CTAs are co-resident, so the queue cannot
+// deadlock.  Every read of T goes through L2 (m4r_tile<.., true>), partial
+// products are OR-ed in with atomics where K is split, and items publish
+// with __threadfence + a counter increment.  Exactness: the same in-place
+// arguments as the blocked schedule (bits read after another item set them
+// are real paths; P* . P* = P*).  tile: 64 rows x 2048 bits, 256 threads.
+using BitsP = BitsCfg<64, 64, 2, 8, 1>;
+constexpr int kPersistBlock = 256;
+constexpr int kPersistMaxN = 8192;
+
+struct PersistArgs {
+    uint32_t* T;
+    int n, nw;
+    long long ld_w;
+    int R, ntw;          // rounds; 2048-bit word tiles per row
+    int ks_rp, ks_b;     // k-splits of the RP / A3 items and of the B3 items
+    unsigned* ctr;       // [0] queue head, [1+r] pivot r done, [1+R+r] RP, [1+2R+r] A3, [1+3R+r] B3 done
+    // development trace (smx_bool_persist_trace_arm; nullptr otherwise): per
+    // item g, 4 u64 at [4 g]: start ns, dependencies met ns, end ns,
+    // (cta << 32 | type << 16 | round); pivots in the last R slots
+    unsigned long long* trace;
+    int trace_cap;
+};
+
+__device__ __forceinline__ unsigned long long gtime_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned v) {
+    while (ld_acquire(p) < v) {
+    }
+}
+
+__device__ __forceinline__ void persist_pivot(const PersistArgs& q, int k0, void* smem) {
+    PivotSmemT<8>& sm = *reinterpret_cast<PivotSmemT<8>*>(smem);
+    const int r = threadIdx.x;
+    uint32_t w[8];
+    const uint32_t* row = q.T + (long long)(k0 + r) * q.ld_w + k0 / 32;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = __ldcg(row + i);
+    __syncthreads();   // smem is reused from the last tile
+    close_tile_bits<8>(w, kPersistBlock, sm);
+    uint32_t* dst = q.T + (long long)(k0 + r) * q.ld_w + k0 / 32;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[i] = w[i];
+}
+
+__global__ void __launch_bounds__(BitsP::THREADS, 1) bool_warshall_persistent_kernel(const PersistArgs q) {
+    extern __shared__ __align__(16) uint32_t m4r_smem[];
+    __shared__ int item;
+    const int R = q.R, B = kPersistBlock;
+    unsigned* piv = q.ctr + 1;
+    unsigned* rp_done = q.ctr + 1 + R;
+    unsigned* a_done = q.ctr + 1 + 2 * R;
+    unsigned* b_done = q.ctr + 1 + 3 * R;
+    const int tiles_k = B / BitsP::BM;                          // row tiles of one pivot block
+    const int n_rp = tiles_k * q.ntw * q.ks_rp;
+    const int rows_t = q.n / BitsP::BM;
+    auto n_b = [&](int r) { return (rows_t - (r + 1 < R ? 2 : 1) * tiles_k) * q.ntw * q.ks_b; };
+    auto n_a = [&](int r) { return r + 1 < R ? n_rp : 0; };
+    const int nkw = B / 32;
+
+    const bool tr = q.trace != nullptr && threadIdx.x == 0;
+    if (blockIdx.x == 0) {   // pivot 0 before anything else
+        if (tr) q.trace[4 * (q.trace_cap - R)] = gtime_ns();
+        persist_pivot(q, 0, m4r_smem);
+        if (tr) q.trace[4 * (q.trace_cap - R) + 2] = gtime_ns();
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicExch(&piv[0], 1u);
+    }
+    for (;;) {
+        if (threadIdx.x == 0) item = (int)atomicAdd(&q.ctr[0], 1u);
+        __syncthreads();
+        int g = item;
+        __syncthreads();
+        const int g_all = g;
+        unsigned long long t_start = tr ? gtime_ns() : 0;
+        // queue order: RP(0) | A3(0) RP(1) B3(0) | A3(1) RP(2) B3(1) | ... | B3(R-1):
+        // the chain's next row panel is handed out ahead of the bulk 3b
+        // tiles, so CTAs are waiting for pivot r+1 when it lands
+        int r = -1, type = -1;
+        if (g < n_rp) { r = 0; type = 0; }
+        else {
+            g -= n_rp;
+            for (int s = 0; s < R; ++s) {
+                const int na = n_a(s), nr = s + 1 < R ? n_rp : 0, nb = n_b(s);
+                if (g < na) { r = s; type = 1; break; }
+                g -= na;
+                if (g < nr) { r = s + 1; type = 0; break; }
+                g -= nr;
+                if (g < nb) { r = s; type = 2; break; }
+                g -= nb;
+            }
+        }
+        if (r < 0) return;
+        const int k0 = r * B, k1 = k0 + B;
+        // dependencies (thread 0 waits, the CTA follows)
+        if (threadIdx.x == 0) {
+            if (type == 0) wait_geq(&piv[r], 1u);
+            else {
+                wait_geq(&rp_done[r], (unsigned)n_rp);
+                if (r > 0) wait_geq(&b_done[r - 1], (unsigned)n_b(r - 1));
+            }
+        }
+        __syncthreads();
+        unsigned long long t_ready = tr ? gtime_ns() : 0;
+        const int ks = type == 2 ? q.ks_b : q.ks_rp;
+        const int kc = g % ks, nt = (g / ks) % q.ntw, mi = g / (ks * q.ntw);
+        const int kw_lo = kc * nkw / ks, kw_hi = (kc + 1) * nkw / ks;
+        BitsArgs p{};
+        p.Nw = q.nw; p.K = B; p.lda = p.ldb = p.ldc = q.ld_w; p.accumulate = 1;
+        p.B = q.T + (long long)k0 * q.ld_w;
+        int mt = mi;
+        if (type == 0) {
+            p.A = q.T + (long long)k0 * q.ld_w + k0 / 32; p.C = q.T + (long long)k0 * q.ld_w; p.M = B;
+        } else if (type == 1) {
+            p.A = q.T + (long long)k1 * q.ld_w + k0 / 32; p.C = q.T + (long long)k1 * q.ld_w; p.M = B;
+        } else {
+            p.A = q.T + k0 / 32; p.C = q.T; p.M = q.n;
+            if (mt >= k0 / BitsP::BM) mt += (r + 1 < R ? 2 : 1) * tiles_k;   // skip K_r (u K_r+1)
+        }
+        m4r_tile<BitsP, true>(p, mt, nt, kw_lo, kw_hi, ks > 1, m4r_smem);
+        __threadfence();
+        __syncthreads();
+        if (tr && g_all < q.trace_cap - R) {
+            unsigned long long* e = q.trace + 4 * g_all;
+            e[0] = t_start; e[1] = t_ready; e[2] = gtime_ns();
+            e[3] = ((unsigned long long)blockIdx.x << 32) | ((unsigned long long)type << 16) | (unsigned)r;
+        }
+        if (type == 0) {
+            if (threadIdx.x == 0) atomicAdd(&rp_done[r], 1u);
+        } else if (type == 2) {
+            if (threadIdx.x == 0) atomicAdd(&b_done[r], 1u);
+        } else {
+            __shared__ unsigned last;
+            if (threadIdx.x == 0) last = atomicAdd(&a_done[r], 1u);
+            __syncthreads();
+            if (last + 1 == (unsigned)n_a(r)) {     // every A3(r) item is in: close pivot r+1
+                __threadfence();
+                if (tr) q.trace[4 * (q.trace_cap - R + r + 1)] = gtime_ns();
+                persist_pivot(q, k1, m4r_smem);
+                if (tr) q.trace[4 * (q.trace_cap - R + r + 1) + 2] = gtime_ns();
+                __threadfence();
+                __syncthreads();
+                if (threadIdx.x == 0) atomicExch(&piv[r + 1], 1u);
+            }
+        }
+    }
+}
+
+// Off by default: measured slower than the blocked schedule at every size
+// (n = 2048 / 4096 / 8192: 0.156 / 0.30-0.40 / 1.33-1.96 ms against 0.128 /
+// 0.250 / 0.85 ms; profiles/r02k_c2_persistent_trace.json).  The per-item
+// timeline shows why: an item costs ~2.3 us of L2 round trips (operand
+// loads through L2, atomics + fence) whatever its size, so the chain pivot
+// (5 us) -> row panel -> 3a is no shorter than three PDL launches.
+static std::atomic<int> g_bits_persistent{0};
+static unsigned long long* g_persist_trace = nullptr;
+static int g_persist_ks_rp = 8;
+static int g_persist_trace_cap = 0;
+
+inline size_t persist_ctr_bytes(int n) { return ((size_t)(1 + 4 * (n / kPersistBlock)) * 4 + 255) & ~size_t(255); }
+
+// The persistent closure, when n fits it (n % 256 == 0, 512 <= n <= 8192).
+static int bool_warshall_persistent(uint32_t* T, int n, long long ld_w, unsigned* ctr, cudaStream_t s) {
+    constexpr size_t smem = M4rSmem<BitsP>::BYTES;
+    static_assert(sizeof(PivotSmemT<8>) <= smem, "pivot smem aliases the tile tables");
+    SMX_TRY(set_max_smem((const void*)bool_warshall_persistent_kernel, smem));
+    int dev = 0, per_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bool_warshall_persistent_kernel, BitsP::THREADS, smem);
+    if (e != cudaSuccess) return (int)e;
+    if (per_sm < 1) return SMX_E_ARG;
+    const int grid = per_sm * sm_count();
+    PersistArgs q{};
+    q.T = T; q.n = n; q.nw = (n + 31) / 32; q.ld_w = ld_w; q.R = n / kPersistBlock;
+    q.ntw = ceil_div(q.nw, BitsP::BNW);
+    q.ks_rp = g_persist_ks_rp;
+    const int b_tiles = (n / BitsP::BM - 2 * (kPersistBlock / BitsP::BM)) * q.ntw;
+    q.ks_b = 1;
+    while (q.ks_b < 8 && b_tiles * q.ks_b * 2 <= grid) q.ks_b *= 2;
+    q.ctr = ctr;
+    q.trace = g_persist_trace;
+    q.trace_cap = g_persist_trace_cap;
+    e = cudaMemsetAsync(ctr, 0, persist_ctr_bytes(n), s);
+    if (e != cudaSuccess) return (int)e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(BitsP::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // every CTA resident: the queue's waits cannot deadlock
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    count_launch();
+    e = cudaLaunchKernelEx(&cfg, bool_warshall_persistent_kernel, q);
+    return e == cudaSuccess ? SMX_OK : (int)e;
+}
+
 inline size_t bits_ws_bytes(int n, long long ld_w) {
     const size_t rp = ((size_t)kMaxWarshallBlock * ld_w * 4 + 255) & ~size_t(255);
     const size_t cp = (size_t)n * (kMaxWarshallBlock / 32) * 4;
-    return rp + ((cp + 255) & ~size_t(255));
+    return rp + ((cp + 255) & ~size_t(255)) + persist_ctr_bytes(n);
 }
 
 // Pivot tile + pivot row panel of block [k0, k0 + bb).
@@ -513,13 +766,19 @@ int bool_warshall_bits(uint32_t* T, int n, long long ld_w, void* ws, size_t ws_b
     uint32_t* RP = reinterpret_cast<uint32_t*>(ws);
     uint32_t* CP = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ws) +
                                                (((size_t)kMaxWarshallBlock * ld_w * 4 + 255) & ~size_t(255)));
+    unsigned* ctr = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + bits_ws_bytes(n, ld_w) -
+                                                persist_ctr_bytes(n));
+    const bool persist = g_bits_persistent.load() && n % kPersistBlock == 0 && n >= 2 * kPersistBlock &&
+                         n <= kPersistMaxN && g_bits_m4r.load();
     GraphKey key;
     key.fn = 200;
     const unsigned long long kv[] = {(uintptr_t)T, (unsigned long long)n, (unsigned long long)ld_w,
                                      (uintptr_t)ws, ws_bytes, (unsigned long long)lookahead_enabled(),
-                                     (unsigned long long)bool_block_for_n(n), (unsigned long long)g_bits_m4r.load()};
+                                     (unsigned long long)bool_block_for_n(n), (unsigned long long)g_bits_m4r.load(),
+                                     (unsigned long long)persist};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     return run_graphed(key, s, false, [&](cudaStream_t st) -> int {
+        if (persist) return bool_warshall_persistent(T, n, ld_w, ctr, st);
         return bool_warshall_schedule(T, n, ld_w, RP, CP, st);
     });
 }
@@ -583,6 +842,28 @@ extern "C" {
 
 int smx_set_bits_m4r(int enable) {
     return g_bits_m4r.exchange(enable ? 1 : 0);
+}
+
+int smx_set_bool_block(int block) {
+    if (block != 0 && block != 128 && block != 256 && block != 512) return SMX_E_ARG;
+    const int old = g_bool_block;
+    g_bool_block = block;
+    return old;
+}
+
+int smx_set_bool_persistent(int enable) {
+    return g_bits_persistent.exchange(enable ? 1 : 0);
+}
+
+// development: per-item trace of the persistent closure (see PersistArgs)
+int smx_bool_persist_trace_arm(unsigned long long* buf, int cap_items) {
+    if (cap_items < 0) {   // (development) k-split of the row-panel / 3a items: -1, -2, -4, -8
+        g_persist_ks_rp = -cap_items;
+        return SMX_OK;
+    }
+    g_persist_trace = buf;
+    g_persist_trace_cap = buf ? cap_items : 0;
+    return SMX_OK;
 }
 
 int smx_bool_gemm_bits(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int Nwords, int K,

@@ -168,3 +168,31 @@ def test_c5_full_size_matches_oracle_digest(config_digests):
            if hashlib.sha256(out[i * d["band_rows"]:(i + 1) * d["band_rows"]].tobytes()).hexdigest() != h]
     assert not bad, f"row bands differing from the oracle: {bad}"
     assert hashlib.sha256(out.tobytes()).hexdigest() == d["output_sha256"]
+
+
+# -- persistent bit Warshall -------------------------------------------------------
+
+@pytest.mark.parametrize("n", [512, 768, 1280, 2048, 4096, 8192])
+def test_bool_warshall_persistent_matches_blocked_and_oracle(n, oracle_lib):
+    """The one-launch persistent closure (smx_set_bool_persistent(1), the
+    default for 512 <= n <= 8192) equals the blocked schedule and the oracle,
+    on the C2 generator (mean out-degree 2) and on a denser graph."""
+    lib = _native.lib()
+    cfg = workloads.CONFIGS["c2_bool_warshall"]
+    (sparse,) = workloads.make_inputs(cfg, n)
+    dense = (np.random.default_rng(n).random((n, n)) < 0.5 / n ** 0.5).astype(np.uint8)
+    for t in (sparse, dense):
+        want = oracle_lib.bool_close(oracle_lib.pack_bits(t)) if n <= 4096 else None
+        m = BoolMatrix.from_numpy(t)
+        got = {}
+        for mode in (1, 0):
+            old = lib.smx_set_bool_persistent(mode)
+            try:
+                got[mode] = m.transitive_closure().blocks
+                got[(mode, "again")] = m.transitive_closure().blocks    # the graph-replayed call
+            finally:
+                lib.smx_set_bool_persistent(old)
+        np.testing.assert_array_equal(got[1], got[0])
+        np.testing.assert_array_equal(got[(1, "again")], got[0])
+        if want is not None:
+            np.testing.assert_array_equal(got[1], want)
