@@ -35,10 +35,10 @@
 namespace smx {
 
 // Largest pivot block: 512 vertices for u16 (the packed phase 3 runs K = 512
-// per CTA), 256 for u8, 128 for u32 (whose 1024-thread pivot tile would not
-// fit the register file).  Tiles above 128 close by 2 x 2 recursion.
-template <typename T> struct FwBlock { static constexpr int value = sizeof(T) == 4 ? 128 : (sizeof(T) == 2 ? 512 : 256); };
-inline int fw_block_for(int eb) { return eb == 4 ? 128 : (eb == 2 ? 512 : 256); }
+// per CTA), 256 for u8 and u32.  Tiles above 128 close by 2 x 2 recursion
+// (the 1024-thread register pivot holds at most 128 x 128).
+template <typename T> struct FwBlock { static constexpr int value = sizeof(T) == 2 ? 512 : 256; };
+inline int fw_block_for(int eb) { return eb == 2 ? 512 : 256; }
 // Block used for an n-vertex closure.  A larger block halves the rounds and
 // doubles phase 3's K per CTA, amortising each CTA's ramp and C fold; it
 // costs a longer pivot chain, which must hide behind one round's phase 3.
@@ -51,7 +51,7 @@ template <typename T> inline int fw_block_for_n(int n) {
     const int ov = g_fw_block_override.load(std::memory_order_relaxed);
     if (ov != 0) return ov < mx ? ov : mx;
     if (sizeof(T) == 2 && n >= 16384) return 512;
-    return (sizeof(T) < 4 && n >= 8192) ? 256 : 128;
+    return n >= 8192 ? 256 : 128;
 }
 
 // ---- phase 1: pivot tile closure ------------------------------------------
@@ -489,29 +489,27 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 inline size_t fw_ws_bytes(int n, long long ld, int eb) {
     // RP: pivot row panel snapshot (B x ld); CP: column panel snapshot (n x B);
-    // u8/u16: the packed phase-3 operand tiles (semiring_packed.cuh) and a
-    // 256-byte slot for the per-round operand certificate (fw_rounds_packed)
+    // the packed phase-3 operand tiles (semiring_packed.cuh) and a 256-byte
+    // slot for the per-round operand certificate (fw_rounds_packed)
     const size_t B = fw_block_for(eb);
     const size_t base = align256(B * ld * eb) + align256((size_t)n * B * eb);
-    return eb <= 2 ? base + align256(packed_ws_bytes(n, n, (int)B)) + 256 : base;
+    return base + align256(packed_ws_bytes_eb(n, n, (int)B, eb)) + 256;
 }
-// The certificate slot: the last 256 bytes of fw_ws_bytes (u8/u16).
+// The certificate slot: the last 256 bytes of fw_ws_bytes.
 inline int* fw_cert_slot(void* ws, int n, long long ld, int eb) {
     return reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + fw_ws_bytes(n, ld, eb) - 256);
 }
 
-// smx_set_fw_packed: u16 phase 3 on the warp-specialised packed-tile kernel
+// smx_set_fw_packed: phase 3 on the warp-specialised packed-tile kernel
 static std::atomic<int> g_fw_packed{1};
 
 // Phase 3 (3b) product: C rows outside [skip0, skip0 + skipn) (+)= CP (x) rowK.
 template <typename T>
 int fw_phase3(const T* CP, long long ldcp, const T* rowK, T* Tm, int n, long long ld, int bb, int kind,
               int skip0, int skipn, void* pws, size_t pws_bytes, cudaStream_t s) {
-    if constexpr (sizeof(T) <= 2) {
-        if (g_fw_packed && pws != nullptr)
-            return semiring_gemm_packed<T>(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, skip0, skipn, pws,
-                                           pws_bytes, s);
-    }
+    if (g_fw_packed && pws != nullptr)
+        return semiring_gemm_packed<T>(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, skip0, skipn, pws,
+                                       pws_bytes, s);
     return semiring_gemm<T>(CP, rowK, Tm, n, n, bb, ldcp, ld, ld, kind, 1, skip0, skipn, s);
 }
 
@@ -545,7 +543,8 @@ template <typename T>
 int fw_pivot_and_row_panel(T* Tm, int n, long long ld, int kind, T* RP, int k0, int bb, cudaStream_t s,
                            bool lite = false) {
     T* rowK = Tm + (long long)k0 * ld;
-    if (lite && bb <= 256) SMX_TRY(fw_pivot_lite<T>(rowK + k0, bb, ld, kind, s));
+    // (the lite pivot's shared-memory tile holds 256 x 256 u16 or 128 x 128 u32)
+    if (lite && bb <= (sizeof(T) == 4 ? 128 : 256)) SMX_TRY(fw_pivot_lite<T>(rowK + k0, bb, ld, kind, s));
     else SMX_TRY(fw_pivot<T>(rowK + k0, bb, ld, kind, s, RP));   // RP: the pivot's scratch
     // Row panel in place, no snapshot: T[K,:] (+)= P* (x) T[K,:] with
     // P* = T[K,K] closed.  A CTA may read (through the read-only path) rows K
@@ -664,16 +663,10 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
         const int k0 = r * BLK, bb = blk(r);
         T* rowK = Tm + (long long)k0 * ld;
         const int* cr = nullptr;
-        if constexpr (sizeof(T) == 2) {
+        if constexpr (!Lane<T>::kOneInstr) {
             if (certified(r)) {
-                if ((e = cudaMemsetAsync(cert, 0xFF, sizeof(int), s)) != cudaSuccess) return (int)e;
-                const int blocks = 4 * sm_count();
-                cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(Tm + (long long)lo * ld + k0),
-                                                       hi - lo, bb, ld, kind == SMX_ANTI, cert);
-                SMX_LAUNCHED_OR_RETURN();
-                cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(rowK), bb, n, ld,
-                                                       kind == SMX_ANTI, cert);
-                SMX_LAUNCHED_OR_RETURN();
+                SMX_TRY(run_cert<T>(Tm + (long long)lo * ld + k0, hi - lo, bb, ld, rowK, bb, n, ld,
+                                    kind == SMX_ANTI, cert, s));
                 cr = cert;
                 SMX_TRY(packed_pack_a_rows<T>(Tm + k0, n, n, bb, ld, kind, pws, pws_bytes, t0, tiles, s, cr));
             }
@@ -754,8 +747,8 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
                                  align256((size_t)FwBlock<T>::value * ld * sizeof(T)));
     const size_t pws_off = align256((size_t)FwBlock<T>::value * ld * sizeof(T)) +
                            align256((size_t)n * FwBlock<T>::value * sizeof(T));
-    void* pws = sizeof(T) <= 2 ? reinterpret_cast<char*>(ws) + pws_off : nullptr;
-    const size_t pws_bytes = sizeof(T) <= 2 ? ws_bytes - pws_off : 0;
+    void* pws = reinterpret_cast<char*>(ws) + pws_off;
+    const size_t pws_bytes = ws_bytes - pws_off;
     GraphKey key;
     key.fn = 100 + (int)sizeof(T);
     const unsigned long long kv[] = {(uintptr_t)Tm, (unsigned long long)n, (unsigned long long)ld,
@@ -767,11 +760,9 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     // the phase-3 trace records host-side state per launch: trace runs stay eager
     return run_graphed(key, s, g_trace.armed, [&](cudaStream_t st) -> int {
-        if constexpr (sizeof(T) <= 2) {
-            if (lookahead_enabled() && g_fw_packed && pws != nullptr)
-                return fw_run_lookahead_packed<T>(Tm, n, ld, kind, RP, pws, pws_bytes, st,
-                                                  fw_cert_slot(ws, n, ld, sizeof(T)));
-        }
+        if (lookahead_enabled() && g_fw_packed)
+            return fw_run_lookahead_packed<T>(Tm, n, ld, kind, RP, pws, pws_bytes, st,
+                                              fw_cert_slot(ws, n, ld, sizeof(T)));
         if (lookahead_enabled()) return fw_run_lookahead<T>(Tm, n, ld, kind, RP, CP, pws, pws_bytes, st);
         return fw_run_serial<T>(Tm, n, ld, kind, RP, CP, pws, pws_bytes, BLK, st);
     });
@@ -875,10 +866,11 @@ constexpr int kFwHostTailBlocks = 4;
 // 141 vs 152 ms; 32768: 1040 vs 1105 ms, tools/perf_host_fw.py).
 static std::atomic<int> g_fw_host_stream{1};
 
-inline size_t fw_host_slot_bytes(int n, int eb) { return align256(packed_ws_bytes(n, n, fw_block_for(eb))); }
+inline size_t fw_host_slot_bytes(int n, int eb) {
+    return align256(packed_ws_bytes_eb(n, n, fw_block_for(eb), eb));
+}
 inline size_t fw_host_ws_bytes(int n, long long ld, int eb) {
-    const size_t base = fw_ws_bytes(n, ld, eb);
-    return eb <= 2 ? base + kFwHostTailBlocks * fw_host_slot_bytes(n, eb) : base;
+    return fw_ws_bytes(n, ld, eb) + kFwHostTailBlocks * fw_host_slot_bytes(n, eb);
 }
 
 // Egress chunk boundaries over rows [0, sL): from the end, 1, 1, 2, 4, 8, 16,
@@ -912,13 +904,10 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
     const int BLK = fw_block_for_n<T>(n);
     const int R = (n + BLK - 1) / BLK;
     cudaError_t e;
-    bool streamed = false;
-    if constexpr (sizeof(T) <= 2) {
-        const int mode = g_fw_host_stream.load(std::memory_order_relaxed);
-        streamed = lookahead_enabled() && g_fw_packed && R >= 2 * kFwHostTailBlocks &&
-                   (mode == 2 || (mode == 1 && n >= 16384));
-    }
-    if (!streamed) {   // small or u32: copy in, close, copy out, in stream order
+    const int mode = g_fw_host_stream.load(std::memory_order_relaxed);
+    const bool streamed = lookahead_enabled() && g_fw_packed && R >= 2 * kFwHostTailBlocks &&
+                          (mode == 2 || (mode == 1 && n >= 16384));
+    if (!streamed) {   // small: copy in, close, copy out, in stream order
         if ((e = cudaMemcpyAsync(Tm, hin, (size_t)n * row_bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
             return (int)e;
         SMX_TRY(fw_run<T>(Tm, n, ld, kind, ws, ws_bytes, s));
@@ -980,16 +969,10 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
         // blocks read rows the first product has already filled in.
         for (int k0 = 0; k0 < (int)r0; k0 += BLK) {
             const int* cr = nullptr;
-            if constexpr (sizeof(T) == 2) {
+            if constexpr (!Lane<T>::kOneInstr) {
                 if (k0 == 0 && bounded_fastpath_enabled()) {
-                    if ((e = cudaMemsetAsync(cert, 0xFF, sizeof(int), s)) != cudaSuccess) return (int)e;
-                    const int blocks = 4 * sm_count();
-                    cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(Tm + r0 * ld),
-                                                           r1 - (int)r0, BLK, ld, kind == SMX_ANTI, cert);
-                    SMX_LAUNCHED_OR_RETURN();
-                    cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(Tm), BLK, n, ld,
-                                                           kind == SMX_ANTI, cert);
-                    SMX_LAUNCHED_OR_RETURN();
+                    SMX_TRY(run_cert<T>(Tm + r0 * ld, r1 - (int)r0, BLK, ld, Tm, BLK, n, ld, kind == SMX_ANTI,
+                                        cert, s));
                     cr = cert;
                 }
             }
@@ -1031,41 +1014,29 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
 template <typename T>
 static int gemm_skip(const T* A, const T* B, T* C, int M, int N, int K, int lda, int ldb, int ldc, int kind,
                      int skip_row0, int skip_rows, cudaStream_t s, bool certify = false) {
-    if constexpr (sizeof(T) <= 2) {
-        // the packed path (and its certificate pass, which reads 16-byte
-        // vectors at X + r*ld) needs 16-byte aligned bases AND row strides;
-        // anything else takes the register-staged GEMM below
-        if (g_fw_packed && (long long)M * N >= (1LL << 24) && K > 0 && aligned16(A) && aligned16(B) &&
-            aligned16(C) && ld_ok(lda, sizeof(T)) && ld_ok(ldb, sizeof(T)) && ld_ok(ldc, sizeof(T)) &&
-            lda >= K && ldb >= N && ldc >= N) {
-            const size_t bytes = packed_ws_bytes(M, N, K);
-            void* ws = nullptr;
-            if (scratch_alloc(&ws, bytes + 256, s) == SMX_OK) {
-                int* cert = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + bytes);
-                const int* cr = nullptr;
-                int rc = SMX_OK;
-                if (sizeof(T) == 2 && certify && bounded_fastpath_enabled()) {
-                    cudaError_t e = cudaMemsetAsync(cert, 0xFF, sizeof(int), s);
-                    if (e != cudaSuccess) rc = (int)e;
-                    const int blocks = 4 * sm_count();
-                    if (rc == SMX_OK) {
-                        cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(A), M, K, lda,
-                                                               kind == SMX_ANTI, cert);
-                        cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(B), K, N, ldb,
-                                                               kind == SMX_ANTI, cert);
-                        count_launch();
-                        count_launch();
-                        const cudaError_t le = cudaGetLastError();
-                        if (le != cudaSuccess) rc = (int)le;
-                    }
+    // the packed path (and its certificate pass, which reads 16-byte
+    // vectors at X + r*ld) needs 16-byte aligned bases AND row strides;
+    // anything else takes the register-staged GEMM below
+    if (g_fw_packed && (long long)M * N >= (1LL << 24) && K > 0 && aligned16(A) && aligned16(B) &&
+        aligned16(C) && ld_ok(lda, sizeof(T)) && ld_ok(ldb, sizeof(T)) && ld_ok(ldc, sizeof(T)) &&
+        lda >= K && ldb >= N && ldc >= N) {
+        const size_t bytes = packed_ws_bytes_t<T>(M, N, K);
+        void* ws = nullptr;
+        if (scratch_alloc(&ws, bytes + 256, s) == SMX_OK) {
+            int* cert = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + bytes);
+            const int* cr = nullptr;
+            int rc = SMX_OK;
+            if constexpr (!Lane<T>::kOneInstr) {
+                if (certify && bounded_fastpath_enabled()) {
+                    rc = run_cert<T>(A, M, K, lda, B, K, N, ldb, kind == SMX_ANTI, cert, s);
                     cr = cert;
                 }
-                if (rc == SMX_OK) rc = packed_pack<T>(A, B, M, N, K, lda, ldb, kind, ws, bytes, s, cr);
-                if (rc == SMX_OK)
-                    rc = packed_run<T>(C, M, N, K, ldc, kind, 1, 0, -1, skip_row0, skip_rows, ws, bytes, s, cr);
-                scratch_free(ws, s);
-                return rc;
             }
+            if (rc == SMX_OK) rc = packed_pack<T>(A, B, M, N, K, lda, ldb, kind, ws, bytes, s, cr);
+            if (rc == SMX_OK)
+                rc = packed_run<T>(C, M, N, K, ldc, kind, 1, 0, -1, skip_row0, skip_rows, ws, bytes, s, cr);
+            scratch_free(ws, s);
+            return rc;
         }
     }
     return semiring_gemm<T>(A, B, C, M, N, K, lda, ldb, ldc, kind, 1, skip_row0, skip_rows, s);
@@ -1095,6 +1066,9 @@ int smx_semiring_gemm_u16(const uint16_t* A, const uint16_t* B, uint16_t* C, int
 }
 int smx_semiring_gemm_u32(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int N, int K,
                           int lda, int ldb, int ldc, int kind, int accumulate, void* stream) {
+    if (g_fw_packed && (long long)M * N >= (1LL << 22) && K >= 256)
+        return semiring_gemm_packed_public<uint32_t>(A, B, C, M, N, K, lda, ldb, ldc, kind, accumulate,
+                                                     as_stream(stream));
     return semiring_gemm<uint32_t>(A, B, C, M, N, K, lda, ldb, ldc, kind, accumulate, 0, 0,
                                    as_stream(stream), /*certify=*/true);
 }
@@ -1108,7 +1082,7 @@ static int gemm_skip_entry(const void* A, const void* B, void* C, int M, int N, 
         case 2: return gemm_skip<uint16_t>((const uint16_t*)A, (const uint16_t*)B, (uint16_t*)C, M, N, K, lda, ldb,
                                            ldc, kind, skip_row0, skip_rows, s, certify);
         case 4: return gemm_skip<uint32_t>((const uint32_t*)A, (const uint32_t*)B, (uint32_t*)C, M, N, K, lda,
-                                           ldb, ldc, kind, skip_row0, skip_rows, s);
+                                           ldb, ldc, kind, skip_row0, skip_rows, s, certify);
         default: return SMX_E_ARG;
     }
 }

@@ -36,12 +36,15 @@ template <> struct Lane<uint16_t> {
     static constexpr int kCellsPerChunk = 8;                 // 16 B of global
     static constexpr int kWordsPerChunk = 4;
     __device__ __forceinline__ static uint32_t splat(uint32_t v) { return v * 0x10001u; }
+    // (+) of two canonical words: lane-wise min
+    __device__ __forceinline__ static uint32_t fold(uint32_t x, uint32_t y) { return __vminu2(x, y); }
     __device__ __forceinline__ static uint32_t step(uint32_t c, uint32_t b, uint32_t a,
                                                     uint32_t sa) {
         return __viaddmin_u16x2(__vminu2(b, sa), a, c);
     }
     // lanes below 2^15 on both sides: a + b <= 65534 < S, no clamp needed
     static constexpr uint32_t kHalfMask = 0x80008000u;
+    static constexpr uint32_t kCellHalf = 0x8000u;    // the same test on one cell value
     __device__ __forceinline__ static uint32_t step_bounded(uint32_t c, uint32_t b, uint32_t a) {
         return __viaddmin_u16x2(a, b, c);
     }
@@ -69,11 +72,13 @@ template <> struct Lane<uint8_t> {
     static constexpr int kCellsPerChunk = 16;
     static constexpr int kWordsPerChunk = 8;
     __device__ __forceinline__ static uint32_t splat(uint32_t v) { return v * 0x10001u; }
+    __device__ __forceinline__ static uint32_t fold(uint32_t x, uint32_t y) { return __vminu2(x, y); }
     __device__ __forceinline__ static uint32_t step(uint32_t c, uint32_t b, uint32_t a,
                                                     uint32_t /*sa*/) {
         return __viaddmin_u16x2(a, b, c);
     }
     static constexpr uint32_t kHalfMask = 0u;   // always the 1-instruction form
+    static constexpr uint32_t kCellHalf = 0u;
     __device__ __forceinline__ static uint32_t step_bounded(uint32_t c, uint32_t b, uint32_t a) {
         return __viaddmin_u16x2(a, b, c);
     }
@@ -90,11 +95,13 @@ template <> struct Lane<uint32_t> {
     static constexpr int kCellsPerChunk = 4;
     static constexpr int kWordsPerChunk = 4;
     __device__ __forceinline__ static uint32_t splat(uint32_t v) { return v; }
+    __device__ __forceinline__ static uint32_t fold(uint32_t x, uint32_t y) { return min(x, y); }
     __device__ __forceinline__ static uint32_t step(uint32_t c, uint32_t b, uint32_t a,
                                                     uint32_t sa) {
         return __viaddmin_u32(min(b, sa), a, c);
     }
     static constexpr uint32_t kHalfMask = 0x80000000u;
+    static constexpr uint32_t kCellHalf = 0x80000000u;
     __device__ __forceinline__ static uint32_t step_bounded(uint32_t c, uint32_t b, uint32_t a) {
         return __viaddmin_u32(a, b, c);
     }
@@ -137,6 +144,17 @@ template <typename T>
 __device__ __forceinline__ uint32_t word_cell(const uint32_t* w, int j) {
     if (Lane<T>::kCellsPerWord == 2) return (w[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
     return w[j];
+}
+
+// Set cell j of a chunk's canonical words to the lane value v.
+template <typename T>
+__device__ __forceinline__ void set_word_cell(uint32_t* w, int j, uint32_t v) {
+    if (Lane<T>::kCellsPerWord == 2) {
+        const int s2 = (j & 1) * 16;
+        w[j >> 1] = (w[j >> 1] & ~(0xFFFFu << s2)) | (v << s2);
+    } else {
+        w[j] = v;
+    }
 }
 
 // Replace cells [valid, kCellsPerChunk) of a chunk by the (+)-identity S.

@@ -15,7 +15,7 @@
 // [BK][BM]) and BK x 128 B tile (canonical words, [BK][BNW]) contiguously,
 // together with a per-tile flag "every lane < 2^15" -- the bounded test,
 // decided once per tile instead of voted per CTA.  Public products may
-// instead be packed in the product-wide shifted encoding (cert_u16_kernel).
+// instead be packed in the product-wide shifted encoding (cert_kernel).
 // The GEMM runs one producer warp that streams tiles with 1-D bulk async
 // copies (cp.async.bulk + mbarrier complete_tx) into a SMX_PACKED_STAGES ring
 // of SMX_PACKED_BK-deep k-tiles (3 x 32 by default: 24 KB stages), and 8
@@ -51,10 +51,13 @@ namespace smx {
 // T = uint16_t, or uint8_t widened to u16 lanes (Lane<uint8_t>: a + b <= 510
 // cannot wrap and C starts <= 255, so every u8 tile takes the 1-instruction
 // update).  The packed tiles hold the same u16x2 lane words for both.
+// T = uint32_t: one cell per word (kernels.py:35), so the same 128 x 64-word
+// tiles cover 128 x 64 cells; the update is VIADDMNMX (bounded / certified
+// tiles) or IMNMX + VIADDMNMX (general), one or two instructions per cell.
 template <typename T>
 struct PackedCfg {
     static constexpr int BM = 128, BNW = 64, BK = SMX_PACKED_BK, TM = 4, TNW = 8, HW = 4;
-    static constexpr int BN = 2 * BNW;                 // cells
+    static constexpr int BN = Lane<T>::kCellsPerWord * BNW;   // cells
     static constexpr int TCOLS = BNW / TNW;            // 8
     static constexpr int CONSUMERS = (BM / TM) * TCOLS;  // 256
     static constexpr int THREADS = CONSUMERS + 32;     // + producer warp
@@ -117,9 +120,7 @@ __global__ void __launch_bounds__(128) pack_a_kernel(const T* __restrict__ A, in
             for (int i = 0; i < WPC; ++i) w[i] = L::kIdentityWord;
             for (int j = 0; j < E; ++j) {
                 if (row >= M || kq + j >= K) break;
-                const uint32_t v = canon_cell<T>(A[(long long)row * lda + kq + j], anti);
-                const int s2 = (j & 1) * 16;
-                w[j >> 1] = (w[j >> 1] & ~(0xFFFFu << s2)) | (v << s2);
+                set_word_cell<T>(w, j, canon_cell<T>(A[(long long)row * lda + kq + j], anti));
             }
         }
 #pragma unroll
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(128) pack_a_kernel(const T* __restrict__ A, in
             dst[(q * E + j) * G::BM] = sh ? L::to_shifted(sw) : sw;
         }
     }
-    const int ok = __syncthreads_and((hi & (L::kHalfMask & 0xFFFFu)) == 0u);
+    const int ok = __syncthreads_and((hi & L::kCellHalf) == 0u);
     if (r == 0) fA[(size_t)mt * KT + kt] = (uint8_t)ok;
 }
 
@@ -161,9 +162,7 @@ __global__ void __launch_bounds__(256) pack_b_kernel(const T* __restrict__ B, in
             for (int i = 0; i < WPC; ++i) w[i] = L::kIdentityWord;
             for (int j = 0; j < E; ++j) {
                 if (k >= K || col + j >= N) break;
-                const uint32_t v = canon_cell<T>(B[(long long)k * ldb + col + j], anti);
-                const int s2 = (j & 1) * 16;
-                w[j >> 1] = (w[j >> 1] & ~(0xFFFFu << s2)) | (v << s2);
+                set_word_cell<T>(w, j, canon_cell<T>(B[(long long)k * ldb + col + j], anti));
             }
         }
         uint32_t* dst = Bp + ((size_t)kt * NT + nt) * G::B_TILE_WORDS + kk * G::BNW + c * WPC;
@@ -369,14 +368,14 @@ packed_gemm_kernel(const PackedArgsT<T> p) {
         T* crow = p.C + (long long)grow * p.ldc;
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
-            const int cc = (g * (BNW / 2) + tc * HW) * 2;   // cell offset in the tile
+            const int cc = (g * (BNW / 2) + tc * HW) * L::kCellsPerWord;   // cell offset in the tile
             uint32_t* w = &acc[i][g * HW];
             if (c_async || p.accumulate) {
                 uint32_t c[HW];
                 if (c_async) load_c_group<T, HW>(Cs + (tr * TM + i) * G::BN, cc, G::BN, anti, c);
                 else load_c_group<T, HW>(crow, col0 + cc, p.N, anti, c);
 #pragma unroll
-                for (int j = 0; j < HW; ++j) w[j] = __vminu2(w[j], c[j]);
+                for (int j = 0; j < HW; ++j) w[j] = L::fold(w[j], c[j]);
             }
             store_c_group<T, HW>(crow, col0 + cc, p.N, anti, w);
         }
@@ -384,16 +383,23 @@ packed_gemm_kernel(const PackedArgsT<T> p) {
 }
 
 // Workspace for one packed product of M x K by K x N (A tiles, B tiles, flags;
-// the same for u8 and u16: both pack u16x2 lane words).
-inline size_t packed_ws_bytes(int M, int N, int K) {
-    using G = PackedU16;
+// the same for u8 and u16, which both pack u16x2 lane words; u32 B tiles
+// cover half as many columns).
+template <typename T>
+inline size_t packed_ws_bytes_t(int M, int N, int K) {
+    using G = PackedCfg<T>;
     const size_t MT = ceil_div(M, G::BM), NT = ceil_div(N, G::BN), KT = ceil_div(K, G::BK);
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     return al(MT * KT * G::A_TILE_WORDS * 4) + al(KT * NT * G::B_TILE_WORDS * 4) + al(MT * KT) + al(KT * NT);
 }
+inline size_t packed_ws_bytes(int M, int N, int K) { return packed_ws_bytes_t<uint16_t>(M, N, K); }
 inline size_t packed_u16_ws_bytes(int M, int N, int K) { return packed_ws_bytes(M, N, K); }
+// by storage element bytes (1, 2: u16x2 lanes; 4: u32 lanes)
+inline size_t packed_ws_bytes_eb(int M, int N, int K, int eb) {
+    return eb == 4 ? packed_ws_bytes_t<uint32_t>(M, N, K) : packed_ws_bytes_t<uint16_t>(M, N, K);
+}
 
-// Views of a packed workspace laid out by packed_ws_bytes(M, N, K).
+// Views of a packed workspace laid out by packed_ws_bytes_t<T>(M, N, K).
 struct PackedWs {
     uint32_t* Ap;
     uint32_t* Bp;
@@ -401,8 +407,9 @@ struct PackedWs {
     uint8_t* fB;
     int MT, NT, KT;
 };
+template <typename T>
 inline PackedWs packed_views(void* ws, int M, int N, int K) {
-    using G = PackedU16;
+    using G = PackedCfg<T>;
     PackedWs v;
     v.MT = ceil_div(M, G::BM);
     v.NT = ceil_div(N, G::BN);
@@ -426,7 +433,7 @@ inline int packed_check(const void* A, const void* B, int M, int N, int K, long 
     if ((A && !aligned16(A)) || (B && !aligned16(B))) return SMX_E_ALIGN;
     if (!ld_ok(lda, sizeof(T)) || !ld_ok(ldb, sizeof(T))) return SMX_E_ALIGN;
     if (lda < K || ldb < N) return SMX_E_ARG;
-    if (ws == nullptr || ws_bytes < packed_ws_bytes(M, N, K)) return SMX_E_WORKSPACE;
+    if (ws == nullptr || ws_bytes < packed_ws_bytes_t<T>(M, N, K)) return SMX_E_WORKSPACE;
     return SMX_OK;
 }
 
@@ -436,7 +443,7 @@ inline int packed_pack(const T* A, const T* B, int M, int N, int K, long long ld
                        size_t ws_bytes, cudaStream_t s, const int* cert = nullptr) {
     SMX_TRY(packed_check<T>(A, B, M, N, K, lda, ldb, kind, ws, ws_bytes));
     if (M == 0 || N == 0 || K == 0) return SMX_OK;
-    const PackedWs v = packed_views(ws, M, N, K);
+    const PackedWs v = packed_views<T>(ws, M, N, K);
     const int anti = kind == SMX_ANTI;
     if (A) {
         pack_a_kernel<T><<<dim3(v.KT, v.MT), 128, 0, s>>>(A, M, K, lda, anti, v.KT, v.Ap, v.fA, cert);
@@ -458,7 +465,7 @@ inline int packed_pack_a_rows(const T* A, int M, int N, int K, long long lda, in
                               int tile0, int tiles, cudaStream_t s, const int* cert = nullptr) {
     SMX_TRY(packed_check<T>(A, nullptr, M, N, K, lda, lda, kind, ws, ws_bytes));   // (no B: ldb unused)
     if (M == 0 || N == 0 || K == 0) return SMX_OK;
-    const PackedWs v = packed_views(ws, M, N, K);
+    const PackedWs v = packed_views<T>(ws, M, N, K);
     if (tile0 < 0 || tile0 > v.MT) return SMX_E_ARG;
     if (tiles < 0 || tile0 + tiles > v.MT) tiles = v.MT - tile0;
     if (tiles == 0) return SMX_OK;
@@ -479,8 +486,8 @@ inline int packed_run(T* C, int M, int N, int K, long long ldc, int kind, int ac
     if (M == 0 || N == 0) return SMX_OK;
     if (!aligned16(C) || !ld_ok(ldc, sizeof(T))) return SMX_E_ALIGN;
     if (ldc < N) return SMX_E_ARG;
-    if (ws == nullptr || ws_bytes < packed_ws_bytes(M, N, K)) return SMX_E_WORKSPACE;
-    const PackedWs v = packed_views(ws, M, N, K);
+    if (ws == nullptr || ws_bytes < packed_ws_bytes_t<T>(M, N, K)) return SMX_E_WORKSPACE;
+    const PackedWs v = packed_views<T>(ws, M, N, K);
     if (row_tile0 < 0 || row_tile0 > v.MT) return SMX_E_ARG;
     if (row_tiles < 0 || row_tile0 + row_tiles > v.MT) row_tiles = v.MT - row_tile0;
     PackedArgsT<T> a{v.Ap, v.Bp, v.fA, v.fB, C, M, N, v.KT, v.NT, ldc, kind == SMX_ANTI, accumulate != 0,
@@ -529,29 +536,51 @@ inline int semiring_gemm_packed_u16(const uint16_t* A, const uint16_t* B, uint16
                                           ws, ws_bytes, s);
 }
 
-// Global sparse-bounded certificate of a u16 operand (rows x cols, ld): clears
-// *cert if any lane in distance form is neither S nor < 2^14 (Lane::cert_ok).
-// Concurrent writers only store 0.
-__global__ void cert_u16_kernel(const uint16_t* __restrict__ X, int rows, int cols, long long ld, int anti,
-                                int* __restrict__ cert) {
-    using L = Lane<uint16_t>;
-    const int cpr = (cols + 7) / 8;
+// Global sparse-bounded certificate of a u16 / u32 operand (rows x cols, ld):
+// clears *cert if any lane in distance form is neither S nor < 2^14 (u16) /
+// 2^30 (u32) (Lane::cert_ok).  Concurrent writers only store 0.
+template <typename T>
+__global__ void cert_kernel(const T* __restrict__ X, int rows, int cols, long long ld, int anti,
+                            int* __restrict__ cert) {
+    using L = Lane<T>;
+    constexpr int E = 16 / (int)sizeof(T);
+    const int cpr = (cols + E - 1) / E;
     const long long total = (long long)rows * cpr;
     const uint32_t m = anti ? 0xFFFFFFFFu : 0u;
     bool ok = true;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(i / cpr), c = (int)(i % cpr) * 8;
+        const int r = (int)(i / cpr), c = (int)(i % cpr) * E;
         uint4 w = __ldg(reinterpret_cast<const uint4*>(X + r * ld + c));
         w.x ^= m; w.y ^= m; w.z ^= m; w.w ^= m;
-        if (c + 8 > cols) {   // cells >= cols: identity (S), which certifies
+        if (c + E > cols) {   // cells >= cols: identity (S), which certifies
             uint32_t e[4] = {w.x, w.y, w.z, w.w};
-            for (int j = cols - c; j < 8; ++j) e[j >> 1] |= 0xFFFFu << ((j & 1) * 16);
+            for (int j = cols - c; j < E; ++j) set_word_cell<T>(e, j, L::kS);
             w = make_uint4(e[0], e[1], e[2], e[3]);
         }
         ok = ok && L::cert_ok(w.x) && L::cert_ok(w.y) && L::cert_ok(w.z) && L::cert_ok(w.w);
     }
     if (!__all_sync(0xFFFFFFFFu, ok) && (threadIdx.x & 31) == 0) *cert = 0;
+}
+
+// Reset *cert and run the certificate over an operand pair (either may be
+// nullptr): the caller's packs and products then read *cert.
+template <typename T>
+inline int run_cert(const T* X, int xr, int xc, long long ldx, const T* Y, int yr, int yc, long long ldy, int anti,
+                    int* cert, cudaStream_t s) {
+    static_assert(sizeof(T) >= 2, "u8 is always the 1-instruction form");
+    cudaError_t e = cudaMemsetAsync(cert, 0xFF, sizeof(int), s);
+    if (e != cudaSuccess) return (int)e;
+    const int blocks = 4 * sm_count();
+    if (X) {
+        cert_kernel<T><<<blocks, 256, 0, s>>>(X, xr, xc, ldx, anti, cert);
+        SMX_LAUNCHED_OR_RETURN();
+    }
+    if (Y) {
+        cert_kernel<T><<<blocks, 256, 0, s>>>(Y, yr, yc, ldy, anti, cert);
+        SMX_LAUNCHED_OR_RETURN();
+    }
+    return SMX_OK;
 }
 
 // Public u16 product on the packed kernel.  K is processed in chunks so the
@@ -569,11 +598,12 @@ inline int semiring_gemm_packed_public(const T* A, const T* B, T* C, int M, int 
     if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return SMX_E_ALIGN;
     if (!ld_ok(lda, sizeof(T)) || !ld_ok(ldb, sizeof(T)) || !ld_ok(ldc, sizeof(T))) return SMX_E_ALIGN;
     if (lda < K || ldb < N || ldc < N) return SMX_E_ARG;
-    long long kc = (384LL << 20) / ((long long)G::BM * ceil_div(M, G::BM) * 4 + (long long)G::BN * ceil_div(N, G::BN) * 2);
+    long long kc = (384LL << 20) / ((long long)G::BM * ceil_div(M, G::BM) * 4 +
+                                    (long long)G::BNW * ceil_div(N, G::BN) * 4);
     kc = kc / 256 * 256;
     if (kc < 256) kc = 256;
     if (kc > K) kc = K;
-    const size_t ws_bytes = packed_ws_bytes(M, N, (int)kc);
+    const size_t ws_bytes = packed_ws_bytes_t<T>(M, N, (int)kc);
     void* scratch = nullptr;
     SMX_TRY(scratch_alloc(&scratch, ws_bytes + 256, s));
     struct FreeOnExit {
@@ -585,15 +615,11 @@ inline int semiring_gemm_packed_public(const T* A, const T* B, T* C, int M, int 
     const int anti = kind == SMX_ANTI;
     const int* certp = nullptr;
     // (u8 needs no certificate: every u8 tile is the 1-instruction form)
-    if (!Lane<T>::kOneInstr && bounded_fastpath_enabled() && K > 0) {
-        cudaError_t e = cudaMemsetAsync(cert, 0xFF, sizeof(int), s);
-        if (e != cudaSuccess) return (int)e;
-        const int blocks = 4 * sm_count();
-        cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(A), M, K, lda, anti, cert);
-        SMX_LAUNCHED_OR_RETURN();
-        cert_u16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(B), K, N, ldb, anti, cert);
-        SMX_LAUNCHED_OR_RETURN();
-        certp = cert;
+    if constexpr (!Lane<T>::kOneInstr) {
+        if (bounded_fastpath_enabled() && K > 0) {
+            SMX_TRY(run_cert<T>(A, M, K, lda, B, K, N, ldb, anti, cert, s));
+            certp = cert;
+        }
     }
     if (K == 0) return packed_run<T>(C, M, N, 0, ldc, kind, accumulate, 0, -1, 0, 0, ws, ws_bytes, s);
     for (long long k0 = 0; k0 < K; k0 += kc) {
