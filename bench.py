@@ -137,6 +137,30 @@ def cuda_time(fn, iters: int, warmup: int = 1):
     return s.elapsed_time(e) / 1e3 / iters
 
 
+def graph_time(fn, per: int = 20, iters: int = 20):
+    """Device time per call of `fn` with the host out of the loop: `per`
+    back-to-back calls captured into one CUDA graph, replayed `iters` times
+    between CUDA events on the capturing stream."""
+    import torch
+    g = torch.cuda.CUDAGraph()
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        fn()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(per):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(st)
+        for _ in range(iters):
+            g.replay()
+        e.record(st)
+        torch.cuda.synchronize()
+    return s.elapsed_time(e) / 1e3 / (iters * per)
+
+
 def measure_issue_peak():
     """Packed-integer issue rate of the semiring inner-loop SASS on every SM."""
     import ctypes
@@ -147,13 +171,13 @@ def measure_issue_peak():
     blocks, threads, iters = sms * 8, 256, 4000
     sink = torch.zeros(blocks * threads, dtype=torch.int32, device="cuda")
     out = {}
-    for one in (0, 1):
+    for one in (0, 1, 2):
         ipt = ctypes.c_longlong(0)
         fn = lambda: _native.check(lib.smx_int_issue_probe(  # noqa: E731
             sink.data_ptr(), blocks, threads, iters, one, ctypes.byref(ipt),
             _native.stream_ptr()), "probe")
         t = cuda_time(fn, 3, 1)
-        out["one" if one else "pair"] = blocks * threads * ipt.value / t
+        out[("pair", "one", "lop3")[one]] = blocks * threads * ipt.value / t
     return out, sms
 
 
@@ -757,9 +781,15 @@ def secondary(dev):
         f = lambda: _native.check(lib.smx_bool_gemm_i8(  # noqa: E731
             A.data_ptr(), Bt.data_ptr(), None, o.data_ptr(), n_tc, n_tc, n_tc, n_tc, n_tc, n_tc // 32, 0,
             _native.stream_ptr(dev)), "tc")
-        t = cuda_time(f, 20 if n_tc <= 4096 else 5, 2)
+        te = cuda_time(f, 20 if n_tc <= 4096 else 5, 2)
+        # device rate: back-to-back launches in one graph (an eager Python
+        # loop of launches is host-bound at this size: ~5 us per launch)
+        t = graph_time(f, 20 if n_tc <= 4096 else 3, 20 if n_tc <= 4096 else 2)
         tc[f"n{n_tc}"] = {"kernel_us": t * 1e6, "ops_per_s": 2 * n_tc ** 3 / t,
-                          "frac_of_int8_peak": 2 * n_tc ** 3 / t / int8_peak}
+                          "frac_of_int8_peak": 2 * n_tc ** 3 / t / int8_peak,
+                          "eager_launch_us": te * 1e6}
+    tc["kernel"] = ("bool_i8_gemm_pair_kernel (split-K CTA pair) at 1024, bool_i8_gemm_kernel<256> at 8192; "
+                    "kernel_us = device time per launch, back-to-back launches replayed from one CUDA graph")
     out["bool_tc_gemm_kernel"] = tc
     cfg = workloads.CONFIGS["c2_bool_warshall"]
     (t2,) = workloads.make_inputs(cfg)
@@ -767,7 +797,14 @@ def secondary(dev):
     for eng in ("bool_closure_tc", "bool_closure_bits"):
         fn = getattr(engines, eng)
         t = cuda_time(lambda: fn(m2), 10, 2)
-        out[f"c2_{eng}"] = {"n": cfg.n, "seconds": t, "cells_per_s": cfg.n ** 3 / t}
+        out[f"c2_{eng}"] = {"n": cfg.n, "seconds": t, "cells_per_s": cfg.n ** 3 / t,
+                            "frac_of_int8_tc_peak": 2 * cfg.n ** 3 / t / int8_peak}
+    # the bit path's own ceiling: one LOP3.LUT (OR of AND on a 32-bit word)
+    # per 32 cell-updates at the measured LOP3 issue rate
+    bits = out["c2_bool_closure_bits"]
+    bits["bit_alu_ceiling_cells_per_s"] = 32 * peaks["lop3"]
+    bits["frac_of_bit_alu_ceiling"] = bits["cells_per_s"] / (32 * peaks["lop3"])
+    bits["lop3_issue_per_s"] = peaks["lop3"]
     return out
 
 

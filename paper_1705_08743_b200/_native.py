@@ -76,6 +76,7 @@ _SIGS.update({
 })
 _SIGS.update({
     "smx_set_tc_tile_n": ([c_int], c_int),
+    "smx_set_tc_pair": ([c_int], c_int),
     "smx_tc_trace_arm": ([c_void_p], c_int),
     "smx_lane_op": ([c_void_p] * 3 + [c_longlong, c_int, c_int, c_void_p], c_int),
     "smx_lanes_from_bits": ([c_void_p, c_int, c_void_p] + [c_int] * 4 + [c_void_p], c_int),

@@ -115,6 +115,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// 32 lanes x 64 columns in one tcgen05.ld, with its wait in the same asm
+// statement (so no use of the registers can be scheduled before it).
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+        : "r"(taddr)
+        : "memory");
+}
+
 struct TcArgs {
     uint8_t* C;          // bytes output (or nullptr)
     uint32_t* Cbits;     // packed output (or nullptr)
@@ -292,6 +304,204 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     }
 }
 
+// ---- split-K pair (small packed-bit products: C1) ------------------------------
+//
+// C1 (1024^3) has 128 output tiles of 128 x 64 in the kernel above: one per
+// SM, each streaming 192 KB of operands for only 8 k-blocks, so the product
+// is bound by the L2 -> SM operand stream (profiles/r02_tc_phases_c1.json:
+// ~49 B/clk per SM, 3900 of the CTA's 6700 cycles), not by the tensor
+// cores.  Here a cluster of two CTAs shares one 128 x 128 output tile and
+// splits K in halves: each CTA streams (128 + 128) x K/2 bytes (128 KB at
+// C1), and the whole product reads 16 MB instead of 24.
+//
+// Merge.  A partial count > 0 already proves the output bit (OR is
+// idempotent), so each CTA thresholds its own half-K counts to bits and the
+// pair only exchanges 1 KB of words: CTA r owns rows [64r, 64r + 64) of the
+// tile and receives the partner's words of those rows by st.async into its
+// shared memory (completing on a local mbarrier: no polling, no second
+// barrier round trip), ORs them into its own and stores.  Eight warps run the
+// epilogue: warps w and w + 4 read the same TMEM lanes (32 rows), columns
+// [0, 64) and [64, 128).
+constexpr int kPairBN = 128;
+constexpr int kPairThreads = 256;
+constexpr int kPairStages = 6;                         // 6 x 32 KB ring
+constexpr uint32_t kPairRecvBytes = 64 * (kPairBN / 32) * 4;   // 64 rows x 4 words
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_v2(uint32_t remote, uint32_t a, uint32_t b, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];"
+                 ::"r"(remote), "r"(a), "r"(b), "r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ uint32_t bits_of(const uint32_t (&r)[32]) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) word |= (r[j] != 0u ? 1u : 0u) << j;
+    return word;
+}
+
+__global__ void __launch_bounds__(kPairThreads, 1)
+bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                         const TcArgs p) {
+    constexpr uint32_t A_BYTES = kTcBM * kTcBK;
+    constexpr uint32_t B_BYTES = kPairBN * kTcBK;
+    extern __shared__ __align__(1024) uint8_t smem_dyn[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kPairStages * A_BYTES;
+    uint32_t* recv = reinterpret_cast<uint32_t*>(sB + kPairStages * B_BYTES);   // [64][4] partner words
+    uint64_t* full = reinterpret_cast<uint64_t*>(recv + kPairRecvBytes / 4);
+    uint64_t* empty = full + kPairStages;
+    uint64_t* accum = empty + kPairStages;
+    uint64_t* recv_bar = accum + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const bool tr0 = p.trace && cta == 0;
+    if (p.trace && threadIdx.x == 0) p.trace[16 + 2 * cta] = gtimer();
+    if (tr0 && threadIdx.x == 0) p.trace[0] = clock64();
+    const int m0 = blockIdx.y * kTcBM, n0 = blockIdx.x * kPairBN;
+    const int nkb_all = (p.K + kTcBK - 1) / kTcBK;
+    const int half = (nkb_all + 1) / 2;
+    const int kb_lo = (int)rank * half;
+    const int kb_hi = min(nkb_all, kb_lo + half);
+    const int nkb = kb_hi > kb_lo ? kb_hi - kb_lo : 0;
+
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+        for (int s = 0; s < kPairStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accum, 1);
+        mbar_init(recv_bar, 1);
+        // the partner's 1 KB lands on recv_bar: expected before the cluster
+        // barrier below, so no complete_tx can precede it
+        mbar_expect_tx(recv_bar, kPairRecvBytes);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (tr0) p.trace[10] = clock64();
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)), "n"(kPairBN) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if (tr0 && lane == 0) p.trace[11] = clock64();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // publish the initialised barriers to the partner (waited on before the
+    // first remote store, long after).  Relaxed: thread 0's
+    // fence.mbarrier_init.release.cluster already orders the inits, and a
+    // release arrive costs ~500 cycles of memory fence here.
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    if (tr0 && threadIdx.x == 0) p.trace[1] = clock64();
+
+    if (threadIdx.x == 0) {
+        // ---- TMA producer (PDL: operands are read only after the preceding
+        // unpack kernel completes; a no-op without the attribute)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % kPairStages;
+            const uint32_t ph = (kb / kPairStages) & 1;
+            mbar_wait(&empty[s], ph ^ 1);
+            mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+            tma_load_2d(&mapA, &full[s], sA + s * A_BYTES, (kb_lo + kb) * kTcBK, m0);
+            tma_load_2d(&mapB, &full[s], sB + s * B_BYTES, (kb_lo + kb) * kTcBK, n0);
+        }
+        if (tr0) p.trace[2] = clock64();
+    } else if (threadIdx.x == 32) {
+        // ---- MMA issuer ----
+        constexpr uint32_t idesc = idesc_i8<kPairBN>();
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % kPairStages;
+            const uint32_t ph = (kb / kPairStages) & 1;
+            mbar_wait(&full[s], ph);
+            if (tr0 && (kb == 0 || kb == nkb - 1)) p.trace[kb == 0 ? 3 : 4] = clock64();
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+            for (int k = 0; k < kTcBK / 32; ++k)
+                umma_i8(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
+                        (kb | k) != 0);
+            umma_commit(&empty[s]);
+        }
+        umma_commit(accum);
+    }
+    __syncwarp();
+
+    // ---- epilogue: this half's counts -> bits ----
+    mbar_wait(accum, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tr0 && threadIdx.x == 0) p.trace[5] = clock64();
+    const int quad = warp & 3, chalf = warp >> 2;          // TMEM lanes 32*quad.., columns 64*chalf..
+    const int trow = quad * 32 + lane;                      // row within the tile
+    const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(chalf * 64);
+    uint32_t w0 = 0, w1 = 0;
+    {
+        uint32_t r[64];
+        tmem_ld64(taddr, r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            w0 |= (r[j] != 0u ? 1u : 0u) << j;
+            w1 |= (r[32 + j] != 0u ? 1u : 0u) << j;
+        }
+    }
+    if (nkb == 0) w0 = w1 = 0u;   // (K shorter than one k-block per CTA: TMEM was never written)
+    if (tr0 && threadIdx.x == 0) p.trace[8] = clock64();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    // rows owned by the partner go to it; words [row][2*chalf, 2*chalf + 1]
+    const uint32_t owner = (uint32_t)(trow >> 6);
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (tr0 && threadIdx.x == 0) p.trace[9] = clock64();
+    if (owner != rank) {
+        const uint32_t off = (uint32_t)(((trow & 63) * 4 + 2 * chalf) * 4);
+        st_async_v2(mapa_shared(smem_u32(recv) + off, owner), w0, w1, mapa_shared(smem_u32(recv_bar), owner));
+    }
+    // No second cluster barrier: every store into this CTA's shared memory
+    // completes on recv_bar, which the owner threads wait on before the CTA
+    // can exit, and this CTA stores into the partner only (the partner
+    // waits on its own recv_bar likewise).
+    if (tr0 && threadIdx.x == 0) p.trace[6] = clock64();
+    if (owner == rank) {
+        mbar_wait(recv_bar, 0);
+        const uint2 o = *reinterpret_cast<const uint2*>(&recv[(trow & 63) * 4 + 2 * chalf]);
+        w0 |= o.x;
+        w1 |= o.y;
+        const int row = m0 + trow, col0 = n0 + chalf * 64;
+        if (row < p.M && col0 < p.N) {
+            uint32_t* dst = p.Cbits + (long long)row * p.ldc + (col0 >> 5);
+            const int left = p.N - col0;
+            if (left < 32) w0 &= (1u << left) - 1u;
+            if (left < 64 && left > 32) w1 &= (1u << (left - 32)) - 1u;
+            if (p.accumulate) {
+                dst[0] |= w0;
+                if (left > 32) dst[1] |= w1;
+            } else {
+                dst[0] = w0;
+                if (left > 32) dst[1] = w1;
+            }
+        }
+    }
+    __syncthreads();
+    if (tr0 && threadIdx.x == 0) p.trace[7] = clock64();
+    if (p.trace && threadIdx.x == 0) p.trace[17 + 2 * cta] = gtimer();
+    if (warp == 2)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kPairBN) : "memory");
+}
+
 // ---- host side ---------------------------------------------------------------
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -380,10 +590,47 @@ static int launch_tc(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long 
 }
 
 
+// Split-K pair launch (packed-bit output, no row skip).  The caller has
+// checked the shape (see bool_i8_gemm).
+static int launch_tc_pair(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long long lda, long long ldbt,
+                          cudaStream_t s, bool pdl) {
+    CUtensorMap mA, mB;
+    SMX_TRY(make_map(&mA, A, a.M, a.K, lda, kTcBM));
+    SMX_TRY(make_map(&mB, Bt, a.N, a.K, ldbt, kPairBN));
+    constexpr size_t smem = 1024 + kPairStages * (size_t)(kTcBM + kPairBN) * kTcBK + kPairRecvBytes +
+                            8 * (2 * kPairStages + 2) + 16;
+    auto kern = bool_i8_gemm_pair_kernel;
+    SMX_TRY(set_max_smem((const void*)kern, smem));
+    TcArgs args = a;
+    args.splits = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ceil_div(a.N, kPairBN), ceil_div(a.M, kTcBM), 2);
+    cfg.blockDim = dim3(kPairThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 2;
+    int na = 1;
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    count_launch();
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mB, args);
+    return e == cudaSuccess ? SMX_OK : (int)e;
+}
+
 // Output tile width of smx_bool_gemm_i8: 0 = automatic (the widest tile that
 // still gives every SM a tile), or force 64 / 128 / 256 (tuning switch;
 // results are identical).
 static int g_tc_tile_n = 0;
+static int g_tc_pair = 1;
 static unsigned long long* g_tc_trace = nullptr;
 
 int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbits, int M, int N, int K,
@@ -401,6 +648,14 @@ int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbit
         a.skip_tiles = ceil_div(skip_rows, kTcBM);
         const int total = ceil_div(M, kTcBM);
         if (a.skip_tile0 + a.skip_tiles > total) a.skip_tiles = total - a.skip_tile0;
+    }
+    // small packed-bit products (C1): split K across a CTA pair when one
+    // wave of 128 x 64 tiles or fewer covers the output (smx_set_tc_pair:
+    // 0 = off, 1 = automatic, 2 = always when the shape allows it)
+    if (Cbits && skip_rows == 0 && g_tc_pair != 0 && K > kTcBK) {
+        const long long tiles64 = (long long)ceil_div(M, kTcBM) * ceil_div(N, 64);
+        if (g_tc_pair == 2 || (tiles64 <= 148 && g_tc_tile_n == 0))
+            return launch_tc_pair(A, Bt, a, lda, ldbt, s, pdl);
     }
     if (g_tc_tile_n == 64) return launch_tc<64>(A, Bt, a, lda, ldbt, s, pdl);
     if (g_tc_tile_n == 128) return launch_tc<128>(A, Bt, a, lda, ldbt, s, pdl);
@@ -594,6 +849,13 @@ int smx_bool_mul_tc(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, in
 int smx_tc_trace_arm(unsigned long long* buf) {
     g_tc_trace = buf;
     return SMX_OK;
+}
+
+int smx_set_tc_pair(int mode) {
+    if (mode < 0 || mode > 2) return SMX_E_ARG;
+    const int old = g_tc_pair;
+    g_tc_pair = mode;
+    return old;
 }
 
 int smx_set_tc_tile_n(int bn) {

@@ -170,39 +170,26 @@ fw_pivot_kernel(T* P, int b, long long ld, int anti) {
 // thread may already have lowered reads the weight of a real walk of the
 // same kind (the fw_pivot_and_row_panel argument), so any interleaving gives
 // the same bits.
-template <typename T>
-__global__ void __launch_bounds__(512, 3)
-fw_pivot_blocked_kernel(T* P, int b, long long ld, int anti) {
+// Sub-block sweep of fw_pivot_blocked_kernel.  BD: every lane of the tile
+// is < 2^15 (voted once after the load), so a + b <= 65534 < S and the
+// clamp is a no-op: the 1-instruction update L::step_bounded replaces the
+// general 2-instruction form.  Values only decrease during the closure, so
+// the bound holds to the end.  After the first few rounds of a closure the
+// pivot tiles are almost always bounded.
+template <typename T, bool BD>
+__device__ __forceinline__ void pivot_blocked_sweep(uint32_t* tile, uint32_t* As, int b) {
     using L = Lane<T>;
-    static_assert(L::kCellsPerWord == 2, "u8 / u16 lanes");
-    constexpr int WPR = 64;                 // words per tile row (128 cells)
-    constexpr int APITCH = 34;              // splat rows: 32 k + 2 (no bank conflicts between row slots)
-    __shared__ __align__(16) uint32_t tile[128 * WPR];
-    __shared__ __align__(16) uint32_t As[96 * APITCH];   // P3's A operand, splat, per row slot
+    constexpr int WPR = 64;
+    constexpr int APITCH = 34;
     const int tid = threadIdx.x;
-    auto to_dist = [&](uint32_t v) { return anti ? (L::kS - v) : v; };
     auto cell = [&](int r, int c) {         // one cell of the tile
         const uint32_t w = tile[r * WPR + (c >> 1)];
         return (c & 1) ? (w >> 16) : (w & 0xFFFFu);
     };
-    // 8 global loads of a thread in flight at a time, then their tile stores
-    for (int i0 = 0; i0 < 128 * WPR / 512; i0 += 4) {
-        uint32_t v[8];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int w = tid + (i0 + i) * 512, r = w / WPR, c = (w % WPR) * 2;
-            v[2 * i] = (r < b && c < b) ? (uint32_t)P[(long long)r * ld + c] : 0u;
-            v[2 * i + 1] = (r < b && c + 1 < b) ? (uint32_t)P[(long long)r * ld + c + 1] : 0u;
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int w = tid + (i0 + i) * 512, r = w / WPR, c = (w % WPR) * 2;
-            const uint32_t v0 = (r < b && c < b) ? to_dist(v[2 * i]) : L::kS;
-            const uint32_t v1 = (r < b && c + 1 < b) ? to_dist(v[2 * i + 1]) : L::kS;
-            tile[w] = v0 | (v1 << 16);
-        }
-    }
-    __syncthreads();
+    auto upd = [](uint32_t c, uint32_t bw, uint32_t a, uint32_t sa) {
+        if constexpr (BD) return L::step_bounded(c, bw, a);
+        else return L::step(c, bw, a, sa);
+    };
     const int nsb = (b + 31) / 32;
     const int g = tid >> 4, q = tid & 15;   // 32 row slots x 16 word slots
     for (int kb = 0; kb < nsb; ++kb) {
@@ -224,7 +211,7 @@ fw_pivot_blocked_kernel(T* P, int b, long long ld, int anti) {
                 const uint32_t e = (w[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
                 const uint32_t a = L::splat(e), sa = L::splat(L::kS - e);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) w[i] = L::step(w[i], __shfl_sync(0xFFFFFFFFu, w[i], k), a, sa);
+                for (int i = 0; i < 16; ++i) w[i] = upd(w[i], __shfl_sync(0xFFFFFFFFu, w[i], k), a, sa);
             }
             uint4* dst = reinterpret_cast<uint4*>(&tile[(K0 + tid) * WPR + KW0]);
 #pragma unroll
@@ -240,10 +227,10 @@ fw_pivot_blocked_kernel(T* P, int b, long long ld, int anti) {
                 const uint32_t e = cell(K0 + g, K0 + k);
                 const uint32_t a = L::splat(e), sa = L::splat(L::kS - e);
                 const uint4 bw = *reinterpret_cast<const uint4*>(&tile[(K0 + k) * WPR + 4 * q]);
-                acc.x = L::step(acc.x, bw.x, a, sa);
-                acc.y = L::step(acc.y, bw.y, a, sa);
-                acc.z = L::step(acc.z, bw.z, a, sa);
-                acc.w = L::step(acc.w, bw.w, a, sa);
+                acc.x = upd(acc.x, bw.x, a, sa);
+                acc.y = upd(acc.y, bw.y, a, sa);
+                acc.z = upd(acc.z, bw.z, a, sa);
+                acc.w = upd(acc.w, bw.w, a, sa);
             }
             *rw = acc;
         }
@@ -276,10 +263,10 @@ fw_pivot_blocked_kernel(T* P, int b, long long ld, int anti) {
                     const uint2 av = *reinterpret_cast<const uint2*>(&As[(3 * g + i) * APITCH + 2 * kk]);
                     const uint32_t a0 = av.x, s0 = L::kIdentityWord - av.x;   // splat(S - e)
                     const uint32_t a1 = av.y, s1 = L::kIdentityWord - av.y;
-                    acc[i].x = L::step(L::step(acc[i].x, b0.x, a0, s0), b1.x, a1, s1);
-                    acc[i].y = L::step(L::step(acc[i].y, b0.y, a0, s0), b1.y, a1, s1);
-                    acc[i].z = L::step(L::step(acc[i].z, b0.z, a0, s0), b1.z, a1, s1);
-                    acc[i].w = L::step(L::step(acc[i].w, b0.w, a0, s0), b1.w, a1, s1);
+                    acc[i].x = upd(upd(acc[i].x, b0.x, a0, s0), b1.x, a1, s1);
+                    acc[i].y = upd(upd(acc[i].y, b0.y, a0, s0), b1.y, a1, s1);
+                    acc[i].z = upd(upd(acc[i].z, b0.z, a0, s0), b1.z, a1, s1);
+                    acc[i].w = upd(upd(acc[i].w, b0.w, a0, s0), b1.w, a1, s1);
                 }
             }
             if (live) {
@@ -290,6 +277,42 @@ fw_pivot_blocked_kernel(T* P, int b, long long ld, int anti) {
         }
         __syncthreads();
     }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512, 3)
+fw_pivot_blocked_kernel(T* P, int b, long long ld, int anti, int allow_bounded) {
+    using L = Lane<T>;
+    static_assert(L::kCellsPerWord == 2, "u8 / u16 lanes");
+    constexpr int WPR = 64;                 // words per tile row (128 cells)
+    constexpr int APITCH = 34;              // splat rows: 32 k + 2 (no bank conflicts between row slots)
+    __shared__ __align__(16) uint32_t tile[128 * WPR];
+    __shared__ __align__(16) uint32_t As[96 * APITCH];   // P3's A operand, splat, per row slot
+    const int tid = threadIdx.x;
+    auto to_dist = [&](uint32_t v) { return anti ? (L::kS - v) : v; };
+    // 8 global loads of a thread in flight at a time, then their tile stores
+    uint32_t high = 0;                      // OR of the stored words: the bounded vote
+    for (int i0 = 0; i0 < 128 * WPR / 512; i0 += 4) {
+        uint32_t v[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int w = tid + (i0 + i) * 512, r = w / WPR, c = (w % WPR) * 2;
+            v[2 * i] = (r < b && c < b) ? (uint32_t)P[(long long)r * ld + c] : 0u;
+            v[2 * i + 1] = (r < b && c + 1 < b) ? (uint32_t)P[(long long)r * ld + c + 1] : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int w = tid + (i0 + i) * 512, r = w / WPR, c = (w % WPR) * 2;
+            const uint32_t v0 = (r < b && c < b) ? to_dist(v[2 * i]) : L::kS;
+            const uint32_t v1 = (r < b && c + 1 < b) ? to_dist(v[2 * i + 1]) : L::kS;
+            tile[w] = v0 | (v1 << 16);
+            high |= tile[w];
+        }
+    }
+    // (padding is S, so a padded tile takes the general form)
+    const bool bd = __syncthreads_and((high & L::kHalfMask) == 0u) && allow_bounded && L::kHalfMask != 0u;
+    if (bd) pivot_blocked_sweep<T, true>(tile, As, b);
+    else pivot_blocked_sweep<T, false>(tile, As, b);
     for (int w = tid; w < 128 * WPR; w += 512) {
         const int r = w / WPR, c = (w % WPR) * 2;
         if (r >= b || c >= b) continue;
@@ -476,7 +499,7 @@ int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s, T* scratch) {
     if constexpr (sizeof(T) <= 2) {
         if (g_pivot_blocked.load(std::memory_order_relaxed)) {
             const cudaError_t e = launch_kernel(fw_pivot_blocked_kernel<T>, dim3(1), dim3(512), 0, s, P, b, ld,
-                                                kind == SMX_ANTI);
+                                                kind == SMX_ANTI, bounded_fastpath_enabled());
             return e == cudaSuccess ? SMX_OK : (int)e;
         }
     }

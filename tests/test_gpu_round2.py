@@ -51,13 +51,59 @@ def test_tc_tile_widths_match_oracle(shape, oracle_lib):
     want = oracle_lib.bool_mul(oracle_lib.pack_bits(a), oracle_lib.pack_bits(b), k)
     ma, mb = BoolMatrix.from_numpy(a), BoolMatrix.from_numpy(b)
     old = lib.smx_set_tc_tile_n(0)
+    old_pair = lib.smx_set_tc_pair(0)
     try:
         for bn in (0, 64, 128, 256):
             lib.smx_set_tc_tile_n(bn)
             np.testing.assert_array_equal((ma * mb).blocks, want, err_msg=f"tile {bn} {shape}")
+        lib.smx_set_tc_tile_n(0)
+        for mode in (1, 2):   # the split-K CTA pair (automatic / forced)
+            lib.smx_set_tc_pair(mode)
+            np.testing.assert_array_equal((ma * mb).blocks, want, err_msg=f"pair {mode} {shape}")
     finally:
         lib.smx_set_tc_tile_n(old)
+        lib.smx_set_tc_pair(old_pair)
     assert lib.smx_set_tc_tile_n(100) < 0
+    assert lib.smx_set_tc_pair(3) < 0
+
+
+@pytest.mark.parametrize("shape", [(1024, 1024, 1024), (1000, 777, 1001), (130, 100, 129), (256, 256, 3000),
+                                   (64, 2000, 384)])
+def test_tc_pair_kernel_bits_accumulate(shape, oracle_lib):
+    """smx_bool_gemm_i8 with packed-bit output on the split-K pair: plain and
+    OR-accumulating into a random output, ragged shapes, K with an odd number
+    of 128-byte k-blocks (the second CTA gets fewer) and K past the 6-stage
+    ring; every padding word past N stays as it was."""
+    m, n, k = shape
+    lib = _native.lib()
+    rng = np.random.default_rng(7 * m + n + k)
+    a = (rng.random((m, k)) < 0.03).astype(np.uint8)
+    b = (rng.random((k, n)) < 0.03).astype(np.uint8)
+    want = (a.astype(np.int64) @ b.astype(np.int64)) > 0
+    ld = ((k + 15) // 16) * 16
+    A = torch.zeros((m, ld), dtype=torch.uint8, device="cuda")
+    A[:, :k] = torch.from_numpy(a).cuda()
+    Bt = torch.zeros((n, ld), dtype=torch.uint8, device="cuda")
+    Bt[:, :k] = torch.from_numpy(np.ascontiguousarray(b.T)).cuda()
+    ldc = (n + 31) // 32 + 3
+    init = rng.integers(0, 2 ** 32, (m, ldc), dtype=np.uint64).astype(np.uint32)
+    old = lib.smx_set_tc_pair(2)
+    try:
+        for acc in (0, 1):
+            C = torch.from_numpy(init.view(np.int32).copy()).cuda()
+            _native.check(lib.smx_bool_gemm_i8(A.data_ptr(), Bt.data_ptr(), None, C.data_ptr(), m, n, k, ld, ld,
+                                               ldc, acc, _native.stream_ptr()), "tc pair")
+            got = C.cpu().numpy().view(np.uint32)
+            bits = np.unpackbits(got.view(np.uint8), axis=1, bitorder="little")[:, :n].astype(bool)
+            prev = np.unpackbits(init.view(np.uint8), axis=1, bitorder="little")[:, :n].astype(bool)
+            np.testing.assert_array_equal(bits, want | prev if acc else want, err_msg=f"acc={acc} {shape}")
+            nw = (n + 31) // 32
+            np.testing.assert_array_equal(got[:, nw:], init[:, nw:])
+            if n % 32:   # bits past N in the last word: zero (plain) or kept (accumulate)
+                tail = got[:, nw - 1] >> (n % 32)
+                np.testing.assert_array_equal(tail, (init[:, nw - 1] >> (n % 32)) if acc else 0)
+    finally:
+        lib.smx_set_tc_pair(old)
 
 
 # -- batched kernels at their limits ----------------------------------------------
@@ -196,3 +242,49 @@ def test_bool_warshall_persistent_matches_blocked_and_oracle(n, oracle_lib):
         np.testing.assert_array_equal(got[(1, "again")], got[0])
         if want is not None:
             np.testing.assert_array_equal(got[1], want)
+
+
+@pytest.mark.parametrize("w", [8, 16])
+def test_pivot_bounded_form_matches_oracle(w, oracle_lib):
+    """Pivot tiles whose lanes are all < 2^15 (in distance form) take the
+    1-instruction update inside the blocked 128 kernel (voted once at load);
+    tiles at the edge of that bound, tiles with one lane above it and the
+    forced general form all equal the oracle closure, anti and dist, on the
+    leaves and through the 2 x 2 recursion (b up to 512)."""
+    lib = _native.lib()
+    S = (1 << w) - 1
+    dt = NP[w]
+    rng = np.random.default_rng(90 + w)
+    hi = S if w == 8 else (1 << 15)
+    sizes = (32, 100, 128, 200, 256) + ((384, 512) if w == 16 else ())
+    for b in sizes:
+        for case in ("small", "edge", "one_high"):
+            for kind in ("anti", "dist"):
+                if case == "small":
+                    tile = rng.integers(0, 300 if w == 16 else 120, (b, b))
+                elif case == "edge":
+                    tile = rng.integers(hi - 400 if w == 16 else 100, hi, (b, b))
+                else:
+                    tile = rng.integers(0, 300 if w == 16 else 120, (b, b))
+                    tile[rng.integers(b), rng.integers(b)] = hi + 5 if w == 16 else 250
+                if kind == "anti":
+                    tile = S - tile
+                ld = ((b + 16 + 15) // 16) * 16
+                full = rng.integers(0, S + 1, (b + 4, ld)).astype(dt)
+                full[:b, :b] = tile.astype(dt)
+                pad = ((b + 15) // 16) * 16 if w == 8 else ((b + 7) // 8) * 8
+                t_or = np.full((b, pad), 0 if kind == "anti" else S, dt)
+                t_or[:, :b] = full[:b, :b]
+                want = oracle_lib.semiring_close(t_or, w, kind)[:, :b]
+                for fast in (1, 0):
+                    old = lib.smx_set_bounded_fastpath(fast)
+                    try:
+                        dev = torch.from_numpy(full.copy()).cuda()
+                        _native.check(lib.smx_fw_pivot(dev.data_ptr(), b, ld, w // 8, 0 if kind == "anti" else 1,
+                                                       _native.stream_ptr()), "pivot")
+                        got = dev.cpu().numpy()
+                    finally:
+                        lib.smx_set_bounded_fastpath(old)
+                    np.testing.assert_array_equal(got[:b, :b], want, err_msg=f"b={b} {case} {kind} fast={fast}")
+                    np.testing.assert_array_equal(got[b:], full[b:])
+                    np.testing.assert_array_equal(got[:b, b:], full[:b, b:])

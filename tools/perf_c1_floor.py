@@ -4,7 +4,7 @@ Back-to-back launches timed with CUDA events on the launching stream:
   null      torch.cuda._sleep(0): the launch floor of any kernel here
   int_mm    torch._int_mm (cuBLAS int8) at 1024^3: the library baseline
   tc        smx_bool_gemm_i8 (our tcgen05 kernel, bytes in, bits out), per
-            output tile width (bn0 = automatic)
+            output tile width (bn0 = automatic), and the split-K CTA pair
   tc_graph  the same, 20 launches per CUDA graph replay
   public    BoolMatrix.__mul__ (unpack + PDL kernel, graph replay)
 Prints one JSON object.
@@ -65,12 +65,16 @@ def main():
         _native.check(lib.smx_bool_gemm_i8(A.data_ptr(), Bt.data_ptr(), None, out.data_ptr(), n, n, n, n, n,
                                            n // 32, 0, _native.stream_ptr(dev)), "tc")
     old = lib.smx_set_tc_tile_n(0)
-    for bn in (0, 64, 128, 256):
+    old_pair = lib.smx_set_tc_pair(0)
+    for pair, bn in ((0, 0), (0, 64), (0, 128), (0, 256), (2, 0)):
+        lib.smx_set_tc_pair(pair)
         lib.smx_set_tc_tile_n(bn)
-        res[f"tc_bn{bn}_us"] = timeit(tc)
+        key = "tc_pair" if pair else f"tc_bn{bn}"
+        res[f"{key}_us"] = timeit(tc)
         f, per = graphed(tc)
-        res[f"tc_bn{bn}_graph_us"] = timeit(f, 50, 5) / per
+        res[f"{key}_graph_us"] = timeit(f, 50, 5) / per
     lib.smx_set_tc_tile_n(old)
+    lib.smx_set_tc_pair(old_pair)
     res["tc_us"], res["tc_graph_us"] = res["tc_bn0_us"], res["tc_bn0_graph_us"]
     if n == 1024:
         a, b = workloads.make_inputs(workloads.CONFIGS["c1_bool_mul"])
