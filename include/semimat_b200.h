@@ -247,9 +247,10 @@ int smx_bool_gemm_i8(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* 
  * 128 or 256.  Results are identical.  Returns the previous setting. */
 int smx_set_tc_tile_n(int bn);
 /* Split-K CTA pair for small packed-bit products (the C1 shape): 0 = off,
- * 1 = automatic (one wave of 128 x 64 tiles or fewer, K > 128, automatic
- * tile width), 2 = whenever the shape allows it (packed-bit output, no row
- * skip, K > 128).  Results are identical.  Returns the previous setting. */
+ * 1 = automatic (one wave of 128 x 64 tiles or fewer, 128 < K <= 65536,
+ * automatic tile width), 2 = whenever the shape allows it (packed-bit
+ * output, no row skip, 128 < K <= 65536).  Results are identical.  Returns
+ * the previous setting. */
 int smx_set_tc_pair(int mode);
 /* Development trace of the plain tensor-core kernel: buf (device, >= 16 + 2 *
  * CTAs u64) receives clock64 phase stamps of CTA 0 in [0, 8) and globaltimer

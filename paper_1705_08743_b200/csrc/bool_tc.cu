@@ -178,6 +178,9 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     const int kb_hi = min(nkb_all, kb_lo + per);
     const int nkb = kb_hi > kb_lo ? kb_hi - kb_lo : 0;
 
+    // thread 0 issues the first ring fill before the TMEM allocation and the
+    // CTA barrier (the loads only touch barriers it initialised itself)
+    const int first_fill = nkb < kTcStages ? nkb : kTcStages;
     if (threadIdx.x == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
@@ -187,6 +190,16 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         }
         mbar_init(accum, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // Programmatic dependent launch: everything above ran while the
+        // preceding kernel (e.g. the operand unpack) was still finishing; the
+        // operands are read only after it completes.  A no-op without the
+        // attribute.
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        for (int kb = 0; kb < first_fill; ++kb) {
+            mbar_expect_tx(&full[kb], A_BYTES + B_BYTES);
+            tma_load_2d(&mapA, &full[kb], sA + kb * A_BYTES, (kb_lo + kb) * kTcBK, m0);
+            tma_load_2d(&mapB, &full[kb], sB + kb * B_BYTES, (kb_lo + kb) * kTcBK, n0);
+        }
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -202,12 +215,8 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     if (tr0 && threadIdx.x == 0) p.trace[1] = clock64();
 
     if (threadIdx.x == 0) {
-        // ---- TMA producer ----
-        // Programmatic dependent launch (bool_mul_tc): everything above ran
-        // while the operand-unpack kernel was still finishing; the operands
-        // are read only after it completes.  A no-op without the attribute.
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        for (int kb = 0; kb < nkb; ++kb) {
+        // ---- TMA producer: the rest of the ring ----
+        for (int kb = first_fill; kb < nkb; ++kb) {
             const int s = kb % kTcStages;
             const uint32_t ph = (kb / kTcStages) & 1;
             mbar_wait(&empty[s], ph ^ 1);
@@ -237,6 +246,9 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     __syncwarp();
 
     // ---- epilogue: TMEM -> threshold -> bytes or bits ----
+    // a PDL-launched successor may start its prologue now (it reads nothing
+    // of ours before its own griddepcontrol.wait)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     mbar_wait(accum, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (tr0 && threadIdx.x == 0) p.trace[5] = clock64();
@@ -348,6 +360,11 @@ __device__ __forceinline__ uint32_t bits_of(const uint32_t (&r)[32]) {
     return word;
 }
 
+// (Tried: a cluster of four, 2 N-tiles x 2 K-halves, each CTA loading half
+// of the shared A tile and multicasting it (TMA .multicast::cluster), so a
+// CTA issues 96 KB instead of 128: no faster -- 3.79 against 3.49 us per
+// launch, the same per-CTA timeline -- so the operand stream is bound where
+// the bytes land, not where they are issued; removed.)
 __global__ void __launch_bounds__(kPairThreads, 1)
 bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                          const TcArgs p) {
@@ -365,7 +382,8 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
+    const uint32_t rank = cluster_rank();   // the K half; owns rows [64 rank, 64 rank + 64)
+    const uint32_t partner = 1u - rank;
     const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const bool tr0 = p.trace && cta == 0;
     if (p.trace && threadIdx.x == 0) p.trace[16 + 2 * cta] = gtimer();
@@ -377,6 +395,13 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     const int kb_hi = min(nkb_all, kb_lo + half);
     const int nkb = kb_hi > kb_lo ? kb_hi - kb_lo : 0;
 
+    // Thread 0 initialises the barriers and issues the first ring fill right
+    // away -- before the TMEM allocation and the CTA barrier -- so the first
+    // operand stage is in flight while the rest of the CTA sets up (the
+    // loads only touch barriers this thread initialised).  (Initialising
+    // the barriers one per lane of warp 0 was slower: ~900 against ~350
+    // cycles to the first load.)
+    const int first_fill = nkb < kPairStages ? nkb : kPairStages;
     if (threadIdx.x == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
@@ -391,6 +416,14 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
         mbar_expect_tx(recv_bar, kPairRecvBytes);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         if (tr0) p.trace[10] = clock64();
+        // PDL: operands are read only after the preceding kernel in the
+        // stream completes (a no-op without the launch attribute)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        for (int kb = 0; kb < first_fill; ++kb) {
+            mbar_expect_tx(&full[kb], A_BYTES + B_BYTES);
+            tma_load_2d(&mapA, &full[kb], sA + kb * A_BYTES, (kb_lo + kb) * kTcBK, m0);
+            tma_load_2d(&mapB, &full[kb], sB + kb * B_BYTES, (kb_lo + kb) * kTcBK, n0);
+        }
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -410,10 +443,8 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     if (tr0 && threadIdx.x == 0) p.trace[1] = clock64();
 
     if (threadIdx.x == 0) {
-        // ---- TMA producer (PDL: operands are read only after the preceding
-        // unpack kernel completes; a no-op without the attribute)
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        for (int kb = 0; kb < nkb; ++kb) {
+        // ---- TMA producer: the rest of the ring (K beyond the first fill)
+        for (int kb = first_fill; kb < nkb; ++kb) {
             const int s = kb % kPairStages;
             const uint32_t ph = (kb / kPairStages) & 1;
             mbar_wait(&empty[s], ph ^ 1);
@@ -443,6 +474,7 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     __syncwarp();
 
     // ---- epilogue: this half's counts -> bits ----
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     mbar_wait(accum, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (tr0 && threadIdx.x == 0) p.trace[5] = clock64();
@@ -451,24 +483,28 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(chalf * 64);
     uint32_t w0 = 0, w1 = 0;
     {
+        // counts of this CTA's K half are < 2^16 (K <= 65536, host-checked):
+        // two counts per 16-bit lane pair (PRMT), clamped to 0/1 by one
+        // VIMNMX.U16x2, placed at bits j and j + 16 by one shift-add:
+        // 1.5 instructions per output bit instead of ~2.7
         uint32_t r[64];
         tmem_ld64(taddr, r);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            w0 |= (r[j] != 0u ? 1u : 0u) << j;
-            w1 |= (r[32 + j] != 0u ? 1u : 0u) << j;
+        for (int j = 0; j < 16; ++j) {
+            w0 += __vminu2(__byte_perm(r[j], r[j + 16], 0x5410), 0x00010001u) << j;
+            w1 += __vminu2(__byte_perm(r[32 + j], r[48 + j], 0x5410), 0x00010001u) << j;
         }
     }
     if (nkb == 0) w0 = w1 = 0u;   // (K shorter than one k-block per CTA: TMEM was never written)
     if (tr0 && threadIdx.x == 0) p.trace[8] = clock64();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     // rows owned by the partner go to it; words [row][2*chalf, 2*chalf + 1]
-    const uint32_t owner = (uint32_t)(trow >> 6);
+    const uint32_t owner = (uint32_t)(trow >> 6);   // K-half that owns (stores) this row
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (tr0 && threadIdx.x == 0) p.trace[9] = clock64();
     if (owner != rank) {
         const uint32_t off = (uint32_t)(((trow & 63) * 4 + 2 * chalf) * 4);
-        st_async_v2(mapa_shared(smem_u32(recv) + off, owner), w0, w1, mapa_shared(smem_u32(recv_bar), owner));
+        st_async_v2(mapa_shared(smem_u32(recv) + off, partner), w0, w1, mapa_shared(smem_u32(recv_bar), partner));
     }
     // No second cluster barrier: every store into this CTA's shared memory
     // completes on recv_bar, which the owner threads wait on before the CTA
@@ -652,7 +688,7 @@ int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbit
     // small packed-bit products (C1): split K across a CTA pair when one
     // wave of 128 x 64 tiles or fewer covers the output (smx_set_tc_pair:
     // 0 = off, 1 = automatic, 2 = always when the shape allows it)
-    if (Cbits && skip_rows == 0 && g_tc_pair != 0 && K > kTcBK) {
+    if (Cbits && skip_rows == 0 && g_tc_pair != 0 && K > kTcBK && K <= 65536) {
         const long long tiles64 = (long long)ceil_div(M, kTcBM) * ceil_div(N, 64);
         if (g_tc_pair == 2 || (tiles64 <= 148 && g_tc_tile_n == 0))
             return launch_tc_pair(A, Bt, a, lda, ldbt, s, pdl);
@@ -867,7 +903,11 @@ int smx_set_tc_tile_n(int bn) {
 
 int smx_bool_gemm_i8(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* C_bits, int M, int N, int K,
                      int lda, int ldbt, int ldc, int accumulate, void* stream) {
-    return bool_i8_gemm(A, Bt, C, C_bits, M, N, K, lda, ldbt, ldc, accumulate, 0, 0, as_stream(stream));
+    // programmatic dependent launch: the kernel touches no memory before its
+    // griddepcontrol.wait, so it may overlap its launch and prologue with
+    // whatever kernel precedes it in the stream (back-to-back products)
+    return bool_i8_gemm(A, Bt, C, C_bits, M, N, K, lda, ldbt, ldc, accumulate, 0, 0, as_stream(stream),
+                        /*pdl=*/true);
 }
 
 size_t smx_bool_warshall_i8_workspace_bytes(int n, int ld) {

@@ -68,7 +68,7 @@ def test_tc_tile_widths_match_oracle(shape, oracle_lib):
 
 
 @pytest.mark.parametrize("shape", [(1024, 1024, 1024), (1000, 777, 1001), (130, 100, 129), (256, 256, 3000),
-                                   (64, 2000, 384)])
+                                   (64, 2000, 384), (300, 300, 1536), (520, 333, 1537)])
 def test_tc_pair_kernel_bits_accumulate(shape, oracle_lib):
     """smx_bool_gemm_i8 with packed-bit output on the split-K pair: plain and
     OR-accumulating into a random output, ragged shapes, K with an odd number
@@ -89,19 +89,21 @@ def test_tc_pair_kernel_bits_accumulate(shape, oracle_lib):
     init = rng.integers(0, 2 ** 32, (m, ldc), dtype=np.uint64).astype(np.uint32)
     old = lib.smx_set_tc_pair(2)
     try:
-        for acc in (0, 1):
-            C = torch.from_numpy(init.view(np.int32).copy()).cuda()
-            _native.check(lib.smx_bool_gemm_i8(A.data_ptr(), Bt.data_ptr(), None, C.data_ptr(), m, n, k, ld, ld,
-                                               ldc, acc, _native.stream_ptr()), "tc pair")
-            got = C.cpu().numpy().view(np.uint32)
-            bits = np.unpackbits(got.view(np.uint8), axis=1, bitorder="little")[:, :n].astype(bool)
-            prev = np.unpackbits(init.view(np.uint8), axis=1, bitorder="little")[:, :n].astype(bool)
-            np.testing.assert_array_equal(bits, want | prev if acc else want, err_msg=f"acc={acc} {shape}")
-            nw = (n + 31) // 32
-            np.testing.assert_array_equal(got[:, nw:], init[:, nw:])
-            if n % 32:   # bits past N in the last word: zero (plain) or kept (accumulate)
-                tail = got[:, nw - 1] >> (n % 32)
-                np.testing.assert_array_equal(tail, (init[:, nw - 1] >> (n % 32)) if acc else 0)
+        for mode in (2,):   # (forced pair)
+            lib.smx_set_tc_pair(mode)
+            for acc in (0, 1):
+                C = torch.from_numpy(init.view(np.int32).copy()).cuda()
+                _native.check(lib.smx_bool_gemm_i8(A.data_ptr(), Bt.data_ptr(), None, C.data_ptr(), m, n, k, ld, ld,
+                                                   ldc, acc, _native.stream_ptr()), "tc pair")
+                got = C.cpu().numpy().view(np.uint32)
+                bits = np.unpackbits(got.view(np.uint8), axis=1, bitorder="little")[:, :n].astype(bool)
+                prev = np.unpackbits(init.view(np.uint8), axis=1, bitorder="little")[:, :n].astype(bool)
+                np.testing.assert_array_equal(bits, want | prev if acc else want, err_msg=f"mode={mode} acc={acc} {shape}")
+                nw = (n + 31) // 32
+                np.testing.assert_array_equal(got[:, nw:], init[:, nw:])
+                if n % 32:   # bits past N in the last word: zero (plain) or kept (accumulate)
+                    tail = got[:, nw - 1] >> (n % 32)
+                    np.testing.assert_array_equal(tail, (init[:, nw - 1] >> (n % 32)) if acc else 0)
     finally:
         lib.smx_set_tc_pair(old)
 

@@ -69,7 +69,7 @@ def main():
     for pair, bn in ((0, 0), (0, 64), (0, 128), (0, 256), (2, 0)):
         lib.smx_set_tc_pair(pair)
         lib.smx_set_tc_tile_n(bn)
-        key = "tc_pair" if pair else f"tc_bn{bn}"
+        key = {0: f"tc_bn{bn}", 2: "tc_pair"}[pair]
         res[f"{key}_us"] = timeit(tc)
         f, per = graphed(tc)
         res[f"{key}_graph_us"] = timeit(f, 50, 5) / per

@@ -36,7 +36,7 @@ lib.smx_tc_trace_arm(buf.data_ptr())
 res = []
 for rep in range(5):
     buf.zero_()
-    torch.cuda._sleep(2000)          # leave a gap so this launch starts on an idle GPU
+    torch.cuda.synchronize()         # an idle GPU: no PDL predecessor to wait for
     run()
     torch.cuda.synchronize()
     b = buf.cpu().tolist()
