@@ -68,9 +68,19 @@ def _from_edges(cls, dim: int, edges, width: int):
 
 
 class _LaneMatrix:
-    """Shared storage and entrywise algebra of the two saturated matrix types."""
+    """Shared storage and entrywise algebra of the two saturated matrix types.
 
-    __slots__ = ("rows", "cols", "width", "_data")
+    Storage lives in HBM (``_dev``, a CUDA tensor).  A matrix built from a
+    host array is *host-backed* until its first device operation, like the
+    reference's ``_data`` (antidist.py:46-51), which is the caller's array
+    itself: ``.data`` is then a read-only view of that array (no copy), and
+    ``transitive_closure()`` runs the host-buffer closure (smx_fw_host_*: the
+    rows stream in through page-locked staging while the closure runs, the
+    finished rows stream out) into page-locked memory, returning a
+    host-backed result.  Any other device use moves the array to HBM once.
+    """
+
+    __slots__ = ("rows", "cols", "width", "_dev", "_host", "_device")
 
     _PAD_IS_LIMIT = False
 
@@ -82,14 +92,16 @@ class _LaneMatrix:
         self.rows = rows
         self.cols = cols
         self.width = width
+        self._dev = self._host = None
         if isinstance(_data, torch.Tensor):
             if tuple(_data.shape) != (rows, padded) or _data.dtype != _TORCH[width]:
                 raise ValueError("backing array does not match the padded shape")
             if _data.device.type != "cuda":
                 _data = _data.to(_native.require_cuda(device))
-            self._data = _data.contiguous()
+            self._dev = _data.contiguous()
+            self._device = self._dev.device
             return
-        dev = _native.require_cuda(device)
+        self._device = _native.require_cuda(device)
         if _data is None:
             fill = self._pad_fill(width)
             host = np.full((rows, padded), fill, dtype=_NP[width])
@@ -97,7 +109,29 @@ class _LaneMatrix:
             host = np.asarray(_data)
             if host.shape != (rows, padded) or host.dtype != _NP[width]:
                 raise ValueError("backing array does not match the padded shape")
-        self._data = torch.from_numpy(np.ascontiguousarray(host)).to(dev)
+        self._host = host
+
+    @property
+    def _data(self) -> torch.Tensor:
+        """The device storage (moves a host-backed matrix to HBM first)."""
+        if self._dev is None:
+            src = np.ascontiguousarray(self._host)
+            if not src.flags.writeable:   # (torch.from_numpy wants a writeable array; only read here)
+                src = src.copy()
+            self._dev = torch.from_numpy(src).to(self._device)
+            self._host = None
+        return self._dev
+
+    @_data.setter
+    def _data(self, value: torch.Tensor) -> None:
+        self._dev = value
+        self._host = None
+        self._device = value.device
+
+    @property
+    def host_backed(self) -> bool:
+        """True while the storage is still the host array the matrix was built on."""
+        return self._dev is None
 
     @classmethod
     def _pad_fill(cls, width):
@@ -111,24 +145,30 @@ class _LaneMatrix:
 
     @property
     def padded_cols(self) -> int:
-        return self._data.shape[1]
+        return -(-self.cols // LANES[self.width]) * LANES[self.width]
 
     @property
     def device(self) -> torch.device:
-        return self._data.device
+        return self._device
 
     @property
     def data(self):
-        """Raw lane storage including padding columns (host copy), read-only."""
-        view = self._data.cpu().numpy()
+        """Raw lane storage including padding columns, read-only: a view of
+        the backing host array (host-backed, as the reference's view,
+        antidist.py:68-73), else a host copy of the device storage."""
+        view = self._host.view() if self._dev is None else self._dev.cpu().numpy()
         view.flags.writeable = False
         return view
 
     def to_numpy(self) -> np.ndarray:
-        return self._data.cpu().numpy()
+        if self._dev is None:
+            return np.array(self._host)
+        return self._dev.cpu().numpy()
 
     def copy(self):
-        return type(self)(self.rows, self.cols, self.width, self._data.clone())
+        if self._dev is None:
+            return type(self)(self.rows, self.cols, self.width, np.array(self._host), device=self._device)
+        return type(self)(self.rows, self.cols, self.width, self._dev.clone())
 
     def _check_index(self, i, j):
         if not (0 <= i < self.rows and 0 <= j < self.cols):
@@ -136,13 +176,18 @@ class _LaneMatrix:
 
     def get(self, i: int, j: int) -> int:
         self._check_index(i, j)
-        return int(self._data[i, j].cpu().numpy())
+        if self._dev is None:
+            return int(self._host[i, j])
+        return int(self._dev[i, j].cpu().numpy())
 
     def set(self, i: int, j: int, value: int) -> None:
         self._check_index(i, j)
         if not 0 <= value <= self.limit:
             raise ValueError(f"entry {value!r} outside [0, {self.limit}]")
-        self._data[i, j] = torch.from_numpy(np.array(value, dtype=_NP[self.width])).to(self.device)
+        if self._dev is None:   # writes the backing array, as the reference does
+            self._host[i, j] = value
+            return
+        self._dev[i, j] = torch.from_numpy(np.array(value, dtype=_NP[self.width])).to(self.device)
 
     def to_lists(self) -> list[list[int]]:
         return self.to_numpy()[:, : self.cols].tolist()
@@ -237,15 +282,42 @@ class _LaneMatrix:
         if self.device != other.device:
             raise ValueError(f"operands live on different devices: {self.device} vs {other.device}")
 
+    def _close_host(self) -> torch.Tensor:
+        """Host-buffer closure of the backing array into page-locked memory
+        (smx_fw_host_*); returns the finished host result."""
+        from . import engines
+        host = torch.from_numpy(np.ascontiguousarray(self._host))
+        res, _ = engines.lane_close_host(host, self.rows, self.width, anti=not self._PAD_IS_LIMIT,
+                                         device=self._device)
+        torch.cuda.current_stream(self._device).synchronize()
+        return res
+
     def transitive_close(self) -> None:
-        """In-place Floyd-Warshall closure (antidist.py:252-261 / :331-340)."""
+        """In-place Floyd-Warshall closure (antidist.py:252-261 / :331-340).
+        Host-backed: the backing array itself receives the result, as the
+        reference's in-place sweep over ``_data`` does."""
         if self.rows != self.cols:
             raise ValueError(f"closure needs a square matrix, got {self.rows}x{self.cols}")
         from . import engines
+        if self._dev is None and self._host.flags.writeable:
+            res = self._close_host()
+            if self._host.flags.c_contiguous:
+                torch.from_numpy(self._host).copy_(res)   # (threaded copy)
+            else:
+                np.copyto(self._host, res.numpy())
+            return
         engines.lane_close_(self._data, self.rows, self.width, anti=not self._PAD_IS_LIMIT)
 
     def transitive_closure(self):
-        """Closure over >= 1 edge on a copy (antidist.py:263-273 / :342-350)."""
+        """Closure over >= 1 edge on a copy (antidist.py:263-273 / :342-350).
+        Host-backed: one host-buffer closure call, whose result is a
+        host-backed matrix over page-locked memory (``.data`` reads it
+        without a copy)."""
+        if self.rows != self.cols:
+            raise ValueError(f"closure needs a square matrix, got {self.rows}x{self.cols}")
+        if self._dev is None:
+            res = self._close_host()
+            return type(self)(self.rows, self.cols, self.width, res.numpy(), device=self._device)
         out = self.copy()
         out.transitive_close()
         return out

@@ -30,6 +30,7 @@
 #include <mutex>
 #include <vector>
 
+#include "host_stage.cuh"
 #include "semiring_packed.cuh"
 
 namespace smx {
@@ -967,11 +968,22 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
     if ((e = cudaEventRecord(ev_fork, s)) != cudaSuccess) return (int)e;
     if ((e = cudaStreamWaitEvent(cs->in, ev_fork, 0)) != cudaSuccess) return (int)e;
     if ((e = cudaStreamWaitEvent(cs->out, ev_fork, 0)) != cudaSuccess) return (int)e;
-    for (size_t g = 0, r0 = 0; g < ends.size(); r0 = ends[g], ++g) {
-        if ((e = cudaMemcpyAsync(Tm + r0 * ld, hin + r0 * ld, (ends[g] - r0) * row_bytes, cudaMemcpyHostToDevice,
-                                 cs->in)) != cudaSuccess)
-            return (int)e;
-        if ((e = cudaEventRecord(ev_in[g], cs->in)) != cudaSuccess) return (int)e;
+    // Page-locked input: every group's H2D is queued now.  Pageable input
+    // (an ordinary numpy array, the reference's own call): staged through
+    // page-locked slots by a coordinator thread (host_stage.cuh), which
+    // records each group's event; the loop below waits on the host for that
+    // record before making the main stream wait on the event.
+    HostStager stager;
+    const bool staged = is_pageable(hin);
+    if (staged) {
+        SMX_TRY(stager.start(hin, Tm, row_bytes, ends, ev_in, cs->in));
+    } else {
+        for (size_t g = 0, r0 = 0; g < ends.size(); r0 = ends[g], ++g) {
+            if ((e = cudaMemcpyAsync(Tm + r0 * ld, hin + r0 * ld, (ends[g] - r0) * row_bytes,
+                                     cudaMemcpyHostToDevice, cs->in)) != cudaSuccess)
+                return (int)e;
+            if ((e = cudaEventRecord(ev_in[g], cs->in)) != cudaSuccess) return (int)e;
+        }
     }
     auto d2h = [&](int r0, int r1, cudaEvent_t ev) -> int {
         cudaError_t e2;
@@ -985,6 +997,7 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
     for (size_t g = 0, r0 = 0; g < ends.size(); r0 = ends[g], ++g) {
         const int r1 = ends[g];
         const int t0 = (int)r0 / G::BM, tiles = ceil_div(r1, G::BM) - t0;
+        if (staged) SMX_TRY(stager.wait_recorded((int)g));
         if ((e = cudaStreamWaitEvent(s, ev_in[g], 0)) != cudaSuccess) return (int)e;
         // ingest: T[G, :] (+)= T[G, 0:r0] (x) T[0:r0, :], one pivot block of K per launch.
         // The first block's A tiles are the raw arrived rows (mostly
@@ -1027,6 +1040,7 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
     }
     if ((e = cudaEventRecord(ev_join, cs->out)) != cudaSuccess) return (int)e;
     e = cudaStreamWaitEvent(s, ev_join, 0);
+    if (staged) SMX_TRY(stager.finish());
     return e == cudaSuccess ? SMX_OK : (int)e;
 }
 

@@ -1,0 +1,198 @@
+// Staged H2D copies from pageable host memory (see host_stage.cuh).
+#include "host_stage.cuh"
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <functional>
+
+#include "common.cuh"
+
+namespace smx {
+
+bool is_pageable(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();   // (older drivers report unregistered memory as an error)
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+namespace {
+
+// Fixed pool of memcpy workers (created on first use, joined at exit).
+class CopyPool {
+public:
+    static CopyPool& get() {
+        static CopyPool pool;
+        return pool;
+    }
+    // memcpy(dst, src, bytes) split over the workers; returns when done.
+    void copy(char* dst, const char* src, size_t bytes) {
+        std::unique_lock<std::mutex> lk(mu_);
+        dst_ = dst;
+        src_ = src;
+        bytes_ = bytes;
+        pending_ = (int)workers_.size();
+        ++gen_;
+        cv_.notify_all();
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+
+private:
+    CopyPool() {
+        const unsigned hw = std::thread::hardware_concurrency();
+        const int n = (int)std::max(1u, std::min(12u, hw > 2 ? hw - 2 : 1u));
+        for (int i = 0; i < n; ++i) workers_.emplace_back([this, i, n] { loop(i, n); });
+    }
+    void loop(int i, int n) {
+        unsigned long long seen = 0;
+        for (;;) {
+            char* d;
+            const char* s;
+            size_t b;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+                d = dst_;
+                s = src_;
+                b = bytes_;
+            }
+            // 4 KB-aligned slices, one per worker
+            const size_t per = ((b + n - 1) / n + 4095) & ~size_t(4095);
+            const size_t lo = std::min(b, per * i), hi = std::min(b, lo + per);
+            if (hi > lo) std::memcpy(d + lo, s + lo, hi - lo);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_all();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0;
+    int pending_ = 0;
+    unsigned long long gen_ = 0;
+    bool stop_ = false;
+};
+
+// Page-locked staging ring: kSlots x kSlotBytes, allocated once per process
+// (256 MB; cudaHostAlloc of 2 GB took 2.1 s on the pool's hosts).
+constexpr int kSlots = 4;
+constexpr size_t kSlotBytes = 64ull << 20;
+struct Ring {
+    char* base = nullptr;
+    cudaEvent_t ev[kSlots] = {};
+    int device = -1;
+};
+std::mutex g_ring_mu;
+int ring_for(int device, Ring** out) {
+    static Ring rings[64];
+    if (device < 0 || device >= 64) return SMX_E_ARG;
+    Ring& r = rings[device];
+    if (!r.base) {
+        cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&r.base), kSlots * kSlotBytes, cudaHostAllocPortable);
+        if (e != cudaSuccess) {
+            r.base = nullptr;
+            return (int)e;
+        }
+        for (int i = 0; i < kSlots; ++i)
+            if ((e = cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming)) != cudaSuccess) return (int)e;
+        r.device = device;
+    }
+    *out = &r;
+    return SMX_OK;
+}
+
+}  // namespace
+
+int HostStager::start(const void* src, void* dst, size_t row_bytes, const std::vector<int>& ends,
+                      const cudaEvent_t* ev, cudaStream_t in) {
+    src_ = static_cast<const char*>(src);
+    dst_ = static_cast<char*>(dst);
+    row_bytes_ = row_bytes;
+    ends_ = ends;
+    ev_ = ev;
+    in_ = in;
+    recorded_ = 0;
+    status_ = 0;
+    cudaError_t e = cudaGetDevice(&device_);
+    if (e != cudaSuccess) return (int)e;
+    th_ = std::thread([this] { run(); });
+    return SMX_OK;
+}
+
+void HostStager::run() {
+    int rc = SMX_OK;
+    cudaSetDevice(device_);
+    Ring* ring = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_ring_mu);   // one staged call per ring at a time
+        rc = ring_for(device_, &ring);
+        if (rc == SMX_OK) {
+            CopyPool& pool = CopyPool::get();
+            size_t chunk = 0;
+            for (size_t g = 0, r0 = 0; g < ends_.size() && rc == SMX_OK; r0 = ends_[g], ++g) {
+                size_t off = r0 * row_bytes_;
+                const size_t end = (size_t)ends_[g] * row_bytes_;
+                while (off < end && rc == SMX_OK) {
+                    const int slot = (int)(chunk % kSlots);
+                    const size_t bytes = std::min(kSlotBytes, end - off);
+                    cudaError_t e = cudaSuccess;
+                    // the slot's previous H2D (this call's, or a previous call's
+                    // still in flight) must be done before it is overwritten; an
+                    // event never recorded completes at once
+                    e = cudaEventSynchronize(ring->ev[slot]);
+                    if (e == cudaSuccess) {
+                        char* s = ring->base + slot * kSlotBytes;
+                        pool.copy(s, src_ + off, bytes);
+                        e = cudaMemcpyAsync(dst_ + off, s, bytes, cudaMemcpyHostToDevice, in_);
+                    }
+                    if (e == cudaSuccess) e = cudaEventRecord(ring->ev[slot], in_);
+                    if (e != cudaSuccess) rc = (int)e;
+                    off += bytes;
+                    ++chunk;
+                }
+                if (rc == SMX_OK) {
+                    cudaError_t e = cudaEventRecord(ev_[g], in_);
+                    if (e != cudaSuccess) rc = (int)e;
+                }
+                if (rc == SMX_OK) {
+                    std::lock_guard<std::mutex> lk(mu_);
+                    recorded_ = (int)g + 1;
+                    cv_.notify_all();
+                }
+            }
+        }
+    }
+    std::lock_guard<std::mutex> lk(mu_);
+    status_ = rc;
+    if (rc != SMX_OK) recorded_ = (int)ends_.size();   // release every waiter
+    cv_.notify_all();
+}
+
+int HostStager::wait_recorded(int g) {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return recorded_ > g; });
+    return status_;
+}
+
+int HostStager::finish() {
+    if (th_.joinable()) th_.join();
+    return status_;
+}
+
+}  // namespace smx

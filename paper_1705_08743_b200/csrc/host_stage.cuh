@@ -1,0 +1,56 @@
+// Staged host -> device copies from pageable memory.
+//
+// The reference's user-visible closure takes an ordinary numpy array
+// (AntidistMatrix(n, n, w, data).transitive_closure(), antidist.py:263-273),
+// i.e. pageable memory.  cudaMemcpyAsync from pageable memory runs at ~11
+// GB/s on the pool's B200 hosts and blocks the launching thread until each
+// copy is staged, so the host-buffer closure could not issue its compute
+// while the input streams in.  Here a coordinator thread copies the input
+// through a ring of page-locked slots: a pool of worker threads memcpy each
+// chunk into a slot (~47 GB/s on 16 cores, tools/perf_host_io.py), the
+// coordinator issues the slot's H2D on the copy stream (55 GB/s) and
+// records the caller's per-group event when a group's last chunk is in.
+// The launching thread only waits (on the host) until a group's event has
+// been recorded before it makes its stream wait on that event.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <condition_variable>
+#include <cstddef>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+namespace smx {
+
+bool is_pageable(const void* p);
+
+class HostStager {
+public:
+    // rows [ends[g-1], ends[g]) of `src` (row_bytes each) form group g; its
+    // H2D into dst lands before ev[g] is recorded on `in`.
+    int start(const void* src, void* dst, size_t row_bytes, const std::vector<int>& ends,
+              const cudaEvent_t* ev, cudaStream_t in);
+    // Blocks until group g's event has been recorded (or the stager failed).
+    int wait_recorded(int g);
+    // Joins the coordinator; returns its status.
+    int finish();
+    ~HostStager() { finish(); }
+
+private:
+    void run();
+    const char* src_ = nullptr;
+    char* dst_ = nullptr;
+    size_t row_bytes_ = 0;
+    std::vector<int> ends_;
+    const cudaEvent_t* ev_ = nullptr;
+    cudaStream_t in_ = nullptr;
+    int device_ = 0;
+    std::thread th_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    int recorded_ = 0;   // groups whose event is recorded
+    int status_ = 0;
+};
+
+}  // namespace smx

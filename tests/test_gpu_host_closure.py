@@ -147,3 +147,53 @@ def test_host_closure_full_size_matches_device_closure():
     dev = AntidistMatrix(n, n, 16, torch.from_numpy(t).cuda()).transitive_closure()
     _, got = host_closure(AntidistMatrix, t, 16)
     assert np.array_equal(got, dev.data)
+
+
+@pytest.mark.parametrize("n", [700, 2048])
+@pytest.mark.parametrize("kind", ["anti", "dist"])
+def test_dropin_host_backed_closure(n, kind, mode, oracle_lib):
+    """The reference's literal call on an ordinary (pageable) numpy array:
+    ``AntidistMatrix(n, n, 16, arr).transitive_closure().data``.  The matrix
+    is host-backed (its ``.data`` is a read-only view of ``arr``, as the
+    reference's is, antidist.py:68-73), the closure runs as one host-buffer
+    call whose input is staged through page-locked slots (host_stage.cuh),
+    and the result is host-backed page-locked memory.  In-place
+    ``transitive_close()`` writes the caller's array, as the reference's
+    in-place sweep over ``_data`` does."""
+    rng = np.random.default_rng(n + 17)
+    t = random_graph(n, 16, 0.03, rng)
+    cls = AntidistMatrix
+    if kind == "dist":
+        t = (65535 - t.astype(np.uint32)).astype(np.uint16)
+        cls = DistMatrix
+    keep = t.copy()
+    want = oracle_lib.semiring_close(t, 16, kind)
+    m = cls(n, n, 16, t)
+    assert m.host_backed and np.shares_memory(m.data, t) and not m.data.flags.writeable
+    r = m.transitive_closure()
+    assert r.host_backed
+    np.testing.assert_array_equal(r.data, want, err_msg=f"n={n} {kind}")
+    np.testing.assert_array_equal(t, keep)                      # closure() leaves the input alone
+    assert m.host_backed
+    np.testing.assert_array_equal((m * m).data, oracle_lib.semiring_mul(keep, keep, n, 16, kind))
+    assert not m.host_backed                                    # the product moved it to HBM
+    m2 = cls(n, n, 16, t)
+    m2.transitive_close()                                       # in place: the caller's array
+    np.testing.assert_array_equal(t, want)
+    assert m2.host_backed and m2.get(3, 5) == int(want[3, 5])
+
+
+def test_dropin_staged_ring_reuse_matches_device_closure():
+    """n = 8192 u16 (128 MB, several 64 MB staging slots), twice in a row
+    (the ring's slots reused across calls), streamed; equal to the
+    device-resident closure of the same input and to the C4 reference digest
+    path's generator output shape."""
+    cfg = workloads.CONFIGS["c4_fw_u16"]
+    (t,) = workloads.make_inputs(cfg, 8192)
+    dev = AntidistMatrix(8192, 8192, 16, torch.from_numpy(t).cuda()).transitive_closure()
+    want = dev._data.cpu().numpy()
+    with stream_mode(2):
+        for _ in range(2):
+            got = AntidistMatrix(8192, 8192, 16, t).transitive_closure()
+            assert got.host_backed
+            assert sha(got.data) == sha(want)

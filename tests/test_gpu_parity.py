@@ -24,7 +24,7 @@ def sha(a):
 
 
 def lane(kind, data, cols, width):
-    return CLS[kind](data.shape[0], cols, width, np.ascontiguousarray(data))
+    return CLS[kind](data.shape[0], cols, width, np.array(data))   # (a copy: the fixtures are shared)
 
 
 # -- golden small cases: products, closures, Boolean ---------------------------

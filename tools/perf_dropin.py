@@ -1,0 +1,48 @@
+"""The reference's literal call on a host array against the page-locked
+host-buffer call and the device-resident closure (development aid):
+    AntidistMatrix(n, n, 16, ndarray).transitive_closure().data
+Prints one JSON object."""
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch  # noqa: E402
+
+from paper_1705_08743_b200 import AntidistMatrix, workloads  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+cfg = workloads.CONFIGS["c5_fw_u16"]
+(host,) = workloads.make_inputs(cfg, n)
+res = {"n": n}
+
+
+def timed(fn, reps=2, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        fn()
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) / reps
+
+
+res["dropin_ms"] = timed(lambda: AntidistMatrix(n, n, 16, host).transitive_closure().data) * 1e3
+pinned = torch.from_numpy(host).pin_memory()
+out = torch.empty_like(pinned).pin_memory()
+res["pinned_call_ms"] = timed(lambda: AntidistMatrix.closure_of_host(pinned, 16, out=out)) * 1e3
+src = torch.from_numpy(host).cuda()
+w = torch.empty_like(src)
+m = AntidistMatrix(n, n, 16, w)
+
+
+def dev():
+    w.copy_(src)
+    m.transitive_close()
+
+
+res["device_ms"] = timed(dev) * 1e3
+res["cells_per_s_dropin"] = n ** 3 / res["dropin_ms"] * 1e3
+print(json.dumps(res))
