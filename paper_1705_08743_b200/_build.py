@@ -2,8 +2,12 @@
 
 nvcc cross-compiles for sm_100a without a GPU, so this runs in the build
 container; the .so is git-ignored but travels to the GPU box with the repo
-snapshot.  Objects are compiled in parallel and relinked only when a source or
-header is newer than the library.
+snapshot.  Objects are compiled in parallel.  The library is rebuilt when the
+content hash of its inputs (every source and header, the nvcc flags and the
+nvcc version) differs from the one recorded beside it at the last build
+(libsemimat_b200.so.stamp), not on file times: a fresh checkout or a copied
+tree with newer mtimes but the same sources does not rebuild, and an edited
+source with an older mtime does.
 """
 
 from __future__ import annotations
@@ -40,11 +44,27 @@ def _deps():
     return _sources() + sorted(CSRC.glob("*.cuh")) + sorted((REPO / "include").glob("*.h"))
 
 
+STAMP = LIB.with_name(LIB.name + ".stamp")
+
+
+def _input_hash() -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for p in _deps():
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    h.update(" ".join(NVCC_FLAGS + os.environ.get("SMX_EXTRA_NVCC_FLAGS", "").split()).encode())
+    try:
+        h.update(subprocess.run([_nvcc(), "--version"], capture_output=True, text=True).stdout.encode())
+    except (RuntimeError, OSError):
+        pass
+    return h.hexdigest()
+
+
 def up_to_date() -> bool:
-    if not LIB.exists():
+    if not LIB.exists() or not STAMP.exists():
         return False
-    t = LIB.stat().st_mtime
-    return all(p.stat().st_mtime <= t for p in _deps())
+    return STAMP.read_text().strip() == _input_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -75,6 +95,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     os.replace(tmp, LIB)
+    STAMP.write_text(_input_hash() + "\n")
     return LIB
 
 
