@@ -465,14 +465,21 @@ int fw_pivot_2x2(T* P, int b, long long ld, int kind, T* scratch, cudaStream_t s
     T* P12 = P + h;
     T* P21 = P + (long long)h * ld;
     T* P22 = P21 + h;
-    SMX_TRY(fw_pivot<T>(P, h, ld, kind, s, scratch));
-    SMX_TRY(semiring_gemm_lite<T>(P, P12, P12, h, m, h, ld, ld, ld, kind, s));     // P12 (+)= P11* (x) P12
-    SMX_TRY(semiring_gemm_lite<T>(P21, P, P21, m, h, h, ld, ld, ld, kind, s));     // P21 (+)= P21 (x) P11*
-    SMX_TRY(semiring_gemm_lite<T>(P21, P12, P22, m, m, h, ld, ld, ld, kind, s));
-    SMX_TRY(fw_pivot<T>(P22, m, ld, kind, s, scratch));
-    SMX_TRY(semiring_gemm_lite<T>(P22, P21, P21, m, h, m, ld, ld, ld, kind, s));   // P21 (+)= P22* (x) P21
-    SMX_TRY(semiring_gemm_lite<T>(P12, P22, P12, h, m, m, ld, ld, ld, kind, s));   // P12 (+)= P12 (x) P22*
-    return semiring_gemm_lite<T>(P12, P21, P, h, h, m, ld, ld, ld, kind, s);
+#ifdef SMX_TRACE_PIVOT_PARTS   // development builds: each step of the recursion (cells -10 .. -17)
+#define SMX_PP(i, expr) do { trace_begin(s, -10 - (i)); SMX_TRY(expr); trace_end(s); } while (0)
+#else
+#define SMX_PP(i, expr) SMX_TRY(expr)
+#endif
+    SMX_PP(0, (fw_pivot<T>(P, h, ld, kind, s, scratch)));
+    SMX_PP(1, (semiring_gemm_lite<T>(P, P12, P12, h, m, h, ld, ld, ld, kind, s)));     // P12 (+)= P11* (x) P12
+    SMX_PP(2, (semiring_gemm_lite<T>(P21, P, P21, m, h, h, ld, ld, ld, kind, s)));     // P21 (+)= P21 (x) P11*
+    SMX_PP(3, (semiring_gemm_lite<T>(P21, P12, P22, m, m, h, ld, ld, ld, kind, s)));
+    SMX_PP(4, (fw_pivot<T>(P22, m, ld, kind, s, scratch)));
+    SMX_PP(5, (semiring_gemm_lite<T>(P22, P21, P21, m, h, m, ld, ld, ld, kind, s)));   // P21 (+)= P22* (x) P21
+    SMX_PP(6, (semiring_gemm_lite<T>(P12, P22, P12, h, m, m, ld, ld, ld, kind, s)));   // P12 (+)= P12 (x) P22*
+    SMX_PP(7, (semiring_gemm_lite<T>(P12, P21, P, h, h, m, ld, ld, ld, kind, s)));
+#undef SMX_PP
+    return SMX_OK;
 }
 
 int scratch_alloc(void** p, size_t bytes, cudaStream_t s);

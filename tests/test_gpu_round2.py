@@ -290,3 +290,37 @@ def test_pivot_bounded_form_matches_oracle(w, oracle_lib):
                     np.testing.assert_array_equal(got[:b, :b], want, err_msg=f"b={b} {case} {kind} fast={fast}")
                     np.testing.assert_array_equal(got[b:], full[b:])
                     np.testing.assert_array_equal(got[:b, b:], full[:b, b:])
+
+
+def test_nccl_broadcast_on_torch_communicator(tmp_path):
+    """The NCCL transport of the C-ABI sharded closure, on a real NCCL
+    communicator: a one-rank ProcessGroupNCCL (this box has one GPU; NCCL
+    refuses two ranks on one device), its ncclComm_t taken from torch exactly
+    as sharded.NativeShardedFW does, and smx_nccl_broadcast (libnccl resolved
+    with dlopen(RTLD_NOLOAD), i.e. torch's own copy) on the library's side
+    stream.  Then the full sharded closure entry at world 1 over that group
+    equals the single-GPU closure."""
+    import torch.distributed as dist
+    from paper_1705_08743_b200 import sharded
+    if dist.is_initialized():
+        pytest.skip("a process group is already initialised")
+    dist.init_process_group("nccl", init_method=f"file://{tmp_path / 'pg'}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        lib = _native.lib()
+        fw = sharded.NativeShardedFW(1024, 0, 1, 16, anti=True, transport="nccl")
+        comm = fw._nccl_comm(torch.device("cuda", 0))
+        assert comm
+        x = torch.arange(4096, dtype=torch.int32, device="cuda")
+        want = x.clone()
+        rc = lib.smx_nccl_broadcast(x.data_ptr(), x.numel() * 4, 0, comm, _native.stream_ptr())
+        assert rc == 0
+        torch.cuda.synchronize()
+        assert torch.equal(x, want)
+        cfg = workloads.CONFIGS["c5_fw_u16"]
+        (t,) = workloads.make_inputs(cfg, 1024)
+        got = fw.run(torch.from_numpy(t).cuda()).cpu().numpy()
+        ref = AntidistMatrix(1024, 1024, 16, torch.from_numpy(t).cuda()).transitive_closure()._data.cpu().numpy()
+        np.testing.assert_array_equal(got, ref)
+    finally:
+        dist.destroy_process_group()

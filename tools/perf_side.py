@@ -19,6 +19,9 @@ for n in [int(x) for x in (sys.argv[1:] or ["8192"])]:
     side = [ms[i] for i in range(k) if cells[i] == -1]
     p3 = [ms[i] for i in range(k) if cells[i] >= 0]
     parts = {name: [ms[i] for i in range(k) if cells[i] == code] for code, name in ((-2, "3a"), (-3, "pivot"), (-4, "row_panel"))}
+    pp = {f"pivot_step{i}": [ms[j] for j in range(k) if cells[j] == -10 - i] for i in range(8)}
+    if any(pp.values()):      # -DSMX_TRACE_PIVOT_PARTS: the 2 x 2 recursion's steps
+        print(json.dumps({"n": n, **{f"{name}_ms_mean": sum(v) / max(len(v), 1) for name, v in pp.items()}}))
     if any(parts.values()):   # -DSMX_TRACE_SIDE_PARTS
         print(json.dumps({"n": n, **{f"{name}_ms_mean": sum(v) / max(len(v), 1) for name, v in parts.items()}}))
     print(json.dumps({"n": n, "rounds": len(p3), "side_ms_mean": sum(side) / max(len(side), 1),
