@@ -158,6 +158,13 @@ int smx_set_graphs(int enable);
  * 0 (default) = the regular pivot and tiles.  Results are identical.
  * Returns the previous setting. */
 int smx_set_fw_side_lite(int enable);
+/* Look-ahead 3a (round r's update of the next pivot block's rows) in two
+ * parts: the diagonal tile first with the pivot right behind it on the side
+ * stream, the other columns on a second side stream beside the pivot.
+ * 0 = never (one launch before the pivot), 1 = automatic (default;
+ * currently never: it measured no net gain), 2 = always.
+ * Results are identical.  Returns the previous setting. */
+int smx_set_fw_split_3a(int mode);
 /* Pivot block of smx_fw_*: 0 = automatic (u16: 512 at n >= 16384, 256 at
  * n >= 8192; u8: 256 at n >= 8192; else 128), or force 128 / 256 / 512
  * (clamped to smx_fw_block: u8 256, u32 128).  Returns the previous setting

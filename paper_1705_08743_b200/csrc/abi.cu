@@ -86,6 +86,8 @@ int side_stream(SideStream** out) {
         if ((e = cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming)) != cudaSuccess) return (int)e;
         if ((e = cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming)) != cudaSuccess) return (int)e;
         if ((e = cudaEventCreateWithFlags(&f.aux, cudaEventDisableTiming)) != cudaSuccess) return (int)e;
+        if ((e = cudaStreamCreateWithPriority(&f.side2, cudaStreamNonBlocking, hi)) != cudaSuccess) return (int)e;
+        if ((e = cudaEventCreateWithFlags(&f.aux2, cudaEventDisableTiming)) != cudaSuccess) return (int)e;
     }
     *out = &f;
     return SMX_OK;

@@ -31,6 +31,10 @@ void trace_end(cudaStream_t s);
 struct SideStream {
     cudaStream_t side = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr, aux = nullptr;
+    // a second side stream at the same priority (the FW look-ahead runs the
+    // off-diagonal part of 3a on it beside the pivot) and its done event
+    cudaStream_t side2 = nullptr;
+    cudaEvent_t aux2 = nullptr;
     int priority = 0;   // the side stream's (highest) priority
 };
 int side_stream(SideStream** out);

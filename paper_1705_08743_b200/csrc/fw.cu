@@ -587,6 +587,12 @@ int fw_pivot_and_row_panel(T* Tm, int n, long long ld, int kind, T* RP, int k0, 
     return semiring_gemm<T>(rowK + k0, rowK, rowK, bb, n, bb, ld, ld, ld, kind, 1, 0, 0, s);
 }
 
+// smx_set_fw_split_3a: the look-ahead's 3a in two parts (diagonal tile
+// first, the pivot right behind it, the rest of the rows on a second side
+// stream): 0 = never, 1 = automatic (currently never: see fw_rounds_packed),
+// 2 = always.
+static std::atomic<int> g_fw_split_3a{1};
+
 // Side-stream kernel footprint.  Measured: the co-residable Lite row-panel
 // tiles gain nothing over the regular ones (the side chain already hides
 // behind phase 3) and lose ~1-2%, so the regular tiles are the default.
@@ -707,6 +713,21 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
             const int k1 = k0 + BLK, bb1 = blk(r + 1);
             if ((e = cudaEventRecord(fs->fork, s)) != cudaSuccess) return (int)e;
             if ((e = cudaStreamWaitEvent(fs->side, fs->fork, 0)) != cudaSuccess) return (int)e;
+            // 3a split (g_fw_split_3a): the pivot only needs the diagonal
+            // tile T[K1, K1] updated by round r, so that part goes first on
+            // the side stream and the pivot follows it at once, while the
+            // rest of rows K1 (every other column) is updated on the second
+            // side stream; the row panel waits for both.  The two parts
+            // write disjoint columns of rows K1, and the pivot touches only
+            // T[K1, K1].
+            // Automatic = off: measured (tools/perf_split3a.py) a gain only
+            // at n = 4096 (2.88 -> 2.69-2.79 ms) and small losses at 1024,
+            // 2048, 6144 and 8192 (17.50 -> 17.65 ms): the extra launches and
+            // the second stream's 3a CTAs beside the pivot cost about what
+            // the shorter chain saves.
+            const int sm3 = g_fw_split_3a.load(std::memory_order_relaxed);
+            const bool split = n > bb1 && sm3 == 2;
+            if (split && (e = cudaStreamWaitEvent(fs->side2, fs->fork, 0)) != cudaSuccess) return (int)e;
             {
                 PriorityScope ps(fs->priority);
 #if defined(SMX_TRACE_SIDE) && !defined(SMX_TRACE_SIDE_PARTS)   // development builds: side-chain spans (cells = -1)
@@ -716,8 +737,19 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
                 trace_begin(fs->side, -2);
 #endif
                 // 3a: the next pivot block's rows
-                SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / G::BM, ceil_div(bb1, G::BM), 0, 0, pws,
-                                      pws_bytes, fs->side, cr));
+                if (split) {
+                    const int c0 = k1 / G::BN, cn = ceil_div(k1 + bb1, G::BN) - c0;
+                    SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / G::BM, ceil_div(bb1, G::BM), 0, 0, pws,
+                                          pws_bytes, fs->side, cr, c0, cn));
+                    SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / G::BM, ceil_div(bb1, G::BM), 0, 0, pws,
+                                          pws_bytes, fs->side2, cr, 0, c0));
+                    SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / G::BM, ceil_div(bb1, G::BM), 0, 0, pws,
+                                          pws_bytes, fs->side2, cr, c0 + cn, -1));
+                    if ((e = cudaEventRecord(fs->aux2, fs->side2)) != cudaSuccess) return (int)e;
+                } else {
+                    SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / G::BM, ceil_div(bb1, G::BM), 0, 0, pws,
+                                          pws_bytes, fs->side, cr));
+                }
 #ifdef SMX_TRACE_SIDE_PARTS
                 trace_end(fs->side);
                 trace_begin(fs->side, -3);
@@ -730,7 +762,15 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
 #endif
                 if ((e = cudaEventRecord(fs->aux, fs->side)) != cudaSuccess) return (int)e;
 #ifndef SMX_TRACE_SIDE_PARTS
-                SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
+                if (split) {
+                    SMX_TRY(fw_pivot<T>(Tm + (long long)k1 * ld + k1, bb1, ld, kind, fs->side, RP));
+                    if ((e = cudaStreamWaitEvent(fs->side, fs->aux2, 0)) != cudaSuccess) return (int)e;
+                    T* rowK1 = Tm + (long long)k1 * ld;
+                    SMX_TRY(semiring_gemm<T>(rowK1 + k1, rowK1, rowK1, bb1, n, bb1, ld, ld, ld, kind, 1, 0, 0,
+                                             fs->side));
+                } else {
+                    SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
+                }
 #endif
 #if defined(SMX_TRACE_SIDE) && !defined(SMX_TRACE_SIDE_PARTS)
                 trace_end(fs->side);
@@ -742,6 +782,8 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
             SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, t0, tiles, k0, bb + bb1, pws, pws_bytes, s, cr));
             trace_end(s);
             if ((e = cudaStreamWaitEvent(s, fs->aux, 0)) != cudaSuccess) return (int)e;
+            // (pack A(r+1) overwrites the packed A tiles both 3a parts read)
+            if (split && (e = cudaStreamWaitEvent(s, fs->aux2, 0)) != cudaSuccess) return (int)e;
             if (!certified(r + 1))   // (a certified round packs its own A after the join)
                 SMX_TRY(packed_pack_a_rows<T>(Tm + k1, n, n, bb1, ld, kind, pws, pws_bytes, t0, tiles, s));
             if ((e = cudaStreamWaitEvent(s, fs->join, 0)) != cudaSuccess) return (int)e;
@@ -787,7 +829,8 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
                                      (unsigned long long)lookahead_enabled(), (unsigned long long)g_side_lite.load(),
                                      (unsigned long long)g_fw_block_override.load(), (unsigned long long)g_fw_packed.load(),
                                      (unsigned long long)bounded_fastpath_enabled(),
-                                     (unsigned long long)g_pivot_blocked.load()};
+                                     (unsigned long long)g_pivot_blocked.load() |
+                                         ((unsigned long long)g_fw_split_3a.load() << 1)};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     // the phase-3 trace records host-side state per launch: trace runs stay eager
     return run_graphed(key, s, g_trace.armed, [&](cudaStream_t st) -> int {
@@ -1165,6 +1208,10 @@ int smx_set_fw_pivot_blocked(int enable) {
     return g_pivot_blocked.exchange(enable ? 1 : 0);
 }
 
+int smx_set_fw_split_3a(int mode) {
+    if (mode < 0 || mode > 2) return SMX_E_ARG;
+    return g_fw_split_3a.exchange(mode);
+}
 int smx_set_fw_side_lite(int enable) {
     return g_side_lite.exchange(enable ? 1 : 0);
 }

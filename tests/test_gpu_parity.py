@@ -381,23 +381,27 @@ def test_fw_lookahead_and_serial_schedules_agree(n, oracle_lib):
     cfg = workloads.CONFIGS["c5_fw_u16"]
     (t,) = workloads.make_inputs(cfg, n)
     want = oracle_lib.semiring_close(t, 16, "anti")
-    for la, lite, blk in ((1, 0, 0), (0, 0, 0), (1, 1, 0), (1, 0, 256), (1, 1, 256), (0, 0, 256),
-                          (1, 0, 128), (1, 0, 512), (0, 0, 512), (1, 1, 512)):
-        olds = (lib.smx_set_fw_lookahead(la), lib.smx_set_fw_side_lite(lite), lib.smx_set_fw_block(blk))
+    for la, lite, blk, split in ((1, 0, 0, 1), (0, 0, 0, 1), (1, 1, 0, 1), (1, 0, 256, 1), (1, 1, 256, 1),
+                                 (0, 0, 256, 1), (1, 0, 128, 1), (1, 0, 512, 1), (0, 0, 512, 1), (1, 1, 512, 1),
+                                 (1, 0, 0, 0), (1, 0, 256, 0), (1, 0, 512, 0), (1, 0, 0, 2), (1, 0, 256, 2),
+                                 (1, 1, 512, 2)):
+        olds = (lib.smx_set_fw_lookahead(la), lib.smx_set_fw_side_lite(lite), lib.smx_set_fw_block(blk),
+                lib.smx_set_fw_split_3a(split))
         try:
             for width_kind in ("anti", "dist"):
                 m = lane("anti", t, n, 16)
                 if width_kind == "dist":
                     m = ~m
                     np.testing.assert_array_equal((~m.transitive_closure()).data, want,
-                                                  err_msg=f"la={la} lite={lite} blk={blk}")
+                                                  err_msg=f"la={la} lite={lite} blk={blk} split={split}")
                 else:
                     np.testing.assert_array_equal(m.transitive_closure().data, want,
-                                                  err_msg=f"la={la} lite={lite} blk={blk}")
+                                                  err_msg=f"la={la} lite={lite} blk={blk} split={split}")
         finally:
             lib.smx_set_fw_lookahead(olds[0])
             lib.smx_set_fw_side_lite(olds[1])
             lib.smx_set_fw_block(olds[2])
+            lib.smx_set_fw_split_3a(olds[3])
 
 
 @pytest.mark.parametrize("n", [640, 2048])
