@@ -165,6 +165,10 @@ int smx_set_fw_side_lite(int enable);
  * currently never: it measured no net gain), 2 = always.
  * Results are identical.  Returns the previous setting. */
 int smx_set_fw_split_3a(int mode);
+/* Pivot tiles above 128 vertices close by a 2 x 2 blocked recursion; its two
+ * independent panel products per half run as one launch (1, default) or as
+ * two (0).  Results are identical.  Returns the previous setting. */
+int smx_set_fw_pivot_pairs(int enable);
 /* Pivot block of smx_fw_*: 0 = automatic (u16: 512 at n >= 16384, 256 at
  * n >= 8192; u8: 256 at n >= 8192; else 128), or force 128 / 256 / 512
  * (clamped to smx_fw_block: u8 256, u32 128).  Returns the previous setting

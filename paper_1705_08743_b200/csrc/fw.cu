@@ -458,6 +458,10 @@ int copy_panel(const T* src, long long ld, T* dst, long long ldd, int rows, int 
 template <typename T>
 int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s, T* scratch);
 
+// smx_set_fw_pivot_pairs: the recursion's two independent panel products per
+// half in one launch (semiring_gemm_lite_pair).
+static std::atomic<int> g_pivot_pairs{1};
+
 template <typename T>
 int fw_pivot_2x2(T* P, int b, long long ld, int kind, T* scratch, cudaStream_t s) {
     const int h = b <= 256 ? 128 : 256;
@@ -471,12 +475,23 @@ int fw_pivot_2x2(T* P, int b, long long ld, int kind, T* scratch, cudaStream_t s
 #define SMX_PP(i, expr) SMX_TRY(expr)
 #endif
     SMX_PP(0, (fw_pivot<T>(P, h, ld, kind, s, scratch)));
-    SMX_PP(1, (semiring_gemm_lite<T>(P, P12, P12, h, m, h, ld, ld, ld, kind, s)));     // P12 (+)= P11* (x) P12
-    SMX_PP(2, (semiring_gemm_lite<T>(P21, P, P21, m, h, h, ld, ld, ld, kind, s)));     // P21 (+)= P21 (x) P11*
+    if (g_pivot_pairs.load(std::memory_order_relaxed)) {
+        // the two independent panel products of each half in one launch
+        SMX_PP(1, (semiring_gemm_lite_pair<T>(P, P12, P12, h, m, h,          // P12 (+)= P11* (x) P12
+                                              P21, P, P21, m, h, h, ld, kind, s)));   // P21 (+)= P21 (x) P11*
+    } else {
+        SMX_PP(1, (semiring_gemm_lite<T>(P, P12, P12, h, m, h, ld, ld, ld, kind, s)));     // P12 (+)= P11* (x) P12
+        SMX_PP(2, (semiring_gemm_lite<T>(P21, P, P21, m, h, h, ld, ld, ld, kind, s)));     // P21 (+)= P21 (x) P11*
+    }
     SMX_PP(3, (semiring_gemm_lite<T>(P21, P12, P22, m, m, h, ld, ld, ld, kind, s)));
     SMX_PP(4, (fw_pivot<T>(P22, m, ld, kind, s, scratch)));
-    SMX_PP(5, (semiring_gemm_lite<T>(P22, P21, P21, m, h, m, ld, ld, ld, kind, s)));   // P21 (+)= P22* (x) P21
-    SMX_PP(6, (semiring_gemm_lite<T>(P12, P22, P12, h, m, m, ld, ld, ld, kind, s)));   // P12 (+)= P12 (x) P22*
+    if (g_pivot_pairs.load(std::memory_order_relaxed)) {
+        SMX_PP(5, (semiring_gemm_lite_pair<T>(P22, P21, P21, m, h, m,        // P21 (+)= P22* (x) P21
+                                              P12, P22, P12, h, m, m, ld, kind, s)));  // P12 (+)= P12 (x) P22*
+    } else {
+        SMX_PP(5, (semiring_gemm_lite<T>(P22, P21, P21, m, h, m, ld, ld, ld, kind, s)));   // P21 (+)= P22* (x) P21
+        SMX_PP(6, (semiring_gemm_lite<T>(P12, P22, P12, h, m, m, ld, ld, ld, kind, s)));   // P12 (+)= P12 (x) P22*
+    }
     SMX_PP(7, (semiring_gemm_lite<T>(P12, P21, P, h, h, m, ld, ld, ld, kind, s)));
 #undef SMX_PP
     return SMX_OK;
@@ -830,7 +845,8 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
                                      (unsigned long long)g_fw_block_override.load(), (unsigned long long)g_fw_packed.load(),
                                      (unsigned long long)bounded_fastpath_enabled(),
                                      (unsigned long long)g_pivot_blocked.load() |
-                                         ((unsigned long long)g_fw_split_3a.load() << 1)};
+                                         ((unsigned long long)g_fw_split_3a.load() << 1) |
+                                         ((unsigned long long)g_pivot_pairs.load() << 3)};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     // the phase-3 trace records host-side state per launch: trace runs stay eager
     return run_graphed(key, s, g_trace.armed, [&](cudaStream_t st) -> int {
@@ -1208,6 +1224,9 @@ int smx_set_fw_pivot_blocked(int enable) {
     return g_pivot_blocked.exchange(enable ? 1 : 0);
 }
 
+int smx_set_fw_pivot_pairs(int enable) {
+    return g_pivot_pairs.exchange(enable != 0);
+}
 int smx_set_fw_split_3a(int mode) {
     if (mode < 0 || mode > 2) return SMX_E_ARG;
     return g_fw_split_3a.exchange(mode);

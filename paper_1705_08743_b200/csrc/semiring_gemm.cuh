@@ -198,7 +198,7 @@ __device__ __forceinline__ uint4 load_b_chunk(const GemmArgs<T>& p, int col0, in
 // public products use it; the Floyd-Warshall instantiation carries none of
 // its registers or branches).
 template <typename Cfg, typename T, bool CERT>
-__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(const GemmArgs<T> p) {
+__device__ __forceinline__ void semiring_gemm_tile(const GemmArgs<T>& p, int bx, int by) {
     using L = Lane<T>;
     constexpr int BM = Cfg::BM, BNW = Cfg::BNW, BK = Cfg::BK, TM = Cfg::TM, TNW = Cfg::TNW;
     constexpr int HW = Cfg::HW, WPC = Cfg::WPC, E = Cfg::E, CPW = Cfg::CPW, AP = Cfg::APLANES;
@@ -208,10 +208,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
     uint32_t* Bs = As + 2 * AP * BK * BM;                     // [2][BK][BNW]
 
     const int tid = threadIdx.x;
-    int mt = blockIdx.y;
+    int mt = by;
     if (mt >= p.skip_tile0) mt += p.skip_tiles;
     const int row0 = mt * BM;
-    const int col0 = blockIdx.x * Cfg::BN;
+    const int col0 = bx * Cfg::BN;
     const bool anti = p.anti != 0;
     const int tc = tid % Cfg::TCOLS, tr = tid / Cfg::TCOLS;
 
@@ -405,6 +405,28 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(
     }
 }
 
+template <typename Cfg, typename T, bool CERT>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) semiring_gemm_kernel(const GemmArgs<T> p) {
+    semiring_gemm_tile<Cfg, T, CERT>(p, blockIdx.x, blockIdx.y);
+}
+
+// Two independent products in one launch (blockIdx.z selects the problem;
+// the grid covers the larger one and the other's spare CTAs exit): the
+// pivot recursion's pairs P12 (+)= P11* (x) P12 | P21 (+)= P21 (x) P11* and
+// P21 (+)= P22* (x) P21 | P12 (+)= P12 (x) P22* (fw.cu fw_pivot_2x2).  On the
+// look-ahead side stream every launch waits for SM slots beside phase-3 CTAs,
+// so two launches cost about twice one (profiles/r02w_pivot_steps_contended.json).
+template <typename Cfg, typename T>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
+semiring_gemm_pair_kernel(const GemmArgs<T> p0, const GemmArgs<T> p1) {
+    const bool second = blockIdx.z != 0;
+    const int M = second ? p1.M : p0.M, N = second ? p1.N : p0.N;
+    const int st = second ? p1.skip_tiles : p0.skip_tiles;
+    if ((int)blockIdx.x >= (N + Cfg::BN - 1) / Cfg::BN || (int)blockIdx.y >= (M + Cfg::BM - 1) / Cfg::BM - st) return;
+    if (second) semiring_gemm_tile<Cfg, T, false>(p1, blockIdx.x, blockIdx.y);
+    else semiring_gemm_tile<Cfg, T, false>(p0, blockIdx.x, blockIdx.y);
+}
+
 // Tile configurations.  "Large" is the throughput tile: 128 x 128 cells
 // (u8/u16; 128 x 64 for u32), 256 threads with 4-row x 8-word thread tiles,
 // 2 CTAs per SM so one CTA's C load / store overlaps the other's k-loop (a
@@ -591,6 +613,31 @@ int semiring_gemm(const T* A, const T* B, T* C, int M, int N, int K, long long l
 template <typename T>
 int launch_large(const GemmArgs<T>& a, cudaStream_t stream) {
     return launch_semiring_gemm<LargeCfg<T>>(a, stream);
+}
+
+// Two independent accumulating products with Lite tiles in one launch
+// (semiring_gemm_pair_kernel); each as semiring_gemm_lite.
+template <typename T>
+int semiring_gemm_lite_pair(const T* A0, const T* B0, T* C0, int M0, int N0, int K0, const T* A1, const T* B1,
+                            T* C1, int M1, int N1, int K1, long long ld, int kind, cudaStream_t stream) {
+    using Cfg = LiteCfg<T>;
+    if (M0 < 0 || N0 < 0 || K0 < 0 || M1 < 0 || N1 < 0 || K1 < 0 || (kind != SMX_ANTI && kind != SMX_DIST))
+        return SMX_E_ARG;
+    for (const void* q : {(const void*)A0, (const void*)B0, (const void*)C0, (const void*)A1, (const void*)B1,
+                          (const void*)C1})
+        if (!aligned16(q)) return SMX_E_ALIGN;
+    if (!ld_ok(ld, sizeof(T))) return SMX_E_ALIGN;
+    GemmArgs<T> a0{A0, B0, C0, M0, N0, K0, ld, ld, ld, kind == SMX_ANTI, 1, 0, 0, bounded_fastpath_enabled(),
+                   nullptr, nullptr};
+    GemmArgs<T> a1{A1, B1, C1, M1, N1, K1, ld, ld, ld, kind == SMX_ANTI, 1, 0, 0, bounded_fastpath_enabled(),
+                   nullptr, nullptr};
+    const int mt = ceil_div(M0 > M1 ? M0 : M1, Cfg::BM), nt = ceil_div(N0 > N1 ? N0 : N1, Cfg::BN);
+    if (mt <= 0 || nt <= 0) return SMX_OK;
+    auto kern = semiring_gemm_pair_kernel<Cfg, T>;
+    SMX_TRY(set_max_smem((const void*)kern, Cfg::SMEM));
+    smx::count_launch();
+    const cudaError_t e = launch_kernel(kern, dim3(nt, mt, 2), dim3(Cfg::THREADS), Cfg::SMEM, stream, a0, a1);
+    return e == cudaSuccess ? SMX_OK : (int)e;
 }
 
 // Accumulating product with the co-residable Lite tiles (no row skip).

@@ -258,7 +258,7 @@ def test_pivot_bounded_form_matches_oracle(w, oracle_lib):
     dt = NP[w]
     rng = np.random.default_rng(90 + w)
     hi = S if w == 8 else (1 << 15)
-    sizes = (32, 100, 128, 200, 256) + ((384, 512) if w == 16 else ())
+    sizes = (32, 100, 128, 200, 256) + ((300, 384, 512) if w == 16 else ())
     for b in sizes:
         for case in ("small", "edge", "one_high"):
             for kind in ("anti", "dist"):
@@ -278,8 +278,9 @@ def test_pivot_bounded_form_matches_oracle(w, oracle_lib):
                 t_or = np.full((b, pad), 0 if kind == "anti" else S, dt)
                 t_or[:, :b] = full[:b, :b]
                 want = oracle_lib.semiring_close(t_or, w, kind)[:, :b]
-                for fast in (1, 0):
+                for fast, pairs in ((1, 1), (0, 1), (1, 0)):   # (pairs: the recursion's paired launches)
                     old = lib.smx_set_bounded_fastpath(fast)
+                    old_pairs = lib.smx_set_fw_pivot_pairs(pairs)
                     try:
                         dev = torch.from_numpy(full.copy()).cuda()
                         _native.check(lib.smx_fw_pivot(dev.data_ptr(), b, ld, w // 8, 0 if kind == "anti" else 1,
@@ -287,7 +288,9 @@ def test_pivot_bounded_form_matches_oracle(w, oracle_lib):
                         got = dev.cpu().numpy()
                     finally:
                         lib.smx_set_bounded_fastpath(old)
-                    np.testing.assert_array_equal(got[:b, :b], want, err_msg=f"b={b} {case} {kind} fast={fast}")
+                        lib.smx_set_fw_pivot_pairs(old_pairs)
+                    np.testing.assert_array_equal(got[:b, :b], want,
+                                                  err_msg=f"b={b} {case} {kind} fast={fast} pairs={pairs}")
                     np.testing.assert_array_equal(got[b:], full[b:])
                     np.testing.assert_array_equal(got[:b, b:], full[:b, b:])
 
