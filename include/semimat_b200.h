@@ -169,6 +169,12 @@ int smx_set_fw_split_3a(int mode);
  * independent panel products per half run as one launch (1, default) or as
  * two (0).  Results are identical.  Returns the previous setting. */
 int smx_set_fw_pivot_pairs(int enable);
+/* Row panel of the look-ahead closure on the packed kernel (the closed
+ * pivot tile and the panel packed into the row-panel workspace region
+ * first) or on the register-staged tiles: 0 = never, 1 = automatic (default:
+ * n >= 8192, where it measured faster), 2 = always.  Results are identical.
+ * Returns the previous setting. */
+int smx_set_fw_packed_panel(int mode);
 /* Pivot block of smx_fw_*: 0 = automatic (u16: 512 at n >= 16384, 256 at
  * n >= 8192; u8: 256 at n >= 8192; else 128), or force 128 / 256 / 512
  * (clamped to smx_fw_block: u8 256, u32 128).  Returns the previous setting
@@ -188,6 +194,10 @@ int smx_set_fw_packed(int enable);
  * each launch's duration (ms) and cell-updates; returns the count (< 0 on a
  * CUDA error).  Reading disarms the trace. */
 int smx_fw_trace_arm(int max_launches);
+/* Begin / end (ms) of every traced launch relative to the first one's
+ * begin: the gaps between phase-3 launches.  Call before smx_fw_trace_read,
+ * which disarms the trace.  Returns the count, or -(cudaError_t). */
+int smx_fw_trace_offsets(float* begin_ms, float* end_ms, int cap);
 int smx_fw_trace_read(float* ms, long long* cells, int cap);
 
 /* Building blocks of the blocked FW, exported for the row-panel-sharded

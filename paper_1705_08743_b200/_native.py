@@ -29,6 +29,7 @@ _SIGS = {
     "smx_set_fw_side_lite": ([c_int], c_int),
     "smx_set_fw_split_3a": ([c_int], c_int),
     "smx_set_fw_pivot_pairs": ([c_int], c_int),
+    "smx_set_fw_packed_panel": ([c_int], c_int),
     "smx_set_fw_pivot_blocked": ([c_int], c_int),
     "smx_set_bits_m4r": ([c_int], c_int),
     "smx_set_bool_persistent": ([c_int], c_int),
@@ -39,6 +40,7 @@ _SIGS = {
     "smx_fw_block_for": ([c_int, c_int], c_int),
     "smx_fw_trace_arm": ([c_int], c_int),
     "smx_fw_trace_read": ([c_void_p, c_void_p, c_int], c_int),
+    "smx_fw_trace_offsets": ([c_void_p, c_void_p, c_int], c_int),
     "smx_semiring_gemm_u8": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),
     "smx_semiring_gemm_u16": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),
     "smx_semiring_gemm_u32": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),

@@ -533,12 +533,22 @@ int fw_pivot(T* P, int b, long long ld, int kind, cudaStream_t s, T* scratch) {
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-inline size_t fw_ws_bytes(int n, long long ld, int eb) {
-    // RP: pivot row panel snapshot (B x ld); CP: column panel snapshot (n x B);
-    // the packed phase-3 operand tiles (semiring_packed.cuh) and a 256-byte
-    // slot for the per-round operand certificate (fw_rounds_packed)
+// RP: the row-panel region: the serial schedule's row-panel snapshot (B x
+// ld), or the look-ahead's packed row-panel operands (semiring_gemm_packed of
+// B x n x B, g_fw_packed_panel) -- whichever is larger.
+inline size_t fw_rp_bytes(int n, long long ld, int eb) {
     const size_t B = fw_block_for(eb);
-    const size_t base = align256(B * ld * eb) + align256((size_t)n * B * eb);
+    const size_t snap = align256(B * ld * eb);
+    const size_t packed = align256(packed_ws_bytes_eb((int)B, n, (int)B, eb));
+    return snap > packed ? snap : packed;
+}
+
+inline size_t fw_ws_bytes(int n, long long ld, int eb) {
+    // RP: the row-panel region (fw_rp_bytes); CP: column panel snapshot
+    // (n x B); the packed phase-3 operand tiles (semiring_packed.cuh) and a
+    // 256-byte slot for the per-round operand certificate (fw_rounds_packed)
+    const size_t B = fw_block_for(eb);
+    const size_t base = fw_rp_bytes(n, ld, eb) + align256((size_t)n * B * eb);
     return base + align256(packed_ws_bytes_eb(n, n, (int)B, eb)) + 256;
 }
 // The certificate slot: the last 256 bytes of fw_ws_bytes.
@@ -585,9 +595,23 @@ void trace_end(cudaStream_t s) {
 }
 
 // Pivot tile + pivot row panel of block [k0, k0+bb): T[K,:] (+)= T[K,K]* (x) T[K,:].
+// smx_set_fw_packed_panel: the look-ahead's row panel on the packed kernel
+// (its A = the closed pivot tile and B = the panel itself packed first, into
+// the RP region, then C = the panel updated in place from the snapshot).
+// 0 = never, 1 = automatic (n >= 8192), 2 = always.  Measured
+// (tools/perf_switch.py, profiles/r03c_packed_panel_ab.jsonl): n = 8192
+// 17.26 -> 16.93-17.11 ms (the 6% of the cells the side chain computes run
+// at the packed kernel's rate); n = 2048 / 4096 +10% / +4.5% (two more
+// launches on a chain that binds there); n = 16384 unchanged.
+static std::atomic<int> g_fw_packed_panel{1};
+inline bool packed_panel_for(int n) {
+    const int m = g_fw_packed_panel.load(std::memory_order_relaxed);
+    return m == 2 || (m == 1 && n >= 8192);
+}
+
 template <typename T>
 int fw_pivot_and_row_panel(T* Tm, int n, long long ld, int kind, T* RP, int k0, int bb, cudaStream_t s,
-                           bool lite = false) {
+                           bool lite = false, bool packed_panel = false) {
     T* rowK = Tm + (long long)k0 * ld;
     // (the lite pivot's shared-memory tile holds 256 x 256 u16 or 128 x 128 u32)
     if (lite && bb <= (sizeof(T) == 4 ? 128 : 256)) SMX_TRY(fw_pivot_lite<T>(rowK + k0, bb, ld, kind, s));
@@ -599,6 +623,9 @@ int fw_pivot_and_row_panel(T* Tm, int n, long long ld, int kind, T* RP, int k0, 
     // P* (x) P* = P* (closure, weights >= 0) -- so the result is the same for
     // any interleaving.  The P* tile itself is rewritten with its own value.
     if (lite) return semiring_gemm_lite<T>(rowK + k0, rowK, rowK, bb, n, bb, ld, ld, ld, kind, s);
+    if (packed_panel && RP != nullptr && packed_panel_for(n))
+        return semiring_gemm_packed<T>(rowK + k0, rowK, rowK, bb, n, bb, ld, ld, ld, kind, 1, 0, 0, RP,
+                                       packed_ws_bytes_t<T>(bb, n, bb), s);
     return semiring_gemm<T>(rowK + k0, rowK, rowK, bb, n, bb, ld, ld, ld, kind, 1, 0, 0, s);
 }
 
@@ -707,7 +734,7 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
     if (ra >= rb) return SMX_OK;
     const bool can_cert = cert != nullptr && !Lane<T>::kOneInstr && bounded_fastpath_enabled();
     auto certified = [&](int r) { return can_cert && r - ra < kFwCertRounds; };
-    SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, ra * BLK, blk(ra), s));
+    SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, ra * BLK, blk(ra), s, false, true));
     if (!certified(ra))
         SMX_TRY(packed_pack_a_rows<T>(Tm + ra * BLK, n, n, blk(ra), ld, kind, pws, pws_bytes, t0, tiles, s));
     cudaError_t e;
@@ -781,10 +808,15 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
                     SMX_TRY(fw_pivot<T>(Tm + (long long)k1 * ld + k1, bb1, ld, kind, fs->side, RP));
                     if ((e = cudaStreamWaitEvent(fs->side, fs->aux2, 0)) != cudaSuccess) return (int)e;
                     T* rowK1 = Tm + (long long)k1 * ld;
-                    SMX_TRY(semiring_gemm<T>(rowK1 + k1, rowK1, rowK1, bb1, n, bb1, ld, ld, ld, kind, 1, 0, 0,
-                                             fs->side));
+                    if (packed_panel_for(n))
+                        SMX_TRY(semiring_gemm_packed<T>(rowK1 + k1, rowK1, rowK1, bb1, n, bb1, ld, ld, ld, kind, 1,
+                                                        0, 0, RP, packed_ws_bytes_t<T>(bb1, n, bb1), fs->side));
+                    else
+                        SMX_TRY(semiring_gemm<T>(rowK1 + k1, rowK1, rowK1, bb1, n, bb1, ld, ld, ld, kind, 1, 0, 0,
+                                                 fs->side));
                 } else {
-                    SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0));
+                    SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, k1, bb1, fs->side, g_side_lite != 0,
+                                                      true));
                 }
 #endif
 #if defined(SMX_TRACE_SIDE) && !defined(SMX_TRACE_SIDE_PARTS)
@@ -831,9 +863,8 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
     if (n <= FwBlock<T>::value) return fw_pivot<T>(Tm, n, ld, kind, s, nullptr);
     if (ws == nullptr || ws_bytes < fw_ws_bytes(n, ld, sizeof(T))) return SMX_E_WORKSPACE;
     T* RP = reinterpret_cast<T*>(ws);
-    T* CP = reinterpret_cast<T*>(reinterpret_cast<char*>(ws) +
-                                 align256((size_t)FwBlock<T>::value * ld * sizeof(T)));
-    const size_t pws_off = align256((size_t)FwBlock<T>::value * ld * sizeof(T)) +
+    T* CP = reinterpret_cast<T*>(reinterpret_cast<char*>(ws) + fw_rp_bytes(n, ld, sizeof(T)));
+    const size_t pws_off = fw_rp_bytes(n, ld, sizeof(T)) +
                            align256((size_t)n * FwBlock<T>::value * sizeof(T));
     void* pws = reinterpret_cast<char*>(ws) + pws_off;
     const size_t pws_bytes = ws_bytes - pws_off;
@@ -846,7 +877,8 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
                                      (unsigned long long)bounded_fastpath_enabled(),
                                      (unsigned long long)g_pivot_blocked.load() |
                                          ((unsigned long long)g_fw_split_3a.load() << 1) |
-                                         ((unsigned long long)g_pivot_pairs.load() << 3)};
+                                         ((unsigned long long)g_pivot_pairs.load() << 3) |
+                                         ((unsigned long long)g_fw_packed_panel.load() << 4)};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     // the phase-3 trace records host-side state per launch: trace runs stay eager
     return run_graphed(key, s, g_trace.armed, [&](cudaStream_t st) -> int {
@@ -1006,7 +1038,7 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
     }
     if (ws == nullptr || ws_bytes < fw_host_ws_bytes(n, ld, sizeof(T))) return SMX_E_WORKSPACE;
     T* RP = reinterpret_cast<T*>(ws);
-    const size_t pws_off = align256((size_t)FwBlock<T>::value * ld * sizeof(T)) +
+    const size_t pws_off = fw_rp_bytes(n, ld, sizeof(T)) +
                            align256((size_t)n * FwBlock<T>::value * sizeof(T));
     void* pws = reinterpret_cast<char*>(ws) + pws_off;
     const size_t slot = fw_host_slot_bytes(n, sizeof(T));
@@ -1224,6 +1256,10 @@ int smx_set_fw_pivot_blocked(int enable) {
     return g_pivot_blocked.exchange(enable ? 1 : 0);
 }
 
+int smx_set_fw_packed_panel(int mode) {
+    if (mode < 0 || mode > 2) return SMX_E_ARG;
+    return g_fw_packed_panel.exchange(mode);
+}
 int smx_set_fw_pivot_pairs(int enable) {
     return g_pivot_pairs.exchange(enable != 0);
 }
@@ -1250,6 +1286,19 @@ int smx_fw_trace_arm(int max_launches) {
     return SMX_OK;
 }
 
+// Begin / end of every traced launch relative to the first begin (ms), for
+// the gaps between phase-3 launches; call before smx_fw_trace_read (which
+// disarms the trace).
+int smx_fw_trace_offsets(float* begin_ms, float* end_ms, int cap) {
+    const int n = g_trace.count < cap ? g_trace.count : cap;
+    for (int i = 0; i < n; ++i) {
+        cudaError_t e = cudaEventSynchronize(g_trace.ev[2 * i + 1]);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&begin_ms[i], g_trace.ev[0], g_trace.ev[2 * i]);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&end_ms[i], g_trace.ev[0], g_trace.ev[2 * i + 1]);
+        if (e != cudaSuccess) return -(int)e;
+    }
+    return n;
+}
 int smx_fw_trace_read(float* ms, long long* cells, int cap) {
     g_trace.armed = false;
     const int n = g_trace.count < cap ? g_trace.count : cap;
