@@ -175,6 +175,11 @@ int smx_set_fw_pivot_pairs(int enable);
  * n >= 8192, where it measured faster), 2 = always.  Results are identical.
  * Returns the previous setting. */
 int smx_set_fw_packed_panel(int mode);
+/* Packed row-panel buffers of the look-ahead closure: 2 (default) = double
+ * buffered, the side stream packs the next round's row panel beside the
+ * current phase 3; 1 = one buffer, packed on the main stream between the
+ * phase-3 launches.  Results are identical.  Returns the previous setting. */
+int smx_set_fw_panel_buffers(int count);
 /* Pivot block of smx_fw_*: 0 = automatic (u16: 512 at n >= 16384, 256 at
  * n >= 8192; u8: 256 at n >= 8192; else 128), or force 128 / 256 / 512
  * (clamped to smx_fw_block: u8 256, u32 128).  Returns the previous setting

@@ -30,6 +30,7 @@ _SIGS = {
     "smx_set_fw_split_3a": ([c_int], c_int),
     "smx_set_fw_pivot_pairs": ([c_int], c_int),
     "smx_set_fw_packed_panel": ([c_int], c_int),
+    "smx_set_fw_panel_buffers": ([c_int], c_int),
     "smx_set_fw_pivot_blocked": ([c_int], c_int),
     "smx_set_bits_m4r": ([c_int], c_int),
     "smx_set_bool_persistent": ([c_int], c_int),

@@ -543,17 +543,25 @@ inline size_t fw_rp_bytes(int n, long long ld, int eb) {
     return snap > packed ? snap : packed;
 }
 
+inline size_t fw_b2_bytes(int n, int eb) { return align256(packed_b_ws_bytes_eb(n, fw_block_for(eb), eb)); }
+
 inline size_t fw_ws_bytes(int n, long long ld, int eb) {
     // RP: the row-panel region (fw_rp_bytes); CP: column panel snapshot
-    // (n x B); the packed phase-3 operand tiles (semiring_packed.cuh) and a
-    // 256-byte slot for the per-round operand certificate (fw_rounds_packed)
+    // (n x B); the packed phase-3 operand tiles (semiring_packed.cuh); a
+    // second block of packed B tiles (the look-ahead's row panels alternate
+    // between the two, fw_rounds_packed); a 256-byte slot for the per-round
+    // operand certificate
     const size_t B = fw_block_for(eb);
     const size_t base = fw_rp_bytes(n, ld, eb) + align256((size_t)n * B * eb);
-    return base + align256(packed_ws_bytes_eb(n, n, (int)B, eb)) + 256;
+    return base + align256(packed_ws_bytes_eb(n, n, (int)B, eb)) + fw_b2_bytes(n, eb) + 256;
 }
 // The certificate slot: the last 256 bytes of fw_ws_bytes.
 inline int* fw_cert_slot(void* ws, int n, long long ld, int eb) {
     return reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + fw_ws_bytes(n, ld, eb) - 256);
+}
+// The second packed-B block: just before the certificate slot.
+inline void* fw_b2_slot(void* ws, int n, long long ld, int eb) {
+    return reinterpret_cast<char*>(ws) + fw_ws_bytes(n, ld, eb) - 256 - fw_b2_bytes(n, eb);
 }
 
 // smx_set_fw_packed: phase 3 on the warp-specialised packed-tile kernel
@@ -724,7 +732,7 @@ constexpr int kFwCertRounds = 2;
 
 template <typename T>
 int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, size_t pws_bytes, int lo, int hi,
-                     int ra, int rb, cudaStream_t s, int* cert = nullptr) {
+                     int ra, int rb, cudaStream_t s, int* cert = nullptr, void* b2 = nullptr) {
     using G = PackedCfg<T>;
     SideStream* fs = nullptr;
     SMX_TRY(side_stream(&fs));
@@ -734,6 +742,16 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
     if (ra >= rb) return SMX_OK;
     const bool can_cert = cert != nullptr && !Lane<T>::kOneInstr && bounded_fastpath_enabled();
     auto certified = [&](int r) { return can_cert && r - ra < kFwCertRounds; };
+    // Double-buffered row panels (b2 != nullptr): round r's packed B lives in
+    // the workspace's own B block (r - ra even) or in b2 (odd), so the side
+    // chain of round r packs round r+1's row panel right after computing it,
+    // beside round r's phase 3, instead of the main stream packing it between
+    // the two phase-3 launches.  Round r+1's buffer was last read by round
+    // r-1's 3a (earlier on the side stream) and 3b (before this round's fork
+    // on the main stream).  A certified round packs its B on the main stream
+    // after its certificate, as before.
+    auto bbuf = [&](int r) -> void* { return (b2 != nullptr && ((r - ra) & 1)) ? b2 : nullptr; };
+    auto side_packs_b = [&](int r) { return b2 != nullptr && r > ra && !certified(r); };
     SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, ra * BLK, blk(ra), s, false, true));
     if (!certified(ra))
         SMX_TRY(packed_pack_a_rows<T>(Tm + ra * BLK, n, n, blk(ra), ld, kind, pws, pws_bytes, t0, tiles, s));
@@ -750,7 +768,9 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
                 SMX_TRY(packed_pack_a_rows<T>(Tm + k0, n, n, bb, ld, kind, pws, pws_bytes, t0, tiles, s, cr));
             }
         }
-        SMX_TRY(packed_pack<T>(nullptr, rowK, n, n, bb, ld, ld, kind, pws, pws_bytes, s, cr));
+        if (!side_packs_b(r))
+            SMX_TRY(packed_pack<T>(nullptr, rowK, n, n, bb, ld, ld, kind, pws, pws_bytes, s, cr, bbuf(r)));
+        void* wb = bbuf(r);
         if (r + 1 < rb) {
             const int k1 = k0 + BLK, bb1 = blk(r + 1);
             if ((e = cudaEventRecord(fs->fork, s)) != cudaSuccess) return (int)e;
@@ -782,15 +802,15 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
                 if (split) {
                     const int c0 = k1 / G::BN, cn = ceil_div(k1 + bb1, G::BN) - c0;
                     SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / G::BM, ceil_div(bb1, G::BM), 0, 0, pws,
-                                          pws_bytes, fs->side, cr, c0, cn));
+                                          pws_bytes, fs->side, cr, c0, cn, wb));
                     SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / G::BM, ceil_div(bb1, G::BM), 0, 0, pws,
-                                          pws_bytes, fs->side2, cr, 0, c0));
+                                          pws_bytes, fs->side2, cr, 0, c0, wb));
                     SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / G::BM, ceil_div(bb1, G::BM), 0, 0, pws,
-                                          pws_bytes, fs->side2, cr, c0 + cn, -1));
+                                          pws_bytes, fs->side2, cr, c0 + cn, -1, wb));
                     if ((e = cudaEventRecord(fs->aux2, fs->side2)) != cudaSuccess) return (int)e;
                 } else {
                     SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, k1 / G::BM, ceil_div(bb1, G::BM), 0, 0, pws,
-                                          pws_bytes, fs->side, cr));
+                                          pws_bytes, fs->side, cr, 0, -1, wb));
                 }
 #ifdef SMX_TRACE_SIDE_PARTS
                 trace_end(fs->side);
@@ -819,6 +839,10 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
                                                       true));
                 }
 #endif
+                // round r+1's row panel, packed as soon as it is final
+                if (side_packs_b(r + 1))
+                    SMX_TRY(packed_pack<T>(nullptr, Tm + (long long)k1 * ld, n, n, bb1, ld, ld, kind, pws, pws_bytes,
+                                           fs->side, nullptr, bbuf(r + 1)));
 #if defined(SMX_TRACE_SIDE) && !defined(SMX_TRACE_SIDE_PARTS)
                 trace_end(fs->side);
 #endif
@@ -826,7 +850,8 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
             if ((e = cudaEventRecord(fs->join, fs->side)) != cudaSuccess) return (int)e;
             // 3b: everything else in the window (skips K_r and K_{r+1}, adjacent tiles)
             trace_begin(s, (long long)(hi - lo - bb - bb1) * n * bb);
-            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, t0, tiles, k0, bb + bb1, pws, pws_bytes, s, cr));
+            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, t0, tiles, k0, bb + bb1, pws, pws_bytes, s, cr, 0, -1,
+                                  wb));
             trace_end(s);
             if ((e = cudaStreamWaitEvent(s, fs->aux, 0)) != cudaSuccess) return (int)e;
             // (pack A(r+1) overwrites the packed A tiles both 3a parts read)
@@ -836,18 +861,22 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
             if ((e = cudaStreamWaitEvent(s, fs->join, 0)) != cudaSuccess) return (int)e;
         } else {
             trace_begin(s, (long long)(hi - lo - bb) * n * bb);
-            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, t0, tiles, k0, bb, pws, pws_bytes, s, cr));
+            SMX_TRY(packed_run<T>(Tm, n, n, bb, ld, kind, 1, t0, tiles, k0, bb, pws, pws_bytes, s, cr, 0, -1, wb));
             trace_end(s);
         }
     }
     return SMX_OK;
 }
 
+// smx_set_fw_panel_buffers: 2 = double-buffered packed row panels (the side
+// chain packs the next one), 1 = one buffer packed on the main stream.
+static std::atomic<int> g_fw_panel_buffers{2};
+
 template <typename T>
 int fw_run_lookahead_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, size_t pws_bytes,
-                            cudaStream_t s, int* cert = nullptr) {
+                            cudaStream_t s, int* cert = nullptr, void* b2 = nullptr) {
     const int BLK = fw_block_for_n<T>(n);
-    return fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, pws_bytes, 0, n, 0, (n + BLK - 1) / BLK, s, cert);
+    return fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, pws_bytes, 0, n, 0, (n + BLK - 1) / BLK, s, cert, b2);
 }
 
 template <typename T>
@@ -878,13 +907,16 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
                                      (unsigned long long)g_pivot_blocked.load() |
                                          ((unsigned long long)g_fw_split_3a.load() << 1) |
                                          ((unsigned long long)g_pivot_pairs.load() << 3) |
-                                         ((unsigned long long)g_fw_packed_panel.load() << 4)};
+                                         ((unsigned long long)g_fw_packed_panel.load() << 4) |
+                                         ((unsigned long long)g_fw_panel_buffers.load() << 6)};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     // the phase-3 trace records host-side state per launch: trace runs stay eager
     return run_graphed(key, s, g_trace.armed, [&](cudaStream_t st) -> int {
         if (lookahead_enabled() && g_fw_packed)
             return fw_run_lookahead_packed<T>(Tm, n, ld, kind, RP, pws, pws_bytes, st,
-                                              fw_cert_slot(ws, n, ld, sizeof(T)));
+                                              fw_cert_slot(ws, n, ld, sizeof(T)),
+                                              g_fw_panel_buffers.load() == 2 ? fw_b2_slot(ws, n, ld, sizeof(T))
+                                                                             : nullptr);
         if (lookahead_enabled()) return fw_run_lookahead<T>(Tm, n, ld, kind, RP, CP, pws, pws_bytes, st);
         return fw_run_serial<T>(Tm, n, ld, kind, RP, CP, pws, pws_bytes, BLK, st);
     });
@@ -1043,6 +1075,7 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
     void* pws = reinterpret_cast<char*>(ws) + pws_off;
     const size_t slot = fw_host_slot_bytes(n, sizeof(T));
     int* cert = fw_cert_slot(ws, n, ld, sizeof(T));
+    void* b2 = g_fw_panel_buffers.load() == 2 ? fw_b2_slot(ws, n, ld, sizeof(T)) : nullptr;
     auto egress_slot = [&](int j) { return reinterpret_cast<char*>(ws) + fw_ws_bytes(n, ld, sizeof(T)) + j * slot; };
 
     const int sL = (R - kFwHostTailBlocks) * BLK;   // L = rows [sL, n)
@@ -1117,10 +1150,10 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
         // the group's rounds over every row that has arrived (the last group:
         // all rows, up to the blocks of L)
         const int rb = (r1 < n ? r1 : sL) / BLK;
-        SMX_TRY(fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, slot, 0, r1, (int)r0 / BLK, rb, s, cert));
+        SMX_TRY(fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, slot, 0, r1, (int)r0 / BLK, rb, s, cert, b2));
     }
     // L: its rounds on rows L alone; then L is final
-    SMX_TRY(fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, slot, sL, n, sL / BLK, R, s, cert));
+    SMX_TRY(fw_rounds_packed<T>(Tm, n, ld, kind, RP, pws, slot, sL, n, sL / BLK, R, s, cert, b2));
     SMX_TRY(d2h(sL, n, ev_out[0]));
     // egress: rows [0, sL) (+)= T[rows, L] (x) T[L, :]; L's blocks packed once as B
     for (int j = 0; j < kFwHostTailBlocks; ++j) {
@@ -1256,6 +1289,10 @@ int smx_set_fw_pivot_blocked(int enable) {
     return g_pivot_blocked.exchange(enable ? 1 : 0);
 }
 
+int smx_set_fw_panel_buffers(int count) {
+    if (count != 1 && count != 2) return SMX_E_ARG;
+    return g_fw_panel_buffers.exchange(count);
+}
 int smx_set_fw_packed_panel(int mode) {
     if (mode < 0 || mode > 2) return SMX_E_ARG;
     return g_fw_packed_panel.exchange(mode);

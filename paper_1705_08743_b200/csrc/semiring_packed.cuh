@@ -394,6 +394,18 @@ inline size_t packed_ws_bytes_t(int M, int N, int K) {
     return al(MT * KT * G::A_TILE_WORDS * 4) + al(KT * NT * G::B_TILE_WORDS * 4) + al(MT * KT) + al(KT * NT);
 }
 inline size_t packed_ws_bytes(int M, int N, int K) { return packed_ws_bytes_t<uint16_t>(M, N, K); }
+// A separate B-only block (B tiles + their flags): a second B operand beside
+// the one in a packed workspace (the closure's double-buffered row panels).
+template <typename T>
+inline size_t packed_b_ws_bytes_t(int N, int K) {
+    using G = PackedCfg<T>;
+    const size_t NT = ceil_div(N, G::BN), KT = ceil_div(K, G::BK);
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    return al(KT * NT * G::B_TILE_WORDS * 4) + al(KT * NT);
+}
+inline size_t packed_b_ws_bytes_eb(int N, int K, int eb) {
+    return eb == 4 ? packed_b_ws_bytes_t<uint32_t>(N, K) : packed_b_ws_bytes_t<uint16_t>(N, K);
+}
 inline size_t packed_u16_ws_bytes(int M, int N, int K) { return packed_ws_bytes(M, N, K); }
 // by storage element bytes (1, 2: u16x2 lanes; 4: u32 lanes)
 inline size_t packed_ws_bytes_eb(int M, int N, int K, int eb) {
@@ -408,8 +420,10 @@ struct PackedWs {
     uint8_t* fB;
     int MT, NT, KT;
 };
+// wsb: a B-only block (packed_b_ws_bytes_t) that replaces the workspace's
+// own B tiles and flags, or nullptr.
 template <typename T>
-inline PackedWs packed_views(void* ws, int M, int N, int K) {
+inline PackedWs packed_views(void* ws, int M, int N, int K, void* wsb = nullptr) {
     using G = PackedCfg<T>;
     PackedWs v;
     v.MT = ceil_div(M, G::BM);
@@ -424,6 +438,10 @@ inline PackedWs packed_views(void* ws, int M, int N, int K) {
     v.fA = reinterpret_cast<uint8_t*>(w);
     w += al((size_t)v.MT * v.KT);
     v.fB = reinterpret_cast<uint8_t*>(w);
+    if (wsb != nullptr) {
+        v.Bp = reinterpret_cast<uint32_t*>(wsb);
+        v.fB = reinterpret_cast<uint8_t*>(wsb) + al((size_t)v.KT * v.NT * G::B_TILE_WORDS * 4);
+    }
     return v;
 }
 
@@ -441,10 +459,10 @@ inline int packed_check(const void* A, const void* B, int M, int N, int K, long 
 // Pack A (M x K; A == nullptr skips it) and/or B (K x N; B == nullptr skips).
 template <typename T>
 inline int packed_pack(const T* A, const T* B, int M, int N, int K, long long lda, long long ldb, int kind, void* ws,
-                       size_t ws_bytes, cudaStream_t s, const int* cert = nullptr) {
+                       size_t ws_bytes, cudaStream_t s, const int* cert = nullptr, void* wsb = nullptr) {
     SMX_TRY(packed_check<T>(A, B, M, N, K, lda, ldb, kind, ws, ws_bytes));
     if (M == 0 || N == 0 || K == 0) return SMX_OK;
-    const PackedWs v = packed_views<T>(ws, M, N, K);
+    const PackedWs v = packed_views<T>(ws, M, N, K, wsb);
     const int anti = kind == SMX_ANTI;
     if (A) {
         pack_a_kernel<T><<<dim3(v.KT, v.MT), 128, 0, s>>>(A, M, K, lda, anti, v.KT, v.Ap, v.fA, cert);
@@ -481,14 +499,14 @@ inline int packed_pack_a_rows(const T* A, int M, int N, int K, long long lda, in
 template <typename T>
 inline int packed_run(T* C, int M, int N, int K, long long ldc, int kind, int accumulate, int row_tile0,
                       int row_tiles, int skip_row0, int skip_rows, void* ws, size_t ws_bytes, cudaStream_t s,
-                      const int* cert = nullptr, int col_tile0 = 0, int col_tiles = -1) {
+                      const int* cert = nullptr, int col_tile0 = 0, int col_tiles = -1, void* wsb = nullptr) {
     using G = PackedCfg<T>;
     if (M < 0 || N < 0 || K < 0 || (kind != SMX_ANTI && kind != SMX_DIST)) return SMX_E_ARG;
     if (M == 0 || N == 0) return SMX_OK;
     if (!aligned16(C) || !ld_ok(ldc, sizeof(T))) return SMX_E_ALIGN;
     if (ldc < N) return SMX_E_ARG;
     if (ws == nullptr || ws_bytes < packed_ws_bytes_t<T>(M, N, K)) return SMX_E_WORKSPACE;
-    const PackedWs v = packed_views<T>(ws, M, N, K);
+    const PackedWs v = packed_views<T>(ws, M, N, K, wsb);
     if (row_tile0 < 0 || row_tile0 > v.MT) return SMX_E_ARG;
     if (row_tiles < 0 || row_tile0 + row_tiles > v.MT) row_tiles = v.MT - row_tile0;
     if (col_tile0 < 0 || col_tile0 > v.NT) return SMX_E_ARG;

@@ -384,11 +384,12 @@ def test_fw_lookahead_and_serial_schedules_agree(n, oracle_lib):
     for la, lite, blk, split in ((1, 0, 0, 1), (0, 0, 0, 1), (1, 1, 0, 1), (1, 0, 256, 1), (1, 1, 256, 1),
                                  (0, 0, 256, 1), (1, 0, 128, 1), (1, 0, 512, 1), (0, 0, 512, 1), (1, 1, 512, 1),
                                  (1, 0, 0, 0), (1, 0, 256, 0), (1, 0, 512, 0), (1, 0, 0, 2), (1, 0, 256, 2),
-                                 (1, 1, 512, 2), (1, 0, 0, 10), (1, 0, 512, 12)):
+                                 (1, 1, 512, 2), (1, 0, 0, 10), (1, 0, 512, 12), (1, 0, 0, 101), (1, 0, 512, 101)):
         # split >= 10: the row panel on the register-staged tiles (smx_set_fw_packed_panel(0)); else
-        # always on the packed kernel (2)
+        # always on the packed kernel (2); split >= 100: one packed row-panel buffer
         olds = (lib.smx_set_fw_lookahead(la), lib.smx_set_fw_side_lite(lite), lib.smx_set_fw_block(blk),
-                lib.smx_set_fw_split_3a(split % 10), lib.smx_set_fw_packed_panel(2 if split < 10 else 0))
+                lib.smx_set_fw_split_3a(split % 10), lib.smx_set_fw_packed_panel(2 if split % 100 < 10 else 0),
+                lib.smx_set_fw_panel_buffers(1 if split >= 100 else 2))
         try:
             for width_kind in ("anti", "dist"):
                 m = lane("anti", t, n, 16)
@@ -405,6 +406,7 @@ def test_fw_lookahead_and_serial_schedules_agree(n, oracle_lib):
             lib.smx_set_fw_block(olds[2])
             lib.smx_set_fw_split_3a(olds[3])
             lib.smx_set_fw_packed_panel(olds[4])
+            lib.smx_set_fw_panel_buffers(olds[5])
 
 
 @pytest.mark.parametrize("n", [640, 2048])
