@@ -245,6 +245,11 @@ int smx_semiring_gemm_skip_certified(const void* A, const void* B, void* C, int 
  * Workspace: smx_fw_sharded_workspace_bytes(rows, ld, elem_bytes, block). */
 typedef int (*smx_bcast_fn)(void* buf, size_t bytes, int root, void* ctx, void* stream);
 int smx_nccl_broadcast(void* buf, size_t bytes, int root, void* nccl_comm, void* stream);
+/* ncclCommGetAsyncError on the communicator: 0 = healthy, SMX_E_COMM = an
+ * asynchronous failure was recorded (smx_nccl_broadcast also checks it before
+ * every broadcast, so a sharded closure on a failed communicator returns
+ * SMX_E_COMM instead of hanging in the next collective). */
+int smx_nccl_async_error(void* nccl_comm);
 int smx_fw_sharded_block(int n, int world, int elem_bytes);
 size_t smx_fw_sharded_workspace_bytes(int rows, int ld, int elem_bytes, int block);
 int smx_fw_sharded(void* T, int n, int row0, int rows, int ld, int elem_bytes, int kind, int rank,

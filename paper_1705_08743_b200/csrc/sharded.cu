@@ -39,8 +39,10 @@ namespace {
 struct NcclApi {
     using BcastFn = int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
     using IntQueryFn = int (*)(void*, int*);
+    using AsyncErrFn = int (*)(void*, int*);   // ncclCommGetAsyncError(comm, ncclResult_t*)
     BcastFn bcast = nullptr;
     IntQueryFn count = nullptr, user_rank = nullptr;
+    AsyncErrFn async_error = nullptr;          // optional
     bool ok = false;
 };
 
@@ -55,6 +57,7 @@ const NcclApi& nccl() {
         a.bcast = reinterpret_cast<NcclApi::BcastFn>(dlsym(h, "ncclBroadcast"));
         a.count = reinterpret_cast<NcclApi::IntQueryFn>(dlsym(h, "ncclCommCount"));
         a.user_rank = reinterpret_cast<NcclApi::IntQueryFn>(dlsym(h, "ncclCommUserRank"));
+        a.async_error = reinterpret_cast<NcclApi::AsyncErrFn>(dlsym(h, "ncclCommGetAsyncError"));
         a.ok = a.bcast && a.count && a.user_rank;
         return a;
     }();
@@ -170,8 +173,23 @@ extern "C" {
 int smx_nccl_broadcast(void* buf, size_t bytes, int root, void* comm, void* stream) {
     const NcclApi& api = nccl();
     if (!api.ok) return SMX_E_COMM;
+    // a communicator that already failed asynchronously (a peer died, a
+    // network error) would hang the next collective: fail fast instead
+    if (api.async_error) {
+        int st = 0;
+        if (api.async_error(comm, &st) != 0 || st != 0) return SMX_E_COMM;
+    }
     const int rc = api.bcast(buf, buf, bytes, kNcclUint8, root, comm, as_stream(stream));
     return rc == 0 ? SMX_OK : SMX_E_COMM;
+}
+
+int smx_nccl_async_error(void* comm) {
+    const NcclApi& api = nccl();
+    if (!api.ok) return SMX_E_COMM;
+    if (!api.async_error) return SMX_OK;
+    int st = 0;
+    const int rc = api.async_error(comm, &st);
+    return (rc == 0 && st == 0) ? SMX_OK : SMX_E_COMM;
 }
 
 int smx_fw_sharded_block(int n, int world, int elem_bytes) {

@@ -316,6 +316,7 @@ def test_nccl_broadcast_on_torch_communicator(tmp_path):
         assert comm
         x = torch.arange(4096, dtype=torch.int32, device="cuda")
         want = x.clone()
+        assert lib.smx_nccl_async_error(comm) == 0
         rc = lib.smx_nccl_broadcast(x.data_ptr(), x.numel() * 4, 0, comm, _native.stream_ptr())
         assert rc == 0
         torch.cuda.synchronize()
