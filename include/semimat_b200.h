@@ -88,6 +88,15 @@ int smx_fw_u16(uint16_t* T, int n, int ld, int kind, void* workspace, size_t ws_
 int smx_fw_u32(uint32_t* T, int n, int ld, int kind, void* workspace, size_t ws_bytes,
                void* stream);
 
+/* Host -> device copy of `bytes` from `src` (any host memory) into `dst`,
+ * ordered on `stream`.  Page-locked sources (and copies under 8 MB) are one
+ * cudaMemcpyAsync; larger pageable ones are staged through the library's
+ * page-locked ring by a pool of memcpy threads (host_stage.cu: ~47 GB/s of
+ * memcpy against ~11 GB/s for a pageable cudaMemcpy on the pool's hosts),
+ * and the call returns once `src` has been read in full.  Used when a
+ * host-backed matrix moves to HBM. */
+int smx_copy_h2d(void* dst, const void* src, size_t bytes, void* stream);
+
 /* Closure of a matrix held in HOST memory: the same result as
  * copying host_in (n x ld, row-major, the reference's padded layout) into T,
  * smx_fw_*, and copying T back into host_out -- the user-visible work of
@@ -98,7 +107,9 @@ int smx_fw_u32(uint32_t* T, int n, int ld, int kind, void* workspace, size_t ws_
  * fw_host_run).  T (device, n x ld) is the working matrix and holds the
  * closure afterwards too.  host_out may equal host_in.  Stream-ordered:
  * host_out is complete once `stream` reaches the end of the call.  Page-locked
- * host buffers give the overlap; pageable ones work but copy synchronously.
+ * host buffers give the overlap; a pageable host_in is staged through the
+ * library's page-locked ring by a memcpy thread pool, overlapped the same way
+ * (host_stage.cu); a pageable host_out copies out synchronously.
  * `workspace`: smx_fw_host_workspace_bytes(n, ld, elem_bytes) bytes. */
 size_t smx_fw_host_workspace_bytes(int n, int ld, int elem_bytes);
 int smx_fw_host_u8(const uint8_t* host_in, uint8_t* host_out, uint8_t* T, int n, int ld, int kind,

@@ -67,6 +67,18 @@ def _from_edges(cls, dim: int, edges, width: int):
     return cls(dim, dim, width, data)
 
 
+def _to_host(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> host array.  Large ones land in page-locked memory
+    from torch's caching host allocator (55 GB/s, no first-touch page faults:
+    a fresh 2 GiB pageable array costs ~0.4 s of faults on the pool's hosts,
+    profiles/r02l_host_io.json)."""
+    if t.numel() * t.element_size() < (8 << 20):
+        return t.cpu().numpy()
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t)
+    return out.numpy()
+
+
 class _LaneMatrix:
     """Shared storage and entrywise algebra of the two saturated matrix types.
 
@@ -113,12 +125,15 @@ class _LaneMatrix:
 
     @property
     def _data(self) -> torch.Tensor:
-        """The device storage (moves a host-backed matrix to HBM first)."""
+        """The device storage (moves a host-backed matrix to HBM first: one
+        smx_copy_h2d, which stages a large pageable array through the
+        library's page-locked ring)."""
         if self._dev is None:
             src = np.ascontiguousarray(self._host)
-            if not src.flags.writeable:   # (torch.from_numpy wants a writeable array; only read here)
-                src = src.copy()
-            self._dev = torch.from_numpy(src).to(self._device)
+            dev = torch.empty(src.shape, dtype=_TORCH[self.width], device=self._device)
+            _native.check(_native.lib().smx_copy_h2d(dev.data_ptr(), src.ctypes.data, src.nbytes,
+                                                     _native.stream_ptr(self._device)), "smx_copy_h2d")
+            self._dev = dev
             self._host = None
         return self._dev
 
@@ -156,14 +171,14 @@ class _LaneMatrix:
         """Raw lane storage including padding columns, read-only: a view of
         the backing host array (host-backed, as the reference's view,
         antidist.py:68-73), else a host copy of the device storage."""
-        view = self._host.view() if self._dev is None else self._dev.cpu().numpy()
+        view = self._host.view() if self._dev is None else _to_host(self._dev)
         view.flags.writeable = False
         return view
 
     def to_numpy(self) -> np.ndarray:
         if self._dev is None:
             return np.array(self._host)
-        return self._dev.cpu().numpy()
+        return _to_host(self._dev)
 
     def copy(self):
         if self._dev is None:

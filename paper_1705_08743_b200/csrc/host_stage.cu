@@ -123,8 +123,22 @@ int HostStager::start(const void* src, void* dst, size_t row_bytes, const std::v
                       const cudaEvent_t* ev, cudaStream_t in) {
     src_ = static_cast<const char*>(src);
     dst_ = static_cast<char*>(dst);
-    row_bytes_ = row_bytes;
-    ends_ = ends;
+    ends_.clear();
+    for (int e : ends) ends_.push_back((size_t)e * row_bytes);
+    ev_ = ev;
+    in_ = in;
+    recorded_ = 0;
+    status_ = 0;
+    cudaError_t e = cudaGetDevice(&device_);
+    if (e != cudaSuccess) return (int)e;
+    th_ = std::thread([this] { run(); });
+    return SMX_OK;
+}
+
+int HostStager::start_bytes(const void* src, void* dst, size_t bytes, const cudaEvent_t* ev, cudaStream_t in) {
+    src_ = static_cast<const char*>(src);
+    dst_ = static_cast<char*>(dst);
+    ends_.assign(1, bytes);
     ev_ = ev;
     in_ = in;
     recorded_ = 0;
@@ -145,9 +159,9 @@ void HostStager::run() {
         if (rc == SMX_OK) {
             CopyPool& pool = CopyPool::get();
             size_t chunk = 0;
-            for (size_t g = 0, r0 = 0; g < ends_.size() && rc == SMX_OK; r0 = ends_[g], ++g) {
-                size_t off = r0 * row_bytes_;
-                const size_t end = (size_t)ends_[g] * row_bytes_;
+            for (size_t g = 0, b0 = 0; g < ends_.size() && rc == SMX_OK; b0 = ends_[g], ++g) {
+                size_t off = b0;
+                const size_t end = ends_[g];
                 while (off < end && rc == SMX_OK) {
                     const int slot = (int)(chunk % kSlots);
                     const size_t bytes = std::min(kSlotBytes, end - off);
@@ -194,5 +208,62 @@ int HostStager::finish() {
     if (th_.joinable()) th_.join();
     return status_;
 }
+
+namespace {
+struct StageStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, done = nullptr;
+    std::mutex mu;
+};
+int stage_stream(StageStream** out) {
+    static StageStream per_dev[64];
+    static std::mutex mu;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return (int)e;
+    if (dev < 0 || dev >= 64) return SMX_E_ARG;
+    std::lock_guard<std::mutex> lk(mu);
+    StageStream& st = per_dev[dev];
+    if (!st.s) {
+        if ((e = cudaStreamCreateWithFlags(&st.s, cudaStreamNonBlocking)) != cudaSuccess) return (int)e;
+        if ((e = cudaEventCreateWithFlags(&st.fork, cudaEventDisableTiming)) != cudaSuccess) return (int)e;
+        if ((e = cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming)) != cudaSuccess) return (int)e;
+    }
+    *out = &st;
+    return SMX_OK;
+}
+}  // namespace
+
+int h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t stream) {
+    if (bytes == 0) return SMX_OK;
+    if (dst == nullptr || src == nullptr) return SMX_E_ARG;
+    cudaError_t e;
+    // small or page-locked: one ordinary async copy
+    if (!is_pageable(src) || bytes < (8u << 20)) {
+        e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream);
+        return e == cudaSuccess ? SMX_OK : (int)e;
+    }
+    StageStream* st = nullptr;
+    SMX_TRY(stage_stream(&st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    // the copy stream starts after the caller's prior work (dst may be in use)
+    if ((e = cudaEventRecord(st->fork, stream)) != cudaSuccess) return (int)e;
+    if ((e = cudaStreamWaitEvent(st->s, st->fork, 0)) != cudaSuccess) return (int)e;
+    HostStager stager;
+    SMX_TRY(stager.start_bytes(src, dst, bytes, &st->done, st->s));
+    SMX_TRY(stager.finish());
+    e = cudaStreamWaitEvent(stream, st->done, 0);
+    return e == cudaSuccess ? SMX_OK : (int)e;
+}
+
+}  // namespace smx
+
+using namespace smx;
+
+extern "C" int smx_copy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
+    return h2d_staged(dst, src, bytes, as_stream(stream));
+}
+
+namespace smx {
 
 }  // namespace smx

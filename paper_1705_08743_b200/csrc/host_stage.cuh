@@ -31,6 +31,8 @@ public:
     // H2D into dst lands before ev[g] is recorded on `in`.
     int start(const void* src, void* dst, size_t row_bytes, const std::vector<int>& ends,
               const cudaEvent_t* ev, cudaStream_t in);
+    // One group of `bytes` bytes (ev[0] recorded after it).
+    int start_bytes(const void* src, void* dst, size_t bytes, const cudaEvent_t* ev, cudaStream_t in);
     // Blocks until group g's event has been recorded (or the stager failed).
     int wait_recorded(int g);
     // Joins the coordinator; returns its status.
@@ -41,8 +43,7 @@ private:
     void run();
     const char* src_ = nullptr;
     char* dst_ = nullptr;
-    size_t row_bytes_ = 0;
-    std::vector<int> ends_;
+    std::vector<size_t> ends_;   // byte offsets
     const cudaEvent_t* ev_ = nullptr;
     cudaStream_t in_ = nullptr;
     int device_ = 0;
@@ -52,5 +53,11 @@ private:
     int recorded_ = 0;   // groups whose event is recorded
     int status_ = 0;
 };
+
+// dst (device) <- src (host), `bytes`, ordered on `stream`: page-locked
+// sources are one async copy; pageable ones go through the staging ring
+// (~4x the pageable cudaMemcpy rate) and this call returns once every byte
+// has been copied out of `src` (so the caller may reuse it).
+int h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t stream);
 
 }  // namespace smx

@@ -45,4 +45,14 @@ def dev():
 
 res["device_ms"] = timed(dev) * 1e3
 res["cells_per_s_dropin"] = n ** 3 / res["dropin_ms"] * 1e3
+del pinned, out, src, w, m
+torch.cuda.empty_cache()
+# the product: (AntidistMatrix(n, n, 16, a) * AntidistMatrix(n, n, 16, b)).data
+mcfg = workloads.CONFIGS["c5_mul_u16"] if "c5_mul_u16" in workloads.CONFIGS else None
+if mcfg is not None:
+    a, b = workloads.make_inputs(mcfg, n)
+    res["mul_dropin_ms"] = timed(lambda: (AntidistMatrix(n, n, 16, a) * AntidistMatrix(n, n, 16, b)).data) * 1e3
+    da = torch.from_numpy(a).cuda()
+    db = torch.from_numpy(b).cuda()
+    res["mul_device_ms"] = timed(lambda: AntidistMatrix(n, n, 16, da) * AntidistMatrix(n, n, 16, db)) * 1e3
 print(json.dumps(res))
