@@ -238,9 +238,13 @@ int h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t stream) {
     if (bytes == 0) return SMX_OK;
     if (dst == nullptr || src == nullptr) return SMX_E_ARG;
     cudaError_t e;
-    // small or page-locked: one ordinary async copy
-    if (!is_pageable(src) || bytes < (8u << 20)) {
+    // small pageable: one ordinary copy (the driver has read the source when
+    // it returns); page-locked: one async copy, then wait for it, since the
+    // contract is that `src` may be reused or freed once this returns
+    const bool pageable = is_pageable(src);
+    if (!pageable || bytes < (8u << 20)) {
         e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream);
+        if (e == cudaSuccess && !pageable) e = cudaStreamSynchronize(stream);
         return e == cudaSuccess ? SMX_OK : (int)e;
     }
     StageStream* st = nullptr;
