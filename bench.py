@@ -784,7 +784,7 @@ def secondary(dev):
     int8_peak = 2 * 8192 ** 3 / t
     del a8
     tc = {"int8_peak_ops_per_s": int8_peak, "peak_source": "measured: torch._int_mm 8192^3 (cuBLAS)"}
-    for n_tc in (1024, 8192):
+    for n_tc in (1024, 2048, 4096, 8192):
         A = (torch.rand((n_tc, n_tc), device=dev) < 0.05).to(torch.uint8)
         Bt = (torch.rand((n_tc, n_tc), device=dev) < 0.05).to(torch.uint8)
         o = torch.zeros((n_tc, n_tc // 32), dtype=torch.int32, device=dev)
@@ -798,8 +798,9 @@ def secondary(dev):
         tc[f"n{n_tc}"] = {"kernel_us": t * 1e6, "ops_per_s": 2 * n_tc ** 3 / t,
                           "frac_of_int8_peak": 2 * n_tc ** 3 / t / int8_peak,
                           "eager_launch_us": te * 1e6}
-    tc["kernel"] = ("bool_i8_gemm_pair_kernel (split-K CTA pair) at 1024, bool_i8_gemm_kernel<256> at 8192; "
-                    "kernel_us = device time per launch, back-to-back launches replayed from one CUDA graph")
+    tc["kernel"] = ("bool_i8_gemm_pair_kernel (split-K CTA pair) at 1024, bool_i8_gemm_kernel (automatic tile "
+                    "width) above; kernel_us = device time per launch, back-to-back launches replayed from one "
+                    "CUDA graph")
     out["bool_tc_gemm_kernel"] = tc
     cfg = workloads.CONFIGS["c2_bool_warshall"]
     (t2,) = workloads.make_inputs(cfg)

@@ -328,3 +328,26 @@ def test_nccl_broadcast_on_torch_communicator(tmp_path):
         np.testing.assert_array_equal(got, ref)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nbytes", [1, 4097, (8 << 20) - 1, 8 << 20, (64 << 20) + 12345, (300 << 20) + 7])
+def test_copy_h2d_staged_exact(nbytes):
+    """smx_copy_h2d: pageable sources above 8 MB go through the page-locked
+    staging ring (several 64 MB slots, reused within and across calls),
+    smaller or page-locked ones are one copy; every byte lands, ragged sizes
+    included, and the source may be overwritten as soon as the call returns."""
+    lib = _native.lib()
+    rng = np.random.default_rng(nbytes % 1000)
+    src = rng.integers(0, 256, nbytes, dtype=np.uint8)
+    dst = torch.empty(nbytes + 64, dtype=torch.uint8, device="cuda")
+    dst.fill_(7)
+    for pinned in (False, True):
+        h = torch.from_numpy(src.copy())
+        if pinned:
+            h = h.pin_memory()
+        _native.check(lib.smx_copy_h2d(dst.data_ptr(), h.data_ptr(), nbytes, _native.stream_ptr()), "h2d")
+        h.fill_(0)                                   # (the call has read the source)
+        torch.cuda.synchronize()
+        got = dst[:nbytes].cpu().numpy()
+        np.testing.assert_array_equal(got, src, err_msg=f"pinned={pinned}")
+        assert (dst[nbytes:].cpu().numpy() == 7).all()   # nothing past the end
