@@ -810,6 +810,26 @@ def secondary(dev):
         t = cuda_time(lambda: fn(m2), 10, 2)
         out[f"c2_{eng}"] = {"n": cfg.n, "seconds": t, "cells_per_s": cfg.n ** 3 / t,
                             "frac_of_int8_tc_peak": 2 * cfg.n ** 3 / t / int8_peak}
+    # entrywise ops at C5 size, HBM-bound (one 16-byte packed
+    # SIMD pass), against the driver-measured HBM copy bandwidth
+    hbm = None
+    mp = REPO / "MEASURED_PEAKS.json"
+    if mp.exists():
+        try:
+            hbm = float(json.loads(mp.read_text()).get("hbm_gbs"))
+        except (TypeError, ValueError):
+            hbm = None
+    ne = 32768
+    ea = torch.randint(0, 65535, (ne, ne), dtype=torch.int32, device=dev).to(torch.uint16)
+    eb = torch.randint(0, 65535, (ne, ne), dtype=torch.int32, device=dev).to(torch.uint16)
+    ec = torch.empty_like(ea)
+    t = cuda_time(lambda: _native.check(lib.smx_lane_entrywise(
+        ea.data_ptr(), eb.data_ptr(), ec.data_ptr(), ne, ne, ne, 2, 1, 0, _native.stream_ptr(dev)), "|"), 10, 2)
+    gbs = 3 * ea.numel() * 2 / t / 1e9
+    out["entrywise_or_u16"] = {"n": ne, "seconds": t, "gbs": gbs, "hbm_gbs_peak": hbm,
+                               "frac_of_hbm": gbs / hbm if hbm else None,
+                               "op": "AntidistMatrix | (lanewise max, antidist.py:128-156), 3 x 2 GiB per call"}
+    del ea, eb, ec
     # the bit path's own ceiling: one LOP3.LUT (OR of AND on a 32-bit word)
     # per 32 cell-updates at the measured LOP3 issue rate
     bits = out["c2_bool_closure_bits"]
