@@ -23,6 +23,14 @@ __global__ void fill_kernel(T* t, long long count, T value) {
          i += (long long)gridDim.x * blockDim.x)
         t[i] = value;
 }
+// The same fill as 16-byte stores (the padded lane rows are whole 16-byte
+// blocks, so the matrix is too); HBM-bound.
+__global__ void fill16_kernel(uint4* t, long long chunks, uint32_t word) {
+    const uint4 v = make_uint4(word, word, word, word);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < chunks;
+         i += (long long)gridDim.x * blockDim.x)
+        t[i] = v;
+}
 
 template <typename T>
 __device__ __forceinline__ void fold_lane(T* cell, uint32_t value, bool take_max) {
@@ -60,9 +68,18 @@ __global__ void scatter_edges_kernel(const long long* __restrict__ edges, long l
 template <typename T>
 int from_edges(const long long* edges, long long m, T* t, int n, long long ld, bool anti, cudaStream_t s) {
     const long long count = (long long)n * ld;
-    long long blocks = (count + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    fill_kernel<T><<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(t, count, anti ? T(0) : T(Limit<T>::value));
+    const T fill = anti ? T(0) : T(Limit<T>::value);
+    if (aligned16(t) && (count * (long long)sizeof(T)) % 16 == 0) {
+        const long long chunks = count * (long long)sizeof(T) / 16;
+        long long blocks = (chunks + 255) / 256;
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        const uint32_t word = anti ? 0u : 0xFFFFFFFFu;   // S in every lane, or 0
+        fill16_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(reinterpret_cast<uint4*>(t), chunks, word);
+    } else {
+        long long blocks = (count + 255) / 256;
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        fill_kernel<T><<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(t, count, fill);
+    }
     SMX_LAUNCHED_OR_RETURN();
     if (m == 0) return SMX_OK;
     long long eb = (m + 255) / 256;

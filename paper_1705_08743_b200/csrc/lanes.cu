@@ -104,35 +104,108 @@ inline unsigned grid_1d(long long n, int threads = 256) {
 // ---- Boolean bridge ------------------------------------------------------------
 
 // from_boolmat: lane (r, c) = S if bit c of row r is set (c < cols), else 0;
-// padding lanes [cols, ld) = 0 (the anti-distance (+)-identity)
+// padding lanes [cols, ld) = 0 (the anti-distance (+)-identity).  One
+// 16-byte chunk of E = 16 / sizeof(T) lanes per thread-iteration: its E bits
+// sit in one word (E divides 32), spread to lanes of all-ones / zero.  Rows
+// are walked incrementally (no per-chunk division).  HBM-bound.
 template <typename T>
-__global__ void lanes_from_bits_kernel(const uint32_t* __restrict__ words, long long ld_w, T* __restrict__ out,
-                                       int rows, int cols, long long ld) {
-    const long long total = (long long)rows * ld;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long r = i / ld;
-        const int c = (int)(i - r * ld);
-        T v = 0;
-        if (c < cols && ((words[r * ld_w + (c >> 5)] >> (c & 31)) & 1u)) v = (T)Limit<T>::value;
-        out[i] = v;
+__device__ __forceinline__ uint4 spread_bits(uint32_t bits) {
+    constexpr int E = 16 / sizeof(T);
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if constexpr (sizeof(T) == 1) {   // 4 bits -> 4 bytes of 0x00 / 0xFF
+            const uint32_t nib = (bits >> (4 * q)) & 0xFu;
+            w[q] = ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;
+        } else if constexpr (sizeof(T) == 2) {   // 2 bits -> 2 halves
+            const uint32_t two = (bits >> (2 * q)) & 3u;
+            w[q] = ((two & 1u) ? 0xFFFFu : 0u) | ((two & 2u) ? 0xFFFF0000u : 0u);
+        } else {
+            w[q] = ((bits >> q) & 1u) ? 0xFFFFFFFFu : 0u;
+        }
+    }
+    (void)E;
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) lanes_from_bits_kernel(const uint32_t* __restrict__ words, long long ld_w,
+                                                              uint4* __restrict__ out, int rows, int cols, int cpr) {
+    constexpr int E = 16 / sizeof(T);
+    const long long total = (long long)rows * cpr;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    long long r = i / cpr;
+    int c = (int)(i - r * cpr);
+    const long long dr = stride / cpr;
+    const int dc = (int)(stride - dr * cpr);
+    for (; i < total; i += stride) {
+        const int col0 = c * E;
+        uint32_t bits = 0;
+        if (col0 < cols) {
+            bits = (__ldg(words + r * ld_w + (col0 >> 5)) >> (col0 & 31)) & ((1u << E) - 1u);   // (E <= 16)
+            const int valid = cols - col0;
+            if (valid < E) bits &= (1u << valid) - 1u;
+        }
+        out[i] = spread_bits<T>(bits);
+        c += dc;
+        r += dr;
+        if (c >= cpr) { c -= cpr; ++r; }
     }
 }
 
 // to_boolmat: bit c of row r = (lane (r, c) > 0) for c < cols; every other
-// bit of the row's ld_w words is 0.  One warp per 32-column word.
+// bit of the row's ld_w words is 0.  One output word (32 lanes: 32 / 64 / 128
+// bytes of 16-byte loads) per thread-iteration.  HBM-bound.
 template <typename T>
-__global__ void lanes_to_bits_kernel(const T* __restrict__ in, long long ld, uint32_t* __restrict__ words,
-                                     long long ld_w, int rows, int cols) {
-    const int lane = threadIdx.x & 31;
-    const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+__device__ __forceinline__ uint32_t nonzero_bits16(uint4 v) {   // one 16-byte chunk -> 16 / sizeof(T) bits
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t out = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if constexpr (sizeof(T) == 1) {
+            const uint32_t nz = __vcmpne4(w[q], 0u);   // 0xFF per nonzero byte
+            out |= ((nz & 0x01u) | ((nz >> 7) & 0x02u) | ((nz >> 14) & 0x04u) | ((nz >> 21) & 0x08u)) << (4 * q);
+        } else if constexpr (sizeof(T) == 2) {
+            const uint32_t nz = __vcmpne2(w[q], 0u);
+            out |= ((nz & 0x1u) | ((nz >> 15) & 0x2u)) << (2 * q);
+        } else {
+            out |= (w[q] != 0u ? 1u : 0u) << q;
+        }
+    }
+    return out;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) lanes_to_bits_kernel(const T* __restrict__ in, long long ld,
+                                                            uint32_t* __restrict__ words, long long ld_w, int rows,
+                                                            int cols) {
+    constexpr int E = 16 / sizeof(T), CH = 32 / E;   // chunks per output word
     const long long total = (long long)rows * ld_w;
-    for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total; w += nwarps) {
-        const long long r = w / ld_w;
-        const int c = (int)(w - r * ld_w) * 32 + lane;
-        const bool set = c < cols && in[r * ld + c] != 0;
-        const uint32_t word = __ballot_sync(0xFFFFFFFFu, set);
-        if (lane == 0) words[w] = word;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    long long r = i / ld_w;
+    int w = (int)(i - r * ld_w);
+    const long long dr = stride / ld_w;
+    const int dw = (int)(stride - dr * ld_w);
+    for (; i < total; i += stride) {
+        const int col0 = w * 32;
+        uint32_t word = 0;
+        if (col0 < cols) {
+            const uint4* src = reinterpret_cast<const uint4*>(in + r * ld + col0);
+            const int nch = min(CH, (cols - col0 + E - 1) / E);   // (ld is whole chunks: reads stay in the row)
+#pragma unroll
+            for (int q = 0; q < CH; ++q)
+                if (q < nch) word |= nonzero_bits16<T>(__ldg(src + q)) << (q * E);
+            const int valid = cols - col0;
+            if (valid < 32) word &= (1u << valid) - 1u;
+        }
+        words[i] = word;
+        w += dw;
+        r += dr;
+        if (w >= ld_w) { w -= (int)ld_w; ++r; }
     }
 }
 
@@ -261,14 +334,18 @@ int smx_lane_op(const void* A, const void* B, void* C, long long nlanes, int ele
 int smx_lanes_from_bits(const uint32_t* words, int ld_w, void* out, int rows, int cols, int ld, int elem_bytes,
                         void* stream) {
     if (rows < 0 || cols < 0 || ld < cols || (long long)ld_w * 32 < cols) return SMX_E_ARG;
+    if (elem_bytes != 1 && elem_bytes != 2 && elem_bytes != 4) return SMX_E_ARG;
     if (rows == 0 || ld == 0) return SMX_OK;
-    const long long total = (long long)rows * ld;
+    if (((long long)ld * elem_bytes) % 16 != 0) return SMX_E_ARG;   // whole 128-bit lane blocks
+    if (!aligned16(out)) return SMX_E_ALIGN;
+    const int cpr = (int)((long long)ld * elem_bytes / 16);
+    const long long total = (long long)rows * cpr;
     cudaStream_t s = as_stream(stream);
+    uint4* o = static_cast<uint4*>(out);
     switch (elem_bytes) {
-        case 1: lanes_from_bits_kernel<uint8_t><<<grid_1d(total), 256, 0, s>>>(words, ld_w, (uint8_t*)out, rows, cols, ld); break;
-        case 2: lanes_from_bits_kernel<uint16_t><<<grid_1d(total), 256, 0, s>>>(words, ld_w, (uint16_t*)out, rows, cols, ld); break;
-        case 4: lanes_from_bits_kernel<uint32_t><<<grid_1d(total), 256, 0, s>>>(words, ld_w, (uint32_t*)out, rows, cols, ld); break;
-        default: return SMX_E_ARG;
+        case 1: lanes_from_bits_kernel<uint8_t><<<grid_1d(total), 256, 0, s>>>(words, ld_w, o, rows, cols, cpr); break;
+        case 2: lanes_from_bits_kernel<uint16_t><<<grid_1d(total), 256, 0, s>>>(words, ld_w, o, rows, cols, cpr); break;
+        default: lanes_from_bits_kernel<uint32_t><<<grid_1d(total), 256, 0, s>>>(words, ld_w, o, rows, cols, cpr); break;
     }
     SMX_RETURN_LAUNCH();
 }
@@ -276,14 +353,16 @@ int smx_lanes_from_bits(const uint32_t* words, int ld_w, void* out, int rows, in
 int smx_lanes_to_bits(const void* in, int ld, uint32_t* words, int ld_w, int rows, int cols, int elem_bytes,
                       void* stream) {
     if (rows < 0 || cols < 0 || ld < cols || (long long)ld_w * 32 < cols) return SMX_E_ARG;
+    if (elem_bytes != 1 && elem_bytes != 2 && elem_bytes != 4) return SMX_E_ARG;
     if (rows == 0 || ld_w == 0) return SMX_OK;
-    const long long total = (long long)rows * ld_w * 32;
+    if (((long long)ld * elem_bytes) % 16 != 0) return SMX_E_ARG;   // whole 128-bit lane blocks
+    if (!aligned16(in)) return SMX_E_ALIGN;
+    const long long total = (long long)rows * ld_w;
     cudaStream_t s = as_stream(stream);
     switch (elem_bytes) {
         case 1: lanes_to_bits_kernel<uint8_t><<<grid_1d(total), 256, 0, s>>>((const uint8_t*)in, ld, words, ld_w, rows, cols); break;
         case 2: lanes_to_bits_kernel<uint16_t><<<grid_1d(total), 256, 0, s>>>((const uint16_t*)in, ld, words, ld_w, rows, cols); break;
-        case 4: lanes_to_bits_kernel<uint32_t><<<grid_1d(total), 256, 0, s>>>((const uint32_t*)in, ld, words, ld_w, rows, cols); break;
-        default: return SMX_E_ARG;
+        default: lanes_to_bits_kernel<uint32_t><<<grid_1d(total), 256, 0, s>>>((const uint32_t*)in, ld, words, ld_w, rows, cols); break;
     }
     SMX_RETURN_LAUNCH();
 }

@@ -50,4 +50,14 @@ sec = t_of(lambda: _native.check(lib.smx_bits_entrywise(wa.data_ptr(), wb.data_p
                                                         n // 32, 0, st), "bits or"))
 gbs = 3 * wa.numel() * 4 / sec / 1e9
 res["bits_or"] = {"n": n, "ms": sec * 1e3, "gbs": gbs, "frac_of_hbm": gbs / peak if peak else None}
+# the Boolean bridge: bits -> u16 lanes (from_boolmat) and back (to_boolmat)
+lanes = torch.empty((n, n), dtype=torch.uint16, device="cuda")
+sec = t_of(lambda: _native.check(lib.smx_lanes_from_bits(wa.data_ptr(), n // 32, lanes.data_ptr(), n, n - 5, n, 2,
+                                                         st), "from_bits"))
+gbs = (wa.numel() * 4 + lanes.numel() * 2) / sec / 1e9
+res["bridge_from_bits_u16"] = {"n": n, "ms": sec * 1e3, "gbs": gbs, "frac_of_hbm": gbs / peak if peak else None}
+sec = t_of(lambda: _native.check(lib.smx_lanes_to_bits(lanes.data_ptr(), n, wc.data_ptr(), n // 32, n, n - 5, 2,
+                                                       st), "to_bits"))
+gbs = (wa.numel() * 4 + lanes.numel() * 2) / sec / 1e9
+res["bridge_to_bits_u16"] = {"n": n, "ms": sec * 1e3, "gbs": gbs, "frac_of_hbm": gbs / peak if peak else None}
 print(json.dumps(res))
