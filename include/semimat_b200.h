@@ -376,6 +376,12 @@ int smx_bool_warshall_batched(uint32_t* T, int batch, int n, int ld_w, long long
 int smx_fw_batched(void* T, int batch, int n, int ld, long long stride, int elem_bytes, int kind,
                    void* stream);
 
+/* The first invalid edge of an edge list on the device (edges: m x 3 int64
+ * rows (u, v, w)): a vertex outside [0, n) or a weight outside [0, limit].
+ * *first (device, u64) receives its index, or m if every edge is valid; the
+ * caller reports it with the reference's message (antidist.py:201-208). */
+int smx_edges_first_invalid(const long long* edges, long long m, int n, long long limit,
+                            unsigned long long* first, void* stream);
 /* ---- construction (antidist.py:191-211, :294-309) ---------------------
  * Fill the n x ld matrix T with the (+)-identity (0 anti / S dist, padding
  * included) and fold m weighted edges edges[3*i .. 3*i+2] = (u, v, w) into it,

@@ -95,6 +95,7 @@ _SIGS.update({
     "smx_nccl_broadcast": ([c_void_p, c_size_t, c_int, c_void_p, c_void_p], c_int),
     "smx_nccl_async_error": ([c_void_p], c_int),
     "smx_copy_h2d": ([c_void_p, c_void_p, c_size_t, c_void_p], c_int),
+    "smx_edges_first_invalid": ([c_void_p, c_longlong, c_int, c_longlong, c_void_p, c_void_p], c_int),
     "smx_fw_sharded_block": ([c_int, c_int, c_int], c_int),
     "smx_fw_sharded_workspace_bytes": ([c_int, c_int, c_int, c_int], c_size_t),
     "smx_fw_sharded": ([c_void_p] + [c_int] * 9 + [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p], c_int),

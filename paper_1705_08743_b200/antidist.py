@@ -38,31 +38,49 @@ def dtype_for(width: int):
 
 def _from_edges(cls, dim: int, edges, width: int):
     """Validate like the reference (first offending edge, in edge order, same
-    messages: antidist.py:201-208) on the host, then fill + scatter on the GPU."""
+    messages: antidist.py:201-208), then fill + scatter on the GPU.  Large
+    edge lists are validated on the device (smx_edges_first_invalid) after
+    one staged upload; only the first offender's row is looked at on the
+    host, to word its message."""
     if dim < 1:
         raise ValueError(f"matrix dimensions must be positive, got {dim}x{dim}")
     limit = sat_limit(width)
     if not isinstance(edges, np.ndarray):
         edges = list(edges)
     arr = np.asarray(edges, dtype=np.int64).reshape(-1, 3) if len(edges) else np.zeros((0, 3), np.int64)
-    u, v, w = arr[:, 0], arr[:, 1], arr[:, 2]
-    bad_u = (u < 0) | (u >= dim)
-    bad_v = (v < 0) | (v >= dim)
-    bad_w = (w < 0) | (w > limit)
-    bad = bad_u | bad_v | bad_w
-    if bad.any():
-        i = int(np.argmax(bad))
-        if bad_u[i]:
-            raise ValueError(f"source vertex {int(u[i])} out of range [0, {dim})")
-        if bad_v[i]:
-            raise ValueError(f"target vertex {int(v[i])} out of range [0, {dim})")
-        raise ValueError(f"weight {int(w[i])} outside [0, {limit}]")
+    arr = np.ascontiguousarray(arr)
+    m = arr.shape[0]
+
+    def reject(i: int):
+        u, v, w = (int(x) for x in arr[i])
+        if not 0 <= u < dim:
+            raise ValueError(f"source vertex {u} out of range [0, {dim})")
+        if not 0 <= v < dim:
+            raise ValueError(f"target vertex {v} out of range [0, {dim})")
+        raise ValueError(f"weight {w} outside [0, {limit}]")
+
+    if m < (1 << 16):   # small lists: host check, nothing launched for a bad one
+        u, v, w = arr[:, 0], arr[:, 1], arr[:, 2]
+        bad = (u < 0) | (u >= dim) | (v < 0) | (v >= dim) | (w < 0) | (w > limit)
+        if bad.any():
+            reject(int(np.argmax(bad)))
     dev = _native.require_cuda()
+    lib = _native.lib()
+    st = _native.stream_ptr(dev)
+    dev_edges = torch.empty(arr.shape, dtype=torch.int64, device=dev)
+    if m:   # (staged through the page-locked ring when large, smx_copy_h2d)
+        _native.check(lib.smx_copy_h2d(dev_edges.data_ptr(), arr.ctypes.data, arr.nbytes, st), "smx_copy_h2d")
+    if m >= (1 << 16):
+        first = torch.empty(1, dtype=torch.int64, device=dev)
+        _native.check(lib.smx_edges_first_invalid(dev_edges.data_ptr(), m, dim, limit, first.data_ptr(), st),
+                      "smx_edges_first_invalid")
+        i = int(first.item())
+        if i < m:
+            reject(i)
     data = torch.empty((dim, -(-dim // LANES[width]) * LANES[width]), dtype=_TORCH[width], device=dev)
-    dev_edges = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
-    _native.check(_native.lib().smx_from_edges(
-        dev_edges.data_ptr(), arr.shape[0], data.data_ptr(), dim, data.shape[1], width // 8,
-        _native.SMX_DIST if cls._PAD_IS_LIMIT else _native.SMX_ANTI, _native.stream_ptr(dev)),
+    _native.check(lib.smx_from_edges(
+        dev_edges.data_ptr(), m, data.data_ptr(), dim, data.shape[1], width // 8,
+        _native.SMX_DIST if cls._PAD_IS_LIMIT else _native.SMX_ANTI, st),
         "smx_from_edges")
     return cls(dim, dim, width, data)
 

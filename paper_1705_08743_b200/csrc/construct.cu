@@ -65,6 +65,20 @@ __global__ void scatter_edges_kernel(const long long* __restrict__ edges, long l
     }
 }
 
+// First invalid edge in edge order (the reference validates in order and
+// reports the first offender, antidist.py:201-208): a vertex outside [0, n)
+// or a weight outside [0, limit].  *first = the smallest offending index, or
+// left at its initial value (the caller sets it to m).
+__global__ void first_invalid_edge_kernel(const long long* __restrict__ edges, long long m, long long n,
+                                          long long limit, unsigned long long* first) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long u = edges[3 * e], v = edges[3 * e + 1], w = edges[3 * e + 2];
+        if (u < 0 || u >= n || v < 0 || v >= n || w < 0 || w > limit)
+            atomicMin(first, (unsigned long long)e);
+    }
+}
+
 template <typename T>
 int from_edges(const long long* edges, long long m, T* t, int n, long long ld, bool anti, cudaStream_t s) {
     const long long count = (long long)n * ld;
@@ -104,4 +118,18 @@ extern "C" int smx_from_edges(const long long* edges, long long m, void* T, int 
         case 4: return from_edges<uint32_t>(edges, m, (uint32_t*)T, n, ld, anti, s);
         default: return SMX_E_ARG;
     }
+}
+
+extern "C" int smx_edges_first_invalid(const long long* edges, long long m, int n, long long limit,
+                                       unsigned long long* first, void* stream) {
+    if (m < 0 || n < 0 || first == nullptr) return SMX_E_ARG;
+    cudaStream_t s = as_stream(stream);
+    const unsigned long long init = (unsigned long long)m;
+    cudaError_t e = cudaMemcpyAsync(first, &init, sizeof(init), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return (int)e;
+    if (m == 0) return SMX_OK;
+    long long blocks = (m + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    first_invalid_edge_kernel<<<(unsigned)blocks, 256, 0, s>>>(edges, m, n, limit, first);
+    SMX_RETURN_LAUNCH();
 }

@@ -351,3 +351,32 @@ def test_copy_h2d_staged_exact(nbytes):
         got = dst[:nbytes].cpu().numpy()
         np.testing.assert_array_equal(got, src, err_msg=f"pinned={pinned}")
         assert (dst[nbytes:].cpu().numpy() == 7).all()   # nothing past the end
+
+
+@pytest.mark.parametrize("kind", ["source", "target", "weight", "none"])
+def test_from_edges_large_lists_validated_on_device(kind, oracle_lib):
+    """Edge lists of >= 2^16 edges are validated on the device
+    (smx_edges_first_invalid): the first offender in edge order is reported
+    with the reference's message (antidist.py:201-208), even when a later
+    edge is also bad; a valid list builds the same matrix as the host path."""
+    rng = np.random.default_rng(3)
+    n, m = 700, 100_000
+    e = np.stack([rng.integers(0, n, m), rng.integers(0, n, m), rng.integers(0, 256, m)], axis=1).astype(np.int64)
+    if kind != "none":
+        col, val = {"source": (0, n + 5), "target": (1, -2), "weight": (2, 256)}[kind]
+        e[70_001, col] = val
+        e[90_000, 0] = -1             # a later offender that must not be the one reported
+        msg = {"source": rf"source vertex {n + 5} out of range \[0, {n}\)",
+               "target": rf"target vertex -2 out of range \[0, {n}\)",
+               "weight": r"weight 256 outside \[0, 255\]"}[kind]
+        with pytest.raises(ValueError, match=msg):
+            AntidistMatrix.from_edges(n, e, 8)
+        return
+    got = AntidistMatrix.from_edges(n, e, 8).data
+    small = AntidistMatrix.from_edges(n, [tuple(x) for x in e[:1000]], 8)   # (host-validated path)
+    want = np.zeros((n, 704), dtype=np.uint8)
+    best = np.full((n, n), -1, dtype=np.int64)
+    np.maximum.at(best, (e[:, 0], e[:, 1]), 255 - e[:, 2])
+    want[:, :n] = np.where(best >= 0, best, 0)
+    np.testing.assert_array_equal(got, want)
+    assert small.rows == n
