@@ -42,7 +42,10 @@ def to_binary(m) -> bytes:
     if isinstance(m, (AntidistMatrix, DistMatrix)):
         tag = _TYPE_ANTIDIST if isinstance(m, AntidistMatrix) else _TYPE_DIST
         header = _HEADER.pack(MAGIC, tag, m.width, m.rows, m.cols)
-        entries = m._data[:, : m.cols].contiguous().cpu().numpy()
+        if m.host_backed:   # (no round trip through HBM for a matrix still on its host array)
+            entries = np.ascontiguousarray(m._host[:, : m.cols])
+        else:
+            entries = m._data[:, : m.cols].contiguous().cpu().numpy()
         return header + entries.astype(_LANE_DTYPES[m.width], copy=False).tobytes()
     raise TypeError(f"cannot serialize {type(m).__name__}")
 
