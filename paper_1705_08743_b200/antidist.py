@@ -85,6 +85,18 @@ def _from_edges(cls, dim: int, edges, width: int):
     return cls(dim, dim, width, data)
 
 
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(dev, which: int) -> torch.cuda.Stream:
+    """Side streams per device for the streamed host product's copies in (0)
+    and out (1)."""
+    key = (torch.device(dev).index, which)
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return _COPY_STREAMS[key]
+
+
 def _to_host(t: torch.Tensor) -> np.ndarray:
     """Device tensor -> host array.  Large ones land in page-locked memory
     from torch's caching host allocator (55 GB/s, no first-touch page faults:
@@ -304,6 +316,60 @@ class _LaneMatrix:
 
     # -- shared product / closure plumbing -----------------------------------
 
+    # Host-backed left operands of at least this many lanes take the streamed
+    # host product (_mul_host); smaller ones move to HBM and stay there.
+    _HOST_MUL_MIN = 1 << 24
+
+    def _mul(self, other, anti: bool):
+        """C = self (x) other: device-resident, or streamed from a large
+        host-backed left operand (the reference's own call on numpy arrays)."""
+        from . import engines
+        if self._dev is None and self.rows * self.padded_cols >= self._HOST_MUL_MIN:
+            return self._mul_host(other, anti)
+        out = engines.lane_mul(self._data, other._data, self.cols, self.width, anti=anti)
+        return type(self)(self.rows, other.cols, self.width, out)
+
+    def _mul_host(self, other, anti: bool):
+        """Row groups of the host-backed left operand stream in (staged,
+        smx_copy_h2d) while the previous group's product runs, and each
+        group's result rows stream out on a copy stream into page-locked
+        memory: the PCIe copies overlap the products, and the result is
+        host-backed like the closure's (transitive_closure)."""
+        from . import engines
+        dev = self._device
+        lib = _native.lib()
+        b = other._data                      # (resident for every group)
+        src = np.ascontiguousarray(self._host)
+        rows, ld_a, cols_p = self.rows, src.shape[1], b.shape[1]
+        out = torch.empty((rows, cols_p), dtype=_TORCH[self.width], pin_memory=True)
+        s = torch.cuda.current_stream(dev)
+        xs, cs = _copy_stream(dev, 0), _copy_stream(dev, 1)   # copies in / out
+        # 4 row groups of whole 128-row tiles: more groups shorten the first
+        # copy in and the last copy out, but each group repacks B (8 groups
+        # cost +18 ms of device time at n = 32768, 4 groups +3 ms)
+        quarter = -(-rows // 4)
+        group = max(128, -(-quarter // 128) * 128)
+        xs.wait_stream(s)   # (b and earlier work first)
+        for r0 in range(0, rows, group):
+            r1 = min(rows, r0 + group)
+            # the copy in runs on its own stream, so staging group g + 1 never
+            # waits for group g's product; the allocator keeps a_g alive
+            # until the product on s has read it (record_stream)
+            with torch.cuda.stream(xs):
+                a_g = torch.empty((r1 - r0, ld_a), dtype=_TORCH[self.width], device=dev)
+                _native.check(lib.smx_copy_h2d(a_g.data_ptr(), src[r0:r1].ctypes.data,
+                                               a_g.numel() * a_g.element_size(), xs.cuda_stream), "smx_copy_h2d")
+            s.wait_stream(xs)
+            a_g.record_stream(s)
+            c_g = engines.lane_mul(a_g, b, self.cols, self.width, anti=anti)
+            cs.wait_stream(s)
+            with torch.cuda.stream(cs):
+                out[r0:r1].copy_(c_g, non_blocking=True)
+            c_g.record_stream(cs)
+        s.wait_stream(cs)
+        s.synchronize()
+        return type(self)(rows, other.cols, self.width, out.numpy(), device=dev)
+
     def _mul_checks(self, other):
         if self.width != other.width:
             raise ValueError(f"width mismatch: {self.width} vs {other.width}")
@@ -425,9 +491,7 @@ class AntidistMatrix(_LaneMatrix):
         if not isinstance(other, AntidistMatrix):
             return NotImplemented
         self._mul_checks(other)
-        from . import engines
-        out = engines.lane_mul(self._data, other._data, self.cols, self.width, anti=True)
-        return AntidistMatrix(self.rows, other.cols, self.width, out)
+        return self._mul(other, anti=True)
 
 
 class DistMatrix(_LaneMatrix):
@@ -459,6 +523,4 @@ class DistMatrix(_LaneMatrix):
         if not isinstance(other, DistMatrix):
             return NotImplemented
         self._mul_checks(other)
-        from . import engines
-        out = engines.lane_mul(self._data, other._data, self.cols, self.width, anti=False)
-        return DistMatrix(self.rows, other.cols, self.width, out)
+        return self._mul(other, anti=False)

@@ -197,3 +197,35 @@ def test_dropin_staged_ring_reuse_matches_device_closure():
             got = AntidistMatrix(8192, 8192, 16, t).transitive_closure()
             assert got.host_backed
             assert sha(got.data) == sha(want)
+
+
+@pytest.mark.parametrize("width,kind,shape", [(16, "anti", (6000, 3000, 2050)), (8, "dist", (4096, 4096, 4096)),
+                                              (32, "anti", (9000, 2000, 1300))])
+def test_streamed_host_product_matches_device(width, kind, shape):
+    """A large host-backed left operand takes the streamed host product (row
+    groups staged in while the previous group's product runs, results copied
+    out into page-locked memory): the result is host-backed and equals the
+    device-resident product of the same operands, ragged shapes included."""
+    m, k, n = shape
+    rng = np.random.default_rng(m + n)
+    lim = (1 << width) - 1
+    dt = {8: np.uint8, 16: np.uint16, 32: np.uint32}[width]
+    cls = AntidistMatrix if kind == "anti" else DistMatrix
+    pad = 128 // width
+
+    def rnd(r, c):
+        a = np.full((r, -(-c // pad) * pad), 0 if kind == "anti" else lim, dtype=dt)
+        v = rng.integers(1, min(lim, 1000), (r, c))
+        keep = rng.random((r, c)) < 0.3
+        a[:, :c] = np.where(keep, (lim - v) if kind == "anti" else v, a[:, :c]).astype(dt)
+        return a
+
+    a, b = rnd(m, k), rnd(k, n)
+    ha, hb = cls(m, k, width, a), cls(k, n, width, b)
+    assert ha.rows * ha.padded_cols >= cls._HOST_MUL_MIN
+    got = ha * hb
+    assert got.host_backed
+    want = cls(m, k, width, torch.from_numpy(a).cuda()) * cls(k, n, width, torch.from_numpy(b).cuda())
+    assert not want.host_backed
+    np.testing.assert_array_equal(got.data, want.data)
+    np.testing.assert_array_equal(ha.data, a)    # the inputs are untouched
