@@ -627,15 +627,14 @@ def run_ours(args, world, rank, local_rank):
                 return AntidistMatrix(n, n, cfg.width, host).transitive_closure().data
             h2d = d2h = host.nbytes
         else:
-            pa, pb = torch.from_numpy(a_host).pin_memory(), torch.from_numpy(b_host).pin_memory()
-            res_host = torch.empty((n, b_host.shape[1]), dtype=pa.dtype).pin_memory()
-
+            # the reference's own product call on numpy arrays:
+            # (AntidistMatrix(n, n, w, a) * AntidistMatrix(n, n, w, b)).data
+            # (antidist.py:226-250): the streamed host product (left operand
+            # staged in by row groups beside the products, result rows out)
             def e2e_step():
-                ma = AntidistMatrix(n, n, cfg.width, pa.to(dev, non_blocking=True))
-                mb = AntidistMatrix(n, n, cfg.width, pb.to(dev, non_blocking=True))
-                res_host.copy_((ma * mb)._data, non_blocking=True)
-            h2d = (pa.numel() + pb.numel()) * pa.element_size()
-            d2h = res_host.numel() * res_host.element_size()
+                return (AntidistMatrix(n, n, cfg.width, a_host) * AntidistMatrix(n, n, cfg.width, b_host)).data
+            h2d = a_host.nbytes + b_host.nbytes
+            d2h = n * b_host.shape[1] * b_host.itemsize
         e2e_steps = 2 if n >= 16384 else 5
         # 3 warm-up calls (the product's public path records one replay graph
         # per buffer layout the caching allocator hands out)
@@ -650,6 +649,9 @@ def run_ours(args, world, rank, local_rank):
         result["e2e"] = {"value": units_per_step / e2e_secs, "unit": UNIT,
                          "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                          "ms_per_step": e2e_secs * 1e3}
+        if cfg.op != "closure":
+            result["e2e"]["call"] = ("(AntidistMatrix(n, n, 16, a) * AntidistMatrix(n, n, 16, b)).data "
+                                     "(pageable numpy in, page-locked result out)")
         if cfg.op == "closure":
             result["e2e"]["call"] = ("AntidistMatrix(n, n, 16, host_ndarray).transitive_closure().data "
                                      "(pageable numpy in, page-locked result out)")
