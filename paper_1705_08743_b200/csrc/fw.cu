@@ -782,7 +782,7 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
             // side stream; the row panel waits for both.  The two parts
             // write disjoint columns of rows K1, and the pivot touches only
             // T[K1, K1].
-            // Automatic = off: measured (tools/perf_split3a.py) a gain only
+            // Automatic = off: measured (tools/perf_switch.py smx_set_fw_split_3a 0 2) a gain only
             // at n = 4096 (2.88 -> 2.69-2.79 ms) and small losses at 1024,
             // 2048, 6144 and 8192 (17.50 -> 17.65 ms): the extra launches and
             // the second stream's 3a CTAs beside the pivot cost about what
