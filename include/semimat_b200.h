@@ -48,6 +48,11 @@ int smx_version(void);
 const char* smx_error_string(int code);
 /* Number of kernels this library has launched in the process so far. */
 unsigned long long smx_launch_count(void);
+/* Output tiles per CTA of the packed semiring GEMM (phase 3 and the large
+ * products): 1 (default) or 2 adjacent row tiles walked through one
+ * continuous operand ring.  Results are identical.  Returns the previous
+ * setting. */
+int smx_set_packed_tiles_per_cta(int tpc);
 /* The u16/u32 semiring kernels run a k-tile with the 1-instruction update
  * c = min(c, a + b) when the CTA has verified that every staged lane of that
  * k-tile is below 2^(w-1) (so a + b cannot reach S and the clamp is a

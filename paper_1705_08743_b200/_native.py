@@ -24,6 +24,7 @@ _SIGS = {
     "smx_error_string": ([c_int], ctypes.c_char_p),
     "smx_launch_count": ([], ctypes.c_ulonglong),
     "smx_set_bounded_fastpath": ([c_int], c_int),
+    "smx_set_packed_tiles_per_cta": ([c_int], c_int),
     "smx_set_fw_lookahead": ([c_int], c_int),
     "smx_set_graphs": ([c_int], c_int),
     "smx_set_fw_side_lite": ([c_int], c_int),

@@ -86,7 +86,12 @@ struct PackedArgsT {
     int skip_tile0, skip_tiles;   // tiles skipped inside the window
     const int* cert;              // nullable: nonzero = operands packed in the shifted encoding
     int col_tile0;                // first output column tile of the launch (grid x counts from it)
+    int mtiles;                   // row tiles of the launch (after the skipped ones)
 };
+
+// smx_set_packed_tiles_per_cta (abi.cu): output tiles per CTA of the packed
+// GEMM (1 or 2).
+int packed_tiles_per_cta();
 
 // ---- pack kernels -----------------------------------------------------------
 // Canonical (distance-form) lane value of one storage cell.
@@ -223,13 +228,19 @@ __device__ __forceinline__ void pk_bulk_load(void* dst, const void* src, uint32_
 // result is bit-identical).  The producer prefetches an interior C tile into
 // shared memory with row bulk copies while the K loop runs, so neither the C
 // read latency nor the operand-flag reads sit on a warp's critical path.
-template <typename T>
+// TPC: output tiles per CTA, walked in sequence through one continuous
+// stage ring: the producer streams the next tile's first stages while the
+// consumers fold and store the previous tile, so a tile's ring fill no longer
+// sits between two tiles of the same CTA.  The tiles of a CTA are adjacent
+// row tiles of one column tile (the same B tiles, hot in L2).
+template <typename T, int TPC>
 __global__ void __launch_bounds__(PackedCfg<T>::THREADS, PackedCfg<T>::MINB)
 packed_gemm_kernel(const PackedArgsT<T> p) {
     using L = Lane<T>;
     using G = PackedCfg<T>;
     constexpr int BM = G::BM, BNW = G::BNW, BK = G::BK, TM = G::TM, TNW = G::TNW, HW = G::HW;
     constexpr int ST = G::STAGES;
+    static_assert(TPC == 1 || !G::CSMEM, "the C-in-shared-memory variant runs one tile per CTA");
 
     extern __shared__ __align__(128) uint4 smem_raw[];
     uint32_t* As = reinterpret_cast<uint32_t*>(smem_raw);              // [ST][BK][BM]
@@ -241,12 +252,22 @@ packed_gemm_kernel(const PackedArgsT<T> p) {
     uint32_t* flag = reinterpret_cast<uint32_t*>(cbar + 1);
 
     const int tid = threadIdx.x, lane = tid & 31;
-    int mt = p.row_tile0 + blockIdx.y;
-    if (mt >= p.skip_tile0) mt += p.skip_tiles;
     const int nt = p.col_tile0 + blockIdx.x;
     const int KT = p.KT;
-    const int row0 = mt * BM, col0 = nt * G::BN;
-    const bool c_async = G::CSMEM && p.accumulate && KT > 0 && row0 + BM <= p.M && col0 + G::BN <= p.N;
+    const int col0 = nt * G::BN;
+    // this CTA's row tiles: compacted indices blockIdx.y * TPC + t of the
+    // launch's p.mtiles (the skipped tiles excluded)
+    int mts[TPC];
+    int ntiles = 0;
+#pragma unroll
+    for (int t = 0; t < TPC; ++t) {
+        const int idx = (int)blockIdx.y * TPC + t;
+        int mt = p.row_tile0 + idx;
+        if (mt >= p.skip_tile0) mt += p.skip_tiles;
+        mts[t] = mt;
+        if (idx < p.mtiles) ntiles = t + 1;
+    }
+    const bool c_async = G::CSMEM && p.accumulate && KT > 0 && mts[0] * BM + BM <= p.M && col0 + G::BN <= p.N;
 
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
@@ -260,11 +281,10 @@ packed_gemm_kernel(const PackedArgsT<T> p) {
 
     if (tid >= G::CONSUMERS) {
         // ---- producer warp ----
-        const uint32_t* a_src = p.Ap + (size_t)mt * KT * G::A_TILE_WORDS;
         const int first = KT < ST ? KT : ST;
-        auto issue = [&](int kt, int s) {
-            pk_bulk_load(As + s * G::A_TILE_WORDS, a_src + (size_t)kt * G::A_TILE_WORDS, G::A_TILE_WORDS * 4,
-                         &full[s]);
+        auto issue = [&](int mt, int kt, int s) {
+            pk_bulk_load(As + s * G::A_TILE_WORDS, p.Ap + ((size_t)mt * KT + kt) * G::A_TILE_WORDS,
+                         G::A_TILE_WORDS * 4, &full[s]);
             pk_bulk_load(Bs + s * G::B_TILE_WORDS, p.Bp + ((size_t)kt * p.NT + nt) * G::B_TILE_WORDS,
                          G::B_TILE_WORDS * 4, &full[s]);
         };
@@ -272,34 +292,39 @@ packed_gemm_kernel(const PackedArgsT<T> p) {
         // complete_tx may land before its expect_tx (the tx-count goes
         // transiently negative; the phase cannot complete until the arrive).
         if (lane == 0)
-            for (int kt = 0; kt < first; ++kt) issue(kt, kt);
-        for (int kb = 0; kb < KT; kb += 32) {
-            // bounded flags of 32 k-tiles in one round trip (one per lane)
-            const int k = kb + lane;
-            // (u8: always -- its update is the 1-instruction form)
-            const bool f = k < KT && (L::kOneInstr || (p.allow_bounded &&
-                           ((p.cert != nullptr && *p.cert != 0) ||
-                            (p.fA[(size_t)mt * KT + k] != 0 && p.fB[(size_t)k * p.NT + nt] != 0))));
-            const uint32_t fmask = __ballot_sync(0xFFFFFFFFu, f);
-            if (lane == 0) {
-                const int kend = KT - kb < 32 ? KT : kb + 32;
-                for (int kt = kb; kt < kend; ++kt) {
-                    const int s = kt % ST;
-                    if (kt >= ST) pk_mbar_wait(&empty[s], ((kt / ST) - 1) & 1);
-                    flag[s] = (fmask >> (kt - kb)) & 1u;
-                    pk_mbar_expect_tx(&full[s], (G::A_TILE_WORDS + G::B_TILE_WORDS) * 4);
-                    if (kt >= first) issue(kt, s);
-                    // the C tile goes behind the first ring fill, so the
-                    // first operand tiles arrive first
-                    if (c_async && kt == first - 1) {
-                        pk_mbar_expect_tx(cbar, G::C_TILE_BYTES);
-                        for (int r = 0; r < BM; ++r)
-                            pk_bulk_load(Cs + r * G::BN, p.C + (long long)(row0 + r) * p.ldc + col0,
-                                         G::BN * (int)sizeof(T), cbar);
+            for (int kt = 0; kt < first; ++kt) issue(mts[0], kt, kt);
+        for (int t = 0; t < ntiles; ++t) {
+            const int mt = mts[t];
+            for (int kb = 0; kb < KT; kb += 32) {
+                // bounded flags of 32 k-tiles in one round trip (one per lane)
+                const int k = kb + lane;
+                // (u8: always -- its update is the 1-instruction form)
+                const bool f = k < KT && (L::kOneInstr || (p.allow_bounded &&
+                               ((p.cert != nullptr && *p.cert != 0) ||
+                                (p.fA[(size_t)mt * KT + k] != 0 && p.fB[(size_t)k * p.NT + nt] != 0))));
+                const uint32_t fmask = __ballot_sync(0xFFFFFFFFu, f);
+                if (lane == 0) {
+                    const int kend = KT - kb < 32 ? KT : kb + 32;
+                    for (int kt = kb; kt < kend; ++kt) {
+                        const int g = t * KT + kt;          // position in the CTA's stage sequence
+                        const int s = g % ST;
+                        if (g >= ST) pk_mbar_wait(&empty[s], ((g / ST) - 1) & 1);
+                        flag[s] = (fmask >> (kt - kb)) & 1u;
+                        pk_mbar_expect_tx(&full[s], (G::A_TILE_WORDS + G::B_TILE_WORDS) * 4);
+                        if (g >= first) issue(mt, kt, s);
+                        // the C tile goes behind the first ring fill, so the
+                        // first operand tiles arrive first
+                        if (c_async && g == first - 1) {
+                            const int row0 = mt * BM;
+                            pk_mbar_expect_tx(cbar, G::C_TILE_BYTES);
+                            for (int r = 0; r < BM; ++r)
+                                pk_bulk_load(Cs + r * G::BN, p.C + (long long)(row0 + r) * p.ldc + col0,
+                                             G::BN * (int)sizeof(T), cbar);
+                        }
                     }
                 }
+                __syncwarp();
             }
-            __syncwarp();
         }
         return;
     }
@@ -307,78 +332,82 @@ packed_gemm_kernel(const PackedArgsT<T> p) {
     const int tc = tid % G::TCOLS, tr = tid / G::TCOLS;
     const bool anti = p.anti != 0;
 
-    uint32_t acc[TM][TNW];
+    for (int t = 0; t < ntiles; ++t) {
+        const int row0 = mts[t] * BM;
+        uint32_t acc[TM][TNW];
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
+        for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TNW; ++j) acc[i][j] = L::kIdentityWord;
+            for (int j = 0; j < TNW; ++j) acc[i][j] = L::kIdentityWord;
 
-    for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % ST;
-        pk_mbar_wait(&full[s], (kt / ST) & 1);
-        const bool bounded = flag[s] != 0;
-        const uint32_t* Ab = As + s * G::A_TILE_WORDS + tr * TM;
-        const uint32_t* Bb = Bs + s * G::B_TILE_WORDS + tc * HW;
-        if (bounded) {
+        for (int kt = 0; kt < KT; ++kt) {
+            const int g = t * KT + kt;
+            const int s = g % ST;
+            pk_mbar_wait(&full[s], (g / ST) & 1);
+            const bool bounded = flag[s] != 0;
+            const uint32_t* Ab = As + s * G::A_TILE_WORDS + tr * TM;
+            const uint32_t* Bb = Bs + s * G::B_TILE_WORDS + tc * HW;
+            if (bounded) {
 #pragma unroll
-            for (int kk = 0; kk < BK; ++kk) {
-                const uint4 b0 = *reinterpret_cast<const uint4*>(Bb + kk * BNW);
-                const uint4 b1 = *reinterpret_cast<const uint4*>(Bb + kk * BNW + BNW / 2);
-                const uint4 av = *reinterpret_cast<const uint4*>(Ab + kk * BM);
-                const uint32_t b[TNW] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-                const uint32_t a[TM] = {av.x, av.y, av.z, av.w};
+                for (int kk = 0; kk < BK; ++kk) {
+                    const uint4 b0 = *reinterpret_cast<const uint4*>(Bb + kk * BNW);
+                    const uint4 b1 = *reinterpret_cast<const uint4*>(Bb + kk * BNW + BNW / 2);
+                    const uint4 av = *reinterpret_cast<const uint4*>(Ab + kk * BM);
+                    const uint32_t b[TNW] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                    const uint32_t a[TM] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+                    for (int i = 0; i < TM; ++i)
+#pragma unroll
+                        for (int j = 0; j < TNW; ++j) acc[i][j] = L::step_bounded(acc[i][j], b[j], a[i]);
+                }
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < BK; ++kk) {
+                    const uint4 b0 = *reinterpret_cast<const uint4*>(Bb + kk * BNW);
+                    const uint4 b1 = *reinterpret_cast<const uint4*>(Bb + kk * BNW + BNW / 2);
+                    const uint4 av = *reinterpret_cast<const uint4*>(Ab + kk * BM);
+                    const uint32_t b[TNW] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                    const uint32_t a[TM] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+                    for (int i = 0; i < TM; ++i) {
+                        const uint32_t sa = ~a[i];   // u16: splat(S - a), S = 0xFFFF per lane (u8: unused)
+#pragma unroll
+                        for (int j = 0; j < TNW; ++j) acc[i][j] = L::step(acc[i][j], b[j], a[i], sa);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) pk_mbar_arrive(&empty[s]);
+        }
+
+        // ---- fold C in and store ----
+        if constexpr (!L::kOneInstr) {
+            if (p.cert != nullptr && *p.cert != 0) {
 #pragma unroll
                 for (int i = 0; i < TM; ++i)
 #pragma unroll
-                    for (int j = 0; j < TNW; ++j) acc[i][j] = L::step_bounded(acc[i][j], b[j], a[i]);
+                    for (int j = 0; j < TNW; ++j) acc[i][j] = L::from_shifted(acc[i][j]);
             }
-        } else {
+        }
+        if (c_async) pk_mbar_wait(cbar, 0);
 #pragma unroll
-            for (int kk = 0; kk < BK; ++kk) {
-                const uint4 b0 = *reinterpret_cast<const uint4*>(Bb + kk * BNW);
-                const uint4 b1 = *reinterpret_cast<const uint4*>(Bb + kk * BNW + BNW / 2);
-                const uint4 av = *reinterpret_cast<const uint4*>(Ab + kk * BM);
-                const uint32_t b[TNW] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-                const uint32_t a[TM] = {av.x, av.y, av.z, av.w};
+        for (int i = 0; i < TM; ++i) {
+            const int grow = row0 + tr * TM + i;
+            if (grow >= p.M) continue;
+            T* crow = p.C + (long long)grow * p.ldc;
 #pragma unroll
-                for (int i = 0; i < TM; ++i) {
-                    const uint32_t sa = ~a[i];   // u16: splat(S - a), S = 0xFFFF per lane (u8: unused)
+            for (int g = 0; g < 2; ++g) {
+                const int cc = (g * (BNW / 2) + tc * HW) * L::kCellsPerWord;   // cell offset in the tile
+                uint32_t* w = &acc[i][g * HW];
+                if (c_async || p.accumulate) {
+                    uint32_t c[HW];
+                    if (c_async) load_c_group<T, HW>(Cs + (tr * TM + i) * G::BN, cc, G::BN, anti, c);
+                    else load_c_group<T, HW>(crow, col0 + cc, p.N, anti, c);
 #pragma unroll
-                    for (int j = 0; j < TNW; ++j) acc[i][j] = L::step(acc[i][j], b[j], a[i], sa);
+                    for (int j = 0; j < HW; ++j) w[j] = L::fold(w[j], c[j]);
                 }
+                store_c_group<T, HW>(crow, col0 + cc, p.N, anti, w);
             }
-        }
-        __syncwarp();
-        if (lane == 0) pk_mbar_arrive(&empty[s]);
-    }
-
-    // ---- fold C in and store ----
-    if constexpr (!L::kOneInstr) {
-        if (p.cert != nullptr && *p.cert != 0) {
-#pragma unroll
-            for (int i = 0; i < TM; ++i)
-#pragma unroll
-                for (int j = 0; j < TNW; ++j) acc[i][j] = L::from_shifted(acc[i][j]);
-        }
-    }
-    if (c_async) pk_mbar_wait(cbar, 0);
-#pragma unroll
-    for (int i = 0; i < TM; ++i) {
-        const int grow = row0 + tr * TM + i;
-        if (grow >= p.M) continue;
-        T* crow = p.C + (long long)grow * p.ldc;
-#pragma unroll
-        for (int g = 0; g < 2; ++g) {
-            const int cc = (g * (BNW / 2) + tc * HW) * L::kCellsPerWord;   // cell offset in the tile
-            uint32_t* w = &acc[i][g * HW];
-            if (c_async || p.accumulate) {
-                uint32_t c[HW];
-                if (c_async) load_c_group<T, HW>(Cs + (tr * TM + i) * G::BN, cc, G::BN, anti, c);
-                else load_c_group<T, HW>(crow, col0 + cc, p.N, anti, c);
-#pragma unroll
-                for (int j = 0; j < HW; ++j) w[j] = L::fold(w[j], c[j]);
-            }
-            store_c_group<T, HW>(crow, col0 + cc, p.N, anti, w);
         }
     }
 }
@@ -523,13 +552,20 @@ inline int packed_run(T* C, int M, int N, int K, long long ldc, int kind, int ac
     }
     const int mtiles = row_tiles - a.skip_tiles;
     if (mtiles <= 0) return SMX_OK;
-    SMX_TRY(set_max_smem((const void*)packed_gemm_kernel<T>, G::SMEM));
+    a.mtiles = mtiles;
+    const int tpc = packed_tiles_per_cta();
     // launch_kernel: a launch on the look-ahead side stream (3a) carries the
     // side stream's priority into a captured graph (PriorityScope)
     // (a plain launch: carrying the side stream's priority into the replay
     // graph for the look-ahead's 3a measured no different, 17.51 vs 17.54 ms
     // at n = 8192)
-    packed_gemm_kernel<T><<<dim3(col_tiles, mtiles), G::THREADS, G::SMEM, s>>>(a);
+    if (tpc == 2 && !G::CSMEM) {
+        SMX_TRY(set_max_smem((const void*)packed_gemm_kernel<T, 2>, G::SMEM));
+        packed_gemm_kernel<T, 2><<<dim3(col_tiles, (mtiles + 1) / 2), G::THREADS, G::SMEM, s>>>(a);
+    } else {
+        SMX_TRY(set_max_smem((const void*)packed_gemm_kernel<T, 1>, G::SMEM));
+        packed_gemm_kernel<T, 1><<<dim3(col_tiles, mtiles), G::THREADS, G::SMEM, s>>>(a);
+    }
     SMX_RETURN_LAUNCH();
 }
 

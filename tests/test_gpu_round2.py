@@ -380,3 +380,38 @@ def test_from_edges_large_lists_validated_on_device(kind, oracle_lib):
     want[:, :n] = np.where(best >= 0, best, 0)
     np.testing.assert_array_equal(got, want)
     assert small.rows == n
+
+
+@pytest.mark.parametrize("width", [8, 16, 32])
+def test_packed_two_tiles_per_cta_matches(width, oracle_lib):
+    """The packed GEMM walking two row tiles per CTA through one continuous
+    ring (smx_set_packed_tiles_per_cta(2)) gives the same bits as one tile per
+    CTA and the oracle: closures (odd tile counts, skipped pivot rows) and
+    ragged products, anti and dist."""
+    lib = _native.lib()
+    rng = np.random.default_rng(width + 5)
+    cls = {"anti": AntidistMatrix, "dist": DistMatrix}
+    old = lib.smx_set_packed_tiles_per_cta(1)
+    try:
+        for n in (1100, 2176):
+            t = _random_lane(rng, n, width, "anti", p=0.02)
+            want = oracle_lib.semiring_close(t, width, "anti")
+            for tpc in (1, 2):
+                lib.smx_set_packed_tiles_per_cta(tpc)
+                got = AntidistMatrix(n, n, width, torch.from_numpy(t).cuda()).transitive_closure().data
+                np.testing.assert_array_equal(got, want, err_msg=f"closure n={n} w={width} tpc={tpc}")
+        for (m, k, n), kind in (((1500, 900, 1100), "anti"), ((1300, 2100, 700), "dist")):
+            ident = 0 if kind == "anti" else (1 << width) - 1
+            a = np.ascontiguousarray(_random_lane(rng, max(m, k), width, kind)[:m, :_pad(width, k)])
+            b = np.ascontiguousarray(_random_lane(rng, max(k, n), width, kind)[:k, :_pad(width, n)])
+            a[:, k:] = ident   # (the padding lanes hold the (+)-identity)
+            b[:, n:] = ident
+            want = oracle_lib.semiring_mul(a, b, k, width, kind)
+            for tpc in (1, 2):
+                lib.smx_set_packed_tiles_per_cta(tpc)
+                got = (cls[kind](m, k, width, torch.from_numpy(a).cuda()) *
+                       cls[kind](k, n, width, torch.from_numpy(b).cuda())).data
+                np.testing.assert_array_equal(got, want, err_msg=f"mul {m}x{k}x{n} {kind} w={width} tpc={tpc}")
+    finally:
+        lib.smx_set_packed_tiles_per_cta(old)
+    assert lib.smx_set_packed_tiles_per_cta(3) < 0
