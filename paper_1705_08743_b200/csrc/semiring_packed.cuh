@@ -600,50 +600,66 @@ inline int semiring_gemm_packed_u16(const uint16_t* A, const uint16_t* B, uint16
 }
 
 // Global sparse-bounded certificate of a u16 / u32 operand (rows x cols, ld):
-// clears *cert if any lane in distance form is neither S nor < 2^14 (u16) /
-// 2^30 (u32) (Lane::cert_ok).  Concurrent writers only store 0.
 template <typename T>
-__global__ void cert_kernel(const T* __restrict__ X, int rows, int cols, long long ld, int anti,
-                            int* __restrict__ cert) {
+__device__ __forceinline__ bool cert_operand(const T* __restrict__ X, int rows, int cols, long long ld, uint32_t m,
+                                             long long i0, long long stride) {
     using L = Lane<T>;
     constexpr int E = 16 / (int)sizeof(T);
     const int cpr = (cols + E - 1) / E;
     const long long total = (long long)rows * cpr;
-    const uint32_t m = anti ? 0xFFFFFFFFu : 0u;
     bool ok = true;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(i / cpr), c = (int)(i % cpr) * E;
-        uint4 w = __ldg(reinterpret_cast<const uint4*>(X + r * ld + c));
+    if (i0 >= total) return ok;
+    // (row, chunk) walked incrementally: one division per thread, not per chunk
+    long long r = i0 / cpr;
+    int c = (int)(i0 - r * cpr);
+    const long long dr = stride / cpr;
+    const int dc = (int)(stride - dr * cpr);
+    for (long long i = i0; i < total; i += stride) {
+        uint4 w = __ldg(reinterpret_cast<const uint4*>(X + r * ld + (long long)c * E));
         w.x ^= m; w.y ^= m; w.z ^= m; w.w ^= m;
-        if (c + E > cols) {   // cells >= cols: identity (S), which certifies
+        if ((c + 1) * E > cols) {   // cells >= cols: identity (S), which certifies
             uint32_t e[4] = {w.x, w.y, w.z, w.w};
-            for (int j = cols - c; j < E; ++j) set_word_cell<T>(e, j, L::kS);
+            for (int j = cols - c * E; j < E; ++j) set_word_cell<T>(e, j, L::kS);
             w = make_uint4(e[0], e[1], e[2], e[3]);
         }
         ok = ok && L::cert_ok(w.x) && L::cert_ok(w.y) && L::cert_ok(w.z) && L::cert_ok(w.w);
+        c += dc;
+        r += dr;
+        if (c >= cpr) { c -= cpr; ++r; }
     }
+    return ok;
+}
+
+// clears *cert if any lane in distance form is neither S nor < 2^14 (u16) /
+// 2^30 (u32) (Lane::cert_ok).  Concurrent writers only store 0.  One launch
+// covers both operands: blocks [0, gridDim.x / 2) read X, the rest Y.
+template <typename T>
+__global__ void __launch_bounds__(256) cert_kernel(const T* __restrict__ X, int xr, int xc, long long ldx,
+                                                   const T* __restrict__ Y, int yr, int yc, long long ldy, int anti,
+                                                   int* __restrict__ cert) {
+    const uint32_t m = anti ? 0xFFFFFFFFu : 0u;
+    const bool second = Y != nullptr && blockIdx.x >= gridDim.x / 2;
+    const int nblk = Y != nullptr ? gridDim.x / 2 : gridDim.x;
+    const int bx = second ? blockIdx.x - nblk : blockIdx.x;
+    const long long i0 = (long long)bx * blockDim.x + threadIdx.x, stride = (long long)nblk * blockDim.x;
+    const bool ok = second ? cert_operand<T>(Y, yr, yc, ldy, m, i0, stride)
+                           : (X == nullptr || cert_operand<T>(X, xr, xc, ldx, m, i0, stride));
     if (!__all_sync(0xFFFFFFFFu, ok) && (threadIdx.x & 31) == 0) *cert = 0;
 }
 
 // Reset *cert and run the certificate over an operand pair (either may be
-// nullptr): the caller's packs and products then read *cert.
+// nullptr) in one launch: the caller's packs and products then read *cert.
 template <typename T>
 inline int run_cert(const T* X, int xr, int xc, long long ldx, const T* Y, int yr, int yc, long long ldy, int anti,
                     int* cert, cudaStream_t s) {
     static_assert(sizeof(T) >= 2, "u8 is always the 1-instruction form");
     cudaError_t e = cudaMemsetAsync(cert, 0xFF, sizeof(int), s);
     if (e != cudaSuccess) return (int)e;
-    const int blocks = 4 * sm_count();
-    if (X) {
-        cert_kernel<T><<<blocks, 256, 0, s>>>(X, xr, xc, ldx, anti, cert);
-        SMX_LAUNCHED_OR_RETURN();
-    }
-    if (Y) {
-        cert_kernel<T><<<blocks, 256, 0, s>>>(Y, yr, yc, ldy, anti, cert);
-        SMX_LAUNCHED_OR_RETURN();
-    }
-    return SMX_OK;
+    if (X == nullptr && Y == nullptr) return SMX_OK;
+    if (X == nullptr) { X = Y; xr = yr; xc = yc; ldx = ldy; Y = nullptr; }
+    const int per = 4 * sm_count();
+    cert_kernel<T><<<Y ? 2 * per : per, 256, 0, s>>>(X, xr, xc, ldx, Y, yr, yc, ldy, anti, cert);
+    SMX_RETURN_LAUNCH();
 }
 
 // Public u16 product on the packed kernel.  K is processed in chunks so the
