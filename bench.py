@@ -800,6 +800,20 @@ def secondary(dev):
         tc[f"n{n_tc}"] = {"kernel_us": t * 1e6, "ops_per_s": 2 * n_tc ** 3 / t,
                           "frac_of_int8_peak": 2 * n_tc ** 3 / t / int8_peak,
                           "eager_launch_us": te * 1e6}
+    # C1-shaped products many per launch (bool_mul_many on 128-multiple
+    # shapes): the batched split-K pair, three CTAs per SM
+    nb = 16
+    A = (torch.rand((nb * 1024, 1024), device=dev) < 0.05).to(torch.uint8)
+    Bt = (torch.rand((nb * 1024, 1024), device=dev) < 0.05).to(torch.uint8)
+    o = torch.zeros((nb * 1024, 32), dtype=torch.int32, device=dev)
+    f = lambda: _native.check(lib.smx_bool_gemm_i8_batched(  # noqa: E731
+        A.data_ptr(), Bt.data_ptr(), o.data_ptr(), nb, 1024, 1024, 1024, 1024, 1024, 32, 0,
+        _native.stream_ptr(dev)), "tc batched")
+    t = graph_time(f, 10, 10) / nb
+    tc["n1024_batch16"] = {"kernel_us_per_product": t * 1e6, "ops_per_s": 2 * 1024 ** 3 / t,
+                           "frac_of_int8_peak": 2 * 1024 ** 3 / t / int8_peak,
+                           "note": "16 independent 1024^3 products per launch (smx_bool_gemm_i8_batched)"}
+    del A, Bt, o
     tc["kernel"] = ("bool_i8_gemm_pair_kernel (split-K CTA pair) at 1024, bool_i8_gemm_kernel (automatic tile "
                     "width) above; kernel_us = device time per launch, back-to-back launches replayed from one "
                     "CUDA graph")

@@ -289,6 +289,18 @@ int smx_fw_sharded_u16(uint16_t* Tpanel, int n, int row0, int rows, int ld, int 
 int smx_bool_gemm_i8(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* C_bits,
                      int M, int N, int K, int lda, int ldbt, int ldc, int accumulate,
                      void* stream);
+/* `batch` Boolean products A_i (M x K) * B_i (K x N) in one call on the
+ * tensor cores: A stacked as batch * M bit rows (lda_w words each), B as
+ * batch * K rows, C as batch * M rows (ldc_w = N / 32).  M and N multiples
+ * of 128, 128 < K <= 65536.  Workspace:
+ * smx_bool_mul_tc_batched_workspace_bytes(batch, M, N, K) bytes. */
+size_t smx_bool_mul_tc_batched_workspace_bytes(int batch, int M, int N, int K);
+int smx_bool_mul_tc_batched(const uint32_t* A, const uint32_t* B, uint32_t* C, int batch, int M, int N, int K,
+                            int lda_w, int ldb_w, int ldc_w, void* workspace, size_t ws_bytes, void* stream);
+/* The same on unpacked operands: A (batch * M rows of 0/1 bytes), B^T
+ * (batch * N rows), packed-bit C (batch * M rows); one split-K pair launch. */
+int smx_bool_gemm_i8_batched(const uint8_t* A, const uint8_t* Bt, uint32_t* C_bits, int batch, int M, int N,
+                             int K, int lda, int ldbt, int ldc, int accumulate, void* stream);
 /* Output tile width (N) of the tensor-core Boolean GEMM: 0 = automatic (the
  * widest of 256 / 128 / 64 that still gives every SM a tile), or force 64,
  * 128 or 256.  Results are identical.  Returns the previous setting. */

@@ -7,7 +7,9 @@ graphs (pkg/tests/test_acceptance.py:28-85) -- would be bound by one launch
 (and one host round trip) per matrix on a GPU, so this module stacks
 same-shaped matrices and runs the batched kernels of csrc/lanes.cu:
 
-* ``bool_mul_many(As, Bs)``     BoolMatrix products      (smx_bool_mul_batched)
+* ``bool_mul_many(As, Bs)``     BoolMatrix products      (smx_bool_mul_tc_batched on the
+                                tensor cores for 128-multiple shapes, else
+                                smx_bool_mul_batched)
 * ``bool_closure_many(Ms)``     Warshall, n <= 512       (smx_bool_warshall_batched)
 * ``closure_many(Ms)``          Floyd-Warshall of AntidistMatrix / DistMatrix,
                                 n <= 128                 (smx_fw_batched)
@@ -79,9 +81,33 @@ def bool_mul_many(As, Bs) -> list[BoolMatrix]:
     if not same or a0.cols != b0.rows:
         return [a * b for a, b in zip(As, Bs)]      # per-pair validation and messages
     dev = a0.device
-    out = bool_mul_stacked(torch.stack([a._words.to(dev) for a in As]),
-                           torch.stack([b._words.to(dev) for b in Bs]), a0.cols, b0.cols)
+    a_st = torch.stack([a._words.to(dev) for a in As])
+    b_st = torch.stack([b._words.to(dev) for b in Bs])
+    if a0.rows % 128 == 0 and b0.cols % 128 == 0 and 128 < a0.cols <= 65536:
+        out = bool_mul_stacked_tc(a_st, b_st, a0.cols, b0.cols)   # tensor cores, one launch
+    else:
+        out = bool_mul_stacked(a_st, b_st, a0.cols, b0.cols)
     return [BoolMatrix(a0.rows, b0.cols, out[i]) for i in range(len(As))]
+
+
+def bool_mul_stacked_tc(a_words: torch.Tensor, b_words: torch.Tensor, inner: int, cols: int) -> torch.Tensor:
+    """The stacked products on the tensor cores (smx_bool_mul_tc_batched: one
+    unpack of every A, the fused B^T unpacks, then one split-K pair launch
+    for all products).  M and ``cols`` multiples of 128, 128 < inner <= 65536."""
+    from .boolmat import _stride_words
+    batch, m = a_words.shape[0], a_words.shape[1]
+    if b_words.shape[0] != batch or b_words.shape[1] != inner:
+        raise ValueError("stacked operands disagree in batch or inner size")
+    a_words, b_words = a_words.contiguous(), b_words.contiguous()
+    lib = _native.lib()
+    out = torch.empty((batch, m, _stride_words(cols)), dtype=torch.int32, device=a_words.device)
+    nbytes = lib.smx_bool_mul_tc_batched_workspace_bytes(batch, m, cols, inner)
+    ws = _native.workspace(nbytes, a_words.device)
+    _native.check(lib.smx_bool_mul_tc_batched(
+        a_words.data_ptr(), b_words.data_ptr(), out.data_ptr(), batch, m, cols, inner, a_words.shape[2],
+        b_words.shape[2], out.shape[2], ws.data_ptr(), nbytes, _native.stream_ptr(a_words.device)),
+        "smx_bool_mul_tc_batched")
+    return out
 
 
 def bool_closure_many(Ms) -> list[BoolMatrix]:

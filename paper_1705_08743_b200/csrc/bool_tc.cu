@@ -135,6 +135,10 @@ struct TcArgs {
     int accumulate;
     int skip_tile0, skip_tiles;
     int splits;          // split-K factor (gridDim.z); > 1 ORs into a pre-set output
+    // batched products (pair kernel): products of batch_mt row tiles each are
+    // stacked in A and C; product i's B^T rows start at i * bt_item_rows of
+    // the stacked B^T operand (0 = one product)
+    int batch_mt, bt_item_rows;
     // development trace (smx_tc_trace_arm; nullptr otherwise): per CTA,
     // globaltimer at entry and exit, and for CTA 0 clock64 at each phase
     unsigned long long* trace;
@@ -336,7 +340,14 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
 // [0, 64) and [64, 128).
 constexpr int kPairBN = 128;
 constexpr int kPairThreads = 256;
-constexpr int kPairStages = 6;                         // 6 x 32 KB ring
+// Stage ring depth: a single product is one wave of CTAs, one per SM, and
+// takes 6 stages of 32 KB (every k-block of C1 in flight at once); batched
+// products run many waves, and 2 stages (~66 KB) let three CTAs share an SM
+// so one CTA's loads and epilogue overlap the others' MMAs: 16 C1 products
+// per launch 2.81 -> 1.43 us each with 2 stages (3 stages: 1.65 us;
+// tools/perf_c1_batched.py, profiles/r04d_c1_batched_stages.json).
+constexpr int kPairStagesSingle = 6;
+constexpr int kPairStagesBatched = 2;
 constexpr uint32_t kPairRecvBytes = 64 * (kPairBN / 32) * 4;   // 64 rows x 4 words
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -365,6 +376,7 @@ __device__ __forceinline__ uint32_t bits_of(const uint32_t (&r)[32]) {
 // CTA issues 96 KB instead of 128: no faster -- 3.79 against 3.49 us per
 // launch, the same per-CTA timeline -- so the operand stream is bound where
 // the bytes land, not where they are issued; removed.)
+template <int kPairStages>
 __global__ void __launch_bounds__(kPairThreads, 1)
 bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                          const TcArgs p) {
@@ -389,6 +401,8 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     if (p.trace && threadIdx.x == 0) p.trace[16 + 2 * cta] = gtimer();
     if (tr0 && threadIdx.x == 0) p.trace[0] = clock64();
     const int m0 = blockIdx.y * kTcBM, n0 = blockIdx.x * kPairBN;
+    // (batched: this CTA's product's B^T rows)
+    const int nb0 = n0 + (p.batch_mt > 0 ? (int)(blockIdx.y / p.batch_mt) * p.bt_item_rows : 0);
     const int nkb_all = (p.K + kTcBK - 1) / kTcBK;
     const int half = (nkb_all + 1) / 2;
     const int kb_lo = (int)rank * half;
@@ -422,7 +436,7 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
         for (int kb = 0; kb < first_fill; ++kb) {
             mbar_expect_tx(&full[kb], A_BYTES + B_BYTES);
             tma_load_2d(&mapA, &full[kb], sA + kb * A_BYTES, (kb_lo + kb) * kTcBK, m0);
-            tma_load_2d(&mapB, &full[kb], sB + kb * B_BYTES, (kb_lo + kb) * kTcBK, n0);
+            tma_load_2d(&mapB, &full[kb], sB + kb * B_BYTES, (kb_lo + kb) * kTcBK, nb0);
         }
     }
     if (warp == 2) {
@@ -450,7 +464,7 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
             mbar_wait(&empty[s], ph ^ 1);
             mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
             tma_load_2d(&mapA, &full[s], sA + s * A_BYTES, (kb_lo + kb) * kTcBK, m0);
-            tma_load_2d(&mapB, &full[s], sB + s * B_BYTES, (kb_lo + kb) * kTcBK, n0);
+            tma_load_2d(&mapB, &full[s], sB + s * B_BYTES, (kb_lo + kb) * kTcBK, nb0);
         }
         if (tr0) p.trace[2] = clock64();
     } else if (threadIdx.x == 32) {
@@ -628,14 +642,15 @@ static int launch_tc(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long 
 
 // Split-K pair launch (packed-bit output, no row skip).  The caller has
 // checked the shape (see bool_i8_gemm).
+template <int kPairStages>
 static int launch_tc_pair(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long long lda, long long ldbt,
-                          cudaStream_t s, bool pdl) {
+                          cudaStream_t s, bool pdl, int bt_rows = -1) {
     CUtensorMap mA, mB;
     SMX_TRY(make_map(&mA, A, a.M, a.K, lda, kTcBM));
-    SMX_TRY(make_map(&mB, Bt, a.N, a.K, ldbt, kPairBN));
+    SMX_TRY(make_map(&mB, Bt, bt_rows < 0 ? a.N : bt_rows, a.K, ldbt, kPairBN));
     constexpr size_t smem = 1024 + kPairStages * (size_t)(kTcBM + kPairBN) * kTcBK + kPairRecvBytes +
                             8 * (2 * kPairStages + 2) + 16;
-    auto kern = bool_i8_gemm_pair_kernel;
+    auto kern = bool_i8_gemm_pair_kernel<kPairStages>;
     SMX_TRY(set_max_smem((const void*)kern, smem));
     TcArgs args = a;
     args.splits = 1;
@@ -677,7 +692,7 @@ int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbit
     if (!aligned16(A) || !aligned16(Bt) || (lda & 15) || (ldbt & 15)) return SMX_E_ALIGN;
     if (lda < K || ldbt < K) return SMX_E_ARG;
     if (Cbits ? ((long long)ldc * 32 < N) : (ldc < N)) return SMX_E_ARG;
-    TcArgs a{C, Cbits, M, N, K, ldc, accumulate != 0, 0, 0, 1, g_tc_trace};
+    TcArgs a{C, Cbits, M, N, K, ldc, accumulate != 0, 0, 0, 1, 0, 0, g_tc_trace};
     if (skip_rows > 0) {
         if (skip_row0 % kTcBM) return SMX_E_ARG;
         a.skip_tile0 = skip_row0 / kTcBM;
@@ -691,7 +706,7 @@ int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbit
     if (Cbits && skip_rows == 0 && g_tc_pair != 0 && K > kTcBK && K <= 65536) {
         const long long tiles64 = (long long)ceil_div(M, kTcBM) * ceil_div(N, 64);
         if (g_tc_pair == 2 || (tiles64 <= 148 && g_tc_tile_n == 0))
-            return launch_tc_pair(A, Bt, a, lda, ldbt, s, pdl);
+            return launch_tc_pair<kPairStagesSingle>(A, Bt, a, lda, ldbt, s, pdl);
     }
     if (g_tc_tile_n == 64) return launch_tc<64>(A, Bt, a, lda, ldbt, s, pdl);
     if (g_tc_tile_n == 128) return launch_tc<128>(A, Bt, a, lda, ldbt, s, pdl);
@@ -701,6 +716,21 @@ int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbit
     if (rows * ceil_div(N, 256) >= 148) return launch_tc<256>(A, Bt, a, lda, ldbt, s, pdl);
     if (rows * ceil_div(N, 128) >= 148) return launch_tc<128>(A, Bt, a, lda, ldbt, s, pdl);
     return launch_tc<64>(A, Bt, a, lda, ldbt, s, pdl);
+}
+
+// Batched products on the split-K pair: `batch` products of M x K by K x N
+// stacked in A (batch * M rows), B^T (batch * N rows) and the packed-bit
+// C (batch * M rows), one launch; M and N multiples of 128 so no tile
+// straddles two products.
+int bool_i8_gemm_batched(const uint8_t* A, const uint8_t* Bt, uint32_t* Cbits, int batch, int M, int N, int K,
+                         long long lda, long long ldbt, long long ldc, int accumulate, cudaStream_t s) {
+    if (batch < 0 || M < 0 || N < 0 || K < 1 || Cbits == nullptr) return SMX_E_ARG;
+    if (batch == 0 || M == 0 || N == 0) return SMX_OK;
+    if (M % kTcBM || N % kPairBN || K <= kTcBK || K > 65536) return SMX_E_ARG;
+    if (!aligned16(A) || !aligned16(Bt) || (lda & 15) || (ldbt & 15)) return SMX_E_ALIGN;
+    if (lda < K || ldbt < K || (long long)ldc * 32 < N) return SMX_E_ARG;
+    TcArgs a{nullptr, Cbits, batch * M, N, K, ldc, accumulate != 0, 0, 0, 1, M / kTcBM, N, g_tc_trace};
+    return launch_tc_pair<kPairStagesBatched>(A, Bt, a, lda, ldbt, s, /*pdl=*/true, batch * N);
 }
 
 // ---- Warshall on bytes with tensor-core phases 2/3 -----------------------------
@@ -824,6 +854,8 @@ int unpack_bits(const uint32_t* words, uint8_t* bytes, int rows, int cols, long 
                 cudaStream_t s);
 int unpack_bits_transposed(const uint32_t* words, uint8_t* out, int rows, int cols, long long ld_w,
                            long long ld_out, cudaStream_t s);
+int unpack_bits_transposed_batched(const uint32_t* words, uint8_t* out, int batch, int rows, int cols, long long ld_w,
+                                   long long ld_out, long long in_stride, long long out_stride, cudaStream_t s);
 int unpack_ab(const uint32_t* a_words, uint8_t* a_bytes, int a_rows, int a_cols, long long a_ldw, long long a_ld,
               const uint32_t* b_words, uint8_t* bt, int b_rows, int b_cols, long long b_ldw, long long b_ldt,
               cudaStream_t s);
@@ -864,11 +896,57 @@ int bool_mul_tc(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int N,
     });
 }
 
+// Batched BoolMatrix products in one call: stacked bit rows in (A: batch x M
+// rows, B: batch x K rows), stacked bit rows out (batch x M rows); A is
+// unpacked in one launch, every B^T by one batched transpose launch, then one
+// pair launch for every product.  Replayed as a graph on repeat calls.
+inline size_t bool_mul_batched_ws_bytes(int batch, int M, int N, int K) {
+    return (size_t)(((long long)batch * M * round16(K) + 255) & ~255LL) + (size_t)batch * N * round16(K);
+}
+
+int bool_mul_tc_batched(const uint32_t* A, const uint32_t* B, uint32_t* C, int batch, int M, int N, int K,
+                        long long lda_w, long long ldb_w, long long ldc_w, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (batch < 0 || M < 0 || N < 0 || K < 1) return SMX_E_ARG;
+    if (batch == 0 || M == 0 || N == 0) return SMX_OK;
+    if (M % kTcBM || N % kPairBN || K <= kTcBK || K > 65536 || ldc_w * 32 != N) return SMX_E_ARG;
+    if (ws == nullptr || ws_bytes < bool_mul_batched_ws_bytes(batch, M, N, K)) return SMX_E_WORKSPACE;
+    uint8_t* a8 = reinterpret_cast<uint8_t*>(ws);
+    uint8_t* bt8 = a8 + (((long long)batch * M * round16(K) + 255) & ~255LL);
+    GraphKey key;
+    key.fn = 302;
+    const unsigned long long kv[] = {(uintptr_t)A, (uintptr_t)B, (uintptr_t)C, (unsigned long long)batch,
+                                     (unsigned long long)M, (unsigned long long)N, (unsigned long long)K,
+                                     (unsigned long long)lda_w, (unsigned long long)ldb_w,
+                                     (unsigned long long)ldc_w, (uintptr_t)ws, ws_bytes};
+    for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
+    return run_graphed(key, s, false, [&](cudaStream_t st) -> int {
+        SMX_TRY(unpack_bits(A, a8, batch * M, K, lda_w, round16(K), st));
+        SMX_TRY(unpack_bits_transposed_batched(B, bt8, batch, K, N, ldb_w, round16(K), (long long)K * ldb_w,
+                                               (long long)N * round16(K), st));
+        return bool_i8_gemm_batched(a8, bt8, C, batch, M, N, K, round16(K), round16(K), ldc_w, 0, st);
+    });
+}
+
 }  // namespace smx
 
 using namespace smx;
 
 extern "C" {
+
+size_t smx_bool_mul_tc_batched_workspace_bytes(int batch, int M, int N, int K) {
+    if (batch <= 0 || M <= 0 || N <= 0 || K <= 0) return 0;
+    return bool_mul_batched_ws_bytes(batch, M, N, K);
+}
+
+int smx_bool_mul_tc_batched(const uint32_t* A, const uint32_t* B, uint32_t* C, int batch, int M, int N, int K,
+                            int lda_w, int ldb_w, int ldc_w, void* ws, size_t ws_bytes, void* stream) {
+    return bool_mul_tc_batched(A, B, C, batch, M, N, K, lda_w, ldb_w, ldc_w, ws, ws_bytes, as_stream(stream));
+}
+
+int smx_bool_gemm_i8_batched(const uint8_t* A, const uint8_t* Bt, uint32_t* C_bits, int batch, int M, int N, int K,
+                             int lda, int ldbt, int ldc, int accumulate, void* stream) {
+    return bool_i8_gemm_batched(A, Bt, C_bits, batch, M, N, K, lda, ldbt, ldc, accumulate, as_stream(stream));
+}
 
 size_t smx_bool_mul_tc_workspace_bytes(int M, int N, int K) {
     if (M <= 0 || N <= 0 || K <= 0) return 0;

@@ -50,8 +50,13 @@ __global__ void unpack_bits_kernel(const uint32_t* __restrict__ words, uint8_t* 
 // tensor-core product straight from the reference's bit rows): a warp takes a
 // 32 (k) x 32 (j) bit tile; lane l holds row k0+l's word, 32 ballots turn the
 // tile around, lane l then owns output row j0+l and writes its 32 bytes.
+// (blockIdx.y: the item of a batch: its words at + y * in_stride, its output
+// at + y * out_stride)
 __global__ void unpack_bits_t_kernel(const uint32_t* __restrict__ words, uint8_t* __restrict__ out,
-                                     int rows, int cols, long long ld_w, long long ld_out) {
+                                     int rows, int cols, long long ld_w, long long ld_out,
+                                     long long in_stride = 0, long long out_stride = 0) {
+    words += (long long)blockIdx.y * in_stride;
+    out += (long long)blockIdx.y * out_stride;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int kt = (rows + 31) / 32, jt = (cols + 31) / 32;
@@ -185,6 +190,18 @@ int unpack_ab(const uint32_t* a_words, uint8_t* a_bytes, int a_rows, int a_cols,
     unpack_ab_kernel<<<(unsigned)(a_blocks + b_blocks), 256, 0, s>>>(a_words, a_bytes, a_rows, a_cols, a_ldw, a_ld,
                                                                    (int)a_blocks, b_words, bt, b_rows, b_cols,
                                                                    b_ldw, b_ldt);
+    SMX_RETURN_LAUNCH();
+}
+
+// `batch` matrices of rows x cols bits (words `in_stride` apart) -> their
+// transposed bytes (`out_stride` apart), one launch.
+int unpack_bits_transposed_batched(const uint32_t* words, uint8_t* out, int batch, int rows, int cols, long long ld_w,
+                                   long long ld_out, long long in_stride, long long out_stride, cudaStream_t s) {
+    if (batch < 0 || rows < 0 || cols < 0 || ld_out < rows || ld_w * 32 < cols) return SMX_E_ARG;
+    if (batch == 0 || rows == 0 || cols == 0) return SMX_OK;
+    const long long warps = (long long)((rows + 31) / 32) * ((cols + 31) / 32);
+    unpack_bits_t_kernel<<<dim3((unsigned)((warps * 32 + 255) / 256), (unsigned)batch), 256, 0, s>>>(
+        words, out, rows, cols, ld_w, ld_out, in_stride, out_stride);
     SMX_RETURN_LAUNCH();
 }
 

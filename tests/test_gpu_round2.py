@@ -16,6 +16,7 @@ import pytest
 import torch
 
 from paper_1705_08743_b200 import AntidistMatrix, BoolMatrix, DistMatrix, _native, batch, workloads
+from paper_1705_08743_b200 import batch as batch_mod
 
 pytestmark = pytest.mark.gpu
 
@@ -415,3 +416,23 @@ def test_packed_two_tiles_per_cta_matches(width, oracle_lib):
     finally:
         lib.smx_set_packed_tiles_per_cta(old)
     assert lib.smx_set_packed_tiles_per_cta(3) < 0
+
+
+@pytest.mark.parametrize("batch,m,k,n", [(5, 256, 300, 384), (16, 1024, 1024, 1024), (3, 128, 129, 128)])
+def test_bool_mul_many_on_tensor_cores(batch, m, k, n, oracle_lib):
+    """Stacked products with 128-multiple shapes take the batched split-K
+    pair (smx_bool_mul_tc_batched: one launch for every product, each CTA's
+    B^T rows offset by its product): every product equals the per-pair call
+    and, for two of them, the oracle."""
+    rng = np.random.default_rng(batch * 7 + k)
+    As = [(rng.random((m, k)) < 0.03) for _ in range(batch)]
+    Bs = [(rng.random((k, n)) < 0.03) for _ in range(batch)]
+    ma = [BoolMatrix.from_numpy(a) for a in As]
+    mb = [BoolMatrix.from_numpy(b) for b in Bs]
+    got = batch_mod.bool_mul_many(ma, mb)
+    for i in range(batch):
+        np.testing.assert_array_equal(got[i].blocks, (ma[i] * mb[i]).blocks, err_msg=f"product {i}")
+    for i in (0, batch - 1):
+        want = oracle_lib.bool_mul(oracle_lib.pack_bits(As[i].astype(np.uint8)),
+                                   oracle_lib.pack_bits(Bs[i].astype(np.uint8)), k)
+        np.testing.assert_array_equal(got[i].blocks, want)
