@@ -305,12 +305,16 @@ int smx_bool_gemm_i8_batched(const uint8_t* A, const uint8_t* Bt, uint32_t* C_bi
  * widest of 256 / 128 / 64 that still gives every SM a tile), or force 64,
  * 128 or 256.  Results are identical.  Returns the previous setting. */
 int smx_set_tc_tile_n(int bn);
-/* Split-K CTA pair for small packed-bit products (the C1 shape): 0 = off,
- * 1 = automatic (one wave of 128 x 64 tiles or fewer, 128 < K <= 65536,
- * automatic tile width), 2 = whenever the shape allows it (packed-bit
- * output, no row skip, 128 < K <= 65536).  Results are identical.  Returns
- * the previous setting. */
+/* Split-K CTA cluster for small packed-bit products (the C1 shape): 0 = off,
+ * 1 = automatic (a pair of CTAs on one wave of 128 x 64 tiles or fewer,
+ * 128 < K <= 65536, automatic tile width), 2 = the pair whenever the shape
+ * allows it (packed-bit output, no row skip, 128 < K <= 65536), 3 = as 2
+ * with four CTAs per tile (a quarter of K each, two-stage rings, two or
+ * three CTAs per SM).  Results are identical.  Returns the previous setting. */
 int smx_set_tc_pair(int mode);
+/* K slices per product of the batched tensor-core products (2 or 4).
+ * Results are identical.  Returns the previous setting. */
+int smx_set_tc_batch_ks(int ks);
 /* Development trace of the plain tensor-core kernel: buf (device, >= 16 + 2 *
  * CTAs u64) receives clock64 phase stamps of CTA 0 in [0, 8) and globaltimer
  * entry/exit of every CTA from [16]; NULL disarms. */

@@ -83,6 +83,7 @@ _SIGS.update({
 _SIGS.update({
     "smx_set_tc_tile_n": ([c_int], c_int),
     "smx_set_tc_pair": ([c_int], c_int),
+    "smx_set_tc_batch_ks": ([c_int], c_int),
     "smx_bool_mul_tc_batched_workspace_bytes": ([c_int, c_int, c_int, c_int], c_size_t),
     "smx_bool_mul_tc_batched": ([c_void_p, c_void_p, c_void_p] + [c_int] * 7 + [c_void_p, c_size_t, c_void_p],
                                 c_int),

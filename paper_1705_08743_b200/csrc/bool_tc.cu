@@ -348,7 +348,13 @@ constexpr int kPairThreads = 256;
 // tools/perf_c1_batched.py, profiles/r04d_c1_batched_stages.json).
 constexpr int kPairStagesSingle = 6;
 constexpr int kPairStagesBatched = 2;
-constexpr uint32_t kPairRecvBytes = 64 * (kPairBN / 32) * 4;   // 64 rows x 4 words
+// A cluster of KS CTAs splits K; CTA r owns rows [r * 128 / KS, ...) of the
+// tile and receives the other KS - 1 CTAs' words of them (one slot each).
+template <int KS>
+struct PairRecv {
+    static constexpr int kRows = kTcBM / KS;                                   // rows owned per CTA
+    static constexpr uint32_t kBytes = (KS - 1) * kRows * (kPairBN / 32) * 4;   // KS=2: 1 KB, KS=4: 1.5 KB
+};
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -376,7 +382,7 @@ __device__ __forceinline__ uint32_t bits_of(const uint32_t (&r)[32]) {
 // CTA issues 96 KB instead of 128: no faster -- 3.79 against 3.49 us per
 // launch, the same per-CTA timeline -- so the operand stream is bound where
 // the bytes land, not where they are issued; removed.)
-template <int kPairStages>
+template <int KS, int kPairStages>
 __global__ void __launch_bounds__(kPairThreads, 1)
 bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                          const TcArgs p) {
@@ -386,16 +392,16 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + kPairStages * A_BYTES;
-    uint32_t* recv = reinterpret_cast<uint32_t*>(sB + kPairStages * B_BYTES);   // [64][4] partner words
-    uint64_t* full = reinterpret_cast<uint64_t*>(recv + kPairRecvBytes / 4);
+    using RV = PairRecv<KS>;
+    uint32_t* recv = reinterpret_cast<uint32_t*>(sB + kPairStages * B_BYTES);   // [KS-1][rows][4] partner words
+    uint64_t* full = reinterpret_cast<uint64_t*>(recv + RV::kBytes / 4);
     uint64_t* empty = full + kPairStages;
     uint64_t* accum = empty + kPairStages;
     uint64_t* recv_bar = accum + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();   // the K half; owns rows [64 rank, 64 rank + 64)
-    const uint32_t partner = 1u - rank;
+    const uint32_t rank = cluster_rank();   // the K slice; owns rows [rank * RV::kRows, ...)
     const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const bool tr0 = p.trace && cta == 0;
     if (p.trace && threadIdx.x == 0) p.trace[16 + 2 * cta] = gtimer();
@@ -404,9 +410,9 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     // (batched: this CTA's product's B^T rows)
     const int nb0 = n0 + (p.batch_mt > 0 ? (int)(blockIdx.y / p.batch_mt) * p.bt_item_rows : 0);
     const int nkb_all = (p.K + kTcBK - 1) / kTcBK;
-    const int half = (nkb_all + 1) / 2;
-    const int kb_lo = (int)rank * half;
-    const int kb_hi = min(nkb_all, kb_lo + half);
+    const int per = (nkb_all + KS - 1) / KS;
+    const int kb_lo = (int)rank * per;
+    const int kb_hi = min(nkb_all, kb_lo + per);
     const int nkb = kb_hi > kb_lo ? kb_hi - kb_lo : 0;
 
     // Thread 0 initialises the barriers and issues the first ring fill right
@@ -427,7 +433,7 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
         mbar_init(recv_bar, 1);
         // the partner's 1 KB lands on recv_bar: expected before the cluster
         // barrier below, so no complete_tx can precede it
-        mbar_expect_tx(recv_bar, kPairRecvBytes);
+        mbar_expect_tx(recv_bar, RV::kBytes);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         if (tr0) p.trace[10] = clock64();
         // PDL: operands are read only after the preceding kernel in the
@@ -487,7 +493,7 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     }
     __syncwarp();
 
-    // ---- epilogue: this half's counts -> bits ----
+    // ---- epilogue: this K slice's counts -> bits ----
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     mbar_wait(accum, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -512,13 +518,16 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     if (nkb == 0) w0 = w1 = 0u;   // (K shorter than one k-block per CTA: TMEM was never written)
     if (tr0 && threadIdx.x == 0) p.trace[8] = clock64();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    // rows owned by the partner go to it; words [row][2*chalf, 2*chalf + 1]
-    const uint32_t owner = (uint32_t)(trow >> 6);   // K-half that owns (stores) this row
+    // rows owned by another CTA go to it, into this CTA's slot there; words
+    // [row][2*chalf, 2*chalf + 1]
+    const uint32_t owner = (uint32_t)(trow / RV::kRows);   // the CTA that stores this row
+    const int orow = trow % RV::kRows;
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (tr0 && threadIdx.x == 0) p.trace[9] = clock64();
     if (owner != rank) {
-        const uint32_t off = (uint32_t)(((trow & 63) * 4 + 2 * chalf) * 4);
-        st_async_v2(mapa_shared(smem_u32(recv) + off, partner), w0, w1, mapa_shared(smem_u32(recv_bar), partner));
+        const int slot = (int)rank < (int)owner ? (int)rank : (int)rank - 1;
+        const uint32_t off = (uint32_t)(((slot * RV::kRows + orow) * 4 + 2 * chalf) * 4);
+        st_async_v2(mapa_shared(smem_u32(recv) + off, owner), w0, w1, mapa_shared(smem_u32(recv_bar), owner));
     }
     // No second cluster barrier: every store into this CTA's shared memory
     // completes on recv_bar, which the owner threads wait on before the CTA
@@ -527,9 +536,12 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     if (tr0 && threadIdx.x == 0) p.trace[6] = clock64();
     if (owner == rank) {
         mbar_wait(recv_bar, 0);
-        const uint2 o = *reinterpret_cast<const uint2*>(&recv[(trow & 63) * 4 + 2 * chalf]);
-        w0 |= o.x;
-        w1 |= o.y;
+#pragma unroll
+        for (int sl = 0; sl < KS - 1; ++sl) {
+            const uint2 o = *reinterpret_cast<const uint2*>(&recv[(sl * RV::kRows + orow) * 4 + 2 * chalf]);
+            w0 |= o.x;
+            w1 |= o.y;
+        }
         const int row = m0 + trow, col0 = n0 + chalf * 64;
         if (row < p.M && col0 < p.N) {
             uint32_t* dst = p.Cbits + (long long)row * p.ldc + (col0 >> 5);
@@ -642,20 +654,20 @@ static int launch_tc(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long 
 
 // Split-K pair launch (packed-bit output, no row skip).  The caller has
 // checked the shape (see bool_i8_gemm).
-template <int kPairStages>
+template <int KS, int kPairStages>
 static int launch_tc_pair(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long long lda, long long ldbt,
                           cudaStream_t s, bool pdl, int bt_rows = -1) {
     CUtensorMap mA, mB;
     SMX_TRY(make_map(&mA, A, a.M, a.K, lda, kTcBM));
     SMX_TRY(make_map(&mB, Bt, bt_rows < 0 ? a.N : bt_rows, a.K, ldbt, kPairBN));
-    constexpr size_t smem = 1024 + kPairStages * (size_t)(kTcBM + kPairBN) * kTcBK + kPairRecvBytes +
+    constexpr size_t smem = 1024 + kPairStages * (size_t)(kTcBM + kPairBN) * kTcBK + PairRecv<KS>::kBytes +
                             8 * (2 * kPairStages + 2) + 16;
-    auto kern = bool_i8_gemm_pair_kernel<kPairStages>;
+    auto kern = bool_i8_gemm_pair_kernel<KS, kPairStages>;
     SMX_TRY(set_max_smem((const void*)kern, smem));
     TcArgs args = a;
     args.splits = 1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ceil_div(a.N, kPairBN), ceil_div(a.M, kTcBM), 2);
+    cfg.gridDim = dim3(ceil_div(a.N, kPairBN), ceil_div(a.M, kTcBM), KS);
     cfg.blockDim = dim3(kPairThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -663,7 +675,7 @@ static int launch_tc_pair(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, 
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 2;
+    attr[0].val.clusterDim.z = KS;
     int na = 1;
     if (pdl) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -682,6 +694,7 @@ static int launch_tc_pair(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, 
 // results are identical).
 static int g_tc_tile_n = 0;
 static int g_tc_pair = 1;
+static int g_tc_batch_ks = 2;   // (experiment switch: K slices per batched product)
 static unsigned long long* g_tc_trace = nullptr;
 
 int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbits, int M, int N, int K,
@@ -705,8 +718,11 @@ int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbit
     // 0 = off, 1 = automatic, 2 = always when the shape allows it)
     if (Cbits && skip_rows == 0 && g_tc_pair != 0 && K > kTcBK && K <= 65536) {
         const long long tiles64 = (long long)ceil_div(M, kTcBM) * ceil_div(N, 64);
-        if (g_tc_pair == 2 || (tiles64 <= 148 && g_tc_tile_n == 0))
-            return launch_tc_pair<kPairStagesSingle>(A, Bt, a, lda, ldbt, s, pdl);
+        if (g_tc_pair >= 2 || (tiles64 <= 148 && g_tc_tile_n == 0))
+        {
+            if (g_tc_pair == 3) return launch_tc_pair<4, 2>(A, Bt, a, lda, ldbt, s, pdl);
+            return launch_tc_pair<2, kPairStagesSingle>(A, Bt, a, lda, ldbt, s, pdl);
+        }
     }
     if (g_tc_tile_n == 64) return launch_tc<64>(A, Bt, a, lda, ldbt, s, pdl);
     if (g_tc_tile_n == 128) return launch_tc<128>(A, Bt, a, lda, ldbt, s, pdl);
@@ -730,7 +746,8 @@ int bool_i8_gemm_batched(const uint8_t* A, const uint8_t* Bt, uint32_t* Cbits, i
     if (!aligned16(A) || !aligned16(Bt) || (lda & 15) || (ldbt & 15)) return SMX_E_ALIGN;
     if (lda < K || ldbt < K || (long long)ldc * 32 < N) return SMX_E_ARG;
     TcArgs a{nullptr, Cbits, batch * M, N, K, ldc, accumulate != 0, 0, 0, 1, M / kTcBM, N, g_tc_trace};
-    return launch_tc_pair<kPairStagesBatched>(A, Bt, a, lda, ldbt, s, /*pdl=*/true, batch * N);
+    if (g_tc_batch_ks == 4) return launch_tc_pair<4, 2>(A, Bt, a, lda, ldbt, s, /*pdl=*/true, batch * N);
+    return launch_tc_pair<2, kPairStagesBatched>(A, Bt, a, lda, ldbt, s, /*pdl=*/true, batch * N);
 }
 
 // ---- Warshall on bytes with tensor-core phases 2/3 -----------------------------
@@ -965,8 +982,15 @@ int smx_tc_trace_arm(unsigned long long* buf) {
     return SMX_OK;
 }
 
+int smx_set_tc_batch_ks(int ks) {
+    if (ks != 2 && ks != 4) return SMX_E_ARG;
+    const int old = g_tc_batch_ks;
+    g_tc_batch_ks = ks;
+    return old;
+}
+
 int smx_set_tc_pair(int mode) {
-    if (mode < 0 || mode > 2) return SMX_E_ARG;
+    if (mode < 0 || mode > 3) return SMX_E_ARG;
     const int old = g_tc_pair;
     g_tc_pair = mode;
     return old;

@@ -58,14 +58,14 @@ def test_tc_tile_widths_match_oracle(shape, oracle_lib):
             lib.smx_set_tc_tile_n(bn)
             np.testing.assert_array_equal((ma * mb).blocks, want, err_msg=f"tile {bn} {shape}")
         lib.smx_set_tc_tile_n(0)
-        for mode in (1, 2):   # the split-K CTA pair (automatic / forced)
+        for mode in (1, 2, 3):   # the split-K CTA pair (automatic / forced), four CTAs per tile
             lib.smx_set_tc_pair(mode)
             np.testing.assert_array_equal((ma * mb).blocks, want, err_msg=f"pair {mode} {shape}")
     finally:
         lib.smx_set_tc_tile_n(old)
         lib.smx_set_tc_pair(old_pair)
     assert lib.smx_set_tc_tile_n(100) < 0
-    assert lib.smx_set_tc_pair(3) < 0
+    assert lib.smx_set_tc_pair(4) < 0
 
 
 @pytest.mark.parametrize("shape", [(1024, 1024, 1024), (1000, 777, 1001), (130, 100, 129), (256, 256, 3000),
@@ -90,7 +90,7 @@ def test_tc_pair_kernel_bits_accumulate(shape, oracle_lib):
     init = rng.integers(0, 2 ** 32, (m, ldc), dtype=np.uint64).astype(np.uint32)
     old = lib.smx_set_tc_pair(2)
     try:
-        for mode in (2,):   # (forced pair)
+        for mode in (2, 3):   # (forced pair, forced quad)
             lib.smx_set_tc_pair(mode)
             for acc in (0, 1):
                 C = torch.from_numpy(init.view(np.int32).copy()).cuda()
@@ -429,9 +429,15 @@ def test_bool_mul_many_on_tensor_cores(batch, m, k, n, oracle_lib):
     Bs = [(rng.random((k, n)) < 0.03) for _ in range(batch)]
     ma = [BoolMatrix.from_numpy(a) for a in As]
     mb = [BoolMatrix.from_numpy(b) for b in Bs]
-    got = batch_mod.bool_mul_many(ma, mb)
-    for i in range(batch):
-        np.testing.assert_array_equal(got[i].blocks, (ma[i] * mb[i]).blocks, err_msg=f"product {i}")
+    lib = _native.lib()
+    for ks in (2, 4):
+        old = lib.smx_set_tc_batch_ks(ks)
+        try:
+            got = batch_mod.bool_mul_many(ma, mb)
+        finally:
+            lib.smx_set_tc_batch_ks(old)
+        for i in range(batch):
+            np.testing.assert_array_equal(got[i].blocks, (ma[i] * mb[i]).blocks, err_msg=f"product {i} ks={ks}")
     for i in (0, batch - 1):
         want = oracle_lib.bool_mul(oracle_lib.pack_bits(As[i].astype(np.uint8)),
                                    oracle_lib.pack_bits(Bs[i].astype(np.uint8)), k)

@@ -62,4 +62,16 @@ with torch.cuda.stream(st):
 t = t_of(lambda: g.replay(), 10, 2) / 10
 res["batched_kernel_us_per_product"] = t / nb * 1e6
 res["batched_kernel_frac_of_int8_peak"] = 2 * n ** 3 * nb / t / peak
+old = lib.smx_set_tc_batch_ks(4)
+g4 = torch.cuda.CUDAGraph()
+with torch.cuda.stream(st):
+    kern()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g4, stream=st):
+        for _ in range(10):
+            kern()
+lib.smx_set_tc_batch_ks(old)
+t = t_of(lambda: g4.replay(), 10, 2) / 10
+res["batched_ks4_us_per_product"] = t / nb * 1e6
+res["batched_ks4_frac_of_int8_peak"] = 2 * n ** 3 * nb / t / peak
 print(json.dumps(res))

@@ -66,10 +66,10 @@ def main():
                                            n // 32, 0, _native.stream_ptr(dev)), "tc")
     old = lib.smx_set_tc_tile_n(0)
     old_pair = lib.smx_set_tc_pair(0)
-    for pair, bn in ((0, 0), (0, 64), (0, 128), (0, 256), (2, 0)):
+    for pair, bn in ((0, 0), (0, 64), (0, 128), (0, 256), (2, 0), (3, 0)):
         lib.smx_set_tc_pair(pair)
         lib.smx_set_tc_tile_n(bn)
-        key = {0: f"tc_bn{bn}", 2: "tc_pair"}[pair]
+        key = {0: f"tc_bn{bn}", 2: "tc_pair", 3: "tc_quad"}[pair]
         res[f"{key}_us"] = timeit(tc)
         f, per = graphed(tc)
         res[f"{key}_graph_us"] = timeit(f, 50, 5) / per
