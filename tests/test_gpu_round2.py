@@ -308,8 +308,12 @@ def test_nccl_broadcast_on_torch_communicator(tmp_path):
     from paper_1705_08743_b200 import sharded
     if dist.is_initialized():
         pytest.skip("a process group is already initialised")
+    # the exact group bench.py builds at N > 1: NCCL's internal stream at high
+    # priority (ProcessGroupNCCL.Options.is_high_priority_stream)
+    opts = dist.ProcessGroupNCCL.Options()
+    opts.is_high_priority_stream = True
     dist.init_process_group("nccl", init_method=f"file://{tmp_path / 'pg'}", rank=0, world_size=1,
-                            device_id=torch.device("cuda", 0))
+                            device_id=torch.device("cuda", 0), pg_options=opts)
     try:
         lib = _native.lib()
         fw = sharded.NativeShardedFW(1024, 0, 1, 16, anti=True, transport="nccl")
@@ -327,6 +331,12 @@ def test_nccl_broadcast_on_torch_communicator(tmp_path):
         got = fw.run(torch.from_numpy(t).cuda()).cpu().numpy()
         ref = AntidistMatrix(1024, 1024, 16, torch.from_numpy(t).cuda()).transitive_closure()._data.cpu().numpy()
         np.testing.assert_array_equal(got, ref)
+        # torch.distributed collectives on the same group still work after the
+        # library's own NCCL calls (the bench's barrier / max-over-ranks)
+        t = torch.tensor([3.0], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        assert float(t.item()) == 3.0
     finally:
         dist.destroy_process_group()
 
