@@ -29,7 +29,9 @@ public:
         return pool;
     }
     // memcpy(dst, src, bytes) split over the workers; returns when done.
+    // One job at a time (concurrent callers queue on job_mu_).
     void copy(char* dst, const char* src, size_t bytes) {
+        std::lock_guard<std::mutex> job(job_mu_);
         std::unique_lock<std::mutex> lk(mu_);
         dst_ = dst;
         src_ = src;
@@ -79,7 +81,7 @@ private:
         }
     }
     std::vector<std::thread> workers_;
-    std::mutex mu_;
+    std::mutex job_mu_, mu_;
     std::condition_variable cv_, done_cv_;
     char* dst_ = nullptr;
     const char* src_ = nullptr;
