@@ -114,7 +114,9 @@ int smx_copy_h2d(void* dst, const void* src, size_t bytes, void* stream);
  * host_out is complete once `stream` reaches the end of the call.  Page-locked
  * host buffers give the overlap; a pageable host_in is staged through the
  * library's page-locked ring by a memcpy thread pool, overlapped the same way
- * (host_stage.cu); a pageable host_out copies out synchronously.
+ * (host_stage.cu); a pageable host_out (e.g. the caller's own array closed
+ * in place) is staged back through the same ring, its copies overlapped with
+ * the rest of the closure, and the call returns once every row is in it.
  * `workspace`: smx_fw_host_workspace_bytes(n, ld, elem_bytes) bytes. */
 size_t smx_fw_host_workspace_bytes(int n, int ld, int elem_bytes);
 int smx_fw_host_u8(const uint8_t* host_in, uint8_t* host_out, uint8_t* T, int n, int ld, int kind,

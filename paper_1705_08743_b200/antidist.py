@@ -381,13 +381,15 @@ class _LaneMatrix:
         if self.device != other.device:
             raise ValueError(f"operands live on different devices: {self.device} vs {other.device}")
 
-    def _close_host(self) -> torch.Tensor:
-        """Host-buffer closure of the backing array into page-locked memory
-        (smx_fw_host_*); returns the finished host result."""
+    def _close_host(self, in_place: bool = False) -> torch.Tensor:
+        """Host-buffer closure of the backing array (smx_fw_host_*) into
+        page-locked memory, or with ``in_place`` into the (contiguous) backing
+        array itself, which the library stages back through its page-locked
+        ring overlapped with the closure; returns the finished host result."""
         from . import engines
         host = torch.from_numpy(np.ascontiguousarray(self._host))
         res, _ = engines.lane_close_host(host, self.rows, self.width, anti=not self._PAD_IS_LIMIT,
-                                         device=self._device)
+                                         out=host if in_place else None, device=self._device)
         torch.cuda.current_stream(self._device).synchronize()
         return res
 
@@ -399,11 +401,10 @@ class _LaneMatrix:
             raise ValueError(f"closure needs a square matrix, got {self.rows}x{self.cols}")
         from . import engines
         if self._dev is None and self._host.flags.writeable:
-            res = self._close_host()
             if self._host.flags.c_contiguous:
-                torch.from_numpy(self._host).copy_(res)   # (threaded copy)
+                self._close_host(in_place=True)
             else:
-                np.copyto(self._host, res.numpy())
+                np.copyto(self._host, self._close_host().numpy())
             return
         engines.lane_close_(self._data, self.rows, self.width, anti=not self._PAD_IS_LIMIT)
 

@@ -1116,9 +1116,22 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
             if ((e = cudaEventRecord(ev_in[g], cs->in)) != cudaSuccess) return (int)e;
         }
     }
+    // Page-locked output: each finished piece is one D2H on the copy-out
+    // stream.  Pageable output (an ordinary numpy array, e.g. the in-place
+    // closure of the caller's own array): staged back through the
+    // page-locked ring by a coordinator thread (HostEgress), so the copy out
+    // still overlaps the rest of the closure; the call then returns once
+    // every row is in host_out.
+    HostEgress egress;
+    const bool egress_staged = is_pageable(hout);
+    if (egress_staged) SMX_TRY(egress.start(Tm, hout, cs->out));
     auto d2h = [&](int r0, int r1, cudaEvent_t ev) -> int {
         cudaError_t e2;
         if ((e2 = cudaEventRecord(ev, s)) != cudaSuccess) return (int)e2;
+        if (egress_staged) {
+            egress.push((size_t)r0 * row_bytes, (size_t)r1 * row_bytes, ev);
+            return SMX_OK;
+        }
         if ((e2 = cudaStreamWaitEvent(cs->out, ev, 0)) != cudaSuccess) return (int)e2;
         e2 = cudaMemcpyAsync(hout + (size_t)r0 * ld, Tm + (size_t)r0 * ld, (size_t)(r1 - r0) * row_bytes,
                              cudaMemcpyDeviceToHost, cs->out);
@@ -1169,6 +1182,7 @@ int fw_host_run(const T* hin, T* hout, T* Tm, int n, long long ld, int kind, voi
         }
         SMX_TRY(d2h(cuts[c], cuts[c + 1], ev_out[1 + c]));
     }
+    if (egress_staged) SMX_TRY(egress.finish());   // (every row is in host_out)
     if ((e = cudaEventRecord(ev_join, cs->out)) != cudaSuccess) return (int)e;
     e = cudaStreamWaitEvent(s, ev_join, 0);
     if (staged) SMX_TRY(stager.finish());

@@ -211,6 +211,92 @@ int HostStager::finish() {
     return status_;
 }
 
+int HostEgress::start(const void* src, void* dst, cudaStream_t out) {
+    src_ = static_cast<const char*>(src);
+    dst_ = static_cast<char*>(dst);
+    out_ = out;
+    queue_.clear();
+    next_ = 0;
+    closed_ = false;
+    status_ = 0;
+    cudaError_t e = cudaGetDevice(&device_);
+    if (e != cudaSuccess) return (int)e;
+    th_ = std::thread([this] { run(); });
+    return SMX_OK;
+}
+
+void HostEgress::push(size_t b0, size_t b1, cudaEvent_t ev) {
+    std::lock_guard<std::mutex> lk(mu_);
+    queue_.push_back({b0, b1, ev});
+    cv_.notify_all();
+}
+
+int HostEgress::finish() {
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        closed_ = true;
+        cv_.notify_all();
+    }
+    if (th_.joinable()) th_.join();
+    return status_;
+}
+
+void HostEgress::run() {
+    int rc = SMX_OK;
+    cudaSetDevice(device_);
+    {
+        // The ring is taken when the first piece arrives, not before: the
+        // same call's ingest stager holds it until every input group has
+        // been issued, and the first piece is pushed only after that.
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return !queue_.empty() || closed_; });
+    }
+    std::lock_guard<std::mutex> ring_lock(g_ring_mu);
+    Ring* ring = nullptr;
+    rc = ring_for(device_, &ring);
+    CopyPool& pool = CopyPool::get();
+    // slots in flight: (slot, destination offset, bytes), oldest first
+    struct Flight { int slot; size_t off, bytes; };
+    std::vector<Flight> flight;
+    size_t slot_seq = 0;
+    auto drain_one = [&]() -> int {
+        const Flight f = flight.front();
+        flight.erase(flight.begin());
+        cudaError_t e = cudaEventSynchronize(ring->ev[f.slot]);
+        if (e != cudaSuccess) return (int)e;
+        pool.copy(dst_ + f.off, ring->base + f.slot * kSlotBytes, f.bytes);
+        return SMX_OK;
+    };
+    for (;;) {
+        Piece pc;
+        {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return next_ < queue_.size() || closed_; });
+            if (next_ >= queue_.size()) break;   // closed and drained
+            pc = queue_[next_++];
+        }
+        if (rc != SMX_OK) continue;          // (keep consuming so finish() returns)
+        cudaError_t e = cudaStreamWaitEvent(out_, pc.ev, 0);
+        for (size_t off = pc.b0; off < pc.b1 && e == cudaSuccess && rc == SMX_OK;) {
+            const size_t bytes = std::min(kSlotBytes, pc.b1 - off);
+            if (flight.size() == (size_t)kSlots) rc = drain_one();   // the slot we are about to reuse
+            if (rc != SMX_OK) break;
+            const int slot = (int)(slot_seq++ % kSlots);
+            // the slot's last H2D (the ingest of this call) must have read it
+            e = cudaStreamWaitEvent(out_, ring->ev[slot], 0);
+            if (e != cudaSuccess) break;
+            e = cudaMemcpyAsync(ring->base + slot * kSlotBytes, src_ + off, bytes, cudaMemcpyDeviceToHost, out_);
+            if (e == cudaSuccess) e = cudaEventRecord(ring->ev[slot], out_);
+            if (e == cudaSuccess) flight.push_back({slot, off, bytes});
+            off += bytes;
+        }
+        if (e != cudaSuccess && rc == SMX_OK) rc = (int)e;
+    }
+    while (rc == SMX_OK && !flight.empty()) rc = drain_one();
+    std::lock_guard<std::mutex> lk(mu_);
+    status_ = rc;
+}
+
 namespace {
 struct StageStream {
     cudaStream_t s = nullptr;

@@ -54,6 +54,37 @@ private:
     int status_ = 0;
 };
 
+// Staged D2H copies into pageable host memory: the mirror of HostStager for
+// the closure's egress.  The caller hands over (byte range, event) pieces in
+// order as their rows become final; a coordinator thread copies each piece
+// into the page-locked ring on the copy stream once its event has fired,
+// and the memcpy pool moves it from the slot into `dst` (up to four slots in
+// flight).  finish() returns when every byte is in `dst`.
+class HostEgress {
+public:
+    int start(const void* src, void* dst, cudaStream_t out);
+    // rows [b0, b1) of the flat buffers are final once `ev` fires (ev must be
+    // recorded before this call; it is consumed in order)
+    void push(size_t b0, size_t b1, cudaEvent_t ev);
+    int finish();
+    ~HostEgress() { finish(); }
+
+private:
+    struct Piece { size_t b0, b1; cudaEvent_t ev; };
+    void run();
+    const char* src_ = nullptr;
+    char* dst_ = nullptr;
+    cudaStream_t out_ = nullptr;
+    int device_ = 0;
+    std::thread th_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::vector<Piece> queue_;
+    size_t next_ = 0;
+    bool closed_ = false;
+    int status_ = 0;
+};
+
 // dst (device) <- src (host), `bytes`, ordered on `stream`: page-locked
 // sources are one async copy; pageable ones go through the staging ring
 // (~4x the pageable cudaMemcpy rate) and this call returns once every byte

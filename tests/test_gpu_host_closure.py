@@ -115,6 +115,31 @@ def test_host_closure_in_place_and_pageable(mode, oracle_lib):
     np.testing.assert_array_equal(buf.numpy(), want)
 
 
+@pytest.mark.parametrize("layout", ["pageable_in_place", "pageable_out", "pinned_in_pageable_out"])
+def test_host_closure_pageable_out_staged(layout):
+    """A pageable host_out is staged back through the page-locked ring
+    (HostEgress, host_stage.cu): n = 8192 u16 streamed (128 MB: the egress
+    runs through every 64 MB slot, after the ingest has used them), in place
+    on the caller's own array, into a separate pageable array, and from a
+    page-locked input; equal to the device-resident closure."""
+    cfg = workloads.CONFIGS["c4_fw_u16"]
+    (t,) = workloads.make_inputs(cfg, 8192)
+    want = sha(AntidistMatrix(8192, 8192, 16, torch.from_numpy(t).cuda()).transitive_closure()._data.cpu().numpy())
+    src = torch.from_numpy(t.copy())
+    if layout == "pinned_in_pageable_out":
+        src = src.pin_memory()
+    out = src if layout == "pageable_in_place" else torch.from_numpy(np.full_like(t, 7))
+    with stream_mode(2):
+        for _ in range(2):
+            if layout == "pageable_in_place":
+                out.copy_(torch.from_numpy(t))
+            AntidistMatrix.closure_of_host(src, 16, out=out)
+            torch.cuda.synchronize()
+            assert sha(out.numpy()) == want, layout
+    if layout != "pageable_in_place":
+        assert sha(src.numpy()) == sha(t)                 # the input is untouched
+
+
 def test_host_closure_rejects_bad_shapes():
     with pytest.raises(ValueError):
         AntidistMatrix.closure_of_host(torch.zeros((10, 10), dtype=torch.uint16), 16)   # not padded
