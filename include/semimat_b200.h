@@ -303,6 +303,20 @@ int smx_bool_mul_tc_batched(const uint32_t* A, const uint32_t* B, uint32_t* C, i
  * (batch * N rows), packed-bit C (batch * M rows); one split-K pair launch. */
 int smx_bool_gemm_i8_batched(const uint8_t* A, const uint8_t* Bt, uint32_t* C_bits, int batch, int M, int N,
                              int K, int lda, int ldbt, int ldc, int accumulate, void* stream);
+/* The same products on E2M1 nibble operands, tcgen05 kind::mxf4 (half the
+ * operand bytes and twice the MMA rate of kind::i8; scale factors 1.0, f32
+ * counts, count > 0 threshold): A is M rows of ceil(K / 2) bytes (lda bytes
+ * apart, lda % 16 == 0), B^T N rows likewise, as smx_unpack_nibbles writes
+ * them; packed-bit output (ldc in u32 words).  Any M, N, K >= 1 (batched: M
+ * and N multiples of 128).  Bit-identical to smx_bool_gemm_i8. */
+int smx_bool_gemm_f4(const uint8_t* A, const uint8_t* Bt, uint32_t* C_bits, int M, int N, int K, int lda,
+                     int ldbt, int ldc, int accumulate, void* stream);
+int smx_bool_gemm_f4_batched(const uint8_t* A, const uint8_t* Bt, uint32_t* C_bits, int batch, int M, int N,
+                             int K, int lda, int ldbt, int ldc, int accumulate, void* stream);
+/* Operands of smx_bool_mul_tc / smx_bool_mul_tc_batched on the split-K pair:
+ * 1 = E2M1 nibbles, kind::mxf4 (default), 0 = bytes, kind::i8.  Results are
+ * identical.  Returns the previous setting. */
+int smx_set_tc_f4(int enable);
 /* Output tile width (N) of the tensor-core Boolean GEMM: 0 = automatic (the
  * widest of 256 / 128 / 64 that still gives every SM a tile), or force 64,
  * 128 or 256.  Results are identical.  Returns the previous setting. */
@@ -314,9 +328,12 @@ int smx_set_tc_tile_n(int bn);
  * with four CTAs per tile (a quarter of K each, two-stage rings, two or
  * three CTAs per SM).  Results are identical.  Returns the previous setting. */
 int smx_set_tc_pair(int mode);
-/* K slices per product of the batched tensor-core products (2 or 4).
+/* K slices per product of the batched tensor-core products (1, 2 or 4).
  * Results are identical.  Returns the previous setting. */
 int smx_set_tc_batch_ks(int ks);
+/* Ring depth (2 or 3 stages) of the batched nibble products.  Results are
+ * identical.  Returns the previous setting. */
+int smx_set_tc_f4_batch_stages(int stages);
 /* Development trace of the plain tensor-core kernel: buf (device, >= 16 + 2 *
  * CTAs u64) receives clock64 phase stamps of CTA 0 in [0, 8) and globaltimer
  * entry/exit of every CTA from [16]; NULL disarms. */
@@ -353,6 +370,14 @@ int smx_unpack_bits(const uint32_t* words, uint8_t* bytes, int rows, int cols, i
  * bytes): the K-major B^T operand of smx_bool_gemm_i8 in one pass */
 int smx_unpack_bits_transposed(const uint32_t* words, uint8_t* bytes_t, int rows, int cols,
                                int ld_w, int ld_out, void* stream);
+/* packed bits -> the E2M1 nibble operands of smx_bool_gemm_f4 in one launch:
+ * A (a_rows x a_cols bits; NULL skips A) -> a_rows rows of nibbles (a_ld
+ * bytes apart), B (b_rows x b_cols bits) -> B^T, b_cols rows of nibbles
+ * (b_ldt bytes apart).  Bit k of a row -> nibble k (byte k / 2, low nibble
+ * first), 0 or 0b0010 (1.0); bytes past ceil(cols / 2) are not written. */
+int smx_unpack_nibbles(const uint32_t* a_words, uint8_t* a_nib, int a_rows, int a_cols, int a_ldw, int a_ld,
+                       const uint32_t* b_words, uint8_t* bt_nib, int b_rows, int b_cols, int b_ldw, int b_ldt,
+                       void* stream);
 /* out (cols x rows) = in^T for bytes */
 int smx_transpose_u8(const uint8_t* in, uint8_t* out, int rows, int cols, int ld_in,
                      int ld_out, void* stream);

@@ -84,6 +84,12 @@ _SIGS.update({
     "smx_set_tc_tile_n": ([c_int], c_int),
     "smx_set_tc_pair": ([c_int], c_int),
     "smx_set_tc_batch_ks": ([c_int], c_int),
+    "smx_set_tc_f4": ([c_int], c_int),
+    "smx_set_tc_f4_batch_stages": ([c_int], c_int),
+    "smx_bool_gemm_f4": ([c_void_p] * 3 + [c_int] * 7 + [c_void_p], c_int),
+    "smx_bool_gemm_f4_batched": ([c_void_p] * 3 + [c_int] * 8 + [c_void_p], c_int),
+    "smx_unpack_nibbles": ([c_void_p, c_void_p] + [c_int] * 4 + [c_void_p, c_void_p] + [c_int] * 4 + [c_void_p],
+                           c_int),
     "smx_bool_mul_tc_batched_workspace_bytes": ([c_int, c_int, c_int, c_int], c_size_t),
     "smx_bool_mul_tc_batched": ([c_void_p, c_void_p, c_void_p] + [c_int] * 7 + [c_void_p, c_size_t, c_void_p],
                                 c_int),

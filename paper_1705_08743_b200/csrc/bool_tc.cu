@@ -95,6 +95,33 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t a, uint64_t b,
         : "memory");
 }
 
+// kind::mxf4 (E2M1 operands, two per byte, UE8M0 scale per 32 elements of
+// K, f32 accumulate): the same product on 0/1 operands (1.0 = 0b0010) at
+// half the operand bytes and twice the MMA rate of kind::i8.  Block-scaled
+// descriptor: a/b format E2M1 (1) @7/@10 | N>>3 @17 | scale UE8M0 @23 |
+// M>>4 @24 | K = 64 per instruction (bit 31 clear) | scale-factor ids 0.
+template <int BN>
+__device__ __forceinline__ constexpr uint32_t idesc_f4() {
+    return (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(kTcBM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_f4(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accumulate, uint32_t tmem_sfa, uint32_t tmem_sfb) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+            tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb)
+        : "memory");
+}
+
+// 8 TMEM columns of this warp's 32 lanes <- v
+__device__ __forceinline__ void tmem_fill8(uint32_t taddr, uint32_t v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(v)
+                 : "memory");
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      smem_u32(bar))
@@ -150,7 +177,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-template <int BN>
+// F4: E2M1 nibble operands (kind::mxf4; a.K in bytes), TMEM columns
+// [BN, 2 BN) hold the scale factors (all 1.0), as in the pair kernel below.
+template <int BN, bool F4 = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
 bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                     const TcArgs p) {
@@ -205,10 +234,11 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             tma_load_2d(&mapB, &full[kb], sB + kb * B_BYTES, (kb_lo + kb) * kTcBK, n0);
         }
     }
+    constexpr uint32_t kTmemCols = F4 ? 2 * BN : BN;
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "n"(BN)
+                     "n"(kTmemCols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -217,6 +247,16 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     if (tr0 && threadIdx.x == 0) p.trace[1] = clock64();
+    if constexpr (F4) {
+        // every warp sets its 32 lanes of the scale-factor columns to 1.0
+        const uint32_t t = tmem + ((uint32_t)(warp * 32) << 16) + BN;
+#pragma unroll
+        for (int c = 0; c < BN; c += 8) tmem_fill8(t + c, 0x7F7F7F7Fu);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
 
     if (threadIdx.x == 0) {
         // ---- TMA producer: the rest of the ring ----
@@ -231,7 +271,7 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         if (tr0) p.trace[2] = clock64();
     } else if (threadIdx.x == 32) {
         // ---- MMA issuer ----
-        constexpr uint32_t idesc = idesc_i8<BN>();
+        constexpr uint32_t idesc = F4 ? idesc_f4<BN>() : idesc_i8<BN>();
         for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % kTcStages;
             const uint32_t ph = (kb / kTcStages) & 1;
@@ -240,16 +280,22 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
 #pragma unroll
-            for (int k = 0; k < kTcBK / 32; ++k)
-                umma_i8(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
-                        (kb | k) != 0);
+            for (int k = 0; k < kTcBK / 32; ++k) {
+                if constexpr (F4)
+                    umma_f4(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
+                            (kb | k) != 0, tmem + BN, tmem + BN + BN / 2);
+                else
+                    umma_i8(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
+                            (kb | k) != 0);
+            }
             umma_commit(&empty[s]);
         }
         umma_commit(accum);
     }
     __syncwarp();
 
-    // ---- epilogue: TMEM -> threshold -> bytes or bits ----
+    // ---- epilogue: TMEM -> threshold -> bytes or bits (F4: f32 counts,
+    // nonzero exactly when positive) ----
     // a PDL-launched successor may start its prologue now (it reads nothing
     // of ours before its own griddepcontrol.wait)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -315,7 +361,7 @@ bool_i8_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     if (tr0 && threadIdx.x == 0) p.trace[6] = clock64();
     if (p.trace && threadIdx.x == 0) p.trace[17 + 2 * cta] = gtimer();
     if (warp == 2) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols)
                      : "memory");
     }
 }
@@ -382,7 +428,11 @@ __device__ __forceinline__ uint32_t bits_of(const uint32_t (&r)[32]) {
 // CTA issues 96 KB instead of 128: no faster -- 3.79 against 3.49 us per
 // launch, the same per-CTA timeline -- so the operand stream is bound where
 // the bytes land, not where they are issued; removed.)
-template <int KS, int kPairStages>
+// F4: operands are E2M1 nibbles (bool_f4_gemm); one 128-byte k-block then
+// holds 256 elements of K, and TMEM columns [128, 256) hold the scale
+// factors, all 1.0 (UE8M0 127): a uniform fill, so their TMEM layout does
+// not matter.
+template <int KS, int kPairStages, bool F4 = false>
 __global__ void __launch_bounds__(kPairThreads, 1)
 bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                          const TcArgs p) {
@@ -399,6 +449,8 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     uint64_t* accum = empty + kPairStages;
     uint64_t* recv_bar = accum + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
+    constexpr uint32_t kTmemCols = F4 ? 2 * kPairBN : kPairBN;
+    constexpr uint32_t kSfa = kPairBN, kSfb = kPairBN + 64;   // (F4) scale-factor columns
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();   // the K slice; owns rows [rank * RV::kRows, ...)
@@ -447,7 +499,7 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(tmem_slot)), "n"(kPairBN) : "memory");
+                         smem_u32(tmem_slot)), "n"(kTmemCols) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
         if (tr0 && lane == 0) p.trace[11] = clock64();
     }
@@ -461,6 +513,22 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     if (tr0 && threadIdx.x == 0) p.trace[1] = clock64();
+    if constexpr (F4) {
+        // warps 4-7 (TMEM lanes 32 * (warp - 4) ...) set every scale factor to
+        // 1.0 while the first operands are in flight; the MMA warp waits on
+        // named barrier 1 for them
+        if (warp >= 4) {
+            const uint32_t t = tmem + ((uint32_t)((warp & 3) * 32) << 16) + kPairBN;
+#pragma unroll
+            for (int c = 0; c < kPairBN; c += 8) tmem_fill8(t + c, 0x7F7F7F7Fu);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            asm volatile("bar.arrive 1, 160;" ::: "memory");
+        } else if (warp == 1) {
+            asm volatile("bar.sync 1, 160;" ::: "memory");
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+    }
 
     if (threadIdx.x == 0) {
         // ---- TMA producer: the rest of the ring (K beyond the first fill)
@@ -475,7 +543,7 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
         if (tr0) p.trace[2] = clock64();
     } else if (threadIdx.x == 32) {
         // ---- MMA issuer ----
-        constexpr uint32_t idesc = idesc_i8<kPairBN>();
+        constexpr uint32_t idesc = F4 ? idesc_f4<kPairBN>() : idesc_i8<kPairBN>();
         for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % kPairStages;
             const uint32_t ph = (kb / kPairStages) & 1;
@@ -483,10 +551,16 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
             if (tr0 && (kb == 0 || kb == nkb - 1)) p.trace[kb == 0 ? 3 : 4] = clock64();
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+            // 32 bytes of K per instruction either way (i8: 32 elements, F4: 64)
 #pragma unroll
-            for (int k = 0; k < kTcBK / 32; ++k)
-                umma_i8(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
-                        (kb | k) != 0);
+            for (int k = 0; k < kTcBK / 32; ++k) {
+                if constexpr (F4)
+                    umma_f4(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
+                            (kb | k) != 0, tmem + kSfa, tmem + kSfb);
+                else
+                    umma_i8(tmem, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
+                            (kb | k) != 0);
+            }
             umma_commit(&empty[s]);
         }
         umma_commit(accum);
@@ -507,12 +581,15 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
         // two counts per 16-bit lane pair (PRMT), clamped to 0/1 by one
         // VIMNMX.U16x2, placed at bits j and j + 16 by one shift-add:
         // 1.5 instructions per output bit instead of ~2.7
+        // (F4: f32 counts; a positive count has a nonzero upper half, so the
+        // same clamp runs on the upper halves)
+        constexpr uint32_t sel = F4 ? 0x7632u : 0x5410u;
         uint32_t r[64];
         tmem_ld64(taddr, r);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            w0 += __vminu2(__byte_perm(r[j], r[j + 16], 0x5410), 0x00010001u) << j;
-            w1 += __vminu2(__byte_perm(r[32 + j], r[48 + j], 0x5410), 0x00010001u) << j;
+            w0 += __vminu2(__byte_perm(r[j], r[j + 16], sel), 0x00010001u) << j;
+            w1 += __vminu2(__byte_perm(r[32 + j], r[48 + j], sel), 0x00010001u) << j;
         }
     }
     if (nkb == 0) w0 = w1 = 0u;   // (K shorter than one k-block per CTA: TMEM was never written)
@@ -561,7 +638,7 @@ bool_i8_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_
     if (tr0 && threadIdx.x == 0) p.trace[7] = clock64();
     if (p.trace && threadIdx.x == 0) p.trace[17 + 2 * cta] = gtimer();
     if (warp == 2)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kPairBN) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
 // ---- host side ---------------------------------------------------------------
@@ -597,7 +674,7 @@ static int make_map(CUtensorMap* map, const uint8_t* base, int rows, int cols, l
     return r == CUDA_SUCCESS ? SMX_OK : SMX_E_DRIVER;
 }
 
-template <int BN>
+template <int BN, bool F4 = false>
 static int launch_tc(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long long lda, long long ldbt,
                      cudaStream_t s, bool pdl = false) {
     CUtensorMap mA, mB;
@@ -605,7 +682,7 @@ static int launch_tc(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long 
     SMX_TRY(make_map(&mB, Bt, a.N, a.K, ldbt, BN));
     constexpr int kTcStages = TcStages<BN>::value;
     constexpr size_t smem = 1024 + kTcStages * (size_t)(kTcBM + BN) * kTcBK + 8 * (2 * kTcStages + 1) + 16;
-    auto kern = bool_i8_gemm_kernel<BN>;
+    auto kern = bool_i8_gemm_kernel<BN, F4>;
     SMX_TRY(set_max_smem((const void*)kern, smem));
     const int mtiles = ceil_div(a.M, kTcBM) - a.skip_tiles;
     if (mtiles <= 0) return SMX_OK;
@@ -654,7 +731,8 @@ static int launch_tc(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long 
 
 // Split-K pair launch (packed-bit output, no row skip).  The caller has
 // checked the shape (see bool_i8_gemm).
-template <int KS, int kPairStages>
+// (F4: a.K is the operand row length in BYTES, ceil(K / 2))
+template <int KS, int kPairStages, bool F4 = false>
 static int launch_tc_pair(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, long long lda, long long ldbt,
                           cudaStream_t s, bool pdl, int bt_rows = -1) {
     CUtensorMap mA, mB;
@@ -662,7 +740,7 @@ static int launch_tc_pair(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, 
     SMX_TRY(make_map(&mB, Bt, bt_rows < 0 ? a.N : bt_rows, a.K, ldbt, kPairBN));
     constexpr size_t smem = 1024 + kPairStages * (size_t)(kTcBM + kPairBN) * kTcBK + PairRecv<KS>::kBytes +
                             8 * (2 * kPairStages + 2) + 16;
-    auto kern = bool_i8_gemm_pair_kernel<KS, kPairStages>;
+    auto kern = bool_i8_gemm_pair_kernel<KS, kPairStages, F4>;
     SMX_TRY(set_max_smem((const void*)kern, smem));
     TcArgs args = a;
     args.splits = 1;
@@ -694,7 +772,7 @@ static int launch_tc_pair(const uint8_t* A, const uint8_t* Bt, const TcArgs& a, 
 // results are identical).
 static int g_tc_tile_n = 0;
 static int g_tc_pair = 1;
-static int g_tc_batch_ks = 2;   // (experiment switch: K slices per batched product)
+static int g_tc_batch_ks = 1;   // K slices per batched product (1: one CTA per tile, fastest measured)
 static unsigned long long* g_tc_trace = nullptr;
 
 int bool_i8_gemm(const uint8_t* A, const uint8_t* Bt, uint8_t* C, uint32_t* Cbits, int M, int N, int K,
@@ -747,7 +825,56 @@ int bool_i8_gemm_batched(const uint8_t* A, const uint8_t* Bt, uint32_t* Cbits, i
     if (lda < K || ldbt < K || (long long)ldc * 32 < N) return SMX_E_ARG;
     TcArgs a{nullptr, Cbits, batch * M, N, K, ldc, accumulate != 0, 0, 0, 1, M / kTcBM, N, g_tc_trace};
     if (g_tc_batch_ks == 4) return launch_tc_pair<4, 2>(A, Bt, a, lda, ldbt, s, /*pdl=*/true, batch * N);
+    // (one CTA per tile: counts up to K must fit the 16-bit clamp)
+    if (g_tc_batch_ks == 1 && K < 65536)
+        return launch_tc_pair<1, 2>(A, Bt, a, lda, ldbt, s, /*pdl=*/true, batch * N);
     return launch_tc_pair<2, kPairStagesBatched>(A, Bt, a, lda, ldbt, s, /*pdl=*/true, batch * N);
+}
+
+// The same products on E2M1 nibble operands (kind::mxf4, the pair kernel):
+// A is M rows of ceil(K / 2) bytes (lda bytes apart), B^T N rows likewise
+// (unpack_nib_ab); packed-bit output.  Any M, N, K >= 1.
+static int g_tc_f4 = 1;   // bool_mul_tc / bool_mul_tc_batched operands: 1 = E2M1 nibbles, 0 = bytes
+static int g_tc_f4_batch_stages = 2;   // (experiment switch: ring depth of the batched nibble products)
+
+int bool_f4_gemm(const uint8_t* A, const uint8_t* Bt, uint32_t* Cbits, int M, int N, int K, long long lda,
+                 long long ldbt, long long ldc, int accumulate, cudaStream_t s, bool pdl) {
+    if (M < 0 || N < 0 || K < 1 || Cbits == nullptr) return SMX_E_ARG;
+    if (M == 0 || N == 0) return SMX_OK;
+    const int kb = (K + 1) / 2;
+    if (!aligned16(A) || !aligned16(Bt) || (lda & 15) || (ldbt & 15)) return SMX_E_ALIGN;
+    if (lda < kb || ldbt < kb || (long long)ldc * 32 < N) return SMX_E_ARG;
+    TcArgs a{nullptr, Cbits, M, N, kb, ldc, accumulate != 0, 0, 0, 1, 0, 0, g_tc_trace};
+    // the same tile choice as bool_i8_gemm: the split-K pair for one wave of
+    // 128 x 64 tiles or fewer, else the widest tile that gives every SM one
+    const long long rows = ceil_div(M, kTcBM);
+    if (g_tc_pair != 0 && (g_tc_pair >= 2 || (rows * ceil_div(N, 64) <= 148 && g_tc_tile_n == 0))) {
+        if (g_tc_pair == 3) return launch_tc_pair<4, 2, true>(A, Bt, a, lda, ldbt, s, pdl);
+        return launch_tc_pair<2, kPairStagesSingle, true>(A, Bt, a, lda, ldbt, s, pdl);
+    }
+    if (g_tc_tile_n == 64) return launch_tc<64, true>(A, Bt, a, lda, ldbt, s, pdl);
+    if (g_tc_tile_n == 128) return launch_tc<128, true>(A, Bt, a, lda, ldbt, s, pdl);
+    if (g_tc_tile_n == 256) return launch_tc<256, true>(A, Bt, a, lda, ldbt, s, pdl);
+    if (rows * ceil_div(N, 256) >= 148) return launch_tc<256, true>(A, Bt, a, lda, ldbt, s, pdl);
+    if (rows * ceil_div(N, 128) >= 148) return launch_tc<128, true>(A, Bt, a, lda, ldbt, s, pdl);
+    return launch_tc<64, true>(A, Bt, a, lda, ldbt, s, pdl);
+}
+
+int bool_f4_gemm_batched(const uint8_t* A, const uint8_t* Bt, uint32_t* Cbits, int batch, int M, int N, int K,
+                         long long lda, long long ldbt, long long ldc, int accumulate, cudaStream_t s) {
+    if (batch < 0 || M < 0 || N < 0 || K < 1 || Cbits == nullptr) return SMX_E_ARG;
+    if (batch == 0 || M == 0 || N == 0) return SMX_OK;
+    if (M % kTcBM || N % kPairBN) return SMX_E_ARG;
+    const int kb = (K + 1) / 2;
+    if (!aligned16(A) || !aligned16(Bt) || (lda & 15) || (ldbt & 15)) return SMX_E_ALIGN;
+    if (lda < kb || ldbt < kb || (long long)ldc * 32 < N) return SMX_E_ARG;
+    TcArgs a{nullptr, Cbits, batch * M, N, kb, ldc, accumulate != 0, 0, 0, 1, M / kTcBM, N, g_tc_trace};
+    const int ks = g_tc_batch_ks, st = g_tc_f4_batch_stages;
+    if (ks == 1) return st == 3 ? launch_tc_pair<1, 3, true>(A, Bt, a, lda, ldbt, s, true, batch * N)
+                                : launch_tc_pair<1, 2, true>(A, Bt, a, lda, ldbt, s, true, batch * N);
+    if (ks == 4) return launch_tc_pair<4, 2, true>(A, Bt, a, lda, ldbt, s, true, batch * N);
+    return st == 3 ? launch_tc_pair<2, 3, true>(A, Bt, a, lda, ldbt, s, true, batch * N)
+                   : launch_tc_pair<2, 2, true>(A, Bt, a, lda, ldbt, s, true, batch * N);
 }
 
 // ---- Warshall on bytes with tensor-core phases 2/3 -----------------------------
@@ -876,6 +1003,9 @@ int unpack_bits_transposed_batched(const uint32_t* words, uint8_t* out, int batc
 int unpack_ab(const uint32_t* a_words, uint8_t* a_bytes, int a_rows, int a_cols, long long a_ldw, long long a_ld,
               const uint32_t* b_words, uint8_t* bt, int b_rows, int b_cols, long long b_ldw, long long b_ldt,
               cudaStream_t s);
+int unpack_nib_ab(const uint32_t* a_words, uint8_t* a_nib, int a_rows, int a_cols, long long a_ldw, long long a_ld,
+                  const uint32_t* b_words, uint8_t* bt, int b_rows, int b_cols, long long b_ldw, long long b_ldt,
+                  int batch, long long a_in, long long a_out, long long b_in, long long b_out, cudaStream_t s);
 
 inline long long round16(long long x) { return (x + 15) & ~15LL; }
 
@@ -893,21 +1023,31 @@ int bool_mul_tc(const uint32_t* A, const uint32_t* B, uint32_t* C, int M, int N,
     if (ws == nullptr || ws_bytes < bool_mul_ws_bytes(M, N, K)) return SMX_E_WORKSPACE;
     uint8_t* a8 = reinterpret_cast<uint8_t*>(ws);
     uint8_t* bt8 = a8 + ((M * round16(K) + 255) & ~255LL);
+    // E2M1 nibble operands (kind::mxf4) unless switched off
+    const bool f4 = g_tc_f4 != 0;
     GraphKey key;
-    key.fn = 300;
+    key.fn = f4 ? 301 : 300;
     const unsigned long long kv[] = {(uintptr_t)A, (uintptr_t)B, (uintptr_t)C, (unsigned long long)M,
                                      (unsigned long long)N, (unsigned long long)K, (unsigned long long)lda_w,
                                      (unsigned long long)ldb_w, (unsigned long long)ldc_w, (uintptr_t)ws,
                                      ws_bytes};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     return run_graphed(key, s, false, [&](cudaStream_t st) -> int {
-        SMX_TRY(unpack_ab(A, a8, M, K, lda_w, round16(K), B, bt8, K, N, ldb_w, round16(K), st));
-        // words past ceil(N/32) in each output row are padding: keep them zero
         const long long nw = (N + 31) / 32;
+        if (f4) {
+            const long long ldn = round16((K + 1) / 2);
+            SMX_TRY(unpack_nib_ab(A, a8, M, K, lda_w, ldn, B, bt8, K, N, ldb_w, ldn, 1, 0, 0, 0, 0, st));
+        } else {
+            SMX_TRY(unpack_ab(A, a8, M, K, lda_w, round16(K), B, bt8, K, N, ldb_w, round16(K), st));
+        }
+        // words past ceil(N/32) in each output row are padding: keep them zero
         if (ldc_w > nw) {
             cudaError_t e = cudaMemset2DAsync(C + nw, ldc_w * 4, 0, (ldc_w - nw) * 4, M, st);
             if (e != cudaSuccess) return (int)e;
         }
+        if (f4)
+            return bool_f4_gemm(a8, bt8, C, M, N, K, round16((K + 1) / 2), round16((K + 1) / 2), ldc_w, 0, st,
+                                /*pdl=*/ldc_w == nw);
         return bool_i8_gemm(a8, bt8, nullptr, C, M, N, K, round16(K), round16(K), ldc_w, 0, 0, 0, st,
                             /*pdl=*/ldc_w == nw);
     });
@@ -929,14 +1069,24 @@ int bool_mul_tc_batched(const uint32_t* A, const uint32_t* B, uint32_t* C, int b
     if (ws == nullptr || ws_bytes < bool_mul_batched_ws_bytes(batch, M, N, K)) return SMX_E_WORKSPACE;
     uint8_t* a8 = reinterpret_cast<uint8_t*>(ws);
     uint8_t* bt8 = a8 + (((long long)batch * M * round16(K) + 255) & ~255LL);
+    const bool f4 = g_tc_f4 != 0;
     GraphKey key;
-    key.fn = 302;
+    key.fn = f4 ? 303 : 302;
     const unsigned long long kv[] = {(uintptr_t)A, (uintptr_t)B, (uintptr_t)C, (unsigned long long)batch,
                                      (unsigned long long)M, (unsigned long long)N, (unsigned long long)K,
                                      (unsigned long long)lda_w, (unsigned long long)ldb_w,
                                      (unsigned long long)ldc_w, (uintptr_t)ws, ws_bytes};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     return run_graphed(key, s, false, [&](cudaStream_t st) -> int {
+        if (f4) {
+            // A as one stacked matrix (item 0 of a batch of B items)
+            const long long ldn = round16((K + 1) / 2);
+            SMX_TRY(unpack_nib_ab(A, a8, batch * M, K, lda_w, ldn, nullptr, nullptr, 0, 0, 1, 1, 1, 0, 0, 0, 0,
+                                  st));
+            SMX_TRY(unpack_nib_ab(nullptr, nullptr, 0, 0, 1, 1, B, bt8, K, N, ldb_w, ldn, batch, 0, 0,
+                                  (long long)K * ldb_w, (long long)N * ldn, st));
+            return bool_f4_gemm_batched(a8, bt8, C, batch, M, N, K, ldn, ldn, ldc_w, 0, st);
+        }
         SMX_TRY(unpack_bits(A, a8, batch * M, K, lda_w, round16(K), st));
         SMX_TRY(unpack_bits_transposed_batched(B, bt8, batch, K, N, ldb_w, round16(K), (long long)K * ldb_w,
                                                (long long)N * round16(K), st));
@@ -982,8 +1132,32 @@ int smx_tc_trace_arm(unsigned long long* buf) {
     return SMX_OK;
 }
 
+int smx_bool_gemm_f4(const uint8_t* A, const uint8_t* Bt, uint32_t* C_bits, int M, int N, int K, int lda, int ldbt,
+                     int ldc, int accumulate, void* stream) {
+    return bool_f4_gemm(A, Bt, C_bits, M, N, K, lda, ldbt, ldc, accumulate, as_stream(stream), /*pdl=*/true);
+}
+
+int smx_bool_gemm_f4_batched(const uint8_t* A, const uint8_t* Bt, uint32_t* C_bits, int batch, int M, int N, int K,
+                             int lda, int ldbt, int ldc, int accumulate, void* stream) {
+    return bool_f4_gemm_batched(A, Bt, C_bits, batch, M, N, K, lda, ldbt, ldc, accumulate, as_stream(stream));
+}
+
+int smx_set_tc_f4(int enable) {
+    if (enable != 0 && enable != 1) return SMX_E_ARG;
+    const int old = g_tc_f4;
+    g_tc_f4 = enable;
+    return old;
+}
+
+int smx_set_tc_f4_batch_stages(int stages) {
+    if (stages != 2 && stages != 3) return SMX_E_ARG;
+    const int old = g_tc_f4_batch_stages;
+    g_tc_f4_batch_stages = stages;
+    return old;
+}
+
 int smx_set_tc_batch_ks(int ks) {
-    if (ks != 2 && ks != 4) return SMX_E_ARG;
+    if (ks != 1 && ks != 2 && ks != 4) return SMX_E_ARG;
     const int old = g_tc_batch_ks;
     g_tc_batch_ks = ks;
     return old;
