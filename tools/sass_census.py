@@ -2,7 +2,7 @@
 
 Counts, per kernel, the opcodes that show which hardware path each kernel takes:
 packed-integer lane updates (VIMNMX.U16x2 / VIADDMNMX.U16x2 and the 32-bit
-forms), tcgen05 (UTCIMMA, LDTM, UTCBAR), TMA tensor loads (UTMALDG), 1-D bulk
+forms), tcgen05 (UTCIMMA for kind::i8, UTCOMMA for the block-scaled kind::mxf4, LDTM, UTCBAR), TMA tensor loads (UTMALDG), 1-D bulk
 async copies (UBLKCP), mbarrier ops (SYNCS.*), shared/global vector loads.
 """
 import re
@@ -13,7 +13,7 @@ from pathlib import Path
 
 REPO = Path(__file__).resolve().parent.parent
 LIB = REPO / "paper_1705_08743_b200" / "libsemimat_b200.so"
-OPS = ["VIMNMX.U16x2", "VIADDMNMX.U16x2", "VIMNMX", "VIADDMNMX", "IMNMX", "UTCIMMA", "UTMALDG", "UBLKCP", "LDTM",
+OPS = ["VIMNMX.U16x2", "VIADDMNMX.U16x2", "VIMNMX", "VIADDMNMX", "IMNMX", "UTCIMMA", "UTCOMMA", "UTMALDG", "UBLKCP", "LDTM",
        "UTCBAR", "SYNCS.ARRIVE.TRANS64", "SYNCS.PHASECHK.TRANS64.TRYWAIT", "LDS.128", "LDG.E.128", "LOP3.LUT",
        "SHFL.IDX", "BAR.SYNC"]
 
