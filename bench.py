@@ -789,34 +789,57 @@ def secondary(dev):
     for n_tc in (1024, 2048, 4096, 8192):
         A = (torch.rand((n_tc, n_tc), device=dev) < 0.05).to(torch.uint8)
         Bt = (torch.rand((n_tc, n_tc), device=dev) < 0.05).to(torch.uint8)
+        # the same 0/1 operands as E2M1 nibbles (1.0 = 0b0010), two per byte
+        A4 = (A[:, 0::2] * 2 + A[:, 1::2] * 32).contiguous()
+        Bt4 = (Bt[:, 0::2] * 2 + Bt[:, 1::2] * 32).contiguous()
         o = torch.zeros((n_tc, n_tc // 32), dtype=torch.int32, device=dev)
-        f = lambda: _native.check(lib.smx_bool_gemm_i8(  # noqa: E731
+        o4 = torch.zeros_like(o)
+        f8 = lambda: _native.check(lib.smx_bool_gemm_i8(  # noqa: E731
             A.data_ptr(), Bt.data_ptr(), None, o.data_ptr(), n_tc, n_tc, n_tc, n_tc, n_tc, n_tc // 32, 0,
             _native.stream_ptr(dev)), "tc")
-        te = cuda_time(f, 20 if n_tc <= 4096 else 5, 2)
+        f4 = lambda: _native.check(lib.smx_bool_gemm_f4(  # noqa: E731
+            A4.data_ptr(), Bt4.data_ptr(), o4.data_ptr(), n_tc, n_tc, n_tc, n_tc // 2, n_tc // 2, n_tc // 32, 0,
+            _native.stream_ptr(dev)), "tc f4")
+        te = cuda_time(f4, 20 if n_tc <= 4096 else 5, 2)
         # device rate: back-to-back launches in one graph (an eager Python
         # loop of launches is host-bound at this size: ~5 us per launch)
-        t = graph_time(f, 20 if n_tc <= 4096 else 3, 20 if n_tc <= 4096 else 2)
+        it, reps = (20, 20) if n_tc <= 4096 else (3, 2)
+        t8 = graph_time(f8, it, reps)
+        t = graph_time(f4, it, reps)
         tc[f"n{n_tc}"] = {"kernel_us": t * 1e6, "ops_per_s": 2 * n_tc ** 3 / t,
                           "frac_of_int8_peak": 2 * n_tc ** 3 / t / int8_peak,
-                          "eager_launch_us": te * 1e6}
+                          "eager_launch_us": te * 1e6,
+                          "i8_kernel_us": t8 * 1e6, "i8_frac_of_int8_peak": 2 * n_tc ** 3 / t8 / int8_peak,
+                          "same_bits_as_i8": bool(torch.equal(o, o4))}
     # C1-shaped products many per launch (bool_mul_many on 128-multiple
-    # shapes): the batched split-K pair, three CTAs per SM
+    # shapes): the batched kernel, three CTAs per SM
     nb = 16
     A = (torch.rand((nb * 1024, 1024), device=dev) < 0.05).to(torch.uint8)
     Bt = (torch.rand((nb * 1024, 1024), device=dev) < 0.05).to(torch.uint8)
+    A4 = (A[:, 0::2] * 2 + A[:, 1::2] * 32).contiguous()
+    Bt4 = (Bt[:, 0::2] * 2 + Bt[:, 1::2] * 32).contiguous()
     o = torch.zeros((nb * 1024, 32), dtype=torch.int32, device=dev)
-    f = lambda: _native.check(lib.smx_bool_gemm_i8_batched(  # noqa: E731
+    o4 = torch.zeros_like(o)
+    f8 = lambda: _native.check(lib.smx_bool_gemm_i8_batched(  # noqa: E731
         A.data_ptr(), Bt.data_ptr(), o.data_ptr(), nb, 1024, 1024, 1024, 1024, 1024, 32, 0,
         _native.stream_ptr(dev)), "tc batched")
-    t = graph_time(f, 10, 10) / nb
+    f4 = lambda: _native.check(lib.smx_bool_gemm_f4_batched(  # noqa: E731
+        A4.data_ptr(), Bt4.data_ptr(), o4.data_ptr(), nb, 1024, 1024, 1024, 512, 512, 32, 0,
+        _native.stream_ptr(dev)), "tc f4 batched")
+    t8 = graph_time(f8, 10, 10) / nb
+    t = graph_time(f4, 10, 10) / nb
     tc["n1024_batch16"] = {"kernel_us_per_product": t * 1e6, "ops_per_s": 2 * 1024 ** 3 / t,
                            "frac_of_int8_peak": 2 * 1024 ** 3 / t / int8_peak,
-                           "note": "16 independent 1024^3 products per launch (smx_bool_gemm_i8_batched)"}
-    del A, Bt, o
-    tc["kernel"] = ("bool_i8_gemm_pair_kernel (split-K CTA pair) at 1024, bool_i8_gemm_kernel (automatic tile "
-                    "width) above; kernel_us = device time per launch, back-to-back launches replayed from one "
-                    "CUDA graph")
+                           "i8_kernel_us_per_product": t8 * 1e6,
+                           "i8_frac_of_int8_peak": 2 * 1024 ** 3 / t8 / int8_peak,
+                           "same_bits_as_i8": bool(torch.equal(o, o4)),
+                           "note": "16 independent 1024^3 products per launch (smx_bool_gemm_f4_batched)"}
+    del A, Bt, A4, Bt4, o, o4
+    tc["kernel"] = ("E2M1 nibble operands, tcgen05 kind::mxf4 with unit scale factors (smx_bool_gemm_f4, the "
+                    "default of the public product): bool_f4 split-K CTA pair at 1024, the plain kernel above; "
+                    "i8_* = the same product on byte operands, kind::i8 (smx_bool_gemm_i8); kernel_us = device "
+                    "time per launch, back-to-back launches replayed from one CUDA graph; the denominator is "
+                    "the dense int8 peak (cuBLAS), which the nibble kernels may exceed")
     out["bool_tc_gemm_kernel"] = tc
     cfg = workloads.CONFIGS["c2_bool_warshall"]
     (t2,) = workloads.make_inputs(cfg)
