@@ -25,6 +25,7 @@ _SIGS = {
     "smx_launch_count": ([], ctypes.c_ulonglong),
     "smx_set_bounded_fastpath": ([c_int], c_int),
     "smx_set_packed_tiles_per_cta": ([c_int], c_int),
+    "smx_set_packed_producer_backoff": ([c_int], c_int),
     "smx_set_fw_lookahead": ([c_int], c_int),
     "smx_set_graphs": ([c_int], c_int),
     "smx_set_fw_side_lite": ([c_int], c_int),

@@ -34,6 +34,8 @@ int set_max_smem(const void* func, size_t bytes) {
 int bounded_fastpath_enabled() { return g_bounded.load(std::memory_order_relaxed); }
 static std::atomic<int> g_packed_tpc{1};
 int packed_tiles_per_cta() { return g_packed_tpc.load(std::memory_order_relaxed); }
+static std::atomic<int> g_packed_backoff{0};
+int packed_producer_backoff() { return g_packed_backoff.load(std::memory_order_relaxed); }
 
 int scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
     static bool pool_configured[64] = {};
@@ -201,6 +203,10 @@ unsigned long long smx_launch_count(void) { return smx::g_launches.load(); }
 int smx_set_packed_tiles_per_cta(int tpc) {
     if (tpc != 1 && tpc != 2) return SMX_E_ARG;
     return smx::g_packed_tpc.exchange(tpc);
+}
+int smx_set_packed_producer_backoff(int ns) {
+    if (ns < -100000 || ns > 100000) return SMX_E_ARG;
+    return smx::g_packed_backoff.exchange(ns);
 }
 int smx_set_bounded_fastpath(int enable) {
     return smx::g_bounded.exchange(enable ? 1 : 0);

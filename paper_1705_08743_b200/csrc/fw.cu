@@ -908,7 +908,8 @@ int fw_run(T* Tm, int n, long long ld, int kind, void* ws, size_t ws_bytes, cuda
                                          ((unsigned long long)g_fw_split_3a.load() << 1) |
                                          ((unsigned long long)g_pivot_pairs.load() << 3) |
                                          ((unsigned long long)g_fw_packed_panel.load() << 4) |
-                                         ((unsigned long long)g_fw_panel_buffers.load() << 6)};
+                                         ((unsigned long long)g_fw_panel_buffers.load() << 6) |
+                                         ((unsigned long long)(unsigned)packed_producer_backoff() << 8)};
     for (size_t i = 0; i < sizeof(kv) / sizeof(kv[0]); ++i) key.v[i] = kv[i];
     // the phase-3 trace records host-side state per launch: trace runs stay eager
     return run_graphed(key, s, g_trace.armed, [&](cudaStream_t st) -> int {

@@ -87,11 +87,14 @@ struct PackedArgsT {
     const int* cert;              // nullable: nonzero = operands packed in the shifted encoding
     int col_tile0;                // first output column tile of the launch (grid x counts from it)
     int mtiles;                   // row tiles of the launch (after the skipped ones)
+    int backoff_ns;               // producer's free-slot wait (pk_mbar_wait_backoff)
 };
 
 // smx_set_packed_tiles_per_cta (abi.cu): output tiles per CTA of the packed
 // GEMM (1 or 2).
 int packed_tiles_per_cta();
+// smx_set_packed_producer_backoff (abi.cu): see pk_mbar_wait_backoff.
+int packed_producer_backoff();
 
 // ---- pack kernels -----------------------------------------------------------
 // Canonical (distance-form) lane value of one storage cell.
@@ -214,6 +217,47 @@ __device__ __forceinline__ void pk_mbar_wait(uint64_t* bar, uint32_t parity) {
             : "memory");
     } while (!ok);
 }
+// 0xFFFF in each 16-bit lane whose sign bit is set (prmt's sign-replicate
+// mode, selector msb; __byte_perm only takes the 3-bit byte indices).
+__device__ __forceinline__ uint32_t pk_lane_sign_masks(uint32_t x) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %1, 0xbb99;" : "=r"(r) : "r"(x));
+    return r;
+}
+// The producer's wait for a free ring slot.  It runs three stages ahead, so it
+// always waits, and a bare try_wait loop issues SYNCS + BRA + YIELD every ~35
+// cycles for the CTA's whole life (ncu at n = 8192: 11% of the kernel's warp
+// instructions, on the consumers' issue slots).  ns > 0: try_wait with that
+// suspend-time hint; ns < 0: nanosleep(-ns) between polls; 0: bare loop.
+__device__ __forceinline__ void pk_mbar_wait_backoff(uint64_t* bar, uint32_t parity, int ns) {
+    if (ns == 0) {
+        pk_mbar_wait(bar, parity);
+        return;
+    }
+    const uint32_t addr = pk_smem(bar);
+    uint32_t ok = 0;
+    for (;;) {
+        if (ns > 0) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(ok)
+                : "r"(addr), "r"(parity), "r"((uint32_t)ns)
+                : "memory");
+        } else {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(ok)
+                : "r"(addr), "r"(parity)
+                : "memory");
+        }
+        if (ok) break;
+        if (ns < 0) __nanosleep((unsigned)(-ns));
+    }
+}
 __device__ __forceinline__ void pk_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -308,7 +352,7 @@ packed_gemm_kernel(const PackedArgsT<T> p) {
                     for (int kt = kb; kt < kend; ++kt) {
                         const int g = t * KT + kt;          // position in the CTA's stage sequence
                         const int s = g % ST;
-                        if (g >= ST) pk_mbar_wait(&empty[s], ((g / ST) - 1) & 1);
+                        if (g >= ST) pk_mbar_wait_backoff(&empty[s], ((g / ST) - 1) & 1, p.backoff_ns);
                         flag[s] = (fmask >> (kt - kb)) & 1u;
                         pk_mbar_expect_tx(&full[s], (G::A_TILE_WORDS + G::B_TILE_WORDS) * 4);
                         if (g >= first) issue(mt, kt, s);
@@ -381,32 +425,75 @@ packed_gemm_kernel(const PackedArgsT<T> p) {
         }
 
         // ---- fold C in and store ----
-        if constexpr (!L::kOneInstr) {
-            if (p.cert != nullptr && *p.cert != 0) {
+        // u16 accumulate launches (every phase-3 launch) fold in the storage
+        // domain: storage = canonical ^ m (m = all ones for anti-distance), so
+        // min over canonical lanes is max (anti) or min (dist) over storage
+        // lanes and C needs no conversion either way.  The shifted encoding's
+        // "lane >= S'" -> S is one add, one PRMT and one LOP3 per word: every
+        // lane is <= 2 S' = 65534 after the first k-step, so lane + 1 cannot
+        // carry into its neighbour and its sign bit is the test; PRMT 0xbb99
+        // spreads the sign bits into lane masks.  (The generic form below
+        // costs 7 instructions per word for from_shifted and 3 for the fold;
+        // ncu at n = 8192: 4.3% of the ALU pipe's instructions.)
+        const bool shifted = !L::kOneInstr && p.cert != nullptr && *p.cert != 0;
+        bool done = false;
+        if constexpr (std::is_same<T, uint16_t>::value && !G::CSMEM) {
+            if (p.accumulate && KT > 0 && col0 + G::BN <= p.N) {
+                const uint32_t m = anti ? 0xFFFFFFFFu : 0u;
+                auto fold_rows = [&](auto sh) {
+#pragma unroll
+                    for (int i = 0; i < TM; ++i) {
+                        const int grow = row0 + tr * TM + i;
+                        if (grow >= p.M) continue;
+                        T* crow = p.C + (long long)grow * p.ldc + col0;
+#pragma unroll
+                        for (int g = 0; g < 2; ++g) {
+                            uint4* cp = reinterpret_cast<uint4*>(crow + (g * (BNW / 2) + tc * HW) * 2);
+                            const uint4 v = *cp;
+                            const uint32_t c[HW] = {v.x, v.y, v.z, v.w};
+                            uint32_t o[HW];
+#pragma unroll
+                            for (int j = 0; j < HW; ++j) {
+                                uint32_t x = acc[i][g * HW + j];
+                                if (decltype(sh)::value) x |= pk_lane_sign_masks(x + 0x00010001u);
+                                x ^= m;
+                                o[j] = anti ? __vmaxu2(x, c[j]) : __vminu2(x, c[j]);
+                            }
+                            *cp = make_uint4(o[0], o[1], o[2], o[3]);
+                        }
+                    }
+                };
+                if (shifted) fold_rows(std::true_type{});
+                else fold_rows(std::false_type{});
+                done = true;
+            }
+        }
+        if (!done) {
+            if (shifted) {
 #pragma unroll
                 for (int i = 0; i < TM; ++i)
 #pragma unroll
                     for (int j = 0; j < TNW; ++j) acc[i][j] = L::from_shifted(acc[i][j]);
             }
-        }
-        if (c_async) pk_mbar_wait(cbar, 0);
+            if (c_async) pk_mbar_wait(cbar, 0);
 #pragma unroll
-        for (int i = 0; i < TM; ++i) {
-            const int grow = row0 + tr * TM + i;
-            if (grow >= p.M) continue;
-            T* crow = p.C + (long long)grow * p.ldc;
+            for (int i = 0; i < TM; ++i) {
+                const int grow = row0 + tr * TM + i;
+                if (grow >= p.M) continue;
+                T* crow = p.C + (long long)grow * p.ldc;
 #pragma unroll
-            for (int g = 0; g < 2; ++g) {
-                const int cc = (g * (BNW / 2) + tc * HW) * L::kCellsPerWord;   // cell offset in the tile
-                uint32_t* w = &acc[i][g * HW];
-                if (c_async || p.accumulate) {
-                    uint32_t c[HW];
-                    if (c_async) load_c_group<T, HW>(Cs + (tr * TM + i) * G::BN, cc, G::BN, anti, c);
-                    else load_c_group<T, HW>(crow, col0 + cc, p.N, anti, c);
+                for (int g = 0; g < 2; ++g) {
+                    const int cc = (g * (BNW / 2) + tc * HW) * L::kCellsPerWord;   // cell offset in the tile
+                    uint32_t* w = &acc[i][g * HW];
+                    if (c_async || p.accumulate) {
+                        uint32_t c[HW];
+                        if (c_async) load_c_group<T, HW>(Cs + (tr * TM + i) * G::BN, cc, G::BN, anti, c);
+                        else load_c_group<T, HW>(crow, col0 + cc, p.N, anti, c);
 #pragma unroll
-                    for (int j = 0; j < HW; ++j) w[j] = L::fold(w[j], c[j]);
+                        for (int j = 0; j < HW; ++j) w[j] = L::fold(w[j], c[j]);
+                    }
+                    store_c_group<T, HW>(crow, col0 + cc, p.N, anti, w);
                 }
-                store_c_group<T, HW>(crow, col0 + cc, p.N, anti, w);
             }
         }
     }
@@ -553,6 +640,7 @@ inline int packed_run(T* C, int M, int N, int K, long long ldc, int kind, int ac
     const int mtiles = row_tiles - a.skip_tiles;
     if (mtiles <= 0) return SMX_OK;
     a.mtiles = mtiles;
+    a.backoff_ns = packed_producer_backoff();
     const int tpc = packed_tiles_per_cta();
     // launch_kernel: a launch on the look-ahead side stream (3a) carries the
     // side stream's priority into a captured graph (PriorityScope)
