@@ -736,12 +736,26 @@ inline size_t bits_ws_bytes(int n, long long ld_w) {
     return rp + ((cp + 255) & ~size_t(255)) + persist_ctr_bytes(n);
 }
 
+// -DSMX_DEV_BOOL_SKIP (tools/perf_c2_legs.py): timing experiments that leave
+// out legs of the schedule by the mask in $SMX_DEV_BOOL_SKIP (1 = 3b, 2 =
+// pivot, 4 = row panel, 8 = 3a).  Results are wrong; never in a normal build.
+#ifdef SMX_DEV_BOOL_SKIP
+#include <cstdlib>
+static int dev_skip(int bit) {
+    static const int mask = [] { const char* e = getenv("SMX_DEV_BOOL_SKIP"); return e ? atoi(e) : 0; }();
+    return mask & bit;
+}
+#else
+static constexpr int dev_skip(int) { return 0; }
+#endif
+
 // Pivot tile + pivot row panel of block [k0, k0 + bb).
 static int bits_pivot_and_row_panel(uint32_t* T, int n, long long ld_w, uint32_t* RP, int k0, int bb,
                                     cudaStream_t s) {
     const int kw0 = k0 / 32, nw = (n + 31) / 32;
     uint32_t* rowK = T + (long long)k0 * ld_w;
-    SMX_TRY(launch_bool_pivot(rowK + kw0, bb, ld_w, s));
+    if (!dev_skip(2)) SMX_TRY(launch_bool_pivot(rowK + kw0, bb, ld_w, s));
+    if (dev_skip(4)) return SMX_OK;
     PdlNext pdl;   // the row panel directly follows the pivot kernel
     // Row panel in place, no snapshot: T[K,:] |= P* . T[K,:] with P* = T[K,K]
     // closed.  A CTA may read rows K that another CTA has already OR-ed into;
@@ -814,8 +828,9 @@ static int bool_warshall_schedule(uint32_t* T, int n, long long ld_w, uint32_t* 
         if (r + 1 < R) {
             const int k1 = k0 + BLK, bb1 = blk(r + 1);
             // 3a: the next pivot block's rows
-            SMX_TRY(bool_bits_gemm(T + (long long)k1 * ld_w + kw0, rowK, T + (long long)k1 * ld_w, bb1, nw, bb,
-                                   ld_w, ld_w, ld_w, 1, 0, 0, s));
+            if (!dev_skip(8))
+                SMX_TRY(bool_bits_gemm(T + (long long)k1 * ld_w + kw0, rowK, T + (long long)k1 * ld_w, bb1, nw, bb,
+                                       ld_w, ld_w, ld_w, 1, 0, 0, s));
             if ((e = cudaEventRecord(ss->fork, s)) != cudaSuccess) return (int)e;
             if ((e = cudaStreamWaitEvent(ss->side, ss->fork, 0)) != cudaSuccess) return (int)e;
             {
@@ -825,7 +840,8 @@ static int bool_warshall_schedule(uint32_t* T, int n, long long ld_w, uint32_t* 
             if ((e = cudaEventRecord(ss->join, ss->side)) != cudaSuccess) return (int)e;
             // 3b: every other row (reads T[:, K_r] of rows outside K_r u K_{r+1}
             // only, which the side stream does not touch)
-            SMX_TRY(bool_bits_gemm(T + kw0, rowK, T, n, nw, bb, ld_w, ld_w, ld_w, 1, k0, bb + bb1, s));
+            if (!dev_skip(1))
+                SMX_TRY(bool_bits_gemm(T + kw0, rowK, T, n, nw, bb, ld_w, ld_w, ld_w, 1, k0, bb + bb1, s));
             if ((e = cudaStreamWaitEvent(s, ss->join, 0)) != cudaSuccess) return (int)e;
         } else {
             SMX_TRY(bool_bits_gemm(T + kw0, rowK, T, n, nw, bb, ld_w, ld_w, ld_w, 1, k0, bb, s));
