@@ -452,3 +452,53 @@ def test_bool_mul_many_on_tensor_cores(batch, m, k, n, oracle_lib):
         want = oracle_lib.bool_mul(oracle_lib.pack_bits(As[i].astype(np.uint8)),
                                    oracle_lib.pack_bits(Bs[i].astype(np.uint8)), k)
         np.testing.assert_array_equal(got[i].blocks, want)
+
+
+# -- the packed kernel's storage-domain epilogue (fold against raw C words) --------
+
+@pytest.mark.parametrize("certified", [True, False])
+@pytest.mark.parametrize("kind", ["anti", "dist"])
+def test_packed_accumulate_epilogue_full_range_c(kind, certified, oracle_lib):
+    """C (+)= A (x) B on the packed kernel with C drawn from the whole u16
+    range: the epilogue folds in the storage domain (max / min against the raw
+    C words) and, for certified operands, maps every lane >= S' = 2^15 - 1 of
+    the shifted accumulator back to S with add + PRMT + LOP3.  Operand lanes sit
+    at the edges of the certificate (0, 1, 2^14 - 1, S) so sums reach S' - 1,
+    S' and 2 S'; C holds 0, S' - 1, S', 2^15, S - 1 and S among random values.
+    M and N are ragged, so both the full-tile and the edge-tile paths run."""
+    from paper_1705_08743_b200 import _native
+    lib = _native.lib()
+    rng = np.random.default_rng(11 + certified)
+    M, N, K = 2100, 2056, 300
+    S = 65535
+    edge = np.array([0, 1, 2, 16382, 16383, S], dtype=np.uint32)
+    def operand(r, c):
+        v = rng.choice(edge, size=(r, c), p=[0.02, 0.02, 0.02, 0.07, 0.07, 0.80]).astype(np.uint32)
+        return v
+    a, b = operand(M, K), operand(K, N)
+    if not certified:
+        a[5, 7] = 40000          # one lane past 2^14 voids the product-wide certificate
+    cvals = np.array([0, 32766, 32767, 32768, 65534, 65535], dtype=np.uint32)
+    c = rng.integers(0, 65536, (M, N), dtype=np.uint32)
+    mask = rng.random((M, N)) < 0.3
+    c[mask] = rng.choice(cvals, size=int(mask.sum()))
+    if kind == "anti":
+        a, b, c = S - a, S - b, S - c
+    a, b, c = a.astype(np.uint16), b.astype(np.uint16), c.astype(np.uint16)
+    lda, ldn = 304, 2064
+    apad = np.zeros((M, lda), np.uint16); apad[:, :K] = a
+    bpad = np.zeros((K, ldn), np.uint16); bpad[:, :N] = b
+    cpad = np.zeros((M, ldn), np.uint16); cpad[:, :N] = c
+    ta = torch.from_numpy(apad.view(np.int16)).cuda()
+    tb = torch.from_numpy(bpad.view(np.int16)).cuda()
+    tc = torch.from_numpy(cpad.view(np.int16)).cuda()
+    _native.check(lib.smx_semiring_gemm_u16(ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), M, N, K, lda, ldn, ldn,
+                                            0 if kind == "anti" else 1, 1, _native.stream_ptr()), "accumulate")
+    torch.cuda.synchronize()
+    got = tc.cpu().numpy().view(np.uint16)
+    rows = np.r_[0:130, 1990:2100]
+    prod = oracle_lib.semiring_mul(apad[rows], b, K, 16, kind)
+    want = np.maximum(c[rows], prod) if kind == "anti" else np.minimum(c[rows], prod)
+    np.testing.assert_array_equal(got[rows, :N], want)
+    # padding columns of C are not touched
+    np.testing.assert_array_equal(got[:, N:], cpad[:, N:])
