@@ -1,0 +1,143 @@
+"""Randomised differential run against the CPU oracle (development aid; the
+oracle is the checker here, as in tests/): products and closures of the lane
+types at random shapes, widths, kinds and value regimes (sparse small weights,
+lanes at the edges of the 2^(w-2) certificate and of the 2^(w-1) bound, full
+range, near S), Boolean products and closures at random densities, all through
+the public classes.  Every result must equal the oracle's bit for bit.
+
+    python tools/fuzz_parity.py [seconds] [seed]
+
+Prints one JSON line per failure and a summary line."""
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import oracle  # noqa: E402
+from paper_1705_08743_b200 import AntidistMatrix, BoolMatrix, DistMatrix  # noqa: E402
+
+budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
+seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+rng = np.random.default_rng(seed)
+DT = {8: np.uint8, 16: np.uint16, 32: np.uint32}
+
+
+def lanes_per_chunk(w):
+    return 16 // (w // 8)
+
+
+def dist_values(r, c, w, regime):
+    """Distance-form cells (S = unreachable)."""
+    S = (1 << w) - 1
+    p = float(rng.choice([0.02, 0.1, 0.5, 1.0]))
+    if regime == "small":
+        v = rng.integers(0, min(S, 1001), (r, c), dtype=np.uint64)
+    elif regime == "cert_edge":      # around 2^(w-2), the product-wide certificate
+        q = 1 << (w - 2)
+        v = q - 3 + rng.integers(0, 6, (r, c), dtype=np.uint64)
+        v[rng.random((r, c)) < 0.7] = rng.integers(0, 50)
+    elif regime == "bound_edge":     # around 2^(w-1), the per-tile bounded test
+        h = 1 << (w - 1)
+        v = h - 3 + rng.integers(0, 6, (r, c), dtype=np.uint64)
+        v[rng.random((r, c)) < 0.7] = rng.integers(0, 50)
+    elif regime == "near_s":
+        v = S - rng.integers(0, 4, (r, c), dtype=np.uint64)
+        v[rng.random((r, c)) < 0.5] = rng.integers(0, 5)
+    else:                            # full range
+        v = rng.integers(0, S + 1, (r, c), dtype=np.uint64)
+    v[rng.random((r, c)) > p] = S
+    return v
+
+
+def padded(v, w, kind):
+    S = (1 << w) - 1
+    r, c = v.shape
+    L = lanes_per_chunk(w)
+    cp = -(-c // L) * L
+    out = np.full((r, cp), S, dtype=np.uint64)     # distance-form pad = S
+    out[:, :c] = v
+    if kind == "anti":
+        out = S - out
+    return out.astype(DT[w])
+
+
+def rand_dim(lo, hi):
+    return int(np.exp(rng.uniform(np.log(lo), np.log(hi))))
+
+
+def case_lane_mul():
+    w = int(rng.choice([8, 16, 16, 32]))
+    kind = str(rng.choice(["anti", "dist"]))
+    if rng.random() < 0.35:          # shapes that take the packed kernel
+        M, N, K = rand_dim(1500, 2600), rand_dim(1500, 2600), rand_dim(256, 700)
+    else:
+        M, N, K = rand_dim(1, 1500), rand_dim(1, 1500), rand_dim(1, 900)
+    regime = str(rng.choice(["small", "cert_edge", "bound_edge", "near_s", "full"]))
+    a = padded(dist_values(M, K, w, regime), w, kind)
+    b = padded(dist_values(K, N, w, regime), w, kind)
+    cls = AntidistMatrix if kind == "anti" else DistMatrix
+    got = (cls(M, K, w, a) * cls(K, N, w, b)).data
+    want = oracle.semiring_mul(a, b, K, w, kind)
+    return {"op": "lane_mul", "w": w, "kind": kind, "M": M, "N": N, "K": K, "regime": regime}, np.array_equal(got, want)
+
+
+def case_lane_close():
+    w = int(rng.choice([8, 16, 16, 32]))
+    kind = str(rng.choice(["anti", "dist"]))
+    n = rand_dim(1, 1300)
+    regime = str(rng.choice(["small", "small", "cert_edge", "bound_edge", "near_s", "full"]))
+    v = dist_values(n, n, w, regime)
+    if rng.random() < 0.7:
+        v[np.arange(n), np.arange(n)] = 0
+    t = padded(v, w, kind)
+    cls = AntidistMatrix if kind == "anti" else DistMatrix
+    got = cls(n, n, w, t).transitive_closure().data
+    want = oracle.semiring_close(t, w, kind)
+    return {"op": "lane_close", "w": w, "kind": kind, "n": n, "regime": regime}, np.array_equal(got, want)
+
+
+def case_bool_mul():
+    M, N, K = rand_dim(1, 2000), rand_dim(1, 2000), rand_dim(1, 2000)
+    p = float(rng.choice([0.001, 0.01, 0.05, 0.3, 0.9]))
+    a = (rng.random((M, K)) < p).astype(np.uint8)
+    b = (rng.random((K, N)) < p).astype(np.uint8)
+    got = (BoolMatrix.from_numpy(a) * BoolMatrix.from_numpy(b)).blocks
+    want = oracle.bool_mul(oracle.pack_bits(a), oracle.pack_bits(b), K)
+    return {"op": "bool_mul", "M": M, "N": N, "K": K, "p": p}, np.array_equal(got, want)
+
+
+def case_bool_close():
+    n = rand_dim(1, 1800)
+    p = float(rng.choice([0.5, 1.0, 2.0, 4.0])) / max(n, 1)
+    t = (rng.random((n, n)) < p).astype(np.uint8)
+    m = BoolMatrix.from_numpy(t)
+    got = (m.transitive_closure() if rng.random() < 0.7 else m.reflexive_transitive_closure())
+    want = oracle.bool_close(oracle.pack_bits(t))
+    gb = got.blocks
+    if not np.array_equal(gb, want):        # (reflexive: join the identity on the oracle side)
+        eye = oracle.pack_bits(np.eye(n, dtype=np.uint8))
+        want = want | eye
+    return {"op": "bool_close", "n": n, "p": p}, np.array_equal(gb, want)
+
+
+cases = [case_lane_mul, case_lane_mul, case_lane_close, case_bool_mul, case_bool_close]
+counts, fails = {}, 0
+t0 = time.time()
+i = 0
+while time.time() - t0 < budget:
+    fn = cases[i % len(cases)]
+    i += 1
+    try:
+        desc, ok = fn()
+    except Exception as ex:   # noqa: BLE001
+        desc, ok = {"op": fn.__name__, "error": repr(ex)[:300]}, False
+    counts[desc["op"]] = counts.get(desc["op"], 0) + 1
+    if not ok:
+        fails += 1
+        print(json.dumps({"FAIL": desc, "case_index": i, "seed": seed}), flush=True)
+torch.cuda.synchronize()
+print(json.dumps({"seed": seed, "seconds": round(time.time() - t0, 1), "cases": counts, "failures": fails}))
