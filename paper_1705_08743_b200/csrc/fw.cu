@@ -751,7 +751,17 @@ int fw_rounds_packed(T* Tm, int n, long long ld, int kind, T* RP, void* pws, siz
     // on the main stream).  A certified round packs its B on the main stream
     // after its certificate, as before.
     auto bbuf = [&](int r) -> void* { return (b2 != nullptr && ((r - ra) & 1)) ? b2 : nullptr; };
-    auto side_packs_b = [&](int r) { return b2 != nullptr && r > ra && !certified(r); };
+    // The workspace's own B block sits behind the packed A tiles, whose size
+    // depends on the round's K: a ragged last block (blk(r) < BLK) puts its B
+    // tiles inside the region round r-1's A tiles still occupy, so the side
+    // chain may not pack them there beside round r-1's phase 3 (it corrupted
+    // A tiles phase 3 had yet to read: wrong closures, timing dependent, for
+    // n with an odd number of rounds and a last block of fewer k-tiles, e.g.
+    // n = 7000 or 8000 at BLK = 128, 8300 at 256).  That round packs its B
+    // on the main stream after the join, as a single-buffered round does.
+    auto side_packs_b = [&](int r) {
+        return b2 != nullptr && r > ra && !certified(r) && (bbuf(r) != nullptr || blk(r) == BLK);
+    };
     SMX_TRY(fw_pivot_and_row_panel<T>(Tm, n, ld, kind, RP, ra * BLK, blk(ra), s, false, true));
     if (!certified(ra))
         SMX_TRY(packed_pack_a_rows<T>(Tm + ra * BLK, n, n, blk(ra), ld, kind, pws, pws_bytes, t0, tiles, s));

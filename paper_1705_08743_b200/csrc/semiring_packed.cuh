@@ -437,6 +437,7 @@ packed_gemm_kernel(const PackedArgsT<T> p) {
         // ncu at n = 8192: 4.3% of the ALU pipe's instructions.)
         const bool shifted = !L::kOneInstr && p.cert != nullptr && *p.cert != 0;
         bool done = false;
+#ifndef SMX_PACKED_GENERIC_EPILOGUE   // (A/B and debugging: the generic fold below for every tile)
         if constexpr (std::is_same<T, uint16_t>::value && !G::CSMEM) {
             if (p.accumulate && KT > 0 && col0 + G::BN <= p.N) {
                 const uint32_t m = anti ? 0xFFFFFFFFu : 0u;
@@ -468,6 +469,7 @@ packed_gemm_kernel(const PackedArgsT<T> p) {
                 done = true;
             }
         }
+#endif
         if (!done) {
             if (shifted) {
 #pragma unroll

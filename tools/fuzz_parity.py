@@ -5,7 +5,10 @@ lanes at the edges of the 2^(w-2) certificate and of the 2^(w-1) bound, full
 range, near S), Boolean products and closures at random densities, all through
 the public classes.  Every result must equal the oracle's bit for bit.
 
-    python tools/fuzz_parity.py [seconds] [seed]
+    python tools/fuzz_parity.py [seconds] [seed] [big]
+
+`big`: only u16 closures near n = 8192 (the packed phase 3) at the same value
+regimes, against the oracle's blocked closure.
 
 Prints one JSON line per failure and a summary line."""
 import json
@@ -124,7 +127,25 @@ def case_bool_close():
     return {"op": "bool_close", "n": n, "p": p}, np.array_equal(gb, want)
 
 
+def case_big_close():
+    """n = 8192 (the packed phase 3 with per-tile flags and certified rounds)
+    at value regimes the configs' generators do not produce; ~9 s of oracle."""
+    w = 16
+    kind = str(rng.choice(["anti", "dist"]))
+    n = 8192 - 8 * int(rng.integers(0, 40))
+    regime = str(rng.choice(["cert_edge", "bound_edge", "near_s", "full", "small"]))
+    v = dist_values(n, n, w, regime)
+    v[np.arange(n), np.arange(n)] = 0
+    t = padded(v, w, kind)
+    cls = AntidistMatrix if kind == "anti" else DistMatrix
+    got = cls(n, n, w, t).transitive_closure().data
+    want = oracle.semiring_close_blocked(t, w, kind)
+    return {"op": "big_close", "w": w, "kind": kind, "n": n, "regime": regime}, np.array_equal(got, want)
+
+
 cases = [case_lane_mul, case_lane_mul, case_lane_close, case_bool_mul, case_bool_close]
+if len(sys.argv) > 3 and sys.argv[3] == "big":
+    cases = [case_big_close]
 counts, fails = {}, 0
 t0 = time.time()
 i = 0
