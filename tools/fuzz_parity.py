@@ -7,8 +7,10 @@ the public classes.  Every result must equal the oracle's bit for bit.
 
     python tools/fuzz_parity.py [seconds] [seed] [big]
 
-`big`: only u16 closures near n = 8192 (the packed phase 3) at the same value
-regimes, against the oracle's blocked closure.
+`big`: closures near n = 8192 / 16384 (the packed phase 3, look-ahead, ragged
+last blocks; against the oracle's blocked closure), products of a few
+thousand squared, Boolean closures and products up to 17000 / 9000, from
+host arrays and device tensors.
 
 Prints one JSON line per failure and a summary line."""
 import json
@@ -127,25 +129,76 @@ def case_bool_close():
     return {"op": "bool_close", "n": n, "p": p}, np.array_equal(gb, want)
 
 
+def _operand(cls, r, c, w, arr):
+    """Half the time a device tensor (device-resident paths), else the numpy
+    array itself (host-backed paths: staged closure, streamed product)."""
+    if rng.random() < 0.5:
+        return cls(r, c, w, arr), "host"
+    st = {8: np.int8, 16: np.int16, 32: np.int32}[w]
+    tt = {8: torch.uint8, 16: torch.uint16, 32: torch.uint32}[w]
+    return cls(r, c, w, torch.from_numpy(arr.view(st)).cuda().view(tt)), "device"
+
+
 def case_big_close():
-    """n = 8192 (the packed phase 3 with per-tile flags and certified rounds)
-    at value regimes the configs' generators do not produce; ~9 s of oracle."""
-    w = 16
+    """Closures near n = 8192 (and sometimes 16384): the packed phase 3 with
+    per-tile flags, certified rounds, look-ahead and ragged last blocks, at
+    value regimes the configs' generators do not produce."""
+    w = int(rng.choice([8, 16, 16, 16, 32]))
     kind = str(rng.choice(["anti", "dist"]))
-    n = 8192 - 8 * int(rng.integers(0, 40))
+    if rng.random() < 0.12 and w == 16:
+        n = 16384 - 8 * int(rng.integers(0, 120))
+    else:
+        n = 8600 - 8 * int(rng.integers(0, 250))
     regime = str(rng.choice(["cert_edge", "bound_edge", "near_s", "full", "small"]))
     v = dist_values(n, n, w, regime)
     v[np.arange(n), np.arange(n)] = 0
     t = padded(v, w, kind)
     cls = AntidistMatrix if kind == "anti" else DistMatrix
-    got = cls(n, n, w, t).transitive_closure().data
+    m, where = _operand(cls, n, n, w, t)
+    got = m.transitive_closure().data
     want = oracle.semiring_close_blocked(t, w, kind)
-    return {"op": "big_close", "w": w, "kind": kind, "n": n, "regime": regime}, np.array_equal(got, want)
+    return ({"op": "big_close", "w": w, "kind": kind, "n": n, "regime": regime, "operand": where},
+            np.array_equal(got, want))
+
+
+def case_big_mul():
+    """Products of a few thousand squared with ragged dimensions: the packed
+    kernel with K chunks, the certificate, the streamed host product."""
+    w = int(rng.choice([8, 16, 16, 32]))
+    kind = str(rng.choice(["anti", "dist"]))
+    M, N, K = (int(rng.integers(2500, 6000)) for _ in range(3))
+    regime = str(rng.choice(["small", "cert_edge", "bound_edge", "near_s", "full"]))
+    a = padded(dist_values(M, K, w, regime), w, kind)
+    b = padded(dist_values(K, N, w, regime), w, kind)
+    cls = AntidistMatrix if kind == "anti" else DistMatrix
+    ma, wa = _operand(cls, M, K, w, a)
+    mb, wb = _operand(cls, K, N, w, b)
+    got = (ma * mb).data
+    want = oracle.semiring_mul(a, b, K, w, kind)
+    return ({"op": "big_mul", "w": w, "kind": kind, "M": M, "N": N, "K": K, "regime": regime,
+             "operands": wa + "/" + wb}, np.array_equal(got, want))
+
+
+def case_big_bool():
+    if rng.random() < 0.5:
+        n = int(rng.integers(7000, 17000))
+        p = float(rng.choice([0.5, 1.0, 2.0, 4.0])) / n
+        t = (rng.random((n, n)) < p).astype(np.uint8)
+        got = BoolMatrix.from_numpy(t).transitive_closure().blocks
+        want = oracle.bool_close(oracle.pack_bits(t))
+        return {"op": "big_bool_close", "n": n, "p": p}, np.array_equal(got, want)
+    M, N, K = (int(rng.integers(3000, 9000)) for _ in range(3))
+    p = float(rng.choice([0.0005, 0.005, 0.05]))
+    a = (rng.random((M, K)) < p).astype(np.uint8)
+    b = (rng.random((K, N)) < p).astype(np.uint8)
+    got = (BoolMatrix.from_numpy(a) * BoolMatrix.from_numpy(b)).blocks
+    want = oracle.bool_mul(oracle.pack_bits(a), oracle.pack_bits(b), K)
+    return {"op": "big_bool_mul", "M": M, "N": N, "K": K, "p": p}, np.array_equal(got, want)
 
 
 cases = [case_lane_mul, case_lane_mul, case_lane_close, case_bool_mul, case_bool_close]
 if len(sys.argv) > 3 and sys.argv[3] == "big":
-    cases = [case_big_close]
+    cases = [case_big_close, case_big_close, case_big_mul, case_big_bool]
 counts, fails = {}, 0
 t0 = time.time()
 i = 0
