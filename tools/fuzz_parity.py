@@ -179,6 +179,51 @@ def case_big_mul():
              "operands": wa + "/" + wb}, np.array_equal(got, want))
 
 
+def case_big_sharded():
+    """The row-panel-sharded closure's GPU ops at sizes that reach the packed
+    (and certified) skip-GEMM: one rank's pipelined schedule (Python and C++
+    orchestration, world = 1), or 2-4 ranks in lockstep on this one GPU (the
+    broadcast becomes a device copy; no rank waits on another)."""
+    from paper_1705_08743_b200 import sharded
+    kind = str(rng.choice(["anti", "dist"]))
+    n = int(rng.integers(500, 1100)) * 8
+    regime = str(rng.choice(["cert_edge", "bound_edge", "full", "small", "small"]))
+    v = dist_values(n, n, 16, regime)
+    v[np.arange(n), np.arange(n)] = 0
+    full = padded(v, 16, kind)
+    mode = str(rng.choice(["python1", "native1", "lockstep"]))
+    anti = kind == "anti"
+    if mode == "python1":
+        fw = sharded.ShardedFW(n=n, rank=0, world=1, ops=sharded.CudaFwOps(16, anti=anti))
+        got = fw.run(torch.from_numpy(full.view(np.int16)).cuda().view(torch.uint16)).cpu().numpy()
+        world = 1
+    elif mode == "native1":
+        fw = sharded.NativeShardedFW(n, 0, 1, 16, anti=anti)
+        got = fw.run(torch.from_numpy(full.view(np.int16)).cuda().view(torch.uint16)).cpu().numpy()
+        world = 1
+    else:
+        world = int(rng.integers(2, 5))
+        ranks = []
+        for r in range(world):
+            fw = sharded.ShardedFW(n=n, rank=r, world=world, ops=sharded.CudaFwOps(16, anti=anti))
+            loc = torch.from_numpy(full[fw.row0:fw.row1].copy().view(np.int16)).cuda().view(torch.uint16)
+            ranks.append((fw, loc))
+        block = ranks[0][0].block
+        for k0 in range(0, n, block):
+            owner = ranks[0][0].owner(k0)
+            begun = [fw.begin_round(local, k0) for fw, local in ranks]
+            src = begun[owner][0]
+            for r, (panel, _) in enumerate(begun):
+                if r != owner:
+                    panel.copy_(src)
+            for (fw, local), (panel, skip) in zip(ranks, begun):
+                fw.end_round(local, panel, k0, skip)
+        got = torch.cat([local for _, local in ranks]).cpu().numpy()
+    want = oracle.semiring_close_blocked(full, 16, kind)
+    return ({"op": "big_sharded", "mode": mode, "world": world, "kind": kind, "n": n, "regime": regime},
+            np.array_equal(got.view(np.uint16), want))
+
+
 def case_big_bool():
     if rng.random() < 0.5:
         n = int(rng.integers(7000, 17000))
@@ -198,7 +243,9 @@ def case_big_bool():
 
 cases = [case_lane_mul, case_lane_mul, case_lane_close, case_bool_mul, case_bool_close]
 if len(sys.argv) > 3 and sys.argv[3] == "big":
-    cases = [case_big_close, case_big_close, case_big_mul, case_big_bool]
+    cases = [case_big_close, case_big_close, case_big_mul, case_big_bool, case_big_sharded]
+if len(sys.argv) > 3 and sys.argv[3] == "sharded":
+    cases = [case_big_sharded]
 counts, fails = {}, 0
 t0 = time.time()
 i = 0
