@@ -241,7 +241,38 @@ def case_big_bool():
     return {"op": "big_bool_mul", "M": M, "N": N, "K": K, "p": p}, np.array_equal(got, want)
 
 
-cases = [case_lane_mul, case_lane_mul, case_lane_close, case_bool_mul, case_bool_close]
+def case_entrywise():
+    """lanewise min / max / absolute difference / complement
+    and the Boolean bridge, against numpy on the valid columns; padding lanes
+    must hold the result type's (+)-identity (antidist.py:128-156, :213-224)."""
+    w = int(rng.choice([8, 16, 32]))
+    kind = str(rng.choice(["anti", "dist"]))
+    S = (1 << w) - 1
+    r, c = rand_dim(1, 3000), rand_dim(1, 3000)
+    a = padded(dist_values(r, c, w, "full"), w, kind)
+    b = padded(dist_values(r, c, w, str(rng.choice(["full", "small", "near_s"]))), w, kind)
+    cls = AntidistMatrix if kind == "anti" else DistMatrix
+    ma, mb = cls(r, c, w, a), cls(r, c, w, b)
+    av, bv = a[:, :c].astype(np.uint64), b[:, :c].astype(np.uint64)
+    pad = 0 if kind == "anti" else S
+    ok = True
+    for name, got, want in (("and", (ma & mb).data, np.minimum(av, bv)), ("or", (ma | mb).data, np.maximum(av, bv)),
+                            ("xor", (ma ^ mb).data, np.maximum(av, bv) - np.minimum(av, bv))):
+        ok = ok and np.array_equal(got[:, :c].astype(np.uint64), want) and bool((got[:, c:] == pad).all())
+    inv = ~ma
+    ok = ok and type(inv) is (DistMatrix if kind == "anti" else AntidistMatrix)
+    ok = ok and np.array_equal(inv.data[:, :c].astype(np.uint64), S - av)
+    ok = ok and bool((inv.data[:, c:] == (S if kind == "anti" else 0)).all())
+    if kind == "anti":
+        bits = (rng.random((r, c)) < 0.3).astype(np.uint8)
+        lanes = AntidistMatrix.from_boolmat(BoolMatrix.from_numpy(bits), w)
+        ok = ok and np.array_equal(lanes.data[:, :c].astype(np.uint64), bits.astype(np.uint64) * S)
+        ok = ok and bool((lanes.data[:, c:] == 0).all())
+        ok = ok and np.array_equal(ma.to_boolmat().to_numpy(), (av != 0).astype(np.uint8))
+    return {"op": "entrywise", "w": w, "kind": kind, "r": r, "c": c}, bool(ok)
+
+
+cases = [case_lane_mul, case_lane_mul, case_lane_close, case_bool_mul, case_bool_close, case_entrywise]
 if len(sys.argv) > 3 and sys.argv[3] == "big":
     cases = [case_big_close, case_big_close, case_big_mul, case_big_bool, case_big_sharded]
 if len(sys.argv) > 3 and sys.argv[3] == "sharded":
