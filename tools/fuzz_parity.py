@@ -272,7 +272,49 @@ def case_entrywise():
     return {"op": "entrywise", "w": w, "kind": kind, "r": r, "c": c}, bool(ok)
 
 
-cases = [case_lane_mul, case_lane_mul, case_lane_close, case_bool_mul, case_bool_close, case_entrywise]
+def case_batch():
+    """Many small problems per launch (batch.py): stacked Boolean products
+    (tensor cores on 128-multiple shapes, bits otherwise), stacked Boolean
+    closures (n <= 512) and stacked lane closures (n <= 128)."""
+    from paper_1705_08743_b200 import batch
+    which = str(rng.choice(["bool_mul_tc", "bool_mul_bits", "bool_close", "lane_close"]))
+    nb = int(rng.integers(1, 24))
+    ok = True
+    if which.startswith("bool_mul"):
+        if which == "bool_mul_tc":
+            M, N, K = (128 * int(rng.integers(1, 6)) for _ in range(3))
+            K += 128
+        else:
+            M, N, K = rand_dim(1, 500), rand_dim(1, 500), rand_dim(1, 500)
+        p = float(rng.choice([0.01, 0.05, 0.3]))
+        As = [(rng.random((M, K)) < p).astype(np.uint8) for _ in range(nb)]
+        Bs = [(rng.random((K, N)) < p).astype(np.uint8) for _ in range(nb)]
+        got = batch.bool_mul_many([BoolMatrix.from_numpy(a) for a in As], [BoolMatrix.from_numpy(b) for b in Bs])
+        for g, a, b in zip(got, As, Bs):
+            ok = ok and np.array_equal(g.blocks, oracle.bool_mul(oracle.pack_bits(a), oracle.pack_bits(b), K))
+        desc = {"M": M, "N": N, "K": K}
+    elif which == "bool_close":
+        n = rand_dim(1, 512)
+        Ts = [(rng.random((n, n)) < 2.0 / n).astype(np.uint8) for _ in range(nb)]
+        got = batch.bool_closure_many([BoolMatrix.from_numpy(t) for t in Ts])
+        for g, t in zip(got, Ts):
+            ok = ok and np.array_equal(g.blocks, oracle.bool_close(oracle.pack_bits(t)))
+        desc = {"n": n}
+    else:
+        w = int(rng.choice([8, 16, 32]))
+        kind = str(rng.choice(["anti", "dist"]))
+        n = rand_dim(1, 128)
+        regime = str(rng.choice(["small", "cert_edge", "bound_edge", "near_s", "full"]))
+        Ts = [padded(dist_values(n, n, w, regime), w, kind) for _ in range(nb)]
+        cls = AntidistMatrix if kind == "anti" else DistMatrix
+        got = batch.closure_many([cls(n, n, w, t) for t in Ts])
+        for g, t in zip(got, Ts):
+            ok = ok and np.array_equal(g.data, oracle.semiring_close(t, w, kind))
+        desc = {"n": n, "w": w, "kind": kind, "regime": regime}
+    return dict({"op": "batch_" + which, "batch": nb}, **desc), bool(ok)
+
+
+cases = [case_lane_mul, case_lane_mul, case_lane_close, case_bool_mul, case_bool_close, case_entrywise, case_batch]
 if len(sys.argv) > 3 and sys.argv[3] == "big":
     cases = [case_big_close, case_big_close, case_big_mul, case_big_bool, case_big_sharded]
 if len(sys.argv) > 3 and sys.argv[3] == "sharded":
