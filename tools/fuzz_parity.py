@@ -5,12 +5,13 @@ lanes at the edges of the 2^(w-2) certificate and of the 2^(w-1) bound, full
 range, near S), Boolean products and closures at random densities, all through
 the public classes.  Every result must equal the oracle's bit for bit.
 
-    python tools/fuzz_parity.py [seconds] [seed] [big]
+    python tools/fuzz_parity.py [seconds] [seed] [big|mid|sharded]
 
 `big`: closures near n = 8192 / 16384 (the packed phase 3, look-ahead, ragged
 last blocks; against the oracle's blocked closure), products of a few
 thousand squared, Boolean closures and products up to 17000 / 9000, from
-host arrays and device tensors.
+host arrays and device tensors.  `mid`: closures at n = 1300-6700 and
+Boolean closures at 1800-7000 (the sizes between the other two modes).
 
 Prints one JSON line per failure and a summary line."""
 import json
@@ -145,7 +146,9 @@ def case_big_close():
     value regimes the configs' generators do not produce."""
     w = int(rng.choice([8, 16, 16, 16, 32]))
     kind = str(rng.choice(["anti", "dist"]))
-    if rng.random() < 0.12 and w == 16:
+    if MID:
+        n = int(rng.integers(1300, 6700))
+    elif rng.random() < 0.12 and w == 16:
         n = 16384 - 8 * int(rng.integers(0, 120))
     else:
         n = 8600 - 8 * int(rng.integers(0, 250))
@@ -226,7 +229,7 @@ def case_big_sharded():
 
 def case_big_bool():
     if rng.random() < 0.5:
-        n = int(rng.integers(7000, 17000))
+        n = int(rng.integers(1800, 7000)) if MID else int(rng.integers(7000, 17000))
         p = float(rng.choice([0.5, 1.0, 2.0, 4.0])) / n
         t = (rng.random((n, n)) < p).astype(np.uint8)
         got = BoolMatrix.from_numpy(t).transitive_closure().blocks
@@ -315,6 +318,9 @@ def case_batch():
 
 
 cases = [case_lane_mul, case_lane_mul, case_lane_close, case_bool_mul, case_bool_close, case_entrywise, case_batch]
+MID = len(sys.argv) > 3 and sys.argv[3] == "mid"
+if MID:
+    cases = [case_big_close, case_big_close, case_big_bool]
 if len(sys.argv) > 3 and sys.argv[3] == "big":
     cases = [case_big_close, case_big_close, case_big_mul, case_big_bool, case_big_sharded]
 if len(sys.argv) > 3 and sys.argv[3] == "sharded":
