@@ -5,13 +5,15 @@ lanes at the edges of the 2^(w-2) certificate and of the 2^(w-1) bound, full
 range, near S), Boolean products and closures at random densities, all through
 the public classes.  Every result must equal the oracle's bit for bit.
 
-    python tools/fuzz_parity.py [seconds] [seed] [big|mid|sharded]
+    python tools/fuzz_parity.py [seconds] [seed] [big|mid|sharded|hoststream]
 
 `big`: closures near n = 8192 / 16384 (the packed phase 3, look-ahead, ragged
 last blocks; against the oracle's blocked closure), products of a few
 thousand squared, Boolean closures and products up to 17000 / 9000, from
 host arrays and device tensors.  `mid`: closures at n = 1300-6700 and
 Boolean closures at 1800-7000 (the sizes between the other two modes).
+`hoststream`: mid-size closures of host arrays with the streamed host-buffer
+schedule forced (smx_set_fw_host_stream(2)).
 
 Prints one JSON line per failure and a summary line."""
 import json
@@ -133,7 +135,7 @@ def case_bool_close():
 def _operand(cls, r, c, w, arr):
     """Half the time a device tensor (device-resident paths), else the numpy
     array itself (host-backed paths: staged closure, streamed product)."""
-    if rng.random() < 0.5:
+    if HOSTSTREAM or rng.random() < 0.5:
         return cls(r, c, w, arr), "host"
     st = {8: np.int8, 16: np.int16, 32: np.int32}[w]
     tt = {8: torch.uint8, 16: torch.uint16, 32: torch.uint32}[w]
@@ -318,9 +320,16 @@ def case_batch():
 
 
 cases = [case_lane_mul, case_lane_mul, case_lane_close, case_bool_mul, case_bool_close, case_entrywise, case_batch]
-MID = len(sys.argv) > 3 and sys.argv[3] == "mid"
+MID = len(sys.argv) > 3 and sys.argv[3] in ("mid", "hoststream")
 if MID:
     cases = [case_big_close, case_big_close, case_big_bool]
+HOSTSTREAM = len(sys.argv) > 3 and sys.argv[3] == "hoststream"
+if HOSTSTREAM:
+    # every host-backed closure takes the streamed schedule (ingest groups,
+    # staged copies in and out, egress products), whatever its size
+    from paper_1705_08743_b200 import _native
+    _native.lib().smx_set_fw_host_stream(2)
+    cases = [case_big_close]
 if len(sys.argv) > 3 and sys.argv[3] == "big":
     cases = [case_big_close, case_big_close, case_big_mul, case_big_bool, case_big_sharded]
 if len(sys.argv) > 3 and sys.argv[3] == "sharded":
