@@ -55,8 +55,8 @@ unsigned long long smx_launch_count(void);
 int smx_set_packed_tiles_per_cta(int tpc);
 /* How the packed GEMM's producer warp waits for a free ring slot: 0 = a bare
  * mbarrier.try_wait loop, ns > 0 = try_wait with that suspend-time hint (ns),
- * ns < 0 = nanosleep(-ns) between polls.  Results are identical.  Returns the
- * previous setting. */
+ * ns < 0 = nanosleep(-ns) between polls (|ns| clamped to 100000).  Results are
+ * identical.  Returns the previous setting. */
 int smx_set_packed_producer_backoff(int ns);
 /* The u16/u32 semiring kernels run a k-tile with the 1-instruction update
  * c = min(c, a + b) when the CTA has verified that every staged lane of that

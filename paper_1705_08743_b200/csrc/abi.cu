@@ -205,7 +205,9 @@ int smx_set_packed_tiles_per_cta(int tpc) {
     return smx::g_packed_tpc.exchange(tpc);
 }
 int smx_set_packed_producer_backoff(int ns) {
-    if (ns < -100000 || ns > 100000) return SMX_E_ARG;
+    // (a negative setting is valid, so the return value is always the previous
+    // setting, never an error code: out-of-range values are clamped)
+    ns = ns < -100000 ? -100000 : (ns > 100000 ? 100000 : ns);
     return smx::g_packed_backoff.exchange(ns);
 }
 int smx_set_bounded_fastpath(int enable) {
