@@ -349,4 +349,10 @@ while time.time() - t0 < budget:
         fails += 1
         print(json.dumps({"FAIL": desc, "case_index": i, "seed": seed}), flush=True)
 torch.cuda.synchronize()
-print(json.dumps({"seed": seed, "seconds": round(time.time() - t0, 1), "cases": counts, "failures": fails}))
+try:   # resident and device memory at the end: a leak in a host or staging path would show here
+    import psutil
+    rss = round(psutil.Process().memory_info().rss / 2 ** 30, 2)
+except Exception:   # noqa: BLE001
+    rss = None
+print(json.dumps({"seed": seed, "seconds": round(time.time() - t0, 1), "cases": counts, "failures": fails,
+                  "rss_gib": rss, "cuda_reserved_gib": round(torch.cuda.memory_reserved() / 2 ** 30, 2)}))
